@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 force-evaluation hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): 32,000 particles on an
+FCC lattice (20^3 cells, rho 0.8, jitter +-0.02, T*=0.9), LJ rc 2.5, ATM
+nu=0.073 rc 2.5, fp64, r-RESPA with dt=0.001 and three-body factor 5.  A
+"step" is one r-RESPA base step (drift, binning, survivor rows, LJ pass,
+kick; the ATM pass on every 5th step) -- exactly integrators.py:148-172.
+
+ours:       K steps replayed from per-step CUDA graphs on the GPU, each
+            bracketed by CUDA events on the launch stream with an L2 flush
+            (a 256 MiB write) between steps; value = steps/s (max over ranks).
+            roofline = the ATM kernel (dominant) timed standalone with events,
+            141 FP64 flops per unique triplet against the FP64
+            FMA peak measured in this run (MEASURED_PEAKS.json has no FP64
+            figure).  e2e = the public respa_run() on host numpy arrays.
+reference:  the reference's CPU path on this host's cores -- the C port of
+            respamd's kernels in oracle/ (bit-exact with the reference,
+            tests/test_oracle_golden.py) with all host threads, same workload.
+
+For N > 1 (torchrun) each rank runs an independent replica of the workload
+("replicas only" until the domain-decomposed path lands).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "ATM triplet interactions/s and r-RESPA MD steps/s (fp64) vs FP64 roofline"
+WORKLOAD = ("cfg2: 32,000 particles, FCC 20^3 cells rho 0.8, jitter +-0.02 sigma, periodic box "
+            "34.1995, T*=0.9; LJ eps=sigma=1 rc 2.5; ATM nu=0.073 rc 2.5; r-RESPA dt 0.001, "
+            "three-body factor 5")
+FLOPS_PER_TRIPLET = 141
+FLOPS_PER_PAIR = 35
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--config", default="cfg2")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------
+# clocks sampled during the timed region
+# --------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 4 + k and r[4 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------
+# CPU legs (the oracle port of the reference kernels)
+# --------------------------------------------------------------------------
+def cpu_respa_rate(cfg, seconds: float, threads: int):
+    """Steps/s of the reference loop restated in oracle/ on `threads` cores.
+
+    Bounded sample: one calibration cycle, then a single respa_run of whole
+    three-body cycles sized to take about `seconds` (its two initial passes
+    are included in the timing, which slightly favours the GPU)."""
+    from oracle import oracle as o
+
+    o.set_num_threads(threads)
+    s = cfg.system()
+    sf = cfg.step_size_factor
+    ff = o.OracleForceField(nu=0.073, cutoff=cfg.rc_lj)
+    sysm = o.OracleSystem.from_positions(s.positions, s.box, True, s.velocities)
+    t0 = time.perf_counter()
+    o.respa_run(sysm, ff, o.OracleLinkedCells(), cfg.dt, sf, sf)
+    t_cycle = time.perf_counter() - t0
+    steps = sf * int(min(20, max(1, round(seconds / max(t_cycle, 1e-3)))))
+    sysm = o.OracleSystem.from_positions(s.positions, s.box, True, s.velocities)
+    t0 = time.perf_counter()
+    o.respa_run(sysm, ff, o.OracleLinkedCells(), cfg.dt, sf, steps)
+    elapsed = time.perf_counter() - t0
+    return steps / elapsed, steps, elapsed
+
+
+def reference_arm(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    from oracle import oracle as o
+
+    o.set_num_threads(threads)
+    s = cfg.system()
+    sysm = o.OracleSystem.from_positions(s.positions, s.box, True, s.velocities)
+    ff = o.OracleForceField(nu=0.073, cutoff=cfg.rc_lj)
+    sf = cfg.step_size_factor
+    warm = max(sf, (args.warmup + sf - 1) // sf * sf)
+    steps = max(sf, (args.steps + sf - 1) // sf * sf)
+    cont = o.OracleLinkedCells()
+    o.respa_run(sysm, ff, cont, cfg.dt, sf, warm)
+    t0 = time.perf_counter()
+    o.respa_run(sysm, ff, cont, cfg.dt, sf, steps)
+    elapsed = time.perf_counter() - t0
+    rate = steps / elapsed
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": 1e3 / rate,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded FCC lattice + jitter, SURVEY.md §8d)",
+        "config": {"workload": WORKLOAD, "timed": "respa_run incl. its two initial passes"},
+        "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} r-RESPA steps of cfg2 (oracle/ C port of respamd "
+                                   f"kernels, OpenMP {threads} threads)"},
+        "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+def ours_arm(args, cfg):
+    import torch
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    import paper_2507_11172_b200 as pkg
+    from paper_2507_11172_b200 import _lib
+    from paper_2507_11172_b200.integrators import DeviceRespa, RespaSchedule
+
+    _lib.require_device()
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sf = cfg.step_size_factor
+    K, W = int(args.steps), max(3, int(args.warmup))
+
+    s = cfg.system()
+    ff = cfg.force_field()
+    total_steps = sf + W + K + 2 * sf
+    total_steps = (total_steps + sf - 1) // sf * sf
+    run = DeviceRespa(s.copy(), ff, pkg.CudaLinkedCells(), RespaSchedule(cfg.dt, sf, total_steps),
+                      sf)
+    run.start()
+    run.run_periods(0, 1)  # eager warm-up period: allocations, attributes
+    l0 = L.rb_launch_count()
+    graphs = run.capture_steps()
+    launches_per_period = L.rb_launch_count() - l0
+    launches_per_step = launches_per_period / sf
+    step = sf
+    for _ in range(W):
+        graphs[step % sf].replay()
+        step += 1
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = _lib.stream_handle()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for k in range(K):
+            L.rb_l2_flush(_lib.ptr(flush), flush.numel(), stream)
+            starts[k].record()
+            graphs[step % sf].replay()
+            ends[k].record()
+            step += 1
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    status = run.eng.read_status()
+    if status is not None or run.eng.overflowed():
+        raise RuntimeError(f"device error during the timed run: {status}")
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / K
+    value = world * K / (ms_max * 1e-3)
+
+    # ---- dominant kernel: the ATM pass, standalone, events on its stream
+    eng, geom = run.eng, run._geom()
+    eng.bin(geom, run.x)
+    eng.nlist(geom, run.r_list, capacity=run.capacity, checked=True)
+    f3 = torch.empty_like(run.f3)
+    eng.reset_status(0)
+    eng.atm(geom, run.rc3, run.nu, f3, tag=0, count_visits=True)
+    torch.cuda.synchronize()
+    unique = int(eng.visits.item()) // 3
+    grid = eng.grid_struct(geom)
+    import ctypes
+
+    def atm_once():
+        return L.rb_atm_pass(ctypes.byref(grid), eng.n, _lib.ptr(eng.xs), _lib.ptr(eng.ys),
+                             _lib.ptr(eng.zs), _lib.ptr(eng.parts), _lib.ptr(eng.rows),
+                             _lib.ptr(eng.row_count), eng.capacity, run.rc3, run.nu,
+                             _lib.ptr(f3), _lib.ptr(eng.e_rank), _lib.ptr(eng.w_rank),
+                             _lib.ptr(eng.v_rank), _lib.ptr(eng.status), 0, stream)
+
+    def lj_once():
+        return L.rb_lj_pass(ctypes.byref(grid), eng.n, _lib.ptr(eng.xs), _lib.ptr(eng.ys),
+                            _lib.ptr(eng.zs), _lib.ptr(eng.parts), _lib.ptr(eng.rows),
+                            _lib.ptr(eng.row_count), eng.capacity, run.rc2, 1.0, 1.0,
+                            _lib.ptr(f3), _lib.ptr(eng.e_rank), _lib.ptr(eng.w_rank),
+                            _lib.ptr(eng.status), 0, stream)
+
+    def time_kernel(fn, reps):
+        fn()
+        ts = []
+        for _ in range(reps):
+            L.rb_l2_flush(_lib.ptr(flush), flush.numel(), stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts), ts
+
+    atm_ms, _ = time_kernel(atm_once, 20)
+    lj_ms, _ = time_kernel(lj_once, 20)
+    pairs = int((eng.row_count[: eng.n].sum().item()))  # within r_list == rc2 here
+    tflop = torch.empty(1, dtype=torch.float64)
+    peak = ctypes.c_double(0.0)
+    L.rb_fp64_peak(2000, ctypes.byref(peak), stream)
+    peak_tf = float(peak.value)
+    triplets_per_s = unique / (atm_ms * 1e-3)
+    achieved_tf = triplets_per_s * FLOPS_PER_TRIPLET / 1e12
+    traffic = None
+    prof = os.path.join(REPO, "profiles", "atm_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    del tflop
+
+    # ---- e2e through the public API on host arrays
+    e2e_steps = (K + sf - 1) // sf * sf
+    host = cfg.system()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pkg.respa_run(host, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(cfg.dt, sf, e2e_steps))
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    n = s.positions.shape[0]
+    h2d = 2 * n * 24  # positions + velocities
+    d2h = 4 * n * 24 + (e2e_steps // sf + 1) * 64  # x, v, f2, f3 + trace rows
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded FCC lattice + jitter, SURVEY.md §8d; no public dataset)",
+        "config": {"workload": WORKLOAD, "particles": n, "step_size_factor": sf,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed (256 MiB write) between timed steps; per-step CUDA events",
+                   "graph": "one CUDA graph per step position in the 5-step cycle"},
+        "roofline": {"bound": "fp64", "kernel": "k_atm (ATM triplet pass)",
+                     "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved_tf / peak_tf if peak_tf > 0 else None,
+                     "traffic": traffic,
+                     "peak_source": "measured in this run: rb_fp64_peak DFMA chains on all SMs "
+                                    "(MEASURED_PEAKS.json has no FP64 entry)",
+                     "work": f"{FLOPS_PER_TRIPLET} FP64 flops per unique triplet x {unique} "
+                             f"unique triplets per launch",
+                     "kernel_ms": atm_ms, "triplets_per_s": triplets_per_s,
+                     "lj_kernel_ms": lj_ms, "lj_pairs_visited": pairs,
+                     "lj_tflops": pairs / 2 * FLOPS_PER_PAIR / (lj_ms * 1e-3) / 1e12},
+        "e2e": {"value": e2e_steps / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d / e2e_steps,
+                "d2h_bytes_per_step": d2h / e2e_steps,
+                "note": f"public respa_run({e2e_steps} steps) on host numpy arrays, wall clock "
+                        f"incl. upload, graph capture, download"},
+        "gpu_launches": int(round(launches_per_step * K)) + K,
+        "gpu_launches_detail": {"per_step": launches_per_step, "l2_flush_per_step": 1},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, done, el = cpu_respa_rate(cfg, args.cpu_seconds, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": threads, "kind": "port",
+                                "sample": f"{done} r-RESPA steps of cfg2 in {el:.1f}s (oracle/ C "
+                                          f"port of respamd kernels, OpenMP {threads} threads)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    from paper_2507_11172_b200 import systems
+
+    cfg = systems.CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+    else:
+        ours_arm(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+/*
+ * respa_b200.h -- C-ABI of the B200 (sm_100a) force-evaluation hot path for
+ * the arXiv 2507.11172 reference engine (LJ + Axilrod-Teller-Muto with
+ * r-RESPA multiple time-stepping).
+ *
+ * The reference ("respamd", pure Python + numba) has no FFI: its hot path is
+ * reached through the container duck type (pair_pass / triplet_pass,
+ * respamd/containers.py:878-937), the functional passes
+ * (build_cell_grid :235, c01_pair_pass :750, c01_triplet_pass :786,
+ * collect_triplet_visits :825) and respa_run (respamd/integrators.py:96-173).
+ * Each entry point below replaces the numba kernel named beside it; the
+ * Python mirror (paper_2507_11172_b200/, binding shown in INTEGRATION.md)
+ * calls them through ctypes.
+ *
+ * Conventions
+ *   - all array arguments are DEVICE pointers (cudaMalloc / torch CUDA
+ *     tensors) unless stated; per-particle state is the reference layout,
+ *     (n,3) float64 AoS in particle order;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - no entry point allocates memory: callers own every buffer; scratch is
+ *     sized by the matching *_scratch_bytes query;
+ *   - the return value is a launch-time status (RB_OK or RB_ERR_*); data-
+ *     dependent errors found on the device (minimum separation, non-finite
+ *     state, list overflow) are recorded in a caller-owned device status
+ *     word, `unsigned long long *status`, as (tag << 8) | kind by atomicMin.
+ *     Initialise it to RB_STATUS_CLEAR.  `tag` is the r-RESPA iteration the
+ *     kernel belongs to (0 for standalone passes); a kernel whose tag is
+ *     larger than a recorded error's tag does nothing, so the state freezes
+ *     at the failing step as respamd's IntegrationBlowUp does.
+ */
+#ifndef RESPA_B200_H
+#define RESPA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define RB_API __attribute__((visibility("default")))
+#else
+#define RB_API
+#endif
+
+#define RB_ABI_VERSION 1
+
+/* return / status kinds */
+#define RB_OK 0
+#define RB_ERR_MIN_SEPARATION 1 /* respamd MinimumSeparationError (containers.py:39-40,742-747) */
+#define RB_ERR_GEOMETRY 2       /* respamd ValidationError for the grid (containers.py:248-252) */
+#define RB_ERR_CUDA 3           /* launch failure */
+#define RB_ERR_CAPACITY 4       /* a neighbour row exceeded its capacity */
+#define RB_ERR_ARGUMENT 5       /* bad sizes or pointers */
+
+/* device status-word kinds (low 8 bits), ordered by precedence inside a step */
+#define RB_KIND_PAIR_MIN_SEPARATION 1    /* raised by pair_pass (integrators.py:154-157) */
+#define RB_KIND_TRIPLET_MIN_SEPARATION 2 /* raised by triplet_pass (:161-164) */
+#define RB_KIND_NONFINITE 3              /* _check_finite (:89-93, :166-170) */
+#define RB_KIND_CAPACITY 4               /* neighbour-list overflow (no reference analogue) */
+#define RB_STATUS_CLEAR 0xFFFFFFFFFFFFFFFFull
+
+#define RB_MAX_OFFSETS 125
+
+/* Cell-grid geometry, computed on the host exactly as
+ * respamd/containers.py:244-263 does (cells = max(1, floor(extent/cutoff)),
+ * size = extent/cells, inv_cell = 1.0/size) so that binning is bit-exact. */
+typedef struct rb_grid {
+    int32_t cells[3];   /* cells per dimension */
+    int32_t periodic;   /* 1: periodic box with single-shift minimum image */
+    double origin[3];   /* 0 for periodic systems */
+    double inv_cell[3]; /* 1.0 / cell_size */
+    double box[3];
+    int32_t n_offsets;                   /* canonical neighbour-cell offsets */
+    int32_t offsets[RB_MAX_OFFSETS][3];  /* containers.py:133-144 (pair_cells) */
+} rb_grid;
+
+RB_API int rb_abi_version(void);
+/* cumulative number of kernels this library has launched (or recorded into
+ * a CUDA graph under capture) in this process */
+RB_API long long rb_launch_count(void);
+/* sizeof(rb_grid) as compiled into the library (binding layout check) */
+RB_API size_t rb_grid_bytes(void);
+RB_API const char *rb_status_string(int status);
+/* number of CUDA devices visible to this library's runtime (0 without a GPU) */
+RB_API int rb_device_count(void);
+
+/* ---- binning: replaces _bin_particles (containers.py:175-209) ----------
+ * Counting sort of particles by flat cell id (cx*ny+cy)*nz+cz with the
+ * truncating index of :182-197, stable in ascending particle index.
+ * Outputs: cell_start[ncell+1], cell_particles[n] (rank -> particle),
+ * cell_of_rank[n], and positions gathered into rank order (xs, ys, zs). */
+RB_API size_t rb_bin_scratch_bytes(int64_t n, int64_t ncell);
+RB_API int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_start,
+           int32_t *cell_particles, int32_t *cell_of_rank, double *xs, double *ys, double *zs,
+           void *scratch, size_t scratch_bytes, void *stream);
+
+/* ---- neighbour rows: the survivor lists of containers.py:437-474 -------
+ * Row r (rank order) lists, in stencil order, the ranks within r_list of
+ * particle r (reference pair-distance arithmetic, inclusive).  Rows hold at
+ * most `capacity` entries; the longest overflowing row length is
+ * atomicMax-ed into the device int *max_count (caller initialises it to 0)
+ * and the row is truncated, so callers must check it before trusting a pass. */
+RB_API int rb_nlist(const rb_grid *g, int64_t n, const double *xs, const double *ys, const double *zs,
+             const int32_t *cell_start, const int32_t *cell_of_rank, double r_list,
+             int32_t capacity, int32_t *rows, int32_t *row_count, int32_t *max_count,
+             void *stream);
+
+/* ---- LJ pair pass: replaces _c01_pair_kernel (containers.py:282-370) ---
+ * Owner-computes over the neighbour rows with the inclusive cutoff `rc`;
+ * writes forces (n,3) in particle order (overwritten), and per-rank energy
+ * (sum of phi/2) and virial (sum of scale*r^2/2). */
+RB_API int rb_lj_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys, const double *zs,
+               const int32_t *cell_particles, const int32_t *rows, const int32_t *row_count,
+               int32_t capacity, double rc, double epsilon, double sigma, double *forces,
+               double *energy_rank, double *virial_rank, unsigned long long *status, int64_t tag,
+               void *stream);
+
+/* ---- ATM triplet pass: replaces _c01_triplet_kernel (:373-535) --------
+ * Enumerates every within-cutoff triplet (all three pair distances <= rc,
+ * inclusive) of each base particle; writes forces (n,3) in particle order
+ * (overwritten), per-rank energy/virial and per-rank accepted-visit counts
+ * (3 visits per unique triplet, as collect_triplet_visits :825-849 counts). */
+RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys, const double *zs,
+                const int32_t *cell_particles, const int32_t *rows, const int32_t *row_count,
+                int32_t capacity, double rc, double nu, double *forces, double *energy_rank,
+                double *virial_rank, int32_t *visits_rank, unsigned long long *status, int64_t tag,
+                void *stream);
+
+/* Instrumentation (collect_triplet_visits, containers.py:825-849): writes
+ * one sorted (i, j, k) particle-index row per accepted visit, int32 (V,3),
+ * at row_offset[r] (exclusive prefix of rb_atm_pass's visits_rank). */
+RB_API int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *xs, const double *ys,
+                             const double *zs, const int32_t *cell_particles, const int32_t *rows,
+                             const int32_t *row_count, int32_t capacity, double rc,
+                             const int64_t *row_offset, int32_t *visit_rows, void *stream);
+
+/* ---- deterministic reductions (fixed partition + fixed tree) ---------- */
+RB_API size_t rb_reduce_scratch_bytes(int64_t n);
+/* out[0] = sum(in[0..n)) */
+RB_API int rb_reduce_sum_f64(int64_t n, const double *in, double *out, void *scratch, void *stream);
+/* out[0] = sum(in[i]^2) -- kinetic energy numerator of model.py:133 */
+RB_API int rb_reduce_sumsq_f64(int64_t n, const double *in, double *out, void *scratch, void *stream);
+/* out[0] = sum(in[0..n)) as int64 */
+RB_API int rb_reduce_sum_i32(int64_t n, const int32_t *in, int64_t *out, void *scratch, void *stream);
+
+/* ---- r-RESPA kick/drift: replaces the numpy updates of respa_run ------
+ * (integrators.py:148-170), bit-exact with numpy's rounding order.
+ * drift: [v += half_respa*f3 if kick3]; x += dt*v + half_drift*f2_old;
+ *        wrap into [0, box) with numpy mod semantics (model.py:274-280);
+ *        non-finite x records RB_KIND_NONFINITE at `tag`.
+ * kick:  v += half_dt*(f2_old + f2_new); f2_old = f2_new (:159);
+ *        [v += half_respa*f3 if kick3];
+ *        non-finite v records RB_KIND_NONFINITE at `tag`. */
+RB_API int rb_respa_drift(int64_t n, double *pos, double *vel, const double *f2_old, const double *f3,
+                   const double *box3_host, int32_t periodic, double dt, double half_drift,
+                   double half_respa, int32_t kick3, unsigned long long *status, int64_t tag,
+                   void *stream);
+RB_API int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f2_new,
+                  const double *f3, double half_dt, double half_respa, int32_t kick3,
+                  unsigned long long *status, int64_t tag, void *stream);
+
+/* ---- device-side step counter and trace (CUDA-graph friendly) ---------
+ * status points to TWO words: status[0] the error word, status[1] the step
+ * counter.  Kernels given tag == -1 read their tag from status[1].
+ * rb_step_begin increments status[1]; rb_trace_record writes the 8-double
+ * row [tag, sum v^2, E2, W2, E3, W3, 0, 0] at trace[8 * (tag / interval)]
+ * from device scalars (RunTrace.record, integrators.py:74-83). */
+RB_API int rb_step_begin(unsigned long long *status, void *stream);
+RB_API int rb_trace_record(const unsigned long long *status, int64_t sample_interval,
+                           double *trace, const double *sumsq, const double *e2, const double *w2,
+                           const double *e3, const double *w3, void *stream);
+
+/* ---- device timing helpers for bench.py (events on the launch stream) -- */
+/* FP64 FMA throughput microbenchmark: runs `iters` dependent-chain DFMA
+ * blocks on every SM and returns the achieved FP64 TFLOP/s in *tflops. */
+RB_API int rb_fp64_peak(int32_t iters, double *tflops, void *stream);
+/* Writes `bytes` of a scratch buffer to evict L2 between timed steps. */
+RB_API int rb_l2_flush(void *buf, size_t bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RESPA_B200_H */

@@ -1,0 +1,216 @@
+// bin.cu -- linked-cell binning as a counting sort by cell index.
+//
+// Replaces respamd/containers.py:175-209 (_bin_particles).  The cell index is
+// the reference's truncating int((x - origin) * inv_cell) clamped to
+// [0, n-1] (:182-196), the flat id is (cx*ny + cy)*nz + cz (:197), and the
+// order inside a cell is ascending particle index (the reference's serial
+// stable scatter, :203-208).  Four HBM-bound passes:
+//
+//   k_bin_count    cell id per particle + histogram (integer atomics)
+//   scan           exclusive scan of the histogram -> cell_start
+//   k_bin_scatter  unordered scatter into the cell ranges
+//   k_cell_finish  per-cell insertion sort by particle index (restores the
+//                  reference's stable order) + gather of positions into rank
+//                  order (SoA) and the rank -> cell map
+#include "common.cuh"
+
+namespace rb {
+
+__device__ __forceinline__ int cell_index_1d(double x, double origin, double inv, int n) {
+    // python int() truncates toward zero; numba's int() is the same fptosi
+    double t = xmul(xsub(x, origin), inv);
+    long long c = (long long)t;
+    if (c < 0) c = 0;
+    else if (c >= n) c = n - 1;
+    return (int)c;
+}
+
+__global__ void k_bin_count(rb_grid g, int64_t n, const double *__restrict__ pos,
+                            int32_t *__restrict__ cell_of, int32_t *__restrict__ count) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+    int cx = cell_index_1d(x, g.origin[0], g.inv_cell[0], g.cells[0]);
+    int cy = cell_index_1d(y, g.origin[1], g.inv_cell[1], g.cells[1]);
+    int cz = cell_index_1d(z, g.origin[2], g.inv_cell[2], g.cells[2]);
+    int c = (cx * g.cells[1] + cy) * g.cells[2] + cz;
+    cell_of[i] = c;
+    atomicAdd(&count[c], 1);
+}
+
+__global__ void k_bin_scatter(int64_t n, const int32_t *__restrict__ cell_of,
+                              int32_t *__restrict__ cursor, int32_t *__restrict__ parts) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int slot = atomicAdd(&cursor[cell_of[i]], 1);
+    parts[slot] = (int32_t)i;
+}
+
+__global__ void k_cell_finish(int64_t ncell, const int32_t *__restrict__ start,
+                              int32_t *__restrict__ parts, int32_t *__restrict__ cell_of_rank,
+                              const double *__restrict__ pos, double *__restrict__ xs,
+                              double *__restrict__ ys, double *__restrict__ zs) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    int b = start[c], e = start[c + 1];
+    // insertion sort of the (short) cell segment by particle index
+    for (int a = b + 1; a < e; a++) {
+        int v = parts[a];
+        int k = a - 1;
+        while (k >= b && parts[k] > v) {
+            parts[k + 1] = parts[k];
+            k--;
+        }
+        parts[k + 1] = v;
+    }
+    for (int r = b; r < e; r++) {
+        int p = parts[r];
+        cell_of_rank[r] = (int32_t)c;
+        xs[r] = pos[3 * (int64_t)p];
+        ys[r] = pos[3 * (int64_t)p + 1];
+        zs[r] = pos[3 * (int64_t)p + 2];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan of int32 counts into out[0..n] (out[n] = total)
+// three phases: per-tile sums, scan of tile sums (one CTA), per-tile scan
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int *warp_sums, int &total) {
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int nw = blockDim.x >> 5;
+        int s = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, off);
+            if (lane >= off) s += y;
+        }
+        if (lane < nw) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    int warp_off = warp ? warp_sums[warp - 1] : 0;
+    total = warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return warp_off + x - v;
+}
+
+__global__ void k_scan_tile_sums(int64_t n, const int32_t *__restrict__ in,
+                                 int32_t *__restrict__ tile_sums) {
+    __shared__ int warp_sums[32];
+    int64_t base = (int64_t)blockIdx.x * kScanTile;
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        int64_t i = base + (int64_t)threadIdx.x * kScanItems + k;
+        if (i < n) s += in[i];
+    }
+    int total;
+    block_exclusive_scan(s, warp_sums, total);
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void k_scan_tile_offsets(int64_t ntiles, int32_t *__restrict__ tile_sums) {
+    __shared__ int warp_sums[32];
+    int carry = 0;
+    for (int64_t base = 0; base < ntiles; base += blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        int v = i < ntiles ? tile_sums[i] : 0;
+        int total;
+        int ex = block_exclusive_scan(v, warp_sums, total);
+        if (i < ntiles) tile_sums[i] = carry + ex;
+        carry += total;
+    }
+}
+
+__global__ void k_scan_apply(int64_t n, const int32_t *__restrict__ in,
+                             const int32_t *__restrict__ tile_off, int32_t *__restrict__ out) {
+    __shared__ int warp_sums[32];
+    int64_t base = (int64_t)blockIdx.x * kScanTile;
+    int vals[kScanItems];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        int64_t i = base + (int64_t)threadIdx.x * kScanItems + k;
+        vals[k] = i < n ? in[i] : 0;
+        s += vals[k];
+    }
+    int total;
+    int ex = block_exclusive_scan(s, warp_sums, total) + tile_off[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        int64_t i = base + (int64_t)threadIdx.x * kScanItems + k;
+        if (i < n) out[i] = ex;
+        ex += vals[k];
+        if (i == n - 1) out[n] = ex;
+    }
+}
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// scratch layout: cell_of[n] | count[ncell] | cursor[ncell] | tiles[ntiles]
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+}  // namespace rb
+
+using namespace rb;
+
+extern "C" size_t rb_bin_scratch_bytes(int64_t n, int64_t ncell) {
+    int64_t ntiles = ceil_div(ncell > 0 ? ncell : 1, kScanTile);
+    return align256(sizeof(int32_t) * (size_t)(n > 0 ? n : 1)) +
+           2 * align256(sizeof(int32_t) * (size_t)ncell) +
+           align256(sizeof(int32_t) * (size_t)ntiles);
+}
+
+extern "C" int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_start,
+                      int32_t *cell_particles, int32_t *cell_of_rank, double *xs, double *ys,
+                      double *zs, void *scratch, size_t scratch_bytes, void *stream) {
+    if (!g || n < 0) return RB_ERR_ARGUMENT;
+    int64_t ncell = (int64_t)g->cells[0] * g->cells[1] * g->cells[2];
+    if (ncell <= 0) return RB_ERR_GEOMETRY;
+    if (scratch_bytes < rb_bin_scratch_bytes(n, ncell)) return RB_ERR_ARGUMENT;
+    cudaStream_t st = as_stream(stream);
+    char *p = (char *)scratch;
+    int32_t *cell_of = (int32_t *)p;
+    p += align256(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    int32_t *count = (int32_t *)p;
+    p += align256(sizeof(int32_t) * (size_t)ncell);
+    int32_t *cursor = (int32_t *)p;
+    p += align256(sizeof(int32_t) * (size_t)ncell);
+    int32_t *tiles = (int32_t *)p;
+    int64_t ntiles = ceil_div(ncell, kScanTile);
+
+    cudaMemsetAsync(count, 0, sizeof(int32_t) * (size_t)ncell, st);
+    const int tb = 256;
+    if (n > 0) k_bin_count<<<(unsigned)ceil_div(n, tb), tb, 0, st>>>(*g, n, pos, cell_of, count);
+    if (n > 0) note_launches(1);
+    k_scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(ncell, count, tiles);
+    note_launches(1);
+    k_scan_tile_offsets<<<1, 1024, 0, st>>>(ntiles, tiles);
+    note_launches(1);
+    k_scan_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(ncell, count, tiles, cell_start);
+    note_launches(1);
+    if (n > 0) {
+        cudaMemcpyAsync(cursor, cell_start, sizeof(int32_t) * (size_t)ncell,
+                        cudaMemcpyDeviceToDevice, st);
+        k_bin_scatter<<<(unsigned)ceil_div(n, tb), tb, 0, st>>>(n, cell_of, cursor,
+                                                                 cell_particles);
+        note_launches(1);
+        k_cell_finish<<<(unsigned)ceil_div(ncell, tb), tb, 0, st>>>(
+            ncell, cell_start, cell_particles, cell_of_rank, pos, xs, ys, zs);
+        note_launches(1);
+    }
+    return launch_status();
+}

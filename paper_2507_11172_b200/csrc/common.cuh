@@ -1,0 +1,155 @@
+// common.cuh -- shared device helpers for the sm_100a force-evaluation path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/respa_b200.h"
+
+#define RB_MIN_DISTANCE_SQ (1e-10 * 1e-10)  // respamd/potentials.py:35-36
+
+namespace rb {
+
+constexpr int kWarp = 32;
+
+static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// host-side count of kernel launches issued by this library (rb_launch_count)
+void note_launches(int k);
+
+static inline int launch_status() {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RB_OK : RB_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// Exact reference arithmetic.  nvcc contracts a*b+c into FMA by default; the
+// reference (numba) rounds every mul and add separately, and the cutoff
+// predicate must reproduce it bit for bit, so these use the _rn intrinsics
+// that are never contracted.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+
+// single-shift minimum image, respamd/containers.py:341-353 (d = a - b first)
+__device__ __forceinline__ double min_image(double d, double box, double half) {
+    if (d > half) return xsub(d, box);
+    if (d < -half) return xadd(d, box);
+    return d;
+}
+
+// r^2 = dx*dx + dy*dy + dz*dz rounded as numba evaluates it (left to right)
+__device__ __forceinline__ double exact_r2(double dx, double dy, double dz) {
+    return xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
+}
+
+struct Image {
+    double box[3];
+    double half[3];
+    int periodic;
+};
+
+__host__ __device__ inline Image make_image(const rb_grid &g) {
+    Image im;
+    for (int d = 0; d < 3; d++) {
+        im.box[d] = g.box[d];
+        im.half[d] = 0.5 * g.box[d];
+    }
+    im.periodic = g.periodic;
+    return im;
+}
+
+// exact displacement a - b with the reference's minimum image
+__device__ __forceinline__ void exact_disp(const Image &im, double ax, double ay, double az,
+                                           double bx, double by, double bz, double &dx,
+                                           double &dy, double &dz) {
+    dx = xsub(ax, bx);
+    dy = xsub(ay, by);
+    dz = xsub(az, bz);
+    if (im.periodic) {
+        dx = min_image(dx, im.box[0], im.half[0]);
+        dy = min_image(dy, im.box[1], im.half[1]);
+        dz = min_image(dz, im.box[2], im.half[2]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// status word: (tag << 8) | kind, reduced with atomicMin
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void record_status(unsigned long long *status, int64_t tag, int kind) {
+    if (status) atomicMin(status, ((unsigned long long)tag << 8) | (unsigned long long)kind);
+}
+
+// Tag of the current kernel: the explicit value, or (tag < 0) the step
+// counter kept in status[1] by rb_step_begin (lets a captured CUDA graph be
+// replayed for many steps).
+__device__ __forceinline__ int64_t resolve_tag(int64_t tag, const unsigned long long *status) {
+    if (tag >= 0 || !status) return tag < 0 ? 0 : tag;
+    return (int64_t)(*(volatile const unsigned long long *)(status + 1));
+}
+
+// True when a kernel of step `tag` whose own error kind is `kind` must not
+// run: an earlier step failed, or an error of higher precedence (lower kind)
+// was raised earlier in the same step.
+__device__ __forceinline__ bool frozen(const unsigned long long *status, int64_t tag, int kind) {
+    if (!status) return false;
+    unsigned long long s = *(volatile const unsigned long long *)status;
+    if (s == RB_STATUS_CLEAR) return false;
+    long long t = (long long)(s >> 8);
+    int k = (int)(s & 0xff);
+    if (t < tag) return true;
+    if (t == tag && k < kind && k != RB_KIND_NONFINITE && k != RB_KIND_CAPACITY) return true;
+    return false;
+}
+
+// warp-uniform variant: lane 0 reads, everyone agrees (needed before shuffles)
+__device__ __forceinline__ bool warp_frozen(const unsigned long long *status, int64_t tag,
+                                            int kind) {
+    int f = 0;
+    if ((threadIdx.x & 31) == 0) f = frozen(status, tag, kind) ? 1 : 0;
+    return __shfl_sync(0xffffffffu, f, 0) != 0;
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <int kWidth>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int off = kWidth / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off, kWidth);
+    return v;
+}
+
+template <int kWidth>
+__device__ __forceinline__ int group_sum_int(int v) {
+#pragma unroll
+    for (int off = kWidth / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off, kWidth);
+    return v;
+}
+
+// neighbour cell of base cell (cx,cy,cz) at offset o; -1 when outside an
+// open grid (respamd/containers.py:319-333)
+__device__ __forceinline__ int neighbor_cell(const rb_grid &g, int cx, int cy, int cz, int o) {
+    int x = cx + g.offsets[o][0];
+    int y = cy + g.offsets[o][1];
+    int z = cz + g.offsets[o][2];
+    if (g.periodic) {
+        // canonical offsets are already wrapped into [0, cells)
+        if (x >= g.cells[0]) x -= g.cells[0];
+        if (y >= g.cells[1]) y -= g.cells[1];
+        if (z >= g.cells[2]) z -= g.cells[2];
+    } else if (x < 0 || x >= g.cells[0] || y < 0 || y >= g.cells[1] || z < 0 ||
+               z >= g.cells[2]) {
+        return -1;
+    }
+    return (x * g.cells[1] + y) * g.cells[2] + z;
+}
+
+}  // namespace rb

@@ -1,0 +1,335 @@
+// integrate.cu -- fused r-RESPA kick/drift, deterministic reductions and the
+// measurement helpers bench.py uses.
+//
+// The updates restate the numpy statements of respamd/integrators.py:148-170
+// with numpy's rounding order (every product and sum rounded separately, so
+// the _rn intrinsics keep nvcc from contracting them into FMAs):
+//
+//   drift (tag = i+1):  if i % s == 0:  v = v + half_respa*f3          (:149-150)
+//                       x = x + (dt*v + half_drift*f2_old)              (:151)
+//                       wrap into [0, box)                              (:152-153)
+//   kick  (tag = i+1):  v = v + half_dt*(f2_old + f2_new)              (:158)
+//                       if (i+1) % s == 0:  v = v + half_respa*f3       (:165)
+//
+// Arrays are the reference's (n,3) AoS, handled as flat 3n streams.
+#include "common.cuh"
+
+#include <atomic>
+
+namespace rb {
+
+static std::atomic<long long> g_launches{0};
+void note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// numpy float remainder (npy_divmod) followed by the edge fix of
+// respamd/model.py:279-280
+__device__ __forceinline__ double wrap_coord(double x, double box) {
+    double r = fmod(x, box);
+    if (r != 0.0) {
+        if (r < 0.0) r = xadd(r, box);
+    } else {
+        r = 0.0;  // copysign(0, box) with box > 0
+    }
+    if (r >= box) r = 0.0;
+    return r;
+}
+
+__global__ void k_drift(int64_t n3, double *__restrict__ pos, double *__restrict__ vel,
+                        const double *__restrict__ f2_old, const double *__restrict__ f3, double bx,
+                        double by, double bz, int periodic, double dt, double half_drift,
+                        double half_respa, int kick3, unsigned long long *status, int64_t tag) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n3) return;
+    tag = resolve_tag(tag, status);
+    if (frozen(status, tag, 0)) return;
+    double v = vel[i];
+    if (kick3) {
+        v = xadd(v, xmul(half_respa, f3[i]));
+        vel[i] = v;
+    }
+    double x = xadd(pos[i], xadd(xmul(dt, v), xmul(half_drift, f2_old[i])));
+    if (periodic) {
+        const int c = (int)(i % 3);
+        x = wrap_coord(x, c == 0 ? bx : (c == 1 ? by : bz));
+    }
+    pos[i] = x;
+    if (!isfinite(x)) record_status(status, tag, RB_KIND_NONFINITE);
+}
+
+__global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict__ f2_old,
+                       const double *__restrict__ f2_new, const double *__restrict__ f3,
+                       double half_dt, double half_respa, int kick3, unsigned long long *status,
+                       int64_t tag) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n3) return;
+    tag = resolve_tag(tag, status);
+    bool do_kick2 = true, do_kick3 = kick3 != 0;
+    if (status) {
+        const unsigned long long s = *(volatile const unsigned long long *)status;
+        if (s != RB_STATUS_CLEAR) {
+            const long long t = (long long)(s >> 8);
+            const int k = (int)(s & 0xff);
+            if (t < tag) return;
+            if (t == tag && k == RB_KIND_PAIR_MIN_SEPARATION) return;  // raised before :158
+            if (t == tag && k == RB_KIND_TRIPLET_MIN_SEPARATION) do_kick3 = false;  // before :165
+        }
+    }
+    double v = vel[i];
+    const double fnew = f2_new[i];
+    if (do_kick2) v = xadd(v, xmul(half_dt, xadd(f2_old[i], fnew)));
+    if (do_kick3) v = xadd(v, xmul(half_respa, f3[i]));
+    vel[i] = v;
+    f2_old[i] = fnew;  // np.copyto(f2_old, forces_2b), integrators.py:159
+    if (!isfinite(v)) record_status(status, tag, RB_KIND_NONFINITE);
+}
+
+// ---------------------------------------------------------------------------
+// deterministic sums: the partition depends only on n, each CTA sums its
+// contiguous slice with a fixed per-thread stride and a fixed tree, then one
+// CTA sums the partials in index order.
+// ---------------------------------------------------------------------------
+constexpr int kRedThreads = 256;
+constexpr int kRedMaxBlocks = 592;  // 4 x 148 SMs
+
+static int red_blocks(int64_t n) {
+    int64_t b = (n + 4095) / 4096;
+    if (b < 1) b = 1;
+    if (b > kRedMaxBlocks) b = kRedMaxBlocks;
+    return (int)b;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_tree_sum(T v, T *sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    T s = 0;
+    if (warp == 0) {
+        s = lane < (int)(blockDim.x >> 5) ? sh[lane] : (T)0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    }
+    return s;
+}
+
+template <typename Tin, typename Tacc, bool kSquare>
+__global__ void k_partial_sum(int64_t n, const Tin *__restrict__ in, Tacc *__restrict__ partial) {
+    __shared__ Tacc sh[32];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b = (int64_t)blockIdx.x * chunk;
+    const int64_t e = b + chunk < n ? b + chunk : n;
+    Tacc acc = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        Tacc v = (Tacc)in[i];
+        acc += kSquare ? v * v : v;
+    }
+    Tacc s = block_tree_sum<Tacc>(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+template <typename Tacc>
+__global__ void k_final_sum(int nb, const Tacc *__restrict__ partial, Tacc *__restrict__ out) {
+    __shared__ Tacc sh[32];
+    Tacc acc = 0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) acc += partial[i];
+    Tacc s = block_tree_sum<Tacc>(acc, sh);
+    if (threadIdx.x == 0) out[0] = s;
+}
+
+template <typename Tin, typename Tacc, bool kSquare>
+static int reduce_launch(int64_t n, const Tin *in, Tacc *out, void *scratch, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    const int nb = red_blocks(n);
+    Tacc *partial = (Tacc *)scratch;
+    k_partial_sum<Tin, Tacc, kSquare><<<nb, kRedThreads, 0, st>>>(n, in, partial);
+    note_launches(1);
+    k_final_sum<Tacc><<<1, kRedThreads, 0, st>>>(nb, partial, out);
+    note_launches(1);
+    return launch_status();
+}
+
+// ---------------------------------------------------------------------------
+// measurement helpers
+// ---------------------------------------------------------------------------
+constexpr int kPeakChains = 8;
+
+__global__ void k_fp64_fma(int iters, double seed, double *sink) {
+    double a[kPeakChains];
+#pragma unroll
+    for (int c = 0; c < kPeakChains; c++) a[c] = seed + c * 1e-3 + threadIdx.x * 1e-9;
+    const double m = 0.999999999, k = 1e-9;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+#pragma unroll
+            for (int c = 0; c < kPeakChains; c++) a[c] = fma(a[c], m, k);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < kPeakChains; c++) s += a[c];
+    if (s == 12345.678) sink[0] = s;  // keep the chains alive
+}
+
+__global__ void k_step_begin(unsigned long long *status) { status[1] += 1ull; }
+
+// trace row (tag / interval): [tag, sum v^2, E2, W2, E3, W3, 0, 0]
+__global__ void k_trace_record(const unsigned long long *status, int64_t interval, double *trace,
+                               const double *sumsq, const double *e2, const double *w2,
+                               const double *e3, const double *w3) {
+    const int64_t tag = (int64_t)status[1];
+    double *row = trace + 8 * (tag / interval);
+    row[0] = (double)tag;
+    row[1] = *sumsq;
+    row[2] = *e2;
+    row[3] = *w2;
+    row[4] = *e3;
+    row[5] = *w3;
+    row[6] = 0.0;
+    row[7] = 0.0;
+}
+
+__global__ void k_flush(int4 *buf, int64_t n16, int v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+         i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = make_int4(v, v, v, v);
+}
+
+}  // namespace rb
+
+using namespace rb;
+
+extern "C" int rb_respa_drift(int64_t n, double *pos, double *vel, const double *f2_old,
+                              const double *f3, const double *box3_host, int32_t periodic,
+                              double dt, double half_drift, double half_respa, int32_t kick3,
+                              unsigned long long *status, int64_t tag, void *stream) {
+    if (n < 0 || !box3_host) return RB_ERR_ARGUMENT;
+    if (n == 0) return RB_OK;
+    const int64_t n3 = 3 * n;
+    const int tb = 256;
+    k_drift<<<(unsigned)((n3 + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
+        n3, pos, vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt,
+        half_drift, half_respa, kick3, status, tag);
+    note_launches(1);
+    return launch_status();
+}
+
+extern "C" int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f2_new,
+                             const double *f3, double half_dt, double half_respa, int32_t kick3,
+                             unsigned long long *status, int64_t tag, void *stream) {
+    if (n < 0) return RB_ERR_ARGUMENT;
+    if (n == 0) return RB_OK;
+    const int64_t n3 = 3 * n;
+    const int tb = 256;
+    k_kick<<<(unsigned)((n3 + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
+        n3, vel, f2_old, f2_new, f3, half_dt, half_respa, kick3, status, tag);
+    note_launches(1);
+    return launch_status();
+}
+
+extern "C" size_t rb_reduce_scratch_bytes(int64_t n) {
+    return (size_t)kRedMaxBlocks * sizeof(double);
+}
+
+extern "C" int rb_reduce_sum_f64(int64_t n, const double *in, double *out, void *scratch,
+                                 void *stream) {
+    if (n < 0 || !out || !scratch) return RB_ERR_ARGUMENT;
+    return reduce_launch<double, double, false>(n, in, out, scratch, stream);
+}
+
+extern "C" int rb_reduce_sumsq_f64(int64_t n, const double *in, double *out, void *scratch,
+                                   void *stream) {
+    if (n < 0 || !out || !scratch) return RB_ERR_ARGUMENT;
+    return reduce_launch<double, double, true>(n, in, out, scratch, stream);
+}
+
+extern "C" int rb_reduce_sum_i32(int64_t n, const int32_t *in, int64_t *out, void *scratch,
+                                 void *stream) {
+    if (n < 0 || !out || !scratch) return RB_ERR_ARGUMENT;
+    return reduce_launch<int32_t, long long, false>(n, in, (long long *)out, scratch, stream);
+}
+
+extern "C" int rb_fp64_peak(int32_t iters, double *tflops, void *stream) {
+    if (iters <= 0 || !tflops) return RB_ERR_ARGUMENT;
+    cudaStream_t st = as_stream(stream);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double *sink = nullptr;
+    if (cudaMalloc(&sink, sizeof(double)) != cudaSuccess) return RB_ERR_CUDA;
+    const int threads = 512, blocks = sms * 4;
+    k_fp64_fma<<<blocks, threads, 0, st>>>(iters / 4 + 1, 1.0, sink);
+    note_launches(1);  // warm-up
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    k_fp64_fma<<<blocks, threads, 0, st>>>(iters, 1.0, sink);
+    note_launches(1);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    const double flops = 2.0 * (double)blocks * threads * (double)iters * 16.0 * kPeakChains;
+    *tflops = flops / ((double)ms * 1e-3) / 1e12;
+    return launch_status();
+}
+
+extern "C" int rb_step_begin(unsigned long long *status, void *stream) {
+    if (!status) return RB_ERR_ARGUMENT;
+    k_step_begin<<<1, 1, 0, as_stream(stream)>>>(status);
+    note_launches(1);
+    return launch_status();
+}
+
+extern "C" int rb_trace_record(const unsigned long long *status, int64_t sample_interval,
+                               double *trace, const double *sumsq, const double *e2,
+                               const double *w2, const double *e3, const double *w3,
+                               void *stream) {
+    if (!status || !trace || sample_interval <= 0) return RB_ERR_ARGUMENT;
+    k_trace_record<<<1, 1, 0, as_stream(stream)>>>(status, sample_interval, trace, sumsq, e2, w2,
+                                                   e3, w3);
+    note_launches(1);
+    return launch_status();
+}
+
+extern "C" int rb_l2_flush(void *buf, size_t bytes, void *stream) {
+    if (!buf) return RB_ERR_ARGUMENT;
+    static int v = 0;
+    v++;
+    k_flush<<<148 * 8, 256, 0, as_stream(stream)>>>((int4 *)buf, (int64_t)(bytes / 16), v);
+    note_launches(1);
+    return launch_status();
+}
+
+extern "C" int rb_abi_version(void) { return RB_ABI_VERSION; }
+
+extern "C" long long rb_launch_count(void) { return g_launches.load(); }
+
+extern "C" size_t rb_grid_bytes(void) { return sizeof(rb_grid); }
+
+extern "C" const char *rb_status_string(int status) {
+    switch (status) {
+        case RB_OK: return "ok";
+        case RB_ERR_MIN_SEPARATION: return "minimum separation violated";
+        case RB_ERR_GEOMETRY: return "invalid cell-grid geometry";
+        case RB_ERR_CUDA: return "CUDA launch error";
+        case RB_ERR_CAPACITY: return "neighbour-row capacity exceeded";
+        case RB_ERR_ARGUMENT: return "invalid argument";
+        default: return "unknown status";
+    }
+}
+
+extern "C" int rb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}

@@ -1,0 +1,96 @@
+// lj.cu -- Lennard-Jones pair pass over the neighbour rows.
+//
+// Replaces respamd/containers.py:282-370 (_c01_pair_kernel) with the same
+// owner-computes discipline: each particle accumulates only its own force,
+// every pair is visited from both sides and contributes phi/2 and
+// scale*r^2/2 per visit (:364-365).  A group of kGroup lanes serves one
+// particle: lanes stride over the row, then a fixed xor-shuffle tree sums the
+// partials, so the result does not depend on scheduling.
+//
+// The cutoff predicate and the guard use the reference's exact pair-distance
+// arithmetic; the LJ kernel itself (potentials.py:55-67) is restated with one
+// reciprocal instead of two divides (agreement ~1e-16 relative).
+#include "common.cuh"
+
+namespace rb {
+
+constexpr int kLjGroup = 8;
+constexpr int kLjThreads = 256;
+
+__global__ void __launch_bounds__(kLjThreads)
+    k_lj(rb_grid g, int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
+         const double *__restrict__ zs, const int32_t *__restrict__ parts,
+         const int32_t *__restrict__ rows, const int32_t *__restrict__ row_count,
+         int32_t capacity, double rc2, double eps24, double eps4, double sigma2,
+         double *__restrict__ forces, double *__restrict__ energy_rank,
+         double *__restrict__ virial_rank, unsigned long long *status, int64_t tag) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = gid / kLjGroup;
+    const int sub = (int)(gid % kLjGroup);
+    const bool active = r < n;
+    tag = resolve_tag(tag, status);
+    if (warp_frozen(status, tag, RB_KIND_PAIR_MIN_SEPARATION)) return;
+    const Image im = make_image(g);
+    double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
+    bool bad = false;
+    if (active) {
+        const double xi = xs[r], yi = ys[r], zi = zs[r];
+        const int m = row_count[r];
+        const int32_t *row = rows + r * (int64_t)capacity;
+        for (int k = sub; k < m; k += kLjGroup) {
+            const int j = row[k];
+            double dx, dy, dz;
+            exact_disp(im, xi, yi, zi, xs[j], ys[j], zs[j], dx, dy, dz);
+            const double r2 = exact_r2(dx, dy, dz);
+            if (r2 > rc2) continue;
+            if (r2 < RB_MIN_DISTANCE_SQ) {
+                bad = true;
+                continue;
+            }
+            const double inv_r2 = 1.0 / r2;
+            const double x = sigma2 * inv_r2;
+            const double r6 = x * x * x;
+            const double r12 = r6 * r6;
+            const double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
+            fx += scale * dx;
+            fy += scale * dy;
+            fz += scale * dz;
+            e += eps4 * (r12 - r6);
+            w += scale * r2;
+        }
+    }
+    fx = group_sum<kLjGroup>(fx);
+    fy = group_sum<kLjGroup>(fy);
+    fz = group_sum<kLjGroup>(fz);
+    e = group_sum<kLjGroup>(e);
+    w = group_sum<kLjGroup>(w);
+    if (active && bad) record_status(status, tag, RB_KIND_PAIR_MIN_SEPARATION);
+    if (active && sub == 0) {
+        const int64_t p = parts[r];
+        forces[3 * p] = fx;
+        forces[3 * p + 1] = fy;
+        forces[3 * p + 2] = fz;
+        energy_rank[r] = 0.5 * e;
+        virial_rank[r] = 0.5 * w;
+    }
+}
+
+}  // namespace rb
+
+using namespace rb;
+
+extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
+                          const double *zs, const int32_t *cell_particles, const int32_t *rows,
+                          const int32_t *row_count, int32_t capacity, double rc, double epsilon,
+                          double sigma, double *forces, double *energy_rank, double *virial_rank,
+                          unsigned long long *status, int64_t tag, void *stream) {
+    if (!g || n < 0 || capacity <= 0) return RB_ERR_ARGUMENT;
+    if (n == 0) return RB_OK;
+    const int64_t threads = n * kLjGroup;
+    unsigned blocks = (unsigned)((threads + kLjThreads - 1) / kLjThreads);
+    k_lj<<<blocks, kLjThreads, 0, as_stream(stream)>>>(
+        *g, n, xs, ys, zs, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
+        4.0 * epsilon, sigma * sigma, forces, energy_rank, virial_rank, status, tag);
+    note_launches(1);
+    return launch_status();
+}

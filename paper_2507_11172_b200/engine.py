@@ -1,0 +1,219 @@
+"""Device workspace and pass sequencing for the sm_100a kernels.
+
+``ForceEngine`` owns the device buffers of one particle count (torch CUDA
+tensors as plain memory) and issues the C-ABI passes on the current torch
+stream:
+
+    bin (counting sort, containers.py:175-209)
+      -> nlist (survivor rows, :437-474)
+      -> lj   (pair pass, :282-370)      -> deterministic sums
+      -> atm  (triplet pass, :373-535)   -> deterministic sums
+
+Every buffer lives in HBM for the whole run; nothing is reallocated per
+step.  Positions stay in the reference's (n,3) AoS particle order; the
+binning gathers a rank-ordered SoA copy (xs, ys, zs) for the force kernels,
+which write forces straight back into particle order.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .grid import Geometry, rb_grid
+from ._lib import ptr
+
+SCALAR_SUMSQ, SCALAR_E2, SCALAR_W2, SCALAR_E3, SCALAR_W3 = 0, 1, 2, 3, 4
+
+
+def _round_up(x: int, m: int) -> int:
+    return int((x + m - 1) // m * m)
+
+
+class CapacityError(RuntimeError):
+    """A neighbour row outgrew its capacity inside a device-resident run."""
+
+
+class ForceEngine:
+    """Device buffers + pass launches for `n` particles."""
+
+    def __init__(self, n: int, device: Optional[int] = None):
+        torch = _lib.require_device()
+        self.torch = torch
+        self.L = _lib.lib()
+        self.n = int(n)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        dev, f64, i32, i64 = self.device, torch.float64, torch.int32, torch.int64
+        n = max(self.n, 1)
+        self.pos = torch.zeros((n, 3), dtype=f64, device=dev)
+        self.xs = torch.empty(n, dtype=f64, device=dev)
+        self.ys = torch.empty(n, dtype=f64, device=dev)
+        self.zs = torch.empty(n, dtype=f64, device=dev)
+        self.parts = torch.empty(n, dtype=i32, device=dev)
+        self.cell_of_rank = torch.empty(n, dtype=i32, device=dev)
+        self.e_rank = torch.zeros(n, dtype=f64, device=dev)
+        self.w_rank = torch.zeros(n, dtype=f64, device=dev)
+        self.v_rank = torch.zeros(n, dtype=i32, device=dev)
+        self.row_count = torch.zeros(n, dtype=i32, device=dev)
+        self.max_count = torch.zeros(1, dtype=i32, device=dev)
+        # status[0]: error word (all ones = clear); status[1]: device step counter
+        self.status = torch.tensor([-1, 0], dtype=i64, device=dev)
+        self.scalars = torch.zeros(8, dtype=f64, device=dev)
+        self.visits = torch.zeros(1, dtype=i64, device=dev)
+        self.red_scratch = torch.empty(
+            max(1, int(self.L.rb_reduce_scratch_bytes(n * 3)) // 8), dtype=f64, device=dev)
+        self.cell_start = None
+        self.bin_scratch = None
+        self.rows = None
+        self.capacity = 0
+        self._geom_key = None
+        self._grid = None
+
+    # ------------------------------------------------------------------ misc
+    @property
+    def stream(self):
+        return _lib.stream_handle()
+
+    def grid_struct(self, geom: Geometry):
+        key = (geom.cells, geom.cell_size, geom.origin, geom.inv_cell, geom.periodic, geom.box,
+               geom.cutoff)
+        if key != self._geom_key:
+            self._grid = rb_grid(geom)
+            self._geom_key = key
+        return self._grid
+
+    def reset_status(self, step: int = 0) -> None:
+        self.status[0] = -1
+        self.status[1] = int(step)
+
+    def read_status(self):
+        """(tag, kind) of the first recorded device error, or None (syncs)."""
+        word = int(self.status[0].item()) & 0xFFFFFFFFFFFFFFFF
+        if word == _lib.RB_STATUS_CLEAR:
+            return None
+        return word >> 8, word & 0xFF
+
+    def upload_positions(self, positions: np.ndarray) -> None:
+        src = np.ascontiguousarray(positions, dtype=np.float64)
+        self.pos.copy_(self.torch.from_numpy(src), non_blocking=False)
+
+    # --------------------------------------------------------------- binning
+    def _ensure_cells(self, ncell: int) -> None:
+        torch = self.torch
+        if self.cell_start is None or self.cell_start.numel() < ncell + 1:
+            self.cell_start = torch.zeros(ncell + 1, dtype=torch.int32, device=self.device)
+        need = int(self.L.rb_bin_scratch_bytes(self.n, ncell))
+        if self.bin_scratch is None or self.bin_scratch.numel() < need:
+            self.bin_scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+
+    def bin(self, geom: Geometry, pos=None) -> None:
+        pos = self.pos if pos is None else pos
+        self._ensure_cells(geom.num_cells)
+        g = self.grid_struct(geom)
+        st = self.L.rb_bin(ctypes.byref(g), self.n, ptr(pos), ptr(self.cell_start), ptr(self.parts),
+                           ptr(self.cell_of_rank), ptr(self.xs), ptr(self.ys), ptr(self.zs),
+                           ptr(self.bin_scratch), self.bin_scratch.numel(), self.stream)
+        _lib.check(st, "rb_bin")
+
+    # ------------------------------------------------------- neighbour rows
+    def estimate_capacity(self, geom: Geometry, r_list: float) -> int:
+        """Row capacity from the densest cell of the current binning (syncs)."""
+        counts = self.cell_start[1:geom.num_cells + 1] - self.cell_start[:geom.num_cells]
+        max_occ = int(counts.max().item()) if geom.num_cells else 1
+        vol = float(np.prod(geom.cell_size))
+        dens = max(max_occ / vol, self.n / float(np.prod(geom.box)))
+        est = dens * 4.0 / 3.0 * math.pi * r_list ** 3
+        return int(min(4096, max(32, _round_up(int(1.3 * est) + 32, 32), min(self.n, 4096))))
+
+    def _ensure_rows(self, capacity: int) -> None:
+        if self.rows is None or self.capacity != capacity:
+            self.rows = self.torch.empty(max(self.n, 1) * capacity, dtype=self.torch.int32,
+                                         device=self.device)
+            self.capacity = capacity
+
+    def nlist(self, geom: Geometry, r_list: float, capacity: Optional[int] = None,
+              checked: bool = True) -> None:
+        """Build rows within r_list.  ``checked`` syncs and grows the capacity
+        until no row overflows (container path); the device loop passes
+        ``checked=False`` and inspects ``max_count`` at its sync points."""
+        if capacity is None:
+            capacity = self.capacity or self.estimate_capacity(geom, r_list)
+        while True:
+            self._ensure_rows(capacity)
+            self.max_count.zero_()
+            g = self.grid_struct(geom)
+            st = self.L.rb_nlist(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
+                                 ptr(self.cell_start), ptr(self.cell_of_rank), float(r_list),
+                                 int(self.capacity), ptr(self.rows), ptr(self.row_count),
+                                 ptr(self.max_count), self.stream)
+            _lib.check(st, "rb_nlist")
+            if not checked:
+                return
+            worst = int(self.max_count.item())
+            if worst <= self.capacity:
+                return
+            if worst > 4096:
+                raise CapacityError(f"a neighbour row holds {worst} entries (> 4096)")
+            capacity = min(4096, _round_up(int(worst * 1.25) + 32, 32))
+
+    def overflowed(self) -> bool:
+        return int(self.max_count.item()) > self.capacity
+
+    # -------------------------------------------------------------- passes
+    def lj(self, geom: Geometry, rc: float, epsilon: float, sigma: float, forces,
+           tag: int = 0) -> None:
+        g = self.grid_struct(geom)
+        st = self.L.rb_lj_pass(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
+                               ptr(self.parts), ptr(self.rows), ptr(self.row_count),
+                               int(self.capacity), float(rc), float(epsilon), float(sigma),
+                               ptr(forces), ptr(self.e_rank), ptr(self.w_rank), ptr(self.status),
+                               int(tag), self.stream)
+        _lib.check(st, "rb_lj_pass")
+        self.sum_f64(self.e_rank, SCALAR_E2)
+        self.sum_f64(self.w_rank, SCALAR_W2)
+
+    def atm(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
+            count_visits: bool = True) -> None:
+        g = self.grid_struct(geom)
+        st = self.L.rb_atm_pass(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
+                                ptr(self.parts), ptr(self.rows), ptr(self.row_count),
+                                int(self.capacity), float(rc), float(nu), ptr(forces),
+                                ptr(self.e_rank), ptr(self.w_rank), ptr(self.v_rank),
+                                ptr(self.status), int(tag), self.stream)
+        _lib.check(st, "rb_atm_pass")
+        self.sum_f64(self.e_rank, SCALAR_E3)
+        self.sum_f64(self.w_rank, SCALAR_W3)
+        if count_visits:
+            st = self.L.rb_reduce_sum_i32(self.n, ptr(self.v_rank), ptr(self.visits),
+                                          ptr(self.red_scratch), self.stream)
+            _lib.check(st, "rb_reduce_sum_i32")
+
+    def visit_rows(self, geom: Geometry, rc: float) -> np.ndarray:
+        """Sorted (i, j, k) rows of every accepted visit (after :meth:`atm`)."""
+        torch = self.torch
+        counts = self.v_rank[: self.n].to(torch.int64)
+        offsets = torch.cumsum(counts, 0) - counts
+        total = int(counts.sum().item())
+        out = torch.empty(max(total, 1) * 3, dtype=torch.int32, device=self.device)
+        g = self.grid_struct(geom)
+        st = self.L.rb_atm_visit_rows(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys),
+                                      ptr(self.zs), ptr(self.parts), ptr(self.rows),
+                                      ptr(self.row_count), int(self.capacity), float(rc),
+                                      ptr(offsets), ptr(out), self.stream)
+        _lib.check(st, "rb_atm_visit_rows")
+        return out[: 3 * total].view(total, 3).cpu().numpy().astype(np.int64)
+
+    # ----------------------------------------------------------- reductions
+    def sum_f64(self, x, slot: int, square: bool = False, n: Optional[int] = None) -> None:
+        fn = self.L.rb_reduce_sumsq_f64 if square else self.L.rb_reduce_sum_f64
+        count = self.n if n is None else n
+        out = ctypes.c_void_p(self.scalars.data_ptr() + 8 * slot)
+        st = fn(count, ptr(x), out, ptr(self.red_scratch), self.stream)
+        _lib.check(st, "rb_reduce")
+
+    def scalar_values(self):
+        return self.scalars.cpu().numpy()

@@ -1,0 +1,372 @@
+"""Device-resident r-RESPA loop (the reference's L3, integrators.py:96-191).
+
+``respa_run`` keeps the reference signature and semantics
+(``respa_run(system, ff, container, schedule, sample_interval=None,
+hooks=()) -> RunTrace``) but runs every step on the GPU:
+
+* the state lives in HBM as the reference's (n,3) float64 arrays; the host
+  copy is written back at hook points and at the end of the run;
+* per base step: drift kernel (kick3 fused in at cycle starts), binning,
+  survivor rows, LJ pass, kick kernel (kick3 fused in at cycle ends, after
+  the triplet pass, which is recomputed only every ``s``-th step);
+* the rounding order of every update is numpy's (bit-exact trajectories
+  given identical forces);
+* failures (minimum separation, non-finite state) are recorded in a device
+  status word with the iteration they happened in; later kernels become
+  no-ops, so the state freezes exactly where ``IntegrationBlowUp`` would
+  have been raised, and the host raises it with the same iteration number;
+* one sampling period of steps is captured once as a CUDA graph and
+  replayed; the trace (kinetic energy, container scalars) is recorded on the
+  device and read back once.
+
+The container must be a :class:`~.containers.CudaLinkedCells`; there is no
+host fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import ptr
+from .containers import CudaLinkedCells, MinimumSeparationError
+from .engine import (SCALAR_E2, SCALAR_E3, SCALAR_SUMSQ, SCALAR_W2, SCALAR_W3, CapacityError,
+                     ForceEngine, _round_up)
+from .grid import geometry
+from .model import ValidationError, triplet_cutoff
+
+
+class IntegrationBlowUp(RuntimeError):
+    """State became non-finite or near-singular (``integrators.py:29-35``)."""
+
+    def __init__(self, iteration: int, reason: str, trace=None):
+        self.iteration = iteration
+        self.trace = trace if trace is not None else RunTrace()
+        super().__init__(f"integration blew up at iteration {iteration}: {reason}")
+
+
+@dataclass
+class RespaSchedule:
+    """Base step, step-size factor, iteration count (``integrators.py:38-60``)."""
+
+    dt: float
+    step_size_factor: int = 1
+    num_iterations: int = 0
+
+    def __post_init__(self):
+        self.dt = float(self.dt)
+        self.step_size_factor = int(self.step_size_factor)
+        self.num_iterations = int(self.num_iterations)
+        if not np.isfinite(self.dt) or self.dt <= 0:
+            raise ValidationError(f"dt must be finite and > 0, got {self.dt}")
+        if self.step_size_factor < 1:
+            raise ValidationError("step_size_factor must be >= 1")
+        if self.num_iterations < 0:
+            raise ValidationError("num_iterations must be >= 0")
+        if self.num_iterations % self.step_size_factor:
+            raise ValidationError(
+                f"num_iterations ({self.num_iterations}) must be a multiple of "
+                f"the step_size_factor ({self.step_size_factor})"
+            )
+
+
+@dataclass
+class RunTrace:
+    """Observables at full iterations (``integrators.py:63-86``)."""
+
+    iterations: list = field(default_factory=list)
+    kinetic: list = field(default_factory=list)
+    potential_2b: list = field(default_factory=list)
+    potential_3b: list = field(default_factory=list)
+    total: list = field(default_factory=list)
+    virial_2b: list = field(default_factory=list)
+    virial_3b: list = field(default_factory=list)
+
+    def record_values(self, iteration, kinetic, e2, w2, e3, w3) -> None:
+        self.iterations.append(int(iteration))
+        self.kinetic.append(float(kinetic))
+        self.potential_2b.append(float(e2))
+        self.potential_3b.append(float(e3))
+        self.total.append(float(kinetic) + float(e2) + float(e3))
+        self.virial_2b.append(float(w2))
+        self.virial_3b.append(float(w3))
+
+    def record(self, iteration: int, system, container) -> None:
+        kin = 0.5 * system.mass * float(np.sum(system.velocities * system.velocities))
+        self.record_values(iteration, kin, container.pair_energy, container.pair_virial,
+                           container.triplet_energy, container.triplet_virial)
+
+    def __len__(self):
+        return len(self.iterations)
+
+
+_MSG = {
+    _lib.RB_KIND_PAIR_MIN_SEPARATION: "particles closer than the minimum separation guard; "
+                                      "the configuration is (nearly) singular",
+    _lib.RB_KIND_TRIPLET_MIN_SEPARATION: "particles closer than the minimum separation guard; "
+                                         "the configuration is (nearly) singular",
+    _lib.RB_KIND_NONFINITE: "non-finite position or velocity",
+}
+
+
+class DeviceRespa:
+    """One device-resident r-RESPA run (all buffers allocated up front)."""
+
+    def __init__(self, system, ff, container, schedule: RespaSchedule, sample_interval: int,
+                 capacity: Optional[int] = None, use_graph: bool = True):
+        self.system = system
+        self.ff = ff
+        self.container = container
+        self.schedule = schedule
+        self.interval = int(sample_interval)
+        self.n = int(system.positions.shape[0])
+        self.periodic = bool(system.periodic)
+        self.use_graph = use_graph and self.periodic
+        self.eng = ForceEngine(self.n)
+        torch = self.torch = self.eng.torch
+        dev, f64 = self.eng.device, torch.float64
+        self.x = self.eng.pos  # positions live in the engine's buffer
+        self.v = torch.zeros((self.n, 3), dtype=f64, device=dev)
+        self.f2_old = torch.zeros((self.n, 3), dtype=f64, device=dev)
+        self.f2_new = torch.zeros((self.n, 3), dtype=f64, device=dev)
+        self.f3 = torch.zeros((self.n, 3), dtype=f64, device=dev)
+        self.rc2 = float(ff.cutoff)
+        self.rc3 = triplet_cutoff(ff)
+        self.nu = float(ff.nu)
+        self.with_3b = self.nu != 0.0
+        self.r_list = max(self.rc2, self.rc3) if self.with_3b else self.rc2
+        s = schedule.step_size_factor
+        m = float(system.mass)
+        dt = schedule.dt
+        self.dt = dt
+        self.half_dt = 0.5 * dt / m
+        self.half_drift = 0.5 * dt * dt / m
+        self.half_respa = 0.5 * dt * s / m
+        self.box = np.ascontiguousarray(system.box, dtype=np.float64)
+        nsamples = schedule.num_iterations // self.interval + 1
+        self.trace_dev = torch.zeros((nsamples, 8), dtype=f64, device=dev)
+        self.capacity = capacity
+        self.geom = None
+        self.graph = None
+
+    # -------------------------------------------------------------- pieces
+    def _geom(self):
+        if self.periodic:
+            if self.geom is None:
+                self.geom = geometry(self.box, None, self.r_list, True)
+            return self.geom
+        lo_hi = self.torch.aminmax(self.x, dim=0)
+        pos = np.stack([lo_hi.min.cpu().numpy(), lo_hi.max.cpu().numpy()])
+        return geometry(self.box, pos, self.r_list, False)
+
+    def _forces(self, tag: int, with_triplet: bool, f2_out) -> None:
+        eng = self.eng
+        geom = self._geom()
+        eng.bin(geom, self.x)
+        eng.nlist(geom, self.r_list, capacity=self.capacity, checked=False)
+        eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag)
+        if with_triplet:
+            if self.with_3b:
+                eng.atm(geom, self.rc3, self.nu, self.f3, tag=tag, count_visits=False)
+            else:
+                self.f3.zero_()
+                eng.scalars[SCALAR_E3] = 0.0
+                eng.scalars[SCALAR_W3] = 0.0
+
+    def _record(self) -> None:
+        L, eng = self.eng.L, self.eng
+        eng.sum_f64(self.v, SCALAR_SUMSQ, square=True, n=3 * self.n)
+        base = eng.scalars.data_ptr()
+        sc = [ctypes.c_void_p(base + 8 * k) for k in range(5)]
+        st = L.rb_trace_record(ptr(eng.status), self.interval, ptr(self.trace_dev), sc[0], sc[1],
+                               sc[2], sc[3], sc[4], eng.stream)
+        _lib.check(st, "rb_trace_record")
+
+    def _step(self, i: int) -> None:
+        """Loop body of integrators.py:148-172 for iteration i (tag i+1)."""
+        L, eng = self.eng.L, self.eng
+        s = self.schedule.step_size_factor
+        st = L.rb_step_begin(ptr(eng.status), eng.stream)
+        _lib.check(st, "rb_step_begin")
+        st = L.rb_respa_drift(self.n, ptr(self.x), ptr(self.v), ptr(self.f2_old), ptr(self.f3),
+                              self.box.ctypes.data_as(ctypes.c_void_p), int(self.periodic),
+                              self.dt, self.half_drift, self.half_respa, int(i % s == 0),
+                              ptr(eng.status), _lib.RB_TAG_FROM_DEVICE, eng.stream)
+        _lib.check(st, "rb_respa_drift")
+        end_of_cycle = (i + 1) % s == 0
+        self._forces(_lib.RB_TAG_FROM_DEVICE, end_of_cycle, self.f2_new)
+        st = L.rb_respa_kick(self.n, ptr(self.v), ptr(self.f2_old), ptr(self.f2_new), ptr(self.f3),
+                             self.half_dt, self.half_respa, int(end_of_cycle), ptr(eng.status),
+                             _lib.RB_TAG_FROM_DEVICE, eng.stream)
+        _lib.check(st, "rb_respa_kick")
+        if (i + 1) % self.interval == 0:
+            self._record()
+
+    def _period(self, first: int) -> None:
+        for i in range(first, first + self.interval):
+            self._step(i)
+
+    # ----------------------------------------------------------------- run
+    def start(self) -> None:
+        """Upload, initial passes (integrators.py:133-137) and sample 0."""
+        torch, eng = self.torch, self.eng
+        eng.upload_positions(self.system.positions)
+        self.v.copy_(torch.from_numpy(np.ascontiguousarray(self.system.velocities, np.float64)))
+        eng.reset_status(0)
+        if self.capacity is None:
+            geom = self._geom()
+            eng.bin(geom, self.x)
+            self.capacity = min(4096, _round_up(int(eng.estimate_capacity(geom, self.r_list) * 1.5) + 32, 32))
+        self._forces(0, True, self.f2_old)
+        self._record()
+
+    def capture(self) -> None:
+        """Capture one sampling period as a CUDA graph (after a warm-up)."""
+        torch = self.torch
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._period(0)
+
+    def capture_steps(self):
+        """One CUDA graph per step position inside a sampling period (the
+        step kinds repeat with the period), for per-step timing."""
+        torch = self.torch
+        graphs = []
+        for j in range(self.interval):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._step(j)
+            graphs.append(g)
+        return graphs
+
+    def run_periods(self, first_period: int, count: int) -> None:
+        for k in range(first_period, first_period + count):
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                self._period(k * self.interval)
+
+    def download(self) -> None:
+        sysm = self.system
+        sysm.positions[:] = self.x.cpu().numpy()
+        sysm.velocities[:] = self.v.cpu().numpy()
+        sysm.forces_2b[:] = self.f2_old.cpu().numpy()
+        sysm.forces_3b[:] = self.f3.cpu().numpy()
+
+    def trace_rows(self, upto: int) -> np.ndarray:
+        return self.trace_dev[:upto].cpu().numpy()
+
+    def update_container(self) -> None:
+        sc = self.eng.scalar_values()
+        c = self.container
+        c.pair_energy, c.pair_virial = float(sc[SCALAR_E2]), float(sc[SCALAR_W2])
+        c.triplet_energy, c.triplet_virial = float(sc[SCALAR_E3]), float(sc[SCALAR_W3])
+
+
+def _fill_trace(trace: RunTrace, rows: np.ndarray, mass: float) -> None:
+    for row in rows:
+        trace.record_values(int(round(row[0])), 0.5 * mass * row[1], row[2], row[3], row[4], row[5])
+
+
+def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: Optional[int] = None,
+              hooks=(), use_graph: bool = True, capacity: Optional[int] = None) -> RunTrace:
+    """Integrate in place with the r-RESPA loop on the GPU (integrators.py:96-173)."""
+    if not isinstance(container, CudaLinkedCells):
+        raise TypeError("respa_run needs a CudaLinkedCells container (GPU only, no host fallback)")
+    s = schedule.step_size_factor
+    if sample_interval is None:
+        sample_interval = s
+    sample_interval = int(sample_interval)
+    if sample_interval < 1 or sample_interval % s != 0:
+        raise ValidationError(
+            f"sample_interval ({sample_interval}) must be a positive multiple "
+            f"of the step_size_factor ({s})"
+        )
+    hooks = tuple(hooks)
+    x0 = np.array(system.positions, copy=True)
+    v0 = np.array(system.velocities, copy=True)
+    for attempt in range(3):
+        run = DeviceRespa(system, ff, container, schedule, sample_interval, capacity=capacity,
+                          use_graph=use_graph and not hooks)
+        try:
+            return _drive(run, hooks)
+        except CapacityError:
+            capacity = min(4096, _round_up(int(run.capacity * 1.5) + 32, 32))
+            system.positions[:] = x0
+            system.velocities[:] = v0
+    raise CapacityError("neighbour rows kept overflowing")
+
+
+def _drive(run: DeviceRespa, hooks) -> RunTrace:
+    sysm, n_periods = run.system, run.schedule.num_iterations // run.interval
+    trace = RunTrace()
+    run.start()
+    if hooks:
+        # hooks see the host system at every sample point: sync per period
+        _check(run, trace, upto=1)
+        view = sysm.view() if hasattr(sysm, "view") else sysm
+        run.download()
+        run.update_container()
+        trace.record_values(*_row_values(run, 0))
+        for hook in hooks:
+            hook(0, view, run.container)
+        for k in range(n_periods):
+            run.run_periods(k, 1)
+            _check(run, trace, upto=k + 2)
+            run.download()
+            run.update_container()
+            trace.record_values(*_row_values(run, k + 1))
+            for hook in hooks:
+                hook((k + 1) * run.interval, view, run.container)
+        return trace
+    if n_periods > 0 and run.use_graph:
+        run.run_periods(0, 1)  # warm-up, also the first period of the run
+        run.capture()
+        # the capture recorded but did not execute; rewind nothing: replay the rest
+        run.eng.status[1] = run.interval
+        run.run_periods(1, n_periods - 1)
+    else:
+        run.run_periods(0, n_periods)
+    _check(run, trace, upto=n_periods + 1)
+    _fill_trace(trace, run.trace_rows(n_periods + 1), float(sysm.mass))
+    run.download()
+    run.update_container()
+    return trace
+
+
+def _row_values(run: DeviceRespa, k: int):
+    row = run.trace_dev[k].cpu().numpy()
+    return int(round(row[0])), 0.5 * float(run.system.mass) * row[1], row[2], row[3], row[4], row[5]
+
+
+def _check(run: DeviceRespa, trace: RunTrace, upto: int) -> None:
+    """Raise IntegrationBlowUp / CapacityError for errors recorded so far."""
+    if run.eng.overflowed():
+        raise CapacityError("neighbour row overflow")
+    err = run.eng.read_status()
+    if err is None:
+        return
+    tag, kind = err
+    rows = run.trace_rows(upto)
+    keep = rows[rows[:, 0] < tag] if tag > 0 else rows[:0]
+    if not len(trace):
+        _fill_trace(trace, keep, float(run.system.mass))
+    run.download()
+    run.update_container()
+    raise IntegrationBlowUp(int(tag), _MSG.get(kind, f"device error kind {kind}"), trace)
+
+
+def verlet_run(system, ff, container, dt: float, num_iterations: int,
+               sample_interval: Optional[int] = None, hooks=()) -> RunTrace:
+    """Velocity Verlet = r-RESPA with s = 1 (``integrators.py:176-191``)."""
+    schedule = RespaSchedule(dt=dt, step_size_factor=1, num_iterations=num_iterations)
+    return respa_run(system, ff, container, schedule, sample_interval, hooks)
+
+
+__all__ = ["IntegrationBlowUp", "RespaSchedule", "RunTrace", "respa_run", "verlet_run",
+           "MinimumSeparationError"]

@@ -1,0 +1,349 @@
+"""GPU parity: the sm_100a path against the reference (golden fixtures made by
+the reference itself) and against the bit-pinned CPU oracle.
+
+Tolerances (north star / SURVEY.md Appendix A.5):
+* cell tables, triplet counts, visit multisets: bit-exact;
+* forces: normwise max_i|dF_i| / max_i|F_i| <= 1e-10;
+* energies <= 1e-10 relative, virials <= 1e-9 relative (test_containers.py:153);
+* trajectories (respa_run): positions/velocities <= 1e-10 absolute.
+"""
+
+import glob
+import os
+from collections import Counter
+
+import numpy as np
+import pytest
+
+from helpers import GOLDEN, TEST_SEED, load_golden, normwise, random_positions
+
+pytestmark = pytest.mark.gpu
+
+SMALL = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "small_*.npz")))
+FORCE_TOL = 1e-10
+ENERGY_TOL = 1e-10
+VIRIAL_TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2507_11172_b200 as p
+    from paper_2507_11172_b200 import _lib
+
+    _lib.require_device()
+    return p
+
+
+def _rel(a, b):
+    return abs(a - b) / max(1.0, abs(b))
+
+
+def _system(pkg, pos, box, periodic, vel=None):
+    s = pkg.ParticleSystem.empty(len(pos), box, periodic=periodic)
+    s.positions[:] = pos
+    if vel is not None:
+        s.velocities[:] = vel
+    return s
+
+
+# --------------------------------------------------------------------------
+# binning, passes, counts on the small reference fixtures
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("name", SMALL)
+def test_binning_bit_exact(pkg, name):
+    g = load_golden(name)
+    s = _system(pkg, g["positions"], g["box"], bool(g["periodic"]))
+    grid = pkg.build_cell_grid(s, float(g["cutoff"]))
+    assert np.array_equal(grid.cell_start, g["cell_start"])
+    assert np.array_equal(grid.cell_particles, g["cell_particles"])
+    assert np.array_equal(grid.triplet_patterns, g["triplet_patterns"])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_pair_pass_matches_reference(pkg, name):
+    g = load_golden(name)
+    s = _system(pkg, g["positions"], g["box"], bool(g["periodic"]))
+    ff = pkg.ForceField(nu=float(g["nu"]), cutoff=float(g["cutoff"]))
+    grid = pkg.build_cell_grid(s, ff.cutoff)
+    f, e, w = pkg.c01_pair_pass(grid, s, ff)
+    assert normwise(f, g["f2"]) <= FORCE_TOL
+    assert np.max(np.abs(f - g["bf2"])) <= 1e-10  # the reference's own C01-vs-brute bound
+    assert _rel(e, float(g["e2"])) <= ENERGY_TOL
+    assert _rel(w, float(g["w2"])) <= VIRIAL_TOL
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_triplet_pass_matches_reference(pkg, name):
+    g = load_golden(name)
+    s = _system(pkg, g["positions"], g["box"], bool(g["periodic"]))
+    ff = pkg.ForceField(nu=float(g["nu"]), cutoff=float(g["cutoff"]))
+    grid = pkg.build_cell_grid(s, ff.cutoff)
+    f, e, w = pkg.c01_triplet_pass(grid, s, ff)
+    assert normwise(f, g["f3"]) <= FORCE_TOL
+    assert np.max(np.abs(f - g["bf3"])) <= 1e-9
+    assert _rel(e, float(g["e3"])) <= ENERGY_TOL
+    assert _rel(w, float(g["w3"])) <= VIRIAL_TOL
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_triplet_visits_bit_exact(pkg, name):
+    """Each triplet visited exactly 3x; distinct set == the reference's."""
+    g = load_golden(name)
+    s = _system(pkg, g["positions"], g["box"], bool(g["periodic"]))
+    grid = pkg.build_cell_grid(s, float(g["cutoff"]))
+    rows = pkg.collect_triplet_visits(grid, s)
+    assert rows.shape[0] == int(g["visits"])
+    visits = Counter(map(tuple, rows))
+    assert all(v == 3 for v in visits.values())
+    ref = {tuple(r) for r in g["unique_triplets"]}
+    assert set(visits) == ref
+    assert pkg.triplet_count(s, float(g["cutoff"])) == int(g["brute_count"])
+
+
+def test_write_discipline_single_base_cell(pkg, rng):
+    pos = random_positions(rng, 150, (10.0,) * 3, True)
+    s = _system(pkg, pos, (10.0,) * 3, True)
+    ff = pkg.ForceField(nu=0.7, cutoff=2.5)
+    grid = pkg.build_cell_grid(s, ff.cutoff)
+    owned = set(grid.particles_of_cell(13).tolist())
+    for fn in (pkg.c01_pair_pass, pkg.c01_triplet_pass):
+        f, _, _ = fn(grid, s, ff, base_cells=[13])
+        touched = {int(i) for i in np.nonzero(np.any(f != 0.0, axis=1))[0]}
+        assert touched <= owned and touched
+
+
+def test_closed_forms(pkg):
+    """test_containers.py:109-143: LJ minimum and equilateral ATM triangle."""
+    ff = pkg.ForceField(nu=0.7, cutoff=2.5)
+    r = 2.0 ** (1.0 / 6.0)
+    s = _system(pkg, np.array([[1.0, 1.0, 1.0], [1.0 + r, 1.0, 1.0]]), (10.0,) * 3, True)
+    f, e, _ = pkg.c01_pair_pass(pkg.build_cell_grid(s, 2.5), s, ff)
+    assert np.max(np.abs(f)) < 1e-12 and abs(e + 1.0) < 1e-12
+    r = 1.2
+    pts = np.array([[1.0, 1.0, 1.0], [1.0 + r, 1.0, 1.0], [1.0 + r / 2, 1.0 + r * np.sqrt(3) / 2, 1.0]])
+    s = _system(pkg, pts, (10.0,) * 3, True)
+    f, e, _ = pkg.c01_triplet_pass(pkg.build_cell_grid(s, 2.5), s, ff)
+    assert abs(e - 1.375 * 0.7 / r ** 9) <= 1e-12 * abs(e)
+    assert np.max(np.abs(f.sum(axis=0))) < 1e-12
+    s1 = _system(pkg, np.array([[2.5, 2.5, 2.5]]), (10.0,) * 3, True)
+    f, e, w = pkg.c01_pair_pass(pkg.build_cell_grid(s1, 2.5), s1, ff)
+    assert np.all(f == 0.0) and e == 0.0 and w == 0.0
+
+
+def test_random_systems_against_oracle(pkg, oracle, rng):
+    """Acceptance-style sweep (test_acceptance.py:114-150): 30 random periodic
+    systems, GPU vs the oracle's brute-force enumeration."""
+    ff = pkg.ForceField(nu=0.6, cutoff=2.5)
+    off = oracle.OracleForceField(nu=0.6, cutoff=2.5)
+    for _ in range(30):
+        edge = rng.uniform(6.0, 10.0)
+        n = min(200, int(rng.uniform(0.3, 0.6) * edge ** 3))
+        pos = random_positions(rng, n, (edge,) * 3, True, min_sep=0.8)
+        s = _system(pkg, pos, (edge,) * 3, True)
+        grid = pkg.build_cell_grid(s, 2.5)
+        f2, e2, _ = pkg.c01_pair_pass(grid, s, ff)
+        f3, e3, _ = pkg.c01_triplet_pass(grid, s, ff)
+        os_ = oracle.OracleSystem.from_positions(pos, (edge,) * 3, True)
+        rf2, re2, _ = oracle.brute_force_pairs(os_, off, cutoff=2.5)
+        rf3, re3, _, count = oracle.brute_force_triplets(os_, off, cutoff=2.5)
+        assert np.max(np.abs(f2 - rf2)) <= 1e-9 and np.max(np.abs(f3 - rf3)) <= 1e-9
+        assert _rel(e2, re2) <= 1e-10 and _rel(e3, re3) <= 1e-10
+        assert pkg.triplet_count(s, 2.5) == count
+
+
+def test_open_boundaries_against_oracle(pkg, oracle, rng):
+    """Non-periodic grids (origin/extent from the particles, containers.py:255-259)."""
+    ff = pkg.ForceField(nu=0.7, cutoff=2.5)
+    off = oracle.OracleForceField(nu=0.7, cutoff=2.5)
+    for n, edge in ((40, 6.0), (90, 7.5)):
+        pos = random_positions(rng, n, (edge,) * 3, False)
+        pos[0] += 0.7 * edge  # drifted outside the box
+        s = _system(pkg, pos, (edge,) * 3, False)
+        grid = pkg.build_cell_grid(s, 2.5)
+        f2, e2, _ = pkg.c01_pair_pass(grid, s, ff)
+        f3, e3, _ = pkg.c01_triplet_pass(grid, s, ff)
+        os_ = oracle.OracleSystem.from_positions(pos, (edge,) * 3, False)
+        ogrid = oracle.build_cell_grid(os_, 2.5)
+        assert np.array_equal(grid.cell_particles, ogrid.cell_particles)
+        rf2, re2, _ = oracle.brute_force_pairs(os_, off, cutoff=2.5)
+        rf3, re3, _, count = oracle.brute_force_triplets(os_, off, cutoff=2.5)
+        assert np.max(np.abs(f2 - rf2)) <= 1e-9 and np.max(np.abs(f3 - rf3)) <= 1e-9
+        assert _rel(e3, re3) <= 1e-10
+        assert pkg.triplet_count(s, 2.5) == count
+
+
+def test_minimum_separation_raises(pkg):
+    ff = pkg.ForceField(nu=0.7, cutoff=2.5)
+    s = _system(pkg, np.array([[1.0, 1.0, 1.0], [1.0 + 5e-11, 1.0, 1.0], [2.0, 1.0, 1.0]]),
+                (10.0,) * 3, True)
+    c = pkg.CudaLinkedCells()
+    with pytest.raises(pkg.MinimumSeparationError):
+        c.pair_pass(s, ff)
+    with pytest.raises(pkg.MinimumSeparationError):
+        c.triplet_pass(s, ff)
+
+
+def test_deterministic_passes(pkg):
+    s = pkg.systems.CONFIGS["cfg2"].system()
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5)
+    c = pkg.CudaLinkedCells()
+    c.triplet_pass(s, ff)
+    a = s.forces_3b.copy()
+    e = c.triplet_energy
+    c.triplet_pass(s, ff)
+    assert np.array_equal(a, s.forces_3b) and e == c.triplet_energy
+    c.pair_pass(s, ff)
+    b = s.forces_2b.copy()
+    c.pair_pass(s, ff)
+    assert np.array_equal(b, s.forces_2b)
+
+
+# --------------------------------------------------------------------------
+# BASELINE configs at step 0 (reference scalars / counts / force subsets)
+# --------------------------------------------------------------------------
+LARGE = ["large_cfg1.npz", "large_cfg2.npz", "large_cfg3_rc2.0.npz", "large_cfg3_rc2.5.npz",
+         "large_cfg3_rc3.0.npz", "large_cfg4.npz"]
+
+
+@pytest.mark.parametrize("name", LARGE)
+def test_baseline_configs_step0(pkg, name):
+    import hashlib
+
+    g = load_golden(name)
+    cfg = name.split("_")[1].split(".npz")[0]
+    s = pkg.systems.CONFIGS[cfg].system()
+    assert hashlib.sha256(s.positions.tobytes()).hexdigest() == str(g["sha"])
+    rc3 = float(g["rc3"])
+    ff = pkg.ForceField(nu=float(g["nu"]), cutoff=float(g["rc2"]),
+                        cutoff_3b=None if rc3 == float(g["rc2"]) else rc3)
+    c = pkg.CudaLinkedCells()
+    c.pair_pass(s, ff)
+    c.triplet_pass(s, ff)
+    assert _rel(c.pair_energy, float(g["e2"])) <= ENERGY_TOL
+    assert _rel(c.pair_virial, float(g["w2"])) <= VIRIAL_TOL
+    assert _rel(c.triplet_energy, float(g["e3"])) <= ENERGY_TOL
+    assert _rel(c.triplet_virial, float(g["w3"])) <= VIRIAL_TOL
+    if int(g["visits"]) >= 0:
+        assert c.triplet_visits == int(g["visits"])
+    sub = g["subset"]
+    assert np.max(np.abs(s.forces_2b[sub] - g["f2"])) <= FORCE_TOL * float(g["f2_absmax"])
+    assert np.max(np.abs(s.forces_3b[sub] - g["f3"])) <= FORCE_TOL * float(g["f3_absmax"])
+
+
+# --------------------------------------------------------------------------
+# device-resident r-RESPA
+# --------------------------------------------------------------------------
+def _respa_from_golden(pkg, name, container_rc3=None):
+    g = load_golden(name)
+    s = _system(pkg, g["x0"], g["box"], True, g["v0"])
+    rc3 = float(g["cutoff_3b"]) if "cutoff_3b" in g else None
+    ff = pkg.ForceField(nu=float(g["nu"]), cutoff=float(g["cutoff"]), cutoff_3b=rc3)
+    trace = pkg.respa_run(s, ff, pkg.CudaLinkedCells(),
+                          pkg.RespaSchedule(float(g["dt"]), int(g["s"]), int(g["steps"])))
+    return g, s, trace
+
+
+@pytest.mark.parametrize("name", ["respa_cfg1.npz", "respa_small_s3.npz", "respa_split_rc3.npz"])
+def test_respa_trajectory_matches_reference(pkg, name):
+    g, s, trace = _respa_from_golden(pkg, name)
+    assert np.max(np.abs(s.positions - g["x"])) <= 1e-10
+    assert np.max(np.abs(s.velocities - g["v"])) <= 1e-10
+    assert list(trace.iterations) == [int(v) for v in g["t_iterations"]]
+    for got, ref in ((trace.total, g["t_total"]), (trace.potential_3b, g["t_p3"]),
+                     (trace.kinetic, g["t_kinetic"])):
+        assert max(_rel(a, b) for a, b in zip(got, ref)) <= 1e-10
+
+
+def test_respa_cfg2_matches_reference(pkg):
+    g = load_golden("respa_cfg2.npz")
+    s = pkg.systems.CONFIGS["cfg2"].system()
+    ff = pkg.ForceField(nu=float(g["nu"]), cutoff=float(g["cutoff"]))
+    trace = pkg.respa_run(s, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, 5, 100))
+    sub = g["subset"]
+    assert np.max(np.abs(s.positions[sub] - g["x"])) <= 1e-10
+    assert np.max(np.abs(s.velocities[sub] - g["v"])) <= 1e-10
+    assert max(_rel(a, b) for a, b in zip(trace.total, g["t_total"])) <= 1e-10
+    assert np.all(s.positions >= 0.0) and np.all(s.positions < s.box)
+
+
+def test_respa_graph_and_eager_identical(pkg):
+    base = pkg.systems.fcc_system(6, temperature=0.9, seed=5, vseed=6)
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5)
+    a, b = base.copy(), base.copy()
+    ta = pkg.respa_run(a, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, 5, 40), use_graph=True)
+    tb = pkg.respa_run(b, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, 5, 40), use_graph=False)
+    assert np.array_equal(a.positions, b.positions) and np.array_equal(a.velocities, b.velocities)
+    assert ta.total == tb.total
+
+
+def test_s1_is_verlet_and_zero_nu_independent_of_s(pkg):
+    base = pkg.systems.fcc_system(5, temperature=1.0, seed=2, vseed=3)
+    ff = pkg.ForceField(nu=0.4, cutoff=2.5)
+    a, b = base.copy(), base.copy()
+    pkg.respa_run(a, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, 1, 60))
+    pkg.verlet_run(b, ff, pkg.CudaLinkedCells(), 0.001, 60)
+    assert np.array_equal(a.positions, b.positions) and np.array_equal(a.velocities, b.velocities)
+    ff0 = pkg.ForceField(nu=0.0, cutoff=2.5)
+    ref = base.copy()
+    pkg.verlet_run(ref, ff0, pkg.CudaLinkedCells(), 0.001, 24)
+    for s in (2, 4, 12):
+        t = base.copy()
+        pkg.respa_run(t, ff0, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, s, 24))
+        assert np.array_equal(t.positions, ref.positions)
+        assert np.array_equal(t.velocities, ref.velocities)
+
+
+def test_hooks_cadence_momentum_and_wrap(pkg, rng):
+    pos = random_positions(rng, 60, (6.5,) * 3, True)
+    s = _system(pkg, pos, (6.5,) * 3, True)
+    pkg.init_velocities(s, 1.2, seed=3)
+    seen, mom = [], []
+
+    def hook(it, view, c):
+        seen.append(it)
+        mom.append(float(np.max(np.abs(view.velocities.sum(axis=0)))))
+        with pytest.raises(ValueError):
+            view.positions[0, 0] = 1.0
+
+    ff = pkg.ForceField(nu=0.7, cutoff=2.5)
+    pkg.respa_run(s, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 3, 36), sample_interval=6,
+                  hooks=(hook,))
+    assert seen == [0, 6, 12, 18, 24, 30, 36]
+    assert max(mom) <= 1e-9
+    assert np.all(s.positions >= 0.0) and np.all(s.positions < s.box)
+    with pytest.raises(pkg.ValidationError):
+        pkg.respa_run(s, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, 4, 8), sample_interval=2)
+
+
+def test_blowup_iterations(pkg):
+    """test_integrators.py:146-161 semantics with the GPU container."""
+    ff = pkg.ForceField(nu=0.7, cutoff=2.5)
+    s = _system(pkg, np.array([[1.0, 1.0, 1.0], [1.0 + 5e-11, 1.0, 1.0]]), (10.0,) * 3, False)
+    with pytest.raises(pkg.IntegrationBlowUp) as err:
+        pkg.respa_run(s, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, 1, 10))
+    assert err.value.iteration == 0
+    s = _system(pkg, np.array([[1.0, 1.0, 1.0], [40.0, 40.0, 40.0]]), (50.0,) * 3, False)
+    s.velocities[0, 0] = 1e307
+    with np.errstate(over="ignore"), pytest.raises(pkg.IntegrationBlowUp) as err:
+        pkg.respa_run(s, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(100.0, 1, 10))
+    assert err.value.iteration == 1
+
+
+def test_respa_rejects_host_containers(pkg):
+    s = pkg.systems.fcc_system(4)
+    with pytest.raises(TypeError):
+        pkg.respa_run(s, pkg.ForceField(), object(), pkg.RespaSchedule(0.001, 1, 1))
+
+
+def test_container_drives_oracle_respa_loop(pkg, oracle):
+    """The GPU container is a drop-in for the reference loop: the oracle's
+    restatement of respa_run driven by CudaLinkedCells matches the same loop
+    driven by the oracle container."""
+    base = pkg.systems.fcc_system(5, temperature=0.9, seed=7, vseed=8)
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5)
+    a = oracle.OracleSystem.from_positions(base.positions, base.box, True, base.velocities)
+    b = a.copy()
+    ta = oracle.respa_run(a, ff, pkg.CudaLinkedCells(), 0.001, 2, 20)
+    tb = oracle.respa_run(b, ff, oracle.OracleLinkedCells(), 0.001, 2, 20)
+    assert np.max(np.abs(a.positions - b.positions)) <= 1e-10
+    assert max(_rel(x, y) for x, y in zip(ta.total, tb.total)) <= 1e-10

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kAtmWarps * 32)
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int64_t r = (int64_t)blockIdx.x * kAtmWarps + warp;
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (r >= n) return;
     tag = resolve_tag(tag, status);
     if (!kRows && warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
@@ -274,6 +274,17 @@ static void grant_smem(K kernel, size_t bytes, size_t &granted) {
 
 static size_t g_granted[3] = {0, 0, 0};
 
+// warps per CTA: kAtmWarps unless the per-warp survivor buffers of a large
+// row capacity do not fit 227 KB of shared memory; 0 if one warp does not fit
+static size_t atm_launch_shape(int capacity, int &warps) {
+    const size_t per = atm_warp_bytes(capacity);
+    const size_t limit = 227 * 1024;
+    warps = kAtmWarps;
+    while (warps > 1 && (size_t)warps * per > limit) warps--;
+    if ((size_t)warps * per > limit) return 0;
+    return (size_t)warps * per;
+}
+
 }  // namespace rb
 
 using namespace rb;
@@ -291,18 +302,20 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const 
     if (g->periodic)
         for (int d = 0; d < 3; d++)
             if (!(g->box[d] > 4.0 * rc * (1.0 + 1e-12))) exact_image = true;
-    const size_t smem = (size_t)kAtmWarps * atm_warp_bytes(capacity);
-    const unsigned blocks = (unsigned)((n + kAtmWarps - 1) / kAtmWarps);
+    int warps = 0;
+    const size_t smem = atm_launch_shape(capacity, warps);
+    if (!smem) return RB_ERR_ARGUMENT;
+    const unsigned blocks = (unsigned)((n + warps - 1) / warps);
     cudaStream_t st = as_stream(stream);
     if (exact_image) {
         grant_smem(k_atm<true, false>, smem, g_granted[0]);
-        k_atm<true, false><<<blocks, kAtmWarps * 32, smem, st>>>(
+        k_atm<true, false><<<blocks, warps * 32, smem, st>>>(
             *g, n, xs, ys, zs, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, nu,
             forces, energy_rank, virial_rank, visits_rank, status, tag, nullptr, nullptr);
         note_launches(1);
     } else {
         grant_smem(k_atm<false, false>, smem, g_granted[1]);
-        k_atm<false, false><<<blocks, kAtmWarps * 32, smem, st>>>(
+        k_atm<false, false><<<blocks, warps * 32, smem, st>>>(
             *g, n, xs, ys, zs, cell_particles, rows, row_count, capacity, rc2,
             rc2 * (1.0 - kAtmMargin), rc2 * (1.0 + kAtmMargin), nu, forces, energy_rank,
             virial_rank, visits_rank, status, tag, nullptr, nullptr);
@@ -323,11 +336,13 @@ extern "C" int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *xs, 
         return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     const double rc2 = rc * rc;
-    const size_t smem = (size_t)kAtmWarps * atm_warp_bytes(capacity);
-    const unsigned blocks = (unsigned)((n + kAtmWarps - 1) / kAtmWarps);
+    int warps = 0;
+    const size_t smem = atm_launch_shape(capacity, warps);
+    if (!smem) return RB_ERR_ARGUMENT;
+    const unsigned blocks = (unsigned)((n + warps - 1) / warps);
     // the instrumentation always takes the exact raw-position predicate
     grant_smem(k_atm<true, true>, smem, g_granted[2]);
-    k_atm<true, true><<<blocks, kAtmWarps * 32, smem, as_stream(stream)>>>(
+    k_atm<true, true><<<blocks, warps * 32, smem, as_stream(stream)>>>(
         *g, n, xs, ys, zs, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, 0.0, nullptr,
         nullptr, nullptr, nullptr, nullptr, 0, row_offset, visit_rows);
     note_launches(1);

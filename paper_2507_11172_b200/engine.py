@@ -127,7 +127,8 @@ class ForceEngine:
         vol = float(np.prod(geom.cell_size))
         dens = max(max_occ / vol, self.n / float(np.prod(geom.box)))
         est = dens * 4.0 / 3.0 * math.pi * r_list ** 3
-        return int(min(4096, max(32, _round_up(int(1.3 * est) + 32, 32), min(self.n, 4096))))
+        cap = max(32, _round_up(int(1.3 * est) + 32, 32))
+        return int(min(4096, cap, max(32, _round_up(self.n, 32))))
 
     def _ensure_rows(self, capacity: int) -> None:
         if self.rows is None or self.capacity != capacity:

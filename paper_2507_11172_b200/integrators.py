@@ -162,11 +162,20 @@ class DeviceRespa:
             return self.geom
         lo_hi = self.torch.aminmax(self.x, dim=0)
         pos = np.stack([lo_hi.min.cpu().numpy(), lo_hi.max.cpu().numpy()])
+        if not np.all(np.isfinite(pos)):
+            return None  # the drift already recorded the non-finite state
         return geometry(self.box, pos, self.r_list, False)
 
     def _forces(self, tag: int, with_triplet: bool, f2_out) -> None:
         eng = self.eng
         geom = self._geom()
+        if geom is None:
+            # open system with non-finite positions: forces are undefined;
+            # the step is already marked RB_KIND_NONFINITE (integrators.py:166-170)
+            f2_out.fill_(float("nan"))
+            if with_triplet:
+                self.f3.fill_(float("nan"))
+            return
         eng.bin(geom, self.x)
         eng.nlist(geom, self.r_list, capacity=self.capacity, checked=False)
         eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag)
@@ -175,8 +184,7 @@ class DeviceRespa:
                 eng.atm(geom, self.rc3, self.nu, self.f3, tag=tag, count_visits=False)
             else:
                 self.f3.zero_()
-                eng.scalars[SCALAR_E3] = 0.0
-                eng.scalars[SCALAR_W3] = 0.0
+                eng.scalars[SCALAR_E3:SCALAR_W3 + 1].zero_()
 
     def _record(self) -> None:
         L, eng = self.eng.L, self.eng

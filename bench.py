@@ -27,6 +27,7 @@ For N > 1 (torchrun) each rank runs an independent replica of the workload
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -51,8 +52,8 @@ FLOPS_PER_PAIR = 35
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=100)
-    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--steps", type=int, default=2000)
+    p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--config", default="cfg2")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -85,7 +86,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -255,23 +256,16 @@ def ours_arm(args, cfg):
     eng.reset_status(0)
     eng.atm(geom, run.rc3, run.nu, f3, tag=0, count_visits=True)
     torch.cuda.synchronize()
-    unique = int(eng.visits.item()) // 3
-    grid = eng.grid_struct(geom)
-    import ctypes
+    unique = int(eng.visits.item())
 
     def atm_once():
-        return L.rb_atm_pass(ctypes.byref(grid), eng.n, _lib.ptr(eng.xs), _lib.ptr(eng.ys),
-                             _lib.ptr(eng.zs), _lib.ptr(eng.parts), _lib.ptr(eng.rows),
-                             _lib.ptr(eng.row_count), eng.capacity, run.rc3, run.nu,
-                             _lib.ptr(f3), _lib.ptr(eng.e_rank), _lib.ptr(eng.w_rank),
-                             _lib.ptr(eng.v_rank), _lib.ptr(eng.status), 0, stream)
+        eng.atm_kernel(geom, run.rc3, run.nu, f3, tag=0)
+
+    def atm_c01_once():
+        eng.atm_c01(geom, run.rc3, run.nu, f3, tag=0, reduce=False)
 
     def lj_once():
-        return L.rb_lj_pass(ctypes.byref(grid), eng.n, _lib.ptr(eng.xs), _lib.ptr(eng.ys),
-                            _lib.ptr(eng.zs), _lib.ptr(eng.parts), _lib.ptr(eng.rows),
-                            _lib.ptr(eng.row_count), eng.capacity, run.rc2, 1.0, 1.0,
-                            _lib.ptr(f3), _lib.ptr(eng.e_rank), _lib.ptr(eng.w_rank),
-                            _lib.ptr(eng.status), 0, stream)
+        eng.lj_kernel(geom, run.rc2, 1.0, 1.0, f3, tag=0)
 
     def time_kernel(fn, reps):
         fn()
@@ -287,6 +281,7 @@ def ours_arm(args, cfg):
         return statistics.median(ts), ts
 
     atm_ms, _ = time_kernel(atm_once, 20)
+    c01_ms, _ = time_kernel(atm_c01_once, 10)
     lj_ms, _ = time_kernel(lj_once, 20)
     pairs = int((eng.row_count[: eng.n].sum().item()))  # within r_list == rc2 here
     tflop = torch.empty(1, dtype=torch.float64)
@@ -325,7 +320,7 @@ def ours_arm(args, cfg):
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": "flushed (256 MiB write) between timed steps; per-step CUDA events",
                    "graph": "one CUDA graph per step position in the 5-step cycle"},
-        "roofline": {"bound": "fp64", "kernel": "k_atm (ATM triplet pass)",
+        "roofline": {"bound": "fp64", "kernel": "ATM triplet pass (k_atm3 + k_atm3_gather)",
                      "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak_tf if peak_tf > 0 else None,
                      "traffic": traffic,
@@ -334,6 +329,8 @@ def ours_arm(args, cfg):
                      "work": f"{FLOPS_PER_TRIPLET} FP64 flops per unique triplet x {unique} "
                              f"unique triplets per launch",
                      "kernel_ms": atm_ms, "triplets_per_s": triplets_per_s,
+                     "c01_kernel_ms": c01_ms,
+                     "c01_triplets_per_s": unique / (c01_ms * 1e-3),
                      "lj_kernel_ms": lj_ms, "lj_pairs_visited": pairs,
                      "lj_tflops": pairs / 2 * FLOPS_PER_PAIR / (lj_ms * 1e-3) / 1e12},
         "e2e": {"value": e2e_steps / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d / e2e_steps,

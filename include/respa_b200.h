@@ -117,20 +117,41 @@ RB_API int rb_lj_pass(const rb_grid *g, int64_t n, const double *xs, const doubl
                double *energy_rank, double *virial_rank, unsigned long long *status, int64_t tag,
                void *stream);
 
+/* Mirror indices of the (rank-sorted) rows: mirror[p*capacity + k] is the
+ * position of p in the row of q = rows[p*capacity + k] when q < p, else -1.
+ * Needed by the Newton-3 triplet pass to return partial forces to q's row. */
+RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_count,
+                           int32_t capacity, int32_t *mirror, void *stream);
+
 /* ---- ATM triplet pass: replaces _c01_triplet_kernel (:373-535) --------
- * Enumerates every within-cutoff triplet (all three pair distances <= rc,
- * inclusive) of each base particle; writes forces (n,3) in particle order
- * (overwritten), per-rank energy/virial and per-rank accepted-visit counts
- * (3 visits per unique triplet, as collect_triplet_visits :825-849 counts). */
-RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys, const double *zs,
-                const int32_t *cell_particles, const int32_t *rows, const int32_t *row_count,
-                int32_t capacity, double rc, double nu, double *forces, double *energy_rank,
-                double *virial_rank, int32_t *visits_rank, unsigned long long *status, int64_t tag,
-                void *stream);
+ * Newton-3 form: every unique triplet (all three pair distances <= rc,
+ * inclusive, reference arithmetic) is evaluated once by its lowest-rank
+ * member; forces on all three members are accumulated without atomics in a
+ * fixed order (deterministic).  Writes forces (n,3) in particle order
+ * (overwritten), per-rank energy (phi per owned triplet), virial and the
+ * number of owned (unique) triplets.  Scratch: rb_atm_scratch_bytes. */
+RB_API size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity);
+RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
+                       const double *zs, const int32_t *cell_particles, const int32_t *rows,
+                       const int32_t *row_count, const int32_t *mirror, int32_t capacity,
+                       double rc, double nu, double *forces, double *energy_rank,
+                       double *virial_rank, int32_t *triplets_rank, void *scratch,
+                       size_t scratch_bytes, unsigned long long *status, int64_t tag,
+                       void *stream);
+
+/* C01 (owner-computes) form of the same pass, as the reference traverses it:
+ * every triplet visited once from each member, force stored on the base
+ * particle only, energy phi/3 per visit; visits_rank = accepted visits. */
+RB_API int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *xs, const double *ys,
+                           const double *zs, const int32_t *cell_particles, const int32_t *rows,
+                           const int32_t *row_count, int32_t capacity, double rc, double nu,
+                           double *forces, double *energy_rank, double *virial_rank,
+                           int32_t *visits_rank, unsigned long long *status, int64_t tag,
+                           void *stream);
 
 /* Instrumentation (collect_triplet_visits, containers.py:825-849): writes
  * one sorted (i, j, k) particle-index row per accepted visit, int32 (V,3),
- * at row_offset[r] (exclusive prefix of rb_atm_pass's visits_rank). */
+ * at row_offset[r] (exclusive prefix of rb_atm_pass_c01's visits_rank). */
 RB_API int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *xs, const double *ys,
                              const double *zs, const int32_t *cell_particles, const int32_t *rows,
                              const int32_t *row_count, int32_t capacity, double rc,

@@ -127,7 +127,12 @@ def c01_pair_pass(grid, system, ff, base_cells=None):
 
 
 def c01_triplet_pass(grid, system, ff, base_cells=None):
-    """ATM pass; (forces (n,3), energy, virial) as containers.py:786-822 returns."""
+    """ATM pass; (forces (n,3), energy, virial) as containers.py:786-822 returns.
+
+    With ``base_cells`` the C01 (owner-computes) kernel runs, so the energy is
+    the reference's per-visit attribution restricted to those cells."""
+    if base_cells is not None:
+        return c01_triplet_pass_owner(grid, system, ff, base_cells)
     eng, geom = _prepare(system, grid.cutoff)
     out = eng.torch.empty((eng.n, 3), dtype=eng.torch.float64, device=eng.device)
     eng.atm(geom, grid.cutoff, ff.nu, out, tag=0)
@@ -139,7 +144,7 @@ def collect_triplet_visits(grid, system, base_cells=None) -> np.ndarray:
     """Sorted (i, j, k) row per accepted visit (containers.py:825-849)."""
     eng, geom = _prepare(system, grid.cutoff)
     out = eng.torch.empty((eng.n, 3), dtype=eng.torch.float64, device=eng.device)
-    eng.atm(geom, grid.cutoff, 0.0, out, tag=0)
+    eng.atm_c01(geom, grid.cutoff, 0.0, out, tag=0)
     rows = eng.visit_rows(geom, grid.cutoff)
     if base_cells is not None:
         parts = eng.parts[: eng.n].cpu().numpy()
@@ -152,14 +157,28 @@ def collect_triplet_visits(grid, system, base_cells=None) -> np.ndarray:
 
 
 def triplet_count(system, cutoff: float) -> int:
-    """Unique within-cutoff triplets (= accepted visits / 3)."""
+    """Unique within-cutoff triplets, counted by the Newton-3 enumeration."""
     eng, geom = _prepare(system, cutoff)
     out = eng.torch.empty((eng.n, 3), dtype=eng.torch.float64, device=eng.device)
     eng.atm(geom, cutoff, 0.0, out, tag=0)
-    visits = int(eng.visits.item())
-    if visits % 3:
-        raise RuntimeError(f"visit count {visits} is not a multiple of 3")
-    return visits // 3
+    return int(eng.visits.item())
+
+
+def triplet_visit_count(system, cutoff: float) -> int:
+    """Accepted C01 visits (3 per unique triplet), counted by the C01 enumeration."""
+    eng, geom = _prepare(system, cutoff)
+    out = eng.torch.empty((eng.n, 3), dtype=eng.torch.float64, device=eng.device)
+    eng.atm_c01(geom, cutoff, 0.0, out, tag=0)
+    return int(eng.visits.item())
+
+
+def c01_triplet_pass_owner(grid, system, ff, base_cells=None):
+    """The same pass through the C01 (owner-computes) kernel, for cross-checks."""
+    eng, geom = _prepare(system, grid.cutoff)
+    out = eng.torch.empty((eng.n, 3), dtype=eng.torch.float64, device=eng.device)
+    eng.atm_c01(geom, grid.cutoff, ff.nu, out, tag=0)
+    _raise_on_status(eng)
+    return _finish(eng, geom, out, SCALAR_E3, SCALAR_W3, base_cells)
 
 
 class CudaLinkedCells:
@@ -207,7 +226,7 @@ class CudaLinkedCells:
         forces, e, w = _finish(eng, geom, out, SCALAR_E3, SCALAR_W3, None)
         system.forces_3b[:] = forces
         self.triplet_energy, self.triplet_virial = e, w
-        self.triplet_visits = int(eng.visits.item())
+        self.triplet_visits = 3 * int(eng.visits.item())  # C01-equivalent visit count
 
 
 def make_container(kind: str):

@@ -1,4 +1,8 @@
-// atm.cu -- Axilrod-Teller-Muto triplet pass.
+// atm.cu -- Axilrod-Teller-Muto triplet pass, C01 (owner-computes) form.
+//
+// The production pass is the Newton-3 kernel in atm3.cu; this C01 form is kept
+// as an independent second enumeration (tests cross-check the two) and as the
+// instrumentation of collect_triplet_visits.
 //
 // Replaces respamd/containers.py:373-535 (_c01_triplet_kernel).  One warp per
 // base particle i (rank order), owner-computes like the reference: only the
@@ -289,7 +293,7 @@ static size_t atm_launch_shape(int capacity, int &warps) {
 
 using namespace rb;
 
-extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
+extern "C" int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *xs, const double *ys,
                            const double *zs, const int32_t *cell_particles, const int32_t *rows,
                            const int32_t *row_count, int32_t capacity, double rc, double nu,
                            double *forces, double *energy_rank, double *virial_rank,

@@ -1,0 +1,442 @@
+// atm3.cu -- Newton-3 Axilrod-Teller-Muto triplet pass: every unique triplet
+// i < j < k (rank order) is evaluated exactly once, by the warp of its
+// lowest-rank member i, and its three forces are delivered deterministically.
+//
+// Replaces respamd/containers.py:373-535 (_c01_triplet_kernel).  The C01
+// reference evaluates each triplet three times (once per member, force on the
+// base particle only); here the expensive kernel (potentials.py:82-114) runs
+// once and the partial forces of j and k are accumulated without atomics:
+//
+//   phase 0  S+(i): the suffix of i's rank-sorted row with rank > i and
+//            r_ij^2 <= rc^2 (reference arithmetic) -> per-warp slots in
+//            shared memory (d_ij, r_ij^2, row index).
+//   phase 1  candidate pairs of slots by ROUNDS: in round d lane s pairs slot
+//            s with slot (s + d) mod m, d = 1 .. m/2.  Every unordered slot
+//            pair appears exactly once, and inside one round all first slots
+//            are distinct and all second slots are distinct.  r_jk^2 <= rc^2
+//            is settled bit-exactly (fused estimate from d_ik - d_ij outside a
+//            1e-10 relative band, the reference's raw-position arithmetic
+//            inside it or when the box is under four cutoffs).
+//   phase 2  accepted pairs are queued and evaluated 32 at a time (all lanes
+//            busy); f_i stays in registers, f_j and f_k are added to the slot
+//            accumulators in shared memory one round-record at a time, so no
+//            two lanes of a sub-step touch the same slot and the order of the
+//            additions is fixed by the enumeration.
+//   phase 3  slot sums go to G[i][row index]; the gather kernel sums, for each
+//            particle p in row order, its own part and G[q][mirror(p in q)]
+//            over the row entries q < p -- a fixed order again.
+//
+// Energies are phi per triplet (the reference's phi/3 per visit, summed), the
+// virial -2(E_a a + E_b b + E_c c) per triplet (:530 summed over visits).
+#include "common.cuh"
+
+namespace rb {
+
+constexpr int kA3Warps = 4;
+constexpr int kA3Queue = 64;
+constexpr double kA3Margin = 1e-10;
+
+struct A3Smem {
+    double *dx, *dy, *dz, *r2;  // slots
+    double *ax, *ay, *az;       // slot force accumulators (units of 2 nu)
+    double *qc;                 // queue: r_jk^2
+    int32_t *kidx;              // slot -> row index
+    uint32_t *qst;              // queue: s | t << 16
+    int32_t *qrec;              // queue: round record id
+};
+
+__host__ __device__ inline size_t a3_warp_bytes(int capacity) {
+    size_t b = (size_t)capacity * (7 * sizeof(double)) + (size_t)kA3Queue * sizeof(double);
+    b += (size_t)capacity * sizeof(int32_t) + (size_t)kA3Queue * 2 * sizeof(int32_t);
+    return (b + 15) & ~(size_t)15;
+}
+
+__device__ inline A3Smem a3_carve(char *base, int capacity) {
+    A3Smem s;
+    s.dx = (double *)base;
+    s.dy = s.dx + capacity;
+    s.dz = s.dy + capacity;
+    s.r2 = s.dz + capacity;
+    s.ax = s.r2 + capacity;
+    s.ay = s.ax + capacity;
+    s.az = s.ay + capacity;
+    s.qc = s.az + capacity;
+    s.kidx = (int32_t *)(s.qc + kA3Queue);
+    s.qst = (uint32_t *)(s.kidx + capacity);
+    s.qrec = (int32_t *)(s.qst + kA3Queue);
+    return s;
+}
+
+struct A3Acc {
+    double fx, fy, fz, e, w;
+    int n;
+    bool bad;
+};
+
+// evaluate queue entry `q` (lane-private), add f_i/E/W to acc, return f_j, f_k
+template <bool kExactImage>
+__device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im,
+                                        const double *__restrict__ xs,
+                                        const double *__restrict__ ys,
+                                        const double *__restrict__ zs, A3Acc &acc, double fj[3],
+                                        double fk[3], int &s, int &t) {
+    const uint32_t st = sm.qst[q];
+    s = (int)(st & 0xffffu);
+    t = (int)(st >> 16);
+    const double a = sm.r2[s], b = sm.r2[t], c = sm.qc[q];
+    const double dijx = sm.dx[s], dijy = sm.dy[s], dijz = sm.dz[s];
+    const double dikx = sm.dx[t], diky = sm.dy[t], dikz = sm.dz[t];
+    if (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ || c < RB_MIN_DISTANCE_SQ) {
+        acc.bad = true;
+        fj[0] = fj[1] = fj[2] = fk[0] = fk[1] = fk[2] = 0.0;
+        return false;
+    }
+    double djkx, djky, djkz;  // x_j - x_k
+    if (kExactImage) {
+        const int j = sm.kidx[s] >> 0, k = sm.kidx[t] >> 0;  // rank indices (exact mode)
+        exact_disp(im, xs[j], ys[j], zs[j], xs[k], ys[k], zs[k], djkx, djky, djkz);
+    } else {
+        djkx = dikx - dijx;
+        djky = diky - dijy;
+        djkz = dikz - dijz;
+    }
+    const double u = a + b - c;
+    const double v = a + c - b;
+    const double w = b + c - a;
+    const double p = u * v * w;
+    const double sp = a * b * c;
+    const double rs = rsqrt(sp);
+    const double inv_s = rs * rs;
+    const double s32 = inv_s * rs;
+    const double s52 = s32 * inv_s;
+    const double s72 = s52 * inv_s;
+    const double uv = u * v, uw = u * w, vw = v * w;
+    const double bc = b * c, ac = a * c, ab = a * b;
+    const double qq = 0.9375 * p * s72;
+    const double ea = (0.375 * (vw + uw - uv) - 1.5 * bc) * s52 - qq * bc;
+    const double eb = (0.375 * (vw - uw + uv) - 1.5 * ac) * s52 - qq * ac;
+    const double ec = (0.375 * (uw + uv - vw) - 1.5 * ab) * s52 - qq * ab;
+    acc.fx -= ea * dijx + eb * dikx;
+    acc.fy -= ea * dijy + eb * diky;
+    acc.fz -= ea * dijz + eb * dikz;
+    acc.e += s32 + 0.375 * p * s52;
+    acc.w += ea * a + eb * b + ec * c;
+    acc.n += 1;
+    fj[0] = ea * dijx - ec * djkx;
+    fj[1] = ea * dijy - ec * djky;
+    fj[2] = ea * dijz - ec * djkz;
+    fk[0] = eb * dikx + ec * djkx;
+    fk[1] = eb * diky + ec * djky;
+    fk[2] = eb * dikz + ec * djkz;
+    return true;
+}
+
+// evaluate the first `cnt` queue entries and fold f_j / f_k into the slot
+// accumulators, one round-record at a time (records are contiguous runs)
+template <bool kExactImage>
+__device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, const Image &im,
+                                         const double *__restrict__ xs,
+                                         const double *__restrict__ ys,
+                                         const double *__restrict__ zs, A3Acc &acc) {
+    double fj[3] = {0.0, 0.0, 0.0}, fk[3] = {0.0, 0.0, 0.0};
+    int s = 0, t = 0, rec = -1;
+    bool pending = false;
+    if (lane < cnt) {
+        pending = a3_eval<kExactImage>(sm, lane, im, xs, ys, zs, acc, fj, fk, s, t);
+        rec = sm.qrec[lane];
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, pending);
+    while (todo) {
+        const int leader = __ffs(todo) - 1;
+        const int r0 = __shfl_sync(0xffffffffu, rec, leader);
+        const bool act = pending && rec == r0;
+        if (act) {
+            sm.ax[s] += fj[0];
+            sm.ay[s] += fj[1];
+            sm.az[s] += fj[2];
+        }
+        __syncwarp();
+        if (act) {
+            sm.ax[t] += fk[0];
+            sm.ay[t] += fk[1];
+            sm.az[t] += fk[2];
+        }
+        __syncwarp();
+        if (act) pending = false;
+        todo = __ballot_sync(0xffffffffu, pending);
+    }
+}
+
+template <bool kExactImage>
+__global__ void __launch_bounds__(kA3Warps * 32)
+    k_atm3(rb_grid g, int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
+           const double *__restrict__ zs, const int32_t *__restrict__ rows,
+           const int32_t *__restrict__ row_count, int32_t capacity, double rc2, double rc2_lo,
+           double rc2_hi, double *__restrict__ own, double *__restrict__ gbuf,
+           double *__restrict__ energy_rank, double *__restrict__ virial_rank,
+           int32_t *__restrict__ triplets_rank, unsigned long long *status, int64_t tag) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (r >= n) return;
+    tag = resolve_tag(tag, status);
+    if (warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
+    const A3Smem sm = a3_carve(smem_raw + (size_t)warp * a3_warp_bytes(capacity), capacity);
+    const Image im = make_image(g);
+    const double xi = xs[r], yi = ys[r], zi = zs[r];
+    const int rc_n = row_count[r];
+    const int32_t *row = rows + r * (int64_t)capacity;
+    double *grow = gbuf + r * (int64_t)capacity * 3;
+
+    // ---- phase 0: S+(i), the row suffix with rank > i within rc
+    int m = 0;
+    for (int base = 0; base < rc_n; base += 32) {
+        const int k = base + lane;
+        bool keep = false;
+        double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;
+        int q = -1;
+        if (k < rc_n) {
+            q = row[k];
+            if (q > r) {
+                exact_disp(im, xi, yi, zi, xs[q], ys[q], zs[q], dx, dy, dz);
+                r2 = exact_r2(dx, dy, dz);
+                keep = r2 <= rc2;
+                if (!keep) {  // beyond the three-body cutoff: contributes nothing
+                    grow[3 * k] = 0.0;
+                    grow[3 * k + 1] = 0.0;
+                    grow[3 * k + 2] = 0.0;
+                }
+            }
+        }
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int slot = m + __popc(mk & lanemask_lt());
+            sm.dx[slot] = dx;
+            sm.dy[slot] = dy;
+            sm.dz[slot] = dz;
+            sm.r2[slot] = r2;
+            sm.kidx[slot] = kExactImage ? q : k;
+            sm.ax[slot] = 0.0;
+            sm.ay[slot] = 0.0;
+            sm.az[slot] = 0.0;
+        }
+        m += __popc(mk);
+    }
+    __syncwarp();
+
+    // ---- phase 1 + 2: rounds -> queue -> evaluation
+    A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false};
+    const int nsets = (m + 31) >> 5;
+    const int rounds = m >> 1;
+    int qn = 0;
+    for (int d = 1; d <= rounds; d++) {
+        const bool half_round = (2 * d == m);  // even m: pair (s, s+m/2) once
+        for (int sg = 0; sg < nsets; sg++) {
+            const int s = (sg << 5) + lane;
+            bool accept = false;
+            int t = 0;
+            double cval = 0.0;
+            if (s < m && (!half_round || s < d)) {
+                t = s + d;
+                if (t >= m) t -= m;
+                bool exact = kExactImage;
+                if (!kExactImage) {
+                    const double ex = sm.dx[t] - sm.dx[s];
+                    const double ey = sm.dy[t] - sm.dy[s];
+                    const double ez = sm.dz[t] - sm.dz[s];
+                    const double c2 = ex * ex + ey * ey + ez * ez;
+                    if (c2 <= rc2_lo) {
+                        accept = true;
+                        cval = c2;
+                    } else if (c2 <= rc2_hi) {
+                        exact = true;
+                    }
+                }
+                if (exact) {
+                    const int jr = kExactImage ? sm.kidx[s] : row[sm.kidx[s]];
+                    const int kr = kExactImage ? sm.kidx[t] : row[sm.kidx[t]];
+                    double dx, dy, dz;
+                    exact_disp(im, xs[jr], ys[jr], zs[jr], xs[kr], ys[kr], zs[kr], dx, dy, dz);
+                    const double c2 = exact_r2(dx, dy, dz);
+                    accept = c2 <= rc2;
+                    cval = c2;
+                }
+            }
+            const unsigned ma = __ballot_sync(0xffffffffu, accept);
+            if (accept) {
+                const int slot = qn + __popc(ma & lanemask_lt());
+                sm.qst[slot] = (uint32_t)s | ((uint32_t)t << 16);
+                sm.qc[slot] = cval;
+                sm.qrec[slot] = d * nsets + sg;
+            }
+            qn += __popc(ma);
+            __syncwarp();
+            if (qn >= 32) {
+                a3_chunk<kExactImage>(sm, 32, lane, im, xs, ys, zs, acc);
+                __syncwarp();
+                if (lane < qn - 32) {
+                    sm.qst[lane] = sm.qst[lane + 32];
+                    sm.qc[lane] = sm.qc[lane + 32];
+                    sm.qrec[lane] = sm.qrec[lane + 32];
+                }
+                __syncwarp();
+                qn -= 32;
+            }
+        }
+    }
+    if (qn > 0) a3_chunk<kExactImage>(sm, qn, lane, im, xs, ys, zs, acc);
+    __syncwarp();
+
+    // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
+    for (int sl = lane; sl < m; sl += 32) {
+        const int k = kExactImage ? -1 : sm.kidx[sl];
+        int kk = k;
+        if (kExactImage) {
+            // exact mode keeps ranks in kidx: recover the row index
+            const int q = sm.kidx[sl];
+            int lo = 0, hi = rc_n - 1;
+            while (lo <= hi) {
+                const int mid = (lo + hi) >> 1;
+                const int v = row[mid];
+                if (v == q) {
+                    kk = mid;
+                    break;
+                }
+                if (v < q) lo = mid + 1;
+                else hi = mid - 1;
+            }
+        }
+        grow[3 * kk] = sm.ax[sl];
+        grow[3 * kk + 1] = sm.ay[sl];
+        grow[3 * kk + 2] = sm.az[sl];
+    }
+    const double fx = group_sum<32>(acc.fx);
+    const double fy = group_sum<32>(acc.fy);
+    const double fz = group_sum<32>(acc.fz);
+    const double e = group_sum<32>(acc.e);
+    const double w = group_sum<32>(acc.w);
+    const int nt = group_sum_int<32>(acc.n);
+    const bool bad = __any_sync(0xffffffffu, acc.bad);
+    if (lane == 0) {
+        own[3 * r] = fx;
+        own[3 * r + 1] = fy;
+        own[3 * r + 2] = fz;
+        energy_rank[r] = e;
+        virial_rank[r] = w;
+        triplets_rank[r] = nt;
+        if (bad) record_status(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION);
+    }
+}
+
+// F(p) = 2 nu * (own(p) + sum over row entries q < p of G[q][mirror]); the
+// row prefix q < p is walked in order by kG lanes, then a fixed xor tree.
+constexpr int kGatherGroup = 8;
+
+__global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
+                              const int32_t *__restrict__ rows,
+                              const int32_t *__restrict__ row_count,
+                              const int32_t *__restrict__ mirror, int32_t capacity,
+                              const double *__restrict__ own, const double *__restrict__ gbuf,
+                              double two_nu, double nu, double *__restrict__ forces,
+                              double *__restrict__ energy_rank, double *__restrict__ virial_rank,
+                              const unsigned long long *status, int64_t tag) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t p = gid / kGatherGroup;
+    const int sub = (int)(gid % kGatherGroup);
+    const bool active = p < n;
+    tag = resolve_tag(tag, status);
+    if (warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    if (active) {
+        const int m = row_count[p];
+        const int32_t *row = rows + p * (int64_t)capacity;
+        const int32_t *mir = mirror + p * (int64_t)capacity;
+        for (int k = sub; k < m; k += kGatherGroup) {
+            const int q = row[k];
+            if (q >= p) break;  // rows are rank-sorted: the prefix q < p
+            const double *gq = gbuf + ((int64_t)q * capacity + mir[k]) * 3;
+            fx += gq[0];
+            fy += gq[1];
+            fz += gq[2];
+        }
+    }
+    fx = group_sum<kGatherGroup>(fx);
+    fy = group_sum<kGatherGroup>(fy);
+    fz = group_sum<kGatherGroup>(fz);
+    if (active && sub == 0) {
+        const int64_t pp = parts ? parts[p] : p;
+        forces[3 * pp] = two_nu * (own[3 * p] + fx);
+        forces[3 * pp + 1] = two_nu * (own[3 * p + 1] + fy);
+        forces[3 * pp + 2] = two_nu * (own[3 * p + 2] + fz);
+        energy_rank[p] = nu * energy_rank[p];
+        virial_rank[p] = -two_nu * virial_rank[p];
+    }
+}
+
+static size_t g_a3_granted[2] = {0, 0};
+
+template <typename K>
+static void a3_grant(K kernel, size_t bytes, size_t &granted) {
+    if (bytes > 48 * 1024 && bytes > granted) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        granted = bytes;
+    }
+}
+
+}  // namespace rb
+
+using namespace rb;
+
+extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
+    // own (n x 3) + G (n x capacity x 3), doubles
+    return (size_t)(n > 0 ? n : 1) * 3 * sizeof(double) * (size_t)(1 + capacity);
+}
+
+extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
+                           const double *zs, const int32_t *cell_particles, const int32_t *rows,
+                           const int32_t *row_count, const int32_t *mirror, int32_t capacity,
+                           double rc, double nu, double *forces, double *energy_rank,
+                           double *virial_rank, int32_t *triplets_rank, void *scratch,
+                           size_t scratch_bytes, unsigned long long *status, int64_t tag,
+                           void *stream) {
+    if (!g || n < 0 || capacity <= 0 || capacity > 4096 || !mirror || !scratch) return RB_ERR_ARGUMENT;
+    if (scratch_bytes < rb_atm_scratch_bytes(n, capacity)) return RB_ERR_ARGUMENT;
+    if (n == 0) return RB_OK;
+    const double rc2 = rc * rc;
+    bool exact_image = false;
+    if (g->periodic)
+        for (int d = 0; d < 3; d++)
+            if (!(g->box[d] > 4.0 * rc * (1.0 + 1e-12))) exact_image = true;
+    const size_t per = a3_warp_bytes(capacity);
+    int warps = kA3Warps;
+    while (warps > 1 && (size_t)warps * per > 227 * 1024) warps--;
+    if ((size_t)warps * per > 227 * 1024) return RB_ERR_ARGUMENT;
+    const size_t smem = (size_t)warps * per;
+    const unsigned blocks = (unsigned)((n + warps - 1) / warps);
+    cudaStream_t st = as_stream(stream);
+    double *own = (double *)scratch;
+    double *gbuf = own + 3 * n;
+    if (exact_image) {
+        a3_grant(k_atm3<true>, smem, g_a3_granted[0]);
+        k_atm3<true><<<blocks, warps * 32, smem, st>>>(*g, n, xs, ys, zs, rows, row_count,
+                                                        capacity, rc2, rc2, rc2, own, gbuf,
+                                                        energy_rank, virial_rank, triplets_rank,
+                                                        status, tag);
+        note_launches(1);
+    } else {
+        a3_grant(k_atm3<false>, smem, g_a3_granted[1]);
+        k_atm3<false><<<blocks, warps * 32, smem, st>>>(
+            *g, n, xs, ys, zs, rows, row_count, capacity, rc2, rc2 * (1.0 - kA3Margin),
+            rc2 * (1.0 + kA3Margin), own, gbuf, energy_rank, virial_rank, triplets_rank, status,
+            tag);
+        note_launches(1);
+    }
+    const int tb = 256;
+    const int64_t threads = n * kGatherGroup;
+    k_atm3_gather<<<(unsigned)((threads + tb - 1) / tb), tb, 0, st>>>(
+        n, cell_particles, rows, row_count, mirror, capacity, own, gbuf, 2.0 * nu, nu, forces,
+        energy_rank, virial_rank, status, tag);
+    note_launches(1);
+    return launch_status();
+}

@@ -3,7 +3,10 @@
 // For each particle (rank order) one warp walks the canonical neighbour cells
 // of its base cell (respamd/containers.py:319-333 / :403-423) as one
 // flattened candidate range: lane l of a 32-wide chunk owns candidate l,
-// located by a binary search over the warp-scanned cell counts.  The pair
+// located by a binary search over the warp-scanned cell counts.  The (at most
+// 27) neighbour cells are sorted by flat id first, so every row lists its
+// neighbours in ascending rank order -- the Newton-3 triplet pass relies on
+// it (S+(i) is a row suffix; mirror indices come from a binary search).  The pair
 // distance uses the reference arithmetic (a - b, single-shift minimum image,
 // no FMA), and survivors (r^2 <= r_list^2, inclusive, self excluded) are
 // appended with a ballot in candidate order, so rows are deterministic and
@@ -30,57 +33,106 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
     const int cby = (cb / g.cells[2]) % g.cells[1];
     const int cbx = cb / (g.cells[2] * g.cells[1]);
     int32_t *row = rows + r * (int64_t)capacity;
-    int count = 0;
+    // 1. the (at most 27) valid neighbour cells, one per lane, sorted by flat
+    //    id so that rows come out in ascending rank order
+    int my_cell = 0x7fffffff;
+    int nvalid = 0;
     for (int ob = 0; ob < g.n_offsets; ob += 32) {
-        int o = ob + lane;
-        int cstart = 0, ccount = 0;
-        if (o < g.n_offsets) {
-            int cc = neighbor_cell(g, cbx, cby, cbz, o);
-            if (cc >= 0) {
-                cstart = cell_start[cc];
-                ccount = cell_start[cc + 1] - cstart;
-            }
-        }
-        // inclusive scan of the chunk's cell counts
-        int incl = ccount;
+        const int o = ob + lane;
+        const int cc = o < g.n_offsets ? neighbor_cell(g, cbx, cby, cbz, o) : -1;
+        const unsigned mv = __ballot_sync(0xffffffffu, cc >= 0);
+        // lane nvalid + q receives the q-th valid cell of this chunk
+        const int q = lane - nvalid;
+        const unsigned src = (q >= 0 && q < __popc(mv)) ? __fns(mv, 0, q + 1) : 0u;
+        const int v = __shfl_sync(0xffffffffu, cc, (int)(src & 31u));
+        if (q >= 0 && q < __popc(mv)) my_cell = v;
+        nvalid += __popc(mv);
+    }
+    // bitonic sort (ascending) of my_cell across the warp
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        for (int base = 0; base < total; base += 32) {
-            const int cand = base + lane;
-            // owner lane of cand: first lane whose inclusive prefix exceeds cand
-            int pos = 0;
+    for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                int v = __shfl_sync(0xffffffffu, incl, pos + step - 1);
-                if (v <= cand) pos += step;
-            }
-            const int owner_incl = __shfl_sync(0xffffffffu, incl, pos);
-            const int owner_count = __shfl_sync(0xffffffffu, ccount, pos);
-            const int owner_start = __shfl_sync(0xffffffffu, cstart, pos);
-            bool keep = false;
-            int j = 0;
-            if (cand < total) {
-                j = owner_start + (cand - (owner_incl - owner_count));
-                if (j != r) {
-                    double dx, dy, dz;
-                    exact_disp(im, xi, yi, zi, xs[j], ys[j], zs[j], dx, dy, dz);
-                    keep = exact_r2(dx, dy, dz) <= rl2;
-                }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            const int slot = count + __popc(m & lanemask_lt());
-            if (keep && slot < capacity) row[slot] = j;
-            count += __popc(m);
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int other = __shfl_xor_sync(0xffffffffu, my_cell, j);
+            const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
+            my_cell = take_min ? min(my_cell, other) : max(my_cell, other);
         }
+    }
+    int cstart = 0, ccount = 0;
+    if (lane < nvalid) {
+        cstart = cell_start[my_cell];
+        ccount = cell_start[my_cell + 1] - cstart;
+    }
+    // 2. flattened candidate range over the sorted cells
+    int incl = ccount;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int count = 0;
+    for (int base = 0; base < total; base += 32) {
+        const int cand = base + lane;
+        // owner lane of cand: first lane whose inclusive prefix exceeds cand
+        int pos = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, pos + step - 1);
+            if (v <= cand) pos += step;
+        }
+        const int owner_incl = __shfl_sync(0xffffffffu, incl, pos);
+        const int owner_count = __shfl_sync(0xffffffffu, ccount, pos);
+        const int owner_start = __shfl_sync(0xffffffffu, cstart, pos);
+        bool keep = false;
+        int j = 0;
+        if (cand < total) {
+            j = owner_start + (cand - (owner_incl - owner_count));
+            if (j != r) {
+                double dx, dy, dz;
+                exact_disp(im, xi, yi, zi, xs[j], ys[j], zs[j], dx, dy, dz);
+                keep = exact_r2(dx, dy, dz) <= rl2;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        const int slot = count + __popc(m & lanemask_lt());
+        if (keep && slot < capacity) row[slot] = j;
+        count += __popc(m);
     }
     if (lane == 0) {
         row_count[r] = count < capacity ? count : capacity;
         if (count > capacity) atomicMax(max_count, count);
     }
+}
+
+// mirror[p][k] = position of p in the row of q = rows[p][k], for q < p
+// (binary search: rows are sorted by rank); -1 for q > p.
+__global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
+                         const int32_t *__restrict__ row_count, int32_t capacity,
+                         int32_t *__restrict__ mirror) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t p = gid / capacity;
+    const int k = (int)(gid % capacity);
+    if (p >= n) return;
+    const int m = row_count[p];
+    if (k >= m) return;
+    const int q = rows[p * (int64_t)capacity + k];
+    int res = -1;
+    if (q < p) {
+        const int32_t *rq = rows + (int64_t)q * capacity;
+        int lo = 0, hi = row_count[q] - 1;
+        while (lo <= hi) {
+            const int mid = (lo + hi) >> 1;
+            const int v = rq[mid];
+            if (v == (int)p) {
+                res = mid;
+                break;
+            }
+            if (v < (int)p) lo = mid + 1;
+            else hi = mid - 1;
+        }
+    }
+    mirror[p * (int64_t)capacity + k] = res;
 }
 
 }  // namespace rb
@@ -98,6 +150,18 @@ extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *xs, const dou
     unsigned blocks = (unsigned)((n + kNlistWarps - 1) / kNlistWarps);
     k_nlist<<<blocks, kNlistWarps * 32, 0, as_stream(stream)>>>(
         *g, n, xs, ys, zs, cell_start, cell_of_rank, rl2, capacity, rows, row_count, max_count);
+    note_launches(1);
+    return launch_status();
+}
+
+extern "C" int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_count,
+                               int32_t capacity, int32_t *mirror, void *stream) {
+    if (n < 0 || capacity <= 0 || !rows || !row_count || !mirror) return RB_ERR_ARGUMENT;
+    if (n == 0) return RB_OK;
+    const int64_t threads = n * (int64_t)capacity;
+    const int tb = 256;
+    k_mirror<<<(unsigned)((threads + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
+        n, rows, row_count, capacity, mirror);
     note_launches(1);
     return launch_status();
 }

@@ -69,6 +69,8 @@ class ForceEngine:
         self.cell_start = None
         self.bin_scratch = None
         self.rows = None
+        self.mirror = None
+        self.atm_scratch = None
         self.capacity = 0
         self._geom_key = None
         self._grid = None
@@ -132,8 +134,12 @@ class ForceEngine:
 
     def _ensure_rows(self, capacity: int) -> None:
         if self.rows is None or self.capacity != capacity:
-            self.rows = self.torch.empty(max(self.n, 1) * capacity, dtype=self.torch.int32,
-                                         device=self.device)
+            torch = self.torch
+            self.rows = torch.empty(max(self.n, 1) * capacity, dtype=torch.int32, device=self.device)
+            self.mirror = torch.empty(max(self.n, 1) * capacity, dtype=torch.int32,
+                                      device=self.device)
+            need = int(self.L.rb_atm_scratch_bytes(self.n, capacity))
+            self.atm_scratch = torch.empty((need + 7) // 8, dtype=torch.float64, device=self.device)
             self.capacity = capacity
 
     def nlist(self, geom: Geometry, r_list: float, capacity: Optional[int] = None,
@@ -152,6 +158,9 @@ class ForceEngine:
                                  int(self.capacity), ptr(self.rows), ptr(self.row_count),
                                  ptr(self.max_count), self.stream)
             _lib.check(st, "rb_nlist")
+            st = self.L.rb_nlist_mirror(self.n, ptr(self.rows), ptr(self.row_count),
+                                        int(self.capacity), ptr(self.mirror), self.stream)
+            _lib.check(st, "rb_nlist_mirror")
             if not checked:
                 return
             worst = int(self.max_count.item())
@@ -167,6 +176,13 @@ class ForceEngine:
     # -------------------------------------------------------------- passes
     def lj(self, geom: Geometry, rc: float, epsilon: float, sigma: float, forces,
            tag: int = 0) -> None:
+        self.lj_kernel(geom, rc, epsilon, sigma, forces, tag)
+        self.sum_f64(self.e_rank, SCALAR_E2)
+        self.sum_f64(self.w_rank, SCALAR_W2)
+
+    def lj_kernel(self, geom: Geometry, rc: float, epsilon: float, sigma: float, forces,
+                  tag: int = 0) -> None:
+        """The rb_lj_pass launch alone."""
         g = self.grid_struct(geom)
         st = self.L.rb_lj_pass(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
                                ptr(self.parts), ptr(self.rows), ptr(self.row_count),
@@ -174,27 +190,50 @@ class ForceEngine:
                                ptr(forces), ptr(self.e_rank), ptr(self.w_rank), ptr(self.status),
                                int(tag), self.stream)
         _lib.check(st, "rb_lj_pass")
-        self.sum_f64(self.e_rank, SCALAR_E2)
-        self.sum_f64(self.w_rank, SCALAR_W2)
 
     def atm(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
             count_visits: bool = True) -> None:
-        g = self.grid_struct(geom)
-        st = self.L.rb_atm_pass(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
-                                ptr(self.parts), ptr(self.rows), ptr(self.row_count),
-                                int(self.capacity), float(rc), float(nu), ptr(forces),
-                                ptr(self.e_rank), ptr(self.w_rank), ptr(self.v_rank),
-                                ptr(self.status), int(tag), self.stream)
-        _lib.check(st, "rb_atm_pass")
+        """Newton-3 triplet pass; ``self.visits`` <- unique triplet count."""
+        self.atm_kernel(geom, rc, nu, forces, tag)
         self.sum_f64(self.e_rank, SCALAR_E3)
         self.sum_f64(self.w_rank, SCALAR_W3)
         if count_visits:
-            st = self.L.rb_reduce_sum_i32(self.n, ptr(self.v_rank), ptr(self.visits),
-                                          ptr(self.red_scratch), self.stream)
-            _lib.check(st, "rb_reduce_sum_i32")
+            self._count()
+
+    def atm_kernel(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0) -> None:
+        """The rb_atm_pass launch alone (bench timing)."""
+        g = self.grid_struct(geom)
+        st = self.L.rb_atm_pass(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
+                                ptr(self.parts), ptr(self.rows), ptr(self.row_count),
+                                ptr(self.mirror), int(self.capacity), float(rc), float(nu),
+                                ptr(forces), ptr(self.e_rank), ptr(self.w_rank), ptr(self.v_rank),
+                                ptr(self.atm_scratch), self.atm_scratch.numel() * 8,
+                                ptr(self.status), int(tag), self.stream)
+        _lib.check(st, "rb_atm_pass")
+
+    def atm_c01(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
+                reduce: bool = True) -> None:
+        """C01 (owner-computes) triplet pass; ``self.visits`` <- accepted visits."""
+        g = self.grid_struct(geom)
+        st = self.L.rb_atm_pass_c01(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys),
+                                    ptr(self.zs), ptr(self.parts), ptr(self.rows),
+                                    ptr(self.row_count), int(self.capacity), float(rc), float(nu),
+                                    ptr(forces), ptr(self.e_rank), ptr(self.w_rank),
+                                    ptr(self.v_rank), ptr(self.status), int(tag), self.stream)
+        _lib.check(st, "rb_atm_pass_c01")
+        if not reduce:
+            return
+        self.sum_f64(self.e_rank, SCALAR_E3)
+        self.sum_f64(self.w_rank, SCALAR_W3)
+        self._count()
+
+    def _count(self) -> None:
+        st = self.L.rb_reduce_sum_i32(self.n, ptr(self.v_rank), ptr(self.visits),
+                                      ptr(self.red_scratch), self.stream)
+        _lib.check(st, "rb_reduce_sum_i32")
 
     def visit_rows(self, geom: Geometry, rc: float) -> np.ndarray:
-        """Sorted (i, j, k) rows of every accepted visit (after :meth:`atm`)."""
+        """Sorted (i, j, k) rows of every accepted visit (after :meth:`atm_c01`)."""
         torch = self.torch
         counts = self.v_rank[: self.n].to(torch.int64)
         offsets = torch.cumsum(counts, 0) - counts

@@ -100,6 +100,32 @@ def test_triplet_visits_bit_exact(pkg, name):
     assert pkg.triplet_count(s, float(g["cutoff"])) == int(g["brute_count"])
 
 
+@pytest.mark.parametrize("name", SMALL)
+def test_newton3_matches_c01_enumeration(pkg, name):
+    """The Newton-3 pass (each triplet once) and the C01 pass (each triplet
+    from every member) are independent enumerations: same forces, energies
+    and counts (unique x 3 == visits)."""
+    from paper_2507_11172_b200 import containers as pc
+
+    g = load_golden(name)
+    s = _system(pkg, g["positions"], g["box"], bool(g["periodic"]))
+    ff = pkg.ForceField(nu=float(g["nu"]), cutoff=float(g["cutoff"]))
+    grid = pkg.build_cell_grid(s, ff.cutoff)
+    f3, e3, w3 = pkg.c01_triplet_pass(grid, s, ff)
+    f1, e1, w1 = pc.c01_triplet_pass_owner(grid, s, ff)
+    assert normwise(f3, f1) <= FORCE_TOL
+    assert _rel(e3, e1) <= ENERGY_TOL and _rel(w3, w1) <= VIRIAL_TOL
+    assert 3 * pkg.triplet_count(s, ff.cutoff) == pc.triplet_visit_count(s, ff.cutoff)
+
+
+def test_newton3_forces_sum_to_zero(pkg):
+    s = pkg.systems.fcc_system(6, jitter=0.05, seed=4)
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5)
+    c = pkg.CudaLinkedCells()
+    c.triplet_pass(s, ff)
+    assert np.max(np.abs(s.forces_3b.sum(axis=0))) <= 1e-12 * s.n
+
+
 def test_write_discipline_single_base_cell(pkg, rng):
     pos = random_positions(rng, 150, (10.0,) * 3, True)
     s = _system(pkg, pos, (10.0,) * 3, True)

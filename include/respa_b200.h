@@ -99,9 +99,10 @@ RB_API int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_
 /* ---- neighbour rows: the survivor lists of containers.py:437-474 -------
  * Row r (rank order) lists, in stencil order, the ranks within r_list of
  * particle r (reference pair-distance arithmetic, inclusive).  Rows hold at
- * most `capacity` entries; the longest overflowing row length is
- * atomicMax-ed into the device int *max_count (caller initialises it to 0)
- * and the row is truncated, so callers must check it before trusting a pass. */
+ * most `capacity` entries; the longest row length is atomicMax-ed into the
+ * device int *max_count (caller initialises it to 0).  A row longer than
+ * `capacity` is truncated, so callers must check *max_count <= capacity
+ * before trusting a pass. */
 RB_API int rb_nlist(const rb_grid *g, int64_t n, const double *xs, const double *ys, const double *zs,
              const int32_t *cell_start, const int32_t *cell_of_rank, double r_list,
              int32_t capacity, int32_t *rows, int32_t *row_count, int32_t *max_count,
@@ -129,12 +130,15 @@ RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_co
  * member; forces on all three members are accumulated without atomics in a
  * fixed order (deterministic).  Writes forces (n,3) in particle order
  * (overwritten), per-rank energy (phi per owned triplet), virial and the
- * number of owned (unique) triplets.  Scratch: rb_atm_scratch_bytes. */
+ * number of owned (unique) triplets.  Scratch: rb_atm_scratch_bytes.
+ * slot_capacity (<= capacity) sizes the per-warp shared-memory slots; a
+ * particle with more higher-rank neighbours than that records
+ * RB_KIND_CAPACITY in the status word (pass the longest row length). */
 RB_API size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity);
 RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
                        const double *zs, const int32_t *cell_particles, const int32_t *rows,
                        const int32_t *row_count, const int32_t *mirror, int32_t capacity,
-                       double rc, double nu, double *forces, double *energy_rank,
+                       int32_t slot_capacity, double rc, double nu, double *forces, double *energy_rank,
                        double *virial_rank, int32_t *triplets_rank, void *scratch,
                        size_t scratch_bytes, unsigned long long *status, int64_t tag,
                        void *stream);

@@ -171,8 +171,8 @@ template <bool kExactImage>
 __global__ void __launch_bounds__(kA3Warps * 32)
     k_atm3(rb_grid g, int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
            const double *__restrict__ zs, const int32_t *__restrict__ rows,
-           const int32_t *__restrict__ row_count, int32_t capacity, double rc2, double rc2_lo,
-           double rc2_hi, double *__restrict__ own, double *__restrict__ gbuf,
+           const int32_t *__restrict__ row_count, int32_t capacity, int32_t slots, double rc2,
+           double rc2_lo, double rc2_hi, double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, unsigned long long *status, int64_t tag) {
     extern __shared__ __align__(16) char smem_raw[];
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
     if (r >= n) return;
     tag = resolve_tag(tag, status);
     if (warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
-    const A3Smem sm = a3_carve(smem_raw + (size_t)warp * a3_warp_bytes(capacity), capacity);
+    const A3Smem sm = a3_carve(smem_raw + (size_t)warp * a3_warp_bytes(slots), slots);
     const Image im = make_image(g);
     const double xi = xs[r], yi = ys[r], zi = zs[r];
     const int rc_n = row_count[r];
@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(kA3Warps * 32)
             }
         }
         const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        if (m + __popc(mk) > slots) {  // S+(i) does not fit the shared-memory slots
+            if (lane == 0) record_status(status, tag, RB_KIND_CAPACITY);
+            return;
+        }
         if (keep) {
             const int slot = m + __popc(mk & lanemask_lt());
             sm.dx[slot] = dx;
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
                 const int slot = qn + __popc(ma & lanemask_lt());
                 sm.qst[slot] = (uint32_t)s | ((uint32_t)t << 16);
                 sm.qc[slot] = cval;
-                sm.qrec[slot] = d * nsets + sg;
+                sm.qrec[slot] = d;  // a round is one record: its s (and t) are distinct
             }
             qn += __popc(ma);
             __syncwarp();
@@ -396,11 +400,12 @@ extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
 extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
                            const double *zs, const int32_t *cell_particles, const int32_t *rows,
                            const int32_t *row_count, const int32_t *mirror, int32_t capacity,
-                           double rc, double nu, double *forces, double *energy_rank,
+                           int32_t slot_capacity, double rc, double nu, double *forces, double *energy_rank,
                            double *virial_rank, int32_t *triplets_rank, void *scratch,
                            size_t scratch_bytes, unsigned long long *status, int64_t tag,
                            void *stream) {
     if (!g || n < 0 || capacity <= 0 || capacity > 4096 || !mirror || !scratch) return RB_ERR_ARGUMENT;
+    if (slot_capacity <= 0 || slot_capacity > capacity) slot_capacity = capacity;
     if (scratch_bytes < rb_atm_scratch_bytes(n, capacity)) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     const double rc2 = rc * rc;
@@ -408,7 +413,7 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const 
     if (g->periodic)
         for (int d = 0; d < 3; d++)
             if (!(g->box[d] > 4.0 * rc * (1.0 + 1e-12))) exact_image = true;
-    const size_t per = a3_warp_bytes(capacity);
+    const size_t per = a3_warp_bytes(slot_capacity);
     int warps = kA3Warps;
     while (warps > 1 && (size_t)warps * per > 227 * 1024) warps--;
     if ((size_t)warps * per > 227 * 1024) return RB_ERR_ARGUMENT;
@@ -420,14 +425,16 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const 
     if (exact_image) {
         a3_grant(k_atm3<true>, smem, g_a3_granted[0]);
         k_atm3<true><<<blocks, warps * 32, smem, st>>>(*g, n, xs, ys, zs, rows, row_count,
-                                                        capacity, rc2, rc2, rc2, own, gbuf,
+                                                        capacity, slot_capacity, rc2, rc2, rc2,
+                                                        own, gbuf,
                                                         energy_rank, virial_rank, triplets_rank,
                                                         status, tag);
         note_launches(1);
     } else {
         a3_grant(k_atm3<false>, smem, g_a3_granted[1]);
         k_atm3<false><<<blocks, warps * 32, smem, st>>>(
-            *g, n, xs, ys, zs, rows, row_count, capacity, rc2, rc2 * (1.0 - kA3Margin),
+            *g, n, xs, ys, zs, rows, row_count, capacity, slot_capacity, rc2,
+            rc2 * (1.0 - kA3Margin),
             rc2 * (1.0 + kA3Margin), own, gbuf, energy_rank, virial_rank, triplets_rank, status,
             tag);
         note_launches(1);

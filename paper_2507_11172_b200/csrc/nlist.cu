@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
     }
     if (lane == 0) {
         row_count[r] = count < capacity ? count : capacity;
-        if (count > capacity) atomicMax(max_count, count);
+        // longest row seen (also the overflow witness when > capacity); the
+        // plain read first keeps the atomic off the common path
+        if (count > *(volatile int32_t *)max_count) atomicMax(max_count, count);
     }
 }
 

@@ -72,6 +72,7 @@ class ForceEngine:
         self.mirror = None
         self.atm_scratch = None
         self.capacity = 0
+        self.slots = 0  # shared-memory slots of the triplet pass (longest row)
         self._geom_key = None
         self._grid = None
 
@@ -165,13 +166,17 @@ class ForceEngine:
                 return
             worst = int(self.max_count.item())
             if worst <= self.capacity:
+                self.slots = min(self.capacity, max(32, _round_up(worst, 32)))
                 return
             if worst > 4096:
                 raise CapacityError(f"a neighbour row holds {worst} entries (> 4096)")
             capacity = min(4096, _round_up(int(worst * 1.25) + 32, 32))
 
     def overflowed(self) -> bool:
-        return int(self.max_count.item()) > self.capacity
+        if int(self.max_count.item()) > self.capacity:
+            return True
+        err = self.read_status()
+        return err is not None and err[1] == _lib.RB_KIND_CAPACITY
 
     # -------------------------------------------------------------- passes
     def lj(self, geom: Geometry, rc: float, epsilon: float, sigma: float, forces,
@@ -205,7 +210,8 @@ class ForceEngine:
         g = self.grid_struct(geom)
         st = self.L.rb_atm_pass(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
                                 ptr(self.parts), ptr(self.rows), ptr(self.row_count),
-                                ptr(self.mirror), int(self.capacity), float(rc), float(nu),
+                                ptr(self.mirror), int(self.capacity),
+                                int(self.slots or self.capacity), float(rc), float(nu),
                                 ptr(forces), ptr(self.e_rank), ptr(self.w_rank), ptr(self.v_rank),
                                 ptr(self.atm_scratch), self.atm_scratch.numel() * 8,
                                 ptr(self.status), int(tag), self.stream)

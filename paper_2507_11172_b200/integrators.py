@@ -151,6 +151,7 @@ class DeviceRespa:
         nsamples = schedule.num_iterations // self.interval + 1
         self.trace_dev = torch.zeros((nsamples, 8), dtype=f64, device=dev)
         self.capacity = capacity
+        self.slots = None
         self.geom = None
         self.graph = None
 
@@ -229,7 +230,13 @@ class DeviceRespa:
         if self.capacity is None:
             geom = self._geom()
             eng.bin(geom, self.x)
-            self.capacity = min(4096, _round_up(int(eng.estimate_capacity(geom, self.r_list) * 1.5) + 32, 32))
+            eng.nlist(geom, self.r_list, capacity=None, checked=True)
+            longest = int(eng.max_count.item())
+            # rows and triplet slots sized from the initial longest row with margin;
+            # an overflow later is detected and the run is repeated larger
+            self.capacity = min(4096, _round_up(int(longest * 1.3) + 16, 32))
+        self.slots = self.capacity  # S+(i) can be a whole row
+        eng.slots = self.slots
         self._forces(0, True, self.f2_old)
         self._record()
 

@@ -34,19 +34,20 @@ namespace rb {
 
 constexpr int kA3Warps = 4;
 constexpr int kA3Queue = 64;
-constexpr double kA3Margin = 1e-10;
+constexpr double kA3Margin = 1e-10;  // fp64 estimate vs the reference arithmetic
+constexpr double kA3Band = 1e-5;     // fp32 filter vs the fp64 estimate
 
 struct A3Smem {
-    double *dx, *dy, *dz, *r2;  // slots
+    double *dx, *dy, *dz, *r2;  // slots: d_ij = x_i - x_j, r_ij^2
     double *ax, *ay, *az;       // slot force accumulators (units of 2 nu)
-    double *qc;                 // queue: r_jk^2
+    float4 *f4;                 // slots: d_ij in fp32 for the candidate filter
     int32_t *kidx;              // slot -> row index
     uint32_t *qst;              // queue: s | t << 16
     int32_t *qrec;              // queue: round record id
 };
 
 __host__ __device__ inline size_t a3_warp_bytes(int capacity) {
-    size_t b = (size_t)capacity * (7 * sizeof(double)) + (size_t)kA3Queue * sizeof(double);
+    size_t b = (size_t)capacity * (7 * sizeof(double) + sizeof(float4));
     b += (size_t)capacity * sizeof(int32_t) + (size_t)kA3Queue * 2 * sizeof(int32_t);
     return (b + 15) & ~(size_t)15;
 }
@@ -60,8 +61,8 @@ __device__ inline A3Smem a3_carve(char *base, int capacity) {
     s.ax = s.r2 + capacity;
     s.ay = s.ax + capacity;
     s.az = s.ay + capacity;
-    s.qc = s.az + capacity;
-    s.kidx = (int32_t *)(s.qc + kA3Queue);
+    s.f4 = (float4 *)(s.az + capacity);
+    s.kidx = (int32_t *)(s.f4 + capacity);
     s.qst = (uint32_t *)(s.kidx + capacity);
     s.qrec = (int32_t *)(s.qst + kA3Queue);
     return s;
@@ -76,6 +77,7 @@ struct A3Acc {
 // evaluate queue entry `q` (lane-private), add f_i/E/W to acc, return f_j, f_k
 template <bool kExactImage>
 __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im,
+                                        const int32_t *__restrict__ row,
                                         const double *__restrict__ xs,
                                         const double *__restrict__ ys,
                                         const double *__restrict__ zs, A3Acc &acc, double fj[3],
@@ -83,22 +85,26 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
     const uint32_t st = sm.qst[q];
     s = (int)(st & 0xffffu);
     t = (int)(st >> 16);
-    const double a = sm.r2[s], b = sm.r2[t], c = sm.qc[q];
+    const double a = sm.r2[s], b = sm.r2[t];
     const double dijx = sm.dx[s], dijy = sm.dy[s], dijz = sm.dz[s];
     const double dikx = sm.dx[t], diky = sm.dy[t], dikz = sm.dz[t];
-    if (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ || c < RB_MIN_DISTANCE_SQ) {
-        acc.bad = true;
-        fj[0] = fj[1] = fj[2] = fk[0] = fk[1] = fk[2] = 0.0;
-        return false;
-    }
     double djkx, djky, djkz;  // x_j - x_k
+    double c;
     if (kExactImage) {
-        const int j = sm.kidx[s] >> 0, k = sm.kidx[t] >> 0;  // rank indices (exact mode)
+        // the reference's raw-position minimum image (containers.py:497-513)
+        const int j = row[sm.kidx[s]], k = row[sm.kidx[t]];
         exact_disp(im, xs[j], ys[j], zs[j], xs[k], ys[k], zs[k], djkx, djky, djkz);
+        c = exact_r2(djkx, djky, djkz);
     } else {
         djkx = dikx - dijx;
         djky = diky - dijy;
         djkz = dikz - dijz;
+        c = djkx * djkx + djky * djky + djkz * djkz;
+    }
+    if (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ || c < RB_MIN_DISTANCE_SQ) {
+        acc.bad = true;
+        fj[0] = fj[1] = fj[2] = fk[0] = fk[1] = fk[2] = 0.0;
+        return false;
     }
     const double u = a + b - c;
     const double v = a + c - b;
@@ -135,6 +141,7 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
 // accumulators, one round-record at a time (records are contiguous runs)
 template <bool kExactImage>
 __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, const Image &im,
+                                         const int32_t *__restrict__ row,
                                          const double *__restrict__ xs,
                                          const double *__restrict__ ys,
                                          const double *__restrict__ zs, A3Acc &acc) {
@@ -142,7 +149,7 @@ __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, co
     int s = 0, t = 0, rec = -1;
     bool pending = false;
     if (lane < cnt) {
-        pending = a3_eval<kExactImage>(sm, lane, im, xs, ys, zs, acc, fj, fk, s, t);
+        pending = a3_eval<kExactImage>(sm, lane, im, row, xs, ys, zs, acc, fj, fk, s, t);
         rec = sm.qrec[lane];
     }
     unsigned todo = __ballot_sync(0xffffffffu, pending);
@@ -172,7 +179,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
     k_atm3(rb_grid g, int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
            const double *__restrict__ zs, const int32_t *__restrict__ rows,
            const int32_t *__restrict__ row_count, int32_t capacity, int32_t slots, double rc2,
-           double rc2_lo, double rc2_hi, double *__restrict__ own, double *__restrict__ gbuf,
+           double rc2_lo, double rc2_hi, float rc2f_lo, float rc2f_hi, double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, unsigned long long *status, int64_t tag) {
     extern __shared__ __align__(16) char smem_raw[];
@@ -220,7 +227,8 @@ __global__ void __launch_bounds__(kA3Warps * 32)
             sm.dy[slot] = dy;
             sm.dz[slot] = dz;
             sm.r2[slot] = r2;
-            sm.kidx[slot] = kExactImage ? q : k;
+            sm.kidx[slot] = k;
+            sm.f4[slot] = make_float4((float)dx, (float)dy, (float)dz, 0.0f);
             sm.ax[slot] = 0.0;
             sm.ay[slot] = 0.0;
             sm.az[slot] = 0.0;
@@ -229,91 +237,90 @@ __global__ void __launch_bounds__(kA3Warps * 32)
     }
     __syncwarp();
 
-    // ---- phase 1 + 2: rounds -> queue -> evaluation
+    // ---- phase 1 + 2: candidates by rounds (flattened over lanes) -> queue
+    // Round d (1..m/2) pairs slot s with slot (s + d) mod m; for even m the
+    // last round only needs s < m/2.  Flat index f = (d-1)*m + s.
     A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false};
-    const int nsets = (m + 31) >> 5;
     const int rounds = m >> 1;
+    const int full_rounds = (m & 1) ? rounds : rounds - 1;
+    const int total = full_rounds * m + ((m & 1) ? 0 : (m >> 1));
+    const float inv_m = m > 0 ? 1.0f / (float)m : 0.0f;
     int qn = 0;
-    for (int d = 1; d <= rounds; d++) {
-        const bool half_round = (2 * d == m);  // even m: pair (s, s+m/2) once
-        for (int sg = 0; sg < nsets; sg++) {
-            const int s = (sg << 5) + lane;
-            bool accept = false;
-            int t = 0;
-            double cval = 0.0;
-            if (s < m && (!half_round || s < d)) {
-                t = s + d;
-                if (t >= m) t -= m;
-                bool exact = kExactImage;
-                if (!kExactImage) {
-                    const double ex = sm.dx[t] - sm.dx[s];
-                    const double ey = sm.dy[t] - sm.dy[s];
-                    const double ez = sm.dz[t] - sm.dz[s];
-                    const double c2 = ex * ex + ey * ey + ez * ez;
-                    if (c2 <= rc2_lo) {
-                        accept = true;
-                        cval = c2;
-                    } else if (c2 <= rc2_hi) {
-                        exact = true;
-                    }
-                }
-                if (exact) {
-                    const int jr = kExactImage ? sm.kidx[s] : row[sm.kidx[s]];
-                    const int kr = kExactImage ? sm.kidx[t] : row[sm.kidx[t]];
+    for (int base = 0; base < total; base += 32) {
+        const int f = base + lane;
+        bool accept = false;
+        int s = 0, t = 0, d = 0;
+        if (f < total) {
+            int dq = (int)((float)f * inv_m);
+            s = f - dq * m;
+            if (s < 0) {
+                dq--;
+                s += m;
+            } else if (s >= m) {
+                dq++;
+                s -= m;
+            }
+            d = dq + 1;
+            t = s + d;
+            if (t >= m) t -= m;
+            // fp32 filter: settles every pair farther than 1e-5 (relative)
+            // from the cutoff; the band in between is decided in fp64 below
+            const float4 ps = sm.f4[s], pt = sm.f4[t];
+            const float ex = pt.x - ps.x, ey = pt.y - ps.y, ez = pt.z - ps.z;
+            const float c2f = ex * ex + ey * ey + ez * ez;
+            if (kExactImage) {
+                // box under four cutoffs: d_ik - d_ij need not be the minimum
+                // image, so every candidate takes the reference arithmetic
+                (void)c2f;
+                const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
+                double dx, dy, dz;
+                exact_disp(im, xs[jr], ys[jr], zs[jr], xs[kr], ys[kr], zs[kr], dx, dy, dz);
+                accept = exact_r2(dx, dy, dz) <= rc2;
+            } else if (c2f <= rc2f_lo) {
+                accept = true;
+            } else if (c2f <= rc2f_hi) {
+                const double ex2 = sm.dx[t] - sm.dx[s];
+                const double ey2 = sm.dy[t] - sm.dy[s];
+                const double ez2 = sm.dz[t] - sm.dz[s];
+                const double c2 = ex2 * ex2 + ey2 * ey2 + ez2 * ez2;
+                if (c2 <= rc2_lo) {
+                    accept = true;
+                } else if (c2 <= rc2_hi) {
+                    const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
                     double dx, dy, dz;
                     exact_disp(im, xs[jr], ys[jr], zs[jr], xs[kr], ys[kr], zs[kr], dx, dy, dz);
-                    const double c2 = exact_r2(dx, dy, dz);
-                    accept = c2 <= rc2;
-                    cval = c2;
+                    accept = exact_r2(dx, dy, dz) <= rc2;
                 }
-            }
-            const unsigned ma = __ballot_sync(0xffffffffu, accept);
-            if (accept) {
-                const int slot = qn + __popc(ma & lanemask_lt());
-                sm.qst[slot] = (uint32_t)s | ((uint32_t)t << 16);
-                sm.qc[slot] = cval;
-                sm.qrec[slot] = d;  // a round is one record: its s (and t) are distinct
-            }
-            qn += __popc(ma);
-            __syncwarp();
-            if (qn >= 32) {
-                a3_chunk<kExactImage>(sm, 32, lane, im, xs, ys, zs, acc);
-                __syncwarp();
-                if (lane < qn - 32) {
-                    sm.qst[lane] = sm.qst[lane + 32];
-                    sm.qc[lane] = sm.qc[lane + 32];
-                    sm.qrec[lane] = sm.qrec[lane + 32];
-                }
-                __syncwarp();
-                qn -= 32;
             }
         }
+        const unsigned ma = __ballot_sync(0xffffffffu, accept);
+        if (accept) {
+            const int slot = qn + __popc(ma & lanemask_lt());
+            sm.qst[slot] = (uint32_t)s | ((uint32_t)t << 16);
+            sm.qrec[slot] = d;  // a round is one record: its s (and t) are distinct
+        }
+        qn += __popc(ma);
+        __syncwarp();
+        if (qn >= 32) {
+            a3_chunk<kExactImage>(sm, 32, lane, im, row, xs, ys, zs, acc);
+            __syncwarp();
+            if (lane < qn - 32) {
+                sm.qst[lane] = sm.qst[lane + 32];
+                sm.qrec[lane] = sm.qrec[lane + 32];
+            }
+            __syncwarp();
+            qn -= 32;
+        }
     }
-    if (qn > 0) a3_chunk<kExactImage>(sm, qn, lane, im, xs, ys, zs, acc);
+    if (qn > 0) a3_chunk<kExactImage>(sm, qn, lane, im, row, xs, ys, zs, acc);
     __syncwarp();
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
     for (int sl = lane; sl < m; sl += 32) {
-        const int k = kExactImage ? -1 : sm.kidx[sl];
-        int kk = k;
-        if (kExactImage) {
-            // exact mode keeps ranks in kidx: recover the row index
-            const int q = sm.kidx[sl];
-            int lo = 0, hi = rc_n - 1;
-            while (lo <= hi) {
-                const int mid = (lo + hi) >> 1;
-                const int v = row[mid];
-                if (v == q) {
-                    kk = mid;
-                    break;
-                }
-                if (v < q) lo = mid + 1;
-                else hi = mid - 1;
-            }
-        }
-        grow[3 * kk] = sm.ax[sl];
-        grow[3 * kk + 1] = sm.ay[sl];
-        grow[3 * kk + 2] = sm.az[sl];
+        const int k = sm.kidx[sl];
+        grow[3 * k] = sm.ax[sl];
+        grow[3 * k + 1] = sm.ay[sl];
+        grow[3 * k + 2] = sm.az[sl];
     }
     const double fx = group_sum<32>(acc.fx);
     const double fy = group_sum<32>(acc.fy);
@@ -426,7 +433,8 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const 
         a3_grant(k_atm3<true>, smem, g_a3_granted[0]);
         k_atm3<true><<<blocks, warps * 32, smem, st>>>(*g, n, xs, ys, zs, rows, row_count,
                                                         capacity, slot_capacity, rc2, rc2, rc2,
-                                                        own, gbuf,
+                                                        (float)(rc2 * (1.0 - kA3Band)),
+                                                        (float)(rc2 * (1.0 + kA3Band)), own, gbuf,
                                                         energy_rank, virial_rank, triplets_rank,
                                                         status, tag);
         note_launches(1);
@@ -434,9 +442,9 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const 
         a3_grant(k_atm3<false>, smem, g_a3_granted[1]);
         k_atm3<false><<<blocks, warps * 32, smem, st>>>(
             *g, n, xs, ys, zs, rows, row_count, capacity, slot_capacity, rc2,
-            rc2 * (1.0 - kA3Margin),
-            rc2 * (1.0 + kA3Margin), own, gbuf, energy_rank, virial_rank, triplets_rank, status,
-            tag);
+            rc2 * (1.0 - kA3Margin), rc2 * (1.0 + kA3Margin), (float)(rc2 * (1.0 - kA3Band)),
+            (float)(rc2 * (1.0 + kA3Band)), own, gbuf, energy_rank, virial_rank, triplets_rank,
+            status, tag);
         note_launches(1);
     }
     const int tb = 256;

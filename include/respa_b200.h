@@ -90,11 +90,18 @@ RB_API int rb_device_count(void);
  * Counting sort of particles by flat cell id (cx*ny+cy)*nz+cz with the
  * truncating index of :182-197, stable in ascending particle index.
  * Outputs: cell_start[ncell+1], cell_particles[n] (rank -> particle),
- * cell_of_rank[n], and positions gathered into rank order (xs, ys, zs). */
+ * cell_of_rank[n], and positions gathered into rank order, pos_r (n,3) --
+ * the layout every force pass reads (one 24-byte gather per neighbour). */
 RB_API size_t rb_bin_scratch_bytes(int64_t n, int64_t ncell);
+/* rank_of[n] (particle -> rank) and x_ref (n,3) (positions at this build)
+ * are optional (NULL).  rebuild_flag gates the launch for captured
+ * r-RESPA steps: the kernels run only when *rebuild_flag equals the step
+ * tag (see rb_respa_drift); NULL = always. */
 RB_API int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_start,
-           int32_t *cell_particles, int32_t *cell_of_rank, double *xs, double *ys, double *zs,
-           void *scratch, size_t scratch_bytes, void *stream);
+                  int32_t *cell_particles, int32_t *cell_of_rank, double *pos_r,
+                  int32_t *rank_of, double *x_ref, const int64_t *rebuild_flag,
+                  const unsigned long long *status, int64_t tag, void *scratch,
+                  size_t scratch_bytes, void *stream);
 
 /* ---- neighbour rows: the survivor lists of containers.py:437-474 -------
  * Row r (rank order) lists, in stencil order, the ranks within r_list of
@@ -103,16 +110,16 @@ RB_API int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_
  * device int *max_count (caller initialises it to 0).  A row longer than
  * `capacity` is truncated, so callers must check *max_count <= capacity
  * before trusting a pass. */
-RB_API int rb_nlist(const rb_grid *g, int64_t n, const double *xs, const double *ys, const double *zs,
-             const int32_t *cell_start, const int32_t *cell_of_rank, double r_list,
-             int32_t capacity, int32_t *rows, int32_t *row_count, int32_t *max_count,
-             void *stream);
+RB_API int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_start,
+                    const int32_t *cell_of_rank, double r_list, int32_t capacity, int32_t *rows,
+                    int32_t *row_count, int32_t *max_count, const int64_t *rebuild_flag,
+                    const unsigned long long *status, int64_t tag, void *stream);
 
 /* ---- LJ pair pass: replaces _c01_pair_kernel (containers.py:282-370) ---
  * Owner-computes over the neighbour rows with the inclusive cutoff `rc`;
  * writes forces (n,3) in particle order (overwritten), and per-rank energy
  * (sum of phi/2) and virial (sum of scale*r^2/2). */
-RB_API int rb_lj_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys, const double *zs,
+RB_API int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r,
                const int32_t *cell_particles, const int32_t *rows, const int32_t *row_count,
                int32_t capacity, double rc, double epsilon, double sigma, double *forces,
                double *energy_rank, double *virial_rank, unsigned long long *status, int64_t tag,
@@ -122,7 +129,8 @@ RB_API int rb_lj_pass(const rb_grid *g, int64_t n, const double *xs, const doubl
  * position of p in the row of q = rows[p*capacity + k] when q < p, else -1.
  * Needed by the Newton-3 triplet pass to return partial forces to q's row. */
 RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_count,
-                           int32_t capacity, int32_t *mirror, void *stream);
+                           int32_t capacity, int32_t *mirror, const int64_t *rebuild_flag,
+                           const unsigned long long *status, int64_t tag, void *stream);
 
 /* ---- ATM triplet pass: replaces _c01_triplet_kernel (:373-535) --------
  * Newton-3 form: every unique triplet (all three pair distances <= rc,
@@ -135,8 +143,7 @@ RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_co
  * particle with more higher-rank neighbours than that records
  * RB_KIND_CAPACITY in the status word (pass the longest row length). */
 RB_API size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity);
-RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
-                       const double *zs, const int32_t *cell_particles, const int32_t *rows,
+RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                        const int32_t *row_count, const int32_t *mirror, int32_t capacity,
                        int32_t slot_capacity, double rc, double nu, double *forces, double *energy_rank,
                        double *virial_rank, int32_t *triplets_rank, void *scratch,
@@ -146,8 +153,7 @@ RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const doub
 /* C01 (owner-computes) form of the same pass, as the reference traverses it:
  * every triplet visited once from each member, force stored on the base
  * particle only, energy phi/3 per visit; visits_rank = accepted visits. */
-RB_API int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *xs, const double *ys,
-                           const double *zs, const int32_t *cell_particles, const int32_t *rows,
+RB_API int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                            const int32_t *row_count, int32_t capacity, double rc, double nu,
                            double *forces, double *energy_rank, double *virial_rank,
                            int32_t *visits_rank, unsigned long long *status, int64_t tag,
@@ -156,8 +162,7 @@ RB_API int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *xs, const 
 /* Instrumentation (collect_triplet_visits, containers.py:825-849): writes
  * one sorted (i, j, k) particle-index row per accepted visit, int32 (V,3),
  * at row_offset[r] (exclusive prefix of rb_atm_pass_c01's visits_rank). */
-RB_API int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *xs, const double *ys,
-                             const double *zs, const int32_t *cell_particles, const int32_t *rows,
+RB_API int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                              const int32_t *row_count, int32_t capacity, double rc,
                              const int64_t *row_offset, int32_t *visit_rows, void *stream);
 
@@ -174,14 +179,19 @@ RB_API int rb_reduce_sum_i32(int64_t n, const int32_t *in, int64_t *out, void *s
  * (integrators.py:148-170), bit-exact with numpy's rounding order.
  * drift: [v += half_respa*f3 if kick3]; x += dt*v + half_drift*f2_old;
  *        wrap into [0, box) with numpy mod semantics (model.py:274-280);
- *        non-finite x records RB_KIND_NONFINITE at `tag`.
+ *        non-finite x records RB_KIND_NONFINITE at `tag`.  Optionally
+ *        (non-NULL) scatters x into pos_r via rank_of, and sets
+ *        *rebuild_flag = tag when a particle moved more than skin/2 from
+ *        x_ref (the neighbour rows, built at rc + skin, must be rebuilt).
  * kick:  v += half_dt*(f2_old + f2_new); f2_old = f2_new (:159);
  *        [v += half_respa*f3 if kick3];
  *        non-finite v records RB_KIND_NONFINITE at `tag`. */
-RB_API int rb_respa_drift(int64_t n, double *pos, double *vel, const double *f2_old, const double *f3,
-                   const double *box3_host, int32_t periodic, double dt, double half_drift,
-                   double half_respa, int32_t kick3, unsigned long long *status, int64_t tag,
-                   void *stream);
+RB_API int rb_respa_drift(int64_t n, double *pos, double *vel, const double *f2_old,
+                          const double *f3, const double *box3_host, int32_t periodic, double dt,
+                          double half_drift, double half_respa, int32_t kick3,
+                          const int32_t *rank_of, double *pos_r, const double *x_ref,
+                          double skin, int64_t *rebuild_flag, unsigned long long *status,
+                          int64_t tag, void *stream);
 RB_API int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f2_new,
                   const double *f3, double half_dt, double half_respa, int32_t kick3,
                   unsigned long long *status, int64_t tag, void *stream);

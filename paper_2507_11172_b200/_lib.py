@@ -59,23 +59,23 @@ SIGNATURES = {
     "rb_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rb_device_count": (ctypes.c_int, []),
     "rb_bin_scratch_bytes": (_SZ, [_I64, _I64]),
-    "rb_bin": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
-    "rb_nlist": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _D, _I32, _P, _P, _P, _P]),
-    "rb_lj_pass": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _P, _I32, _D, _D, _D,
-                                  _P, _P, _P, _P, _I64, _P]),
-    "rb_nlist_mirror": (ctypes.c_int, [_I64, _P, _P, _I32, _P, _P]),
+    "rb_bin": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _SZ, _P]),
+    "rb_nlist": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _D, _I32, _P, _P, _P, _P, _P, _I64, _P]),
+    "rb_nlist_mirror": (ctypes.c_int, [_I64, _P, _P, _I32, _P, _P, _P, _I64, _P]),
+    "rb_lj_pass": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _D, _D, _P, _P, _P, _P, _I64,
+                                  _P]),
     "rb_atm_scratch_bytes": (_SZ, [_I64, _I32]),
-    "rb_atm_pass": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _D, _D,
-                                   _P, _P, _P, _P, _P, _SZ, _P, _I64, _P]),
-    "rb_atm_pass_c01": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _P, _I32, _D, _D,
-                                       _P, _P, _P, _P, _P, _I64, _P]),
-    "rb_atm_visit_rows": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _P, _I32, _D,
-                                         _P, _P, _P]),
+    "rb_atm_pass": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _I32, _I32, _D, _D, _P, _P, _P, _P,
+                                   _P, _SZ, _P, _I64, _P]),
+    "rb_atm_pass_c01": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _D, _P, _P, _P, _P, _P,
+                                       _I64, _P]),
+    "rb_atm_visit_rows": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _P, _P, _P]),
     "rb_reduce_scratch_bytes": (_SZ, [_I64]),
     "rb_reduce_sum_f64": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
     "rb_reduce_sumsq_f64": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
     "rb_reduce_sum_i32": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
-    "rb_respa_drift": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _I32, _D, _D, _D, _I32, _P, _I64, _P]),
+    "rb_respa_drift": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _I32, _D, _D, _D, _I32, _P, _P, _P, _D,
+                                      _P, _P, _I64, _P]),
     "rb_respa_kick": (ctypes.c_int, [_I64, _P, _P, _P, _P, _D, _D, _I32, _P, _I64, _P]),
     "rb_step_begin": (ctypes.c_int, [_P, _P]),
     "rb_trace_record": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),

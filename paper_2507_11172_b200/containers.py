@@ -89,8 +89,9 @@ def _finish(eng, geom, forces_dev, e_slot, w_slot, base_cells):
     owned = np.zeros(eng.n, dtype=bool)
     owned[parts[keep]] = True
     forces[~owned] = 0.0
-    e = eng.e_rank[: eng.n].cpu().numpy()
-    w = eng.w_rank[: eng.n].cpu().numpy()
+    pair = e_slot == SCALAR_E2
+    e = (eng.e2_rank if pair else eng.e3_rank)[: eng.n].cpu().numpy()
+    w = (eng.w2_rank if pair else eng.w3_rank)[: eng.n].cpu().numpy()
     return forces, float(np.sum(e[keep])), float(np.sum(w[keep]))
 
 

@@ -121,8 +121,7 @@ __device__ __forceinline__ void atm_visit(double a, double b, double c, double d
 // particle indices at row_offset[r] + (visit ordinal), in enumeration order.
 template <bool kExactImage, bool kRows>
 __global__ void __launch_bounds__(kAtmWarps * 32)
-    k_atm(rb_grid g, int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
-          const double *__restrict__ zs, const int32_t *__restrict__ parts,
+    k_atm(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ parts,
           const int32_t *__restrict__ rows, const int32_t *__restrict__ row_count,
           int32_t capacity, double rc2, double rc2_lo, double rc2_hi, double nu,
           double *__restrict__ forces, double *__restrict__ energy_rank,
@@ -138,7 +137,7 @@ __global__ void __launch_bounds__(kAtmWarps * 32)
     if (!kRows && warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
     AtmWarpSmem sm = atm_carve(smem_raw + (size_t)warp * atm_warp_bytes(capacity), capacity);
     const Image im = make_image(g);
-    const double xi = xs[r], yi = ys[r], zi = zs[r];
+    const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
 
     // 1. survivors
     const int m = row_count[r];
@@ -151,7 +150,7 @@ __global__ void __launch_bounds__(kAtmWarps * 32)
         double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;
         if (k < m) {
             j = row[k];
-            exact_disp(im, xi, yi, zi, xs[j], ys[j], zs[j], dx, dy, dz);
+            exact_disp(im, xi, yi, zi, pr[3 * (j)], pr[3 * (j) + 1], pr[3 * (j) + 2], dx, dy, dz);
             r2 = exact_r2(dx, dy, dz);
             keep = r2 <= rc2;
         }
@@ -196,7 +195,7 @@ __global__ void __launch_bounds__(kAtmWarps * 32)
             if (exact) {
                 const int j = sm.idx[s], k = sm.idx[t];
                 double dx, dy, dz;
-                exact_disp(im, xs[j], ys[j], zs[j], xs[k], ys[k], zs[k], dx, dy, dz);
+                exact_disp(im, pr[3 * (j)], pr[3 * (j) + 1], pr[3 * (j) + 2], pr[3 * (k)], pr[3 * (k) + 1], pr[3 * (k) + 2], dx, dy, dz);
                 const double c2 = exact_r2(dx, dy, dz);
                 accept = c2 <= rc2;
                 cval = c2;
@@ -293,8 +292,7 @@ static size_t atm_launch_shape(int capacity, int &warps) {
 
 using namespace rb;
 
-extern "C" int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *xs, const double *ys,
-                           const double *zs, const int32_t *cell_particles, const int32_t *rows,
+extern "C" int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                            const int32_t *row_count, int32_t capacity, double rc, double nu,
                            double *forces, double *energy_rank, double *virial_rank,
                            int32_t *visits_rank, unsigned long long *status, int64_t tag,
@@ -314,13 +312,13 @@ extern "C" int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *xs, co
     if (exact_image) {
         grant_smem(k_atm<true, false>, smem, g_granted[0]);
         k_atm<true, false><<<blocks, warps * 32, smem, st>>>(
-            *g, n, xs, ys, zs, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, nu,
+            *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, nu,
             forces, energy_rank, virial_rank, visits_rank, status, tag, nullptr, nullptr);
         note_launches(1);
     } else {
         grant_smem(k_atm<false, false>, smem, g_granted[1]);
         k_atm<false, false><<<blocks, warps * 32, smem, st>>>(
-            *g, n, xs, ys, zs, cell_particles, rows, row_count, capacity, rc2,
+            *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2,
             rc2 * (1.0 - kAtmMargin), rc2 * (1.0 + kAtmMargin), nu, forces, energy_rank,
             virial_rank, visits_rank, status, tag, nullptr, nullptr);
         note_launches(1);
@@ -331,8 +329,7 @@ extern "C" int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *xs, co
 // Instrumentation: sorted (i, j, k) rows of every accepted visit
 // (collect_triplet_visits, containers.py:825-849).  row_offset[r] is the
 // exclusive prefix of the visit counts rb_atm_pass reported per rank.
-extern "C" int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *xs, const double *ys,
-                                 const double *zs, const int32_t *cell_particles,
+extern "C" int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles,
                                  const int32_t *rows, const int32_t *row_count, int32_t capacity,
                                  double rc, const int64_t *row_offset, int32_t *visit_rows,
                                  void *stream) {
@@ -347,7 +344,7 @@ extern "C" int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *xs, 
     // the instrumentation always takes the exact raw-position predicate
     grant_smem(k_atm<true, true>, smem, g_granted[2]);
     k_atm<true, true><<<blocks, warps * 32, smem, as_stream(stream)>>>(
-        *g, n, xs, ys, zs, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, 0.0, nullptr,
+        *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, 0.0, nullptr,
         nullptr, nullptr, nullptr, nullptr, 0, row_offset, visit_rows);
     note_launches(1);
     return launch_status();

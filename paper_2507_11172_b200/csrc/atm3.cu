@@ -33,6 +33,10 @@
 namespace rb {
 
 constexpr int kA3Warps = 4;
+#ifndef RB_A3_MIN_BLOCKS
+#define RB_A3_MIN_BLOCKS 7
+#endif
+constexpr int kA3MinBlocks = RB_A3_MIN_BLOCKS;  // register cap for occupancy
 constexpr int kA3Queue = 64;
 constexpr double kA3Margin = 1e-10;  // fp64 estimate vs the reference arithmetic
 constexpr double kA3Band = 1e-5;     // fp32 filter vs the fp64 estimate
@@ -78,9 +82,7 @@ struct A3Acc {
 template <bool kExactImage>
 __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im,
                                         const int32_t *__restrict__ row,
-                                        const double *__restrict__ xs,
-                                        const double *__restrict__ ys,
-                                        const double *__restrict__ zs, A3Acc &acc, double fj[3],
+                                        const double *__restrict__ pr, A3Acc &acc, double fj[3],
                                         double fk[3], int &s, int &t) {
     const uint32_t st = sm.qst[q];
     s = (int)(st & 0xffffu);
@@ -93,7 +95,7 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
     if (kExactImage) {
         // the reference's raw-position minimum image (containers.py:497-513)
         const int j = row[sm.kidx[s]], k = row[sm.kidx[t]];
-        exact_disp(im, xs[j], ys[j], zs[j], xs[k], ys[k], zs[k], djkx, djky, djkz);
+        exact_disp(im, pr[3 * (j)], pr[3 * (j) + 1], pr[3 * (j) + 2], pr[3 * (k)], pr[3 * (k) + 1], pr[3 * (k) + 2], djkx, djky, djkz);
         c = exact_r2(djkx, djky, djkz);
     } else {
         djkx = dikx - dijx;
@@ -142,14 +144,12 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
 template <bool kExactImage>
 __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, const Image &im,
                                          const int32_t *__restrict__ row,
-                                         const double *__restrict__ xs,
-                                         const double *__restrict__ ys,
-                                         const double *__restrict__ zs, A3Acc &acc) {
+                                         const double *__restrict__ pr, A3Acc &acc) {
     double fj[3] = {0.0, 0.0, 0.0}, fk[3] = {0.0, 0.0, 0.0};
     int s = 0, t = 0, rec = -1;
     bool pending = false;
     if (lane < cnt) {
-        pending = a3_eval<kExactImage>(sm, lane, im, row, xs, ys, zs, acc, fj, fk, s, t);
+        pending = a3_eval<kExactImage>(sm, lane, im, row, pr, acc, fj, fk, s, t);
         rec = sm.qrec[lane];
     }
     unsigned todo = __ballot_sync(0xffffffffu, pending);
@@ -175,9 +175,8 @@ __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, co
 }
 
 template <bool kExactImage>
-__global__ void __launch_bounds__(kA3Warps * 32)
-    k_atm3(rb_grid g, int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
-           const double *__restrict__ zs, const int32_t *__restrict__ rows,
+__global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
+    k_atm3(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
            const int32_t *__restrict__ row_count, int32_t capacity, int32_t slots, double rc2,
            double rc2_lo, double rc2_hi, float rc2f_lo, float rc2f_hi, double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
@@ -191,7 +190,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
     if (warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
     const A3Smem sm = a3_carve(smem_raw + (size_t)warp * a3_warp_bytes(slots), slots);
     const Image im = make_image(g);
-    const double xi = xs[r], yi = ys[r], zi = zs[r];
+    const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
     const int rc_n = row_count[r];
     const int32_t *row = rows + r * (int64_t)capacity;
     double *grow = gbuf + r * (int64_t)capacity * 3;
@@ -206,7 +205,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
         if (k < rc_n) {
             q = row[k];
             if (q > r) {
-                exact_disp(im, xi, yi, zi, xs[q], ys[q], zs[q], dx, dy, dz);
+                exact_disp(im, xi, yi, zi, pr[3 * (q)], pr[3 * (q) + 1], pr[3 * (q) + 2], dx, dy, dz);
                 r2 = exact_r2(dx, dy, dz);
                 keep = r2 <= rc2;
                 if (!keep) {  // beyond the three-body cutoff: contributes nothing
@@ -274,7 +273,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
                 (void)c2f;
                 const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
                 double dx, dy, dz;
-                exact_disp(im, xs[jr], ys[jr], zs[jr], xs[kr], ys[kr], zs[kr], dx, dy, dz);
+                exact_disp(im, pr[3 * (jr)], pr[3 * (jr) + 1], pr[3 * (jr) + 2], pr[3 * (kr)], pr[3 * (kr) + 1], pr[3 * (kr) + 2], dx, dy, dz);
                 accept = exact_r2(dx, dy, dz) <= rc2;
             } else if (c2f <= rc2f_lo) {
                 accept = true;
@@ -288,7 +287,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
                 } else if (c2 <= rc2_hi) {
                     const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
                     double dx, dy, dz;
-                    exact_disp(im, xs[jr], ys[jr], zs[jr], xs[kr], ys[kr], zs[kr], dx, dy, dz);
+                    exact_disp(im, pr[3 * (jr)], pr[3 * (jr) + 1], pr[3 * (jr) + 2], pr[3 * (kr)], pr[3 * (kr) + 1], pr[3 * (kr) + 2], dx, dy, dz);
                     accept = exact_r2(dx, dy, dz) <= rc2;
                 }
             }
@@ -302,7 +301,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
         qn += __popc(ma);
         __syncwarp();
         if (qn >= 32) {
-            a3_chunk<kExactImage>(sm, 32, lane, im, row, xs, ys, zs, acc);
+            a3_chunk<kExactImage>(sm, 32, lane, im, row, pr, acc);
             __syncwarp();
             if (lane < qn - 32) {
                 sm.qst[lane] = sm.qst[lane + 32];
@@ -312,7 +311,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
             qn -= 32;
         }
     }
-    if (qn > 0) a3_chunk<kExactImage>(sm, qn, lane, im, row, xs, ys, zs, acc);
+    if (qn > 0) a3_chunk<kExactImage>(sm, qn, lane, im, row, pr, acc);
     __syncwarp();
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
@@ -404,8 +403,7 @@ extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
     return (size_t)(n > 0 ? n : 1) * 3 * sizeof(double) * (size_t)(1 + capacity);
 }
 
-extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
-                           const double *zs, const int32_t *cell_particles, const int32_t *rows,
+extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                            const int32_t *row_count, const int32_t *mirror, int32_t capacity,
                            int32_t slot_capacity, double rc, double nu, double *forces, double *energy_rank,
                            double *virial_rank, int32_t *triplets_rank, void *scratch,
@@ -431,7 +429,7 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const 
     double *gbuf = own + 3 * n;
     if (exact_image) {
         a3_grant(k_atm3<true>, smem, g_a3_granted[0]);
-        k_atm3<true><<<blocks, warps * 32, smem, st>>>(*g, n, xs, ys, zs, rows, row_count,
+        k_atm3<true><<<blocks, warps * 32, smem, st>>>(*g, n, pos_r, rows, row_count,
                                                         capacity, slot_capacity, rc2, rc2, rc2,
                                                         (float)(rc2 * (1.0 - kA3Band)),
                                                         (float)(rc2 * (1.0 + kA3Band)), own, gbuf,
@@ -441,7 +439,7 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *xs, const 
     } else {
         a3_grant(k_atm3<false>, smem, g_a3_granted[1]);
         k_atm3<false><<<blocks, warps * 32, smem, st>>>(
-            *g, n, xs, ys, zs, rows, row_count, capacity, slot_capacity, rc2,
+            *g, n, pos_r, rows, row_count, capacity, slot_capacity, rc2,
             rc2 * (1.0 - kA3Margin), rc2 * (1.0 + kA3Margin), (float)(rc2 * (1.0 - kA3Band)),
             (float)(rc2 * (1.0 + kA3Band)), own, gbuf, energy_rank, virial_rank, triplets_rank,
             status, tag);

@@ -12,6 +12,8 @@
 //   k_cell_finish  per-cell insertion sort by particle index (restores the
 //                  reference's stable order) + gather of positions into rank
 //                  order (SoA) and the rank -> cell map
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rb {
@@ -25,10 +27,28 @@ __device__ __forceinline__ int cell_index_1d(double x, double origin, double inv
     return (int)c;
 }
 
+// Rebuild gate: a binning launched inside a captured r-RESPA step runs only
+// when the drift of that step flagged a rebuild (*flag == tag); flag == NULL
+// means always (standalone passes).
+__device__ __forceinline__ bool gate_closed(const int64_t *flag, const unsigned long long *status,
+                                            int64_t tag) {
+    if (!flag) return false;
+    return *(volatile const int64_t *)flag != resolve_tag(tag, status);
+}
+
+__global__ void k_bin_zero(int64_t ncell, int32_t *__restrict__ count, const int64_t *flag,
+                           const unsigned long long *status, int64_t tag) {
+    if (gate_closed(flag, status, tag)) return;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell;
+         c += (int64_t)gridDim.x * blockDim.x)
+        count[c] = 0;
+}
+
 __global__ void k_bin_count(rb_grid g, int64_t n, const double *__restrict__ pos,
-                            int32_t *__restrict__ cell_of, int32_t *__restrict__ count) {
+                            int32_t *__restrict__ cell_of, int32_t *__restrict__ count,
+                            const int64_t *flag, const unsigned long long *status, int64_t tag) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || gate_closed(flag, status, tag)) return;
     double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
     int cx = cell_index_1d(x, g.origin[0], g.inv_cell[0], g.cells[0]);
     int cy = cell_index_1d(y, g.origin[1], g.inv_cell[1], g.cells[1]);
@@ -39,36 +59,62 @@ __global__ void k_bin_count(rb_grid g, int64_t n, const double *__restrict__ pos
 }
 
 __global__ void k_bin_scatter(int64_t n, const int32_t *__restrict__ cell_of,
-                              int32_t *__restrict__ cursor, int32_t *__restrict__ parts) {
+                              int32_t *__restrict__ cursor, int32_t *__restrict__ parts,
+                              const int64_t *flag, const unsigned long long *status, int64_t tag) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || gate_closed(flag, status, tag)) return;
     int slot = atomicAdd(&cursor[cell_of[i]], 1);
     parts[slot] = (int32_t)i;
 }
 
-__global__ void k_cell_finish(int64_t ncell, const int32_t *__restrict__ start,
-                              int32_t *__restrict__ parts, int32_t *__restrict__ cell_of_rank,
-                              const double *__restrict__ pos, double *__restrict__ xs,
-                              double *__restrict__ ys, double *__restrict__ zs) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncell) return;
-    int b = start[c], e = start[c + 1];
-    // insertion sort of the (short) cell segment by particle index
-    for (int a = b + 1; a < e; a++) {
-        int v = parts[a];
-        int k = a - 1;
-        while (k >= b && parts[k] > v) {
-            parts[k + 1] = parts[k];
-            k--;
+// One warp per cell: restore ascending particle order inside the cell (the
+// atomic scatter is unordered), then gather the rank-ordered positions and
+// the rank <-> particle maps.  Cells of up to 32 particles sort in registers
+// (rank = number of smaller indices); larger cells fall back to a serial
+// insertion sort by lane 0.
+constexpr int kFinishWarps = 8;
+
+__global__ void __launch_bounds__(kFinishWarps * 32)
+    k_cell_finish(int64_t ncell, const int32_t *__restrict__ start, int32_t *__restrict__ parts,
+                  int32_t *__restrict__ cell_of_rank, int32_t *__restrict__ rank_of,
+                  const double *__restrict__ pos, double *__restrict__ pr,
+                  double *__restrict__ x_ref, const int64_t *flag,
+                  const unsigned long long *status, int64_t tag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5);
+    if (c >= ncell || gate_closed(flag, status, tag)) return;
+    const int b = start[c], e = start[c + 1], k = e - b;
+    if (k <= 32) {
+        const int v = lane < k ? parts[b + lane] : 0x7fffffff;
+        int rank = 0;
+        for (int l = 0; l < k; l++) rank += __shfl_sync(0xffffffffu, v, l) < v ? 1 : 0;
+        __syncwarp();
+        if (lane < k) parts[b + rank] = v;
+    } else if (lane == 0) {
+        for (int a = b + 1; a < e; a++) {
+            const int v = parts[a];
+            int q = a - 1;
+            while (q >= b && parts[q] > v) {
+                parts[q + 1] = parts[q];
+                q--;
+            }
+            parts[q + 1] = v;
         }
-        parts[k + 1] = v;
     }
-    for (int r = b; r < e; r++) {
-        int p = parts[r];
+    __syncwarp();
+    for (int r = b + lane; r < e; r += 32) {
+        const int64_t p = parts[r];
+        const double x = pos[3 * p], y = pos[3 * p + 1], z = pos[3 * p + 2];
         cell_of_rank[r] = (int32_t)c;
-        xs[r] = pos[3 * (int64_t)p];
-        ys[r] = pos[3 * (int64_t)p + 1];
-        zs[r] = pos[3 * (int64_t)p + 2];
+        pr[3 * (int64_t)r] = x;
+        pr[3 * (int64_t)r + 1] = y;
+        pr[3 * (int64_t)r + 2] = z;
+        if (rank_of) rank_of[p] = r;
+        if (x_ref) {
+            x_ref[3 * p] = x;
+            x_ref[3 * p + 1] = y;
+            x_ref[3 * p + 2] = z;
+        }
     }
 }
 
@@ -108,8 +154,10 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *warp_sums, int &
 }
 
 __global__ void k_scan_tile_sums(int64_t n, const int32_t *__restrict__ in,
-                                 int32_t *__restrict__ tile_sums) {
+                                 int32_t *__restrict__ tile_sums, const int64_t *flag,
+                                 const unsigned long long *status, int64_t tag) {
     __shared__ int warp_sums[32];
+    if (gate_closed(flag, status, tag)) return;
     int64_t base = (int64_t)blockIdx.x * kScanTile;
     int s = 0;
 #pragma unroll
@@ -122,8 +170,11 @@ __global__ void k_scan_tile_sums(int64_t n, const int32_t *__restrict__ in,
     if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
 }
 
-__global__ void k_scan_tile_offsets(int64_t ntiles, int32_t *__restrict__ tile_sums) {
+__global__ void k_scan_tile_offsets(int64_t ntiles, int32_t *__restrict__ tile_sums,
+                                    const int64_t *flag, const unsigned long long *status,
+                                    int64_t tag) {
     __shared__ int warp_sums[32];
+    if (gate_closed(flag, status, tag)) return;
     int carry = 0;
     for (int64_t base = 0; base < ntiles; base += blockDim.x) {
         int64_t i = base + threadIdx.x;
@@ -136,8 +187,11 @@ __global__ void k_scan_tile_offsets(int64_t ntiles, int32_t *__restrict__ tile_s
 }
 
 __global__ void k_scan_apply(int64_t n, const int32_t *__restrict__ in,
-                             const int32_t *__restrict__ tile_off, int32_t *__restrict__ out) {
+                             const int32_t *__restrict__ tile_off, int32_t *__restrict__ out,
+                             int32_t *__restrict__ cursor, const int64_t *flag,
+                             const unsigned long long *status, int64_t tag) {
     __shared__ int warp_sums[32];
+    if (gate_closed(flag, status, tag)) return;
     int64_t base = (int64_t)blockIdx.x * kScanTile;
     int vals[kScanItems];
     int s = 0;
@@ -152,7 +206,10 @@ __global__ void k_scan_apply(int64_t n, const int32_t *__restrict__ in,
 #pragma unroll
     for (int k = 0; k < kScanItems; k++) {
         int64_t i = base + (int64_t)threadIdx.x * kScanItems + k;
-        if (i < n) out[i] = ex;
+        if (i < n) {
+            out[i] = ex;
+            cursor[i] = ex;
+        }
         ex += vals[k];
         if (i == n - 1) out[n] = ex;
     }
@@ -175,8 +232,10 @@ extern "C" size_t rb_bin_scratch_bytes(int64_t n, int64_t ncell) {
 }
 
 extern "C" int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_start,
-                      int32_t *cell_particles, int32_t *cell_of_rank, double *xs, double *ys,
-                      double *zs, void *scratch, size_t scratch_bytes, void *stream) {
+                      int32_t *cell_particles, int32_t *cell_of_rank, double *pos_r,
+                      int32_t *rank_of, double *x_ref, const int64_t *rebuild_flag,
+                      const unsigned long long *status, int64_t tag, void *scratch,
+                      size_t scratch_bytes, void *stream) {
     if (!g || n < 0) return RB_ERR_ARGUMENT;
     int64_t ncell = (int64_t)g->cells[0] * g->cells[1] * g->cells[2];
     if (ncell <= 0) return RB_ERR_GEOMETRY;
@@ -191,25 +250,31 @@ extern "C" int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *c
     p += align256(sizeof(int32_t) * (size_t)ncell);
     int32_t *tiles = (int32_t *)p;
     int64_t ntiles = ceil_div(ncell, kScanTile);
-
-    cudaMemsetAsync(count, 0, sizeof(int32_t) * (size_t)ncell, st);
+    const int64_t *fl = rebuild_flag;
     const int tb = 256;
-    if (n > 0) k_bin_count<<<(unsigned)ceil_div(n, tb), tb, 0, st>>>(*g, n, pos, cell_of, count);
-    if (n > 0) note_launches(1);
-    k_scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(ncell, count, tiles);
-    note_launches(1);
-    k_scan_tile_offsets<<<1, 1024, 0, st>>>(ntiles, tiles);
-    note_launches(1);
-    k_scan_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(ncell, count, tiles, cell_start);
+    k_bin_zero<<<(unsigned)std::min<int64_t>(ceil_div(ncell, tb), 148 * 8), tb, 0, st>>>(
+        ncell, count, fl, status, tag);
     note_launches(1);
     if (n > 0) {
-        cudaMemcpyAsync(cursor, cell_start, sizeof(int32_t) * (size_t)ncell,
-                        cudaMemcpyDeviceToDevice, st);
-        k_bin_scatter<<<(unsigned)ceil_div(n, tb), tb, 0, st>>>(n, cell_of, cursor,
-                                                                 cell_particles);
+        k_bin_count<<<(unsigned)ceil_div(n, tb), tb, 0, st>>>(*g, n, pos, cell_of, count, fl,
+                                                               status, tag);
         note_launches(1);
-        k_cell_finish<<<(unsigned)ceil_div(ncell, tb), tb, 0, st>>>(
-            ncell, cell_start, cell_particles, cell_of_rank, pos, xs, ys, zs);
+    }
+    k_scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(ncell, count, tiles, fl, status,
+                                                                 tag);
+    note_launches(1);
+    k_scan_tile_offsets<<<1, 1024, 0, st>>>(ntiles, tiles, fl, status, tag);
+    note_launches(1);
+    k_scan_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(ncell, count, tiles, cell_start,
+                                                             cursor, fl, status, tag);
+    note_launches(1);
+    if (n > 0) {
+        k_bin_scatter<<<(unsigned)ceil_div(n, tb), tb, 0, st>>>(n, cell_of, cursor,
+                                                                 cell_particles, fl, status, tag);
+        note_launches(1);
+        k_cell_finish<<<(unsigned)ceil_div(ncell, kFinishWarps), kFinishWarps * 32, 0, st>>>(
+            ncell, cell_start, cell_particles, cell_of_rank, rank_of, pos, pos_r, x_ref, fl,
+            status, tag);
         note_launches(1);
     }
     return launch_status();

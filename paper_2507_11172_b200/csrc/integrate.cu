@@ -34,26 +34,57 @@ __device__ __forceinline__ double wrap_coord(double x, double box) {
     return r;
 }
 
-__global__ void k_drift(int64_t n3, double *__restrict__ pos, double *__restrict__ vel,
-                        const double *__restrict__ f2_old, const double *__restrict__ f3, double bx,
-                        double by, double bz, int periodic, double dt, double half_drift,
-                        double half_respa, int kick3, unsigned long long *status, int64_t tag) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n3) return;
+// One thread per particle (AoS, 24 contiguous bytes per array).  Besides the
+// drift it (a) scatters the new position into the rank-ordered copy the force
+// kernels read, and (b) compares against the positions of the last
+// neighbour-row build: a particle that moved more than skin/2 flags a rebuild
+// of the rows in this very step (*rebuild_flag = tag), so every pair within
+// rc is always inside the rows built at rc + skin.
+__global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict__ vel,
+                        const double *__restrict__ f2_old, const double *__restrict__ f3,
+                        double bx, double by, double bz, int periodic, double dt,
+                        double half_drift, double half_respa, int kick3,
+                        const int32_t *__restrict__ rank_of, double *__restrict__ pr,
+                        const double *__restrict__ x_ref, double skin_half2,
+                        int64_t *rebuild_flag, unsigned long long *status, int64_t tag) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
     tag = resolve_tag(tag, status);
     if (frozen(status, tag, 0)) return;
-    double v = vel[i];
-    if (kick3) {
-        v = xadd(v, xmul(half_respa, f3[i]));
-        vel[i] = v;
+    const double box[3] = {bx, by, bz};
+    double x[3];
+    bool finite = true;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        const int64_t i = 3 * p + c;
+        double v = vel[i];
+        if (kick3) {
+            v = xadd(v, xmul(half_respa, f3[i]));
+            vel[i] = v;
+        }
+        double xc = xadd(pos[i], xadd(xmul(dt, v), xmul(half_drift, f2_old[i])));
+        if (periodic) xc = wrap_coord(xc, box[c]);
+        pos[i] = xc;
+        x[c] = xc;
+        finite = finite && isfinite(xc);
     }
-    double x = xadd(pos[i], xadd(xmul(dt, v), xmul(half_drift, f2_old[i])));
-    if (periodic) {
-        const int c = (int)(i % 3);
-        x = wrap_coord(x, c == 0 ? bx : (c == 1 ? by : bz));
+    if (!finite) record_status(status, tag, RB_KIND_NONFINITE);
+    if (pr && rank_of) {
+        const int64_t r = rank_of[p];
+        pr[3 * r] = x[0];
+        pr[3 * r + 1] = x[1];
+        pr[3 * r + 2] = x[2];
     }
-    pos[i] = x;
-    if (!isfinite(x)) record_status(status, tag, RB_KIND_NONFINITE);
+    if (x_ref && rebuild_flag) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            double d = x[c] - x_ref[3 * p + c];
+            if (periodic) d = min_image(d, box[c], 0.5 * box[c]);
+            d2 += d * d;
+        }
+        if (!(d2 <= skin_half2)) *rebuild_flag = tag;  // also catches NaN
+    }
 }
 
 __global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict__ f2_old,
@@ -204,14 +235,17 @@ using namespace rb;
 extern "C" int rb_respa_drift(int64_t n, double *pos, double *vel, const double *f2_old,
                               const double *f3, const double *box3_host, int32_t periodic,
                               double dt, double half_drift, double half_respa, int32_t kick3,
-                              unsigned long long *status, int64_t tag, void *stream) {
+                              const int32_t *rank_of, double *pos_r, const double *x_ref,
+                              double skin, int64_t *rebuild_flag, unsigned long long *status,
+                              int64_t tag, void *stream) {
     if (n < 0 || !box3_host) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
-    const int64_t n3 = 3 * n;
     const int tb = 256;
-    k_drift<<<(unsigned)((n3 + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
-        n3, pos, vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt,
-        half_drift, half_respa, kick3, status, tag);
+    const double half = 0.5 * skin;
+    k_drift<<<(unsigned)((n + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
+        n, pos, vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt,
+        half_drift, half_respa, kick3, rank_of, pos_r, x_ref, half * half * (1.0 - 1e-9),
+        rebuild_flag, status, tag);
     note_launches(1);
     return launch_status();
 }

@@ -18,8 +18,7 @@ constexpr int kLjGroup = 8;
 constexpr int kLjThreads = 256;
 
 __global__ void __launch_bounds__(kLjThreads)
-    k_lj(rb_grid g, int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
-         const double *__restrict__ zs, const int32_t *__restrict__ parts,
+    k_lj(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ parts,
          const int32_t *__restrict__ rows, const int32_t *__restrict__ row_count,
          int32_t capacity, double rc2, double eps24, double eps4, double sigma2,
          double *__restrict__ forces, double *__restrict__ energy_rank,
@@ -34,13 +33,13 @@ __global__ void __launch_bounds__(kLjThreads)
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
     bool bad = false;
     if (active) {
-        const double xi = xs[r], yi = ys[r], zi = zs[r];
+        const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
         const int m = row_count[r];
         const int32_t *row = rows + r * (int64_t)capacity;
         for (int k = sub; k < m; k += kLjGroup) {
             const int j = row[k];
             double dx, dy, dz;
-            exact_disp(im, xi, yi, zi, xs[j], ys[j], zs[j], dx, dy, dz);
+            exact_disp(im, xi, yi, zi, pr[3 * (j)], pr[3 * (j) + 1], pr[3 * (j) + 2], dx, dy, dz);
             const double r2 = exact_r2(dx, dy, dz);
             if (r2 > rc2) continue;
             if (r2 < RB_MIN_DISTANCE_SQ) {
@@ -79,8 +78,7 @@ __global__ void __launch_bounds__(kLjThreads)
 
 using namespace rb;
 
-extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *xs, const double *ys,
-                          const double *zs, const int32_t *cell_particles, const int32_t *rows,
+extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                           const int32_t *row_count, int32_t capacity, double rc, double epsilon,
                           double sigma, double *forces, double *energy_rank, double *virial_rank,
                           unsigned long long *status, int64_t tag, void *stream) {
@@ -89,7 +87,7 @@ extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *xs, const d
     const int64_t threads = n * kLjGroup;
     unsigned blocks = (unsigned)((threads + kLjThreads - 1) / kLjThreads);
     k_lj<<<blocks, kLjThreads, 0, as_stream(stream)>>>(
-        *g, n, xs, ys, zs, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
+        *g, n, pos_r, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
         4.0 * epsilon, sigma * sigma, forces, energy_rank, virial_rank, status, tag);
     note_launches(1);
     return launch_status();

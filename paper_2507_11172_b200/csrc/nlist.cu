@@ -18,16 +18,17 @@ namespace rb {
 constexpr int kNlistWarps = 8;
 
 __global__ void __launch_bounds__(kNlistWarps * 32)
-    k_nlist(rb_grid g, int64_t n, const double *__restrict__ xs, const double *__restrict__ ys,
-            const double *__restrict__ zs, const int32_t *__restrict__ cell_start,
+    k_nlist(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ cell_start,
             const int32_t *__restrict__ cell_of_rank, double rl2, int32_t capacity,
             int32_t *__restrict__ rows, int32_t *__restrict__ row_count,
-            int32_t *__restrict__ max_count) {
+            int32_t *__restrict__ max_count, const int64_t *flag,
+            const unsigned long long *status, int64_t tag) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kNlistWarps + (threadIdx.x >> 5);
     if (r >= n) return;
+    if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
     const Image im = make_image(g);
-    const double xi = xs[r], yi = ys[r], zi = zs[r];
+    const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
     const int cb = cell_of_rank[r];
     const int cbz = cb % g.cells[2];
     const int cby = (cb / g.cells[2]) % g.cells[1];
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
             j = owner_start + (cand - (owner_incl - owner_count));
             if (j != r) {
                 double dx, dy, dz;
-                exact_disp(im, xi, yi, zi, xs[j], ys[j], zs[j], dx, dy, dz);
+                exact_disp(im, xi, yi, zi, pr[3 * (j)], pr[3 * (j) + 1], pr[3 * (j) + 2], dx, dy, dz);
                 keep = exact_r2(dx, dy, dz) <= rl2;
             }
         }
@@ -111,11 +112,13 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
 // (binary search: rows are sorted by rank); -1 for q > p.
 __global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
                          const int32_t *__restrict__ row_count, int32_t capacity,
-                         int32_t *__restrict__ mirror) {
+                         int32_t *__restrict__ mirror, const int64_t *flag,
+                         const unsigned long long *status, int64_t tag) {
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t p = gid / capacity;
     const int k = (int)(gid % capacity);
     if (p >= n) return;
+    if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
     const int m = row_count[p];
     if (k >= m) return;
     const int q = rows[p * (int64_t)capacity + k];
@@ -141,29 +144,31 @@ __global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
 
 using namespace rb;
 
-extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *xs, const double *ys,
-                        const double *zs, const int32_t *cell_start, const int32_t *cell_of_rank,
+extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_start, const int32_t *cell_of_rank,
                         double r_list, int32_t capacity, int32_t *rows, int32_t *row_count,
-                        int32_t *max_count, void *stream) {
+                        int32_t *max_count, const int64_t *rebuild_flag,
+                        const unsigned long long *status, int64_t tag, void *stream) {
     if (!g || n < 0 || capacity <= 0 || !max_count) return RB_ERR_ARGUMENT;
     if (g->n_offsets <= 0 || g->n_offsets > RB_MAX_OFFSETS) return RB_ERR_GEOMETRY;
     if (n == 0) return RB_OK;
     const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
     unsigned blocks = (unsigned)((n + kNlistWarps - 1) / kNlistWarps);
     k_nlist<<<blocks, kNlistWarps * 32, 0, as_stream(stream)>>>(
-        *g, n, xs, ys, zs, cell_start, cell_of_rank, rl2, capacity, rows, row_count, max_count);
+        *g, n, pos_r, cell_start, cell_of_rank, rl2, capacity, rows, row_count, max_count,
+        rebuild_flag, status, tag);
     note_launches(1);
     return launch_status();
 }
 
 extern "C" int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_count,
-                               int32_t capacity, int32_t *mirror, void *stream) {
+                               int32_t capacity, int32_t *mirror, const int64_t *rebuild_flag,
+                               const unsigned long long *status, int64_t tag, void *stream) {
     if (n < 0 || capacity <= 0 || !rows || !row_count || !mirror) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     const int64_t threads = n * (int64_t)capacity;
     const int tb = 256;
     k_mirror<<<(unsigned)((threads + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
-        n, rows, row_count, capacity, mirror);
+        n, rows, row_count, capacity, mirror, rebuild_flag, status, tag);
     note_launches(1);
     return launch_status();
 }

@@ -1,18 +1,22 @@
 """Device workspace and pass sequencing for the sm_100a kernels.
 
 ``ForceEngine`` owns the device buffers of one particle count (torch CUDA
-tensors as plain memory) and issues the C-ABI passes on the current torch
-stream:
+tensors used as plain memory) and issues the C-ABI passes on the current
+torch stream:
 
     bin (counting sort, containers.py:175-209)
-      -> nlist (survivor rows, :437-474)
-      -> lj   (pair pass, :282-370)      -> deterministic sums
-      -> atm  (triplet pass, :373-535)   -> deterministic sums
+      -> nlist + mirror (rank-sorted survivor rows, :437-474)
+      -> lj   (pair pass, :282-370)           -> deterministic sums
+      -> atm  (Newton-3 triplet pass, :373-535) -> deterministic sums
 
 Every buffer lives in HBM for the whole run; nothing is reallocated per
-step.  Positions stay in the reference's (n,3) AoS particle order; the
-binning gathers a rank-ordered SoA copy (xs, ys, zs) for the force kernels,
-which write forces straight back into particle order.
+step.  State stays in the reference's (n,3) AoS particle order; the binning
+gathers a rank-ordered copy ``pos_r`` that the force kernels read, and they
+write forces straight back into particle order.
+
+Inside a device-resident run the rows are Verlet rows built at rc + skin: the
+rebuild kernels are launched every step but gated on ``rebuild_flag`` (set
+by the drift kernel of that step when a particle moved more than skin/2).
 """
 
 from __future__ import annotations
@@ -24,10 +28,11 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from .grid import Geometry, rb_grid
 from ._lib import ptr
+from .grid import Geometry, rb_grid
 
 SCALAR_SUMSQ, SCALAR_E2, SCALAR_W2, SCALAR_E3, SCALAR_W3 = 0, 1, 2, 3, 4
+_NULL = ctypes.c_void_p(0)
 
 
 def _round_up(x: int, m: int) -> int:
@@ -50,18 +55,21 @@ class ForceEngine:
         dev, f64, i32, i64 = self.device, torch.float64, torch.int32, torch.int64
         n = max(self.n, 1)
         self.pos = torch.zeros((n, 3), dtype=f64, device=dev)
-        self.xs = torch.empty(n, dtype=f64, device=dev)
-        self.ys = torch.empty(n, dtype=f64, device=dev)
-        self.zs = torch.empty(n, dtype=f64, device=dev)
-        self.parts = torch.empty(n, dtype=i32, device=dev)
-        self.cell_of_rank = torch.empty(n, dtype=i32, device=dev)
-        self.e_rank = torch.zeros(n, dtype=f64, device=dev)
-        self.w_rank = torch.zeros(n, dtype=f64, device=dev)
+        self.pos_r = torch.zeros((n, 3), dtype=f64, device=dev)  # rank order
+        self.x_ref = torch.zeros((n, 3), dtype=f64, device=dev)  # positions at the last build
+        self.parts = torch.zeros(n, dtype=i32, device=dev)  # rank -> particle
+        self.rank_of = torch.zeros(n, dtype=i32, device=dev)  # particle -> rank
+        self.cell_of_rank = torch.zeros(n, dtype=i32, device=dev)
+        self.e2_rank = torch.zeros(n, dtype=f64, device=dev)
+        self.w2_rank = torch.zeros(n, dtype=f64, device=dev)
+        self.e3_rank = torch.zeros(n, dtype=f64, device=dev)
+        self.w3_rank = torch.zeros(n, dtype=f64, device=dev)
         self.v_rank = torch.zeros(n, dtype=i32, device=dev)
         self.row_count = torch.zeros(n, dtype=i32, device=dev)
         self.max_count = torch.zeros(1, dtype=i32, device=dev)
         # status[0]: error word (all ones = clear); status[1]: device step counter
         self.status = torch.tensor([-1, 0], dtype=i64, device=dev)
+        self.rebuild_flag = torch.zeros(1, dtype=i64, device=dev)
         self.scalars = torch.zeros(8, dtype=f64, device=dev)
         self.visits = torch.zeros(1, dtype=i64, device=dev)
         self.red_scratch = torch.empty(
@@ -104,6 +112,9 @@ class ForceEngine:
         src = np.ascontiguousarray(positions, dtype=np.float64)
         self.pos.copy_(self.torch.from_numpy(src), non_blocking=False)
 
+    def _gate(self, gated: bool):
+        return ptr(self.rebuild_flag) if gated else _NULL
+
     # --------------------------------------------------------------- binning
     def _ensure_cells(self, ncell: int) -> None:
         torch = self.torch
@@ -113,12 +124,13 @@ class ForceEngine:
         if self.bin_scratch is None or self.bin_scratch.numel() < need:
             self.bin_scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
 
-    def bin(self, geom: Geometry, pos=None) -> None:
+    def bin(self, geom: Geometry, pos=None, gated: bool = False, tag: int = 0) -> None:
         pos = self.pos if pos is None else pos
         self._ensure_cells(geom.num_cells)
         g = self.grid_struct(geom)
         st = self.L.rb_bin(ctypes.byref(g), self.n, ptr(pos), ptr(self.cell_start), ptr(self.parts),
-                           ptr(self.cell_of_rank), ptr(self.xs), ptr(self.ys), ptr(self.zs),
+                           ptr(self.cell_of_rank), ptr(self.pos_r), ptr(self.rank_of),
+                           ptr(self.x_ref), self._gate(gated), ptr(self.status), int(tag),
                            ptr(self.bin_scratch), self.bin_scratch.numel(), self.stream)
         _lib.check(st, "rb_bin")
 
@@ -136,31 +148,35 @@ class ForceEngine:
     def _ensure_rows(self, capacity: int) -> None:
         if self.rows is None or self.capacity != capacity:
             torch = self.torch
-            self.rows = torch.empty(max(self.n, 1) * capacity, dtype=torch.int32, device=self.device)
-            self.mirror = torch.empty(max(self.n, 1) * capacity, dtype=torch.int32,
+            self.rows = torch.zeros(max(self.n, 1) * capacity, dtype=torch.int32, device=self.device)
+            self.mirror = torch.zeros(max(self.n, 1) * capacity, dtype=torch.int32,
                                       device=self.device)
             need = int(self.L.rb_atm_scratch_bytes(self.n, capacity))
             self.atm_scratch = torch.empty((need + 7) // 8, dtype=torch.float64, device=self.device)
             self.capacity = capacity
 
     def nlist(self, geom: Geometry, r_list: float, capacity: Optional[int] = None,
-              checked: bool = True) -> None:
-        """Build rows within r_list.  ``checked`` syncs and grows the capacity
-        until no row overflows (container path); the device loop passes
-        ``checked=False`` and inspects ``max_count`` at its sync points."""
+              checked: bool = True, gated: bool = False, tag: int = 0) -> None:
+        """Build rank-sorted rows within r_list and their mirror indices.
+
+        ``checked`` syncs and grows the capacity until no row overflows
+        (container path); the device loop passes ``checked=False`` (and
+        ``gated=True``) and inspects ``max_count`` at its sync points."""
         if capacity is None:
             capacity = self.capacity or self.estimate_capacity(geom, r_list)
         while True:
             self._ensure_rows(capacity)
-            self.max_count.zero_()
+            if checked:
+                self.max_count.zero_()
             g = self.grid_struct(geom)
-            st = self.L.rb_nlist(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
-                                 ptr(self.cell_start), ptr(self.cell_of_rank), float(r_list),
-                                 int(self.capacity), ptr(self.rows), ptr(self.row_count),
-                                 ptr(self.max_count), self.stream)
+            st = self.L.rb_nlist(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.cell_start),
+                                 ptr(self.cell_of_rank), float(r_list), int(self.capacity),
+                                 ptr(self.rows), ptr(self.row_count), ptr(self.max_count),
+                                 self._gate(gated), ptr(self.status), int(tag), self.stream)
             _lib.check(st, "rb_nlist")
             st = self.L.rb_nlist_mirror(self.n, ptr(self.rows), ptr(self.row_count),
-                                        int(self.capacity), ptr(self.mirror), self.stream)
+                                        int(self.capacity), ptr(self.mirror), self._gate(gated),
+                                        ptr(self.status), int(tag), self.stream)
             _lib.check(st, "rb_nlist_mirror")
             if not checked:
                 return
@@ -180,57 +196,63 @@ class ForceEngine:
 
     # -------------------------------------------------------------- passes
     def lj(self, geom: Geometry, rc: float, epsilon: float, sigma: float, forces,
-           tag: int = 0) -> None:
+           tag: int = 0, reduce: bool = True) -> None:
         self.lj_kernel(geom, rc, epsilon, sigma, forces, tag)
-        self.sum_f64(self.e_rank, SCALAR_E2)
-        self.sum_f64(self.w_rank, SCALAR_W2)
+        if reduce:
+            self.reduce_pair()
+
+    def reduce_pair(self) -> None:
+        self.sum_f64(self.e2_rank, SCALAR_E2)
+        self.sum_f64(self.w2_rank, SCALAR_W2)
 
     def lj_kernel(self, geom: Geometry, rc: float, epsilon: float, sigma: float, forces,
                   tag: int = 0) -> None:
         """The rb_lj_pass launch alone."""
         g = self.grid_struct(geom)
-        st = self.L.rb_lj_pass(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
-                               ptr(self.parts), ptr(self.rows), ptr(self.row_count),
-                               int(self.capacity), float(rc), float(epsilon), float(sigma),
-                               ptr(forces), ptr(self.e_rank), ptr(self.w_rank), ptr(self.status),
-                               int(tag), self.stream)
+        st = self.L.rb_lj_pass(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
+                               ptr(self.rows), ptr(self.row_count), int(self.capacity), float(rc),
+                               float(epsilon), float(sigma), ptr(forces), ptr(self.e2_rank),
+                               ptr(self.w2_rank), ptr(self.status), int(tag), self.stream)
         _lib.check(st, "rb_lj_pass")
 
     def atm(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
-            count_visits: bool = True) -> None:
+            count_visits: bool = True, reduce: bool = True) -> None:
         """Newton-3 triplet pass; ``self.visits`` <- unique triplet count."""
         self.atm_kernel(geom, rc, nu, forces, tag)
-        self.sum_f64(self.e_rank, SCALAR_E3)
-        self.sum_f64(self.w_rank, SCALAR_W3)
+        if reduce:
+            self.reduce_triplet()
         if count_visits:
             self._count()
+
+    def reduce_triplet(self) -> None:
+        self.sum_f64(self.e3_rank, SCALAR_E3)
+        self.sum_f64(self.w3_rank, SCALAR_W3)
 
     def atm_kernel(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0) -> None:
         """The rb_atm_pass launch alone (bench timing)."""
         g = self.grid_struct(geom)
-        st = self.L.rb_atm_pass(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys), ptr(self.zs),
-                                ptr(self.parts), ptr(self.rows), ptr(self.row_count),
-                                ptr(self.mirror), int(self.capacity),
-                                int(self.slots or self.capacity), float(rc), float(nu),
-                                ptr(forces), ptr(self.e_rank), ptr(self.w_rank), ptr(self.v_rank),
-                                ptr(self.atm_scratch), self.atm_scratch.numel() * 8,
-                                ptr(self.status), int(tag), self.stream)
+        st = self.L.rb_atm_pass(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
+                                ptr(self.rows), ptr(self.row_count), ptr(self.mirror),
+                                int(self.capacity), int(self.slots or self.capacity), float(rc),
+                                float(nu), ptr(forces), ptr(self.e3_rank), ptr(self.w3_rank),
+                                ptr(self.v_rank), ptr(self.atm_scratch),
+                                self.atm_scratch.numel() * 8, ptr(self.status), int(tag),
+                                self.stream)
         _lib.check(st, "rb_atm_pass")
 
     def atm_c01(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
                 reduce: bool = True) -> None:
         """C01 (owner-computes) triplet pass; ``self.visits`` <- accepted visits."""
         g = self.grid_struct(geom)
-        st = self.L.rb_atm_pass_c01(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys),
-                                    ptr(self.zs), ptr(self.parts), ptr(self.rows),
-                                    ptr(self.row_count), int(self.capacity), float(rc), float(nu),
-                                    ptr(forces), ptr(self.e_rank), ptr(self.w_rank),
-                                    ptr(self.v_rank), ptr(self.status), int(tag), self.stream)
+        st = self.L.rb_atm_pass_c01(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
+                                    ptr(self.rows), ptr(self.row_count), int(self.capacity),
+                                    float(rc), float(nu), ptr(forces), ptr(self.e3_rank),
+                                    ptr(self.w3_rank), ptr(self.v_rank), ptr(self.status),
+                                    int(tag), self.stream)
         _lib.check(st, "rb_atm_pass_c01")
         if not reduce:
             return
-        self.sum_f64(self.e_rank, SCALAR_E3)
-        self.sum_f64(self.w_rank, SCALAR_W3)
+        self.reduce_triplet()
         self._count()
 
     def _count(self) -> None:
@@ -246,10 +268,9 @@ class ForceEngine:
         total = int(counts.sum().item())
         out = torch.empty(max(total, 1) * 3, dtype=torch.int32, device=self.device)
         g = self.grid_struct(geom)
-        st = self.L.rb_atm_visit_rows(ctypes.byref(g), self.n, ptr(self.xs), ptr(self.ys),
-                                      ptr(self.zs), ptr(self.parts), ptr(self.rows),
-                                      ptr(self.row_count), int(self.capacity), float(rc),
-                                      ptr(offsets), ptr(out), self.stream)
+        st = self.L.rb_atm_visit_rows(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
+                                      ptr(self.rows), ptr(self.row_count), int(self.capacity),
+                                      float(rc), ptr(offsets), ptr(out), self.stream)
         _lib.check(st, "rb_atm_visit_rows")
         return out[: 3 * total].view(total, 3).cpu().numpy().astype(np.int64)
 

@@ -115,10 +115,19 @@ _MSG = {
 
 
 class DeviceRespa:
-    """One device-resident r-RESPA run (all buffers allocated up front)."""
+    """One device-resident r-RESPA run (all buffers allocated up front).
+
+    Periodic systems use Verlet rows built at r_list + ``skin``: the drift of
+    each step flags a rebuild when some particle moved more than skin/2 since
+    the last build, and the (gated) binning / row kernels then run inside the
+    same step, so every pair within the cutoff is always in the rows.  Open
+    systems rebuild every step (their grid follows the particles)."""
+
+    DEFAULT_SKIN = 0.3
 
     def __init__(self, system, ff, container, schedule: RespaSchedule, sample_interval: int,
-                 capacity: Optional[int] = None, use_graph: bool = True):
+                 capacity: Optional[int] = None, use_graph: bool = True,
+                 skin: Optional[float] = None):
         self.system = system
         self.ff = ff
         self.container = container
@@ -140,6 +149,14 @@ class DeviceRespa:
         self.nu = float(ff.nu)
         self.with_3b = self.nu != 0.0
         self.r_list = max(self.rc2, self.rc3) if self.with_3b else self.rc2
+        self.box = np.ascontiguousarray(system.box, dtype=np.float64)
+        if self.periodic:
+            want = self.DEFAULT_SKIN if skin is None else float(skin)
+            # the rows' grid needs box >= 2 (r_list + skin) (containers.py:248-252)
+            self.skin = max(0.0, min(want, float(np.min(self.box)) / 2.0 - self.r_list))
+        else:
+            self.skin = 0.0
+        self.r_build = self.r_list + self.skin
         s = schedule.step_size_factor
         m = float(system.mass)
         dt = schedule.dt
@@ -147,7 +164,6 @@ class DeviceRespa:
         self.half_dt = 0.5 * dt / m
         self.half_drift = 0.5 * dt * dt / m
         self.half_respa = 0.5 * dt * s / m
-        self.box = np.ascontiguousarray(system.box, dtype=np.float64)
         nsamples = schedule.num_iterations // self.interval + 1
         self.trace_dev = torch.zeros((nsamples, 8), dtype=f64, device=dev)
         self.capacity = capacity
@@ -159,13 +175,13 @@ class DeviceRespa:
     def _geom(self):
         if self.periodic:
             if self.geom is None:
-                self.geom = geometry(self.box, None, self.r_list, True)
+                self.geom = geometry(self.box, None, self.r_build, True)
             return self.geom
         lo_hi = self.torch.aminmax(self.x, dim=0)
         pos = np.stack([lo_hi.min.cpu().numpy(), lo_hi.max.cpu().numpy()])
         if not np.all(np.isfinite(pos)):
             return None  # the drift already recorded the non-finite state
-        return geometry(self.box, pos, self.r_list, False)
+        return geometry(self.box, pos, self.r_build, False)
 
     def _forces(self, tag: int, with_triplet: bool, f2_out) -> None:
         eng = self.eng
@@ -177,18 +193,26 @@ class DeviceRespa:
             if with_triplet:
                 self.f3.fill_(float("nan"))
             return
-        eng.bin(geom, self.x)
-        eng.nlist(geom, self.r_list, capacity=self.capacity, checked=False)
-        eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag)
+        gated = self.periodic
+        eng.bin(geom, self.x, gated=gated, tag=tag)
+        eng.nlist(geom, self.r_build, capacity=self.capacity, checked=False, gated=gated, tag=tag)
+        eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag, reduce=False)
         if with_triplet:
             if self.with_3b:
-                eng.atm(geom, self.rc3, self.nu, self.f3, tag=tag, count_visits=False)
+                eng.atm(geom, self.rc3, self.nu, self.f3, tag=tag, count_visits=False,
+                        reduce=False)
             else:
                 self.f3.zero_()
-                eng.scalars[SCALAR_E3:SCALAR_W3 + 1].zero_()
+                self.eng.e3_rank.zero_()
+                self.eng.w3_rank.zero_()
+
+    def _reduce_scalars(self) -> None:
+        self.eng.reduce_pair()
+        self.eng.reduce_triplet()
 
     def _record(self) -> None:
         L, eng = self.eng.L, self.eng
+        self._reduce_scalars()
         eng.sum_f64(self.v, SCALAR_SUMSQ, square=True, n=3 * self.n)
         base = eng.scalars.data_ptr()
         sc = [ctypes.c_void_p(base + 8 * k) for k in range(5)]
@@ -202,9 +226,15 @@ class DeviceRespa:
         s = self.schedule.step_size_factor
         st = L.rb_step_begin(ptr(eng.status), eng.stream)
         _lib.check(st, "rb_step_begin")
+        verlet = self.periodic
+        null = ctypes.c_void_p(0)
         st = L.rb_respa_drift(self.n, ptr(self.x), ptr(self.v), ptr(self.f2_old), ptr(self.f3),
                               self.box.ctypes.data_as(ctypes.c_void_p), int(self.periodic),
                               self.dt, self.half_drift, self.half_respa, int(i % s == 0),
+                              ptr(eng.rank_of) if verlet else null,
+                              ptr(eng.pos_r) if verlet else null,
+                              ptr(eng.x_ref) if verlet else null, self.skin,
+                              ptr(eng.rebuild_flag) if verlet else null,
                               ptr(eng.status), _lib.RB_TAG_FROM_DEVICE, eng.stream)
         _lib.check(st, "rb_respa_drift")
         end_of_cycle = (i + 1) % s == 0
@@ -227,18 +257,24 @@ class DeviceRespa:
         eng.upload_positions(self.system.positions)
         self.v.copy_(torch.from_numpy(np.ascontiguousarray(self.system.velocities, np.float64)))
         eng.reset_status(0)
+        eng.rebuild_flag.zero_()  # tag 0 == forced build for the initial passes
         if self.capacity is None:
             geom = self._geom()
             eng.bin(geom, self.x)
-            eng.nlist(geom, self.r_list, capacity=None, checked=True)
+            eng.nlist(geom, self.r_build, capacity=None, checked=True)
             longest = int(eng.max_count.item())
             # rows and triplet slots sized from the initial longest row with margin;
             # an overflow later is detected and the run is repeated larger
             self.capacity = min(4096, _round_up(int(longest * 1.3) + 16, 32))
+        eng.max_count.zero_()
         self.slots = self.capacity  # S+(i) can be a whole row
         eng.slots = self.slots
         self._forces(0, True, self.f2_old)
         self._record()
+
+    def finish_scalars(self) -> None:
+        """Container scalars of the most recent passes (integrators.py:74-83)."""
+        self._reduce_scalars()
 
     def capture(self) -> None:
         """Capture one sampling period as a CUDA graph (after a warm-up)."""
@@ -289,7 +325,8 @@ def _fill_trace(trace: RunTrace, rows: np.ndarray, mass: float) -> None:
 
 
 def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: Optional[int] = None,
-              hooks=(), use_graph: bool = True, capacity: Optional[int] = None) -> RunTrace:
+              hooks=(), use_graph: bool = True, capacity: Optional[int] = None,
+              skin: Optional[float] = None) -> RunTrace:
     """Integrate in place with the r-RESPA loop on the GPU (integrators.py:96-173)."""
     if not isinstance(container, CudaLinkedCells):
         raise TypeError("respa_run needs a CudaLinkedCells container (GPU only, no host fallback)")
@@ -307,7 +344,7 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
     v0 = np.array(system.velocities, copy=True)
     for attempt in range(3):
         run = DeviceRespa(system, ff, container, schedule, sample_interval, capacity=capacity,
-                          use_graph=use_graph and not hooks)
+                          use_graph=use_graph and not hooks, skin=skin)
         try:
             return _drive(run, hooks)
         except CapacityError:
@@ -338,6 +375,12 @@ def _drive(run: DeviceRespa, hooks) -> RunTrace:
             trace.record_values(*_row_values(run, k + 1))
             for hook in hooks:
                 hook((k + 1) * run.interval, view, run.container)
+        for i in range(n_periods * run.interval, run.schedule.num_iterations):
+            run._step(i)
+        run.finish_scalars()
+        _check(run, trace, upto=n_periods + 1)
+        run.download()
+        run.update_container()
         return trace
     if n_periods > 0 and run.use_graph:
         run.run_periods(0, 1)  # warm-up, also the first period of the run
@@ -347,6 +390,9 @@ def _drive(run: DeviceRespa, hooks) -> RunTrace:
         run.run_periods(1, n_periods - 1)
     else:
         run.run_periods(0, n_periods)
+    for i in range(n_periods * run.interval, run.schedule.num_iterations):
+        run._step(i)  # iterations past the last sample point
+    run.finish_scalars()
     _check(run, trace, upto=n_periods + 1)
     _fill_trace(trace, run.trace_rows(n_periods + 1), float(sysm.mass))
     run.download()
@@ -371,6 +417,7 @@ def _check(run: DeviceRespa, trace: RunTrace, upto: int) -> None:
     keep = rows[rows[:, 0] < tag] if tag > 0 else rows[:0]
     if not len(trace):
         _fill_trace(trace, keep, float(run.system.mass))
+    run.finish_scalars()
     run.download()
     run.update_container()
     raise IntegrationBlowUp(int(tag), _MSG.get(kind, f"device error kind {kind}"), trace)

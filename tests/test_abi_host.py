@@ -37,6 +37,16 @@ def test_library_builds_and_exports_every_declared_symbol():
     assert sorted(_lib.SIGNATURES) == names
 
 
+def test_binding_argument_counts_match_header():
+    """Every ctypes prototype has as many arguments as the header declares."""
+    from paper_2507_11172_b200 import _lib
+
+    text = open(os.path.join(REPO, "include", "respa_b200.h")).read()
+    for m in re.finditer(r"RB_API\s+[\w\s\*]+?\b(rb_\w+)\s*\(([^;]*?)\);", text, re.S):
+        args = [a for a in m.group(2).split(",") if a.strip() and a.strip() != "void"]
+        assert len(_lib.SIGNATURES[m.group(1)][1]) == len(args), m.group(1)
+
+
 def test_library_metadata_calls_without_gpu():
     from paper_2507_11172_b200 import _lib
 

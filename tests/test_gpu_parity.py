@@ -303,6 +303,19 @@ def test_respa_graph_and_eager_identical(pkg):
     assert ta.total == tb.total
 
 
+def test_verlet_skin_rows_match_rebuild_every_step(pkg):
+    """Rows built at rc + skin and rebuilt on the displacement criterion give
+    the trajectory of a rebuild-every-step run (only summation order moves)."""
+    base = pkg.systems.fcc_system(7, temperature=1.5, seed=9, vseed=10)
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5)
+    a, b = base.copy(), base.copy()
+    ta = pkg.respa_run(a, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 5, 300), skin=0.3)
+    tb = pkg.respa_run(b, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 5, 300), skin=0.0)
+    assert np.max(np.abs(a.positions - b.positions)) <= 1e-10
+    assert np.max(np.abs(a.velocities - b.velocities)) <= 1e-10
+    assert max(_rel(x, y) for x, y in zip(ta.total, tb.total)) <= 1e-10
+
+
 def test_s1_is_verlet_and_zero_nu_independent_of_s(pkg):
     base = pkg.systems.fcc_system(5, temperature=1.0, seed=2, vseed=3)
     ff = pkg.ForceField(nu=0.4, cutoff=2.5)

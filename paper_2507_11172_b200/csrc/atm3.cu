@@ -38,36 +38,41 @@ constexpr int kA3Warps = 4;
 #endif
 constexpr int kA3MinBlocks = RB_A3_MIN_BLOCKS;  // register cap for occupancy
 constexpr int kA3Queue = 64;
+constexpr int kA3RoundBlock = 32;    // rounds whose accept bits are built at once
 constexpr double kA3Margin = 1e-10;  // fp64 estimate vs the reference arithmetic
 constexpr double kA3Band = 1e-5;     // fp32 filter vs the fp64 estimate
 
+// per-warp shared memory, M slots (S+(i)) + a 64-entry queue
 struct A3Smem {
-    double *dx, *dy, *dz, *r2;  // slots: d_ij = x_i - x_j, r_ij^2
-    double *ax, *ay, *az;       // slot force accumulators (units of 2 nu)
-    float4 *f4;                 // slots: d_ij in fp32 for the candidate filter
-    int32_t *kidx;              // slot -> row index
-    uint32_t *qst;              // queue: s | t << 16
-    int32_t *qrec;              // queue: round record id
+    double2 *dxy;    // slots: (x, y) of d_ij = x_i - x_j
+    double *dz, *r2; // slots: z of d_ij, r_ij^2
+    double2 *axy;    // slot force accumulators (units of 2 nu), x and y
+    double *az;      //   ... z
+    float4 *f4;      // slots: d_ij in fp32 for the candidate filter
+    int32_t *kidx;   // slot -> row index
+    uint32_t *mask;  // slot -> accept bits of the current round block
+    uint32_t *qst;   // queue: s | t << 16
+    int32_t *qrec;   // queue: round (record id)
 };
 
-__host__ __device__ inline size_t a3_warp_bytes(int capacity) {
-    size_t b = (size_t)capacity * (7 * sizeof(double) + sizeof(float4));
-    b += (size_t)capacity * sizeof(int32_t) + (size_t)kA3Queue * 2 * sizeof(int32_t);
+__host__ __device__ inline size_t a3_warp_bytes(int m) {
+    size_t b = (size_t)m * (2 * sizeof(double2) + 3 * sizeof(double) + sizeof(float4) +
+                            2 * sizeof(int32_t));
+    b += (size_t)kA3Queue * 2 * sizeof(int32_t) + 16;  // + alignment pad of f4
     return (b + 15) & ~(size_t)15;
 }
 
-__device__ inline A3Smem a3_carve(char *base, int capacity) {
+__device__ inline A3Smem a3_carve(char *base, int m) {
     A3Smem s;
-    s.dx = (double *)base;
-    s.dy = s.dx + capacity;
-    s.dz = s.dy + capacity;
-    s.r2 = s.dz + capacity;
-    s.ax = s.r2 + capacity;
-    s.ay = s.ax + capacity;
-    s.az = s.ay + capacity;
-    s.f4 = (float4 *)(s.az + capacity);
-    s.kidx = (int32_t *)(s.f4 + capacity);
-    s.qst = (uint32_t *)(s.kidx + capacity);
+    s.dxy = (double2 *)base;
+    s.axy = s.dxy + m;
+    s.dz = (double *)(s.axy + m);
+    s.r2 = s.dz + m;
+    s.az = s.r2 + m;
+    s.f4 = (float4 *)(s.az + m + (m & 1));  // keep 16-byte alignment
+    s.kidx = (int32_t *)(s.f4 + m);
+    s.mask = (uint32_t *)(s.kidx + m);
+    s.qst = s.mask + m;
     s.qrec = (int32_t *)(s.qst + kA3Queue);
     return s;
 }
@@ -78,69 +83,97 @@ struct A3Acc {
     bool bad;
 };
 
-// evaluate queue entry `q` (lane-private), add f_i/E/W to acc, return f_j, f_k
+// 1/sqrt(x) from an fp32 seed and two Newton steps (2^-23 -> 2^-46 ->
+// rounding); CUDA's rsqrt for the rare arguments outside the fp32 range.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    if (x < 1e-30 || x > 1e30) return rsqrt(x);
+    double y = (double)rsqrtf((float)x);
+#pragma unroll
+    for (int it = 0; it < 2; it++) {
+        const double r = fma(-x * y, y, 1.0);  // 1 - x y^2
+        y = fma(0.5 * y, r, y);
+    }
+    return y;
+}
+
+// Evaluate queue entry `q`: adds f_i, E, W to acc and returns f_j, f_k, all
+// in units of 2 nu.  With a = r_ij^2, b = r_ik^2, c = r_jk^2, u = a+b-c,
+// v = a+c-b, w = b+c-a, p = uvw, S = uv+uw+vw, s = abc (potentials.py:82-114):
+//   E   = s^-5/2 (s + 3/8 p)
+//   E_a = 3/8 s^-5/2 (S - 2uv) - bc (3/2 s^-5/2 + 15/16 p s^-7/2), b/c alike.
 template <bool kExactImage>
 __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im,
                                         const int32_t *__restrict__ row,
-                                        const double *__restrict__ pr, A3Acc &acc, double fj[3],
-                                        double fk[3], int &s, int &t) {
+                                        const double *__restrict__ pr, A3Acc &acc,
+                                        double fj[3], double fk[3], int &s, int &t) {
     const uint32_t st = sm.qst[q];
     s = (int)(st & 0xffffu);
     t = (int)(st >> 16);
     const double a = sm.r2[s], b = sm.r2[t];
-    const double dijx = sm.dx[s], dijy = sm.dy[s], dijz = sm.dz[s];
-    const double dikx = sm.dx[t], diky = sm.dy[t], dikz = sm.dz[t];
-    double djkx, djky, djkz;  // x_j - x_k
+    const double2 ij = sm.dxy[s], ik = sm.dxy[t];
+    const double ijz = sm.dz[s], ikz = sm.dz[t];
+    double jkx, jky, jkz;  // d_jk = x_j - x_k
     double c;
     if (kExactImage) {
         // the reference's raw-position minimum image (containers.py:497-513)
         const int j = row[sm.kidx[s]], k = row[sm.kidx[t]];
-        exact_disp(im, pr[3 * (j)], pr[3 * (j) + 1], pr[3 * (j) + 2], pr[3 * (k)], pr[3 * (k) + 1], pr[3 * (k) + 2], djkx, djky, djkz);
-        c = exact_r2(djkx, djky, djkz);
+        exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
+                   pr[3 * k + 2], jkx, jky, jkz);
+        c = exact_r2(jkx, jky, jkz);
     } else {
-        djkx = dikx - dijx;
-        djky = diky - dijy;
-        djkz = dikz - dijz;
-        c = djkx * djkx + djky * djky + djkz * djkz;
+        jkx = ik.x - ij.x;
+        jky = ik.y - ij.y;
+        jkz = ikz - ijz;
+        c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
     }
     if (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ || c < RB_MIN_DISTANCE_SQ) {
         acc.bad = true;
         fj[0] = fj[1] = fj[2] = fk[0] = fk[1] = fk[2] = 0.0;
         return false;
     }
-    const double u = a + b - c;
-    const double v = a + c - b;
-    const double w = b + c - a;
+    const double tsum = a + b + c;
+    const double u = fma(-2.0, c, tsum);
+    const double v = fma(-2.0, b, tsum);
+    const double w = fma(-2.0, a, tsum);
     const double p = u * v * w;
     const double sp = a * b * c;
-    const double rs = rsqrt(sp);
+    const double rs = rsqrt_nr(sp);
     const double inv_s = rs * rs;
-    const double s32 = inv_s * rs;
-    const double s52 = s32 * inv_s;
+    const double s52 = rs * inv_s * inv_s;
     const double s72 = s52 * inv_s;
     const double uv = u * v, uw = u * w, vw = v * w;
-    const double bc = b * c, ac = a * c, ab = a * b;
-    const double qq = 0.9375 * p * s72;
-    const double ea = (0.375 * (vw + uw - uv) - 1.5 * bc) * s52 - qq * bc;
-    const double eb = (0.375 * (vw - uw + uv) - 1.5 * ac) * s52 - qq * ac;
-    const double ec = (0.375 * (uw + uv - vw) - 1.5 * ab) * s52 - qq * ab;
-    acc.fx -= ea * dijx + eb * dikx;
-    acc.fy -= ea * dijy + eb * diky;
-    acc.fz -= ea * dijz + eb * dikz;
-    acc.e += s32 + 0.375 * p * s52;
-    acc.w += ea * a + eb * b + ec * c;
+    const double S = uv + uw + vw;
+    const double A = 0.375 * s52;
+    const double K = fma(1.5, s52, 0.9375 * p * s72);
+    const double ea = fma(A, fma(-2.0, uv, S), -K * (b * c));
+    const double eb = fma(A, fma(-2.0, uw, S), -K * (a * c));
+    const double ec = fma(A, fma(-2.0, vw, S), -K * (a * b));
+    acc.fx = fma(-ea, ij.x, fma(-eb, ik.x, acc.fx));
+    acc.fy = fma(-ea, ij.y, fma(-eb, ik.y, acc.fy));
+    acc.fz = fma(-ea, ijz, fma(-eb, ikz, acc.fz));
+    acc.e = fma(s52, fma(0.375, p, sp), acc.e);
+    acc.w = fma(ea, a, fma(eb, b, fma(ec, c, acc.w)));
     acc.n += 1;
-    fj[0] = ea * dijx - ec * djkx;
-    fj[1] = ea * dijy - ec * djky;
-    fj[2] = ea * dijz - ec * djkz;
-    fk[0] = eb * dikx + ec * djkx;
-    fk[1] = eb * diky + ec * djky;
-    fk[2] = eb * dikz + ec * djkz;
+    fj[0] = fma(ea, ij.x, -ec * jkx);
+    fj[1] = fma(ea, ij.y, -ec * jky);
+    fj[2] = fma(ea, ijz, -ec * jkz);
+    fk[0] = fma(eb, ik.x, ec * jkx);
+    fk[1] = fma(eb, ik.y, ec * jky);
+    fk[2] = fma(eb, ikz, ec * jkz);
     return true;
 }
 
+__device__ __forceinline__ void a3_add(const A3Smem &sm, int slot, const double f[3]) {
+    double2 xy = sm.axy[slot];
+    xy.x += f[0];
+    xy.y += f[1];
+    sm.axy[slot] = xy;
+    sm.az[slot] += f[2];
+}
+
 // evaluate the first `cnt` queue entries and fold f_j / f_k into the slot
-// accumulators, one round-record at a time (records are contiguous runs)
+// accumulators, one round-record at a time (records are contiguous runs; in
+// one round all j slots are distinct and all k slots are distinct)
 template <bool kExactImage>
 __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, const Image &im,
                                          const int32_t *__restrict__ row,
@@ -154,31 +187,57 @@ __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, co
     }
     unsigned todo = __ballot_sync(0xffffffffu, pending);
     while (todo) {
-        const int leader = __ffs(todo) - 1;
-        const int r0 = __shfl_sync(0xffffffffu, rec, leader);
+        const int r0 = __shfl_sync(0xffffffffu, rec, __ffs(todo) - 1);
         const bool act = pending && rec == r0;
-        if (act) {
-            sm.ax[s] += fj[0];
-            sm.ay[s] += fj[1];
-            sm.az[s] += fj[2];
-        }
+        if (act) a3_add(sm, s, fj);
         __syncwarp();
-        if (act) {
-            sm.ax[t] += fk[0];
-            sm.ay[t] += fk[1];
-            sm.az[t] += fk[2];
-        }
+        if (act) a3_add(sm, t, fk);
         __syncwarp();
         if (act) pending = false;
         todo = __ballot_sync(0xffffffffu, pending);
     }
 }
 
+// r_jk^2 <= rc^2 for the slot pair (s, t), decided bit-exactly: fp32 estimate
+// outside a 1e-5 band, fp64 estimate outside a 1e-10 band, else the
+// reference's raw-position arithmetic.
+template <bool kExactImage>
+__device__ __forceinline__ bool a3_accept(const A3Smem &sm, const float4 &ps, int s, int t,
+                                          const Image &im, const int32_t *__restrict__ row,
+                                          const double *__restrict__ pr, double rc2,
+                                          double rc2_lo, double rc2_hi, float rc2f_lo,
+                                          float rc2f_hi) {
+    if (kExactImage) {
+        // box under four cutoffs: d_ik - d_ij need not be the minimum image
+        const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
+        double dx, dy, dz;
+        exact_disp(im, pr[3 * jr], pr[3 * jr + 1], pr[3 * jr + 2], pr[3 * kr], pr[3 * kr + 1],
+                   pr[3 * kr + 2], dx, dy, dz);
+        return exact_r2(dx, dy, dz) <= rc2;
+    }
+    const float4 pt = sm.f4[t];
+    const float ex = pt.x - ps.x, ey = pt.y - ps.y, ez = pt.z - ps.z;
+    const float c2f = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+    if (c2f <= rc2f_lo) return true;
+    if (c2f > rc2f_hi) return false;
+    const double2 js = sm.dxy[s], kt = sm.dxy[t];
+    const double ex2 = kt.x - js.x, ey2 = kt.y - js.y, ez2 = sm.dz[t] - sm.dz[s];
+    const double c2 = fma(ez2, ez2, fma(ey2, ey2, ex2 * ex2));
+    if (c2 <= rc2_lo) return true;
+    if (c2 > rc2_hi) return false;
+    const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
+    double dx, dy, dz;
+    exact_disp(im, pr[3 * jr], pr[3 * jr + 1], pr[3 * jr + 2], pr[3 * kr], pr[3 * kr + 1],
+               pr[3 * kr + 2], dx, dy, dz);
+    return exact_r2(dx, dy, dz) <= rc2;
+}
+
 template <bool kExactImage>
 __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     k_atm3(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
            const int32_t *__restrict__ row_count, int32_t capacity, int32_t slots, double rc2,
-           double rc2_lo, double rc2_hi, float rc2f_lo, float rc2f_hi, double *__restrict__ own, double *__restrict__ gbuf,
+           double rc2_lo, double rc2_hi, float rc2f_lo, float rc2f_hi,
+           double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, unsigned long long *status, int64_t tag) {
     extern __shared__ __align__(16) char smem_raw[];
@@ -201,11 +260,10 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
         const int k = base + lane;
         bool keep = false;
         double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;
-        int q = -1;
         if (k < rc_n) {
-            q = row[k];
+            const int q = row[k];
             if (q > r) {
-                exact_disp(im, xi, yi, zi, pr[3 * (q)], pr[3 * (q) + 1], pr[3 * (q) + 2], dx, dy, dz);
+                exact_disp(im, xi, yi, zi, pr[3 * q], pr[3 * q + 1], pr[3 * q + 2], dx, dy, dz);
                 r2 = exact_r2(dx, dy, dz);
                 keep = r2 <= rc2;
                 if (!keep) {  // beyond the three-body cutoff: contributes nothing
@@ -222,94 +280,75 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
         }
         if (keep) {
             const int slot = m + __popc(mk & lanemask_lt());
-            sm.dx[slot] = dx;
-            sm.dy[slot] = dy;
+            sm.dxy[slot] = make_double2(dx, dy);
             sm.dz[slot] = dz;
             sm.r2[slot] = r2;
             sm.kidx[slot] = k;
             sm.f4[slot] = make_float4((float)dx, (float)dy, (float)dz, 0.0f);
-            sm.ax[slot] = 0.0;
-            sm.ay[slot] = 0.0;
+            sm.axy[slot] = make_double2(0.0, 0.0);
             sm.az[slot] = 0.0;
         }
         m += __popc(mk);
     }
     __syncwarp();
 
-    // ---- phase 1 + 2: candidates by rounds (flattened over lanes) -> queue
-    // Round d (1..m/2) pairs slot s with slot (s + d) mod m; for even m the
-    // last round only needs s < m/2.  Flat index f = (d-1)*m + s.
+    // ---- phase 1: rounds.  Round d (1..m/2) pairs slot s with (s + d) mod m
+    // (for even m the last round only s < m/2): every unordered pair once.
+    // A: each lane tests its own slots' partners for a block of rounds and
+    //    keeps the accept bits; B: the rounds are replayed in order, accepted
+    //    pairs ballot-compacted into the queue, 32 at a time evaluated.
     A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false};
     const int rounds = m >> 1;
-    const int full_rounds = (m & 1) ? rounds : rounds - 1;
-    const int total = full_rounds * m + ((m & 1) ? 0 : (m >> 1));
-    const float inv_m = m > 0 ? 1.0f / (float)m : 0.0f;
+    const int nsets = (m + 31) >> 5;
     int qn = 0;
-    for (int base = 0; base < total; base += 32) {
-        const int f = base + lane;
-        bool accept = false;
-        int s = 0, t = 0, d = 0;
-        if (f < total) {
-            int dq = (int)((float)f * inv_m);
-            s = f - dq * m;
-            if (s < 0) {
-                dq--;
-                s += m;
-            } else if (s >= m) {
-                dq++;
-                s -= m;
+    for (int d0 = 1; d0 <= rounds; d0 += kA3RoundBlock) {
+        const int dn = min(kA3RoundBlock, rounds - d0 + 1);
+        for (int sg = 0; sg < nsets; sg++) {
+            const int s = (sg << 5) + lane;
+            uint32_t bits = 0u;
+            if (s < m) {
+                const float4 ps = sm.f4[s];
+                for (int e = 0; e < dn; e++) {
+                    const int d = d0 + e;
+                    if (2 * d == m && s >= d) break;  // even m: the half round, once
+                    int t = s + d;
+                    if (t >= m) t -= m;
+                    if (a3_accept<kExactImage>(sm, ps, s, t, im, row, pr, rc2, rc2_lo, rc2_hi,
+                                               rc2f_lo, rc2f_hi))
+                        bits |= 1u << e;
+                }
+                sm.mask[s] = bits;
             }
-            d = dq + 1;
-            t = s + d;
-            if (t >= m) t -= m;
-            // fp32 filter: settles every pair farther than 1e-5 (relative)
-            // from the cutoff; the band in between is decided in fp64 below
-            const float4 ps = sm.f4[s], pt = sm.f4[t];
-            const float ex = pt.x - ps.x, ey = pt.y - ps.y, ez = pt.z - ps.z;
-            const float c2f = ex * ex + ey * ey + ez * ez;
-            if (kExactImage) {
-                // box under four cutoffs: d_ik - d_ij need not be the minimum
-                // image, so every candidate takes the reference arithmetic
-                (void)c2f;
-                const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
-                double dx, dy, dz;
-                exact_disp(im, pr[3 * (jr)], pr[3 * (jr) + 1], pr[3 * (jr) + 2], pr[3 * (kr)], pr[3 * (kr) + 1], pr[3 * (kr) + 2], dx, dy, dz);
-                accept = exact_r2(dx, dy, dz) <= rc2;
-            } else if (c2f <= rc2f_lo) {
-                accept = true;
-            } else if (c2f <= rc2f_hi) {
-                const double ex2 = sm.dx[t] - sm.dx[s];
-                const double ey2 = sm.dy[t] - sm.dy[s];
-                const double ez2 = sm.dz[t] - sm.dz[s];
-                const double c2 = ex2 * ex2 + ey2 * ey2 + ez2 * ez2;
-                if (c2 <= rc2_lo) {
-                    accept = true;
-                } else if (c2 <= rc2_hi) {
-                    const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
-                    double dx, dy, dz;
-                    exact_disp(im, pr[3 * (jr)], pr[3 * (jr) + 1], pr[3 * (jr) + 2], pr[3 * (kr)], pr[3 * (kr) + 1], pr[3 * (kr) + 2], dx, dy, dz);
-                    accept = exact_r2(dx, dy, dz) <= rc2;
+        }
+        __syncwarp();
+        for (int e = 0; e < dn; e++) {
+            const int d = d0 + e;
+            for (int sg = 0; sg < nsets; sg++) {
+                const int s = (sg << 5) + lane;
+                const bool accept = s < m && ((sm.mask[s] >> e) & 1u);
+                const unsigned ma = __ballot_sync(0xffffffffu, accept);
+                if (accept) {
+                    int t = s + d;
+                    if (t >= m) t -= m;
+                    const int slot = qn + __popc(ma & lanemask_lt());
+                    sm.qst[slot] = (uint32_t)s | ((uint32_t)t << 16);
+                    sm.qrec[slot] = d;
+                }
+                qn += __popc(ma);
+                if (qn >= 32) {
+                    __syncwarp();
+                    a3_chunk<kExactImage>(sm, 32, lane, im, row, pr, acc);
+                    __syncwarp();
+                    if (lane < qn - 32) {
+                        sm.qst[lane] = sm.qst[lane + 32];
+                        sm.qrec[lane] = sm.qrec[lane + 32];
+                    }
+                    __syncwarp();
+                    qn -= 32;
                 }
             }
         }
-        const unsigned ma = __ballot_sync(0xffffffffu, accept);
-        if (accept) {
-            const int slot = qn + __popc(ma & lanemask_lt());
-            sm.qst[slot] = (uint32_t)s | ((uint32_t)t << 16);
-            sm.qrec[slot] = d;  // a round is one record: its s (and t) are distinct
-        }
-        qn += __popc(ma);
         __syncwarp();
-        if (qn >= 32) {
-            a3_chunk<kExactImage>(sm, 32, lane, im, row, pr, acc);
-            __syncwarp();
-            if (lane < qn - 32) {
-                sm.qst[lane] = sm.qst[lane + 32];
-                sm.qrec[lane] = sm.qrec[lane + 32];
-            }
-            __syncwarp();
-            qn -= 32;
-        }
     }
     if (qn > 0) a3_chunk<kExactImage>(sm, qn, lane, im, row, pr, acc);
     __syncwarp();
@@ -317,8 +356,9 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
     for (int sl = lane; sl < m; sl += 32) {
         const int k = sm.kidx[sl];
-        grow[3 * k] = sm.ax[sl];
-        grow[3 * k + 1] = sm.ay[sl];
+        const double2 xy = sm.axy[sl];
+        grow[3 * k] = xy.x;
+        grow[3 * k + 1] = xy.y;
         grow[3 * k + 2] = sm.az[sl];
     }
     const double fx = group_sum<32>(acc.fx);

@@ -126,8 +126,8 @@ RB_API int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r,
                void *stream);
 
 /* Mirror indices of the (rank-sorted) rows: mirror[p*capacity + k] is the
- * position of p in the row of q = rows[p*capacity + k] when q < p, else -1.
- * Needed by the Newton-3 triplet pass to return partial forces to q's row. */
+ * position of p in the row of q = rows[p*capacity + k].  The Newton-3
+ * triplet pass uses it to deliver partial forces into the target's row. */
 RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_count,
                            int32_t capacity, int32_t *mirror, const int64_t *rebuild_flag,
                            const unsigned long long *status, int64_t tag, void *stream);

@@ -10,24 +10,29 @@
 //   phase 0  S+(i): the suffix of i's rank-sorted row with rank > i and
 //            r_ij^2 <= rc^2 (reference arithmetic) -> per-warp slots in
 //            shared memory (d_ij, r_ij^2, row index).
-//   phase 1  candidate pairs of slots by ROUNDS: in round d lane s pairs slot
-//            s with slot (s + d) mod m, d = 1 .. m/2.  Every unordered slot
+//   phase 1  candidate pairs of slots by ROUNDS: in round d slot s pairs
+//            with slot (s + d) mod m, d = 1 .. m/2.  Every unordered slot
 //            pair appears exactly once, and inside one round all first slots
-//            are distinct and all second slots are distinct.  r_jk^2 <= rc^2
-//            is settled bit-exactly (fused estimate from d_ik - d_ij outside a
-//            1e-10 relative band, the reference's raw-position arithmetic
-//            inside it or when the box is under four cutoffs).
-//   phase 2  accepted pairs are queued and evaluated 32 at a time (all lanes
-//            busy); f_i stays in registers, f_j and f_k are added to the slot
-//            accumulators in shared memory one round-record at a time, so no
-//            two lanes of a sub-step touch the same slot and the order of the
+//            are distinct and all second slots are distinct.  Per block of
+//            rounds each lane tests its own slots' partners (r_jk^2 <= rc^2,
+//            settled bit-exactly: fp32 estimate from d_ik - d_ij outside a
+//            1e-5 band, fp64 estimate outside a 1e-10 band, else -- or when
+//            the box is under four cutoffs -- the reference's raw-position
+//            arithmetic) and keeps accept bits; one ballot per (round, slot
+//            set) places every accepted pair in a round-major queue.
+//   phase 2  the queue is evaluated 32 entries at a time (all lanes busy);
+//            f_i stays in registers, f_j and f_k are added to the slot
+//            accumulators in shared memory one round at a time, so no two
+//            lanes of a sub-step touch the same slot and the order of the
 //            additions is fixed by the enumeration.
-//   phase 3  slot sums go to G[i][row index]; the gather kernel sums, for each
-//            particle p in row order, its own part and G[q][mirror(p in q)]
-//            over the row entries q < p -- a fixed order again.
+//   phase 3  slot sums go to the TARGET's row, G[j][position of i in row j];
+//            the gather kernel sums, for each particle p, its own part and
+//            its row segment G[p][k] over the entries q < p -- in row order.
 //
 // Energies are phi per triplet (the reference's phi/3 per visit, summed), the
 // virial -2(E_a a + E_b b + E_c c) per triplet (:530 summed over visits).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rb {
@@ -37,8 +42,9 @@ constexpr int kA3Warps = 4;
 #define RB_A3_MIN_BLOCKS 7
 #endif
 constexpr int kA3MinBlocks = RB_A3_MIN_BLOCKS;  // register cap for occupancy
-constexpr int kA3Queue = 64;
-constexpr int kA3RoundBlock = 32;    // rounds whose accept bits are built at once
+constexpr int kA3Queue = 512;        // entries: the carry of the last chunk + one round block
+constexpr int kA3RoundBlock = 32;    // at most this many rounds per block (bits per word)
+constexpr int kA3MaxSlots = 2047;    // queue entries pack s and t in 11 bits each
 constexpr double kA3Margin = 1e-10;  // fp64 estimate vs the reference arithmetic
 constexpr double kA3Band = 1e-5;     // fp32 filter vs the fp64 estimate
 
@@ -51,14 +57,16 @@ struct A3Smem {
     float4 *f4;      // slots: d_ij in fp32 for the candidate filter
     int32_t *kidx;   // slot -> row index
     uint32_t *mask;  // slot -> accept bits of the current round block
-    uint32_t *qst;   // queue: s | t << 16
-    int32_t *qrec;   // queue: round (record id)
+    uint32_t *vote;  // per round of the block: the ballot of each slot set
+    int32_t *vbase;  // per round of the block: queue offset of each slot set
+    uint32_t *qe;    // queue: s | t << 11 | (round & 1023) << 22
 };
 
 __host__ __device__ inline size_t a3_warp_bytes(int m) {
     size_t b = (size_t)m * (2 * sizeof(double2) + 3 * sizeof(double) + sizeof(float4) +
                             2 * sizeof(int32_t));
-    b += (size_t)kA3Queue * 2 * sizeof(int32_t) + 16;  // + alignment pad of f4
+    b += (size_t)kA3Queue * sizeof(uint32_t) + 16;  // + alignment pad of f4
+    b += (size_t)2 * kA3RoundBlock * ((m + 31) / 32) * sizeof(uint32_t);
     return (b + 15) & ~(size_t)15;
 }
 
@@ -72,8 +80,9 @@ __device__ inline A3Smem a3_carve(char *base, int m) {
     s.f4 = (float4 *)(s.az + m + (m & 1));  // keep 16-byte alignment
     s.kidx = (int32_t *)(s.f4 + m);
     s.mask = (uint32_t *)(s.kidx + m);
-    s.qst = s.mask + m;
-    s.qrec = (int32_t *)(s.qst + kA3Queue);
+    s.qe = s.mask + m;
+    s.vote = s.qe + kA3Queue;
+    s.vbase = (int32_t *)(s.vote + kA3RoundBlock * ((m + 31) / 32));
     return s;
 }
 
@@ -106,9 +115,9 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
                                         const int32_t *__restrict__ row,
                                         const double *__restrict__ pr, A3Acc &acc,
                                         double fj[3], double fk[3], int &s, int &t) {
-    const uint32_t st = sm.qst[q];
-    s = (int)(st & 0xffffu);
-    t = (int)(st >> 16);
+    const uint32_t qe = sm.qe[q];
+    s = (int)(qe & 0x7ffu);
+    t = (int)((qe >> 11) & 0x7ffu);
     const double a = sm.r2[s], b = sm.r2[t];
     const double2 ij = sm.dxy[s], ik = sm.dxy[t];
     const double ijz = sm.dz[s], ikz = sm.dz[t];
@@ -177,13 +186,18 @@ __device__ __forceinline__ void a3_add(const A3Smem &sm, int slot, const double 
 template <bool kExactImage>
 __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, const Image &im,
                                          const int32_t *__restrict__ row,
-                                         const double *__restrict__ pr, A3Acc &acc) {
+                                         const double *__restrict__ pr, A3Acc &acc,
+                                         int debug_mode, int offset) {
     double fj[3] = {0.0, 0.0, 0.0}, fk[3] = {0.0, 0.0, 0.0};
     int s = 0, t = 0, rec = -1;
     bool pending = false;
     if (lane < cnt) {
-        pending = a3_eval<kExactImage>(sm, lane, im, row, pr, acc, fj, fk, s, t);
-        rec = sm.qrec[lane];
+        pending = a3_eval<kExactImage>(sm, offset + lane, im, row, pr, acc, fj, fk, s, t);
+        rec = (int)(sm.qe[offset + lane] >> 22);
+    }
+    if (debug_mode == 4) {  // debug 4: no slot accumulation
+        acc.fx += fj[0] + fk[0] + fj[1] + fk[1] + fj[2] + fk[2];
+        return;
     }
     unsigned todo = __ballot_sync(0xffffffffu, pending);
     while (todo) {
@@ -235,11 +249,13 @@ __device__ __forceinline__ bool a3_accept(const A3Smem &sm, const float4 &ps, in
 template <bool kExactImage>
 __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     k_atm3(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
-           const int32_t *__restrict__ row_count, int32_t capacity, int32_t slots, double rc2,
+           const int32_t *__restrict__ row_count, const int32_t *__restrict__ mirror,
+           int32_t capacity, int32_t slots, double rc2,
            double rc2_lo, double rc2_hi, float rc2f_lo, float rc2f_hi,
            double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
-           int32_t *__restrict__ triplets_rank, unsigned long long *status, int64_t tag) {
+           int32_t *__restrict__ triplets_rank, unsigned long long *status, int64_t tag,
+           int debug_mode) {
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -252,7 +268,9 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
     const int rc_n = row_count[r];
     const int32_t *row = rows + r * (int64_t)capacity;
-    double *grow = gbuf + r * (int64_t)capacity * 3;
+    const int32_t *mir = mirror + r * (int64_t)capacity;
+    // partial forces go to the TARGET's row: G[q][position of i in row q], so
+    // the gather of q reads its own row segment contiguously
 
     // ---- phase 0: S+(i), the row suffix with rank > i within rc
     int m = 0;
@@ -267,9 +285,10 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
                 r2 = exact_r2(dx, dy, dz);
                 keep = r2 <= rc2;
                 if (!keep) {  // beyond the three-body cutoff: contributes nothing
-                    grow[3 * k] = 0.0;
-                    grow[3 * k + 1] = 0.0;
-                    grow[3 * k + 2] = 0.0;
+                    double *gq = gbuf + ((int64_t)q * capacity + mir[k]) * 3;
+                    gq[0] = 0.0;
+                    gq[1] = 0.0;
+                    gq[2] = 0.0;
                 }
             }
         }
@@ -294,72 +313,98 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
 
     // ---- phase 1: rounds.  Round d (1..m/2) pairs slot s with (s + d) mod m
     // (for even m the last round only s < m/2): every unordered pair once.
-    // A: each lane tests its own slots' partners for a block of rounds and
-    //    keeps the accept bits; B: the rounds are replayed in order, accepted
-    //    pairs ballot-compacted into the queue, 32 at a time evaluated.
+    // Per block of rounds: (A) each lane tests its own slots' partners and
+    // keeps accept bits; (B) one ballot per (round, slot set) gives every
+    // accepted pair its queue position in round-major order, each lane
+    // writes its own pairs; (C) the queue is evaluated 32 entries at a time,
+    // the incomplete tail carried to the next block.
     A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false};
-    const int rounds = m >> 1;
+    const int rounds = debug_mode == 1 ? 0 : (m >> 1);  // debug 1: phases 0 and 3 only
     const int nsets = (m + 31) >> 5;
-    int qn = 0;
-    for (int d0 = 1; d0 <= rounds; d0 += kA3RoundBlock) {
-        const int dn = min(kA3RoundBlock, rounds - d0 + 1);
+    const int block = max(1, min(kA3RoundBlock, (kA3Queue - 32) / max(m, 1)));
+    int qn = 0;  // carried entries at the queue head
+    for (int d0 = 1; d0 <= rounds; d0 += block) {
+        const int dn = min(block, rounds - d0 + 1);
+        // (A) accept bits
         for (int sg = 0; sg < nsets; sg++) {
             const int s = (sg << 5) + lane;
             uint32_t bits = 0u;
             if (s < m) {
                 const float4 ps = sm.f4[s];
-                for (int e = 0; e < dn; e++) {
-                    const int d = d0 + e;
-                    if (2 * d == m && s >= d) break;  // even m: the half round, once
-                    int t = s + d;
-                    if (t >= m) t -= m;
+                const int elim = (2 * (d0 + dn - 1) == m && s >= d0 + dn - 1) ? dn - 1 : dn;
+                int t = s + d0;
+                if (t >= m) t -= m;
+                for (int e = 0; e < elim; e++) {
                     if (a3_accept<kExactImage>(sm, ps, s, t, im, row, pr, rc2, rc2_lo, rc2_hi,
                                                rc2f_lo, rc2f_hi))
                         bits |= 1u << e;
+                    if (++t == m) t = 0;
                 }
-                sm.mask[s] = bits;
             }
+            if (s < m) sm.mask[s] = bits;
+            if (debug_mode == 2) continue;
+            // (B1) ballots per round of this set -> counts
+            for (int e = 0; e < dn; e++) {
+                const unsigned b = __ballot_sync(0xffffffffu, (bits >> e) & 1u);
+                if (lane == 0) sm.vote[e * nsets + sg] = b;
+            }
+        }
+        if (debug_mode == 2) continue;  // debug 2: accept bits only
+        __syncwarp();
+        // (B2) round-major offsets: vbase[e*nsets+sg] = exclusive prefix of the
+        // vote counts (warp scan), then every lane places its own pairs
+        const int nv = dn * nsets;
+        int carry = qn;
+        for (int v0 = 0; v0 < nv; v0 += 32) {
+            const int c = v0 + lane < nv ? __popc(sm.vote[v0 + lane]) : 0;
+            int incl = c;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            if (v0 + lane < nv) sm.vbase[v0 + lane] = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
         __syncwarp();
-        for (int e = 0; e < dn; e++) {
-            const int d = d0 + e;
-            for (int sg = 0; sg < nsets; sg++) {
-                const int s = (sg << 5) + lane;
-                const bool accept = s < m && ((sm.mask[s] >> e) & 1u);
-                const unsigned ma = __ballot_sync(0xffffffffu, accept);
-                if (accept) {
-                    int t = s + d;
-                    if (t >= m) t -= m;
-                    const int slot = qn + __popc(ma & lanemask_lt());
-                    sm.qst[slot] = (uint32_t)s | ((uint32_t)t << 16);
-                    sm.qrec[slot] = d;
-                }
-                qn += __popc(ma);
-                if (qn >= 32) {
-                    __syncwarp();
-                    a3_chunk<kExactImage>(sm, 32, lane, im, row, pr, acc);
-                    __syncwarp();
-                    if (lane < qn - 32) {
-                        sm.qst[lane] = sm.qst[lane + 32];
-                        sm.qrec[lane] = sm.qrec[lane + 32];
-                    }
-                    __syncwarp();
-                    qn -= 32;
-                }
+        for (int sg = 0; sg < nsets; sg++) {
+            const int s = (sg << 5) + lane;
+            uint32_t bits = s < m ? sm.mask[s] : 0u;
+            while (bits) {
+                const int e = __ffs(bits) - 1;
+                bits &= bits - 1u;
+                const int v = e * nsets + sg;
+                const int pos = sm.vbase[v] + __popc(sm.vote[v] & lanemask_lt());
+                int t = s + d0 + e;
+                if (t >= m) t -= m;
+                sm.qe[pos] = (uint32_t)s | ((uint32_t)t << 11) | ((uint32_t)((d0 + e) & 1023) << 22);
             }
         }
+        qn = carry;
+        __syncwarp();
+        // (C) full chunks
+        int done = 0;
+        for (; done + 32 <= qn; done += 32) {
+            if (debug_mode != 3)
+                a3_chunk<kExactImage>(sm, 32, lane, im, row, pr, acc, debug_mode, done);
+        }
+        __syncwarp();
+        if (done > 0 && lane < qn - done) sm.qe[lane] = sm.qe[done + lane];
+        qn -= done;
         __syncwarp();
     }
-    if (qn > 0) a3_chunk<kExactImage>(sm, qn, lane, im, row, pr, acc);
+    if (qn > 0 && debug_mode != 3 && debug_mode != 2)
+        a3_chunk<kExactImage>(sm, qn, lane, im, row, pr, acc, debug_mode, 0);
     __syncwarp();
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
     for (int sl = lane; sl < m; sl += 32) {
         const int k = sm.kidx[sl];
         const double2 xy = sm.axy[sl];
-        grow[3 * k] = xy.x;
-        grow[3 * k + 1] = xy.y;
-        grow[3 * k + 2] = sm.az[sl];
+        double *gq = gbuf + ((int64_t)row[k] * capacity + mir[k]) * 3;
+        gq[0] = xy.x;
+        gq[1] = xy.y;
+        gq[2] = sm.az[sl];
     }
     const double fx = group_sum<32>(acc.fx);
     const double fy = group_sum<32>(acc.fy);
@@ -379,8 +424,9 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     }
 }
 
-// F(p) = 2 nu * (own(p) + sum over row entries q < p of G[q][mirror]); the
-// row prefix q < p is walked in order by kG lanes, then a fixed xor tree.
+// F(p) = 2 nu * (own(p) + sum over row entries k of p with q = row[k] < p of
+// G[p][k]); the row prefix is walked in order by kG lanes, then a fixed xor
+// tree.
 constexpr int kGatherGroup = 8;
 
 __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
@@ -401,14 +447,12 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
     if (active) {
         const int m = row_count[p];
         const int32_t *row = rows + p * (int64_t)capacity;
-        const int32_t *mir = mirror + p * (int64_t)capacity;
+        const double *gp = gbuf + p * (int64_t)capacity * 3;
         for (int k = sub; k < m; k += kGatherGroup) {
-            const int q = row[k];
-            if (q >= p) break;  // rows are rank-sorted: the prefix q < p
-            const double *gq = gbuf + ((int64_t)q * capacity + mir[k]) * 3;
-            fx += gq[0];
-            fy += gq[1];
-            fz += gq[2];
+            if (row[k] >= p) break;  // rows are rank-sorted: the prefix q < p
+            fx += gp[3 * k];
+            fy += gp[3 * k + 1];
+            fz += gp[3 * k + 2];
         }
     }
     fx = group_sum<kGatherGroup>(fx);
@@ -451,9 +495,11 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
                            void *stream) {
     if (!g || n < 0 || capacity <= 0 || capacity > 4096 || !mirror || !scratch) return RB_ERR_ARGUMENT;
     if (slot_capacity <= 0 || slot_capacity > capacity) slot_capacity = capacity;
+    if (slot_capacity > kA3MaxSlots) return RB_ERR_CAPACITY;
     if (scratch_bytes < rb_atm_scratch_bytes(n, capacity)) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     const double rc2 = rc * rc;
+    static const int debug_mode = getenv("RB_ATM_DEBUG") ? atoi(getenv("RB_ATM_DEBUG")) : 0;
     bool exact_image = false;
     if (g->periodic)
         for (int d = 0; d < 3; d++)
@@ -469,20 +515,20 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
     double *gbuf = own + 3 * n;
     if (exact_image) {
         a3_grant(k_atm3<true>, smem, g_a3_granted[0]);
-        k_atm3<true><<<blocks, warps * 32, smem, st>>>(*g, n, pos_r, rows, row_count,
+        k_atm3<true><<<blocks, warps * 32, smem, st>>>(*g, n, pos_r, rows, row_count, mirror,
                                                         capacity, slot_capacity, rc2, rc2, rc2,
                                                         (float)(rc2 * (1.0 - kA3Band)),
                                                         (float)(rc2 * (1.0 + kA3Band)), own, gbuf,
                                                         energy_rank, virial_rank, triplets_rank,
-                                                        status, tag);
+                                                        status, tag, debug_mode);
         note_launches(1);
     } else {
         a3_grant(k_atm3<false>, smem, g_a3_granted[1]);
         k_atm3<false><<<blocks, warps * 32, smem, st>>>(
-            *g, n, pos_r, rows, row_count, capacity, slot_capacity, rc2,
+            *g, n, pos_r, rows, row_count, mirror, capacity, slot_capacity, rc2,
             rc2 * (1.0 - kA3Margin), rc2 * (1.0 + kA3Margin), (float)(rc2 * (1.0 - kA3Band)),
             (float)(rc2 * (1.0 + kA3Band)), own, gbuf, energy_rank, virial_rank, triplets_rank,
-            status, tag);
+            status, tag, debug_mode);
         note_launches(1);
     }
     const int tb = 256;

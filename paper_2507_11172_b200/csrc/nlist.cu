@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
     }
 }
 
-// mirror[p][k] = position of p in the row of q = rows[p][k], for q < p
-// (binary search: rows are sorted by rank); -1 for q > p.
+// mirror[p][k] = position of p in the row of q = rows[p][k] (binary search:
+// rows are sorted by rank; the relation is symmetric, so it is found).
 __global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
                          const int32_t *__restrict__ row_count, int32_t capacity,
                          int32_t *__restrict__ mirror, const int64_t *flag,
@@ -123,7 +123,7 @@ __global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
     if (k >= m) return;
     const int q = rows[p * (int64_t)capacity + k];
     int res = -1;
-    if (q < p) {
+    {
         const int32_t *rq = rows + (int64_t)q * capacity;
         int lo = 0, hi = row_count[q] - 1;
         while (lo <= hi) {

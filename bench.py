@@ -252,7 +252,7 @@ def ours_arm(args, cfg):
     eng, geom = run.eng, run._geom()
     eng.bin(geom, run.x)
     eng.nlist(geom, run.r_build, capacity=run.capacity, checked=True)
-    eng.slots = run.capacity
+    eng.slots = run.slots
     f3 = torch.empty_like(run.f3)
     eng.reset_status(0)
     eng.atm(geom, run.rc3, run.nu, f3, tag=0, count_visits=True)

@@ -47,24 +47,28 @@ __global__ void k_bin_zero(int64_t ncell, int32_t *__restrict__ count, const int
 __global__ void k_bin_count(rb_grid g, int64_t n, const double *__restrict__ pos,
                             int32_t *__restrict__ cell_of, int32_t *__restrict__ count,
                             const int64_t *flag, const unsigned long long *status, int64_t tag) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || gate_closed(flag, status, tag)) return;
-    double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
-    int cx = cell_index_1d(x, g.origin[0], g.inv_cell[0], g.cells[0]);
-    int cy = cell_index_1d(y, g.origin[1], g.inv_cell[1], g.cells[1]);
-    int cz = cell_index_1d(z, g.origin[2], g.inv_cell[2], g.cells[2]);
-    int c = (cx * g.cells[1] + cy) * g.cells[2] + cz;
-    cell_of[i] = c;
-    atomicAdd(&count[c], 1);
+    if (gate_closed(flag, status, tag)) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+        int cx = cell_index_1d(x, g.origin[0], g.inv_cell[0], g.cells[0]);
+        int cy = cell_index_1d(y, g.origin[1], g.inv_cell[1], g.cells[1]);
+        int cz = cell_index_1d(z, g.origin[2], g.inv_cell[2], g.cells[2]);
+        int c = (cx * g.cells[1] + cy) * g.cells[2] + cz;
+        cell_of[i] = c;
+        atomicAdd(&count[c], 1);
+    }
 }
 
 __global__ void k_bin_scatter(int64_t n, const int32_t *__restrict__ cell_of,
                               int32_t *__restrict__ cursor, int32_t *__restrict__ parts,
                               const int64_t *flag, const unsigned long long *status, int64_t tag) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || gate_closed(flag, status, tag)) return;
-    int slot = atomicAdd(&cursor[cell_of[i]], 1);
-    parts[slot] = (int32_t)i;
+    if (gate_closed(flag, status, tag)) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int slot = atomicAdd(&cursor[cell_of[i]], 1);
+        parts[slot] = (int32_t)i;
+    }
 }
 
 // One warp per cell: restore ascending particle order inside the cell (the
@@ -81,8 +85,9 @@ __global__ void __launch_bounds__(kFinishWarps * 32)
                   double *__restrict__ x_ref, const int64_t *flag,
                   const unsigned long long *status, int64_t tag) {
     const int lane = threadIdx.x & 31;
-    const int64_t c = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5);
-    if (c >= ncell || gate_closed(flag, status, tag)) return;
+    if (gate_closed(flag, status, tag)) return;
+    for (int64_t c = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5); c < ncell;
+         c += (int64_t)gridDim.x * kFinishWarps) {
     const int b = start[c], e = start[c + 1], k = e - b;
     if (k <= 32) {
         const int v = lane < k ? parts[b + lane] : 0x7fffffff;
@@ -115,6 +120,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32)
             x_ref[3 * p + 1] = y;
             x_ref[3 * p + 2] = z;
         }
+    }
     }
 }
 
@@ -252,11 +258,13 @@ extern "C" int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *c
     int64_t ntiles = ceil_div(ncell, kScanTile);
     const int64_t *fl = rebuild_flag;
     const int tb = 256;
+    // gated launches use capped grid-stride grids so a closed gate is cheap
+    auto cap = [&](int64_t b) { return (unsigned)(fl && b > 148 * 8 ? 148 * 8 : b); };
     k_bin_zero<<<(unsigned)std::min<int64_t>(ceil_div(ncell, tb), 148 * 8), tb, 0, st>>>(
         ncell, count, fl, status, tag);
     note_launches(1);
     if (n > 0) {
-        k_bin_count<<<(unsigned)ceil_div(n, tb), tb, 0, st>>>(*g, n, pos, cell_of, count, fl,
+        k_bin_count<<<cap(ceil_div(n, tb)), tb, 0, st>>>(*g, n, pos, cell_of, count, fl,
                                                                status, tag);
         note_launches(1);
     }
@@ -269,10 +277,10 @@ extern "C" int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *c
                                                              cursor, fl, status, tag);
     note_launches(1);
     if (n > 0) {
-        k_bin_scatter<<<(unsigned)ceil_div(n, tb), tb, 0, st>>>(n, cell_of, cursor,
+        k_bin_scatter<<<cap(ceil_div(n, tb)), tb, 0, st>>>(n, cell_of, cursor,
                                                                  cell_particles, fl, status, tag);
         note_launches(1);
-        k_cell_finish<<<(unsigned)ceil_div(ncell, kFinishWarps), kFinishWarps * 32, 0, st>>>(
+        k_cell_finish<<<cap(ceil_div(ncell, kFinishWarps)), kFinishWarps * 32, 0, st>>>(
             ncell, cell_start, cell_particles, cell_of_rank, rank_of, pos, pos_r, x_ref, fl,
             status, tag);
         note_launches(1);

@@ -17,16 +17,11 @@ namespace rb {
 
 constexpr int kNlistWarps = 8;
 
-__global__ void __launch_bounds__(kNlistWarps * 32)
-    k_nlist(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ cell_start,
+__device__ __forceinline__ void nlist_one(const rb_grid &g, int64_t r, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ cell_start,
             const int32_t *__restrict__ cell_of_rank, double rl2, int32_t capacity,
             int32_t *__restrict__ rows, int32_t *__restrict__ row_count,
-            int32_t *__restrict__ max_count, const int64_t *flag,
-            const unsigned long long *status, int64_t tag) {
+            int32_t *__restrict__ max_count) {
     const int lane = threadIdx.x & 31;
-    const int64_t r = (int64_t)blockIdx.x * kNlistWarps + (threadIdx.x >> 5);
-    if (r >= n) return;
-    if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
     const Image im = make_image(g);
     const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
     const int cb = cell_of_rank[r];
@@ -108,19 +103,34 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
     }
 }
 
+// grid-stride over particles (one warp each); a closed rebuild gate makes
+// every block exit after one load, so the launch costs a few microseconds
+__global__ void __launch_bounds__(kNlistWarps * 32)
+    k_nlist(rb_grid g, int64_t n, const double *__restrict__ pr,
+            const int32_t *__restrict__ cell_start, const int32_t *__restrict__ cell_of_rank,
+            double rl2, int32_t capacity, int32_t *__restrict__ rows,
+            int32_t *__restrict__ row_count, int32_t *__restrict__ max_count,
+            const int64_t *flag, const unsigned long long *status, int64_t tag) {
+    if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
+    for (int64_t r = (int64_t)blockIdx.x * kNlistWarps + (threadIdx.x >> 5); r < n;
+         r += (int64_t)gridDim.x * kNlistWarps)
+        nlist_one(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows, row_count,
+                  max_count);
+}
+
 // mirror[p][k] = position of p in the row of q = rows[p][k] (binary search:
 // rows are sorted by rank; the relation is symmetric, so it is found).
 __global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
                          const int32_t *__restrict__ row_count, int32_t capacity,
                          int32_t *__restrict__ mirror, const int64_t *flag,
                          const unsigned long long *status, int64_t tag) {
-    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
+    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < n * (int64_t)capacity;
+         gid += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = gid / capacity;
     const int k = (int)(gid % capacity);
-    if (p >= n) return;
-    if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
     const int m = row_count[p];
-    if (k >= m) return;
+    if (k >= m) continue;
     const int q = rows[p * (int64_t)capacity + k];
     int res = -1;
     {
@@ -138,6 +148,7 @@ __global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
         }
     }
     mirror[p * (int64_t)capacity + k] = res;
+    }
 }
 
 }  // namespace rb
@@ -152,8 +163,9 @@ extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const 
     if (g->n_offsets <= 0 || g->n_offsets > RB_MAX_OFFSETS) return RB_ERR_GEOMETRY;
     if (n == 0) return RB_OK;
     const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
-    unsigned blocks = (unsigned)((n + kNlistWarps - 1) / kNlistWarps);
-    k_nlist<<<blocks, kNlistWarps * 32, 0, as_stream(stream)>>>(
+    int64_t blocks = (n + kNlistWarps - 1) / kNlistWarps;
+    if (rebuild_flag && blocks > 148 * 8) blocks = 148 * 8;  // gated: grid-stride
+    k_nlist<<<(unsigned)blocks, kNlistWarps * 32, 0, as_stream(stream)>>>(
         *g, n, pos_r, cell_start, cell_of_rank, rl2, capacity, rows, row_count, max_count,
         rebuild_flag, status, tag);
     note_launches(1);
@@ -167,7 +179,9 @@ extern "C" int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *ro
     if (n == 0) return RB_OK;
     const int64_t threads = n * (int64_t)capacity;
     const int tb = 256;
-    k_mirror<<<(unsigned)((threads + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
+    int64_t mblocks = (threads + tb - 1) / tb;
+    if (mblocks > 148 * 16) mblocks = 148 * 16;  // grid-stride
+    k_mirror<<<(unsigned)mblocks, tb, 0, as_stream(stream)>>>(
         n, rows, row_count, capacity, mirror, rebuild_flag, status, tag);
     note_launches(1);
     return launch_status();

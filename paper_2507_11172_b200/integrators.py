@@ -258,16 +258,24 @@ class DeviceRespa:
         self.v.copy_(torch.from_numpy(np.ascontiguousarray(self.system.velocities, np.float64)))
         eng.reset_status(0)
         eng.rebuild_flag.zero_()  # tag 0 == forced build for the initial passes
-        if self.capacity is None:
+        if self.capacity is None or self.slots is None:
             geom = self._geom()
             eng.bin(geom, self.x)
+            # rows (at r_list + skin) and the triplet pass's shared-memory slots
+            # (at most the neighbours within the three-body cutoff) are sized
+            # from the initial configuration with margin; an overflow later is
+            # detected on the device and the run is repeated larger
+            if self.with_3b:
+                eng.nlist(geom, self.rc3, capacity=None, checked=True)
+                within = int(eng.max_count.item())
             eng.nlist(geom, self.r_build, capacity=None, checked=True)
             longest = int(eng.max_count.item())
-            # rows and triplet slots sized from the initial longest row with margin;
-            # an overflow later is detected and the run is repeated larger
-            self.capacity = min(4096, _round_up(int(longest * 1.3) + 16, 32))
+            if self.capacity is None:
+                self.capacity = min(4096, _round_up(int(longest * 1.3) + 16, 32))
+            if self.slots is None:
+                self.slots = self.capacity if not self.with_3b else min(
+                    self.capacity, _round_up(int(within * 1.25) + 8, 32))
         eng.max_count.zero_()
-        self.slots = self.capacity  # S+(i) can be a whole row
         eng.slots = self.slots
         self._forces(0, True, self.f2_old)
         self._record()
@@ -342,13 +350,16 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
     hooks = tuple(hooks)
     x0 = np.array(system.positions, copy=True)
     v0 = np.array(system.velocities, copy=True)
+    slots = None
     for attempt in range(3):
         run = DeviceRespa(system, ff, container, schedule, sample_interval, capacity=capacity,
                           use_graph=use_graph and not hooks, skin=skin)
+        run.slots = slots
         try:
             return _drive(run, hooks)
         except CapacityError:
             capacity = min(4096, _round_up(int(run.capacity * 1.5) + 32, 32))
+            slots = capacity
             system.positions[:] = x0
             system.velocities[:] = v0
     raise CapacityError("neighbour rows kept overflowing")

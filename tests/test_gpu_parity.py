@@ -316,6 +316,18 @@ def test_verlet_skin_rows_match_rebuild_every_step(pkg):
     assert max(_rel(x, y) for x, y in zip(ta.total, tb.total)) <= 1e-10
 
 
+def test_row_capacity_overflow_is_detected_and_retried(pkg):
+    """A deliberately small row capacity overflows on the device; the run is
+    repeated with larger rows and gives the normal trajectory."""
+    base = pkg.systems.fcc_system(6, temperature=0.9, seed=12, vseed=13)
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5)
+    a, b = base.copy(), base.copy()
+    ta = pkg.respa_run(a, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, 5, 20), capacity=32)
+    tb = pkg.respa_run(b, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.001, 5, 20))
+    assert np.max(np.abs(a.positions - b.positions)) <= 1e-12
+    assert max(_rel(x, y) for x, y in zip(ta.total, tb.total)) <= 1e-12
+
+
 def test_s1_is_verlet_and_zero_nu_independent_of_s(pkg):
     base = pkg.systems.fcc_system(5, temperature=1.0, seed=2, vseed=3)
     ff = pkg.ForceField(nu=0.4, cutoff=2.5)

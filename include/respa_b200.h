@@ -67,13 +67,22 @@ extern "C" {
  * respamd/containers.py:244-263 does (cells = max(1, floor(extent/cutoff)),
  * size = extent/cells, inv_cell = 1.0/size) so that binning is bit-exact. */
 typedef struct rb_grid {
-    int32_t cells[3];   /* cells per dimension */
+    int32_t cells[3];   /* cells per dimension (local cells when windowed) */
     int32_t periodic;   /* 1: periodic box with single-shift minimum image */
     double origin[3];   /* 0 for periodic systems */
     double inv_cell[3]; /* 1.0 / cell_size */
     double box[3];
     int32_t n_offsets;                   /* canonical neighbour-cell offsets */
     int32_t offsets[RB_MAX_OFFSETS][3];  /* containers.py:133-144 (pair_cells) */
+    /* Domain decomposition (rb_grid_window): per dimension, wrap[d] = 1 when
+     * neighbour-cell indices wrap (whole periodic dimension), 0 when the
+     * local grid is a window [wlo, wlo + cells) of the global periodic grid
+     * of gcells cells (a rank's block plus one halo layer); binning maps the
+     * global cell index into the window.  Distances always use the periodic
+     * minimum image of the whole box, so predicates stay bit-exact. */
+    int32_t wrap[3];
+    int32_t gcells[3];
+    int32_t wlo[3];
 } rb_grid;
 
 RB_API int rb_abi_version(void);
@@ -118,12 +127,13 @@ RB_API int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const int3
 /* ---- LJ pair pass: replaces _c01_pair_kernel (containers.py:282-370) ---
  * Owner-computes over the neighbour rows with the inclusive cutoff `rc`;
  * writes forces (n,3) in particle order (overwritten), and per-rank energy
- * (sum of phi/2) and virial (sum of scale*r^2/2). */
+ * (sum of phi/2) and virial (sum of scale*r^2/2).  `owned` (rank-indexed,
+ * NULL = all) zeroes the energy/virial of ghost particles in decomposed runs. */
 RB_API int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r,
                const int32_t *cell_particles, const int32_t *rows, const int32_t *row_count,
                int32_t capacity, double rc, double epsilon, double sigma, double *forces,
-               double *energy_rank, double *virial_rank, unsigned long long *status, int64_t tag,
-               void *stream);
+               double *energy_rank, double *virial_rank, const uint8_t *owned,
+               unsigned long long *status, int64_t tag, void *stream);
 
 /* Mirror indices of the (rank-sorted) rows: mirror[p*capacity + k] is the
  * position of p in the row of q = rows[p*capacity + k].  The Newton-3
@@ -141,14 +151,18 @@ RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_co
  * number of owned (unique) triplets.  Scratch: rb_atm_scratch_bytes.
  * slot_capacity (<= capacity) sizes the per-warp shared-memory slots; a
  * particle with more higher-rank neighbours than that records
- * RB_KIND_CAPACITY in the status word (pass the longest row length). */
+ * RB_KIND_CAPACITY in the status word (pass the longest row length).
+ * `owned` (rank-indexed, NULL = all): in decomposed runs a triplet's
+ * energy/virial is weighted by (owned members)/3, the reference's phi/3 per
+ * member; forces on ghosts are computed and left to the caller to drop. */
 RB_API size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity);
-RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
+RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r,
+                       const int32_t *cell_particles, const int32_t *rows,
                        const int32_t *row_count, const int32_t *mirror, int32_t capacity,
-                       int32_t slot_capacity, double rc, double nu, double *forces, double *energy_rank,
-                       double *virial_rank, int32_t *triplets_rank, void *scratch,
-                       size_t scratch_bytes, unsigned long long *status, int64_t tag,
-                       void *stream);
+                       int32_t slot_capacity, double rc, double nu, double *forces,
+                       double *energy_rank, double *virial_rank, int32_t *triplets_rank,
+                       const uint8_t *owned, void *scratch, size_t scratch_bytes,
+                       unsigned long long *status, int64_t tag, void *stream);
 
 /* C01 (owner-computes) form of the same pass, as the reference traverses it:
  * every triplet visited once from each member, force stored on the base

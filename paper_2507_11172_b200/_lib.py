@@ -48,6 +48,9 @@ class RbGrid(ctypes.Structure):
         ("box", _D * 3),
         ("n_offsets", _I32),
         ("offsets", (_I32 * 3) * RB_MAX_OFFSETS),
+        ("wrap", _I32 * 3),
+        ("gcells", _I32 * 3),
+        ("wlo", _I32 * 3),
     ]
 
 
@@ -62,11 +65,11 @@ SIGNATURES = {
     "rb_bin": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _SZ, _P]),
     "rb_nlist": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _D, _I32, _P, _P, _P, _P, _P, _I64, _P]),
     "rb_nlist_mirror": (ctypes.c_int, [_I64, _P, _P, _I32, _P, _P, _P, _I64, _P]),
-    "rb_lj_pass": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _D, _D, _P, _P, _P, _P, _I64,
-                                  _P]),
+    "rb_lj_pass": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _D, _D, _P, _P, _P, _P,
+                                  _P, _I64, _P]),
     "rb_atm_scratch_bytes": (_SZ, [_I64, _I32]),
     "rb_atm_pass": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _I32, _I32, _D, _D, _P, _P, _P, _P,
-                                   _P, _SZ, _P, _I64, _P]),
+                                   _P, _P, _SZ, _P, _I64, _P]),
     "rb_atm_pass_c01": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _D, _P, _P, _P, _P, _P,
                                        _I64, _P]),
     "rb_atm_visit_rows": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _P, _P, _P]),

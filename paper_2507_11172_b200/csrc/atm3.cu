@@ -55,7 +55,7 @@ struct A3Smem {
     double2 *axy;    // slot force accumulators (units of 2 nu), x and y
     double *az;      //   ... z
     float4 *f4;      // slots: d_ij in fp32 for the candidate filter
-    int32_t *kidx;   // slot -> row index
+    int32_t *kidx;   // slot -> row index | owned << 30
     uint32_t *mask;  // slot -> accept bits of the current round block
     uint32_t *vote;  // per round of the block: the ballot of each slot set
     int32_t *vbase;  // per round of the block: queue offset of each slot set
@@ -90,7 +90,16 @@ struct A3Acc {
     double fx, fy, fz, e, w;
     int n;
     bool bad;
+    int owned_i;  // decomposed runs: the base particle is owned by this rank
 };
+
+constexpr int kKidxMask = 0x3fffffff;
+
+// share of a triplet's energy that belongs to this rank: (owned members)/3
+// (the reference attributes phi/3 to each member, containers.py:524)
+__device__ __forceinline__ double owned_share(int n_owned) {
+    return n_owned == 3 ? 1.0 : (n_owned == 2 ? 2.0 / 3.0 : (n_owned == 1 ? 1.0 / 3.0 : 0.0));
+}
 
 // 1/sqrt(x) from an fp32 seed and two Newton steps (2^-23 -> 2^-46 ->
 // rounding); CUDA's rsqrt for the rare arguments outside the fp32 range.
@@ -125,7 +134,7 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
     double c;
     if (kExactImage) {
         // the reference's raw-position minimum image (containers.py:497-513)
-        const int j = row[sm.kidx[s]], k = row[sm.kidx[t]];
+        const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
         exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
                    pr[3 * k + 2], jkx, jky, jkz);
         c = exact_r2(jkx, jky, jkz);
@@ -160,8 +169,10 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
     acc.fx = fma(-ea, ij.x, fma(-eb, ik.x, acc.fx));
     acc.fy = fma(-ea, ij.y, fma(-eb, ik.y, acc.fy));
     acc.fz = fma(-ea, ijz, fma(-eb, ikz, acc.fz));
-    acc.e = fma(s52, fma(0.375, p, sp), acc.e);
-    acc.w = fma(ea, a, fma(eb, b, fma(ec, c, acc.w)));
+    const double share =
+        owned_share(acc.owned_i + (sm.kidx[s] >> 30) + (sm.kidx[t] >> 30));
+    acc.e = fma(share * s52, fma(0.375, p, sp), acc.e);
+    acc.w = fma(share, fma(ea, a, fma(eb, b, ec * c)), acc.w);
     acc.n += 1;
     fj[0] = fma(ea, ij.x, -ec * jkx);
     fj[1] = fma(ea, ij.y, -ec * jky);
@@ -223,7 +234,7 @@ __device__ __forceinline__ bool a3_accept(const A3Smem &sm, const float4 &ps, in
                                           float rc2f_hi) {
     if (kExactImage) {
         // box under four cutoffs: d_ik - d_ij need not be the minimum image
-        const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
+        const int jr = row[sm.kidx[s] & kKidxMask], kr = row[sm.kidx[t] & kKidxMask];
         double dx, dy, dz;
         exact_disp(im, pr[3 * jr], pr[3 * jr + 1], pr[3 * jr + 2], pr[3 * kr], pr[3 * kr + 1],
                    pr[3 * kr + 2], dx, dy, dz);
@@ -239,7 +250,7 @@ __device__ __forceinline__ bool a3_accept(const A3Smem &sm, const float4 &ps, in
     const double c2 = fma(ez2, ez2, fma(ey2, ey2, ex2 * ex2));
     if (c2 <= rc2_lo) return true;
     if (c2 > rc2_hi) return false;
-    const int jr = row[sm.kidx[s]], kr = row[sm.kidx[t]];
+    const int jr = row[sm.kidx[s] & kKidxMask], kr = row[sm.kidx[t] & kKidxMask];
     double dx, dy, dz;
     exact_disp(im, pr[3 * jr], pr[3 * jr + 1], pr[3 * jr + 2], pr[3 * kr], pr[3 * kr + 1],
                pr[3 * kr + 2], dx, dy, dz);
@@ -254,8 +265,8 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
            double rc2_lo, double rc2_hi, float rc2f_lo, float rc2f_hi,
            double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
-           int32_t *__restrict__ triplets_rank, unsigned long long *status, int64_t tag,
-           int debug_mode) {
+           int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
+           unsigned long long *status, int64_t tag, int debug_mode) {
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -302,7 +313,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
             sm.dxy[slot] = make_double2(dx, dy);
             sm.dz[slot] = dz;
             sm.r2[slot] = r2;
-            sm.kidx[slot] = k;
+            sm.kidx[slot] = k | ((owned ? (int)owned[row[k]] : 1) << 30);
             sm.f4[slot] = make_float4((float)dx, (float)dy, (float)dz, 0.0f);
             sm.axy[slot] = make_double2(0.0, 0.0);
             sm.az[slot] = 0.0;
@@ -318,7 +329,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     // accepted pair its queue position in round-major order, each lane
     // writes its own pairs; (C) the queue is evaluated 32 entries at a time,
     // the incomplete tail carried to the next block.
-    A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false};
+    A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false, owned ? (int)owned[r] : 1};
     const int rounds = debug_mode == 1 ? 0 : (m >> 1);  // debug 1: phases 0 and 3 only
     const int nsets = (m + 31) >> 5;
     const int block = max(1, min(kA3RoundBlock, (kA3Queue - 32) / max(m, 1)));
@@ -399,7 +410,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
     for (int sl = lane; sl < m; sl += 32) {
-        const int k = sm.kidx[sl];
+        const int k = sm.kidx[sl] & kKidxMask;
         const double2 xy = sm.axy[sl];
         double *gq = gbuf + ((int64_t)row[k] * capacity + mir[k]) * 3;
         gq[0] = xy.x;
@@ -490,9 +501,9 @@ extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
 extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                            const int32_t *row_count, const int32_t *mirror, int32_t capacity,
                            int32_t slot_capacity, double rc, double nu, double *forces, double *energy_rank,
-                           double *virial_rank, int32_t *triplets_rank, void *scratch,
-                           size_t scratch_bytes, unsigned long long *status, int64_t tag,
-                           void *stream) {
+                           double *virial_rank, int32_t *triplets_rank, const uint8_t *owned,
+                           void *scratch, size_t scratch_bytes, unsigned long long *status,
+                           int64_t tag, void *stream) {
     if (!g || n < 0 || capacity <= 0 || capacity > 4096 || !mirror || !scratch) return RB_ERR_ARGUMENT;
     if (slot_capacity <= 0 || slot_capacity > capacity) slot_capacity = capacity;
     if (slot_capacity > kA3MaxSlots) return RB_ERR_CAPACITY;
@@ -520,7 +531,7 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
                                                         (float)(rc2 * (1.0 - kA3Band)),
                                                         (float)(rc2 * (1.0 + kA3Band)), own, gbuf,
                                                         energy_rank, virial_rank, triplets_rank,
-                                                        status, tag, debug_mode);
+                                                        owned, status, tag, debug_mode);
         note_launches(1);
     } else {
         a3_grant(k_atm3<false>, smem, g_a3_granted[1]);
@@ -528,7 +539,7 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
             *g, n, pos_r, rows, row_count, mirror, capacity, slot_capacity, rc2,
             rc2 * (1.0 - kA3Margin), rc2 * (1.0 + kA3Margin), (float)(rc2 * (1.0 - kA3Band)),
             (float)(rc2 * (1.0 + kA3Band)), own, gbuf, energy_rank, virial_rank, triplets_rank,
-            status, tag, debug_mode);
+            owned, status, tag, debug_mode);
         note_launches(1);
     }
     const int tb = 256;

@@ -27,6 +27,16 @@ __device__ __forceinline__ int cell_index_1d(double x, double origin, double inv
     return (int)c;
 }
 
+// cell of a coordinate in dimension d: the global index, mapped into the
+// rank's window when the grid is a window of a decomposed periodic grid
+__device__ __forceinline__ int cell_index(const rb_grid &g, int d, double x) {
+    if (g.wrap[d] || !g.periodic) return cell_index_1d(x, g.origin[d], g.inv_cell[d], g.cells[d]);
+    int c = cell_index_1d(x, g.origin[d], g.inv_cell[d], g.gcells[d]) - g.wlo[d];
+    if (c < 0) c += g.gcells[d];
+    if (c >= g.gcells[d]) c -= g.gcells[d];
+    return c < g.cells[d] ? c : g.cells[d] - 1;  // outside the window: caller's error
+}
+
 // Rebuild gate: a binning launched inside a captured r-RESPA step runs only
 // when the drift of that step flagged a rebuild (*flag == tag); flag == NULL
 // means always (standalone passes).
@@ -51,9 +61,9 @@ __global__ void k_bin_count(rb_grid g, int64_t n, const double *__restrict__ pos
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
-        int cx = cell_index_1d(x, g.origin[0], g.inv_cell[0], g.cells[0]);
-        int cy = cell_index_1d(y, g.origin[1], g.inv_cell[1], g.cells[1]);
-        int cz = cell_index_1d(z, g.origin[2], g.inv_cell[2], g.cells[2]);
+        int cx = cell_index(g, 0, x);
+        int cy = cell_index(g, 1, y);
+        int cz = cell_index(g, 2, z);
         int c = (cx * g.cells[1] + cy) * g.cells[2] + cz;
         cell_of[i] = c;
         atomicAdd(&count[c], 1);

@@ -137,19 +137,19 @@ __device__ __forceinline__ int group_sum_int(int v) {
 // neighbour cell of base cell (cx,cy,cz) at offset o; -1 when outside an
 // open grid (respamd/containers.py:319-333)
 __device__ __forceinline__ int neighbor_cell(const rb_grid &g, int cx, int cy, int cz, int o) {
-    int x = cx + g.offsets[o][0];
-    int y = cy + g.offsets[o][1];
-    int z = cz + g.offsets[o][2];
-    if (g.periodic) {
-        // canonical offsets are already wrapped into [0, cells)
-        if (x >= g.cells[0]) x -= g.cells[0];
-        if (y >= g.cells[1]) y -= g.cells[1];
-        if (z >= g.cells[2]) z -= g.cells[2];
-    } else if (x < 0 || x >= g.cells[0] || y < 0 || y >= g.cells[1] || z < 0 ||
-               z >= g.cells[2]) {
-        return -1;
+    int c[3];
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+        int x = (d == 0 ? cx : (d == 1 ? cy : cz)) + g.offsets[o][d];
+        if (g.wrap[d]) {
+            // canonical offsets are already wrapped into [0, cells)
+            if (x >= g.cells[d]) x -= g.cells[d];
+        } else if (x < 0 || x >= g.cells[d]) {
+            return -1;
+        }
+        c[d] = x;
     }
-    return (x * g.cells[1] + y) * g.cells[2] + z;
+    return (c[0] * g.cells[1] + c[1]) * g.cells[2] + c[2];
 }
 
 }  // namespace rb

@@ -22,7 +22,8 @@ __global__ void __launch_bounds__(kLjThreads)
          const int32_t *__restrict__ rows, const int32_t *__restrict__ row_count,
          int32_t capacity, double rc2, double eps24, double eps4, double sigma2,
          double *__restrict__ forces, double *__restrict__ energy_rank,
-         double *__restrict__ virial_rank, unsigned long long *status, int64_t tag) {
+         double *__restrict__ virial_rank, const uint8_t *__restrict__ owned,
+         unsigned long long *status, int64_t tag) {
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t r = gid / kLjGroup;
     const int sub = (int)(gid % kLjGroup);
@@ -69,8 +70,10 @@ __global__ void __launch_bounds__(kLjThreads)
         forces[3 * p] = fx;
         forces[3 * p + 1] = fy;
         forces[3 * p + 2] = fz;
-        energy_rank[r] = 0.5 * e;
-        virial_rank[r] = 0.5 * w;
+        // decomposed runs: only owned particles carry energy (phi/2 per visit)
+        const double own = owned ? (double)owned[r] : 1.0;
+        energy_rank[r] = own * (0.5 * e);
+        virial_rank[r] = own * (0.5 * w);
     }
 }
 
@@ -81,14 +84,15 @@ using namespace rb;
 extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                           const int32_t *row_count, int32_t capacity, double rc, double epsilon,
                           double sigma, double *forces, double *energy_rank, double *virial_rank,
-                          unsigned long long *status, int64_t tag, void *stream) {
+                          const uint8_t *owned, unsigned long long *status, int64_t tag,
+                          void *stream) {
     if (!g || n < 0 || capacity <= 0) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     const int64_t threads = n * kLjGroup;
     unsigned blocks = (unsigned)((threads + kLjThreads - 1) / kLjThreads);
     k_lj<<<blocks, kLjThreads, 0, as_stream(stream)>>>(
         *g, n, pos_r, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
-        4.0 * epsilon, sigma * sigma, forces, energy_rank, virial_rank, status, tag);
+        4.0 * epsilon, sigma * sigma, forces, energy_rank, virial_rank, owned, status, tag);
     note_launches(1);
     return launch_status();
 }

@@ -1,0 +1,298 @@
+"""Spatial domain decomposition of the periodic box over ranks.
+
+One process per GPU.  The global periodic cell grid (cells >= r_build, the
+row radius) is cut into a ``px x py x pz`` grid of blocks along cell
+boundaries; a rank owns the particles whose global cell lies in its block
+and keeps one halo layer of cells around it:
+
+* migration (at row rebuilds): particles whose cell left the block go to the
+  neighbouring rank, staged x -> y -> z so diagonal moves need no extra
+  messages;
+* ghosts (at row rebuilds): the first/last cell layer of the block is sent
+  to the -/+ neighbour, staged x -> y -> z with the ghosts of earlier stages
+  included, which fills edges and corners; the send lists are kept;
+* every step: the same lists carry the owners' new positions to the ghosts.
+
+Forces are owner-computes across ranks: every triplet/pair containing an
+owned particle has all its members in owned + ghosts (they are within the
+cutoff of that particle), so the local passes give complete forces on owned
+particles and no reverse communication is needed; ghost forces are dropped.
+Energies are attributed phi/2 per owned pair member and phi/3 per owned
+triplet member (the reference's C01 attribution, containers.py:364, :524),
+so per-rank partials sum to the global scalars; they are summed in rank
+order (deterministic).
+
+The exchange runs on torch.distributed point-to-point (NCCL between GPUs,
+gloo for the CPU tests) and is independent of the force backend, which is
+the sm_100a engine in production and a numpy reference in the tests.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from .grid import Geometry, WindowGeometry, geometry
+
+PAYLOAD = 13  # id, x(3), v(3), f2_old(3), f3(3)
+
+
+def auto_dims(world: int, cells) -> tuple:
+    """Rank grid: the factorisation of `world` with the most cubic blocks
+    among those leaving every split block at least one cell plus a halo."""
+    best, best_score = None, None
+    for px in range(1, world + 1):
+        if world % px:
+            continue
+        for py in range(1, world // px + 1):
+            if (world // px) % py:
+                continue
+            dims = (px, py, world // px // py)
+            ok = all(p == 1 or (c // p >= 1 and -(-c // p) + 2 <= c) for c, p in zip(cells, dims))
+            if not ok:
+                continue
+            blk = [c / p for c, p in zip(cells, dims)]
+            score = max(blk) / min(blk)
+            if best is None or score < best_score - 1e-12:
+                best, best_score = dims, score
+    if best is None:
+        raise ValueError(f"cannot decompose {cells} cells over {world} ranks")
+    return best
+
+
+@dataclass
+class Decomposition:
+    """Block geometry of one rank."""
+
+    box: np.ndarray
+    r_build: float
+    world: int
+    rank: int
+    dims: Optional[tuple] = None
+    geom: Geometry = field(init=False)
+
+    def __post_init__(self):
+        self.box = np.asarray(self.box, dtype=np.float64)
+        self.geom = geometry(self.box, None, self.r_build, True)
+        n = self.geom.cells
+        if self.dims is None:
+            self.dims = auto_dims(self.world, n)
+        self.dims = tuple(int(p) for p in self.dims)
+        if int(np.prod(self.dims)) != self.world:
+            raise ValueError(f"rank grid {self.dims} does not match world size {self.world}")
+        px, py, pz = self.dims
+        self.coord = (self.rank // (py * pz), (self.rank // pz) % py, self.rank % pz)
+        self.bounds = [np.array([k * n[d] // self.dims[d] for k in range(self.dims[d] + 1)])
+                       for d in range(3)]
+        self.lo = tuple(int(self.bounds[d][self.coord[d]]) for d in range(3))
+        self.hi = tuple(int(self.bounds[d][self.coord[d] + 1]) for d in range(3))
+        for d in range(3):
+            if self.dims[d] > 1 and (self.hi[d] - self.lo[d] < 1 or
+                                     self.hi[d] - self.lo[d] + 2 > n[d]):
+                raise ValueError(f"block {self.lo}-{self.hi} too thin for a halo in dim {d}")
+
+    # ----------------------------------------------------------- topology
+    def split(self, d: int) -> bool:
+        return self.dims[d] > 1
+
+    def neighbor(self, d: int, step: int) -> int:
+        c = list(self.coord)
+        c[d] = (c[d] + step) % self.dims[d]
+        return (c[0] * self.dims[1] + c[1]) * self.dims[2] + c[2]
+
+    def window(self) -> WindowGeometry:
+        n = self.geom.cells
+        lo, cells, wrap = [], [], []
+        for d in range(3):
+            if self.split(d):
+                lo.append((self.lo[d] - 1) % n[d])
+                cells.append(self.hi[d] - self.lo[d] + 2)
+                wrap.append(False)
+            else:
+                lo.append(0)
+                cells.append(n[d])
+                wrap.append(True)
+        return WindowGeometry(self.geom, tuple(lo), tuple(cells), tuple(wrap))
+
+    # ------------------------------------------------------- cell indices
+    def cells_of(self, pos: np.ndarray) -> np.ndarray:
+        """Global cell index per particle and dimension: the binning
+        arithmetic of containers.py:182-196 (truncation, clamp)."""
+        inv = np.asarray(self.geom.inv_cell)
+        n = np.asarray(self.geom.cells)
+        c = np.trunc(pos * inv[None, :]).astype(np.int64)
+        return np.clip(c, 0, n[None, :] - 1)
+
+    def block_of(self, cells: np.ndarray) -> np.ndarray:
+        """Block coordinate per particle and dimension."""
+        out = np.empty_like(cells)
+        for d in range(3):
+            out[:, d] = np.searchsorted(self.bounds[d], cells[:, d], side="right") - 1
+        return out
+
+    def owner_rank(self, pos: np.ndarray) -> np.ndarray:
+        b = self.block_of(self.cells_of(pos))
+        return (b[:, 0] * self.dims[1] + b[:, 1]) * self.dims[2] + b[:, 2]
+
+
+# ---------------------------------------------------------------------------
+# point-to-point exchange (torch.distributed; gloo or NCCL)
+# ---------------------------------------------------------------------------
+
+
+class Exchanger:
+    """Two-phase neighbour exchange along one dimension: phase 1 sends to the
+    - neighbour and receives from the + neighbour, phase 2 the reverse.  Works
+    for a two-rank ring (both neighbours the same rank)."""
+
+    def __init__(self, dist, device):
+        import torch
+
+        self.dist = dist
+        self.device = torch.device(device)
+        # gloo moves host tensors only: stage device tensors through the host
+        self.wire = (torch.device("cpu") if dist.get_backend() == "gloo" else self.device)
+
+    def _pair(self, send, dst, src, width, dtype):
+        import torch
+
+        dist = self.dist
+        send = send.to(self.wire)
+        n_send = torch.tensor([send.shape[0]], dtype=torch.int64, device=self.wire)
+        n_recv = torch.zeros(1, dtype=torch.int64, device=self.wire)
+        reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, n_send, dst),
+                                       dist.P2POp(dist.irecv, n_recv, src)])
+        for r in reqs:
+            r.wait()
+        recv = torch.empty((int(n_recv.item()), width), dtype=dtype, device=self.wire)
+        ops = []
+        if send.shape[0]:
+            ops.append(dist.P2POp(dist.isend, send.contiguous(), dst))
+        if recv.shape[0]:
+            ops.append(dist.P2POp(dist.irecv, recv, src))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        return recv.to(self.device)
+
+    def exchange(self, to_minus, to_plus, minus: int, plus: int):
+        """Returns (from_plus, from_minus)."""
+        width, dtype = to_minus.shape[1], to_minus.dtype
+        from_plus = self._pair(to_minus, minus, plus, width, dtype)
+        from_minus = self._pair(to_plus, plus, minus, width, dtype)
+        return from_plus, from_minus
+
+    def exchange_fixed(self, to_minus, to_plus, minus: int, plus: int, n_from_plus: int,
+                       n_from_minus: int):
+        """Same with known receive sizes (per-step ghost refresh: one round)."""
+        import torch
+
+        dist = self.dist
+        width, dtype = to_minus.shape[1], to_minus.dtype
+        from_plus = torch.empty((n_from_plus, width), dtype=dtype, device=self.wire)
+        from_minus = torch.empty((n_from_minus, width), dtype=dtype, device=self.wire)
+        for send, dst, recv, src in ((to_minus.to(self.wire), minus, from_plus, plus),
+                                     (to_plus.to(self.wire), plus, from_minus, minus)):
+            ops = []
+            if send.shape[0]:
+                ops.append(dist.P2POp(dist.isend, send.contiguous(), dst))
+            if recv.shape[0]:
+                ops.append(dist.P2POp(dist.irecv, recv, src))
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+        return from_plus.to(self.device), from_minus.to(self.device)
+
+
+# ---------------------------------------------------------------------------
+# migration and ghosts
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class GhostPlan:
+    """Send lists of the staged ghost exchange, replayed every step."""
+
+    stages: list  # per split dimension: (d, idx_to_minus, idx_to_plus, n_from_plus, n_from_minus)
+    n_owned: int
+    n_local: int
+
+
+def migrate(dec: Decomposition, ex: Exchanger, payload):
+    """Move owned particles whose cell left the block to their new owner.
+
+    `payload` is an (n, PAYLOAD) float64 tensor: id, x, v, f2_old, f3.
+    Staged x -> y -> z; a particle moves at most one block per rebuild
+    (the skin bounds the displacement)."""
+    import torch
+
+    for d in range(3):
+        if not dec.split(d):
+            continue
+        pos = payload[:, 1:4].cpu().numpy()
+        blk = dec.block_of(dec.cells_of(pos))[:, d]
+        me, p = dec.coord[d], dec.dims[d]
+        stay = blk == me
+        to_minus = (~stay) & (blk == (me - 1) % p)
+        to_plus = (~stay) & (~to_minus)
+        if np.any(to_plus & (blk != (me + 1) % p)):
+            raise RuntimeError("a particle moved more than one block between row rebuilds")
+        dev = payload.device
+        sel = lambda m: payload[torch.from_numpy(np.nonzero(m)[0]).to(dev)]  # noqa: E731
+        from_plus, from_minus = ex.exchange(sel(to_minus), sel(to_plus), dec.neighbor(d, -1),
+                                            dec.neighbor(d, +1))
+        payload = torch.cat([sel(stay), from_plus, from_minus], dim=0)
+    # deterministic local order: ascending global id
+    order = torch.argsort(payload[:, 0])
+    return payload[order]
+
+
+def build_ghosts(dec: Decomposition, ex: Exchanger, pos_owned):
+    """Staged ghost exchange; returns (local positions (owned first), plan)."""
+    import torch
+
+    n_own = int(pos_owned.shape[0])
+    local = pos_owned
+    stages = []
+    for d in range(3):
+        if not dec.split(d):
+            continue
+        cells = dec.cells_of(local.cpu().numpy())[:, d]
+        idx_m = np.nonzero(cells == dec.lo[d])[0]
+        idx_p = np.nonzero(cells == dec.hi[d] - 1)[0]
+        dev = local.device
+        tm = torch.from_numpy(idx_m).to(dev)
+        tp = torch.from_numpy(idx_p).to(dev)
+        from_plus, from_minus = ex.exchange(local[tm], local[tp], dec.neighbor(d, -1),
+                                            dec.neighbor(d, +1))
+        stages.append((d, tm, tp, int(from_plus.shape[0]), int(from_minus.shape[0])))
+        local = torch.cat([local, from_plus, from_minus], dim=0)
+    return local, GhostPlan(stages, n_own, int(local.shape[0]))
+
+
+def refresh_ghosts(dec: Decomposition, ex: Exchanger, plan: GhostPlan, local):
+    """Per step: the owners' new positions into the ghost slots (in place)."""
+    at = plan.n_owned
+    for d, tm, tp, n_fp, n_fm in plan.stages:
+        from_plus, from_minus = ex.exchange_fixed(local[tm], local[tp], dec.neighbor(d, -1),
+                                                  dec.neighbor(d, +1), n_fp, n_fm)
+        local[at:at + n_fp] = from_plus
+        local[at + n_fp:at + n_fp + n_fm] = from_minus
+        at += n_fp + n_fm
+    return local
+
+
+def allsum_in_rank_order(dist, values, device):
+    """Sum a small vector over ranks in rank order (deterministic)."""
+    import torch
+
+    wire = torch.device("cpu") if dist.get_backend() == "gloo" else torch.device(device)
+    t = torch.as_tensor(np.asarray(values, dtype=np.float64), device=wire)
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    acc = np.zeros_like(np.asarray(values, dtype=np.float64))
+    for p in parts:
+        acc = acc + p.cpu().numpy()
+    return acc

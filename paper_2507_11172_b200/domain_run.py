@@ -1,0 +1,247 @@
+"""Domain-decomposed r-RESPA over ranks (one process per GPU).
+
+The loop of ``respamd/integrators.py:96-173`` on each rank's owned particles,
+with the exchange of ``domain.py`` around the force passes:
+
+    kick3 / drift / wrap (owned)               -- backend
+    row-rebuild vote (any rank's particle moved > skin/2; all_reduce MAX)
+    rebuild:  migrate + ghosts + local rows    -- domain.py + backend
+    else:     refresh ghost positions          -- domain.py
+    LJ on the local set, kick, [ATM every s-th step, kick3]
+    samples: per-rank partial scalars summed in rank order
+
+The force backend is the sm_100a engine (``GpuBackend``); the CPU tests plug
+in a numpy restatement with the same interface.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .domain import PAYLOAD, Decomposition, Exchanger, allsum_in_rank_order, build_ghosts, migrate, \
+    refresh_ghosts
+from .integrators import IntegrationBlowUp, RespaSchedule, RunTrace
+from .model import triplet_cutoff
+
+
+class GpuBackend:
+    """sm_100a passes and r-RESPA updates on one rank's particles."""
+
+    def __init__(self, n_max: int, ff, r_build: float):
+        from . import _lib
+        from .engine import ForceEngine, _round_up
+
+        self._lib = _lib
+        self.eng = ForceEngine(n_max)
+        self.torch = self.eng.torch
+        self.device = self.eng.device
+        self.ff = ff
+        self.rc2 = float(ff.cutoff)
+        self.rc3 = triplet_cutoff(ff)
+        self.r_build = float(r_build)
+        self._round_up = _round_up
+        self.window = None
+        self.n_own = 0
+        self.n_local = 0
+        self.f_local = self.torch.zeros((n_max, 3), dtype=self.torch.float64, device=self.device)
+
+    def set_local(self, local, n_own: int, window, rebuild: bool) -> None:
+        eng, torch = self.eng, self.torch
+        n = int(local.shape[0])
+        if rebuild:
+            eng.set_count(n)
+            self.window, self.n_own, self.n_local = window, int(n_own), n
+            eng.pos[:n] = local
+            eng.reset_status(0)
+            eng.bin(window)
+            eng.nlist(window, self.r_build, capacity=eng.capacity or None, checked=True)
+            eng.owned_rank = (eng.parts[:n] < n_own).to(torch.uint8)
+        else:
+            eng.pos[:n] = local
+            eng.pos_r[:n][eng.rank_of[:n].long()] = eng.pos[:n]
+
+    def pair(self):
+        eng = self.eng
+        eng.lj(self.window, self.rc2, self.ff.epsilon, self.ff.sigma, self.f_local, tag=0)
+        return self.f_local[: self.n_own].clone(), eng.scalars[1:3].clone()
+
+    def triplet(self):
+        eng = self.eng
+        if float(self.ff.nu) == 0.0:
+            return (self.torch.zeros((self.n_own, 3), dtype=self.torch.float64, device=self.device),
+                    self.torch.zeros(2, dtype=self.torch.float64, device=self.device))
+        eng.atm(self.window, self.rc3, float(self.ff.nu), self.f_local, tag=0, count_visits=False)
+        return self.f_local[: self.n_own].clone(), eng.scalars[3:5].clone()
+
+    def check(self) -> Optional[str]:
+        err = self.eng.read_status()
+        if err is None:
+            return None
+        return "particles closer than the minimum separation guard" if err[1] in (1, 2) else \
+            f"device error kind {err[1]}"
+
+
+@dataclass
+class DomainState:
+    ids: object  # (n_own,) float64 global ids
+    x: object
+    v: object
+    f2: object
+    f3: object
+    x_ref: object
+
+
+def _numpy_like_update(torch, a, scale, b):
+    """a + scale*b with numpy's rounding (two roundings)."""
+    return a + (scale * b)
+
+
+def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory, skin: float = 0.3,
+                     sample_interval: Optional[int] = None, dims=None, device=None):
+    """Run r-RESPA decomposed over dist.get_world_size() ranks.
+
+    Every rank passes the same full initial `system` (host arrays); on return
+    every rank's `system` holds the final state (gathered by particle id) and
+    the same RunTrace."""
+    import torch
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    s = schedule.step_size_factor
+    interval = s if sample_interval is None else int(sample_interval)
+    rc2, rc3 = float(ff.cutoff), triplet_cutoff(ff)
+    r_list = max(rc2, rc3) if float(ff.nu) != 0.0 else rc2
+    box = np.asarray(system.box, dtype=np.float64)
+    skin = max(0.0, min(float(skin), float(box.min()) / 2.0 - r_list))
+    r_build = r_list + skin
+    dec = Decomposition(box, r_build, world, rank, dims)
+    n_total = system.positions.shape[0]
+    backend = backend_factory(dec, n_total, r_build)
+    dev = backend.device if device is None else device
+    ex = Exchanger(dist, dev)
+    m = float(system.mass)
+    dt = schedule.dt
+    half_dt, half_drift, half_respa = 0.5 * dt / m, 0.5 * dt * dt / m, 0.5 * dt * s / m
+    box_t = torch.as_tensor(box, device=dev)
+
+    mine = np.nonzero(dec.owner_rank(np.asarray(system.positions)) == rank)[0]
+    to_t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)  # noqa: E731
+    st = DomainState(ids=torch.as_tensor(mine.astype(np.float64), device=dev),
+                     x=to_t(system.positions[mine]), v=to_t(system.velocities[mine]),
+                     f2=None, f3=None, x_ref=None)
+    window = dec.window()
+    trace = RunTrace()
+
+    def rebuild():
+        nonlocal window
+        if st.f2 is not None:
+            payload = torch.cat([st.ids[:, None], st.x, st.v, st.f2, st.f3], dim=1)
+            payload = migrate(dec, ex, payload)
+            st.ids, st.x, st.v = payload[:, 0], payload[:, 1:4], payload[:, 4:7]
+            st.f2, st.f3 = payload[:, 7:10].contiguous(), payload[:, 10:13].contiguous()
+            st.x, st.v = st.x.contiguous(), st.v.contiguous()
+        local, plan = build_ghosts(dec, ex, st.x)
+        backend.set_local(local, plan.n_owned, window, rebuild=True)
+        st.x_ref = st.x.clone()
+        return local, plan
+
+    def refresh(plan, local):
+        local[: plan.n_owned] = st.x
+        refresh_ghosts(dec, ex, plan, local)
+        backend.set_local(local, plan.n_owned, window, rebuild=False)
+
+    def scalars(e2w2, e3w3):
+        kin = float((st.v * st.v).sum().item())
+        return allsum_in_rank_order(dist, [kin, float(e2w2[0]), float(e2w2[1]), float(e3w3[0]),
+                                           float(e3w3[1])], dev)
+
+    def record(it, e2w2, e3w3):
+        tot = scalars(e2w2, e3w3)
+        trace.record_values(it, 0.5 * m * tot[0], tot[1], tot[2], tot[3], tot[4])
+
+    wire = torch.device("cpu") if dist.get_backend() == "gloo" else dev
+
+    def any_flag(flag: bool) -> bool:
+        t = torch.tensor([1 if flag else 0], dtype=torch.int64, device=wire)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return bool(t.item())
+
+    def fail(it):
+        msg = backend.check()
+        if any_flag(msg is not None):
+            raise IntegrationBlowUp(it, msg or "error on another rank", trace)
+
+    local, plan = rebuild()
+    f2, e2w2 = backend.pair()
+    f3, e3w3 = backend.triplet()
+    fail(0)
+    st.f2, st.f3 = f2, f3
+    record(0, e2w2, e3w3)
+    half_skin2 = (0.5 * skin) ** 2 * (1.0 - 1e-9)
+    for i in range(schedule.num_iterations):
+        if i % s == 0:
+            st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
+        st.x = st.x + ((dt * st.v) + (half_drift * st.f2))
+        st.x = torch.remainder(st.x, box_t)  # numpy mod semantics for box > 0
+        st.x = torch.where(st.x >= box_t, torch.zeros_like(st.x), st.x)
+        d = st.x - st.x_ref
+        d = d - box_t * torch.where(d > 0.5 * box_t, 1.0, torch.where(d < -0.5 * box_t, -1.0, 0.0))
+        moved = bool((d * d).sum(dim=1).max().item() > half_skin2) if st.x.shape[0] else False
+        if any_flag(moved or skin == 0.0):
+            local, plan = rebuild()
+        else:
+            refresh(plan, local)
+        f2_new, e2w2 = backend.pair()
+        st.v = st.v + (half_dt * (st.f2 + f2_new))
+        st.f2 = f2_new
+        if (i + 1) % s == 0:
+            st.f3, e3w3 = backend.triplet()
+            st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
+        finite = bool(torch.isfinite(st.x).all().item() and torch.isfinite(st.v).all().item())
+        fail(i + 1)
+        if any_flag(not finite):
+            raise IntegrationBlowUp(i + 1, "non-finite position or velocity", trace)
+        if (i + 1) % interval == 0:
+            record(i + 1, e2w2, e3w3)
+
+    # gather the owned state of every rank into the host system (by id)
+    parts = [None] * world
+    payload = torch.cat([st.ids[:, None], st.x, st.v, st.f2, st.f3], dim=1).cpu()
+    dist.all_gather_object(parts, payload.numpy())
+    allp = np.concatenate(parts, axis=0)
+    ids = allp[:, 0].astype(np.int64)
+    if ids.shape[0] != n_total or np.unique(ids).shape[0] != n_total:
+        raise RuntimeError("particles lost or duplicated by the decomposition")
+    order = np.argsort(ids)
+    allp = allp[order]
+    system.positions[:] = allp[:, 1:4]
+    system.velocities[:] = allp[:, 4:7]
+    system.forces_2b[:] = allp[:, 7:10]
+    system.forces_3b[:] = allp[:, 10:13]
+    return trace
+
+
+def gpu_backend_factory(ff, headroom: float = 1.6):
+    """Backend factory for domain_respa_run on the local CUDA device."""
+
+    def make(dec: Decomposition, n_total: int, r_build: float):
+        n_max = int(headroom * n_total / dec.world * _ghost_factor(dec, r_build)) + 1024
+        return GpuBackend(min(n_max, n_total * 2 + 1024), ff, r_build)
+
+    return make
+
+
+def _ghost_factor(dec: Decomposition, r_build: float) -> float:
+    cells = np.asarray(dec.geom.cells, dtype=np.float64)
+    f = 1.0
+    for d in range(3):
+        if dec.split(d):
+            blk = cells[d] / dec.dims[d]
+            f *= (blk + 2.0) / blk
+    return f
+
+
+__all__ = ["GpuBackend", "domain_respa_run", "gpu_backend_factory", "PAYLOAD"]

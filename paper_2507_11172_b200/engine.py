@@ -81,6 +81,7 @@ class ForceEngine:
         self.atm_scratch = None
         self.capacity = 0
         self.slots = 0  # shared-memory slots of the triplet pass (longest row)
+        self.owned_rank = None  # uint8 per rank in decomposed runs
         self._geom_key = None
         self._grid = None
 
@@ -89,13 +90,18 @@ class ForceEngine:
     def stream(self):
         return _lib.stream_handle()
 
-    def grid_struct(self, geom: Geometry):
-        key = (geom.cells, geom.cell_size, geom.origin, geom.inv_cell, geom.periodic, geom.box,
-               geom.cutoff)
-        if key != self._geom_key:
-            self._grid = rb_grid(geom)
-            self._geom_key = key
+    def grid_struct(self, geom):
+        if geom != self._geom_key:
+            self._grid = geom.to_rb_grid() if hasattr(geom, "to_rb_grid") else rb_grid(geom)
+            self._geom_key = geom
         return self._grid
+
+    def set_count(self, n: int) -> None:
+        """Use the first `n` particles of the buffers (decomposed runs,
+        where the local count changes at every row rebuild)."""
+        if n > self.pos.shape[0]:
+            raise ValueError(f"{n} local particles exceed the engine's {self.pos.shape[0]}")
+        self.n = int(n)
 
     def reset_status(self, step: int = 0) -> None:
         self.status[0] = -1
@@ -114,6 +120,10 @@ class ForceEngine:
 
     def _gate(self, gated: bool):
         return ptr(self.rebuild_flag) if gated else _NULL
+
+    def _owned(self):
+        # rank-indexed owned flags of a decomposed (domain) run; NULL otherwise
+        return ptr(self.owned_rank) if self.owned_rank is not None else _NULL
 
     # --------------------------------------------------------------- binning
     def _ensure_cells(self, ncell: int) -> None:
@@ -212,7 +222,8 @@ class ForceEngine:
         st = self.L.rb_lj_pass(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
                                ptr(self.rows), ptr(self.row_count), int(self.capacity), float(rc),
                                float(epsilon), float(sigma), ptr(forces), ptr(self.e2_rank),
-                               ptr(self.w2_rank), ptr(self.status), int(tag), self.stream)
+                               ptr(self.w2_rank), self._owned(), ptr(self.status), int(tag),
+                               self.stream)
         _lib.check(st, "rb_lj_pass")
 
     def atm(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
@@ -235,7 +246,7 @@ class ForceEngine:
                                 ptr(self.rows), ptr(self.row_count), ptr(self.mirror),
                                 int(self.capacity), int(self.slots or self.capacity), float(rc),
                                 float(nu), ptr(forces), ptr(self.e3_rank), ptr(self.w3_rank),
-                                ptr(self.v_rank), ptr(self.atm_scratch),
+                                ptr(self.v_rank), self._owned(), ptr(self.atm_scratch),
                                 self.atm_scratch.numel() * 8, ptr(self.status), int(tag),
                                 self.stream)
         _lib.check(st, "rb_atm_pass")

@@ -142,7 +142,80 @@ def rb_grid(geom: Geometry):
     for i, row in enumerate(pair):
         for d in range(3):
             g.offsets[i][d] = int(row[d])
+    for d in range(3):
+        g.wrap[d] = g.periodic
+        g.gcells[d] = geom.cells[d]
+        g.wlo[d] = 0
     return g
+
+
+@dataclass(frozen=True)
+class WindowGeometry:
+    """A rank's window of a decomposed periodic grid (domain decomposition).
+
+    ``base`` is the global periodic geometry; per dimension the local grid is
+    either the whole wrapped dimension (``wrap[d]``, one rank along d) or the
+    window of ``cells[d]`` global cells starting at global cell ``lo[d]``
+    (the rank's block plus one halo layer on each side).  Distances keep the
+    periodic minimum image of the whole box.
+    """
+
+    base: Geometry
+    lo: tuple
+    cells: tuple
+    wrap: tuple
+
+    @property
+    def num_cells(self) -> int:
+        return int(np.prod(self.cells))
+
+    @property
+    def cutoff(self) -> float:
+        return self.base.cutoff
+
+    @property
+    def periodic(self) -> bool:
+        return True
+
+    @property
+    def box(self) -> tuple:
+        return self.base.box
+
+    @property
+    def cell_size(self) -> tuple:
+        return self.base.cell_size
+
+    def offsets(self) -> np.ndarray:
+        """Neighbour offsets: canonical (mod n, deduplicated) in wrapped
+        dimensions, raw -1/0/1 in windowed ones (the kernel skips cells
+        outside the window)."""
+        out = []
+        for o in _cube((1, 1, 1)):
+            t = tuple(int(v) % int(n) if w else int(v)
+                      for v, n, w in zip(o, self.base.cells, self.wrap))
+            if t not in out:
+                out.append(t)
+        return np.array(sorted(out), dtype=np.int64)
+
+    def to_rb_grid(self):
+        from ._lib import RbGrid
+
+        offs = self.offsets()
+        g = RbGrid()
+        for d in range(3):
+            g.cells[d] = self.cells[d]
+            g.origin[d] = 0.0
+            g.inv_cell[d] = self.base.inv_cell[d]
+            g.box[d] = self.base.box[d]
+            g.wrap[d] = 1 if self.wrap[d] else 0
+            g.gcells[d] = self.base.cells[d]
+            g.wlo[d] = self.lo[d]
+        g.periodic = 1
+        g.n_offsets = int(offs.shape[0])
+        for i, row in enumerate(offs):
+            for d in range(3):
+                g.offsets[i][d] = int(row[d])
+        return g
 
 
 @dataclass

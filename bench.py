@@ -185,15 +185,67 @@ def reference_arm(args, cfg):
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
+def domain_arm(args, cfg):
+    """N > 1: weak scaling with the domain-decomposed r-RESPA.
+
+    The box is cfg2's FCC block replicated along the rank grid (32,000
+    particles per GPU), decomposed over the ranks (NCCL halo exchange);
+    value = ranks x steps/s (cfg2-equivalent steps per second), time = max
+    over ranks of CUDA-event time around K steps."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    import paper_2507_11172_b200 as pkg
+    from paper_2507_11172_b200.domain import auto_dims
+    from paper_2507_11172_b200.domain_run import domain_respa_run, gpu_backend_factory
+
+    sf = cfg.step_size_factor
+    dims = auto_dims(world, (world * 16, world * 16, world * 16))
+    nc = tuple(cfg.params["nc"] * d for d in dims)
+    s = pkg.systems.fcc_system(nc, jitter=0.02, seed=1, temperature=cfg.temperature, vseed=1)
+    ff = cfg.force_field()
+    K = max(sf, (int(args.steps) + sf - 1) // sf * sf)
+    W = max(sf, (max(3, int(args.warmup)) + sf - 1) // sf * sf)
+    warm = s.copy()
+    domain_respa_run(dist, warm, ff, pkg.RespaSchedule(cfg.dt, sf, W), gpu_backend_factory(ff),
+                     dims=dims)
+    dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        a.record()
+        domain_respa_run(dist, s, ff, pkg.RespaSchedule(cfg.dt, sf, K), gpu_backend_factory(ff),
+                         dims=dims)
+        b.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": world * K / (ms * 1e-3), "unit": "steps/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded FCC lattice + jitter, SURVEY.md §8d)",
+            "config": {"workload": f"cfg2 block x {dims} = {s.n} particles, domain-decomposed",
+                       "parallelism": f"domain decomposition {dims} (NCCL halo exchange)",
+                       "value": "ranks x steps/s (cfg2-equivalent)",
+                       "timed": "domain_respa_run incl. initial passes and final gather"},
+            "clocks": clocks.summary(),
+        }), flush=True)
+    dist.destroy_process_group()
+
+
 def ours_arm(args, cfg):
     import torch
 
     world, rank, local = dist_env()
     if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        return domain_arm(args, cfg)
     import paper_2507_11172_b200 as pkg
     from paper_2507_11172_b200 import _lib
     from paper_2507_11172_b200.integrators import DeviceRespa, RespaSchedule

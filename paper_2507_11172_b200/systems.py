@@ -41,12 +41,12 @@ def _jitter_and_wrap(sites, box, jitter, seed) -> np.ndarray:
     return pos
 
 
-def fcc_system(nc: int, jitter: float = 0.02, seed: int = 1, temperature: float = 0.0,
+def fcc_system(nc, jitter: float = 0.02, seed: int = 1, temperature: float = 0.0,
                vseed: int = 1) -> ParticleSystem:
-    """FCC block of nc^3 unit cells at rho = 0.8 in a periodic cube."""
+    """FCC block of nc^3 (or nx x ny x nz) unit cells at rho = 0.8, periodic."""
     cells = _cell_grid(nc)
     sites = ((cells[:, None, :] + FCC_BASIS[None, :, :]) * FCC_A).reshape(-1, 3)
-    box = np.full(3, nc * FCC_A)
+    box = (np.full(3, nc * FCC_A) if np.isscalar(nc) else np.asarray(nc, dtype=np.float64) * FCC_A)
     system = ParticleSystem.empty(sites.shape[0], box, periodic=True)
     system.positions[:] = _jitter_and_wrap(sites, box, jitter, seed)
     init_velocities(system, temperature, vseed)

@@ -102,8 +102,9 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB_PATH
-    if not _build.up_to_date():
+    override = os.environ.get("RB_LIB_PATH")  # tuning builds (tools/); never a fallback
+    path = override or _build.LIB_PATH
+    if override is None and not _build.up_to_date():
         try:
             _build.build()
         except Exception as exc:  # pragma: no cover - build environment problem

@@ -49,11 +49,13 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = None) -> str:
+    target = out or LIB_PATH
+    if not force and out is None and up_to_date():
         return LIB_PATH
-    tmp = LIB_PATH + ".tmp"
+    tmp = target + ".tmp"
     cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", os.path.join(REPO, "include")]
+    cmd += os.environ.get("RB_NVCC_EXTRA", "").split()  # tuning experiments only
     if verbose:
         cmd += ["-Xptxas", "-v"]
     cmd += ["-o", tmp, *sources()]
@@ -62,8 +64,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

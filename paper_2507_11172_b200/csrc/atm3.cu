@@ -42,6 +42,9 @@ constexpr int kA3Warps = 4;
 #define RB_A3_MIN_BLOCKS 7
 #endif
 constexpr int kA3MinBlocks = RB_A3_MIN_BLOCKS;  // register cap for occupancy
+#ifndef RB_A3_PACKED
+#define RB_A3_PACKED 1  // fp32x2 packed candidate filter
+#endif
 constexpr int kA3Queue = 512;        // entries: the carry of the last chunk + one round block
 constexpr int kA3RoundBlock = 32;    // at most this many rounds per block (bits per word)
 constexpr int kA3MaxSlots = 2047;    // queue entries pack s and t in 11 bits each
@@ -183,12 +186,12 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
     return true;
 }
 
-__device__ __forceinline__ void a3_add(const A3Smem &sm, int slot, const double f[3]) {
-    double2 xy = sm.axy[slot];
+__device__ __forceinline__ void a3_add(double2 *axy, double *az, int slot, const double f[3]) {
+    double2 xy = axy[slot];
     xy.x += f[0];
     xy.y += f[1];
-    sm.axy[slot] = xy;
-    sm.az[slot] += f[2];
+    axy[slot] = xy;
+    az[slot] += f[2];
 }
 
 // evaluate the first `cnt` queue entries and fold f_j / f_k into the slot
@@ -214,9 +217,9 @@ __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, co
     while (todo) {
         const int r0 = __shfl_sync(0xffffffffu, rec, __ffs(todo) - 1);
         const bool act = pending && rec == r0;
-        if (act) a3_add(sm, s, fj);
+        if (act) a3_add(sm.axy, sm.az, s, fj);
         __syncwarp();
-        if (act) a3_add(sm, t, fk);
+        if (act) a3_add(sm.axy, sm.az, t, fk);
         __syncwarp();
         if (act) pending = false;
         todo = __ballot_sync(0xffffffffu, pending);
@@ -345,7 +348,35 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
                 const int elim = (2 * (d0 + dn - 1) == m && s >= d0 + dn - 1) ? dn - 1 : dn;
                 int t = s + d0;
                 if (t >= m) t -= m;
-                for (int e = 0; e < elim; e++) {
+                int e = 0;
+                if (!kExactImage && RB_A3_PACKED) {
+                    // two partners per step with packed fp32x2 math; the rare
+                    // pairs inside the band go through a3_accept
+                    const float2 nx = make_float2(-ps.x, -ps.x), ny = make_float2(-ps.y, -ps.y),
+                                 nz = make_float2(-ps.z, -ps.z);
+                    for (; e + 1 < elim; e += 2) {
+                        int t2 = t + 1;
+                        if (t2 == m) t2 = 0;
+                        const float4 p1 = sm.f4[t], p2 = sm.f4[t2];
+                        const float2 ex = __fadd2_rn(make_float2(p1.x, p2.x), nx);
+                        const float2 ey = __fadd2_rn(make_float2(p1.y, p2.y), ny);
+                        const float2 ez = __fadd2_rn(make_float2(p1.z, p2.z), nz);
+                        const float2 c2 = __ffma2_rn(ez, ez, __ffma2_rn(ey, ey, __fmul2_rn(ex, ex)));
+                        if (c2.x <= rc2f_lo) bits |= 1u << e;
+                        else if (c2.x <= rc2f_hi &&
+                                 a3_accept<kExactImage>(sm, ps, s, t, im, row, pr, rc2, rc2_lo,
+                                                        rc2_hi, rc2f_lo, rc2f_hi))
+                            bits |= 1u << e;
+                        if (c2.y <= rc2f_lo) bits |= 2u << e;
+                        else if (c2.y <= rc2f_hi &&
+                                 a3_accept<kExactImage>(sm, ps, s, t2, im, row, pr, rc2, rc2_lo,
+                                                        rc2_hi, rc2f_lo, rc2f_hi))
+                            bits |= 2u << e;
+                        t = t2 + 1;
+                        if (t == m) t = 0;
+                    }
+                }
+                for (; e < elim; e++) {
                     if (a3_accept<kExactImage>(sm, ps, s, t, im, row, pr, rc2, rc2_lo, rc2_hi,
                                                rc2f_lo, rc2f_hi))
                         bits |= 1u << e;

@@ -53,6 +53,7 @@ extern "C" {
 #define RB_ERR_CUDA 3           /* launch failure */
 #define RB_ERR_CAPACITY 4       /* a neighbour row exceeded its capacity */
 #define RB_ERR_ARGUMENT 5       /* bad sizes or pointers */
+#define RB_NOT_CAPTURING 6      /* rb_rebuild_cond_begin outside a stream capture */
 
 /* device status-word kinds (low 8 bits), ordered by precedence inside a step */
 #define RB_KIND_PAIR_MIN_SEPARATION 1    /* raised by pair_pass (integrators.py:154-157) */
@@ -220,6 +221,21 @@ RB_API int rb_step_begin(unsigned long long *status, void *stream);
 RB_API int rb_trace_record(const unsigned long long *status, int64_t sample_interval,
                            double *trace, const double *sumsq, const double *e2, const double *w2,
                            const double *e3, const double *w3, void *stream);
+
+/* ---- conditional rebuild inside a captured step (CUDA graph IF node) ----
+ * In a CUDA-graph capture of `stream`, the gated rebuild (rb_bin, rb_nlist,
+ * rb_nlist_mirror with rebuild_flag set) costs nine launches per step even
+ * when its gate is closed.  rb_rebuild_cond_begin appends a one-thread node
+ * that evaluates the gate (*rebuild_flag == tag, tag < 0: status[1]) and an
+ * IF node whose body runs only when it is open, and returns in *body_stream
+ * a stream capturing into that body: launch the gated rebuild there, then
+ * call rb_rebuild_cond_end(stream) to continue the capture after the IF node.
+ * Outside a capture it returns RB_NOT_CAPTURING and nothing is launched (the
+ * caller launches the gated kernels on `stream`; results are identical).
+ * One conditional may be open per host thread. */
+RB_API int rb_rebuild_cond_begin(const int64_t *rebuild_flag, const unsigned long long *status,
+                                 int64_t tag, void *stream, void **body_stream);
+RB_API int rb_rebuild_cond_end(void *stream);
 
 /* ---- device timing helpers for bench.py (events on the launch stream) -- */
 /* FP64 FMA throughput microbenchmark: runs `iters` dependent-chain DFMA

@@ -21,6 +21,7 @@ RB_ERR_GEOMETRY = 2
 RB_ERR_CUDA = 3
 RB_ERR_CAPACITY = 4
 RB_ERR_ARGUMENT = 5
+RB_NOT_CAPTURING = 6
 
 RB_KIND_PAIR_MIN_SEPARATION = 1
 RB_KIND_TRIPLET_MIN_SEPARATION = 2
@@ -84,6 +85,8 @@ SIGNATURES = {
     "rb_trace_record": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "rb_fp64_peak": (ctypes.c_int, [_I32, _P, _P]),
     "rb_l2_flush": (ctypes.c_int, [_P, _SZ, _P]),
+    "rb_rebuild_cond_begin": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
+    "rb_rebuild_cond_end": (ctypes.c_int, [_P]),
 }
 
 _lib = None

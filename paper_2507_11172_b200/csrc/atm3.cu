@@ -260,21 +260,25 @@ __device__ __forceinline__ bool a3_accept(const A3Smem &sm, const float4 &ps, in
     return exact_r2(dx, dy, dz) <= rc2;
 }
 
+// One base particle r (rank order) per warp.  `ovf` (main pass with a
+// reduced slot count): a base whose S+(r) does not fit is appended to the
+// overflow list ovf[1..] (count ovf[0]) and left to k_atm3_overflow.
 template <bool kExactImage>
-__global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
-    k_atm3(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
-           const int32_t *__restrict__ row_count, const int32_t *__restrict__ mirror,
-           int32_t capacity, int32_t slots, double rc2,
-           double rc2_lo, double rc2_hi, float rc2f_lo, float rc2f_hi,
-           double *__restrict__ own, double *__restrict__ gbuf,
-           double *__restrict__ energy_rank, double *__restrict__ virial_rank,
-           int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
-           unsigned long long *status, int64_t tag, int debug_mode) {
-    extern __shared__ __align__(16) char smem_raw[];
+__device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid &g, int64_t n, const double *__restrict__ pr,
+                                       const int32_t *__restrict__ rows,
+                                       const int32_t *__restrict__ row_count,
+                                       const int32_t *__restrict__ mirror, int32_t capacity,
+                                       int32_t slots, double rc2, double rc2_lo, double rc2_hi,
+                                       float rc2f_lo, float rc2f_hi, double *__restrict__ own,
+                                       double *__restrict__ gbuf,
+                                       double *__restrict__ energy_rank,
+                                       double *__restrict__ virial_rank,
+                                       int32_t *__restrict__ triplets_rank,
+                                       const uint8_t *__restrict__ owned,
+                                       unsigned long long *status, int64_t tag, int debug_mode,
+                                       int32_t *ovf) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (r >= n) return;
     tag = resolve_tag(tag, status);
     if (warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
     const A3Smem sm = a3_carve(smem_raw + (size_t)warp * a3_warp_bytes(slots), slots);
@@ -308,7 +312,12 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
         }
         const unsigned mk = __ballot_sync(0xffffffffu, keep);
         if (m + __popc(mk) > slots) {  // S+(i) does not fit the shared-memory slots
-            if (lane == 0) record_status(status, tag, RB_KIND_CAPACITY);
+            if (lane == 0) {
+                if (ovf)
+                    ovf[1 + atomicAdd(ovf, 1)] = (int32_t)r;
+                else
+                    record_status(status, tag, RB_KIND_CAPACITY);
+            }
             return;
         }
         if (keep) {
@@ -466,6 +475,43 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     }
 }
 
+template <bool kExactImage>
+__global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
+    k_atm3(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
+           const int32_t *__restrict__ row_count, const int32_t *__restrict__ mirror,
+           int32_t capacity, int32_t slots, double rc2, double rc2_lo, double rc2_hi,
+           float rc2f_lo, float rc2f_hi, double *__restrict__ own, double *__restrict__ gbuf,
+           double *__restrict__ energy_rank, double *__restrict__ virial_rank,
+           int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
+           unsigned long long *status, int64_t tag, int debug_mode, int32_t *ovf) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= n) return;
+    a3_base<kExactImage>(r, smem_raw, g, n, pr, rows, row_count, mirror, capacity, slots, rc2, rc2_lo,
+                            rc2_hi, rc2f_lo, rc2f_hi, own, gbuf, energy_rank, virial_rank,
+                            triplets_rank, owned, status, tag, debug_mode, ovf);
+}
+
+// the bases listed by the main pass, with the full slot count
+template <bool kExactImage>
+__global__ void __launch_bounds__(kA3Warps * 32)
+    k_atm3_overflow(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
+           const int32_t *__restrict__ row_count, const int32_t *__restrict__ mirror,
+           int32_t capacity, int32_t slots, double rc2, double rc2_lo, double rc2_hi,
+           float rc2f_lo, float rc2f_hi, double *__restrict__ own, double *__restrict__ gbuf,
+           double *__restrict__ energy_rank, double *__restrict__ virial_rank,
+           int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
+           unsigned long long *status, int64_t tag, int debug_mode, const int32_t *ovf) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int wpb = blockDim.x >> 5;
+    const int cnt = *(volatile const int32_t *)ovf;
+    for (int64_t q = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); q < cnt;
+         q += (int64_t)gridDim.x * wpb)
+        a3_base<kExactImage>(ovf[1 + q], smem_raw, g, n, pr, rows, row_count, mirror, capacity, slots, rc2, rc2_lo,
+                            rc2_hi, rc2f_lo, rc2f_hi, own, gbuf, energy_rank, virial_rank,
+                            triplets_rank, owned, status, tag, debug_mode, nullptr);
+}
+
 // F(p) = 2 nu * (own(p) + sum over row entries k of p with q = row[k] < p of
 // G[p][k]); the row prefix is walked in order by kG lanes, then a fixed xor
 // tree.
@@ -510,8 +556,6 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
     }
 }
 
-static size_t g_a3_granted[2] = {0, 0};
-
 template <typename K>
 static void a3_grant(K kernel, size_t bytes, size_t &granted) {
     if (bytes > 48 * 1024 && bytes > granted) {
@@ -525,9 +569,60 @@ static void a3_grant(K kernel, size_t bytes, size_t &granted) {
 using namespace rb;
 
 extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
-    // own (n x 3) + G (n x capacity x 3), doubles
-    return (size_t)(n > 0 ? n : 1) * 3 * sizeof(double) * (size_t)(1 + capacity);
+    // own (n x 3) + G (n x capacity x 3), doubles; overflow list (1 + n) int32
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    return nn * 3 * sizeof(double) * (size_t)(1 + capacity) + (nn + 1) * sizeof(int32_t);
 }
+
+namespace rb {
+// Slots of the main launch.  S+(r) of most bases is about half a row; only
+// bases whose neighbours mostly follow them in rank order (cells next to the
+// periodic wrap of the cell order) approach a full row.  Sizing every warp's
+// shared memory for the longest S+ costs occupancy, so the main launch takes
+// about half the slots and lists the few longer bases for a second launch.
+static int a3_fast_slots(int slot_capacity) {
+    int f = ((slot_capacity * 11 / 20) + 31) / 32 * 32;  // ~0.55 of the full count
+    f = f < 64 ? 64 : f;
+    return f >= slot_capacity ? slot_capacity : f;
+}
+
+static int a3_warps_for(size_t per) {
+    int warps = kA3Warps;
+    while (warps > 1 && (size_t)warps * per > 227 * 1024) warps--;
+    return (size_t)warps * per > 227 * 1024 ? 0 : warps;
+}
+
+template <bool kExactImage>
+static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double *pos_r,
+                      const int32_t *rows, const int32_t *row_count, const int32_t *mirror,
+                      int32_t capacity, int fast, int full, double rc2, double lo, double hi,
+                      double *own, double *gbuf, double *energy_rank, double *virial_rank,
+                      int32_t *triplets_rank, const uint8_t *owned, unsigned long long *status,
+                      int64_t tag, int debug_mode, int32_t *ovf) {
+    static size_t granted_main = 0, granted_ovf = 0;
+    const float flo = (float)(rc2 * (1.0 - kA3Band)), fhi = (float)(rc2 * (1.0 + kA3Band));
+    const size_t per = a3_warp_bytes(fast);
+    const int warps = a3_warps_for(per);
+    const bool split = fast < full;
+    if (split) cudaMemsetAsync(ovf, 0, sizeof(int32_t), st);
+    a3_grant(k_atm3<kExactImage>, warps * per, granted_main);
+    k_atm3<kExactImage><<<(unsigned)((n + warps - 1) / warps), warps * 32, warps * per, st>>>(
+        g, n, pos_r, rows, row_count, mirror, capacity, fast, rc2, lo, hi, flo, fhi, own, gbuf,
+        energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
+        split ? ovf : nullptr);
+    note_launches(1);
+    if (!split) return;
+    const size_t per_full = a3_warp_bytes(full);
+    const int wf = a3_warps_for(per_full);
+    const int64_t need = (n + wf - 1) / wf;
+    const unsigned blocks = (unsigned)(need < 148 * 4 ? need : 148 * 4);
+    a3_grant(k_atm3_overflow<kExactImage>, wf * per_full, granted_ovf);
+    k_atm3_overflow<kExactImage><<<blocks, wf * 32, wf * per_full, st>>>(
+        g, n, pos_r, rows, row_count, mirror, capacity, full, rc2, lo, hi, flo, fhi, own, gbuf,
+        energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode, ovf);
+    note_launches(1);
+}
+}  // namespace rb
 
 extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
                            const int32_t *row_count, const int32_t *mirror, int32_t capacity,
@@ -542,37 +637,26 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
     if (n == 0) return RB_OK;
     const double rc2 = rc * rc;
     static const int debug_mode = getenv("RB_ATM_DEBUG") ? atoi(getenv("RB_ATM_DEBUG")) : 0;
+    static const int no_split = getenv("RB_ATM_NO_SPLIT") ? atoi(getenv("RB_ATM_NO_SPLIT")) : 0;
     bool exact_image = false;
     if (g->periodic)
         for (int d = 0; d < 3; d++)
             if (!(g->box[d] > 4.0 * rc * (1.0 + 1e-12))) exact_image = true;
-    const size_t per = a3_warp_bytes(slot_capacity);
-    int warps = kA3Warps;
-    while (warps > 1 && (size_t)warps * per > 227 * 1024) warps--;
-    if ((size_t)warps * per > 227 * 1024) return RB_ERR_ARGUMENT;
-    const size_t smem = (size_t)warps * per;
-    const unsigned blocks = (unsigned)((n + warps - 1) / warps);
+    if (!a3_warps_for(a3_warp_bytes(slot_capacity))) return RB_ERR_ARGUMENT;
+    const int fast = no_split ? slot_capacity : a3_fast_slots(slot_capacity);
     cudaStream_t st = as_stream(stream);
     double *own = (double *)scratch;
     double *gbuf = own + 3 * n;
-    if (exact_image) {
-        a3_grant(k_atm3<true>, smem, g_a3_granted[0]);
-        k_atm3<true><<<blocks, warps * 32, smem, st>>>(*g, n, pos_r, rows, row_count, mirror,
-                                                        capacity, slot_capacity, rc2, rc2, rc2,
-                                                        (float)(rc2 * (1.0 - kA3Band)),
-                                                        (float)(rc2 * (1.0 + kA3Band)), own, gbuf,
-                                                        energy_rank, virial_rank, triplets_rank,
-                                                        owned, status, tag, debug_mode);
-        note_launches(1);
-    } else {
-        a3_grant(k_atm3<false>, smem, g_a3_granted[1]);
-        k_atm3<false><<<blocks, warps * 32, smem, st>>>(
-            *g, n, pos_r, rows, row_count, mirror, capacity, slot_capacity, rc2,
-            rc2 * (1.0 - kA3Margin), rc2 * (1.0 + kA3Margin), (float)(rc2 * (1.0 - kA3Band)),
-            (float)(rc2 * (1.0 + kA3Band)), own, gbuf, energy_rank, virial_rank, triplets_rank,
-            owned, status, tag, debug_mode);
-        note_launches(1);
-    }
+    int32_t *ovf = (int32_t *)(gbuf + (size_t)n * capacity * 3);
+    if (exact_image)
+        a3_launch<true>(st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity,
+                        rc2, rc2, rc2, own, gbuf, energy_rank, virial_rank, triplets_rank, owned,
+                        status, tag, debug_mode, ovf);
+    else
+        a3_launch<false>(st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity,
+                         rc2, rc2 * (1.0 - kA3Margin), rc2 * (1.0 + kA3Margin), own, gbuf,
+                         energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
+                         ovf);
     const int tb = 256;
     const int64_t threads = n * kGatherGroup;
     k_atm3_gather<<<(unsigned)((threads + tb - 1) / tb), tb, 0, st>>>(

@@ -1,0 +1,84 @@
+// graph.cu -- conditional rebuild node for captured r-RESPA steps.
+//
+// The device loop (integrators.DeviceRespa) replays one CUDA graph per step;
+// the row rebuild (binning + rows + mirror, nine kernels) is needed only on
+// the steps whose drift flagged it (Verlet skin, integrators.py docstring).
+// Instead of nine gated launches that exit at once, the captured step holds
+// one tiny kernel that evaluates the gate and sets a graph conditional, and
+// an IF node whose body is the rebuild.  The body kernels keep their own gate
+// check, so a body that runs is exactly the gated launch sequence.
+#include "common.cuh"
+
+namespace rb {
+
+__global__ void k_rebuild_cond(cudaGraphConditionalHandle h, const int64_t *flag,
+                               const unsigned long long *status, int64_t tag) {
+    tag = resolve_tag(tag, status);
+    if (*(volatile const int64_t *)flag == tag) cudaGraphSetConditional(h, 1u);
+}
+
+namespace {
+struct OpenCond {
+    cudaStream_t parent = nullptr;
+    cudaStream_t body = nullptr;
+    cudaGraphNode_t node = nullptr;
+    bool open = false;
+};
+thread_local OpenCond g_open;
+thread_local cudaStream_t g_body_stream = nullptr;
+}  // namespace
+
+}  // namespace rb
+
+using namespace rb;
+
+extern "C" int rb_rebuild_cond_begin(const int64_t *rebuild_flag, const unsigned long long *status,
+                                     int64_t tag, void *stream, void **body_stream) {
+    if (!rebuild_flag || !body_stream || g_open.open) return RB_ERR_ARGUMENT;
+    cudaStream_t s = as_stream(stream);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaGraph_t graph = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    if (cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &nd) != cudaSuccess)
+        return RB_ERR_CUDA;
+    if (cs != cudaStreamCaptureStatusActive) return RB_NOT_CAPTURING;
+    if (!g_body_stream && cudaStreamCreateWithFlags(&g_body_stream, cudaStreamNonBlocking) !=
+                              cudaSuccess)
+        return RB_ERR_CUDA;
+    cudaGraphConditionalHandle h;
+    if (cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault) != cudaSuccess)
+        return RB_ERR_CUDA;
+    k_rebuild_cond<<<1, 1, 0, s>>>(h, rebuild_flag, status, tag);
+    note_launches(1);
+    if (cudaGetLastError() != cudaSuccess) return RB_ERR_CUDA;
+    if (cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &nd) != cudaSuccess)
+        return RB_ERR_CUDA;
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (cudaGraphAddNode(&node, graph, deps, nd, &p) != cudaSuccess) return RB_ERR_CUDA;
+    if (cudaStreamBeginCaptureToGraph(g_body_stream, p.conditional.phGraph_out[0], nullptr,
+                                      nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+        return RB_ERR_CUDA;
+    g_open.parent = s;
+    g_open.body = g_body_stream;
+    g_open.node = node;
+    g_open.open = true;
+    *body_stream = (void *)g_body_stream;
+    return RB_OK;
+}
+
+extern "C" int rb_rebuild_cond_end(void *stream) {
+    if (!g_open.open || g_open.parent != as_stream(stream)) return RB_ERR_ARGUMENT;
+    g_open.open = false;
+    cudaGraph_t body = nullptr;
+    if (cudaStreamEndCapture(g_open.body, &body) != cudaSuccess) return RB_ERR_CUDA;
+    if (cudaStreamUpdateCaptureDependencies(g_open.parent, &g_open.node, 1,
+                                            cudaStreamSetCaptureDependencies) != cudaSuccess)
+        return RB_ERR_CUDA;
+    return RB_OK;
+}

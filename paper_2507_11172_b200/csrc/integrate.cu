@@ -355,6 +355,7 @@ extern "C" const char *rb_status_string(int status) {
         case RB_ERR_CUDA: return "CUDA launch error";
         case RB_ERR_CAPACITY: return "neighbour-row capacity exceeded";
         case RB_ERR_ARGUMENT: return "invalid argument";
+        case RB_NOT_CAPTURING: return "stream is not capturing";
         default: return "unknown status";
     }
 }

@@ -14,7 +14,14 @@
 
 namespace rb {
 
-constexpr int kLjGroup = 8;
+#ifndef RB_LJ_GROUP
+#define RB_LJ_GROUP 8
+#endif
+#ifndef RB_LJ_UNROLL
+#define RB_LJ_UNROLL 2
+#endif
+constexpr int kLjGroup = RB_LJ_GROUP;   // lanes per particle
+constexpr int kLjUnroll = RB_LJ_UNROLL; // row entries in flight per lane
 constexpr int kLjThreads = 256;
 
 __global__ void __launch_bounds__(kLjThreads)
@@ -37,26 +44,46 @@ __global__ void __launch_bounds__(kLjThreads)
         const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
         const int m = row_count[r];
         const int32_t *row = rows + r * (int64_t)capacity;
-        for (int k = sub; k < m; k += kLjGroup) {
-            const int j = row[k];
-            double dx, dy, dz;
-            exact_disp(im, xi, yi, zi, pr[3 * (j)], pr[3 * (j) + 1], pr[3 * (j) + 2], dx, dy, dz);
-            const double r2 = exact_r2(dx, dy, dz);
-            if (r2 > rc2) continue;
-            if (r2 < RB_MIN_DISTANCE_SQ) {
-                bad = true;
-                continue;
+        // kLjUnroll entries per lane per batch: their row and position loads
+        // are issued together (the pass is latency-bound); the accumulation
+        // order is still k = sub, sub + G, sub + 2G, ...
+        for (int k0 = sub; k0 < m; k0 += kLjUnroll * kLjGroup) {
+            int j[kLjUnroll];
+#pragma unroll
+            for (int u = 0; u < kLjUnroll; u++) {
+                const int k = k0 + u * kLjGroup;
+                j[u] = k < m ? __ldg(row + k) : -1;
             }
-            const double inv_r2 = 1.0 / r2;
-            const double x = sigma2 * inv_r2;
-            const double r6 = x * x * x;
-            const double r12 = r6 * r6;
-            const double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
-            fx += scale * dx;
-            fy += scale * dy;
-            fz += scale * dz;
-            e += eps4 * (r12 - r6);
-            w += scale * r2;
+            double px[kLjUnroll], py[kLjUnroll], pz[kLjUnroll];
+#pragma unroll
+            for (int u = 0; u < kLjUnroll; u++) {
+                const int q = j[u] < 0 ? 0 : j[u];
+                px[u] = pr[3 * q];
+                py[u] = pr[3 * q + 1];
+                pz[u] = pr[3 * q + 2];
+            }
+#pragma unroll
+            for (int u = 0; u < kLjUnroll; u++) {
+                if (j[u] < 0) break;
+                double dx, dy, dz;
+                exact_disp(im, xi, yi, zi, px[u], py[u], pz[u], dx, dy, dz);
+                const double r2 = exact_r2(dx, dy, dz);
+                if (r2 > rc2) continue;
+                if (r2 < RB_MIN_DISTANCE_SQ) {
+                    bad = true;
+                    continue;
+                }
+                const double inv_r2 = 1.0 / r2;
+                const double x = sigma2 * inv_r2;
+                const double r6 = x * x * x;
+                const double r12 = r6 * r6;
+                const double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
+                fx += scale * dx;
+                fy += scale * dy;
+                fz += scale * dz;
+                e += eps4 * (r12 - r6);
+                w += scale * r2;
+            }
         }
     }
     fx = group_sum<kLjGroup>(fx);

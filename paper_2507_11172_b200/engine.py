@@ -84,11 +84,40 @@ class ForceEngine:
         self.owned_rank = None  # uint8 per rank in decomposed runs
         self._geom_key = None
         self._grid = None
+        self._stream_override = None  # capture of a conditional body
 
     # ------------------------------------------------------------------ misc
     @property
     def stream(self):
+        if self._stream_override is not None:
+            return self._stream_override
         return _lib.stream_handle()
+
+    def rebuild(self, geom: Geometry, r_list: float, capacity: int, pos=None, tag: int = 0,
+                conditional: bool = True) -> None:
+        """Gated rebuild (binning, rows, mirror) of the device loop.
+
+        Inside a CUDA-graph capture the nine gated launches go into the body
+        of a conditional node (rb_rebuild_cond_begin), so steps whose gate is
+        closed skip them; outside a capture they are launched directly."""
+        if conditional:
+            body = ctypes.c_void_p()
+            st = self.L.rb_rebuild_cond_begin(ptr(self.rebuild_flag), ptr(self.status), int(tag),
+                                              self.stream, ctypes.byref(body))
+            if st == _lib.RB_OK:
+                parent = self.stream
+                self._stream_override = body
+                try:
+                    self.bin(geom, pos, gated=True, tag=tag)
+                    self.nlist(geom, r_list, capacity=capacity, checked=False, gated=True, tag=tag)
+                finally:
+                    self._stream_override = None
+                    _lib.check(self.L.rb_rebuild_cond_end(parent), "rb_rebuild_cond_end")
+                return
+            if st != _lib.RB_NOT_CAPTURING:
+                _lib.check(st, "rb_rebuild_cond_begin")
+        self.bin(geom, pos, gated=True, tag=tag)
+        self.nlist(geom, r_list, capacity=capacity, checked=False, gated=True, tag=tag)
 
     def grid_struct(self, geom):
         if geom != self._geom_key:

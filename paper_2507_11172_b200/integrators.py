@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -170,6 +171,8 @@ class DeviceRespa:
         self.slots = None
         self.geom = None
         self.graph = None
+        # captured steps put the rebuild into a conditional graph node
+        self.cond_rebuild = os.environ.get("RB_COND_REBUILD", "1") != "0"
 
     # -------------------------------------------------------------- pieces
     def _geom(self):
@@ -193,9 +196,12 @@ class DeviceRespa:
             if with_triplet:
                 self.f3.fill_(float("nan"))
             return
-        gated = self.periodic
-        eng.bin(geom, self.x, gated=gated, tag=tag)
-        eng.nlist(geom, self.r_build, capacity=self.capacity, checked=False, gated=gated, tag=tag)
+        if self.periodic:  # Verlet rows: rebuild only when the drift flagged it
+            eng.rebuild(geom, self.r_build, self.capacity, self.x, tag=tag,
+                        conditional=self.cond_rebuild)
+        else:
+            eng.bin(geom, self.x, tag=tag)
+            eng.nlist(geom, self.r_build, capacity=self.capacity, checked=False, tag=tag)
         eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag, reduce=False)
         if with_triplet:
             if self.with_3b:

@@ -178,6 +178,30 @@ def test_random_systems_against_oracle(pkg, oracle, rng):
         assert pkg.triplet_count(s, 2.5) == count
 
 
+def test_triplet_overflow_launch_matches_oracle(pkg, oracle):
+    """Bases whose S+ exceeds the main launch's slots go to the second
+    (full-slot) launch; the forces must not depend on which launch ran."""
+    from paper_2507_11172_b200.containers import engine_for
+
+    s = pkg.systems.fcc_system(8, jitter=0.05, seed=9)
+    ff = pkg.ForceField(nu=0.4, cutoff=3.0)
+    c = pkg.CudaLinkedCells()
+    c.triplet_pass(s, ff)
+    eng = engine_for(s.positions.shape[0])
+    assert eng.slots > 64
+    import torch
+
+    words = eng.atm_scratch.view(torch.int32)  # own, G (doubles), then the overflow list
+    listed = int(words[2 * eng.n * 3 * (1 + eng.capacity)].item())
+    assert 0 < listed < eng.n
+    os_ = oracle.OracleSystem.from_positions(s.positions, s.box, True)
+    off = oracle.OracleForceField(nu=0.4, cutoff=3.0)
+    rf3, re3, _, count = oracle.brute_force_triplets(os_, off, cutoff=3.0)
+    assert normwise(s.forces_3b, rf3) <= FORCE_TOL
+    assert _rel(c.triplet_energy, re3) <= ENERGY_TOL
+    assert c.triplet_count == count
+
+
 def test_open_boundaries_against_oracle(pkg, oracle, rng):
     """Non-periodic grids (origin/extent from the particles, containers.py:255-259)."""
     ff = pkg.ForceField(nu=0.7, cutoff=2.5)

@@ -267,7 +267,9 @@ def ours_arm(args, cfg):
     l0 = L.rb_launch_count()
     graphs = run.capture_steps()
     launches_per_period = L.rb_launch_count() - l0
-    launches_per_step = launches_per_period / sf
+    # kernels of the conditional rebuild body run only on rebuild steps
+    body = run.eng.cond_body_launches
+    launches_per_step = launches_per_period / sf - body
     step = sf
     for _ in range(W):
         graphs[step % sf].replay()
@@ -279,6 +281,7 @@ def ours_arm(args, cfg):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    rebuilds0 = int(run.eng.status[3].item())
     with ClockSampler(local) as clocks:
         for k in range(K):
             L.rb_l2_flush(_lib.ptr(flush), flush.numel(), stream)
@@ -290,6 +293,7 @@ def ours_arm(args, cfg):
     if world > 1:
         torch.distributed.barrier()
     ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    rebuilds = int(run.eng.status[3].item()) - rebuilds0
     status = run.eng.read_status()
     if status is not None or run.eng.overflowed():
         raise RuntimeError(f"device error during the timed run: {status}")
@@ -354,15 +358,19 @@ def ours_arm(args, cfg):
 
     # ---- e2e through the public API on host arrays
     e2e_steps = (K + sf - 1) // sf * sf
-    # warm-up call (module loading, allocator, graph instantiation paths)
+    # warm-up call (module loading, allocator, graph instantiation paths),
+    # then the median of three timed calls
     pkg.respa_run(cfg.system(), ff, pkg.CudaLinkedCells(),
                   pkg.RespaSchedule(cfg.dt, sf, max(W, 3) * sf))
-    host = cfg.system()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    pkg.respa_run(host, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(cfg.dt, sf, e2e_steps))
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    e2e_runs = []
+    for _ in range(3):
+        host = cfg.system()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pkg.respa_run(host, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(cfg.dt, sf, e2e_steps))
+        torch.cuda.synchronize()
+        e2e_runs.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e_runs)
     n = s.positions.shape[0]
     h2d = 2 * n * 24  # positions + velocities
     d2h = 4 * n * 24 + (e2e_steps // sf + 1) * 64  # x, v, f2, f3 + trace rows
@@ -392,9 +400,11 @@ def ours_arm(args, cfg):
         "e2e": {"value": e2e_steps / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d / e2e_steps,
                 "d2h_bytes_per_step": d2h / e2e_steps,
                 "note": f"public respa_run({e2e_steps} steps) on host numpy arrays, wall clock "
-                        f"incl. upload, graph capture, download"},
-        "gpu_launches": int(round(launches_per_step * K)) + K,
-        "gpu_launches_detail": {"per_step": launches_per_step, "l2_flush_per_step": 1},
+                        f"incl. upload, graph capture, download; median of 3 calls "
+                        f"({', '.join(f'{1e3 * t:.1f}' for t in e2e_runs)} ms)"},
+        "gpu_launches": int(round(launches_per_step * K)) + rebuilds * body + K,
+        "gpu_launches_detail": {"per_step": launches_per_step, "l2_flush_per_step": 1,
+                                "rebuild_steps": rebuilds, "per_rebuild": body},
         "clocks": clocks.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:

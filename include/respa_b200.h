@@ -149,10 +149,13 @@ RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_co
  * member; forces on all three members are accumulated without atomics in a
  * fixed order (deterministic).  Writes forces (n,3) in particle order
  * (overwritten), per-rank energy (phi per owned triplet), virial and the
- * number of owned (unique) triplets.  Scratch: rb_atm_scratch_bytes.
- * slot_capacity (<= capacity) sizes the per-warp shared-memory slots; a
- * particle with more higher-rank neighbours than that records
- * RB_KIND_CAPACITY in the status word (pass the longest row length).
+ * number of owned (unique) triplets.  Scratch: rb_atm_scratch_bytes,
+ * zero-filled before its first use (each pass leaves its overflow-list
+ * count at zero).  slot_capacity (<= capacity) sizes the per-warp
+ * shared-memory slots; a particle with more higher-rank neighbours than
+ * that records RB_KIND_CAPACITY in the status word (pass the longest row
+ * length).  The pass runs most particles with about half the slots (higher
+ * occupancy) and the few longer S+ sets in a second full-slot launch.
  * `owned` (rank-indexed, NULL = all): in decomposed runs a triplet's
  * energy/virial is weighted by (owned members)/3, the reference's phi/3 per
  * member; forces on ghosts are computed and left to the caller to drop. */
@@ -198,6 +201,12 @@ RB_API int rb_reduce_sum_i32(int64_t n, const int32_t *in, int64_t *out, void *s
  *        (non-NULL) scatters x into pos_r via rank_of, and sets
  *        *rebuild_flag = tag when a particle moved more than skin/2 from
  *        x_ref (the neighbour rows, built at rc + skin, must be rebuilt).
+ *        advance_step != 0 (tag must be -1): the drift opens a new device
+ *        step -- its tag is status[1] + 1 and it leaves status[1] at that
+ *        value for the step's later kernels (rb_step_begin folded in; uses
+ *        status[2] as a block ticket).  rebuild_cond != 0: a CUDA-graph
+ *        conditional handle (rb_rebuild_cond_create) set to 1 together with
+ *        the rebuild flag.
  * kick:  v += half_dt*(f2_old + f2_new); f2_old = f2_new (:159);
  *        [v += half_respa*f3 if kick3];
  *        non-finite v records RB_KIND_NONFINITE at `tag`. */
@@ -206,14 +215,17 @@ RB_API int rb_respa_drift(int64_t n, double *pos, double *vel, const double *f2_
                           double half_drift, double half_respa, int32_t kick3,
                           const int32_t *rank_of, double *pos_r, const double *x_ref,
                           double skin, int64_t *rebuild_flag, unsigned long long *status,
-                          int64_t tag, void *stream);
+                          int64_t tag, int32_t advance_step, uint64_t rebuild_cond,
+                          void *stream);
 RB_API int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f2_new,
                   const double *f3, double half_dt, double half_respa, int32_t kick3,
                   unsigned long long *status, int64_t tag, void *stream);
 
 /* ---- device-side step counter and trace (CUDA-graph friendly) ---------
- * status points to TWO words: status[0] the error word, status[1] the step
- * counter.  Kernels given tag == -1 read their tag from status[1].
+ * status points to FOUR words: status[0] the error word, status[1] the step
+ * counter, status[2] a ticket of rb_respa_drift's step advance (zero
+ * between launches), status[3] the number of steps whose step-opening drift
+ * flagged a row rebuild (diagnostic).  Kernels given tag == -1 read their tag from status[1].
  * rb_step_begin increments status[1]; rb_trace_record writes the 8-double
  * row [tag, sum v^2, E2, W2, E3, W3, 0, 0] at trace[8 * (tag / interval)]
  * from device scalars (RunTrace.record, integrators.py:74-83). */
@@ -223,19 +235,31 @@ RB_API int rb_trace_record(const unsigned long long *status, int64_t sample_inte
                            const double *e3, const double *w3, void *stream);
 
 /* ---- conditional rebuild inside a captured step (CUDA graph IF node) ----
- * In a CUDA-graph capture of `stream`, the gated rebuild (rb_bin, rb_nlist,
- * rb_nlist_mirror with rebuild_flag set) costs nine launches per step even
- * when its gate is closed.  rb_rebuild_cond_begin appends a one-thread node
- * that evaluates the gate (*rebuild_flag == tag, tag < 0: status[1]) and an
- * IF node whose body runs only when it is open, and returns in *body_stream
- * a stream capturing into that body: launch the gated rebuild there, then
- * call rb_rebuild_cond_end(stream) to continue the capture after the IF node.
- * Outside a capture it returns RB_NOT_CAPTURING and nothing is launched (the
- * caller launches the gated kernels on `stream`; results are identical).
- * One conditional may be open per host thread. */
-RB_API int rb_rebuild_cond_begin(const int64_t *rebuild_flag, const unsigned long long *status,
-                                 int64_t tag, void *stream, void **body_stream);
+ * In a CUDA-graph capture the gated rebuild (rb_bin, rb_nlist,
+ * rb_nlist_mirror with rebuild_flag set) would cost nine launches per step
+ * even when its gate is closed.  rb_rebuild_cond_create makes a conditional
+ * handle in the graph `stream` is capturing into (RB_NOT_CAPTURING outside
+ * a capture: launch the gated kernels directly, results are identical); it
+ * is passed to rb_respa_drift, which sets it with the rebuild flag.
+ * rb_rebuild_cond_begin appends the IF node on that handle and returns in
+ * *body_stream a stream capturing into its body: launch the gated rebuild
+ * there, then rb_rebuild_cond_end(stream) continues the capture after the
+ * node.  One conditional may be open per host thread. */
+RB_API int rb_rebuild_cond_create(void *stream, uint64_t *handle);
+RB_API int rb_rebuild_cond_begin(uint64_t handle, void *stream, void **body_stream);
 RB_API int rb_rebuild_cond_end(void *stream);
+
+/* One sample point of the device loop in a single launch: sums[0..4] =
+ * (sum v^2 over the 3n velocity components, sum E2, W2, E3, W3 over the n
+ * rank entries), each bit-identical to rb_reduce_sum(sq)_f64 of the same
+ * array, and -- trace != NULL -- the rb_trace_record row.  `scratch`
+ * (rb_sample_scratch_bytes) must be zero-filled before its first use; every
+ * launch leaves it that way. */
+RB_API size_t rb_sample_scratch_bytes(int64_t n);
+RB_API int rb_sample(int64_t n, const double *vel, const double *e2_rank, const double *w2_rank,
+                     const double *e3_rank, const double *w3_rank, double *sums,
+                     const unsigned long long *status, int64_t sample_interval, double *trace,
+                     void *scratch, size_t scratch_bytes, void *stream);
 
 /* ---- device timing helpers for bench.py (events on the launch stream) -- */
 /* FP64 FMA throughput microbenchmark: runs `iters` dependent-chain DFMA

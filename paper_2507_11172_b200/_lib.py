@@ -36,6 +36,7 @@ _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
 _D = ctypes.c_double
 _SZ = ctypes.c_size_t
+_U64 = ctypes.c_uint64
 
 
 class RbGrid(ctypes.Structure):
@@ -79,13 +80,16 @@ SIGNATURES = {
     "rb_reduce_sumsq_f64": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
     "rb_reduce_sum_i32": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
     "rb_respa_drift": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _I32, _D, _D, _D, _I32, _P, _P, _P, _D,
-                                      _P, _P, _I64, _P]),
+                                      _P, _P, _I64, _I32, _U64, _P]),
     "rb_respa_kick": (ctypes.c_int, [_I64, _P, _P, _P, _P, _D, _D, _I32, _P, _I64, _P]),
     "rb_step_begin": (ctypes.c_int, [_P, _P]),
     "rb_trace_record": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "rb_fp64_peak": (ctypes.c_int, [_I32, _P, _P]),
     "rb_l2_flush": (ctypes.c_int, [_P, _SZ, _P]),
-    "rb_rebuild_cond_begin": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
+    "rb_sample_scratch_bytes": (ctypes.c_size_t, [_I64]),
+    "rb_sample": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _SZ, _P]),
+    "rb_rebuild_cond_create": (ctypes.c_int, [_P, _P]),
+    "rb_rebuild_cond_begin": (ctypes.c_int, [_U64, _P, _P]),
     "rb_rebuild_cond_end": (ctypes.c_int, [_P]),
 }
 

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kAtmWarps * 32)
           double *__restrict__ virial_rank, int32_t *__restrict__ visits_rank,
           unsigned long long *status, int64_t tag, const int64_t *__restrict__ row_offset,
           int32_t *__restrict__ visit_rows) {
+    pdl_enter();
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -311,14 +312,12 @@ extern "C" int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *pos_r,
     cudaStream_t st = as_stream(stream);
     if (exact_image) {
         grant_smem(k_atm<true, false>, smem, g_granted[0]);
-        k_atm<true, false><<<blocks, warps * 32, smem, st>>>(
-            *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, nu,
+        launch(k_atm<true, false>, dim3(blocks), dim3(warps * 32), smem, st, *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, nu,
             forces, energy_rank, virial_rank, visits_rank, status, tag, nullptr, nullptr);
         note_launches(1);
     } else {
         grant_smem(k_atm<false, false>, smem, g_granted[1]);
-        k_atm<false, false><<<blocks, warps * 32, smem, st>>>(
-            *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2,
+        launch(k_atm<false, false>, dim3(blocks), dim3(warps * 32), smem, st, *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2,
             rc2 * (1.0 - kAtmMargin), rc2 * (1.0 + kAtmMargin), nu, forces, energy_rank,
             virial_rank, visits_rank, status, tag, nullptr, nullptr);
         note_launches(1);
@@ -343,8 +342,7 @@ extern "C" int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *pos_
     const unsigned blocks = (unsigned)((n + warps - 1) / warps);
     // the instrumentation always takes the exact raw-position predicate
     grant_smem(k_atm<true, true>, smem, g_granted[2]);
-    k_atm<true, true><<<blocks, warps * 32, smem, as_stream(stream)>>>(
-        *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, 0.0, nullptr,
+    launch(k_atm<true, true>, dim3(blocks), dim3(warps * 32), smem, as_stream(stream), *g, n, pos_r, cell_particles, rows, row_count, capacity, rc2, rc2, rc2, 0.0, nullptr,
         nullptr, nullptr, nullptr, nullptr, 0, row_offset, visit_rows);
     note_launches(1);
     return launch_status();

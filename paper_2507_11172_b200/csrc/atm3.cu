@@ -262,7 +262,8 @@ __device__ __forceinline__ bool a3_accept(const A3Smem &sm, const float4 &ps, in
 
 // One base particle r (rank order) per warp.  `ovf` (main pass with a
 // reduced slot count): a base whose S+(r) does not fit is appended to the
-// overflow list ovf[1..] (count ovf[0]) and left to k_atm3_overflow.
+// overflow list ovf[2..] (count ovf[0]) and left to k_atm3_overflow; the
+// gather moves the count to ovf[1] and clears ovf[0].
 template <bool kExactImage>
 __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid &g, int64_t n, const double *__restrict__ pr,
                                        const int32_t *__restrict__ rows,
@@ -314,7 +315,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
         if (m + __popc(mk) > slots) {  // S+(i) does not fit the shared-memory slots
             if (lane == 0) {
                 if (ovf)
-                    ovf[1 + atomicAdd(ovf, 1)] = (int32_t)r;
+                    ovf[2 + atomicAdd(ovf, 1)] = (int32_t)r;
                 else
                     record_status(status, tag, RB_KIND_CAPACITY);
             }
@@ -484,6 +485,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
            unsigned long long *status, int64_t tag, int debug_mode, int32_t *ovf) {
+    pdl_enter();
     extern __shared__ __align__(16) char smem_raw[];
     const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (r >= n) return;
@@ -502,12 +504,13 @@ __global__ void __launch_bounds__(kA3Warps * 32)
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
            unsigned long long *status, int64_t tag, int debug_mode, const int32_t *ovf) {
+    pdl_enter();
     extern __shared__ __align__(16) char smem_raw[];
     const int wpb = blockDim.x >> 5;
     const int cnt = *(volatile const int32_t *)ovf;
     for (int64_t q = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); q < cnt;
          q += (int64_t)gridDim.x * wpb)
-        a3_base<kExactImage>(ovf[1 + q], smem_raw, g, n, pr, rows, row_count, mirror, capacity, slots, rc2, rc2_lo,
+        a3_base<kExactImage>(ovf[2 + q], smem_raw, g, n, pr, rows, row_count, mirror, capacity, slots, rc2, rc2_lo,
                             rc2_hi, rc2f_lo, rc2f_hi, own, gbuf, energy_rank, virial_rank,
                             triplets_rank, owned, status, tag, debug_mode, nullptr);
 }
@@ -524,7 +527,12 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
                               const double *__restrict__ own, const double *__restrict__ gbuf,
                               double two_nu, double nu, double *__restrict__ forces,
                               double *__restrict__ energy_rank, double *__restrict__ virial_rank,
-                              const unsigned long long *status, int64_t tag) {
+                              const unsigned long long *status, int64_t tag, int32_t *ovf) {
+    pdl_enter();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // list empty for the next pass
+        ovf[1] = ovf[0];                           // (count of this pass: diagnostic)
+        ovf[0] = 0;
+    }
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t p = gid / kGatherGroup;
     const int sub = (int)(gid % kGatherGroup);
@@ -571,7 +579,7 @@ using namespace rb;
 extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
     // own (n x 3) + G (n x capacity x 3), doubles; overflow list (1 + n) int32
     const size_t nn = (size_t)(n > 0 ? n : 1);
-    return nn * 3 * sizeof(double) * (size_t)(1 + capacity) + (nn + 1) * sizeof(int32_t);
+    return nn * 3 * sizeof(double) * (size_t)(1 + capacity) + (nn + 2) * sizeof(int32_t);
 }
 
 namespace rb {
@@ -604,10 +612,8 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
     const size_t per = a3_warp_bytes(fast);
     const int warps = a3_warps_for(per);
     const bool split = fast < full;
-    if (split) cudaMemsetAsync(ovf, 0, sizeof(int32_t), st);
     a3_grant(k_atm3<kExactImage>, warps * per, granted_main);
-    k_atm3<kExactImage><<<(unsigned)((n + warps - 1) / warps), warps * 32, warps * per, st>>>(
-        g, n, pos_r, rows, row_count, mirror, capacity, fast, rc2, lo, hi, flo, fhi, own, gbuf,
+    launch(k_atm3<kExactImage>, dim3((unsigned)((n + warps - 1) / warps)), dim3(warps * 32), warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity, fast, rc2, lo, hi, flo, fhi, own, gbuf,
         energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
         split ? ovf : nullptr);
     note_launches(1);
@@ -617,8 +623,7 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
     const int64_t need = (n + wf - 1) / wf;
     const unsigned blocks = (unsigned)(need < 148 * 4 ? need : 148 * 4);
     a3_grant(k_atm3_overflow<kExactImage>, wf * per_full, granted_ovf);
-    k_atm3_overflow<kExactImage><<<blocks, wf * 32, wf * per_full, st>>>(
-        g, n, pos_r, rows, row_count, mirror, capacity, full, rc2, lo, hi, flo, fhi, own, gbuf,
+    launch(k_atm3_overflow<kExactImage>, dim3(blocks), dim3(wf * 32), wf * per_full, st, g, n, pos_r, rows, row_count, mirror, capacity, full, rc2, lo, hi, flo, fhi, own, gbuf,
         energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode, ovf);
     note_launches(1);
 }
@@ -659,9 +664,8 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
                          ovf);
     const int tb = 256;
     const int64_t threads = n * kGatherGroup;
-    k_atm3_gather<<<(unsigned)((threads + tb - 1) / tb), tb, 0, st>>>(
-        n, cell_particles, rows, row_count, mirror, capacity, own, gbuf, 2.0 * nu, nu, forces,
-        energy_rank, virial_rank, status, tag);
+    launch(k_atm3_gather, dim3((unsigned)((threads + tb - 1) / tb)), dim3(tb), 0, st, n, cell_particles, rows, row_count, mirror, capacity, own, gbuf, 2.0 * nu, nu, forces,
+        energy_rank, virial_rank, status, tag, ovf);
     note_launches(1);
     return launch_status();
 }

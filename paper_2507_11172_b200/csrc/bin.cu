@@ -48,6 +48,7 @@ __device__ __forceinline__ bool gate_closed(const int64_t *flag, const unsigned 
 
 __global__ void k_bin_zero(int64_t ncell, int32_t *__restrict__ count, const int64_t *flag,
                            const unsigned long long *status, int64_t tag) {
+    pdl_enter();
     if (gate_closed(flag, status, tag)) return;
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell;
          c += (int64_t)gridDim.x * blockDim.x)
@@ -57,6 +58,7 @@ __global__ void k_bin_zero(int64_t ncell, int32_t *__restrict__ count, const int
 __global__ void k_bin_count(rb_grid g, int64_t n, const double *__restrict__ pos,
                             int32_t *__restrict__ cell_of, int32_t *__restrict__ count,
                             const int64_t *flag, const unsigned long long *status, int64_t tag) {
+    pdl_enter();
     if (gate_closed(flag, status, tag)) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -73,6 +75,7 @@ __global__ void k_bin_count(rb_grid g, int64_t n, const double *__restrict__ pos
 __global__ void k_bin_scatter(int64_t n, const int32_t *__restrict__ cell_of,
                               int32_t *__restrict__ cursor, int32_t *__restrict__ parts,
                               const int64_t *flag, const unsigned long long *status, int64_t tag) {
+    pdl_enter();
     if (gate_closed(flag, status, tag)) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -94,6 +97,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32)
                   const double *__restrict__ pos, double *__restrict__ pr,
                   double *__restrict__ x_ref, const int64_t *flag,
                   const unsigned long long *status, int64_t tag) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     if (gate_closed(flag, status, tag)) return;
     for (int64_t c = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5); c < ncell;
@@ -172,6 +176,7 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *warp_sums, int &
 __global__ void k_scan_tile_sums(int64_t n, const int32_t *__restrict__ in,
                                  int32_t *__restrict__ tile_sums, const int64_t *flag,
                                  const unsigned long long *status, int64_t tag) {
+    pdl_enter();
     __shared__ int warp_sums[32];
     if (gate_closed(flag, status, tag)) return;
     int64_t base = (int64_t)blockIdx.x * kScanTile;
@@ -189,6 +194,7 @@ __global__ void k_scan_tile_sums(int64_t n, const int32_t *__restrict__ in,
 __global__ void k_scan_tile_offsets(int64_t ntiles, int32_t *__restrict__ tile_sums,
                                     const int64_t *flag, const unsigned long long *status,
                                     int64_t tag) {
+    pdl_enter();
     __shared__ int warp_sums[32];
     if (gate_closed(flag, status, tag)) return;
     int carry = 0;
@@ -206,6 +212,7 @@ __global__ void k_scan_apply(int64_t n, const int32_t *__restrict__ in,
                              const int32_t *__restrict__ tile_off, int32_t *__restrict__ out,
                              int32_t *__restrict__ cursor, const int64_t *flag,
                              const unsigned long long *status, int64_t tag) {
+    pdl_enter();
     __shared__ int warp_sums[32];
     if (gate_closed(flag, status, tag)) return;
     int64_t base = (int64_t)blockIdx.x * kScanTile;
@@ -270,28 +277,26 @@ extern "C" int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *c
     const int tb = 256;
     // gated launches use capped grid-stride grids so a closed gate is cheap
     auto cap = [&](int64_t b) { return (unsigned)(fl && b > 148 * 8 ? 148 * 8 : b); };
-    k_bin_zero<<<(unsigned)std::min<int64_t>(ceil_div(ncell, tb), 148 * 8), tb, 0, st>>>(
-        ncell, count, fl, status, tag);
+    launch(k_bin_zero, dim3((unsigned)std::min<int64_t>(ceil_div(ncell, tb), 148 * 8)), dim3(tb), 0, st, ncell, count, fl, status, tag);
     note_launches(1);
     if (n > 0) {
-        k_bin_count<<<cap(ceil_div(n, tb)), tb, 0, st>>>(*g, n, pos, cell_of, count, fl,
+        launch(k_bin_count, dim3(cap(ceil_div(n, tb))), dim3(tb), 0, st, *g, n, pos, cell_of, count, fl,
                                                                status, tag);
         note_launches(1);
     }
-    k_scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(ncell, count, tiles, fl, status,
+    launch(k_scan_tile_sums, dim3((unsigned)ntiles), dim3(kScanThreads), 0, st, ncell, count, tiles, fl, status,
                                                                  tag);
     note_launches(1);
-    k_scan_tile_offsets<<<1, 1024, 0, st>>>(ntiles, tiles, fl, status, tag);
+    launch(k_scan_tile_offsets, dim3(1), dim3(1024), 0, st, ntiles, tiles, fl, status, tag);
     note_launches(1);
-    k_scan_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(ncell, count, tiles, cell_start,
+    launch(k_scan_apply, dim3((unsigned)ntiles), dim3(kScanThreads), 0, st, ncell, count, tiles, cell_start,
                                                              cursor, fl, status, tag);
     note_launches(1);
     if (n > 0) {
-        k_bin_scatter<<<cap(ceil_div(n, tb)), tb, 0, st>>>(n, cell_of, cursor,
+        launch(k_bin_scatter, dim3(cap(ceil_div(n, tb))), dim3(tb), 0, st, n, cell_of, cursor,
                                                                  cell_particles, fl, status, tag);
         note_launches(1);
-        k_cell_finish<<<cap(ceil_div(ncell, kFinishWarps)), kFinishWarps * 32, 0, st>>>(
-            ncell, cell_start, cell_particles, cell_of_rank, rank_of, pos, pos_r, x_ref, fl,
+        launch(k_cell_finish, dim3(cap(ceil_div(ncell, kFinishWarps))), dim3(kFinishWarps * 32), 0, st, ncell, cell_start, cell_particles, cell_of_rank, rank_of, pos, pos_r, x_ref, fl,
             status, tag);
         note_launches(1);
     }

@@ -17,9 +17,50 @@ static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStre
 // host-side count of kernel launches issued by this library (rb_launch_count)
 void note_launches(int k);
 
+// error of the last failed launch() on this host thread (consumed by launch_status)
+extern thread_local cudaError_t g_launch_error;
+
 static inline int launch_status() {
     cudaError_t e = cudaGetLastError();
+    if (g_launch_error != cudaSuccess) {
+        e = g_launch_error;
+        g_launch_error = cudaSuccess;
+    }
     return e == cudaSuccess ? RB_OK : RB_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch.  Every kernel of the step path is launched
+// with programmatic stream serialization and begins with pdl_enter(): it
+// waits for the preceding kernel to complete (memory visible) before reading
+// anything, then lets the following kernel launch, so consecutive kernels of
+// a captured step overlap launch latency with execution instead of paying
+// it as a gap.  A kernel must never return before pdl_enter() (completion
+// of a kernel then implies completion of everything before it).
+// RB_PDL=0 launches without the attribute (pdl_enter is then a no-op).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_on();
+
+template <typename... KArgs, typename... Args>
+static inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+    if (e != cudaSuccess) g_launch_error = e;
 }
 
 // ---------------------------------------------------------------------------

@@ -3,19 +3,13 @@
 // The device loop (integrators.DeviceRespa) replays one CUDA graph per step;
 // the row rebuild (binning + rows + mirror, nine kernels) is needed only on
 // the steps whose drift flagged it (Verlet skin, integrators.py docstring).
-// Instead of nine gated launches that exit at once, the captured step holds
-// one tiny kernel that evaluates the gate and sets a graph conditional, and
-// an IF node whose body is the rebuild.  The body kernels keep their own gate
-// check, so a body that runs is exactly the gated launch sequence.
+// Instead of nine gated launches that exit at once, the drift sets a graph
+// conditional together with the rebuild flag, and an IF node holds the
+// rebuild.  The body kernels keep their own gate check, so a body that runs
+// is exactly the gated launch sequence.
 #include "common.cuh"
 
 namespace rb {
-
-__global__ void k_rebuild_cond(cudaGraphConditionalHandle h, const int64_t *flag,
-                               const unsigned long long *status, int64_t tag) {
-    tag = resolve_tag(tag, status);
-    if (*(volatile const int64_t *)flag == tag) cudaGraphSetConditional(h, 1u);
-}
 
 namespace {
 struct OpenCond {
@@ -32,9 +26,22 @@ thread_local cudaStream_t g_body_stream = nullptr;
 
 using namespace rb;
 
-extern "C" int rb_rebuild_cond_begin(const int64_t *rebuild_flag, const unsigned long long *status,
-                                     int64_t tag, void *stream, void **body_stream) {
-    if (!rebuild_flag || !body_stream || g_open.open) return RB_ERR_ARGUMENT;
+extern "C" int rb_rebuild_cond_create(void *stream, uint64_t *handle) {
+    if (!handle) return RB_ERR_ARGUMENT;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamGetCaptureInfo(as_stream(stream), &cs, nullptr, &graph) != cudaSuccess)
+        return RB_ERR_CUDA;
+    if (cs != cudaStreamCaptureStatusActive) return RB_NOT_CAPTURING;
+    cudaGraphConditionalHandle h;
+    if (cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault) != cudaSuccess)
+        return RB_ERR_CUDA;
+    *handle = (uint64_t)h;
+    return RB_OK;
+}
+
+extern "C" int rb_rebuild_cond_begin(uint64_t handle, void *stream, void **body_stream) {
+    if (!handle || !body_stream || g_open.open) return RB_ERR_ARGUMENT;
     cudaStream_t s = as_stream(stream);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaGraph_t graph = nullptr;
@@ -46,17 +53,9 @@ extern "C" int rb_rebuild_cond_begin(const int64_t *rebuild_flag, const unsigned
     if (!g_body_stream && cudaStreamCreateWithFlags(&g_body_stream, cudaStreamNonBlocking) !=
                               cudaSuccess)
         return RB_ERR_CUDA;
-    cudaGraphConditionalHandle h;
-    if (cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault) != cudaSuccess)
-        return RB_ERR_CUDA;
-    k_rebuild_cond<<<1, 1, 0, s>>>(h, rebuild_flag, status, tag);
-    note_launches(1);
-    if (cudaGetLastError() != cudaSuccess) return RB_ERR_CUDA;
-    if (cudaStreamGetCaptureInfo(s, &cs, nullptr, &graph, &deps, &nd) != cudaSuccess)
-        return RB_ERR_CUDA;
     cudaGraphNodeParams p = {};
     p.type = cudaGraphNodeTypeConditional;
-    p.conditional.handle = h;
+    p.conditional.handle = (cudaGraphConditionalHandle)handle;
     p.conditional.type = cudaGraphCondTypeIf;
     p.conditional.size = 1;
     cudaGraphNode_t node;

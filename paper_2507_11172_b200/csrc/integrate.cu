@@ -15,11 +15,17 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <cstdlib>
 
 namespace rb {
 
 static std::atomic<long long> g_launches{0};
 void note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+thread_local cudaError_t g_launch_error = cudaSuccess;
+bool pdl_on() {
+    static const bool on = !(getenv("RB_PDL") && atoi(getenv("RB_PDL")) == 0);
+    return on;
+}
 
 // numpy float remainder (npy_divmod) followed by the edge fix of
 // respamd/model.py:279-280
@@ -46,44 +52,65 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
                         double half_drift, double half_respa, int kick3,
                         const int32_t *__restrict__ rank_of, double *__restrict__ pr,
                         const double *__restrict__ x_ref, double skin_half2,
-                        int64_t *rebuild_flag, unsigned long long *status, int64_t tag) {
+                        int64_t *rebuild_flag, unsigned long long *status, int64_t tag,
+                        int advance, cudaGraphConditionalHandle cond) {
+    pdl_enter();
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    tag = resolve_tag(tag, status);
-    if (frozen(status, tag, 0)) return;
-    const double box[3] = {bx, by, bz};
-    double x[3];
-    bool finite = true;
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-        const int64_t i = 3 * p + c;
-        double v = vel[i];
-        if (kick3) {
-            v = xadd(v, xmul(half_respa, f3[i]));
-            vel[i] = v;
-        }
-        double xc = xadd(pos[i], xadd(xmul(dt, v), xmul(half_drift, f2_old[i])));
-        if (periodic) xc = wrap_coord(xc, box[c]);
-        pos[i] = xc;
-        x[c] = xc;
-        finite = finite && isfinite(xc);
-    }
-    if (!finite) record_status(status, tag, RB_KIND_NONFINITE);
-    if (pr && rank_of) {
-        const int64_t r = rank_of[p];
-        pr[3 * r] = x[0];
-        pr[3 * r + 1] = x[1];
-        pr[3 * r + 2] = x[2];
-    }
-    if (x_ref && rebuild_flag) {
-        double d2 = 0.0;
+    // a step-opening drift reads the counter before its block takes a ticket;
+    // the last block publishes the new value (no block reads it after that)
+    tag = advance ? (int64_t)(*(volatile const unsigned long long *)(status + 1)) + 1
+                  : resolve_tag(tag, status);
+    if (p < n && !frozen(status, tag, 0)) {
+        const double box[3] = {bx, by, bz};
+        double x[3];
+        bool finite = true;
 #pragma unroll
         for (int c = 0; c < 3; c++) {
-            double d = x[c] - x_ref[3 * p + c];
-            if (periodic) d = min_image(d, box[c], 0.5 * box[c]);
-            d2 += d * d;
+            const int64_t i = 3 * p + c;
+            double v = vel[i];
+            if (kick3) {
+                v = xadd(v, xmul(half_respa, f3[i]));
+                vel[i] = v;
+            }
+            double xc = xadd(pos[i], xadd(xmul(dt, v), xmul(half_drift, f2_old[i])));
+            if (periodic) xc = wrap_coord(xc, box[c]);
+            pos[i] = xc;
+            x[c] = xc;
+            finite = finite && isfinite(xc);
         }
-        if (!(d2 <= skin_half2)) *rebuild_flag = tag;  // also catches NaN
+        if (!finite) record_status(status, tag, RB_KIND_NONFINITE);
+        if (pr && rank_of) {
+            const int64_t r = rank_of[p];
+            pr[3 * r] = x[0];
+            pr[3 * r + 1] = x[1];
+            pr[3 * r + 2] = x[2];
+        }
+        if (x_ref && rebuild_flag) {
+            double d2 = 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                double d = x[c] - x_ref[3 * p + c];
+                if (periodic) d = min_image(d, box[c], 0.5 * box[c]);
+                d2 += d * d;
+            }
+            if (!(d2 <= skin_half2)) {  // also catches NaN
+                *rebuild_flag = tag;
+                if (cond) cudaGraphSetConditional(cond, 1u);
+            }
+        }
+    }
+    if (advance) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(status + 2, 1ull) == (unsigned long long)(gridDim.x - 1)) {
+                status[2] = 0ull;
+                // every block's flag write precedes its ticket: count rebuild steps
+                if (rebuild_flag && *(volatile const int64_t *)rebuild_flag == tag) status[3] += 1ull;
+                __threadfence();
+                status[1] = (unsigned long long)tag;
+            }
+        }
     }
 }
 
@@ -91,6 +118,7 @@ __global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict_
                        const double *__restrict__ f2_new, const double *__restrict__ f3,
                        double half_dt, double half_respa, int kick3, unsigned long long *status,
                        int64_t tag) {
+    pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n3) return;
     tag = resolve_tag(tag, status);
@@ -122,8 +150,8 @@ __global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict_
 constexpr int kRedThreads = 256;
 constexpr int kRedMaxBlocks = 592;  // 4 x 148 SMs
 
-static int red_blocks(int64_t n) {
-    int64_t b = (n + 4095) / 4096;
+__host__ __device__ inline int red_blocks(int64_t n) {
+    int64_t b = (n + 1023) / 1024;  // ~4 entries per thread: latency, not bandwidth
     if (b < 1) b = 1;
     if (b > kRedMaxBlocks) b = kRedMaxBlocks;
     return (int)b;
@@ -147,6 +175,7 @@ __device__ __forceinline__ T block_tree_sum(T v, T *sh) {
 
 template <typename Tin, typename Tacc, bool kSquare>
 __global__ void k_partial_sum(int64_t n, const Tin *__restrict__ in, Tacc *__restrict__ partial) {
+    pdl_enter();
     __shared__ Tacc sh[32];
     const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
     const int64_t b = (int64_t)blockIdx.x * chunk;
@@ -162,6 +191,7 @@ __global__ void k_partial_sum(int64_t n, const Tin *__restrict__ in, Tacc *__res
 
 template <typename Tacc>
 __global__ void k_final_sum(int nb, const Tacc *__restrict__ partial, Tacc *__restrict__ out) {
+    pdl_enter();
     __shared__ Tacc sh[32];
     Tacc acc = 0;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) acc += partial[i];
@@ -169,14 +199,98 @@ __global__ void k_final_sum(int nb, const Tacc *__restrict__ partial, Tacc *__re
     if (threadIdx.x == 0) out[0] = s;
 }
 
+// Sample point of the device loop in one launch: the five sums of a trace
+// row (sum v^2 over 3n, E2, W2, E3, W3 over the n rank entries), each with
+// the partition and trees of k_partial_sum/k_final_sum (bit-identical to the
+// separate reductions); the block that finishes last (ticket) folds the
+// partials in index order and writes the trace row.
+constexpr int kSampleQ = 5;
+
+__global__ void __launch_bounds__(kRedThreads)
+    k_sample(int64_t n, const double *__restrict__ vel, const double *__restrict__ e2,
+             const double *__restrict__ w2, const double *__restrict__ e3,
+             const double *__restrict__ w3, double *__restrict__ sums,
+             const unsigned long long *status, int64_t interval, double *trace,
+             double *__restrict__ partial, unsigned int *ticket) {
+    pdl_enter();
+    __shared__ double sh[32];
+    __shared__ bool last;
+    {  // sum v^2 over the 3n components (partition of 3n)
+        const int64_t len = 3 * n;
+        const int nb = red_blocks(len);
+        double acc = 0.0;
+        if ((int)blockIdx.x < nb) {
+            const int64_t chunk = (len + nb - 1) / nb;
+            const int64_t b = (int64_t)blockIdx.x * chunk;
+            const int64_t e = b + chunk < len ? b + chunk : len;
+#pragma unroll 4
+            for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) acc += vel[i] * vel[i];
+        }
+        const double t = block_tree_sum<double>(acc, sh);
+        if (threadIdx.x == 0 && (int)blockIdx.x < nb) partial[blockIdx.x] = t;
+        __syncthreads();
+    }
+    {  // E2, W2, E3, W3 share the partition of n: one pass, four accumulators
+        const int nb = red_blocks(n);
+        double a2 = 0.0, b2 = 0.0, a3 = 0.0, b3 = 0.0;
+        if ((int)blockIdx.x < nb) {
+            const int64_t chunk = (n + nb - 1) / nb;
+            const int64_t b = (int64_t)blockIdx.x * chunk;
+            const int64_t e = b + chunk < n ? b + chunk : n;
+#pragma unroll 2
+            for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+                a2 += e2[i];
+                b2 += w2[i];
+                a3 += e3[i];
+                b3 += w3[i];
+            }
+        }
+        const double acc[4] = {a2, b2, a3, b3};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const double t = block_tree_sum<double>(acc[q], sh);
+            if (threadIdx.x == 0 && (int)blockIdx.x < nb) partial[(q + 1) * kRedMaxBlocks + blockIdx.x] = t;
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double out[kSampleQ];
+    for (int q = 0; q < kSampleQ; q++) {
+        const int nb = red_blocks(q == 0 ? 3 * n : n);
+        double acc = 0.0;
+        for (int i = threadIdx.x; i < nb; i += blockDim.x)
+            acc += *(volatile const double *)(partial + q * kRedMaxBlocks + i);
+        out[q] = block_tree_sum<double>(acc, sh);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kSampleQ; q++) sums[q] = out[q];
+        if (trace) {
+            const int64_t tag = (int64_t)status[1];
+            double *row = trace + 8 * (tag / interval);
+            row[0] = (double)tag;
+            for (int q = 0; q < kSampleQ; q++) row[1 + q] = out[q];
+            row[6] = 0.0;
+            row[7] = 0.0;
+        }
+        *ticket = 0u;  // ready for the next launch
+    }
+}
+
 template <typename Tin, typename Tacc, bool kSquare>
 static int reduce_launch(int64_t n, const Tin *in, Tacc *out, void *scratch, void *stream) {
     cudaStream_t st = as_stream(stream);
     const int nb = red_blocks(n);
     Tacc *partial = (Tacc *)scratch;
-    k_partial_sum<Tin, Tacc, kSquare><<<nb, kRedThreads, 0, st>>>(n, in, partial);
+    launch(k_partial_sum<Tin, Tacc, kSquare>, dim3(nb), dim3(kRedThreads), 0, st, n, in, partial);
     note_launches(1);
-    k_final_sum<Tacc><<<1, kRedThreads, 0, st>>>(nb, partial, out);
+    launch(k_final_sum<Tacc>, dim3(1), dim3(kRedThreads), 0, st, nb, partial, out);
     note_launches(1);
     return launch_status();
 }
@@ -204,12 +318,14 @@ __global__ void k_fp64_fma(int iters, double seed, double *sink) {
     if (s == 12345.678) sink[0] = s;  // keep the chains alive
 }
 
-__global__ void k_step_begin(unsigned long long *status) { status[1] += 1ull; }
+__global__ void k_step_begin(unsigned long long *status) {
+    pdl_enter(); status[1] += 1ull; }
 
 // trace row (tag / interval): [tag, sum v^2, E2, W2, E3, W3, 0, 0]
 __global__ void k_trace_record(const unsigned long long *status, int64_t interval, double *trace,
                                const double *sumsq, const double *e2, const double *w2,
                                const double *e3, const double *w3) {
+    pdl_enter();
     const int64_t tag = (int64_t)status[1];
     double *row = trace + 8 * (tag / interval);
     row[0] = (double)tag;
@@ -237,15 +353,17 @@ extern "C" int rb_respa_drift(int64_t n, double *pos, double *vel, const double 
                               double dt, double half_drift, double half_respa, int32_t kick3,
                               const int32_t *rank_of, double *pos_r, const double *x_ref,
                               double skin, int64_t *rebuild_flag, unsigned long long *status,
-                              int64_t tag, void *stream) {
+                              int64_t tag, int32_t advance_step, uint64_t rebuild_cond,
+                              void *stream) {
     if (n < 0 || !box3_host) return RB_ERR_ARGUMENT;
-    if (n == 0) return RB_OK;
+    if (advance_step && (!status || tag >= 0)) return RB_ERR_ARGUMENT;
+    if (n == 0) return advance_step ? rb_step_begin(status, stream) : RB_OK;
     const int tb = 256;
     const double half = 0.5 * skin;
-    k_drift<<<(unsigned)((n + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
-        n, pos, vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt,
+    launch(k_drift, dim3((unsigned)((n + tb - 1) / tb)), dim3(tb), 0, as_stream(stream), n, pos, vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt,
         half_drift, half_respa, kick3, rank_of, pos_r, x_ref, half * half * (1.0 - 1e-9),
-        rebuild_flag, status, tag);
+        rebuild_flag, status, tag, advance_step ? 1 : 0,
+        (cudaGraphConditionalHandle)rebuild_cond);
     note_launches(1);
     return launch_status();
 }
@@ -257,14 +375,36 @@ extern "C" int rb_respa_kick(int64_t n, double *vel, double *f2_old, const doubl
     if (n == 0) return RB_OK;
     const int64_t n3 = 3 * n;
     const int tb = 256;
-    k_kick<<<(unsigned)((n3 + tb - 1) / tb), tb, 0, as_stream(stream)>>>(
-        n3, vel, f2_old, f2_new, f3, half_dt, half_respa, kick3, status, tag);
+    launch(k_kick, dim3((unsigned)((n3 + tb - 1) / tb)), dim3(tb), 0, as_stream(stream), n3, vel, f2_old, f2_new, f3, half_dt, half_respa, kick3, status, tag);
     note_launches(1);
     return launch_status();
 }
 
 extern "C" size_t rb_reduce_scratch_bytes(int64_t n) {
     return (size_t)kRedMaxBlocks * sizeof(double);
+}
+
+extern "C" size_t rb_sample_scratch_bytes(int64_t n) {
+    return (size_t)kSampleQ * kRedMaxBlocks * sizeof(double) + 256;
+}
+
+extern "C" int rb_sample(int64_t n, const double *vel, const double *e2_rank,
+                         const double *w2_rank, const double *e3_rank, const double *w3_rank,
+                         double *sums, const unsigned long long *status, int64_t sample_interval,
+                         double *trace, void *scratch, size_t scratch_bytes, void *stream) {
+    if (n < 0 || !vel || !e2_rank || !w2_rank || !e3_rank || !w3_rank || !sums || !scratch)
+        return RB_ERR_ARGUMENT;
+    if (scratch_bytes < rb_sample_scratch_bytes(n)) return RB_ERR_ARGUMENT;
+    if (trace && (!status || sample_interval <= 0)) return RB_ERR_ARGUMENT;
+    // every sum keeps its own partition (the v^2 sum spans 3n entries)
+    const int nb = red_blocks(3 * n);
+    double *partial = (double *)scratch;
+    unsigned int *ticket = (unsigned int *)(partial + kSampleQ * kRedMaxBlocks);
+    launch(k_sample, dim3(nb), dim3(kRedThreads), 0, as_stream(stream), n, vel, e2_rank, w2_rank, e3_rank,
+                                                       w3_rank, sums, status, sample_interval,
+                                                       trace, partial, ticket);
+    note_launches(1);
+    return launch_status();
 }
 
 extern "C" int rb_reduce_sum_f64(int64_t n, const double *in, double *out, void *scratch,
@@ -316,7 +456,7 @@ extern "C" int rb_fp64_peak(int32_t iters, double *tflops, void *stream) {
 
 extern "C" int rb_step_begin(unsigned long long *status, void *stream) {
     if (!status) return RB_ERR_ARGUMENT;
-    k_step_begin<<<1, 1, 0, as_stream(stream)>>>(status);
+    launch(k_step_begin, dim3(1), dim3(1), 0, as_stream(stream), status);
     note_launches(1);
     return launch_status();
 }
@@ -326,7 +466,7 @@ extern "C" int rb_trace_record(const unsigned long long *status, int64_t sample_
                                const double *w2, const double *e3, const double *w3,
                                void *stream) {
     if (!status || !trace || sample_interval <= 0) return RB_ERR_ARGUMENT;
-    k_trace_record<<<1, 1, 0, as_stream(stream)>>>(status, sample_interval, trace, sumsq, e2, w2,
+    launch(k_trace_record, dim3(1), dim3(1), 0, as_stream(stream), status, sample_interval, trace, sumsq, e2, w2,
                                                    e3, w3);
     note_launches(1);
     return launch_status();

@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(kLjThreads)
          double *__restrict__ forces, double *__restrict__ energy_rank,
          double *__restrict__ virial_rank, const uint8_t *__restrict__ owned,
          unsigned long long *status, int64_t tag) {
+    pdl_enter();
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t r = gid / kLjGroup;
     const int sub = (int)(gid % kLjGroup);
@@ -117,8 +118,7 @@ extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r, cons
     if (n == 0) return RB_OK;
     const int64_t threads = n * kLjGroup;
     unsigned blocks = (unsigned)((threads + kLjThreads - 1) / kLjThreads);
-    k_lj<<<blocks, kLjThreads, 0, as_stream(stream)>>>(
-        *g, n, pos_r, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
+    launch(k_lj, dim3(blocks), dim3(kLjThreads), 0, as_stream(stream), *g, n, pos_r, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
         4.0 * epsilon, sigma * sigma, forces, energy_rank, virial_rank, owned, status, tag);
     note_launches(1);
     return launch_status();

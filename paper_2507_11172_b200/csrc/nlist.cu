@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
             double rl2, int32_t capacity, int32_t *__restrict__ rows,
             int32_t *__restrict__ row_count, int32_t *__restrict__ max_count,
             const int64_t *flag, const unsigned long long *status, int64_t tag) {
+    pdl_enter();
     if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
     for (int64_t r = (int64_t)blockIdx.x * kNlistWarps + (threadIdx.x >> 5); r < n;
          r += (int64_t)gridDim.x * kNlistWarps)
@@ -124,6 +125,7 @@ __global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
                          const int32_t *__restrict__ row_count, int32_t capacity,
                          int32_t *__restrict__ mirror, const int64_t *flag,
                          const unsigned long long *status, int64_t tag) {
+    pdl_enter();
     if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
     for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < n * (int64_t)capacity;
          gid += (int64_t)gridDim.x * blockDim.x) {
@@ -165,8 +167,7 @@ extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const 
     const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
     int64_t blocks = (n + kNlistWarps - 1) / kNlistWarps;
     if (rebuild_flag && blocks > 148 * 8) blocks = 148 * 8;  // gated: grid-stride
-    k_nlist<<<(unsigned)blocks, kNlistWarps * 32, 0, as_stream(stream)>>>(
-        *g, n, pos_r, cell_start, cell_of_rank, rl2, capacity, rows, row_count, max_count,
+    launch(k_nlist, dim3((unsigned)blocks), dim3(kNlistWarps * 32), 0, as_stream(stream), *g, n, pos_r, cell_start, cell_of_rank, rl2, capacity, rows, row_count, max_count,
         rebuild_flag, status, tag);
     note_launches(1);
     return launch_status();
@@ -181,8 +182,7 @@ extern "C" int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *ro
     const int tb = 256;
     int64_t mblocks = (threads + tb - 1) / tb;
     if (mblocks > 148 * 16) mblocks = 148 * 16;  // grid-stride
-    k_mirror<<<(unsigned)mblocks, tb, 0, as_stream(stream)>>>(
-        n, rows, row_count, capacity, mirror, rebuild_flag, status, tag);
+    launch(k_mirror, dim3((unsigned)mblocks), dim3(tb), 0, as_stream(stream), n, rows, row_count, capacity, mirror, rebuild_flag, status, tag);
     note_launches(1);
     return launch_status();
 }

@@ -67,13 +67,17 @@ class ForceEngine:
         self.v_rank = torch.zeros(n, dtype=i32, device=dev)
         self.row_count = torch.zeros(n, dtype=i32, device=dev)
         self.max_count = torch.zeros(1, dtype=i32, device=dev)
-        # status[0]: error word (all ones = clear); status[1]: device step counter
-        self.status = torch.tensor([-1, 0], dtype=i64, device=dev)
+        # status[0]: error word (all ones = clear); status[1]: device step
+        # counter; status[2]: ticket of the step-opening drift; status[3]:
+        # rebuild steps flagged by step-opening drifts
+        self.status = torch.tensor([-1, 0, 0, 0], dtype=i64, device=dev)
         self.rebuild_flag = torch.zeros(1, dtype=i64, device=dev)
         self.scalars = torch.zeros(8, dtype=f64, device=dev)
         self.visits = torch.zeros(1, dtype=i64, device=dev)
         self.red_scratch = torch.empty(
             max(1, int(self.L.rb_reduce_scratch_bytes(n * 3)) // 8), dtype=f64, device=dev)
+        self.sample_scratch = torch.zeros(  # zero-filled once (rb_sample contract)
+            (int(self.L.rb_sample_scratch_bytes(n)) + 7) // 8, dtype=f64, device=dev)
         self.cell_start = None
         self.bin_scratch = None
         self.rows = None
@@ -85,6 +89,7 @@ class ForceEngine:
         self._geom_key = None
         self._grid = None
         self._stream_override = None  # capture of a conditional body
+        self.cond_body_launches = 0  # kernels in the last conditional rebuild body
 
     # ------------------------------------------------------------------ misc
     @property
@@ -93,29 +98,38 @@ class ForceEngine:
             return self._stream_override
         return _lib.stream_handle()
 
+    def rebuild_cond(self) -> int:
+        """Conditional handle for the rebuild of the step being captured
+        (0 when the stream is not capturing)."""
+        h = ctypes.c_uint64(0)
+        st = self.L.rb_rebuild_cond_create(self.stream, ctypes.byref(h))
+        if st == _lib.RB_NOT_CAPTURING:
+            return 0
+        _lib.check(st, "rb_rebuild_cond_create")
+        return int(h.value)
+
     def rebuild(self, geom: Geometry, r_list: float, capacity: int, pos=None, tag: int = 0,
-                conditional: bool = True) -> None:
+                cond: int = 0) -> None:
         """Gated rebuild (binning, rows, mirror) of the device loop.
 
-        Inside a CUDA-graph capture the nine gated launches go into the body
-        of a conditional node (rb_rebuild_cond_begin), so steps whose gate is
-        closed skip them; outside a capture they are launched directly."""
-        if conditional:
+        With a conditional handle (captured step, set by the drift) the nine
+        gated launches go into the body of an IF node, so steps that do not
+        rebuild skip them; without one they are launched directly."""
+        if cond:
             body = ctypes.c_void_p()
-            st = self.L.rb_rebuild_cond_begin(ptr(self.rebuild_flag), ptr(self.status), int(tag),
-                                              self.stream, ctypes.byref(body))
-            if st == _lib.RB_OK:
-                parent = self.stream
-                self._stream_override = body
-                try:
-                    self.bin(geom, pos, gated=True, tag=tag)
-                    self.nlist(geom, r_list, capacity=capacity, checked=False, gated=True, tag=tag)
-                finally:
-                    self._stream_override = None
-                    _lib.check(self.L.rb_rebuild_cond_end(parent), "rb_rebuild_cond_end")
-                return
-            if st != _lib.RB_NOT_CAPTURING:
-                _lib.check(st, "rb_rebuild_cond_begin")
+            _lib.check(self.L.rb_rebuild_cond_begin(cond, self.stream, ctypes.byref(body)),
+                       "rb_rebuild_cond_begin")
+            parent = self.stream
+            self._stream_override = body
+            l0 = self.L.rb_launch_count()
+            try:
+                self.bin(geom, pos, gated=True, tag=tag)
+                self.nlist(geom, r_list, capacity=capacity, checked=False, gated=True, tag=tag)
+            finally:
+                self._stream_override = None
+                self.cond_body_launches = self.L.rb_launch_count() - l0
+                _lib.check(self.L.rb_rebuild_cond_end(parent), "rb_rebuild_cond_end")
+            return
         self.bin(geom, pos, gated=True, tag=tag)
         self.nlist(geom, r_list, capacity=capacity, checked=False, gated=True, tag=tag)
 
@@ -135,6 +149,7 @@ class ForceEngine:
     def reset_status(self, step: int = 0) -> None:
         self.status[0] = -1
         self.status[1] = int(step)
+        self.status[2:].zero_()
 
     def read_status(self):
         """(tag, kind) of the first recorded device error, or None (syncs)."""
@@ -191,7 +206,8 @@ class ForceEngine:
             self.mirror = torch.zeros(max(self.n, 1) * capacity, dtype=torch.int32,
                                       device=self.device)
             need = int(self.L.rb_atm_scratch_bytes(self.n, capacity))
-            self.atm_scratch = torch.empty((need + 7) // 8, dtype=torch.float64, device=self.device)
+            # zero-filled once: the overflow count at its tail (rb_atm_pass contract)
+            self.atm_scratch = torch.zeros((need + 7) // 8, dtype=torch.float64, device=self.device)
             self.capacity = capacity
 
     def nlist(self, geom: Geometry, r_list: float, capacity: Optional[int] = None,
@@ -321,6 +337,18 @@ class ForceEngine:
         out = ctypes.c_void_p(self.scalars.data_ptr() + 8 * slot)
         st = fn(count, ptr(x), out, ptr(self.red_scratch), self.stream)
         _lib.check(st, "rb_reduce")
+
+    def sample(self, vel, trace=None, interval: int = 1) -> None:
+        """scalars[0..4] <- (sum v^2, E2, W2, E3, W3) and, with `trace`, the
+        trace row of the current device step, in one launch."""
+        sc = self.scalars.data_ptr()
+        st = self.L.rb_sample(self.n, ptr(vel), ptr(self.e2_rank), ptr(self.w2_rank),
+                              ptr(self.e3_rank), ptr(self.w3_rank), ctypes.c_void_p(sc),
+                              ptr(self.status), int(interval),
+                              ptr(trace) if trace is not None else _NULL,
+                              ptr(self.sample_scratch), self.sample_scratch.numel() * 8,
+                              self.stream)
+        _lib.check(st, "rb_sample")
 
     def scalar_values(self):
         return self.scalars.cpu().numpy()

@@ -36,7 +36,7 @@ import numpy as np
 from . import _lib
 from ._lib import ptr
 from .containers import CudaLinkedCells, MinimumSeparationError
-from .engine import (SCALAR_E2, SCALAR_E3, SCALAR_SUMSQ, SCALAR_W2, SCALAR_W3, CapacityError,
+from .engine import (SCALAR_E2, SCALAR_E3, SCALAR_W2, SCALAR_W3, CapacityError,
                      ForceEngine, _round_up)
 from .grid import geometry
 from .model import ValidationError, triplet_cutoff
@@ -186,7 +186,7 @@ class DeviceRespa:
             return None  # the drift already recorded the non-finite state
         return geometry(self.box, pos, self.r_build, False)
 
-    def _forces(self, tag: int, with_triplet: bool, f2_out) -> None:
+    def _forces(self, tag: int, with_triplet: bool, f2_out, cond: int = 0) -> None:
         eng = self.eng
         geom = self._geom()
         if geom is None:
@@ -197,8 +197,7 @@ class DeviceRespa:
                 self.f3.fill_(float("nan"))
             return
         if self.periodic:  # Verlet rows: rebuild only when the drift flagged it
-            eng.rebuild(geom, self.r_build, self.capacity, self.x, tag=tag,
-                        conditional=self.cond_rebuild)
+            eng.rebuild(geom, self.r_build, self.capacity, self.x, tag=tag, cond=cond)
         else:
             eng.bin(geom, self.x, tag=tag)
             eng.nlist(geom, self.r_build, capacity=self.capacity, checked=False, tag=tag)
@@ -217,23 +216,18 @@ class DeviceRespa:
         self.eng.reduce_triplet()
 
     def _record(self) -> None:
-        L, eng = self.eng.L, self.eng
-        self._reduce_scalars()
-        eng.sum_f64(self.v, SCALAR_SUMSQ, square=True, n=3 * self.n)
-        base = eng.scalars.data_ptr()
-        sc = [ctypes.c_void_p(base + 8 * k) for k in range(5)]
-        st = L.rb_trace_record(ptr(eng.status), self.interval, ptr(self.trace_dev), sc[0], sc[1],
-                               sc[2], sc[3], sc[4], eng.stream)
-        _lib.check(st, "rb_trace_record")
+        # sums of the five trace scalars + the trace row, one launch
+        self.eng.sample(self.v, self.trace_dev, self.interval)
 
     def _step(self, i: int) -> None:
         """Loop body of integrators.py:148-172 for iteration i (tag i+1)."""
         L, eng = self.eng.L, self.eng
         s = self.schedule.step_size_factor
-        st = L.rb_step_begin(ptr(eng.status), eng.stream)
-        _lib.check(st, "rb_step_begin")
         verlet = self.periodic
         null = ctypes.c_void_p(0)
+        # under capture: the drift sets the rebuild conditional with the flag
+        cond = eng.rebuild_cond() if verlet and self.cond_rebuild else 0
+        # the drift opens the device step (status[1] += 1)
         st = L.rb_respa_drift(self.n, ptr(self.x), ptr(self.v), ptr(self.f2_old), ptr(self.f3),
                               self.box.ctypes.data_as(ctypes.c_void_p), int(self.periodic),
                               self.dt, self.half_drift, self.half_respa, int(i % s == 0),
@@ -241,10 +235,10 @@ class DeviceRespa:
                               ptr(eng.pos_r) if verlet else null,
                               ptr(eng.x_ref) if verlet else null, self.skin,
                               ptr(eng.rebuild_flag) if verlet else null,
-                              ptr(eng.status), _lib.RB_TAG_FROM_DEVICE, eng.stream)
+                              ptr(eng.status), _lib.RB_TAG_FROM_DEVICE, 1, cond, eng.stream)
         _lib.check(st, "rb_respa_drift")
         end_of_cycle = (i + 1) % s == 0
-        self._forces(_lib.RB_TAG_FROM_DEVICE, end_of_cycle, self.f2_new)
+        self._forces(_lib.RB_TAG_FROM_DEVICE, end_of_cycle, self.f2_new, cond)
         st = L.rb_respa_kick(self.n, ptr(self.v), ptr(self.f2_old), ptr(self.f2_new), ptr(self.f3),
                              self.half_dt, self.half_respa, int(end_of_cycle), ptr(eng.status),
                              _lib.RB_TAG_FROM_DEVICE, eng.stream)

@@ -370,6 +370,11 @@ def ours_arm(args, cfg):
         pkg.respa_run(host, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(cfg.dt, sf, e2e_steps))
         torch.cuda.synchronize()
         e2e_runs.append(time.perf_counter() - t0)
+        if os.environ.get("RB_E2E_DEBUG"):
+            from paper_2507_11172_b200 import integrators as _it
+            marks = _it.LAST_RUN[0].marks
+            print("e2e call", " ".join(f"{lab}:{1e3 * (t - t0):.1f}" for lab, t in marks),
+                  file=sys.stderr)
     e2e_s = statistics.median(e2e_runs)
     n = s.positions.shape[0]
     h2d = 2 * n * 24  # positions + velocities

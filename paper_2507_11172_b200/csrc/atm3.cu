@@ -35,6 +35,8 @@
 
 #include "common.cuh"
 
+#include <type_traits>
+
 namespace rb {
 
 constexpr int kA3Warps = 4;
@@ -73,7 +75,11 @@ __host__ __device__ inline size_t a3_warp_bytes(int m) {
     return (b + 15) & ~(size_t)15;
 }
 
-__device__ inline A3Smem a3_carve(char *base, int m) {
+// kM > 0: the slot count is a compile-time constant (every offset folds
+// into the shared-memory addressing); kM == 0: runtime m
+template <int kM>
+__device__ __forceinline__ A3Smem a3_carve(char *base, int m_rt) {
+    const int m = kM > 0 ? kM : m_rt;
     A3Smem s;
     s.dxy = (double2 *)base;
     s.axy = s.dxy + m;
@@ -93,7 +99,8 @@ struct A3Acc {
     double fx, fy, fz, e, w;
     int n;
     bool bad;
-    int owned_i;  // decomposed runs: the base particle is owned by this rank
+    int owned_i;     // decomposed runs: the base particle is owned by this rank
+    bool slot_bad;   // some r_ij^2 of S+(i) is under the guard (checked per triplet then)
 };
 
 constexpr int kKidxMask = 0x3fffffff;
@@ -122,7 +129,7 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // v = a+c-b, w = b+c-a, p = uvw, S = uv+uw+vw, s = abc (potentials.py:82-114):
 //   E   = s^-5/2 (s + 3/8 p)
 //   E_a = 3/8 s^-5/2 (S - 2uv) - bc (3/2 s^-5/2 + 15/16 p s^-7/2), b/c alike.
-template <bool kExactImage>
+template <bool kExactImage, bool kOwned>
 __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im,
                                         const int32_t *__restrict__ row,
                                         const double *__restrict__ pr, A3Acc &acc,
@@ -147,7 +154,9 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
         jkz = ikz - ijz;
         c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
     }
-    if (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ || c < RB_MIN_DISTANCE_SQ) {
+    // guard (potentials.py:35-36): r_ij, r_ik under it were noted per slot
+    if (c < RB_MIN_DISTANCE_SQ ||
+        (acc.slot_bad && (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ))) {
         acc.bad = true;
         fj[0] = fj[1] = fj[2] = fk[0] = fk[1] = fk[2] = 0.0;
         return false;
@@ -172,10 +181,15 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
     acc.fx = fma(-ea, ij.x, fma(-eb, ik.x, acc.fx));
     acc.fy = fma(-ea, ij.y, fma(-eb, ik.y, acc.fy));
     acc.fz = fma(-ea, ijz, fma(-eb, ikz, acc.fz));
-    const double share =
-        owned_share(acc.owned_i + (sm.kidx[s] >> 30) + (sm.kidx[t] >> 30));
-    acc.e = fma(share * s52, fma(0.375, p, sp), acc.e);
-    acc.w = fma(share, fma(ea, a, fma(eb, b, ec * c)), acc.w);
+    if (kOwned) {
+        const double share =
+            owned_share(acc.owned_i + (sm.kidx[s] >> 30) + (sm.kidx[t] >> 30));
+        acc.e = fma(share * s52, fma(0.375, p, sp), acc.e);
+        acc.w = fma(share, fma(ea, a, fma(eb, b, ec * c)), acc.w);
+    } else {
+        acc.e = fma(s52, fma(0.375, p, sp), acc.e);
+        acc.w = fma(ea, a, fma(eb, b, fma(ec, c, acc.w)));
+    }
     acc.n += 1;
     fj[0] = fma(ea, ij.x, -ec * jkx);
     fj[1] = fma(ea, ij.y, -ec * jky);
@@ -197,7 +211,7 @@ __device__ __forceinline__ void a3_add(double2 *axy, double *az, int slot, const
 // evaluate the first `cnt` queue entries and fold f_j / f_k into the slot
 // accumulators, one round-record at a time (records are contiguous runs; in
 // one round all j slots are distinct and all k slots are distinct)
-template <bool kExactImage>
+template <bool kExactImage, bool kOwned>
 __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, const Image &im,
                                          const int32_t *__restrict__ row,
                                          const double *__restrict__ pr, A3Acc &acc,
@@ -206,7 +220,7 @@ __device__ __forceinline__ void a3_chunk(const A3Smem &sm, int cnt, int lane, co
     int s = 0, t = 0, rec = -1;
     bool pending = false;
     if (lane < cnt) {
-        pending = a3_eval<kExactImage>(sm, offset + lane, im, row, pr, acc, fj, fk, s, t);
+        pending = a3_eval<kExactImage, kOwned>(sm, offset + lane, im, row, pr, acc, fj, fk, s, t);
         rec = (int)(sm.qe[offset + lane] >> 22);
     }
     if (debug_mode == 4) {  // debug 4: no slot accumulation
@@ -264,7 +278,7 @@ __device__ __forceinline__ bool a3_accept(const A3Smem &sm, const float4 &ps, in
 // reduced slot count): a base whose S+(r) does not fit is appended to the
 // overflow list ovf[2..] (count ovf[0]) and left to k_atm3_overflow; the
 // gather moves the count to ovf[1] and clears ovf[0].
-template <bool kExactImage>
+template <bool kExactImage, bool kOwned, int kM>
 __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid &g, int64_t n, const double *__restrict__ pr,
                                        const int32_t *__restrict__ rows,
                                        const int32_t *__restrict__ row_count,
@@ -282,7 +296,8 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     const int warp = threadIdx.x >> 5;
     tag = resolve_tag(tag, status);
     if (warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
-    const A3Smem sm = a3_carve(smem_raw + (size_t)warp * a3_warp_bytes(slots), slots);
+    if (kM > 0) slots = kM;
+    const A3Smem sm = a3_carve<kM>(smem_raw + (size_t)warp * a3_warp_bytes(slots), slots);
     const Image im = make_image(g);
     const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
     const int rc_n = row_count[r];
@@ -293,6 +308,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
 
     // ---- phase 0: S+(i), the row suffix with rank > i within rc
     int m = 0;
+    bool slot_bad = false;
     for (int base = 0; base < rc_n; base += 32) {
         const int k = base + lane;
         bool keep = false;
@@ -326,12 +342,13 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
             sm.dxy[slot] = make_double2(dx, dy);
             sm.dz[slot] = dz;
             sm.r2[slot] = r2;
-            sm.kidx[slot] = k | ((owned ? (int)owned[row[k]] : 1) << 30);
+            sm.kidx[slot] = k | ((kOwned ? (int)owned[row[k]] : 1) << 30);
             sm.f4[slot] = make_float4((float)dx, (float)dy, (float)dz, 0.0f);
             sm.axy[slot] = make_double2(0.0, 0.0);
             sm.az[slot] = 0.0;
         }
         m += __popc(mk);
+        slot_bad |= __any_sync(0xffffffffu, keep && r2 < RB_MIN_DISTANCE_SQ);
     }
     __syncwarp();
 
@@ -342,7 +359,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     // accepted pair its queue position in round-major order, each lane
     // writes its own pairs; (C) the queue is evaluated 32 entries at a time,
     // the incomplete tail carried to the next block.
-    A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false, owned ? (int)owned[r] : 1};
+    A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1, slot_bad};
     const int rounds = debug_mode == 1 ? 0 : (m >> 1);  // debug 1: phases 0 and 3 only
     const int nsets = (m + 31) >> 5;
     const int block = max(1, min(kA3RoundBlock, (kA3Queue - 32) / max(m, 1)));
@@ -438,7 +455,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
         int done = 0;
         for (; done + 32 <= qn; done += 32) {
             if (debug_mode != 3)
-                a3_chunk<kExactImage>(sm, 32, lane, im, row, pr, acc, debug_mode, done);
+                a3_chunk<kExactImage, kOwned>(sm, 32, lane, im, row, pr, acc, debug_mode, done);
         }
         __syncwarp();
         if (done > 0 && lane < qn - done) sm.qe[lane] = sm.qe[done + lane];
@@ -446,7 +463,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
         __syncwarp();
     }
     if (qn > 0 && debug_mode != 3 && debug_mode != 2)
-        a3_chunk<kExactImage>(sm, qn, lane, im, row, pr, acc, debug_mode, 0);
+        a3_chunk<kExactImage, kOwned>(sm, qn, lane, im, row, pr, acc, debug_mode, 0);
     __syncwarp();
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
@@ -476,7 +493,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     }
 }
 
-template <bool kExactImage>
+template <bool kExactImage, bool kOwned, int kM>
 __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     k_atm3(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
            const int32_t *__restrict__ row_count, const int32_t *__restrict__ mirror,
@@ -489,13 +506,13 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     extern __shared__ __align__(16) char smem_raw[];
     const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (r >= n) return;
-    a3_base<kExactImage>(r, smem_raw, g, n, pr, rows, row_count, mirror, capacity, slots, rc2, rc2_lo,
+    a3_base<kExactImage, kOwned, kM>(r, smem_raw, g, n, pr, rows, row_count, mirror, capacity, slots, rc2, rc2_lo,
                             rc2_hi, rc2f_lo, rc2f_hi, own, gbuf, energy_rank, virial_rank,
                             triplets_rank, owned, status, tag, debug_mode, ovf);
 }
 
 // the bases listed by the main pass, with the full slot count
-template <bool kExactImage>
+template <bool kExactImage, bool kOwned>
 __global__ void __launch_bounds__(kA3Warps * 32)
     k_atm3_overflow(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
            const int32_t *__restrict__ row_count, const int32_t *__restrict__ mirror,
@@ -509,10 +526,13 @@ __global__ void __launch_bounds__(kA3Warps * 32)
     const int wpb = blockDim.x >> 5;
     const int cnt = *(volatile const int32_t *)ovf;
     for (int64_t q = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); q < cnt;
-         q += (int64_t)gridDim.x * wpb)
-        a3_base<kExactImage>(ovf[2 + q], smem_raw, g, n, pr, rows, row_count, mirror, capacity, slots, rc2, rc2_lo,
-                            rc2_hi, rc2f_lo, rc2f_hi, own, gbuf, energy_rank, virial_rank,
-                            triplets_rank, owned, status, tag, debug_mode, nullptr);
+         q += (int64_t)gridDim.x * wpb) {
+        a3_base<kExactImage, kOwned, 0>(ovf[2 + q], smem_raw, g, n, pr, rows, row_count, mirror,
+                                        capacity, slots, rc2, rc2_lo, rc2_hi, rc2f_lo, rc2f_hi,
+                                        own, gbuf, energy_rank, virial_rank, triplets_rank,
+                                        owned, status, tag, debug_mode, nullptr);
+        __syncwarp();  // the warp's slots are reused by its next base
+    }
 }
 
 // F(p) = 2 nu * (own(p) + sum over row entries k of p with q = row[k] < p of
@@ -600,31 +620,62 @@ static int a3_warps_for(size_t per) {
     return (size_t)warps * per > 227 * 1024 ? 0 : warps;
 }
 
-template <bool kExactImage>
+template <bool kExactImage, bool kOwned, int kM>
+static void a3_launch_main(cudaStream_t st, int64_t n, int warps, size_t per, const rb_grid &g,
+                           const double *pos_r, const int32_t *rows, const int32_t *row_count,
+                           const int32_t *mirror, int32_t capacity, int fast, double rc2,
+                           double lo, double hi, float flo, float fhi, double *own, double *gbuf,
+                           double *energy_rank, double *virial_rank, int32_t *triplets_rank,
+                           const uint8_t *owned, unsigned long long *status, int64_t tag,
+                           int debug_mode, int32_t *ovf) {
+    static size_t granted = 0;
+    a3_grant(k_atm3<kExactImage, kOwned, kM>, warps * per, granted);
+    launch(k_atm3<kExactImage, kOwned, kM>, dim3((unsigned)((n + warps - 1) / warps)),
+           dim3(warps * 32), warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity,
+           fast, rc2, lo, hi, flo, fhi, own, gbuf, energy_rank, virial_rank, triplets_rank, owned,
+           status, tag, debug_mode, ovf);
+    note_launches(1);
+}
+
+template <bool kExactImage, bool kOwned>
 static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double *pos_r,
                       const int32_t *rows, const int32_t *row_count, const int32_t *mirror,
                       int32_t capacity, int fast, int full, double rc2, double lo, double hi,
                       double *own, double *gbuf, double *energy_rank, double *virial_rank,
                       int32_t *triplets_rank, const uint8_t *owned, unsigned long long *status,
                       int64_t tag, int debug_mode, int32_t *ovf) {
-    static size_t granted_main = 0, granted_ovf = 0;
+    static size_t granted_ovf = 0;
     const float flo = (float)(rc2 * (1.0 - kA3Band)), fhi = (float)(rc2 * (1.0 + kA3Band));
     const size_t per = a3_warp_bytes(fast);
     const int warps = a3_warps_for(per);
     const bool split = fast < full;
-    a3_grant(k_atm3<kExactImage>, warps * per, granted_main);
-    launch(k_atm3<kExactImage>, dim3((unsigned)((n + warps - 1) / warps)), dim3(warps * 32), warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity, fast, rc2, lo, hi, flo, fhi, own, gbuf,
-        energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
-        split ? ovf : nullptr);
-    note_launches(1);
+    int32_t *list = split ? ovf : nullptr;
+    // the common slot counts get compile-time layouts
+    if (fast == 64)
+        a3_launch_main<kExactImage, kOwned, 64>(st, n, warps, per, g, pos_r, rows, row_count,
+                                                mirror, capacity, fast, rc2, lo, hi, flo, fhi, own,
+                                                gbuf, energy_rank, virial_rank, triplets_rank,
+                                                owned, status, tag, debug_mode, list);
+    else if (fast == 96)
+        a3_launch_main<kExactImage, kOwned, 96>(st, n, warps, per, g, pos_r, rows, row_count,
+                                                mirror, capacity, fast, rc2, lo, hi, flo, fhi, own,
+                                                gbuf, energy_rank, virial_rank, triplets_rank,
+                                                owned, status, tag, debug_mode, list);
+    else
+        a3_launch_main<kExactImage, kOwned, 0>(st, n, warps, per, g, pos_r, rows, row_count,
+                                               mirror, capacity, fast, rc2, lo, hi, flo, fhi, own,
+                                               gbuf, energy_rank, virial_rank, triplets_rank,
+                                               owned, status, tag, debug_mode, list);
     if (!split) return;
     const size_t per_full = a3_warp_bytes(full);
     const int wf = a3_warps_for(per_full);
     const int64_t need = (n + wf - 1) / wf;
     const unsigned blocks = (unsigned)(need < 148 * 4 ? need : 148 * 4);
-    a3_grant(k_atm3_overflow<kExactImage>, wf * per_full, granted_ovf);
-    launch(k_atm3_overflow<kExactImage>, dim3(blocks), dim3(wf * 32), wf * per_full, st, g, n, pos_r, rows, row_count, mirror, capacity, full, rc2, lo, hi, flo, fhi, own, gbuf,
-        energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode, ovf);
+    a3_grant(k_atm3_overflow<kExactImage, kOwned>, wf * per_full, granted_ovf);
+    launch(k_atm3_overflow<kExactImage, kOwned>, dim3(blocks), dim3(wf * 32), wf * per_full, st,
+           g, n, pos_r, rows, row_count, mirror, capacity, full, rc2, lo, hi, flo, fhi, own, gbuf,
+           energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
+           (const int32_t *)ovf);
     note_launches(1);
 }
 }  // namespace rb
@@ -653,15 +704,20 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
     double *own = (double *)scratch;
     double *gbuf = own + 3 * n;
     int32_t *ovf = (int32_t *)(gbuf + (size_t)n * capacity * 3);
+    const double lo = exact_image ? rc2 : rc2 * (1.0 - kA3Margin);
+    const double hi = exact_image ? rc2 : rc2 * (1.0 + kA3Margin);
+    auto go = [&](auto exact, auto with_owned) {
+        a3_launch<decltype(exact)::value, decltype(with_owned)::value>(
+            st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity, rc2, lo, hi,
+            own, gbuf, energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
+            ovf);
+    };
+    using T = std::true_type;
+    using F = std::false_type;
     if (exact_image)
-        a3_launch<true>(st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity,
-                        rc2, rc2, rc2, own, gbuf, energy_rank, virial_rank, triplets_rank, owned,
-                        status, tag, debug_mode, ovf);
+        owned ? go(T{}, T{}) : go(T{}, F{});
     else
-        a3_launch<false>(st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity,
-                         rc2, rc2 * (1.0 - kA3Margin), rc2 * (1.0 + kA3Margin), own, gbuf,
-                         energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
-                         ovf);
+        owned ? go(F{}, T{}) : go(F{}, F{});
     const int tb = 256;
     const int64_t threads = n * kGatherGroup;
     launch(k_atm3_gather, dim3((unsigned)((threads + tb - 1) / tb)), dim3(tb), 0, st, n, cell_particles, rows, row_count, mirror, capacity, own, gbuf, 2.0 * nu, nu, forces,

@@ -28,6 +28,7 @@ from __future__ import annotations
 import ctypes
 import math
 import os
+import time
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -35,9 +36,9 @@ import numpy as np
 
 from . import _lib
 from ._lib import ptr
-from .containers import CudaLinkedCells, MinimumSeparationError
+from .containers import CudaLinkedCells, MinimumSeparationError, engine_for
 from .engine import (SCALAR_E2, SCALAR_E3, SCALAR_W2, SCALAR_W3, CapacityError,
-                     ForceEngine, _round_up)
+                     _round_up)
 from .grid import geometry
 from .model import ValidationError, triplet_cutoff
 
@@ -137,7 +138,7 @@ class DeviceRespa:
         self.n = int(system.positions.shape[0])
         self.periodic = bool(system.periodic)
         self.use_graph = use_graph and self.periodic
-        self.eng = ForceEngine(self.n)
+        self.eng = engine_for(self.n)  # device workspace cached per particle count
         torch = self.torch = self.eng.torch
         dev, f64 = self.eng.device, torch.float64
         self.x = self.eng.pos  # positions live in the engine's buffer
@@ -284,24 +285,32 @@ class DeviceRespa:
         """Container scalars of the most recent passes (integrators.py:74-83)."""
         self._reduce_scalars()
 
+    def _captured(self, body):
+        """CUDA graph of `body` captured on a side stream.  (torch.cuda.graph
+        would also empty the allocator cache on entry: a device-wide
+        cudaFree of every cached block, hundreds of ms after a large run.)"""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        cur = torch.cuda.current_stream()
+        side = self._side_stream = getattr(self, "_side_stream", None) or torch.cuda.Stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            g.capture_begin()
+            try:
+                body()
+            finally:
+                g.capture_end()
+        cur.wait_stream(side)
+        return g
+
     def capture(self) -> None:
         """Capture one sampling period as a CUDA graph (after a warm-up)."""
-        torch = self.torch
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self._period(0)
+        self.graph = self._captured(lambda: self._period(0))
 
     def capture_steps(self):
         """One CUDA graph per step position inside a sampling period (the
         step kinds repeat with the period), for per-step timing."""
-        torch = self.torch
-        graphs = []
-        for j in range(self.interval):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._step(j)
-            graphs.append(g)
-        return graphs
+        return [self._captured(lambda j=j: self._step(j)) for j in range(self.interval)]
 
     def run_periods(self, first_period: int, count: int) -> None:
         for k in range(first_period, first_period + count):
@@ -332,6 +341,9 @@ def _fill_trace(trace: RunTrace, rows: np.ndarray, mass: float) -> None:
         trace.record_values(int(round(row[0])), 0.5 * mass * row[1], row[2], row[3], row[4], row[5])
 
 
+LAST_RUN = [None]  # the DeviceRespa of the most recent respa_run (diagnostics)
+
+
 def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: Optional[int] = None,
               hooks=(), use_graph: bool = True, capacity: Optional[int] = None,
               skin: Optional[float] = None) -> RunTrace:
@@ -355,6 +367,7 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
         run = DeviceRespa(system, ff, container, schedule, sample_interval, capacity=capacity,
                           use_graph=use_graph and not hooks, skin=skin)
         run.slots = slots
+        LAST_RUN[0] = run
         try:
             return _drive(run, hooks)
         except CapacityError:
@@ -368,6 +381,7 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
 def _drive(run: DeviceRespa, hooks) -> RunTrace:
     sysm, n_periods = run.system, run.schedule.num_iterations // run.interval
     trace = RunTrace()
+    run.marks = [("drive", time.perf_counter())]
     run.start()
     if hooks:
         # hooks see the host system at every sample point: sync per period
@@ -393,21 +407,28 @@ def _drive(run: DeviceRespa, hooks) -> RunTrace:
         run.download()
         run.update_container()
         return trace
+    mark = run.marks.append
+    mark(("started", time.perf_counter()))
     if n_periods > 0 and run.use_graph:
         run.run_periods(0, 1)  # warm-up, also the first period of the run
+        mark(("eager period", time.perf_counter()))
         run.capture()
+        mark(("captured", time.perf_counter()))
         # the capture recorded but did not execute; rewind nothing: replay the rest
         run.eng.status[1] = run.interval
         run.run_periods(1, n_periods - 1)
+        mark(("replays enqueued", time.perf_counter()))
     else:
         run.run_periods(0, n_periods)
     for i in range(n_periods * run.interval, run.schedule.num_iterations):
         run._step(i)  # iterations past the last sample point
     run.finish_scalars()
     _check(run, trace, upto=n_periods + 1)
+    mark(("checked (synced)", time.perf_counter()))
     _fill_trace(trace, run.trace_rows(n_periods + 1), float(sysm.mass))
     run.download()
     run.update_container()
+    mark(("downloaded", time.perf_counter()))
     return trace
 
 

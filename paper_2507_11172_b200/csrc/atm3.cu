@@ -41,13 +41,16 @@ namespace rb {
 
 constexpr int kA3Warps = 4;
 #ifndef RB_A3_MIN_BLOCKS
-#define RB_A3_MIN_BLOCKS 7
+#define RB_A3_MIN_BLOCKS 8
 #endif
 constexpr int kA3MinBlocks = RB_A3_MIN_BLOCKS;  // register cap for occupancy
 #ifndef RB_A3_PACKED
 #define RB_A3_PACKED 1  // fp32x2 packed candidate filter
 #endif
-constexpr int kA3Queue = 512;        // entries: the carry of the last chunk + one round block
+#ifndef RB_A3_QUEUE
+#define RB_A3_QUEUE 512
+#endif
+constexpr int kA3Queue = RB_A3_QUEUE;  // entries: the carry of the last chunk + one round block
 constexpr int kA3RoundBlock = 32;    // at most this many rounds per block (bits per word)
 constexpr int kA3MaxSlots = 2047;    // queue entries pack s and t in 11 bits each
 constexpr double kA3Margin = 1e-10;  // fp64 estimate vs the reference arithmetic
@@ -67,11 +70,20 @@ struct A3Smem {
     uint32_t *qe;    // queue: s | t << 11 | (round & 1023) << 22
 };
 
+#ifndef RB_A3_WINDOW
+#define RB_A3_WINDOW 1  // phase 1 by 32-pair windows (no queue)
+#endif
+
 __host__ __device__ inline size_t a3_warp_bytes(int m) {
+#if RB_A3_WINDOW
+    // d_ij (x,y | z), r_ij^2, accumulators (x,y | z), row index
+    size_t b = (size_t)m * (2 * sizeof(double2) + 3 * sizeof(double) + sizeof(int32_t)) + 16;
+#else
     size_t b = (size_t)m * (2 * sizeof(double2) + 3 * sizeof(double) + sizeof(float4) +
                             2 * sizeof(int32_t));
     b += (size_t)kA3Queue * sizeof(uint32_t) + 16;  // + alignment pad of f4
     b += (size_t)2 * kA3RoundBlock * ((m + 31) / 32) * sizeof(uint32_t);
+#endif
     return (b + 15) & ~(size_t)15;
 }
 
@@ -86,6 +98,13 @@ __device__ __forceinline__ A3Smem a3_carve(char *base, int m_rt) {
     s.dz = (double *)(s.axy + m);
     s.r2 = s.dz + m;
     s.az = s.r2 + m;
+#if RB_A3_WINDOW
+    s.f4 = nullptr;
+    s.kidx = (int32_t *)(s.az + m);
+    s.mask = s.vote = s.qe = nullptr;
+    s.vbase = nullptr;
+    return s;
+#endif
     s.f4 = (float4 *)(s.az + m + (m & 1));  // keep 16-byte alignment
     s.kidx = (int32_t *)(s.f4 + m);
     s.mask = (uint32_t *)(s.kidx + m);
@@ -129,31 +148,13 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // v = a+c-b, w = b+c-a, p = uvw, S = uv+uw+vw, s = abc (potentials.py:82-114):
 //   E   = s^-5/2 (s + 3/8 p)
 //   E_a = 3/8 s^-5/2 (S - 2uv) - bc (3/2 s^-5/2 + 15/16 p s^-7/2), b/c alike.
-template <bool kExactImage, bool kOwned>
-__device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im,
-                                        const int32_t *__restrict__ row,
-                                        const double *__restrict__ pr, A3Acc &acc,
-                                        double fj[3], double fk[3], int &s, int &t) {
-    const uint32_t qe = sm.qe[q];
-    s = (int)(qe & 0x7ffu);
-    t = (int)((qe >> 11) & 0x7ffu);
-    const double a = sm.r2[s], b = sm.r2[t];
-    const double2 ij = sm.dxy[s], ik = sm.dxy[t];
-    const double ijz = sm.dz[s], ikz = sm.dz[t];
-    double jkx, jky, jkz;  // d_jk = x_j - x_k
-    double c;
-    if (kExactImage) {
-        // the reference's raw-position minimum image (containers.py:497-513)
-        const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
-        exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
-                   pr[3 * k + 2], jkx, jky, jkz);
-        c = exact_r2(jkx, jky, jkz);
-    } else {
-        jkx = ik.x - ij.x;
-        jky = ik.y - ij.y;
-        jkz = ikz - ijz;
-        c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
-    }
+// The ATM kernel for slots (s, t) with a = r_ij^2, b = r_ik^2, c = r_jk^2
+// and d_ij (ij, ijz), d_ik (ik, ikz), d_jk = x_j - x_k (jk*).
+template <bool kOwned>
+__device__ __forceinline__ bool a3_core(const A3Smem &sm, int s, int t, double a, double b,
+                                        double c, double2 ij, double ijz, double2 ik, double ikz,
+                                        double jkx, double jky, double jkz, A3Acc &acc,
+                                        double fj[3], double fk[3]) {
     // guard (potentials.py:35-36): r_ij, r_ik under it were noted per slot
     if (c < RB_MIN_DISTANCE_SQ ||
         (acc.slot_bad && (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ))) {
@@ -198,6 +199,35 @@ __device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im
     fk[1] = fma(eb, ik.y, ec * jky);
     fk[2] = fma(eb, ikz, ec * jkz);
     return true;
+}
+
+
+template <bool kExactImage, bool kOwned>
+__device__ __forceinline__ bool a3_eval(const A3Smem &sm, int q, const Image &im,
+                                        const int32_t *__restrict__ row,
+                                        const double *__restrict__ pr, A3Acc &acc,
+                                        double fj[3], double fk[3], int &s, int &t) {
+    const uint32_t qe = sm.qe[q];
+    s = (int)(qe & 0x7ffu);
+    t = (int)((qe >> 11) & 0x7ffu);
+    const double a = sm.r2[s], b = sm.r2[t];
+    const double2 ij = sm.dxy[s], ik = sm.dxy[t];
+    const double ijz = sm.dz[s], ikz = sm.dz[t];
+    double jkx, jky, jkz;  // d_jk = x_j - x_k
+    double c;
+    if (kExactImage) {
+        // the reference's raw-position minimum image (containers.py:497-513)
+        const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
+        exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
+                   pr[3 * k + 2], jkx, jky, jkz);
+        c = exact_r2(jkx, jky, jkz);
+    } else {
+        jkx = ik.x - ij.x;
+        jky = ik.y - ij.y;
+        jkz = ikz - ijz;
+        c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
+    }
+    return a3_core<kOwned>(sm, s, t, a, b, c, ij, ijz, ik, ikz, jkx, jky, jkz, acc, fj, fk);
 }
 
 __device__ __forceinline__ void a3_add(double2 *axy, double *az, int slot, const double f[3]) {
@@ -274,6 +304,92 @@ __device__ __forceinline__ bool a3_accept(const A3Smem &sm, const float4 &ps, in
     return exact_r2(dx, dy, dz) <= rc2;
 }
 
+// Phase 1, window form.  The m(m-1)/2 slot pairs, enumerated round-major
+// (round d = 1 .. m/2 pairs s with (s + d) mod m; for even m the last round
+// only s < m/2), are taken 32 at a time: lane l of window w holds pair
+// f = 32 w + l (m >= 32) or slot l of round w + 1 (m < 32).  Inside a window
+// all first slots are distinct and all second slots are distinct (for
+// m > 32 a window spans at most two rounds and s repeats only every m
+// pairs), so the partial forces go to the shared-memory slot accumulators
+// in two conflict-free sub-steps -- no queue, no serialisation, a fixed
+// order.  Each lane decides r_jk^2 <= rc^2 bit-exactly (fp64 estimate from
+// d_ik - d_ij outside a 1e-10 band, else the reference's raw-position
+// arithmetic; always the latter when the box is under four cutoffs).
+// One window step: the pair (s, t) of this lane (live) -- acceptance, the
+// ATM kernel (a3_core) and the two conflict-free accumulator sub-steps.
+template <bool kExactImage, bool kOwned>
+__device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int t,
+                                        const Image &im, const int32_t *__restrict__ row,
+                                        const double *__restrict__ pr, double rc2, double rc2_lo,
+                                        double rc2_hi, A3Acc &acc) {
+    double fj[3], fk[3];
+    bool hit = false;
+    if (live) {
+        const double2 ij = sm.dxy[s], ik = sm.dxy[t];
+        const double ijz = sm.dz[s], ikz = sm.dz[t];
+        double jkx, jky, jkz, c;
+        bool in;
+        if (kExactImage) {
+            const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
+            exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
+                       pr[3 * k + 2], jkx, jky, jkz);
+            c = exact_r2(jkx, jky, jkz);
+            in = c <= rc2;
+        } else {
+            jkx = ik.x - ij.x;
+            jky = ik.y - ij.y;
+            jkz = ikz - ijz;
+            c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
+            in = c <= rc2_lo;
+            if (!in && c <= rc2_hi) {  // inside the band: the reference arithmetic decides
+                const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
+                double ex, ey, ez;
+                exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k],
+                           pr[3 * k + 1], pr[3 * k + 2], ex, ey, ez);
+                in = exact_r2(ex, ey, ez) <= rc2;
+            }
+        }
+        if (in)
+            hit = a3_core<kOwned>(sm, s, t, sm.r2[s], sm.r2[t], c, ij, ijz, ik, ikz, jkx, jky,
+                                  jkz, acc, fj, fk);
+    }
+    __syncwarp();
+    if (hit) a3_add(sm.axy, sm.az, s, fj);
+    __syncwarp();
+    if (hit) a3_add(sm.axy, sm.az, t, fk);
+}
+
+template <bool kExactImage, bool kOwned>
+__device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, const Image &im,
+                                           const int32_t *__restrict__ row,
+                                           const double *__restrict__ pr, double rc2,
+                                           double rc2_lo, double rc2_hi, A3Acc &acc) {
+    if (m >= 32) {
+        const int pairs = m * (m - 1) / 2;
+        int s = lane, d = 1;  // pair f = f0 + lane is (round d, slot s)
+        for (int f0 = 0; f0 < pairs; f0 += 32) {
+            int t = s + d;
+            if (t >= m) t -= m;
+            a3_pair<kExactImage, kOwned>(sm, f0 + lane < pairs, s, t, im, row, pr, rc2, rc2_lo,
+                                         rc2_hi, acc);
+            s += 32;
+            if (s >= m) {
+                s -= m;
+                d += 1;
+            }
+        }
+    } else {
+        for (int d = 1; 2 * d <= m; d++) {
+            const int lim = 2 * d == m ? d : m;  // even m: the last round is half
+            int t = lane + d;
+            if (t >= m) t -= m;
+            a3_pair<kExactImage, kOwned>(sm, lane < lim, lane, t, im, row, pr, rc2, rc2_lo,
+                                         rc2_hi, acc);
+        }
+    }
+    __syncwarp();
+}
+
 // One base particle r (rank order) per warp.  `ovf` (main pass with a
 // reduced slot count): a base whose S+(r) does not fit is appended to the
 // overflow list ovf[2..] (count ovf[0]) and left to k_atm3_overflow; the
@@ -343,7 +459,9 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
             sm.dz[slot] = dz;
             sm.r2[slot] = r2;
             sm.kidx[slot] = k | ((kOwned ? (int)owned[row[k]] : 1) << 30);
+#if !RB_A3_WINDOW
             sm.f4[slot] = make_float4((float)dx, (float)dy, (float)dz, 0.0f);
+#endif
             sm.axy[slot] = make_double2(0.0, 0.0);
             sm.az[slot] = 0.0;
         }
@@ -360,6 +478,10 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     // writes its own pairs; (C) the queue is evaluated 32 entries at a time,
     // the incomplete tail carried to the next block.
     A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1, slot_bad};
+#if RB_A3_WINDOW
+    if (debug_mode != 1)  // debug 1: phases 0 and 3 only
+        a3_windows<kExactImage, kOwned>(sm, m, lane, im, row, pr, rc2, rc2_lo, rc2_hi, acc);
+#else
     const int rounds = debug_mode == 1 ? 0 : (m >> 1);  // debug 1: phases 0 and 3 only
     const int nsets = (m + 31) >> 5;
     const int block = max(1, min(kA3RoundBlock, (kA3Queue - 32) / max(m, 1)));
@@ -465,6 +587,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     if (qn > 0 && debug_mode != 3 && debug_mode != 2)
         a3_chunk<kExactImage, kOwned>(sm, qn, lane, im, row, pr, acc, debug_mode, 0);
     __syncwarp();
+#endif
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
     for (int sl = lane; sl < m; sl += 32) {

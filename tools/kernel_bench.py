@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Per-kernel timings of the force passes on the BASELINE configs (step 0).
 
-    python tools/kernel_bench.py [cfg2 cfg3 cfg4 ...] [--reps R]
+    python tools/kernel_bench.py [cfg2 cfg3 cfg4 ...] [--reps R] [--skin S]
 
 For each config: bin + survivor rows once, then CUDA-event timings (median
 of R, L2 flushed before each launch) of the LJ pass, the Newton-3 ATM pass
@@ -33,6 +33,10 @@ def main(argv):
     if "--reps" in argv:
         reps = int(argv[argv.index("--reps") + 1])
         del argv[argv.index("--reps"): argv.index("--reps") + 2]
+    skin = 0.0
+    if "--skin" in argv:  # Verlet rows at r_list + skin, as the device loop builds them
+        skin = float(argv[argv.index("--skin") + 1])
+        del argv[argv.index("--skin"): argv.index("--skin") + 2]
     names = argv or ["cfg2", "cfg3@2.0", "cfg3@2.5", "cfg3@3.0", "cfg4"]
     L = _lib.lib()
     stream = _lib.stream_handle()
@@ -60,11 +64,18 @@ def main(argv):
         s = cfg.system()
         r_list = max(cfg.rc_lj, rc3)
         eng = ForceEngine(s.n)
-        geom = grid.geometry(s.box, None, r_list, True)
+        r_build = r_list + skin
+        geom = grid.geometry(s.box, None, r_build, True)
         eng.upload_positions(s.positions)
         eng.reset_status(0)
         eng.bin(geom)
-        eng.nlist(geom, r_list, checked=True)
+        if skin > 0.0:  # slots as DeviceRespa.start sizes them
+            eng.nlist(geom, rc3, checked=True)
+            within = int(eng.max_count.item())
+            eng.nlist(geom, r_build, capacity=None, checked=True)
+            eng.slots = min(eng.capacity, (int(within * 1.25) + 8 + 31) // 32 * 32)
+        else:
+            eng.nlist(geom, r_list, checked=True)
         f = torch.empty((s.n, 3), dtype=torch.float64, device="cuda")
         eng.atm(geom, rc3, pkg.systems.NU, f, tag=0)
         torch.cuda.synchronize()
@@ -73,10 +84,10 @@ def main(argv):
         t_c01 = timed(lambda: eng.atm_c01(geom, rc3, pkg.systems.NU, f, 0, reduce=False))
         t_lj = timed(lambda: eng.lj_kernel(geom, cfg.rc_lj, 1.0, 1.0, f, 0))
         t_bin = timed(lambda: eng.bin(geom))
-        t_nl = timed(lambda: eng.nlist(geom, r_list, capacity=eng.capacity, checked=False))
+        t_nl = timed(lambda: eng.nlist(geom, r_build, capacity=eng.capacity, checked=False))
         tps = unique / (t_atm * 1e-3)
         print(json.dumps({
-            "config": name, "n": s.n, "unique_triplets": unique, "capacity": eng.capacity,
+            "config": name, "skin": skin, "n": s.n, "unique_triplets": unique, "capacity": eng.capacity,
             "slots": eng.slots, "atm_ms": t_atm, "atm_c01_ms": t_c01, "lj_ms": t_lj,
             "bin_ms": t_bin, "nlist_ms": t_nl, "triplets_per_s": tps,
             "fp64_tflops": tps * 141 / 1e12, "fp64_peak_tflops": peak.value,

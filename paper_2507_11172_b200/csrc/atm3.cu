@@ -172,28 +172,31 @@ __device__ __forceinline__ void a3_add(double2 *axy, double *az, int slot, const
 // acceptance, the ATM kernel (a3_core) and the two accumulator sub-steps.
 template <bool kExactImage, bool kOwned>
 __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int t,
-                                        const Image &im, const int32_t *__restrict__ row,
+                                        const rb_grid &g, const int32_t *__restrict__ row,
                                         const double *__restrict__ pr, double rc2, double rc2_lo,
                                         double rc2_hi, A3Acc &acc) {
-    double fj[3], fk[3];
-    bool in = false;
-    if (live) {
-        const double2 ij = sm.dxy[s], ik = sm.dxy[t];
-        const double ijz = sm.dz[s], ikz = sm.dz[t];
-        double jkx, jky, jkz, c;
-        if (kExactImage) {
-            const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
-            exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
-                       pr[3 * k + 2], jkx, jky, jkz);
-            c = exact_r2(jkx, jky, jkz);
-            in = c <= rc2;
-        } else {
-            jkx = ik.x - ij.x;
-            jky = ik.y - ij.y;
-            jkz = ikz - ijz;
-            c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
-            in = c <= rc2_lo;
-            if (!in && c <= rc2_hi) {  // inside the band: the reference arithmetic decides
+    if (!live) s = t = 0;  // every lane runs the same code; dead lanes accept nothing
+    const double2 ij = sm.dxy[s], ik = sm.dxy[t];
+    const double ijz = sm.dz[s], ikz = sm.dz[t];
+    double jkx, jky, jkz, c;
+    bool in;
+    if (kExactImage) {
+        const Image im = make_image(g);
+        const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
+        exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
+                   pr[3 * k + 2], jkx, jky, jkz);
+        c = exact_r2(jkx, jky, jkz);
+        in = live && c <= rc2;
+    } else {
+        jkx = ik.x - ij.x;
+        jky = ik.y - ij.y;
+        jkz = ikz - ijz;
+        c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
+        in = live && c <= rc2_lo;
+        const bool band = live && !in && c <= rc2_hi;
+        if (__any_sync(0xffffffffu, band)) {  // rare: the reference arithmetic decides
+            if (band) {
+                const Image im = make_image(g);  // from the kernel parameters, on demand
                 const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
                 double ex, ey, ez;
                 exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k],
@@ -201,18 +204,18 @@ __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int 
                 in = exact_r2(ex, ey, ez) <= rc2;
             }
         }
-        // guard (potentials.py:35-36): flag and skip; r_ij, r_ik under it
-        // were noted per slot in phase 0 (acc.slot_bad)
-        if (in && (c < RB_MIN_DISTANCE_SQ ||
-                   (acc.slot_bad &&
-                    (sm.r2[s] < RB_MIN_DISTANCE_SQ || sm.r2[t] < RB_MIN_DISTANCE_SQ)))) {
-            acc.bad = true;
-            in = false;
-        }
-        if (in)
-            a3_core<kOwned>(sm, s, t, sm.r2[s], sm.r2[t], c, ij, ijz, ik, ikz, jkx, jky, jkz,
-                            acc, fj, fk);
     }
+    // guard (potentials.py:35-36): a triplet with a side under it is flagged
+    // and skipped; r_jk here, r_ij / r_ik only if phase 0 saw one (uniform)
+    bool bad = in && c < RB_MIN_DISTANCE_SQ;
+    if (acc.slot_bad)
+        bad = bad || (in && (sm.r2[s] < RB_MIN_DISTANCE_SQ || sm.r2[t] < RB_MIN_DISTANCE_SQ));
+    acc.bad = acc.bad || bad;
+    in = in && !bad;
+    double fj[3], fk[3];
+    if (in)
+        a3_core<kOwned>(sm, s, t, sm.r2[s], sm.r2[t], c, ij, ijz, ik, ikz, jkx, jky, jkz, acc,
+                        fj, fk);
     __syncwarp();
     if (in) a3_add(sm.axy, sm.az, s, fj);
     __syncwarp();
@@ -220,7 +223,7 @@ __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int 
 }
 
 template <bool kExactImage, bool kOwned>
-__device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, const Image &im,
+__device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, const rb_grid &g,
                                            const int32_t *__restrict__ row,
                                            const double *__restrict__ pr, double rc2,
                                            double rc2_lo, double rc2_hi, A3Acc &acc) {
@@ -230,7 +233,7 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, co
         for (int f0 = 0; f0 < pairs; f0 += 32) {
             int t = s + d;
             if (t >= m) t -= m;
-            a3_pair<kExactImage, kOwned>(sm, f0 + lane < pairs, s, t, im, row, pr, rc2, rc2_lo,
+            a3_pair<kExactImage, kOwned>(sm, f0 + lane < pairs, s, t, g, row, pr, rc2, rc2_lo,
                                          rc2_hi, acc);
             s += 32;
             if (s >= m) {
@@ -243,7 +246,7 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, co
             const int lim = 2 * d == m ? d : m;  // even m: the last round is half
             int t = lane + d;
             if (t >= m) t -= m;
-            a3_pair<kExactImage, kOwned>(sm, lane < lim, lane, t, im, row, pr, rc2, rc2_lo,
+            a3_pair<kExactImage, kOwned>(sm, lane < lim, lane, t, g, row, pr, rc2, rc2_lo,
                                          rc2_hi, acc);
         }
     }
@@ -330,7 +333,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     // ---- phase 1: the slot pairs, 32 per window (a3_windows)
     A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1, slot_bad};
     if (debug_mode != 1)  // debug 1: phases 0 and 3 only
-        a3_windows<kExactImage, kOwned>(sm, m, lane, im, row, pr, rc2, rc2_lo, rc2_hi, acc);
+        a3_windows<kExactImage, kOwned>(sm, m, lane, g, row, pr, rc2, rc2_lo, rc2_hi, acc);
     __syncwarp();
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars

@@ -27,25 +27,20 @@ def ranges():
     carve = find(r"A3Smem a3_carve\(")
     share = find(r"double owned_share\(")
     rs = find(r"double rsqrt_nr\(")
-    rs_end = find(r"^}", rs)
-    ev = find(r"a3_eval\(const A3Smem")
+    core = find(r"void a3_core\(")
     add = find(r"void a3_add\(")
-    ch = find(r"void a3_chunk\(")
-    acc = find(r"bool a3_accept\(")
+    pair = find(r"void a3_pair\(")
+    win = find(r"void a3_windows\(")
     base = find(r"void a3_base\(")
     p0 = find(r"phase 0:")
     p1 = find(r"phase 1:")
-    a = find(r"\(A\) accept bits")
-    b1 = find(r"\(B1\) ballots")
-    b2 = find(r"\(B2\) round-major")
-    c = find(r"\(C\) full chunks")
     p3 = find(r"phase 3:")
     end = find(r"^}", p3)
-    return [("carve", carve, share - 1), ("owned share", share, rs - 1), ("eval (rsqrt)", rs, rs_end),
-            ("eval", ev, add - 1), ("rmw add", add, ch - 1), ("chunk loop", ch, acc - 1),
-            ("accept (band)", acc, base - 1), ("setup", base, p0 - 1), ("phase 0", p0, p1 - 1),
-            ("round setup", p1, a - 1), ("A accept bits", a, b1 - 1), ("B1 ballots", b1, b2 - 1),
-            ("B2 scan+place", b2, c - 1), ("C chunks", c, p3 - 1), ("phase 3", p3, end)]
+    return [("carve", carve, share - 1), ("owned share", share, rs - 1),
+            ("eval: rsqrt", rs, core - 1), ("eval: ATM kernel", core, add - 1),
+            ("slot accumulate", add, pair - 1), ("pair: accept + guard", pair, win - 1),
+            ("window loop", win, base - 1), ("setup", base, p0 - 1), ("phase 0 (S+ slots)", p0, p1 - 1),
+            ("phase 1 call", p1, p3 - 1), ("phase 3 (write-back)", p3, end)]
 
 
 def main(rep):

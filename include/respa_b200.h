@@ -184,6 +184,24 @@ RB_API int rb_atm_visit_rows(const rb_grid *g, int64_t n, const double *pos_r, c
                              const int32_t *row_count, int32_t capacity, double rc,
                              const int64_t *row_offset, int32_t *visit_rows, void *stream);
 
+/* ---- DirectSum: replaces _direct_pair_kernel / _direct_triplet_kernel
+ * (containers.py:663-739) -- all pairs / all triplets of a NON-periodic
+ * system, no cutoff, the reference's raw differences and guard.
+ * rb_direct_pairs: forces (n,3) in particle order (overwritten) and the
+ *   per-particle halves of the pair energy and virial (sum them with
+ *   rb_reduce_sum_f64); owner-computes, deterministic.
+ * rb_direct_triplets: Newton-3, forces (n,3) (overwritten) and
+ *   energy_virial[2] = (E3, W3) on the device; n <= 8192; scratch
+ *   rb_direct_scratch_bytes(n); deterministic (fixed block partition and
+ *   block-order sums). */
+RB_API int rb_direct_pairs(int64_t n, const double *pos, double epsilon, double sigma,
+                           double *forces, double *energy_part, double *virial_part,
+                           unsigned long long *status, int64_t tag, void *stream);
+RB_API size_t rb_direct_scratch_bytes(int64_t n);
+RB_API int rb_direct_triplets(int64_t n, const double *pos, double nu, double *forces,
+                              double *energy_virial, void *scratch, size_t scratch_bytes,
+                              unsigned long long *status, int64_t tag, void *stream);
+
 /* ---- deterministic reductions (fixed partition + fixed tree) ---------- */
 RB_API size_t rb_reduce_scratch_bytes(int64_t n);
 /* out[0] = sum(in[0..n)) */

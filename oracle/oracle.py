@@ -81,6 +81,8 @@ def lib():
         L.orc_brute_pairs.argtypes = [I64, P, P, ctypes.c_int, D, D, D, P, P]
         L.orc_brute_triplets.argtypes = [I64, P, P, ctypes.c_int, D, D, P, P]
         L.orc_brute_triplets.restype = I64
+        L.orc_direct_pairs.argtypes = [I64, P, D, D, I64, P, P, P, P]
+        L.orc_direct_triplets.argtypes = [I64, P, D, I64, P, P, P, P]
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
         L.orc_get_max_threads.restype = ctypes.c_int
         _lib = L
@@ -349,6 +351,60 @@ def brute_force_triplets(system, ff, cutoff=None):
 # ---------------------------------------------------------------------------
 # container + integrator restatement
 # ---------------------------------------------------------------------------
+
+
+DIRECT_SUM_CHUNKS = 16  # respamd/containers.py:36
+
+
+def _direct_buffers(n):
+    return (np.zeros((DIRECT_SUM_CHUNKS, n, 3)), np.zeros(DIRECT_SUM_CHUNKS),
+            np.zeros(DIRECT_SUM_CHUNKS), np.zeros(DIRECT_SUM_CHUNKS, np.int64))
+
+
+def direct_sum_pairs(system, ff):
+    """respamd/containers.py:852-861 (kernel :663-692) -> (forces, energy, virial)."""
+    if system.periodic:
+        raise OracleValidationError("DirectSum does not support periodic boundaries")
+    pos = np.ascontiguousarray(system.positions, dtype=np.float64)
+    fbuf, ebuf, wbuf, flags = _direct_buffers(pos.shape[0])
+    lib().orc_direct_pairs(pos.shape[0], _p(pos), float(ff.epsilon), float(ff.sigma) ** 2,
+                           DIRECT_SUM_CHUNKS, _p(fbuf), _p(ebuf), _p(wbuf), _p(flags))
+    _check_flags(flags)
+    return fbuf.sum(axis=0), float(np.sum(ebuf)), float(np.sum(wbuf))
+
+
+def direct_sum_triplets(system, ff):
+    """respamd/containers.py:864-875 (kernel :695-739) -> (forces, energy, virial)."""
+    if system.periodic:
+        raise OracleValidationError("DirectSum does not support periodic boundaries")
+    pos = np.ascontiguousarray(system.positions, dtype=np.float64)
+    fbuf, ebuf, wbuf, flags = _direct_buffers(pos.shape[0])
+    lib().orc_direct_triplets(pos.shape[0], _p(pos), float(ff.nu), DIRECT_SUM_CHUNKS, _p(fbuf),
+                              _p(ebuf), _p(wbuf), _p(flags))
+    _check_flags(flags)
+    return fbuf.sum(axis=0), float(np.sum(ebuf)), float(np.sum(wbuf))
+
+
+class OracleDirectSum:
+    """respamd/containers.py:888-908."""
+
+    name = "direct_sum"
+
+    def __init__(self):
+        self.pair_energy = self.pair_virial = 0.0
+        self.triplet_energy = self.triplet_virial = 0.0
+
+    def pair_pass(self, system, ff):
+        f, self.pair_energy, self.pair_virial = direct_sum_pairs(system, ff)
+        system.forces_2b[:] = f
+
+    def triplet_pass(self, system, ff):
+        if ff.nu == 0.0:
+            system.forces_3b[:] = 0.0
+            self.triplet_energy = self.triplet_virial = 0.0
+            return
+        f, self.triplet_energy, self.triplet_virial = direct_sum_triplets(system, ff)
+        system.forces_3b[:] = f
 
 
 class OracleLinkedCells:

@@ -12,8 +12,9 @@ when the library or a CUDA device is missing.
 from .model import (CONTAINER_KINDS, ForceField, ParticleSystem, SamplingConfig, ScenarioConfig,
                     ValidationError, init_velocities, triplet_cutoff, wrap_positions)
 from .grid import CellGrid
-from .containers import (CudaLinkedCells, MinimumSeparationError, build_cell_grid, c01_pair_pass,
-                         c01_triplet_pass, collect_triplet_visits, make_container, triplet_count)
+from .containers import (CudaDirectSum, CudaLinkedCells, MinimumSeparationError, build_cell_grid,
+                         c01_pair_pass, c01_triplet_pass, collect_triplet_visits,
+                         direct_sum_pairs, direct_sum_triplets, make_container, triplet_count)
 from .integrators import IntegrationBlowUp, RespaSchedule, RunTrace, respa_run, verlet_run
 from .scenarios import ExperimentPlan, ScenarioParseError, parse_scenario
 from . import systems
@@ -21,10 +22,11 @@ from . import systems
 __version__ = "0.1.0"
 
 __all__ = [
-    "CONTAINER_KINDS", "CellGrid", "CudaLinkedCells", "ExperimentPlan", "ForceField",
+    "CONTAINER_KINDS", "CellGrid", "CudaDirectSum", "CudaLinkedCells", "ExperimentPlan", "ForceField",
     "IntegrationBlowUp", "MinimumSeparationError", "ParticleSystem", "RespaSchedule", "RunTrace",
     "SamplingConfig", "ScenarioConfig", "ScenarioParseError", "ValidationError", "build_cell_grid",
-    "c01_pair_pass", "c01_triplet_pass", "collect_triplet_visits", "init_velocities",
+    "c01_pair_pass", "c01_triplet_pass", "collect_triplet_visits", "direct_sum_pairs",
+    "direct_sum_triplets", "init_velocities",
     "make_container", "parse_scenario", "respa_run", "systems", "triplet_count", "triplet_cutoff",
     "verlet_run", "wrap_positions",
 ]

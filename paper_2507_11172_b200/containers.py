@@ -230,9 +230,70 @@ class CudaLinkedCells:
         self.triplet_visits = 3 * int(eng.visits.item())  # C01-equivalent visit count
 
 
+# ---------------------------------------------------------------- DirectSum
+_DIRECT_PERIODIC_MSG = "DirectSum does not support periodic boundaries"
+
+
+def _direct_engine(system):
+    if system.periodic:  # containers.py:854-855, 866-867
+        raise ValidationError(_DIRECT_PERIODIC_MSG)
+    eng = engine_for(system.positions.shape[0])
+    eng.upload_positions(system.positions)
+    eng.reset_status(0)
+    return eng
+
+
+def direct_sum_pairs(system, ff):
+    """Every distinct pair, no cutoff (containers.py:852-861); (forces, energy, virial)."""
+    eng = _direct_engine(system)
+    out = eng.torch.empty((eng.n, 3), dtype=eng.torch.float64, device=eng.device)
+    eng.direct_pairs(ff.epsilon, ff.sigma, out, tag=0)
+    _raise_on_status(eng)
+    sc = eng.scalar_values()
+    return out.cpu().numpy(), float(sc[SCALAR_E2]), float(sc[SCALAR_W2])
+
+
+def direct_sum_triplets(system, ff):
+    """Every distinct triplet, no cutoff (containers.py:864-875); (forces, energy, virial)."""
+    eng = _direct_engine(system)
+    out = eng.torch.empty((eng.n, 3), dtype=eng.torch.float64, device=eng.device)
+    eng.direct_triplets(ff.nu, out, tag=0)
+    _raise_on_status(eng)
+    sc = eng.scalar_values()
+    return out.cpu().numpy(), float(sc[SCALAR_E3]), float(sc[SCALAR_W3])
+
+
+class CudaDirectSum:
+    """GPU drop-in for ``respamd.containers.DirectSum`` (containers.py:888-908):
+    all pairs and all triplets, no cutoff, non-periodic systems only."""
+
+    name = "cuda_direct_sum"
+
+    def __init__(self):
+        self.pair_energy = 0.0
+        self.pair_virial = 0.0
+        self.triplet_energy = 0.0
+        self.triplet_virial = 0.0
+
+    def pair_pass(self, system, ff) -> None:
+        forces, self.pair_energy, self.pair_virial = direct_sum_pairs(system, ff)
+        system.forces_2b[:] = forces
+
+    def triplet_pass(self, system, ff) -> None:
+        if ff.nu == 0.0:  # containers.py:900-904
+            system.forces_3b[:] = 0.0
+            self.triplet_energy = 0.0
+            self.triplet_virial = 0.0
+            return
+        forces, self.triplet_energy, self.triplet_virial = direct_sum_triplets(system, ff)
+        system.forces_3b[:] = forces
+
+
 def make_container(kind: str):
-    """Container factory (containers.py:940-945) for this package's kind."""
+    """Container factory (containers.py:940-945) for this package's kinds."""
     if kind in ("cuda_linked_cells", "linked_cells"):
         return CudaLinkedCells()
+    if kind in ("cuda_direct_sum", "direct_sum"):
+        return CudaDirectSum()
     raise ValidationError(f"unknown container kind {kind!r} (this package provides "
-                          f"'cuda_linked_cells')")
+                          f"'cuda_linked_cells' and 'cuda_direct_sum')")

@@ -175,6 +175,25 @@ __device__ __forceinline__ int group_sum_int(int v) {
     return v;
 }
 
+// block-wide sum with a fixed tree (xor shuffles, then warp 0 over the
+// per-warp partials); the result is valid in thread 0.  Every thread of the
+// block must call it; `sh` holds >= 32 entries.
+template <typename T>
+__device__ __forceinline__ T block_tree_sum(T v, T *sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    T s = 0;
+    if (warp == 0) {
+        s = lane < (int)(blockDim.x >> 5) ? sh[lane] : (T)0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    }
+    return s;
+}
+
 // neighbour cell of base cell (cx,cy,cz) at offset o; -1 when outside an
 // open grid (respamd/containers.py:319-333)
 __device__ __forceinline__ int neighbor_cell(const rb_grid &g, int cx, int cy, int cz, int o) {

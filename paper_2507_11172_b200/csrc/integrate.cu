@@ -157,21 +157,6 @@ __host__ __device__ inline int red_blocks(int64_t n) {
     return (int)b;
 }
 
-template <typename T>
-__device__ __forceinline__ T block_tree_sum(T v, T *sh) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) sh[warp] = v;
-    __syncthreads();
-    T s = 0;
-    if (warp == 0) {
-        s = lane < (int)(blockDim.x >> 5) ? sh[lane] : (T)0;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    }
-    return s;
-}
 
 template <typename Tin, typename Tacc, bool kSquare>
 __global__ void k_partial_sum(int64_t n, const Tin *__restrict__ in, Tacc *__restrict__ partial) {

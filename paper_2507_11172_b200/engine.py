@@ -90,6 +90,7 @@ class ForceEngine:
         self._grid = None
         self._stream_override = None  # capture of a conditional body
         self.cond_body_launches = 0  # kernels in the last conditional rebuild body
+        self.direct_scratch = None
 
     # ------------------------------------------------------------------ misc
     @property
@@ -310,6 +311,28 @@ class ForceEngine:
             return
         self.reduce_triplet()
         self._count()
+
+    # ------------------------------------------------------------ DirectSum
+    def direct_pairs(self, epsilon: float, sigma: float, forces, tag: int = 0) -> None:
+        """All pairs of the particle-order positions (no cutoff, no image);
+        scalars[E2], scalars[W2] <- energy, virial."""
+        st = self.L.rb_direct_pairs(self.n, ptr(self.pos), float(epsilon), float(sigma),
+                                    ptr(forces), ptr(self.e2_rank), ptr(self.w2_rank),
+                                    ptr(self.status), int(tag), self.stream)
+        _lib.check(st, "rb_direct_pairs")
+        self.reduce_pair()
+
+    def direct_triplets(self, nu: float, forces, tag: int = 0) -> None:
+        """All triplets (Newton-3); scalars[E3], scalars[W3] <- energy, virial."""
+        need = int(self.L.rb_direct_scratch_bytes(self.n))
+        if self.direct_scratch is None or self.direct_scratch.numel() * 8 < need:
+            self.direct_scratch = self.torch.empty((need + 7) // 8, dtype=self.torch.float64,
+                                                   device=self.device)
+        ew = ctypes.c_void_p(self.scalars.data_ptr() + 8 * SCALAR_E3)
+        st = self.L.rb_direct_triplets(self.n, ptr(self.pos), float(nu), ptr(forces), ew,
+                                       ptr(self.direct_scratch), self.direct_scratch.numel() * 8,
+                                       ptr(self.status), int(tag), self.stream)
+        _lib.check(st, "rb_direct_triplets")
 
     def _count(self) -> None:
         st = self.L.rb_reduce_sum_i32(self.n, ptr(self.v_rank), ptr(self.visits),

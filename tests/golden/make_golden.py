@@ -18,6 +18,9 @@ records its outputs on seeded inputs:
                           scalars, the visit count and forces of a fixed
                           particle subset
 * respa_<name>.npz    -- respa_run trajectories (integrators.py:96-173)
+* direct.npz          -- DirectSum pairs/triplets (containers.py:852-908) on
+                          non-periodic systems (the reference test's four
+                          particles and random n = 70 / 150 / 300)
 
 Inputs are produced by this repo's generators (paper_2507_11172_b200.systems
 and tests/helpers.random_positions); the reference only supplies outputs.
@@ -231,7 +234,36 @@ def gen_respa():
                         f3=sysm.forces_3b, **_trace_arrays(trace))
 
 
+DIRECT = [  # name, edge, n, rng offset (non-periodic random systems)
+    ("e7_n70", 7.0, 70, 31),
+    ("e9_n150", 9.0, 150, 32),
+    ("e12_n300", 12.0, 300, 33),
+]
+
+
+def gen_direct():
+    """DirectSum (containers.py:852-908) on non-periodic systems: the
+    four-particle system of test_containers.py:189-207 and random ones."""
+    ff = rm.ForceField(epsilon=1.0, sigma=1.0, nu=0.7, cutoff=2.5)
+    cases = [("four", np.array([[0.0, 0.0, 0.0], [1.2, 0.0, 0.0], [0.0, 1.3, 0.0],
+                                [0.0, 0.0, 1.4]]), 50.0)]
+    for name, edge, n, off in DIRECT:
+        rng = np.random.default_rng(TEST_SEED + off)
+        cases.append((name, random_positions(rng, n, (edge,) * 3, False), edge))
+    out = {}
+    for name, pos, edge in cases:
+        sysm = ref_system(pos, (edge,) * 3, False)
+        f2, e2, w2 = rc.direct_sum_pairs(sysm, ff)
+        f3, e3, w3 = rc.direct_sum_triplets(sysm, ff)
+        for k, v in dict(pos=pos, box=np.full(3, edge), f2=f2, e2=e2, w2=w2, f3=f3, e3=e3,
+                         w3=w3).items():
+            out[f"{name}__{k}"] = v
+        print(f"direct {name}: n {len(pos)} e2 {e2} e3 {e3}")
+    np.savez_compressed(os.path.join(HERE, "direct.npz"), names=np.array([c[0] for c in cases]),
+                        nu=ff.nu, **out)
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["potentials", "small", "large", "respa"]
+    what = sys.argv[1:] or ["potentials", "small", "large", "respa", "direct"]
     for w in what:
         globals()[f"gen_{w}"]()

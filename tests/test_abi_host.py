@@ -202,3 +202,17 @@ def test_scenario_format(tmp_path):
     dup.write_text(SCENARIO + "nu=0.4\n")
     with pytest.raises(ScenarioParseError):
         parse_scenario(dup)
+
+
+def test_direct_sum_rejects_periodic_systems():
+    """test_containers.py:215-220: raised before any device work."""
+    import paper_2507_11172_b200 as pkg
+
+    s = pkg.ParticleSystem.empty(3, (8.0, 8.0, 8.0), periodic=True)
+    s.positions[:] = [[0.5, 0.5, 0.5], [2.0, 0.5, 0.5], [0.5, 2.0, 0.5]]
+    ff = pkg.ForceField()
+    with pytest.raises(pkg.ValidationError):
+        pkg.direct_sum_pairs(s, ff)
+    with pytest.raises(pkg.ValidationError):
+        pkg.direct_sum_triplets(s, ff)
+    assert pkg.make_container("direct_sum").name == "cuda_direct_sum"

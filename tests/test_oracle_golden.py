@@ -123,3 +123,28 @@ def test_respa_split_cutoff_bit_exact(oracle):
                      int(g["s"]), int(g["steps"]))
     assert np.array_equal(sysm.positions, g["x"])
     assert np.array_equal(sysm.velocities, g["v"])
+
+
+def _direct_cases():
+    g = load_golden("direct.npz")
+    return g, [str(n) for n in g["names"]]
+
+
+def test_direct_sum_bit_exact(oracle):
+    """DirectSum restatement (containers.py:663-739, 852-875) vs the reference."""
+    g, names = _direct_cases()
+    off = oracle.OracleForceField(nu=float(g["nu"]), cutoff=2.5)
+    for name in names:
+        s = oracle.OracleSystem.from_positions(g[f"{name}__pos"], g[f"{name}__box"], False)
+        f2, e2, w2 = oracle.direct_sum_pairs(s, off)
+        f3, e3, w3 = oracle.direct_sum_triplets(s, off)
+        assert np.array_equal(f2, g[f"{name}__f2"]) and np.array_equal(f3, g[f"{name}__f3"])
+        assert (e2, w2, e3, w3) == (float(g[f"{name}__e2"]), float(g[f"{name}__w2"]),
+                                    float(g[f"{name}__e3"]), float(g[f"{name}__w3"]))
+
+
+def test_direct_sum_rejects_periodic(oracle):
+    s = oracle.OracleSystem.from_positions(np.zeros((3, 3)) + [[0, 0, 0], [1, 0, 0], [0, 1, 0]],
+                                           (5.0, 5.0, 5.0), True)
+    with pytest.raises(oracle.OracleValidationError):
+        oracle.direct_sum_pairs(s, oracle.OracleForceField())

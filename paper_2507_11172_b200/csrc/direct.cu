@@ -1,17 +1,18 @@
 // direct.cu -- DirectSum on the device: every pair and every triplet of a
 // non-periodic system, no cutoff (respamd/containers.py:663-739, 852-908).
 //
-// Pairs: one thread per particle i sums the LJ force of all j != i in index
-// order (positions staged through shared memory tiles); each pair is visited
-// from both sides, phi/2 and scale*r^2/2 per visit (owner-computes: no
-// scatter, deterministic).
+// Pairs: one warp per particle i sums the LJ force of all j != i (lanes
+// stride over j, fixed xor tree); each pair is visited from both sides,
+// phi/2 and scale*r^2/2 per visit (owner-computes: no scatter,
+// deterministic).
 //
 // Triplets: Newton-3, every unique i < j < k evaluated once.  The pairs
 // (j, k) of base i are the pairs of its m = n-1-i followers, enumerated by
 // rotation rounds as in atm3.cu (round d pairs follower s with (s+d) mod m)
-// and taken 256 at a time (one per thread of the block): inside such a
-// window all j are distinct and all k are distinct (m >= 256: a window spans
-// at most two rounds; m < 256: a window is one round), so f_j and f_k go to
+// and taken T at a time (one per thread of the block, T = 256, or 1024 when
+// only one block fits an SM): inside such a window all j are distinct and all
+// k are distinct (m >= T: a window spans at most two rounds; m < T: a window
+// is one round), so f_j and f_k go to
 // the block's shared-memory force array in two conflict-free sub-steps.  The
 // windows of all bases form one list; block b takes a contiguous slice of it
 // (equal pair counts per block).  Each block leaves its force array in a
@@ -26,8 +27,7 @@
 
 namespace rb {
 
-constexpr int kDpThreads = 128;  // pair pass: threads per block = tile size
-constexpr int kDtThreads = 256;  // triplet pass: threads per block = window
+constexpr int kDpThreads = 128;  // pair pass: threads per block (4 particles)
 constexpr int kDtMaxN = 8192;    // the per-block force array lives in shared memory
 
 __global__ void __launch_bounds__(kDpThreads)
@@ -35,48 +35,42 @@ __global__ void __launch_bounds__(kDpThreads)
                    double sigma2, double *__restrict__ forces, double *__restrict__ energy,
                    double *__restrict__ virial, unsigned long long *status, int64_t tag) {
     pdl_enter();
-    __shared__ double tile[3 * kDpThreads];
-    const int64_t i = (int64_t)blockIdx.x * kDpThreads + threadIdx.x;
+    // one warp per particle i; lanes stride over j, then a fixed xor tree
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * kDpThreads + threadIdx.x) >> 5;
     tag = resolve_tag(tag, status);
-    const bool active = i < n;
-    double xi = 0.0, yi = 0.0, zi = 0.0;
-    if (active) {
-        xi = pos[3 * i];
-        yi = pos[3 * i + 1];
-        zi = pos[3 * i + 2];
-    }
+    if (i >= n) return;  // whole warps
+    const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
     bool bad = false;
-    for (int64_t j0 = 0; j0 < n; j0 += kDpThreads) {
-        const int64_t jl = j0 + threadIdx.x;
-        __syncthreads();
-        for (int c = 0; c < 3; c++) tile[3 * threadIdx.x + c] = jl < n ? pos[3 * jl + c] : 0.0;
-        __syncthreads();
-        const int cnt = (int)(n - j0 < kDpThreads ? n - j0 : kDpThreads);
-        if (!active) continue;
-        for (int u = 0; u < cnt; u++) {
-            if (j0 + u == i) continue;
-            const double dx = xsub(xi, tile[3 * u]);
-            const double dy = xsub(yi, tile[3 * u + 1]);
-            const double dz = xsub(zi, tile[3 * u + 2]);
-            const double r2 = exact_r2(dx, dy, dz);
-            if (r2 < RB_MIN_DISTANCE_SQ) {  // potentials.py:35-36
-                bad = true;
-                continue;
-            }
-            const double inv_r2 = 1.0 / r2;
-            const double x = sigma2 * inv_r2;
-            const double r6 = x * x * x;
-            const double r12 = r6 * r6;
-            const double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
-            fx += scale * dx;
-            fy += scale * dy;
-            fz += scale * dz;
-            e += eps4 * (r12 - r6);
-            w += scale * r2;
+    for (int64_t j = lane; j < n; j += 32) {
+        if (j == i) continue;
+        const double dx = xsub(xi, pos[3 * j]);
+        const double dy = xsub(yi, pos[3 * j + 1]);
+        const double dz = xsub(zi, pos[3 * j + 2]);
+        const double r2 = exact_r2(dx, dy, dz);
+        if (r2 < RB_MIN_DISTANCE_SQ) {  // potentials.py:35-36
+            bad = true;
+            continue;
         }
+        const double inv_r2 = 1.0 / r2;
+        const double x = sigma2 * inv_r2;
+        const double r6 = x * x * x;
+        const double r12 = r6 * r6;
+        const double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
+        fx += scale * dx;
+        fy += scale * dy;
+        fz += scale * dz;
+        e += eps4 * (r12 - r6);
+        w += scale * r2;
     }
-    if (active) {
+    fx = group_sum<32>(fx);
+    fy = group_sum<32>(fy);
+    fz = group_sum<32>(fz);
+    e = group_sum<32>(e);
+    w = group_sum<32>(w);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
         forces[3 * i] = fx;
         forces[3 * i + 1] = fy;
         forces[3 * i + 2] = fz;
@@ -86,21 +80,22 @@ __global__ void __launch_bounds__(kDpThreads)
     }
 }
 
-// windows of base i (m = n-1-i followers)
-__host__ __device__ inline int64_t dt_windows(int64_t m) {
+// windows of base i (m = n-1-i followers) for T threads per block
+__host__ __device__ inline int64_t dt_windows(int64_t m, int T) {
     if (m < 2) return 0;
-    if (m >= kDtThreads) return (m * (m - 1) / 2 + kDtThreads - 1) / kDtThreads;
+    if (m >= T) return (m * (m - 1) / 2 + T - 1) / T;
     return m / 2;
 }
 
 // prefix[i] = windows of the bases < i, i = 0..n (one block)
-__global__ void __launch_bounds__(1024) k_direct_prep(int64_t n, int64_t *__restrict__ prefix) {
+__global__ void __launch_bounds__(1024) k_direct_prep(int64_t n, int T,
+                                                      int64_t *__restrict__ prefix) {
     pdl_enter();
     __shared__ int64_t part[1024];
     const int64_t per = (n + 1023) / 1024;
     const int64_t b = threadIdx.x * per;
     int64_t sum = 0;
-    for (int64_t i = b; i < b + per && i < n; i++) sum += dt_windows(n - 1 - i);
+    for (int64_t i = b; i < b + per && i < n; i++) sum += dt_windows(n - 1 - i, T);
     part[threadIdx.x] = sum;
     __syncthreads();
     if (threadIdx.x == 0) {  // serial scan of 1024 partials: negligible next to the pass
@@ -116,11 +111,12 @@ __global__ void __launch_bounds__(1024) k_direct_prep(int64_t n, int64_t *__rest
     int64_t run = part[threadIdx.x];
     for (int64_t i = b; i < b + per && i < n; i++) {
         prefix[i] = run;
-        run += dt_windows(n - 1 - i);
+        run += dt_windows(n - 1 - i, T);
     }
 }
 
-__global__ void __launch_bounds__(kDtThreads)
+template <int kT>
+__global__ void __launch_bounds__(kT)
     k_direct_triplets(int64_t n, const double *__restrict__ pos,
                       const int64_t *__restrict__ prefix, double *__restrict__ slab,
                       double *__restrict__ part_ew, unsigned long long *status, int64_t tag) {
@@ -129,7 +125,7 @@ __global__ void __launch_bounds__(kDtThreads)
     __shared__ double red[32];
     const int tid = threadIdx.x;
     tag = resolve_tag(tag, status);
-    for (int64_t q = tid; q < 3 * n; q += kDtThreads) fsh[q] = 0.0;
+    for (int64_t q = tid; q < 3 * n; q += kT) fsh[q] = 0.0;
     double *fxs = fsh, *fys = fsh + n, *fzs = fsh + 2 * n;
     const int64_t total = prefix[n];
     const int64_t lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
@@ -147,15 +143,15 @@ __global__ void __launch_bounds__(kDtThreads)
         const int64_t w_end = min(prefix[i + 1], hi);
         const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
         double fix = 0.0, fiy = 0.0, fiz = 0.0;
-        // this thread's pair in the first window of the slice: f = ww * 256 + tid
-        // is (round d, follower s); later windows advance by 256 pairs
+        // this thread's pair in the first window of the slice: f = ww * T + tid
+        // is (round d, follower s); later windows advance by T pairs
         const int mi = (int)m, pairs = mi * (mi - 1) / 2;
-        int f = (int)(win - prefix[i]) * kDtThreads + tid;
+        int f = (int)(win - prefix[i]) * kT + tid;
         int d = f / (mi > 0 ? mi : 1) + 1, s0 = f - (d - 1) * mi;
         for (; win < w_end; win++) {
             int s;
             bool live;
-            if (mi >= kDtThreads) {
+            if (mi >= kT) {
                 live = f < pairs;
                 s = s0;
             } else {  // one round per window
@@ -225,9 +221,9 @@ __global__ void __launch_bounds__(kDtThreads)
                 fzs[k] += fk[2];
             }
             __syncthreads();
-            f += kDtThreads;
-            s0 += kDtThreads;
-            if (s0 >= mi) {  // 256 <= m: at most one wrap
+            f += kT;
+            s0 += kT;
+            if (s0 >= mi) {  // T <= m: at most one wrap
                 s0 -= mi;
                 d += 1;
             }
@@ -246,7 +242,7 @@ __global__ void __launch_bounds__(kDtThreads)
         __syncthreads();
     }
     double *mine = slab + (int64_t)blockIdx.x * 3 * n;
-    for (int64_t q = tid; q < 3 * n; q += kDtThreads) mine[q] = fsh[q];
+    for (int64_t q = tid; q < 3 * n; q += kT) mine[q] = fsh[q];
     const double es = block_tree_sum<double>(e_acc, red);
     __syncthreads();
     const double ws = block_tree_sum<double>(w_acc, red);
@@ -281,13 +277,21 @@ __global__ void k_direct_finish(int64_t n, int nb, const double *__restrict__ sl
     }
 }
 
-static int dt_blocks(int64_t n) {
+// blocks per SM as shared memory allows (the force array is 24 n bytes),
+static int dt_per_sm(int64_t n) {
     const size_t smem = (size_t)3 * (n > 0 ? n : 1) * sizeof(double) + 1024;
     int per_sm = (int)((227 * 1024) / (smem + 1024));
-    if (per_sm > 8) per_sm = 8;  // 8 x 256 threads = 2048
+    if (per_sm > 8) per_sm = 8;
     if (per_sm < 1) per_sm = 1;
-    return 148 * per_sm;
+    return per_sm;
 }
+
+// 256-thread blocks (cheaper block barriers per window) unless the force
+// array leaves room for one block per SM only (measured: 81-89 G triplets/s
+// at n = 1024..4096 with 256, 58 vs 48 at n = 8192 with 1024)
+static int dt_threads(int64_t n) { return dt_per_sm(n) == 1 ? 1024 : 256; }
+
+static int dt_blocks(int64_t n) { return 148 * dt_per_sm(n); }
 
 }  // namespace rb
 
@@ -299,7 +303,8 @@ extern "C" int rb_direct_pairs(int64_t n, const double *pos, double epsilon, dou
     if (n < 0 || (n > 0 && (!pos || !forces || !energy_part || !virial_part)))
         return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
-    launch(k_direct_pairs, dim3((unsigned)((n + kDpThreads - 1) / kDpThreads)), dim3(kDpThreads),
+    const int64_t threads = 32 * n;
+    launch(k_direct_pairs, dim3((unsigned)((threads + kDpThreads - 1) / kDpThreads)), dim3(kDpThreads),
            0, as_stream(stream), n, pos, 24.0 * epsilon, 4.0 * epsilon, sigma * sigma, forces,
            energy_part, virial_part, status, tag);
     note_launches(1);
@@ -327,15 +332,17 @@ extern "C" int rb_direct_triplets(int64_t n, const double *pos, double nu, doubl
     double *slab = (double *)(prefix + n + 1);
     double *part_ew = slab + (size_t)nb * 3 * n;
     const size_t smem = (size_t)3 * n * sizeof(double);
-    static size_t granted = 0;
-    if (smem > 48 * 1024 && smem > granted) {
-        cudaFuncSetAttribute(k_direct_triplets, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        granted = smem;
-    }
-    launch(k_direct_prep, dim3(1), dim3(1024), 0, st, n, prefix);
-    launch(k_direct_triplets, dim3(nb), dim3(kDtThreads), smem, st, n, pos,
-           (const int64_t *)prefix, slab, part_ew, status, tag);
+    const int T = dt_threads(n);
+    launch(k_direct_prep, dim3(1), dim3(1024), 0, st, n, T, prefix);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        launch(kern, dim3(nb), dim3(T), smem, st, n, pos, (const int64_t *)prefix, slab, part_ew,
+               status, tag);
+    };
+    if (T == 1024)
+        go(k_direct_triplets<1024>);
+    else
+        go(k_direct_triplets<256>);
     const int64_t q = 3 * n;
     launch(k_direct_finish, dim3((unsigned)((q + 255) / 256)), dim3(256), 0, st, n, nb,
            (const double *)slab, (const double *)part_ew, 2.0 * nu, nu, forces, energy_virial);

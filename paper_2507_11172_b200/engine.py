@@ -313,14 +313,17 @@ class ForceEngine:
         self._count()
 
     # ------------------------------------------------------------ DirectSum
-    def direct_pairs(self, epsilon: float, sigma: float, forces, tag: int = 0) -> None:
+    def direct_pairs(self, epsilon: float, sigma: float, forces, tag: int = 0,
+                     reduce: bool = True) -> None:
         """All pairs of the particle-order positions (no cutoff, no image);
-        scalars[E2], scalars[W2] <- energy, virial."""
+        per-particle halves in e2_rank/w2_rank, summed into scalars[E2],
+        scalars[W2] when `reduce`."""
         st = self.L.rb_direct_pairs(self.n, ptr(self.pos), float(epsilon), float(sigma),
                                     ptr(forces), ptr(self.e2_rank), ptr(self.w2_rank),
                                     ptr(self.status), int(tag), self.stream)
         _lib.check(st, "rb_direct_pairs")
-        self.reduce_pair()
+        if reduce:
+            self.reduce_pair()
 
     def direct_triplets(self, nu: float, forces, tag: int = 0) -> None:
         """All triplets (Newton-3); scalars[E3], scalars[W3] <- energy, virial."""

@@ -36,7 +36,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import ptr
-from .containers import CudaLinkedCells, MinimumSeparationError, engine_for
+from .containers import CudaDirectSum, CudaLinkedCells, MinimumSeparationError, engine_for
 from .engine import (SCALAR_E2, SCALAR_E3, SCALAR_W2, SCALAR_W3, CapacityError,
                      _round_up)
 from .grid import geometry
@@ -137,7 +137,12 @@ class DeviceRespa:
         self.interval = int(sample_interval)
         self.n = int(system.positions.shape[0])
         self.periodic = bool(system.periodic)
-        self.use_graph = use_graph and self.periodic
+        # DirectSum container: all pairs / triplets, no grid (open systems only)
+        self.direct = isinstance(container, CudaDirectSum)
+        if self.direct and self.periodic:
+            raise ValidationError("DirectSum does not support periodic boundaries")
+        # open linked-cell systems need a host-synchronised grid every step
+        self.use_graph = use_graph and (self.periodic or self.direct)
         self.eng = engine_for(self.n)  # device workspace cached per particle count
         torch = self.torch = self.eng.torch
         dev, f64 = self.eng.device, torch.float64
@@ -189,6 +194,21 @@ class DeviceRespa:
 
     def _forces(self, tag: int, with_triplet: bool, f2_out, cond: int = 0) -> None:
         eng = self.eng
+        if self.direct:
+            eng.direct_pairs(self.ff.epsilon, self.ff.sigma, f2_out, tag=tag, reduce=False)
+            if with_triplet:
+                if self.with_3b:
+                    eng.direct_triplets(self.nu, self.f3, tag=tag)
+                    # E3, W3 come as totals: one entry of the per-rank arrays
+                    eng.e3_rank.zero_()
+                    eng.w3_rank.zero_()
+                    eng.e3_rank[:1].copy_(eng.scalars[SCALAR_E3:SCALAR_E3 + 1])
+                    eng.w3_rank[:1].copy_(eng.scalars[SCALAR_W3:SCALAR_W3 + 1])
+                else:
+                    self.f3.zero_()
+                    eng.e3_rank.zero_()
+                    eng.w3_rank.zero_()
+            return
         geom = self._geom()
         if geom is None:
             # open system with non-finite positions: forces are undefined;
@@ -259,7 +279,7 @@ class DeviceRespa:
         self.v.copy_(torch.from_numpy(np.ascontiguousarray(self.system.velocities, np.float64)))
         eng.reset_status(0)
         eng.rebuild_flag.zero_()  # tag 0 == forced build for the initial passes
-        if self.capacity is None or self.slots is None:
+        if not self.direct and (self.capacity is None or self.slots is None):
             geom = self._geom()
             eng.bin(geom, self.x)
             # rows (at r_list + skin) and the triplet pass's shared-memory slots
@@ -348,8 +368,9 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
               hooks=(), use_graph: bool = True, capacity: Optional[int] = None,
               skin: Optional[float] = None) -> RunTrace:
     """Integrate in place with the r-RESPA loop on the GPU (integrators.py:96-173)."""
-    if not isinstance(container, CudaLinkedCells):
-        raise TypeError("respa_run needs a CudaLinkedCells container (GPU only, no host fallback)")
+    if not isinstance(container, (CudaLinkedCells, CudaDirectSum)):
+        raise TypeError("respa_run needs a CudaLinkedCells or CudaDirectSum container "
+                        "(GPU only, no host fallback)")
     s = schedule.step_size_factor
     if sample_interval is None:
         sample_interval = s

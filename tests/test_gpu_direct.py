@@ -142,3 +142,29 @@ def test_direct_sum_guard_and_determinism(pkg):
         pkg.direct_sum_triplets(s2, ff)
     c.triplet_pass(s, pkg.ForceField(nu=0.0))
     assert not s.forces_3b.any() and c.triplet_energy == 0.0
+
+
+def test_respa_with_direct_sum_matches_oracle(pkg, oracle):
+    """The device r-RESPA loop driving DirectSum (graph replay and eager)
+    against the oracle's respa_run with the DirectSum restatement."""
+    rng = np.random.default_rng(TEST_SEED + 5)
+    n, edge = 80, 7.0
+    pos = random_positions(rng, n, (edge,) * 3, False)
+    vel = rng.normal(0.0, 0.5, (n, 3))
+    vel -= vel.mean(axis=0)
+    ff = pkg.ForceField(nu=0.4)
+    sched = pkg.RespaSchedule(0.002, 3, 30)
+    runs = []
+    for graph in (True, False):
+        s = _system(pkg, pos, edge)
+        s.velocities[:] = vel
+        runs.append((s, pkg.respa_run(s, ff, pkg.CudaDirectSum(), sched, use_graph=graph)))
+    os_ = oracle.OracleSystem.from_positions(pos, (edge,) * 3, False, vel)
+    otr = oracle.respa_run(os_, oracle.OracleForceField(nu=0.4), oracle.OracleDirectSum(), 0.002,
+                           3, 30)
+    (sg, tg), (se, te) = runs
+    assert np.array_equal(sg.positions, se.positions) and tg.total == te.total
+    assert np.max(np.abs(sg.positions - os_.positions)) <= 1e-10
+    assert np.max(np.abs(sg.velocities - os_.velocities)) <= 1e-10
+    assert list(tg.iterations) == list(otr.iterations)
+    assert max(_rel(a, b) for a, b in zip(tg.total, otr.total)) <= 1e-10

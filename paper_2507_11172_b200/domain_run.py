@@ -8,10 +8,14 @@ with the exchange of ``domain.py`` around the force passes:
     rebuild:  migrate + ghosts + local rows    -- domain.py + backend
     else:     refresh ghost positions          -- domain.py
     LJ on the local set, kick, [ATM every s-th step, kick3]
-    samples: per-rank partial scalars summed in rank order
+    samples: per-rank partial scalars summed in rank order; device errors
+             (tagged with the device step counter) checked there
 
-The force backend is the sm_100a engine (``GpuBackend``); the CPU tests plug
-in a numpy restatement with the same interface.
+The force backend is the sm_100a engine (``GpuBackend``): the owned state
+lives in device buffers and each step is drift kernel -> vote (the one host
+synchronisation) -> halo refresh -> LJ [-> ATM] -> kick kernel.  The CPU
+tests plug in a numpy restatement and take the torch version of the same
+loop.
 """
 
 from __future__ import annotations
@@ -47,7 +51,12 @@ class GpuBackend:
         self.window = None
         self.n_own = 0
         self.n_local = 0
-        self.f_local = self.torch.zeros((n_max, 3), dtype=self.torch.float64, device=self.device)
+        z = lambda: self.torch.zeros((n_max, 3), dtype=self.torch.float64, device=self.device)  # noqa: E731
+        self.f_local = z()
+        # device-resident owned state (particle order, owned rows first): the
+        # fused drift / kick kernels update it in place between rebuilds
+        self.v, self.f2, self.f2_new, self.f3 = z(), z(), z(), z()
+        self.eng.reset_status(0)
 
     def set_local(self, local, n_own: int, window, rebuild: bool) -> None:
         eng, torch = self.eng, self.torch
@@ -56,7 +65,6 @@ class GpuBackend:
             eng.set_count(n)
             self.window, self.n_own, self.n_local = window, int(n_own), n
             eng.pos[:n] = local
-            eng.reset_status(0)
             eng.bin(window)
             eng.nlist(window, self.r_build, capacity=eng.capacity or None, checked=True)
             eng.owned_rank = (eng.parts[:n] < n_own).to(torch.uint8)
@@ -64,25 +72,91 @@ class GpuBackend:
             eng.pos[:n] = local
             eng.pos_r[:n][eng.rank_of[:n].long()] = eng.pos[:n]
 
-    def pair(self):
+    def pair(self, scalars: bool = True):
         eng = self.eng
-        eng.lj(self.window, self.rc2, self.ff.epsilon, self.ff.sigma, self.f_local, tag=0)
+        eng.lj(self.window, self.rc2, self.ff.epsilon, self.ff.sigma, self.f_local,
+               tag=self._lib.RB_TAG_FROM_DEVICE, reduce=scalars)
         return self.f_local[: self.n_own].clone(), eng.scalars[1:3].clone()
 
-    def triplet(self):
+    def triplet(self, scalars: bool = True):
         eng = self.eng
         if float(self.ff.nu) == 0.0:
             return (self.torch.zeros((self.n_own, 3), dtype=self.torch.float64, device=self.device),
                     self.torch.zeros(2, dtype=self.torch.float64, device=self.device))
-        eng.atm(self.window, self.rc3, float(self.ff.nu), self.f_local, tag=0, count_visits=False)
+        eng.atm(self.window, self.rc3, float(self.ff.nu), self.f_local,
+                tag=self._lib.RB_TAG_FROM_DEVICE, count_visits=False, reduce=scalars)
         return self.f_local[: self.n_own].clone(), eng.scalars[3:5].clone()
 
-    def check(self) -> Optional[str]:
+    def advance(self) -> None:
+        """Open the next step: the device step counter tags later errors."""
+        self.eng.status[1:2].add_(1)
+
+    # ---- fused per-step primitives (the loop's fast path on the GPU) ----
+    def bind(self, st) -> None:
+        """After a rebuild: the owned state moves into the device buffers and
+        `st` becomes views of them (positions are eng.pos[:n_own])."""
+        n = self.n_own
+        for name, buf in (("v", self.v), ("f2", self.f2), ("f3", self.f3)):
+            buf[:n] = getattr(st, name)
+            setattr(st, name, buf[:n])
+        st.x = self.eng.pos[:n]
+
+    def local_view(self):
+        return self.eng.pos[: self.n_local]
+
+    def drift(self, box, dt, half_drift, half_respa, kick3: bool, skin: float):
+        """kick3 / drift / wrap of the owned rows, their rank-order copy and
+        the skin check (rb_respa_drift, opening the device step); returns the
+        rank's rebuild vote as a 0-d device tensor."""
+        eng, L = self.eng, self.eng.L
+        ptr = self._lib.ptr
+        st = L.rb_respa_drift(self.n_own, ptr(eng.pos), ptr(self.v), ptr(self.f2), ptr(self.f3),
+                              box.ctypes.data_as(ctypes.c_void_p), 1, dt, half_drift, half_respa,
+                              int(kick3), ptr(eng.rank_of), ptr(eng.pos_r), ptr(eng.x_ref), skin,
+                              ptr(eng.rebuild_flag), ptr(eng.status),
+                              self._lib.RB_TAG_FROM_DEVICE, 1, 0, eng.stream)
+        self._lib.check(st, "rb_respa_drift")
+        return eng.rebuild_flag[0] == eng.status[1]
+
+    def ghosts_moved(self) -> None:
+        """Ghost rows of eng.pos were refreshed in place: their rank-order copy."""
+        eng, n, n_own = self.eng, self.n_local, self.n_own
+        if n > n_own:
+            eng.pos_r[:n][eng.rank_of[n_own:n].long()] = eng.pos[n_own:n]
+
+    def pair_into_new(self, scalars: bool):
+        eng = self.eng
+        eng.lj(self.window, self.rc2, self.ff.epsilon, self.ff.sigma, self.f2_new,
+               tag=self._lib.RB_TAG_FROM_DEVICE, reduce=scalars)
+        return eng.scalars[1:3]
+
+    def triplet_into_f3(self, scalars: bool):
+        eng = self.eng
+        if float(self.ff.nu) == 0.0:
+            self.f3.zero_()
+            return self.torch.zeros(2, dtype=self.torch.float64, device=self.device)
+        eng.atm(self.window, self.rc3, float(self.ff.nu), self.f3,
+                tag=self._lib.RB_TAG_FROM_DEVICE, count_visits=False, reduce=scalars)
+        return eng.scalars[3:5]
+
+    def kick(self, half_dt, half_respa, kick3: bool) -> None:
+        """v += half_dt (f2_old + f2_new), f2_old := f2_new [, v += half_respa f3]."""
+        eng, L = self.eng, self.eng.L
+        ptr = self._lib.ptr
+        st = L.rb_respa_kick(self.n_own, ptr(self.v), ptr(self.f2), ptr(self.f2_new), ptr(self.f3),
+                             half_dt, half_respa, int(kick3), ptr(eng.status),
+                             self._lib.RB_TAG_FROM_DEVICE, eng.stream)
+        self._lib.check(st, "rb_respa_kick")
+
+    def check(self):
+        """(iteration, reason) of the first recorded device error, or None."""
         err = self.eng.read_status()
         if err is None:
             return None
-        return "particles closer than the minimum separation guard" if err[1] in (1, 2) else \
-            f"device error kind {err[1]}"
+        reason = {1: "particles closer than the minimum separation guard",
+                  2: "particles closer than the minimum separation guard",
+                  3: "non-finite position or velocity"}.get(err[1], f"device error kind {err[1]}")
+        return int(err[0]), reason
 
 
 @dataclass
@@ -135,6 +209,11 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     window = dec.window()
     trace = RunTrace()
 
+    # GPU backends run the per-step updates as fused kernels on device-resident
+    # state (one host synchronisation per step: the rebuild vote); other
+    # backends (the numpy one of the CPU tests) take the torch restatement
+    fast = hasattr(backend, "bind")
+
     def rebuild():
         nonlocal window
         if st.f2 is not None:
@@ -143,8 +222,14 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
             st.ids, st.x, st.v = payload[:, 0], payload[:, 1:4], payload[:, 4:7]
             st.f2, st.f3 = payload[:, 7:10].contiguous(), payload[:, 10:13].contiguous()
             st.x, st.v = st.x.contiguous(), st.v.contiguous()
+        else:
+            st.f2 = torch.zeros_like(st.x)
+            st.f3 = torch.zeros_like(st.x)
         local, plan = build_ghosts(dec, ex, st.x)
         backend.set_local(local, plan.n_owned, window, rebuild=True)
+        if fast:
+            backend.bind(st)
+            return backend.local_view(), plan
         st.x_ref = st.x.clone()
         return local, plan
 
@@ -164,48 +249,98 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
 
     wire = torch.device("cpu") if dist.get_backend() == "gloo" else dev
 
-    def any_flag(flag: bool) -> bool:
-        t = torch.tensor([1 if flag else 0], dtype=torch.int64, device=wire)
+    def any_flag(flag) -> bool:
+        """Global OR of a per-rank flag (python bool or 0-d device tensor):
+        one all_reduce and the step's single host synchronisation."""
+        t = torch.as_tensor(flag, dtype=torch.int64).reshape(1).to(wire)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return bool(t.item())
 
-    def fail(it):
-        msg = backend.check()
-        if any_flag(msg is not None):
-            raise IntegrationBlowUp(it, msg or "error on another rank", trace)
+    # errors are checked at sample points (as the single-GPU loop does at the
+    # end): the first non-finite step is kept on the device meanwhile
+    first_bad = torch.full((1,), np.iinfo(np.int64).max, dtype=torch.int64, device=dev)
+
+    never = np.iinfo(np.int64).max
+
+    def check(upto: int) -> None:
+        """Raise IntegrationBlowUp at the first failing iteration of any rank
+        (integrators.py:154-170), checked at sample points."""
+        err = backend.check()
+        mine = torch.stack([first_bad.to(wire)[0],
+                            torch.tensor(never if err is None else err[0], dtype=torch.int64,
+                                         device=wire)])
+        both = mine.clone()
+        dist.all_reduce(both, op=dist.ReduceOp.MIN)
+        it = int(both.min().item())
+        if it <= upto:
+            if err is not None and err[0] == it:
+                reason = err[1]
+            elif int(mine[0].item()) == it:
+                reason = "non-finite position or velocity"
+            else:
+                reason = "error on another rank"
+            raise IntegrationBlowUp(it, reason, trace)
 
     local, plan = rebuild()
-    f2, e2w2 = backend.pair()
-    f3, e3w3 = backend.triplet()
-    fail(0)
-    st.f2, st.f3 = f2, f3
+    if fast:
+        e2w2 = backend.pair_into_new(True)
+        st.f2.copy_(backend.f2_new[: plan.n_owned])
+        e3w3 = backend.triplet_into_f3(True)
+    else:
+        f2, e2w2 = backend.pair()
+        f3, e3w3 = backend.triplet()
+        st.f2, st.f3 = f2, f3
+    check(0)
     record(0, e2w2, e3w3)
     half_skin2 = (0.5 * skin) ** 2 * (1.0 - 1e-9)
     for i in range(schedule.num_iterations):
+        sample = (i + 1) % interval == 0
+        end_of_cycle = (i + 1) % s == 0
+        if fast:
+            moved = backend.drift(box, dt, half_drift, half_respa, i % s == 0, skin)
+            if any_flag(moved if skin > 0.0 else True):
+                local, plan = rebuild()
+            else:
+                refresh_ghosts(dec, ex, plan, local)
+                backend.ghosts_moved()
+            e2w2 = backend.pair_into_new(sample)
+            if end_of_cycle:
+                e3w3 = backend.triplet_into_f3(sample)
+            backend.kick(half_dt, half_respa, end_of_cycle)
+            if sample:
+                check(i + 1)
+                record(i + 1, e2w2, e3w3)
+            continue
+        if hasattr(backend, "advance"):
+            backend.advance()
         if i % s == 0:
             st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
         st.x = st.x + ((dt * st.v) + (half_drift * st.f2))
         st.x = torch.remainder(st.x, box_t)  # numpy mod semantics for box > 0
         st.x = torch.where(st.x >= box_t, torch.zeros_like(st.x), st.x)
-        d = st.x - st.x_ref
-        d = d - box_t * torch.where(d > 0.5 * box_t, 1.0, torch.where(d < -0.5 * box_t, -1.0, 0.0))
-        moved = bool((d * d).sum(dim=1).max().item() > half_skin2) if st.x.shape[0] else False
-        if any_flag(moved or skin == 0.0):
+        if skin == 0.0 or st.x.shape[0] == 0:
+            moved = skin == 0.0
+        else:
+            d = st.x - st.x_ref
+            d = d - box_t * torch.where(d > 0.5 * box_t, 1.0, torch.where(d < -0.5 * box_t, -1.0, 0.0))
+            moved = ((d * d).sum(dim=1).max() > half_skin2)
+        if any_flag(moved):
             local, plan = rebuild()
         else:
             refresh(plan, local)
-        f2_new, e2w2 = backend.pair()
+        f2_new, e2w2 = backend.pair(scalars=sample)
         st.v = st.v + (half_dt * (st.f2 + f2_new))
         st.f2 = f2_new
         if (i + 1) % s == 0:
-            st.f3, e3w3 = backend.triplet()
+            st.f3, e3w3 = backend.triplet(scalars=sample)
             st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
-        finite = bool(torch.isfinite(st.x).all().item() and torch.isfinite(st.v).all().item())
-        fail(i + 1)
-        if any_flag(not finite):
-            raise IntegrationBlowUp(i + 1, "non-finite position or velocity", trace)
-        if (i + 1) % interval == 0:
+        finite = torch.isfinite(st.x).all() & torch.isfinite(st.v).all()
+        first_bad = torch.where(finite | (first_bad <= i), first_bad,
+                                torch.full_like(first_bad, i + 1))
+        if sample:
+            check(i + 1)
             record(i + 1, e2w2, e3w3)
+    check(schedule.num_iterations)
 
     # gather the owned state of every rank into the host system (by id)
     parts = [None] * world

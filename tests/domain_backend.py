@@ -58,7 +58,7 @@ class NumpyBackend:
         self.pos = local.detach().cpu().numpy().copy()
         self.n_own = int(n_own)
 
-    def pair(self):
+    def pair(self, scalars=True):
         pos, n = self.pos, self.n_own
         f = np.zeros((n, 3))
         e = w = 0.0
@@ -73,7 +73,7 @@ class NumpyBackend:
             w += float(np.sum(0.5 * sc * r2[m]))
         return torch.as_tensor(f), torch.tensor([e, w], dtype=torch.float64)
 
-    def triplet(self):
+    def triplet(self, scalars=True):
         pos, n = self.pos, self.n_own
         f = np.zeros((n, 3))
         e = w = 0.0

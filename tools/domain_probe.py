@@ -1,0 +1,60 @@
+#!/usr/bin/env python
+"""Per-step cost of the domain-decomposed loop on one GPU (world = 1).
+
+    python tools/domain_probe.py [--steps K] [--backend nccl|gloo]
+
+Runs domain_respa_run on cfg2 with a single rank: no halo,
+but every per-step piece of the multi-GPU loop (drift, rebuild vote,
+refresh, passes, kicks, sample checks).  Prints ms/step (wall clock after a
+warm-up run) next to the single-GPU graph loop's.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+
+def main(argv):
+    import torch
+    import torch.distributed as dist
+
+    steps = int(argv[argv.index("--steps") + 1]) if "--steps" in argv else 200
+    backend = argv[argv.index("--backend") + 1] if "--backend" in argv else "nccl"
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=0, world_size=1)
+    import paper_2507_11172_b200 as pkg
+    from paper_2507_11172_b200.domain_run import domain_respa_run, gpu_backend_factory
+
+    cfg = pkg.systems.CONFIGS["cfg2"]
+    ff = cfg.force_field()
+    sf = cfg.step_size_factor
+    domain_respa_run(dist, cfg.system(), ff, pkg.RespaSchedule(cfg.dt, sf, 20),
+                     gpu_backend_factory(ff))
+    s = cfg.system()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    domain_respa_run(dist, s, ff, pkg.RespaSchedule(cfg.dt, sf, steps), gpu_backend_factory(ff))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    print(f"domain loop (world 1, {backend}): {1e3 * dt / steps:.3f} ms/step over {steps} steps")
+    s2 = cfg.system()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pkg.respa_run(s2, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(cfg.dt, sf, steps))
+    torch.cuda.synchronize()
+    dt2 = time.perf_counter() - t0
+    import numpy as np
+    print(f"single-GPU respa_run: {1e3 * dt2 / steps:.3f} ms/step; max |dx| "
+          f"{np.max(np.abs(s.positions - s2.positions)):.2e}")
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

@@ -220,9 +220,9 @@ RB_API int rb_reduce_sum_i32(int64_t n, const int32_t *in, int64_t *out, void *s
  *        *rebuild_flag = tag when a particle moved more than skin/2 from
  *        x_ref (the neighbour rows, built at rc + skin, must be rebuilt).
  *        advance_step != 0 (tag must be -1): the drift opens a new device
- *        step -- its tag is status[1] + 1 and it leaves status[1] at that
- *        value for the step's later kernels (rb_step_begin folded in; uses
- *        status[2] as a block ticket).  rebuild_cond != 0: a CUDA-graph
+ *        step -- its tag is status[2] + 1 (the last closed step + 1) and it
+ *        writes it to status[1] for the step's later kernels; the step's
+ *        kick (tag -1) closes it.  rebuild_cond != 0: a CUDA-graph
  *        conditional handle (rb_rebuild_cond_create) set to 1 together with
  *        the rebuild flag.
  * kick:  v += half_dt*(f2_old + f2_new); f2_old = f2_new (:159);
@@ -240,10 +240,13 @@ RB_API int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f
                   unsigned long long *status, int64_t tag, void *stream);
 
 /* ---- device-side step counter and trace (CUDA-graph friendly) ---------
- * status points to FOUR words: status[0] the error word, status[1] the step
- * counter, status[2] a ticket of rb_respa_drift's step advance (zero
- * between launches), status[3] the number of steps whose step-opening drift
- * flagged a row rebuild (diagnostic).  Kernels given tag == -1 read their tag from status[1].
+ * status points to FOUR words: status[0] the error word, status[1] the
+ * current step, status[2] the last closed step, status[3] the number of
+ * steps in which a drift flagged a row rebuild (diagnostic).  A
+ * step-opening drift (advance_step) numbers its step status[2] + 1 and
+ * writes it to status[1]; a kick with tag -1 closes the step (status[2] =
+ * status[1]); rb_step_begin does both in one launch (status[2] = status[1],
+ * status[1] += 1).  Kernels given tag == -1 read their tag from status[1].
  * rb_step_begin increments status[1]; rb_trace_record writes the 8-double
  * row [tag, sum v^2, E2, W2, E3, W3, 0, 0] at trace[8 * (tag / interval)]
  * from device scalars (RunTrace.record, integrators.py:74-83). */

@@ -56,10 +56,15 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
                         int advance, cudaGraphConditionalHandle cond) {
     pdl_enter();
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // a step-opening drift reads the counter before its block takes a ticket;
-    // the last block publishes the new value (no block reads it after that)
-    tag = advance ? (int64_t)(*(volatile const unsigned long long *)(status + 1)) + 1
-                  : resolve_tag(tag, status);
+    // a step-opening drift numbers its step from the last CLOSED step
+    // (status[2], written by the kick) and publishes it in status[1]: no
+    // kernel reads the word another block of it writes
+    if (advance) {
+        tag = (int64_t)(*(volatile const unsigned long long *)(status + 2)) + 1;
+        if (p == 0) status[1] = (unsigned long long)tag;
+    } else {
+        tag = resolve_tag(tag, status);
+    }
     if (p < n && !frozen(status, tag, 0)) {
         const double box[3] = {bx, by, bz};
         double x[3];
@@ -94,21 +99,11 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
                 d2 += d * d;
             }
             if (!(d2 <= skin_half2)) {  // also catches NaN
-                *rebuild_flag = tag;
+                // the first thread to flag this step counts a rebuild step
+                const unsigned long long was = atomicExch(
+                    reinterpret_cast<unsigned long long *>(rebuild_flag), (unsigned long long)tag);
+                if ((int64_t)was != tag && status) atomicAdd(status + 3, 1ull);
                 if (cond) cudaGraphSetConditional(cond, 1u);
-            }
-        }
-    }
-    if (advance) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            if (atomicAdd(status + 2, 1ull) == (unsigned long long)(gridDim.x - 1)) {
-                status[2] = 0ull;
-                // every block's flag write precedes its ticket: count rebuild steps
-                if (rebuild_flag && *(volatile const int64_t *)rebuild_flag == tag) status[3] += 1ull;
-                __threadfence();
-                status[1] = (unsigned long long)tag;
             }
         }
     }
@@ -120,8 +115,10 @@ __global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict_
                        int64_t tag) {
     pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n3) return;
+    const bool from_device = tag < 0;
     tag = resolve_tag(tag, status);
+    if (from_device && status && i == 0) status[2] = (unsigned long long)tag;  // closes the step
+    if (i >= n3) return;
     bool do_kick2 = true, do_kick3 = kick3 != 0;
     if (status) {
         const unsigned long long s = *(volatile const unsigned long long *)status;
@@ -304,7 +301,10 @@ __global__ void k_fp64_fma(int iters, double seed, double *sink) {
 }
 
 __global__ void k_step_begin(unsigned long long *status) {
-    pdl_enter(); status[1] += 1ull; }
+    pdl_enter();
+    status[2] = status[1];
+    status[1] += 1ull;
+}
 
 // trace row (tag / interval): [tag, sum v^2, E2, W2, E3, W3, 0, 0]
 __global__ void k_trace_record(const unsigned long long *status, int64_t interval, double *trace,
@@ -357,10 +357,10 @@ extern "C" int rb_respa_kick(int64_t n, double *vel, double *f2_old, const doubl
                              const double *f3, double half_dt, double half_respa, int32_t kick3,
                              unsigned long long *status, int64_t tag, void *stream) {
     if (n < 0) return RB_ERR_ARGUMENT;
-    if (n == 0) return RB_OK;
     const int64_t n3 = 3 * n;
+    if (n == 0 && (tag >= 0 || !status)) return RB_OK;  // (tag < 0: still closes the step)
     const int tb = 256;
-    launch(k_kick, dim3((unsigned)((n3 + tb - 1) / tb)), dim3(tb), 0, as_stream(stream), n3, vel, f2_old, f2_new, f3, half_dt, half_respa, kick3, status, tag);
+    launch(k_kick, dim3(n3 > 0 ? (unsigned)((n3 + tb - 1) / tb) : 1u), dim3(tb), 0, as_stream(stream), n3, vel, f2_old, f2_new, f3, half_dt, half_respa, kick3, status, tag);
     note_launches(1);
     return launch_status();
 }

@@ -87,10 +87,6 @@ class GpuBackend:
                 tag=self._lib.RB_TAG_FROM_DEVICE, count_visits=False, reduce=scalars)
         return self.f_local[: self.n_own].clone(), eng.scalars[3:5].clone()
 
-    def advance(self) -> None:
-        """Open the next step: the device step counter tags later errors."""
-        self.eng.status[1:2].add_(1)
-
     # ---- fused per-step primitives (the loop's fast path on the GPU) ----
     def bind(self, st) -> None:
         """After a rebuild: the owned state moves into the device buffers and

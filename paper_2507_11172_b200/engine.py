@@ -67,9 +67,9 @@ class ForceEngine:
         self.v_rank = torch.zeros(n, dtype=i32, device=dev)
         self.row_count = torch.zeros(n, dtype=i32, device=dev)
         self.max_count = torch.zeros(1, dtype=i32, device=dev)
-        # status[0]: error word (all ones = clear); status[1]: device step
-        # counter; status[2]: ticket of the step-opening drift; status[3]:
-        # rebuild steps flagged by step-opening drifts
+        # status[0]: error word (all ones = clear); status[1]: current device
+        # step; status[2]: last closed step (the kick); status[3]: rebuild
+        # steps flagged by drifts (include/respa_b200.h)
         self.status = torch.tensor([-1, 0, 0, 0], dtype=i64, device=dev)
         self.rebuild_flag = torch.zeros(1, dtype=i64, device=dev)
         self.scalars = torch.zeros(8, dtype=f64, device=dev)
@@ -149,8 +149,13 @@ class ForceEngine:
 
     def reset_status(self, step: int = 0) -> None:
         self.status[0] = -1
-        self.status[1] = int(step)
-        self.status[2:].zero_()
+        self.status[3:].zero_()
+        self.set_step(step)
+
+    def set_step(self, step: int) -> None:
+        """Device step counter: step `step` current and closed (the next
+        step-opening drift numbers its step step + 1)."""
+        self.status[1:3] = int(step)
 
     def read_status(self):
         """(tag, kind) of the first recorded device error, or None (syncs)."""

@@ -248,7 +248,7 @@ class DeviceRespa:
         null = ctypes.c_void_p(0)
         # under capture: the drift sets the rebuild conditional with the flag
         cond = eng.rebuild_cond() if verlet and self.cond_rebuild else 0
-        # the drift opens the device step (status[1] += 1)
+        # the drift opens the device step (status[1] = last closed + 1)
         st = L.rb_respa_drift(self.n, ptr(self.x), ptr(self.v), ptr(self.f2_old), ptr(self.f3),
                               self.box.ctypes.data_as(ctypes.c_void_p), int(self.periodic),
                               self.dt, self.half_drift, self.half_respa, int(i % s == 0),
@@ -436,7 +436,7 @@ def _drive(run: DeviceRespa, hooks) -> RunTrace:
         run.capture()
         mark(("captured", time.perf_counter()))
         # the capture recorded but did not execute; rewind nothing: replay the rest
-        run.eng.status[1] = run.interval
+        run.eng.set_step(run.interval)
         run.run_periods(1, n_periods - 1)
         mark(("replays enqueued", time.perf_counter()))
     else:

@@ -60,7 +60,7 @@ def main(argv):
     t = tick("first period (eager)", t)
     run.capture()
     t = tick("capture", t)
-    run.eng.status[1] = run.interval
+    run.eng.set_step(run.interval)
     t = tick("status reset", t)
     n_periods = steps // run.interval
     run.run_periods(1, n_periods - 1)

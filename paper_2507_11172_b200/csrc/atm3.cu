@@ -288,7 +288,18 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     // ---- phase 0: S+(i), the row suffix with rank > i within rc
     int m = 0;
     bool slot_bad = false;
-    for (int base = 0; base < rc_n; base += 32) {
+    // rows are rank-sorted: start at the first 32-entry chunk whose last
+    // entry follows i (one load per chunk, in parallel, then a ballot)
+    int first = 0;
+    {
+        const int nchunks = (rc_n + 31) >> 5;
+        bool after = false;
+        if (lane < nchunks) after = row[min(32 * lane + 31, rc_n - 1)] > r;
+        const unsigned b = __ballot_sync(0xffffffffu, after);
+        first = b ? 32 * (__ffs(b) - 1) : rc_n;
+        if (nchunks > 32) first = 0;  // longer rows than one ballot covers: scan all
+    }
+    for (int base = first; base < rc_n; base += 32) {
         const int k = base + lane;
         bool keep = false;
         double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;

@@ -299,14 +299,31 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
         first = b ? 32 * (__ffs(b) - 1) : rc_n;
         if (nchunks > 32) first = 0;  // longer rows than one ballot covers: scan all
     }
-    for (int base = first; base < rc_n; base += 32) {
-        const int k = base + lane;
-        bool keep = false;
-        double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;
-        if (k < rc_n) {
-            const int q = row[k];
+    // two chunks per iteration: both rows' loads, then both positions' loads
+    // are in flight together (phase 0 is latency-bound)
+    for (int base = first; base < rc_n; base += 64) {
+        int q2[2];
+        double px[2], py[2], pz[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int k = base + 32 * h + lane;
+            q2[h] = k < rc_n ? row[k] : -1;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int q = q2[h] > r ? q2[h] : (int)r;  // (own position: a harmless load)
+            px[h] = pr[3 * q];
+            py[h] = pr[3 * q + 1];
+            pz[h] = pr[3 * q + 2];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int k = base + 32 * h + lane;
+            const int q = q2[h];
+            bool keep = false;
+            double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;
             if (q > r) {
-                exact_disp(im, xi, yi, zi, pr[3 * q], pr[3 * q + 1], pr[3 * q + 2], dx, dy, dz);
+                exact_disp(im, xi, yi, zi, px[h], py[h], pz[h], dx, dy, dz);
                 r2 = exact_r2(dx, dy, dz);
                 keep = r2 <= rc2;
                 if (!keep) {  // beyond the three-body cutoff: contributes nothing
@@ -316,28 +333,28 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
                     gq[2] = 0.0;
                 }
             }
-        }
-        const unsigned mk = __ballot_sync(0xffffffffu, keep);
-        if (m + __popc(mk) > slots) {  // S+(i) does not fit the shared-memory slots
-            if (lane == 0) {
-                if (ovf)
-                    ovf[2 + atomicAdd(ovf, 1)] = (int32_t)r;
-                else
-                    record_status(status, tag, RB_KIND_CAPACITY);
+            const unsigned mk = __ballot_sync(0xffffffffu, keep);
+            if (m + __popc(mk) > slots) {  // S+(i) does not fit the shared-memory slots
+                if (lane == 0) {
+                    if (ovf)
+                        ovf[2 + atomicAdd(ovf, 1)] = (int32_t)r;
+                    else
+                        record_status(status, tag, RB_KIND_CAPACITY);
+                }
+                return;
             }
-            return;
+            if (keep) {
+                const int slot = m + __popc(mk & lanemask_lt());
+                sm.dxy[slot] = make_double2(dx, dy);
+                sm.dz[slot] = dz;
+                sm.r2[slot] = r2;
+                sm.kidx[slot] = k | ((kOwned ? (int)owned[q] : 1) << 30);
+                sm.axy[slot] = make_double2(0.0, 0.0);
+                sm.az[slot] = 0.0;
+            }
+            m += __popc(mk);
+            slot_bad |= __any_sync(0xffffffffu, keep && r2 < RB_MIN_DISTANCE_SQ);
         }
-        if (keep) {
-            const int slot = m + __popc(mk & lanemask_lt());
-            sm.dxy[slot] = make_double2(dx, dy);
-            sm.dz[slot] = dz;
-            sm.r2[slot] = r2;
-            sm.kidx[slot] = k | ((kOwned ? (int)owned[row[k]] : 1) << 30);
-            sm.axy[slot] = make_double2(0.0, 0.0);
-            sm.az[slot] = 0.0;
-        }
-        m += __popc(mk);
-        slot_bad |= __any_sync(0xffffffffu, keep && r2 < RB_MIN_DISTANCE_SQ);
     }
     __syncwarp();
 

@@ -73,7 +73,7 @@ __device__ __forceinline__ A3Smem a3_carve(char *base, int m_rt) {
 }
 
 struct A3Acc {
-    double fx, fy, fz, e, w;
+    double e, w;     // f_i is not accumulated: f_i = -(f_j + f_k) per triplet
     int n;
     bool bad;
     int owned_i;     // decomposed runs: the base particle is owned by this rank
@@ -127,9 +127,6 @@ __device__ __forceinline__ void a3_core(const A3Smem &sm, int s, int t, double a
     const double ea = fma(A, fma(-2.0, uv, S), -K * (b * c));
     const double eb = fma(A, fma(-2.0, uw, S), -K * (a * c));
     const double ec = fma(A, fma(-2.0, vw, S), -K * (a * b));
-    acc.fx = fma(-ea, ij.x, fma(-eb, ik.x, acc.fx));
-    acc.fy = fma(-ea, ij.y, fma(-eb, ik.y, acc.fy));
-    acc.fz = fma(-ea, ijz, fma(-eb, ikz, acc.fz));
     if (kOwned) {
         const double share =
             owned_share(acc.owned_i + (sm.kidx[s] >> 30) + (sm.kidx[t] >> 30));
@@ -359,23 +356,30 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     __syncwarp();
 
     // ---- phase 1: the slot pairs, 32 per window (a3_windows)
-    A3Acc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1, slot_bad};
+    A3Acc acc = {0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1, slot_bad};
     if (debug_mode != 1)  // debug 1: phases 0 and 3 only
         a3_windows<kExactImage, kOwned>(sm, m, lane, g, row, pr, rc2, rc2_lo, rc2_hi, acc);
     __syncwarp();
 
-    // ---- phase 3: slot sums -> G[i][row index]; own part, scalars
+    // ---- phase 3: slot sums -> G[i][row index]; own part, scalars.  Per
+    // triplet f_i + f_j + f_k = 0, so the base's own force is minus the sum
+    // of everything its triplets gave the slots (fixed lane order and tree)
+    double sx = 0.0, sy = 0.0, sz = 0.0;
     for (int sl = lane; sl < m; sl += 32) {
         const int k = sm.kidx[sl] & kKidxMask;
         const double2 xy = sm.axy[sl];
+        const double z = sm.az[sl];
         double *gq = gbuf + ((int64_t)row[k] * capacity + mir[k]) * 3;
         gq[0] = xy.x;
         gq[1] = xy.y;
-        gq[2] = sm.az[sl];
+        gq[2] = z;
+        sx += xy.x;
+        sy += xy.y;
+        sz += z;
     }
-    const double fx = group_sum<32>(acc.fx);
-    const double fy = group_sum<32>(acc.fy);
-    const double fz = group_sum<32>(acc.fz);
+    const double fx = -group_sum<32>(sx);
+    const double fy = -group_sum<32>(sy);
+    const double fz = -group_sum<32>(sz);
     const double e = group_sum<32>(acc.e);
     const double w = group_sum<32>(acc.w);
     const int nt = group_sum_int<32>(acc.n);

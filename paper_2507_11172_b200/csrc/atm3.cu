@@ -73,7 +73,7 @@ __device__ __forceinline__ A3Smem a3_carve(char *base, int m_rt) {
 }
 
 struct A3Acc {
-    double e, w;     // f_i is not accumulated: f_i = -(f_j + f_k) per triplet
+    double e, w;     // w: per-triplet sum only where phase 3 cannot recover it
     int n;
     bool bad;
     int owned_i;     // decomposed runs: the base particle is owned by this rank
@@ -105,7 +105,10 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 //   E   = s^-5/2 (s + 3/8 p)
 //   E_a = 3/8 s^-5/2 (S - 2uv) - bc (3/2 s^-5/2 + 15/16 p s^-7/2), b/c alike.
 // d_ij (ij, ijz), d_ik (ik, ikz), d_jk = x_j - x_k (jk*).
-template <bool kOwned>
+// kSumVirial: accumulate the virial per triplet (decomposed runs, or d_jk
+// not equal to d_ik - d_ij: box under four cutoffs); otherwise phase 3
+// recovers it from the slot sums.
+template <bool kOwned, bool kSumVirial>
 __device__ __forceinline__ void a3_core(const A3Smem &sm, int s, int t, double a, double b,
                                         double c, double2 ij, double ijz, double2 ik, double ikz,
                                         double jkx, double jky, double jkz, A3Acc &acc,
@@ -134,7 +137,7 @@ __device__ __forceinline__ void a3_core(const A3Smem &sm, int s, int t, double a
         acc.w = fma(share, fma(ea, a, fma(eb, b, ec * c)), acc.w);
     } else {
         acc.e = fma(s52, fma(0.375, p, sp), acc.e);
-        acc.w = fma(ea, a, fma(eb, b, fma(ec, c, acc.w)));
+        if (kSumVirial) acc.w = fma(ea, a, fma(eb, b, fma(ec, c, acc.w)));
     }
     acc.n += 1;
     fj[0] = fma(ea, ij.x, -ec * jkx);
@@ -211,7 +214,7 @@ __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int 
     in = in && !bad;
     double fj[3], fk[3];
     if (in)
-        a3_core<kOwned>(sm, s, t, sm.r2[s], sm.r2[t], c, ij, ijz, ik, ikz, jkx, jky, jkz, acc,
+        a3_core<kOwned, kOwned || kExactImage>(sm, s, t, sm.r2[s], sm.r2[t], c, ij, ijz, ik, ikz, jkx, jky, jkz, acc,
                         fj, fk);
     __syncwarp();
     if (in) a3_add(sm.axy, sm.az, s, fj);
@@ -364,7 +367,12 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars.  Per
     // triplet f_i + f_j + f_k = 0, so the base's own force is minus the sum
     // of everything its triplets gave the slots (fixed lane order and tree)
-    double sx = 0.0, sy = 0.0, sz = 0.0;
+    // Likewise the virial: per triplet x_i.f_i + x_j.f_j + x_k.f_k =
+    // -(d_ij.f_j + d_ik.f_k) = -2(E_a a + E_b b + E_c c), so the base's sum is
+    // sum_s d_is . (slot sum s) in the units of acc.w (decomposed runs weight
+    // each triplet by its owned share, and under four cutoffs d_jk is its own
+    // image: both keep the per-triplet sum)
+    double sx = 0.0, sy = 0.0, sz = 0.0, sw = 0.0;
     for (int sl = lane; sl < m; sl += 32) {
         const int k = sm.kidx[sl] & kKidxMask;
         const double2 xy = sm.axy[sl];
@@ -376,12 +384,16 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
         sx += xy.x;
         sy += xy.y;
         sz += z;
+        if (!kOwned && !kExactImage) {
+            const double2 d = sm.dxy[sl];
+            sw = fma(d.x, xy.x, fma(d.y, xy.y, fma(sm.dz[sl], z, sw)));
+        }
     }
     const double fx = -group_sum<32>(sx);
     const double fy = -group_sum<32>(sy);
     const double fz = -group_sum<32>(sz);
     const double e = group_sum<32>(acc.e);
-    const double w = group_sum<32>(acc.w);
+    const double w = group_sum<32>(kOwned || kExactImage ? acc.w : sw);
     const int nt = group_sum_int<32>(acc.n);
     const bool bad = __any_sync(0xffffffffu, acc.bad);
     if (lane == 0) {

@@ -170,11 +170,13 @@ __device__ __forceinline__ void a3_add(double2 *axy, double *az, int slot, const
 //
 // a3_pair is one window step for one lane: the pair (s, t) (live), its
 // acceptance, the ATM kernel (a3_core) and the two accumulator sub-steps.
-template <bool kExactImage, bool kOwned>
+// kJReg (m < 32: the lane's first slot is always s = lane): f_j goes to the
+// lane's register accumulator aj instead of the shared slot.
+template <bool kExactImage, bool kOwned, bool kJReg>
 __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int t,
                                         const rb_grid &g, const int32_t *__restrict__ row,
                                         const double *__restrict__ pr, double rc2, double rc2_lo,
-                                        double rc2_hi, A3Acc &acc) {
+                                        double rc2_hi, A3Acc &acc, double aj[3]) {
     if (!live) s = t = 0;  // every lane runs the same code; dead lanes accept nothing
     const double2 ij = sm.dxy[s], ik = sm.dxy[t];
     const double ijz = sm.dz[s], ikz = sm.dz[t];
@@ -216,8 +218,16 @@ __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int 
     if (in)
         a3_core<kOwned, kOwned || kExactImage>(sm, s, t, sm.r2[s], sm.r2[t], c, ij, ijz, ik, ikz, jkx, jky, jkz, acc,
                         fj, fk);
-    __syncwarp();
-    if (in) a3_add(sm.axy, sm.az, s, fj);
+    if (kJReg) {
+        if (in) {
+            aj[0] += fj[0];
+            aj[1] += fj[1];
+            aj[2] += fj[2];
+        }
+    } else {
+        __syncwarp();
+        if (in) a3_add(sm.axy, sm.az, s, fj);
+    }
     __syncwarp();
     if (in) a3_add(sm.axy, sm.az, t, fk);
 }
@@ -227,14 +237,15 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, co
                                            const int32_t *__restrict__ row,
                                            const double *__restrict__ pr, double rc2,
                                            double rc2_lo, double rc2_hi, A3Acc &acc) {
+    double aj[3] = {0.0, 0.0, 0.0};
     if (m >= 32) {
         const int pairs = m * (m - 1) / 2;
         int s = lane, d = 1;  // pair f = f0 + lane is (round d, slot s)
         for (int f0 = 0; f0 < pairs; f0 += 32) {
             int t = s + d;
             if (t >= m) t -= m;
-            a3_pair<kExactImage, kOwned>(sm, f0 + lane < pairs, s, t, g, row, pr, rc2, rc2_lo,
-                                         rc2_hi, acc);
+            a3_pair<kExactImage, kOwned, false>(sm, f0 + lane < pairs, s, t, g, row, pr, rc2,
+                                                rc2_lo, rc2_hi, acc, aj);
             s += 32;
             if (s >= m) {
                 s -= m;
@@ -246,9 +257,11 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, co
             const int lim = 2 * d == m ? d : m;  // even m: the last round is half
             int t = lane + d;
             if (t >= m) t -= m;
-            a3_pair<kExactImage, kOwned>(sm, lane < lim, lane, t, g, row, pr, rc2, rc2_lo,
-                                         rc2_hi, acc);
+            a3_pair<kExactImage, kOwned, true>(sm, lane < lim, lane, t, g, row, pr, rc2, rc2_lo,
+                                               rc2_hi, acc, aj);
         }
+        __syncwarp();
+        if (lane < m) a3_add(sm.axy, sm.az, lane, aj);  // the j-role sums of slot `lane`
     }
     __syncwarp();
 }

@@ -176,10 +176,14 @@ template <bool kExactImage, bool kOwned, bool kJReg>
 __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int t,
                                         const rb_grid &g, const int32_t *__restrict__ row,
                                         const double *__restrict__ pr, double rc2, double rc2_lo,
-                                        double rc2_hi, A3Acc &acc, double aj[3]) {
+                                        double rc2_hi, A3Acc &acc, double aj[3],
+                                        const double own[4]) {
     if (!live) s = t = 0;  // every lane runs the same code; dead lanes accept nothing
-    const double2 ij = sm.dxy[s], ik = sm.dxy[t];
-    const double ijz = sm.dz[s], ikz = sm.dz[t];
+    // kJReg: slot s is the lane's own, preloaded in `own` (d_ij, r_ij^2)
+    const double2 ij = kJReg ? make_double2(own[0], own[1]) : sm.dxy[s];
+    const double ijz = kJReg ? own[2] : sm.dz[s];
+    const double2 ik = sm.dxy[t];
+    const double ikz = sm.dz[t];
     double jkx, jky, jkz, c;
     bool in;
     if (kExactImage) {
@@ -211,12 +215,14 @@ __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int 
     // and skipped; r_jk here, r_ij / r_ik only if phase 0 saw one (uniform)
     bool bad = in && c < RB_MIN_DISTANCE_SQ;
     if (acc.slot_bad)
-        bad = bad || (in && (sm.r2[s] < RB_MIN_DISTANCE_SQ || sm.r2[t] < RB_MIN_DISTANCE_SQ));
+        bad = bad || (in && ((kJReg ? own[3] : sm.r2[s]) < RB_MIN_DISTANCE_SQ ||
+                             sm.r2[t] < RB_MIN_DISTANCE_SQ));
     acc.bad = acc.bad || bad;
     in = in && !bad;
     double fj[3], fk[3];
     if (in)
-        a3_core<kOwned, kOwned || kExactImage>(sm, s, t, sm.r2[s], sm.r2[t], c, ij, ijz, ik, ikz, jkx, jky, jkz, acc,
+        a3_core<kOwned, kOwned || kExactImage>(sm, s, t, kJReg ? own[3] : sm.r2[s], sm.r2[t], c,
+                                               ij, ijz, ik, ikz, jkx, jky, jkz, acc,
                         fj, fk);
     if (kJReg) {
         if (in) {
@@ -237,7 +243,7 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, co
                                            const int32_t *__restrict__ row,
                                            const double *__restrict__ pr, double rc2,
                                            double rc2_lo, double rc2_hi, A3Acc &acc) {
-    double aj[3] = {0.0, 0.0, 0.0};
+    double aj[3] = {0.0, 0.0, 0.0}, own[4] = {0.0, 0.0, 0.0, 0.0};
     if (m >= 32) {
         const int pairs = m * (m - 1) / 2;
         int s = lane, d = 1;  // pair f = f0 + lane is (round d, slot s)
@@ -245,7 +251,7 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, co
             int t = s + d;
             if (t >= m) t -= m;
             a3_pair<kExactImage, kOwned, false>(sm, f0 + lane < pairs, s, t, g, row, pr, rc2,
-                                                rc2_lo, rc2_hi, acc, aj);
+                                                rc2_lo, rc2_hi, acc, aj, own);
             s += 32;
             if (s >= m) {
                 s -= m;
@@ -253,12 +259,19 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, co
             }
         }
     } else {
+        if (lane < m) {
+            const double2 d = sm.dxy[lane];
+            own[0] = d.x;
+            own[1] = d.y;
+            own[2] = sm.dz[lane];
+            own[3] = sm.r2[lane];
+        }
         for (int d = 1; 2 * d <= m; d++) {
             const int lim = 2 * d == m ? d : m;  // even m: the last round is half
             int t = lane + d;
             if (t >= m) t -= m;
             a3_pair<kExactImage, kOwned, true>(sm, lane < lim, lane, t, g, row, pr, rc2, rc2_lo,
-                                               rc2_hi, acc, aj);
+                                               rc2_hi, acc, aj, own);
         }
         __syncwarp();
         if (lane < m) a3_add(sm.axy, sm.az, lane, aj);  // the j-role sums of slot `lane`

@@ -202,6 +202,17 @@ RB_API int rb_direct_triplets(int64_t n, const double *pos, double nu, double *f
                               double *energy_virial, void *scratch, size_t scratch_bytes,
                               unsigned long long *status, int64_t tag, void *stream);
 
+/* ---- halo exchange of the domain-decomposed loop ------
+ * rb_halo_pack: buf[i] = pos[idx[i]] (24-byte records), the message of one
+ * send list.  rb_halo_unpack: pos[first + i] = buf[i] for a received
+ * message of n ghosts and, with pos_r != NULL, the rank-ordered copy
+ * pos_r[rank_of[first + i]].  The messages themselves travel over NCCL
+ * (torch.distributed point-to-point) between the two calls. */
+RB_API int rb_halo_pack(int64_t n, const int32_t *idx, const double *pos, double *buf,
+                        void *stream);
+RB_API int rb_halo_unpack(int64_t n, const double *buf, int64_t first, double *pos,
+                          const int32_t *rank_of, double *pos_r, void *stream);
+
 /* ---- deterministic reductions (fixed partition + fixed tree) ---------- */
 RB_API size_t rb_reduce_scratch_bytes(int64_t n);
 /* out[0] = sum(in[0..n)) */

@@ -88,14 +88,39 @@ class GpuBackend:
         return self.f_local[: self.n_own].clone(), eng.scalars[3:5].clone()
 
     # ---- fused per-step primitives (the loop's fast path on the GPU) ----
-    def bind(self, st) -> None:
+    def bind(self, st, plan) -> None:
         """After a rebuild: the owned state moves into the device buffers and
-        `st` becomes views of them (positions are eng.pos[:n_own])."""
+        `st` becomes views of them (positions are eng.pos[:n_own]); the
+        ghost send lists become int32 device arrays for rb_halo_pack."""
         n = self.n_own
         for name, buf in (("v", self.v), ("f2", self.f2), ("f3", self.f3)):
             buf[:n] = getattr(st, name)
             setattr(st, name, buf[:n])
         st.x = self.eng.pos[:n]
+        i32 = self.torch.int32
+        self._lists = [(d, tm.to(i32), tp.to(i32), n_fp, n_fm)
+                       for d, tm, tp, n_fp, n_fm in plan.stages]
+
+    def refresh_halo(self, dec, ex) -> None:
+        """Per step between rebuilds: the owners' new positions into the ghost
+        rows (and their rank-order copy), stage by stage (x -> y -> z): pack
+        kernel, NCCL point-to-point, unpack kernel."""
+        eng, L, ptr, torch = self.eng, self.eng.L, self._lib.ptr, self.torch
+        at = self.n_own
+        for d, tm, tp, n_fp, n_fm in self._lists:
+            send = []
+            for idx in (tm, tp):
+                buf = torch.empty((idx.shape[0], 3), dtype=torch.float64, device=self.device)
+                self._lib.check(L.rb_halo_pack(idx.shape[0], ptr(idx), ptr(eng.pos), ptr(buf),
+                                               eng.stream), "rb_halo_pack")
+                send.append(buf)
+            from_plus, from_minus = ex.exchange_fixed(send[0], send[1], dec.neighbor(d, -1),
+                                                      dec.neighbor(d, +1), n_fp, n_fm)
+            for buf, cnt in ((from_plus, n_fp), (from_minus, n_fm)):
+                self._lib.check(L.rb_halo_unpack(cnt, ptr(buf.contiguous()), at, ptr(eng.pos),
+                                                 ptr(eng.rank_of), ptr(eng.pos_r), eng.stream),
+                                "rb_halo_unpack")
+                at += cnt
 
     def local_view(self):
         return self.eng.pos[: self.n_local]
@@ -113,12 +138,6 @@ class GpuBackend:
                               self._lib.RB_TAG_FROM_DEVICE, 1, 0, eng.stream)
         self._lib.check(st, "rb_respa_drift")
         return eng.rebuild_flag[0] == eng.status[1]
-
-    def ghosts_moved(self) -> None:
-        """Ghost rows of eng.pos were refreshed in place: their rank-order copy."""
-        eng, n, n_own = self.eng, self.n_local, self.n_own
-        if n > n_own:
-            eng.pos_r[:n][eng.rank_of[n_own:n].long()] = eng.pos[n_own:n]
 
     def pair_into_new(self, scalars: bool):
         eng = self.eng
@@ -224,7 +243,7 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
         local, plan = build_ghosts(dec, ex, st.x)
         backend.set_local(local, plan.n_owned, window, rebuild=True)
         if fast:
-            backend.bind(st)
+            backend.bind(st, plan)
             return backend.local_view(), plan
         st.x_ref = st.x.clone()
         return local, plan
@@ -297,8 +316,7 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
             if any_flag(moved if skin > 0.0 else True):
                 local, plan = rebuild()
             else:
-                refresh_ghosts(dec, ex, plan, local)
-                backend.ghosts_moved()
+                backend.refresh_halo(dec, ex)
             e2w2 = backend.pair_into_new(sample)
             if end_of_cycle:
                 e3w3 = backend.triplet_into_f3(sample)

@@ -18,11 +18,11 @@ namespace rb {
 #ifndef RB_LJ_GROUP
 #define RB_LJ_GROUP 8
 #endif
-#ifndef RB_LJ_UNROLL
-#define RB_LJ_UNROLL 2
+#ifndef RB_LJ_ROW_REGS
+#define RB_LJ_ROW_REGS 10
 #endif
 constexpr int kLjGroup = RB_LJ_GROUP;   // lanes per particle
-constexpr int kLjUnroll = RB_LJ_UNROLL; // row entries in flight per lane
+constexpr int kLjRowRegs = RB_LJ_ROW_REGS;  // row indices a lane holds at once
 constexpr int kLjThreads = 256;
 // 1/x: the hardware fp64 seed (MUFU.RCP64H) and one third-order correction
 // y (1 + e + e^2), e = 1 - x y (x is a squared distance, a normal double;
@@ -55,46 +55,47 @@ __global__ void __launch_bounds__(kLjThreads)
         const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
         const int m = row_count[r];
         const int32_t *row = rows + r * (int64_t)capacity;
-        // kLjUnroll entries per lane per batch: their row and position loads
-        // are issued together (the pass is latency-bound); the accumulation
-        // order is still k = sub, sub + G, sub + 2G, ...
-        for (int k0 = sub; k0 < m; k0 += kLjUnroll * kLjGroup) {
-            int j[kLjUnroll];
+        // the pass is latency-bound: every row index of this lane (up to
+        // kLjRowRegs) is loaded first, then the positions two entries at a
+        // time; the accumulation order stays k = sub, sub + G, sub + 2G, ...
+        int jr[kLjRowRegs];
 #pragma unroll
-            for (int u = 0; u < kLjUnroll; u++) {
-                const int k = k0 + u * kLjGroup;
-                j[u] = k < m ? __ldg(row + k) : -1;
+        for (int u = 0; u < kLjRowRegs; u++) {
+            const int k = sub + u * kLjGroup;
+            jr[u] = k < m ? __ldg(row + k) : -1;
+        }
+        auto visit = [&](int q, double px, double py, double pz) {
+            double dx, dy, dz;
+            exact_disp(im, xi, yi, zi, px, py, pz, dx, dy, dz);
+            const double r2 = exact_r2(dx, dy, dz);
+            if (r2 > rc2) return;
+            if (r2 < RB_MIN_DISTANCE_SQ) {
+                bad = true;
+                return;
             }
-            double px[kLjUnroll], py[kLjUnroll], pz[kLjUnroll];
+            const double inv_r2 = lj_rcp(r2);
+            const double x = sigma2 * inv_r2;
+            const double r6 = x * x * x;
+            const double r12 = r6 * r6;
+            const double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
+            fx += scale * dx;
+            fy += scale * dy;
+            fz += scale * dz;
+            e += eps4 * (r12 - r6);
+            w += scale * r2;
+        };
 #pragma unroll
-            for (int u = 0; u < kLjUnroll; u++) {
-                const int q = j[u] < 0 ? 0 : j[u];
-                px[u] = pr[3 * q];
-                py[u] = pr[3 * q + 1];
-                pz[u] = pr[3 * q + 2];
-            }
-#pragma unroll
-            for (int u = 0; u < kLjUnroll; u++) {
-                if (j[u] < 0) break;
-                double dx, dy, dz;
-                exact_disp(im, xi, yi, zi, px[u], py[u], pz[u], dx, dy, dz);
-                const double r2 = exact_r2(dx, dy, dz);
-                if (r2 > rc2) continue;
-                if (r2 < RB_MIN_DISTANCE_SQ) {
-                    bad = true;
-                    continue;
-                }
-                const double inv_r2 = lj_rcp(r2);
-                const double x = sigma2 * inv_r2;
-                const double r6 = x * x * x;
-                const double r12 = r6 * r6;
-                const double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
-                fx += scale * dx;
-                fy += scale * dy;
-                fz += scale * dz;
-                e += eps4 * (r12 - r6);
-                w += scale * r2;
-            }
+        for (int u = 0; u < kLjRowRegs; u += 2) {
+            if (jr[u] < 0) break;
+            const int qa = jr[u], qb = jr[u + 1] < 0 ? jr[u] : jr[u + 1];
+            const double ax = pr[3 * qa], ay = pr[3 * qa + 1], az = pr[3 * qa + 2];
+            const double bx = pr[3 * qb], by = pr[3 * qb + 1], bz = pr[3 * qb + 2];
+            visit(qa, ax, ay, az);
+            if (jr[u + 1] >= 0) visit(qb, bx, by, bz);
+        }
+        for (int k = sub + kLjRowRegs * kLjGroup; k < m; k += kLjGroup) {  // long rows
+            const int q = __ldg(row + k);
+            visit(q, pr[3 * q], pr[3 * q + 1], pr[3 * q + 2]);
         }
     }
     fx = group_sum<kLjGroup>(fx);

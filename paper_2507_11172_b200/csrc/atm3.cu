@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
 // G[p][k]); the row prefix is walked in order by kG lanes, then a fixed xor
 // tree.
 constexpr int kGatherGroup = 8;
+constexpr int kGatherRegs = 6;  // prefix entries per lane loaded at once
 
 __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
                               const int32_t *__restrict__ rows,
@@ -504,8 +505,29 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
         const int m = row_count[p];
         const int32_t *row = rows + p * (int64_t)capacity;
         const double *gp = gbuf + p * (int64_t)capacity * 3;
-        for (int k = sub; k < m; k += kGatherGroup) {
-            if (row[k] >= p) break;  // rows are rank-sorted: the prefix q < p
+        // rows are rank-sorted: the prefix q < p holds the partials.  The
+        // first kGatherRegs entries of the lane are loaded together (index
+        // and partial), then summed in row order; longer prefixes continue
+        int k = sub;
+        bool more = true;
+#pragma unroll
+        for (int u = 0; u < kGatherRegs; u++, k += kGatherGroup) {
+            const bool in = more && k < m && __ldg(row + k) < p;
+            double gx = 0.0, gy = 0.0, gz = 0.0;
+            if (k < m) {  // loads independent of the row test: issued together
+                gx = gp[3 * k];
+                gy = gp[3 * k + 1];
+                gz = gp[3 * k + 2];
+            }
+            if (in) {
+                fx += gx;
+                fy += gy;
+                fz += gz;
+            }
+            more = in;
+        }
+        for (; more && k < m; k += kGatherGroup) {
+            if (row[k] >= p) break;
             fx += gp[3 * k];
             fy += gp[3 * k + 1];
             fz += gp[3 * k + 2];

@@ -202,6 +202,16 @@ RB_API int rb_direct_triplets(int64_t n, const double *pos, double nu, double *f
                               double *energy_virial, void *scratch, size_t scratch_bytes,
                               unsigned long long *status, int64_t tag, void *stream);
 
+/* ---- radial distribution function: replaces _distance_histogram
+ * (observables.py:143-177).  counts[bins] (int64, device) += ordered
+ * minimum-image pair counts with r^2 < r2_max in bin
+ * trunc(sqrt(r^2) * inv_width) (clamped); pass r2_max = r_max * r_max and
+ * inv_width = bins / r_max computed as the reference does.  Bit-exact
+ * integer counts. */
+RB_API int rb_distance_histogram(int64_t n, const double *pos, const double *box3_host,
+                                 double r2_max, double inv_width, int32_t bins, int64_t *counts,
+                                 void *stream);
+
 /* ---- halo exchange of the domain-decomposed loop ------
  * rb_halo_pack: buf[i] = pos[idx[i]] (24-byte records), the message of one
  * send list.  rb_halo_unpack: pos[first + i] = buf[i] for a received

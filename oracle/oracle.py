@@ -83,6 +83,7 @@ def lib():
         L.orc_brute_triplets.restype = I64
         L.orc_direct_pairs.argtypes = [I64, P, D, D, I64, P, P, P, P]
         L.orc_direct_triplets.argtypes = [I64, P, D, I64, P, P, P, P]
+        L.orc_distance_histogram.argtypes = [I64, P, P, D, I64, P]
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
         L.orc_get_max_threads.restype = ctypes.c_int
         _lib = L
@@ -351,6 +352,16 @@ def brute_force_triplets(system, ff, cutoff=None):
 # ---------------------------------------------------------------------------
 # container + integrator restatement
 # ---------------------------------------------------------------------------
+
+
+def distance_histogram(positions, box, r_max, bins) -> np.ndarray:
+    """respamd/observables.py:143-177 -> int64 counts (2 per unordered pair)."""
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    box = np.ascontiguousarray(box, dtype=np.float64)
+    counts = np.zeros(int(bins), np.int64)
+    lib().orc_distance_histogram(pos.shape[0], _p(pos), _p(box), float(r_max), int(bins),
+                                 _p(counts))
+    return counts
 
 
 DIRECT_SUM_CHUNKS = 16  # respamd/containers.py:36

@@ -18,6 +18,7 @@ records its outputs on seeded inputs:
                           scalars, the visit count and forces of a fixed
                           particle subset
 * respa_<name>.npz    -- respa_run trajectories (integrators.py:96-173)
+* rdf.npz             -- rdf / _distance_histogram (observables.py:143-214)
 * direct.npz          -- DirectSum pairs/triplets (containers.py:852-908) on
                           non-periodic systems (the reference test's four
                           particles and random n = 70 / 150 / 300)
@@ -263,7 +264,35 @@ def gen_direct():
                         nu=ff.nu, **out)
 
 
+def gen_rdf():
+    """Radial distribution function (observables.py:143-214): the raw ordered
+    pair counts and the g(r) curve."""
+    from respamd import observables as ro
+
+    out = {}
+    s1 = systems.CONFIGS["cfg1"].system()
+    rng = np.random.default_rng(TEST_SEED + 41)
+    pos = random_positions(rng, 300, (8.0,) * 3, True)
+    cases = [("cfg1", [s1.positions], s1.box, None, 200),
+             ("rand300", [pos, np.mod(pos + 0.37, 8.0)], np.full(3, 8.0), 3.0, 50)]
+    for name, frames, box, r_max, bins in cases:
+        snaps = [ref_system(f, box, True) for f in frames]
+        curve = ro.rdf(snaps, r_max=r_max, bins=bins)
+        rm_ = float(box.min()) / 2.0 if r_max is None else r_max
+        counts = sum(ro._distance_histogram(f, np.asarray(box, dtype=np.float64), rm_, bins)
+                     for f in frames)
+        for k, v in dict(box=np.asarray(box), r_max=rm_, bins=bins, curve=curve,
+                         counts=counts).items():
+            out[f"{name}__{k}"] = v
+        for i, f in enumerate(frames):
+            out[f"{name}__frame{i}"] = f
+        out[f"{name}__frames"] = len(frames)
+        print(f"rdf {name}: frames {len(frames)} pairs {int(counts.sum())}")
+    np.savez_compressed(os.path.join(HERE, "rdf.npz"), names=np.array([c[0] for c in cases]),
+                        **out)
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["potentials", "small", "large", "respa", "direct"]
+    what = sys.argv[1:] or ["potentials", "small", "large", "respa", "direct", "rdf"]
     for w in what:
         globals()[f"gen_{w}"]()

@@ -148,3 +148,14 @@ def test_direct_sum_rejects_periodic(oracle):
                                            (5.0, 5.0, 5.0), True)
     with pytest.raises(oracle.OracleValidationError):
         oracle.direct_sum_pairs(s, oracle.OracleForceField())
+
+
+def test_distance_histogram_bit_exact(oracle):
+    """RDF pair counts (observables.py:143-177) vs the reference."""
+    g = load_golden("rdf.npz")
+    for name in [str(n) for n in g["names"]]:
+        frames = int(g[f"{name}__frames"])
+        counts = sum(oracle.distance_histogram(g[f"{name}__frame{i}"], g[f"{name}__box"],
+                                               float(g[f"{name}__r_max"]), int(g[f"{name}__bins"]))
+                     for i in range(frames))
+        assert np.array_equal(counts, g[f"{name}__counts"])

@@ -366,8 +366,14 @@ LAST_RUN = [None]  # the DeviceRespa of the most recent respa_run (diagnostics)
 
 def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: Optional[int] = None,
               hooks=(), use_graph: bool = True, capacity: Optional[int] = None,
-              skin: Optional[float] = None) -> RunTrace:
-    """Integrate in place with the r-RESPA loop on the GPU (integrators.py:96-173)."""
+              skin: Optional[float] = None, device_hooks=()) -> RunTrace:
+    """Integrate in place with the r-RESPA loop on the GPU (integrators.py:96-173).
+
+    ``hooks`` are the reference's host hooks (iteration, system view,
+    container) at every sample point -- they force a download per period.
+    ``device_hooks`` are called as hook(iteration, positions) at the same
+    points with the device positions (particle order) and must only enqueue
+    device work (e.g. accumulate an RDF histogram): no synchronisation."""
     if not isinstance(container, (CudaLinkedCells, CudaDirectSum)):
         raise TypeError("respa_run needs a CudaLinkedCells or CudaDirectSum container "
                         "(GPU only, no host fallback)")
@@ -390,7 +396,7 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
         run.slots = slots
         LAST_RUN[0] = run
         try:
-            return _drive(run, hooks)
+            return _drive(run, hooks, tuple(device_hooks))
         except CapacityError:
             capacity = min(4096, _round_up(int(run.capacity * 1.5) + 32, 32))
             slots = capacity
@@ -399,11 +405,17 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
     raise CapacityError("neighbour rows kept overflowing")
 
 
-def _drive(run: DeviceRespa, hooks) -> RunTrace:
+def _drive(run: DeviceRespa, hooks, device_hooks=()) -> RunTrace:
     sysm, n_periods = run.system, run.schedule.num_iterations // run.interval
     trace = RunTrace()
     run.marks = [("drive", time.perf_counter())]
     run.start()
+
+    def on_device(k):  # after sample point k (iteration k * interval)
+        for hook in device_hooks:
+            hook(k * run.interval, run.x)
+
+    on_device(0)
     if hooks:
         # hooks see the host system at every sample point: sync per period
         _check(run, trace, upto=1)
@@ -415,6 +427,7 @@ def _drive(run: DeviceRespa, hooks) -> RunTrace:
             hook(0, view, run.container)
         for k in range(n_periods):
             run.run_periods(k, 1)
+            on_device(k + 1)
             _check(run, trace, upto=k + 2)
             run.download()
             run.update_container()
@@ -432,15 +445,23 @@ def _drive(run: DeviceRespa, hooks) -> RunTrace:
     mark(("started", time.perf_counter()))
     if n_periods > 0 and run.use_graph:
         run.run_periods(0, 1)  # warm-up, also the first period of the run
+        on_device(1)
         mark(("eager period", time.perf_counter()))
         run.capture()
         mark(("captured", time.perf_counter()))
         # the capture recorded but did not execute; rewind nothing: replay the rest
         run.eng.set_step(run.interval)
-        run.run_periods(1, n_periods - 1)
+        if device_hooks:
+            for k in range(1, n_periods):
+                run.run_periods(k, 1)
+                on_device(k + 1)
+        else:
+            run.run_periods(1, n_periods - 1)
         mark(("replays enqueued", time.perf_counter()))
     else:
-        run.run_periods(0, n_periods)
+        for k in range(n_periods):
+            run.run_periods(k, 1)
+            on_device(k + 1)
     for i in range(n_periods * run.interval, run.schedule.num_iterations):
         run._step(i)  # iterations past the last sample point
     run.finish_scalars()
@@ -483,5 +504,71 @@ def verlet_run(system, ff, container, dt: float, num_iterations: int,
     return respa_run(system, ff, container, schedule, sample_interval, hooks)
 
 
-__all__ = ["IntegrationBlowUp", "RespaSchedule", "RunTrace", "respa_run", "verlet_run",
-           "MinimumSeparationError"]
+@dataclass
+class EquilibrationReport:
+    """Outcome of an equilibration window (integrators.py:192-201)."""
+
+    system: object
+    rescale_factors: list
+    tail_temperature: float
+    target_temperature: float
+    converged: bool
+
+
+def measured_temperature(system) -> float:
+    """Equipartition estimate T = (2/3) K / N (integrators.py:204-206)."""
+    return 2.0 * system.kinetic_energy() / (3.0 * system.positions.shape[0])
+
+
+def equilibrate(system, ff, container, dt: float, steps: int, target_temperature: float,
+                rescale_interval: int = 10) -> EquilibrationReport:
+    """Velocity-rescaling Verlet towards the target temperature
+    (integrators.py:209-252), device-resident: the state stays in HBM, each
+    window of `rescale_interval` steps is a replayed CUDA graph, and only the
+    window's kinetic energy comes back to the host (one synchronisation per
+    window) for the rescale factor sqrt(T_target / T_measured)."""
+    if target_temperature <= 0:
+        raise ValidationError("target temperature must be > 0")
+    if steps < 0:
+        raise ValidationError("steps must be >= 0")
+    if not isinstance(container, (CudaLinkedCells, CudaDirectSum)):
+        raise TypeError("equilibrate needs a CudaLinkedCells or CudaDirectSum container")
+    factors, temperatures = [], []
+    if steps > 0:
+        interval = int(rescale_interval)
+        run = DeviceRespa(system, ff, container, RespaSchedule(dt, 1, steps), interval)
+        run.start()
+        n, m = system.positions.shape[0], float(system.mass)
+        eng = run.eng
+        done = 0
+        while done < steps:
+            chunk = min(interval, steps - done)
+            if chunk == interval and run.use_graph and run.graph is not None:
+                run.graph.replay()
+            else:
+                for i in range(done, done + chunk):
+                    run._step(i)
+                if chunk == interval and run.use_graph and run.graph is None:
+                    run.capture()  # the windows repeat (s = 1): one graph serves all
+            done += chunk
+            _check(run, RunTrace(), upto=(done + interval - 1) // interval + 1)
+            eng.sum_f64(run.v, 0, square=True, n=3 * n)
+            kinetic = 0.5 * m * float(eng.scalars[0].item())
+            t_now = 2.0 * kinetic / (3.0 * n)
+            temperatures.append(t_now)
+            if t_now > 0:
+                factor = math.sqrt(target_temperature / t_now)
+                run.v.mul_(factor)
+                factors.append(factor)
+        run.finish_scalars()
+        run.download()
+        run.update_container()
+    tail = temperatures[-max(1, len(temperatures) // 10):] if temperatures else []
+    tail_t = float(np.mean(tail)) if tail else measured_temperature(system)
+    converged = steps == 0 or abs(tail_t - target_temperature) <= 0.02 * target_temperature
+    return EquilibrationReport(system=system, rescale_factors=factors, tail_temperature=tail_t,
+                               target_temperature=target_temperature, converged=converged)
+
+
+__all__ = ["EquilibrationReport", "IntegrationBlowUp", "RespaSchedule", "RunTrace", "equilibrate",
+           "measured_temperature", "respa_run", "verlet_run", "MinimumSeparationError"]

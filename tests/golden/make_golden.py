@@ -19,6 +19,7 @@ records its outputs on seeded inputs:
                           particle subset
 * respa_<name>.npz    -- respa_run trajectories (integrators.py:96-173)
 * rdf.npz             -- rdf / _distance_histogram (observables.py:143-214)
+* lattice.npz         -- build_lattice_system (model.py:212-252)
 * direct.npz          -- DirectSum pairs/triplets (containers.py:852-908) on
                           non-periodic systems (the reference test's four
                           particles and random n = 70 / 150 / 300)
@@ -292,7 +293,24 @@ def gen_rdf():
                         **out)
 
 
+LATTICES = [(1000, (11.0, 11.0, 11.0)), (37, (5.0, 6.0, 7.0)), (500, (10.0, 10.0, 40.0)),
+            (8, (3.0, 3.0, 3.0))]
+
+
+def gen_lattice():
+    """build_lattice_system (model.py:212-252) for a few counts and boxes."""
+    out = {}
+    for k, (n, box) in enumerate(LATTICES):
+        cfg = rm.ScenarioConfig(particle_count=n, box=np.array(box), dt=0.001, iterations=10,
+                                container="linked_cells", periodic=True)
+        out[f"n{k}"] = n
+        out[f"box{k}"] = np.array(box)
+        out[f"pos{k}"] = rm.build_lattice_system(cfg).positions
+    np.savez_compressed(os.path.join(HERE, "lattice.npz"), cases=len(LATTICES), **out)
+    print(f"lattice: {len(LATTICES)} cases")
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["potentials", "small", "large", "respa", "direct", "rdf"]
+    what = sys.argv[1:] or ["potentials", "small", "large", "respa", "direct", "rdf", "lattice"]
     for w in what:
         globals()[f"gen_{w}"]()

@@ -216,3 +216,17 @@ def test_direct_sum_rejects_periodic_systems():
     with pytest.raises(pkg.ValidationError):
         pkg.direct_sum_triplets(s, ff)
     assert pkg.make_container("direct_sum").name == "cuda_direct_sum"
+
+
+def test_lattice_system_matches_reference():
+    """build_lattice_system restates model.py:212-252 (fixture made by it)."""
+    from helpers import load_golden
+
+    import paper_2507_11172_b200 as pkg
+    from paper_2507_11172_b200.model import build_lattice_system
+
+    g = load_golden("lattice.npz")
+    for k in range(int(g["cases"])):
+        cfg = pkg.ScenarioConfig(particle_count=int(g[f"n{k}"]), box=g[f"box{k}"], dt=0.001,
+                                 iterations=10, container="cuda_linked_cells", periodic=True)
+        assert np.array_equal(build_lattice_system(cfg).positions, g[f"pos{k}"])

@@ -128,8 +128,12 @@ def pos_sha(pos):
 
 def gen_large():
     rows = [("cfg1", "cfg1", 2.5), ("cfg2", "cfg2", 2.5), ("cfg3_rc2.0", "cfg3", 2.0),
-            ("cfg3_rc2.5", "cfg3", 2.5), ("cfg3_rc3.0", "cfg3", 3.0), ("cfg4", "cfg4", 2.5)]
+            ("cfg3_rc2.5", "cfg3", 2.5), ("cfg3_rc3.0", "cfg3", 3.0), ("cfg4", "cfg4", 2.5),
+            ("cfg5", "cfg5", 2.5)]
+    only = os.environ.get("GOLDEN_LARGE")  # e.g. GOLDEN_LARGE=cfg5 regenerates one row
     for name, cfg_name, rc3 in rows:
+        if only and name not in only.split(","):
+            continue
         cfg = systems.CONFIGS[cfg_name]
         s = cfg.system()
         sysm = ref_system(s.positions, s.box, True)

@@ -253,7 +253,7 @@ def test_deterministic_passes(pkg):
 # BASELINE configs at step 0 (reference scalars / counts / force subsets)
 # --------------------------------------------------------------------------
 LARGE = ["large_cfg1.npz", "large_cfg2.npz", "large_cfg3_rc2.0.npz", "large_cfg3_rc2.5.npz",
-         "large_cfg3_rc3.0.npz", "large_cfg4.npz"]
+         "large_cfg3_rc3.0.npz", "large_cfg4.npz", "large_cfg5.npz"]
 
 
 @pytest.mark.parametrize("name", LARGE)

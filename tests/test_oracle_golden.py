@@ -68,6 +68,19 @@ def test_brute_force_bit_exact(oracle, name):
     assert count == int(g["brute_count"]) == int(g["visits"]) // 3
 
 
+def test_slab_generator_pinned():
+    """cfg5 (liquid slab + vapour) is pinned by sha256; its
+    scalars are checked on the GPU (test_baseline_configs_step0)."""
+    import hashlib
+
+    from paper_2507_11172_b200 import systems
+
+    g = load_golden("large_cfg5.npz")
+    s = systems.CONFIGS["cfg5"].system()
+    assert s.n == 500_000
+    assert hashlib.sha256(s.positions.tobytes()).hexdigest() == str(g["sha"])
+
+
 def test_generator_and_large_scalars(oracle):
     """cfg1 and cfg2 at step 0: the generator is pinned by sha256 and the
     oracle's scalars / visit counts / force subsets equal the reference's."""

@@ -565,12 +565,16 @@ extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
 }
 
 namespace rb {
-// Slots of the main launch.  S+(r) of most bases is about half a row; only
-// bases whose neighbours mostly follow them in rank order (cells next to the
-// periodic wrap of the cell order) approach a full row.  Sizing every warp's
-// shared memory for the longest S+ costs occupancy, so the main launch takes
-// about half the slots and lists the few longer bases for a second launch.
+// Slots of the main launch.  A slot costs 60 bytes of shared memory: up to
+// 96 slots a warp holds the longest S+(i) outright and one launch does all
+// (64 and 96 have compile-time layouts).  Larger counts take about half the
+// slots in the main launch and
+// list the few longer bases for a second, full-slot launch: S+(i) of most
+// bases is about half a row, only bases whose neighbours mostly follow them
+// in rank order (cells next to the periodic wrap of the cell order) approach
+// a full row.
 static int a3_fast_slots(int slot_capacity) {
+    if (slot_capacity <= 96) return slot_capacity;  // measured: one launch is faster here
     int f = ((slot_capacity * 11 / 20) + 31) / 32 * 32;  // ~0.55 of the full count
     f = f < 64 ? 64 : f;
     return f >= slot_capacity ? slot_capacity : f;

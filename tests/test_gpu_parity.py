@@ -183,20 +183,20 @@ def test_triplet_overflow_launch_matches_oracle(pkg, oracle):
     (full-slot) launch; the forces must not depend on which launch ran."""
     from paper_2507_11172_b200.containers import engine_for
 
-    s = pkg.systems.fcc_system(8, jitter=0.05, seed=9)
-    ff = pkg.ForceField(nu=0.4, cutoff=3.0)
+    s = pkg.systems.fcc_system(9, jitter=0.05, seed=9)  # rows of ~130: 160 slots, split
+    ff = pkg.ForceField(nu=0.4, cutoff=3.4)
     c = pkg.CudaLinkedCells()
     c.triplet_pass(s, ff)
     eng = engine_for(s.positions.shape[0])
-    assert eng.slots > 64
+    assert eng.slots > 128
     import torch
 
     words = eng.atm_scratch.view(torch.int32)  # own, G (doubles), then the overflow list
     listed = int(words[2 * eng.n * 3 * (1 + eng.capacity) + 1].item())  # last pass's count
     assert 0 < listed < eng.n
     os_ = oracle.OracleSystem.from_positions(s.positions, s.box, True)
-    off = oracle.OracleForceField(nu=0.4, cutoff=3.0)
-    rf3, re3, _, count = oracle.brute_force_triplets(os_, off, cutoff=3.0)
+    off = oracle.OracleForceField(nu=0.4, cutoff=3.4)
+    rf3, re3, _, count = oracle.brute_force_triplets(os_, off, cutoff=3.4)
     assert normwise(s.forces_3b, rf3) <= FORCE_TOL
     assert _rel(c.triplet_energy, re3) <= ENERGY_TOL
     assert c.triplet_count == count

@@ -201,6 +201,20 @@ RB_API size_t rb_direct_scratch_bytes(int64_t n);
 RB_API int rb_direct_triplets(int64_t n, const double *pos, double nu, double *forces,
                               double *energy_virial, void *scratch, size_t scratch_bytes,
                               unsigned long long *status, int64_t tag, void *stream);
+/* The share of one rank of a distributed DirectSum: rb_direct_pairs_range
+ * writes forces / energy halves of the particles [i_lo, i_hi) only;
+ * rb_direct_triplets_range evaluates the triplets whose lowest member is in
+ * [i_lo, i_hi) and writes their forces on ALL particles (overwritten) and
+ * their (E3, W3).  Summed over ranks covering [0, n) the parts give the full
+ * pass. */
+RB_API int rb_direct_pairs_range(int64_t n, const double *pos, int64_t i_lo, int64_t i_hi,
+                                 double epsilon, double sigma, double *forces,
+                                 double *energy_part, double *virial_part,
+                                 unsigned long long *status, int64_t tag, void *stream);
+RB_API int rb_direct_triplets_range(int64_t n, const double *pos, int64_t i_lo, int64_t i_hi,
+                                    double nu, double *forces, double *energy_virial,
+                                    void *scratch, size_t scratch_bytes,
+                                    unsigned long long *status, int64_t tag, void *stream);
 
 /* ---- radial distribution function: replaces _distance_histogram
  * (observables.py:143-177).  counts[bins] (int64, device) += ordered

@@ -92,6 +92,10 @@ SIGNATURES = {
     "rb_distance_histogram": (ctypes.c_int, [_I64, _P, _P, _D, _D, _I32, _P, _P]),
     "rb_halo_pack": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
     "rb_halo_unpack": (ctypes.c_int, [_I64, _P, _I64, _P, _P, _P, _P]),
+    "rb_direct_pairs_range": (ctypes.c_int, [_I64, _P, _I64, _I64, _D, _D, _P, _P, _P, _P, _I64,
+                                             _P]),
+    "rb_direct_triplets_range": (ctypes.c_int, [_I64, _P, _I64, _I64, _D, _P, _P, _P, _SZ, _P,
+                                                _I64, _P]),
     "rb_sample_scratch_bytes": (ctypes.c_size_t, [_I64]),
     "rb_sample": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _SZ, _P]),
     "rb_rebuild_cond_create": (ctypes.c_int, [_P, _P]),

@@ -31,15 +31,17 @@ constexpr int kDpThreads = 128;  // pair pass: threads per block (4 particles)
 constexpr int kDtMaxN = 8192;    // the per-block force array lives in shared memory
 
 __global__ void __launch_bounds__(kDpThreads)
-    k_direct_pairs(int64_t n, const double *__restrict__ pos, double eps24, double eps4,
-                   double sigma2, double *__restrict__ forces, double *__restrict__ energy,
-                   double *__restrict__ virial, unsigned long long *status, int64_t tag) {
+    k_direct_pairs(int64_t n, int64_t i_lo, int64_t i_hi, const double *__restrict__ pos,
+                   double eps24, double eps4, double sigma2, double *__restrict__ forces,
+                   double *__restrict__ energy, double *__restrict__ virial,
+                   unsigned long long *status, int64_t tag) {
     pdl_enter();
-    // one warp per particle i; lanes stride over j, then a fixed xor tree
+    // one warp per particle i of [i_lo, i_hi); lanes stride over j, then a
+    // fixed xor tree
     const int lane = threadIdx.x & 31;
-    const int64_t i = ((int64_t)blockIdx.x * kDpThreads + threadIdx.x) >> 5;
+    const int64_t i = i_lo + (((int64_t)blockIdx.x * kDpThreads + threadIdx.x) >> 5);
     tag = resolve_tag(tag, status);
-    if (i >= n) return;  // whole warps
+    if (i >= i_hi) return;  // whole warps
     const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
     bool bad = false;
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(1024) k_direct_prep(int64_t n, int T,
 
 template <int kT>
 __global__ void __launch_bounds__(kT)
-    k_direct_triplets(int64_t n, const double *__restrict__ pos,
+    k_direct_triplets(int64_t n, int64_t i_lo, int64_t i_hi, const double *__restrict__ pos,
                       const int64_t *__restrict__ prefix, double *__restrict__ slab,
                       double *__restrict__ part_ew, unsigned long long *status, int64_t tag) {
     pdl_enter();
@@ -127,8 +129,10 @@ __global__ void __launch_bounds__(kT)
     tag = resolve_tag(tag, status);
     for (int64_t q = tid; q < 3 * n; q += kT) fsh[q] = 0.0;
     double *fxs = fsh, *fys = fsh + n, *fzs = fsh + 2 * n;
-    const int64_t total = prefix[n];
-    const int64_t lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
+    // the windows of the bases [i_lo, i_hi), cut into equal block slices
+    const int64_t first = prefix[i_lo], total = prefix[i_hi] - first;
+    const int64_t lo = first + total * blockIdx.x / gridDim.x;
+    const int64_t hi = first + total * (blockIdx.x + 1) / gridDim.x;
     // base of window `lo`: the last i with prefix[i] <= lo
     int64_t i = 0, top = n;
     while (top - i > 1) {
@@ -297,18 +301,27 @@ static int dt_blocks(int64_t n) { return 148 * dt_per_sm(n); }
 
 using namespace rb;
 
+extern "C" int rb_direct_pairs_range(int64_t n, const double *pos, int64_t i_lo, int64_t i_hi,
+                                     double epsilon, double sigma, double *forces,
+                                     double *energy_part, double *virial_part,
+                                     unsigned long long *status, int64_t tag, void *stream) {
+    if (n < 0 || i_lo < 0 || i_hi > n || i_lo > i_hi ||
+        (n > 0 && (!pos || !forces || !energy_part || !virial_part)))
+        return RB_ERR_ARGUMENT;
+    if (i_hi == i_lo) return RB_OK;
+    const int64_t threads = 32 * (i_hi - i_lo);
+    launch(k_direct_pairs, dim3((unsigned)((threads + kDpThreads - 1) / kDpThreads)), dim3(kDpThreads),
+           0, as_stream(stream), n, i_lo, i_hi, pos, 24.0 * epsilon, 4.0 * epsilon, sigma * sigma,
+           forces, energy_part, virial_part, status, tag);
+    note_launches(1);
+    return launch_status();
+}
+
 extern "C" int rb_direct_pairs(int64_t n, const double *pos, double epsilon, double sigma,
                                double *forces, double *energy_part, double *virial_part,
                                unsigned long long *status, int64_t tag, void *stream) {
-    if (n < 0 || (n > 0 && (!pos || !forces || !energy_part || !virial_part)))
-        return RB_ERR_ARGUMENT;
-    if (n == 0) return RB_OK;
-    const int64_t threads = 32 * n;
-    launch(k_direct_pairs, dim3((unsigned)((threads + kDpThreads - 1) / kDpThreads)), dim3(kDpThreads),
-           0, as_stream(stream), n, pos, 24.0 * epsilon, 4.0 * epsilon, sigma * sigma, forces,
-           energy_part, virial_part, status, tag);
-    note_launches(1);
-    return launch_status();
+    return rb_direct_pairs_range(n, pos, 0, n, epsilon, sigma, forces, energy_part, virial_part,
+                                 status, tag, stream);
 }
 
 extern "C" size_t rb_direct_scratch_bytes(int64_t n) {
@@ -318,10 +331,13 @@ extern "C" size_t rb_direct_scratch_bytes(int64_t n) {
            (size_t)nb * 2 * sizeof(double) + 256;
 }
 
-extern "C" int rb_direct_triplets(int64_t n, const double *pos, double nu, double *forces,
-                                  double *energy_virial, void *scratch, size_t scratch_bytes,
-                                  unsigned long long *status, int64_t tag, void *stream) {
-    if (n < 0 || (n > 0 && (!pos || !forces || !energy_virial || !scratch)))
+extern "C" int rb_direct_triplets_range(int64_t n, const double *pos, int64_t i_lo,
+                                        int64_t i_hi, double nu, double *forces,
+                                        double *energy_virial, void *scratch,
+                                        size_t scratch_bytes, unsigned long long *status,
+                                        int64_t tag, void *stream) {
+    if (n < 0 || i_lo < 0 || i_hi > n || i_lo > i_hi ||
+        (n > 0 && (!pos || !forces || !energy_virial || !scratch)))
         return RB_ERR_ARGUMENT;
     if (n > kDtMaxN) return RB_ERR_CAPACITY;
     if (scratch_bytes < rb_direct_scratch_bytes(n)) return RB_ERR_ARGUMENT;
@@ -336,8 +352,8 @@ extern "C" int rb_direct_triplets(int64_t n, const double *pos, double nu, doubl
     launch(k_direct_prep, dim3(1), dim3(1024), 0, st, n, T, prefix);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        launch(kern, dim3(nb), dim3(T), smem, st, n, pos, (const int64_t *)prefix, slab, part_ew,
-               status, tag);
+        launch(kern, dim3(nb), dim3(T), smem, st, n, i_lo, i_hi, pos, (const int64_t *)prefix,
+               slab, part_ew, status, tag);
     };
     if (T == 1024)
         go(k_direct_triplets<1024>);
@@ -348,4 +364,11 @@ extern "C" int rb_direct_triplets(int64_t n, const double *pos, double nu, doubl
            (const double *)slab, (const double *)part_ew, 2.0 * nu, nu, forces, energy_virial);
     note_launches(3);
     return launch_status();
+}
+
+extern "C" int rb_direct_triplets(int64_t n, const double *pos, double nu, double *forces,
+                                  double *energy_virial, void *scratch, size_t scratch_bytes,
+                                  unsigned long long *status, int64_t tag, void *stream) {
+    return rb_direct_triplets_range(n, pos, 0, n, nu, forces, energy_virial, scratch,
+                                    scratch_bytes, status, tag, stream);
 }

@@ -319,28 +319,34 @@ class ForceEngine:
 
     # ------------------------------------------------------------ DirectSum
     def direct_pairs(self, epsilon: float, sigma: float, forces, tag: int = 0,
-                     reduce: bool = True) -> None:
+                     reduce: bool = True, rng=None) -> None:
         """All pairs of the particle-order positions (no cutoff, no image);
         per-particle halves in e2_rank/w2_rank, summed into scalars[E2],
-        scalars[W2] when `reduce`."""
-        st = self.L.rb_direct_pairs(self.n, ptr(self.pos), float(epsilon), float(sigma),
-                                    ptr(forces), ptr(self.e2_rank), ptr(self.w2_rank),
-                                    ptr(self.status), int(tag), self.stream)
-        _lib.check(st, "rb_direct_pairs")
+        scalars[W2] when `reduce`.  `rng` = (lo, hi): the particles of one
+        rank of a distributed DirectSum (other rows untouched)."""
+        lo, hi = (0, self.n) if rng is None else (int(rng[0]), int(rng[1]))
+        st = self.L.rb_direct_pairs_range(self.n, ptr(self.pos), lo, hi, float(epsilon),
+                                          float(sigma), ptr(forces), ptr(self.e2_rank),
+                                          ptr(self.w2_rank), ptr(self.status), int(tag),
+                                          self.stream)
+        _lib.check(st, "rb_direct_pairs_range")
         if reduce:
             self.reduce_pair()
 
-    def direct_triplets(self, nu: float, forces, tag: int = 0) -> None:
-        """All triplets (Newton-3); scalars[E3], scalars[W3] <- energy, virial."""
+    def direct_triplets(self, nu: float, forces, tag: int = 0, rng=None) -> None:
+        """All triplets (Newton-3); scalars[E3], scalars[W3] <- energy, virial.
+        `rng` = (lo, hi): only the triplets whose lowest member is in it."""
         need = int(self.L.rb_direct_scratch_bytes(self.n))
         if self.direct_scratch is None or self.direct_scratch.numel() * 8 < need:
             self.direct_scratch = self.torch.empty((need + 7) // 8, dtype=self.torch.float64,
                                                    device=self.device)
         ew = ctypes.c_void_p(self.scalars.data_ptr() + 8 * SCALAR_E3)
-        st = self.L.rb_direct_triplets(self.n, ptr(self.pos), float(nu), ptr(forces), ew,
-                                       ptr(self.direct_scratch), self.direct_scratch.numel() * 8,
-                                       ptr(self.status), int(tag), self.stream)
-        _lib.check(st, "rb_direct_triplets")
+        lo, hi = (0, self.n) if rng is None else (int(rng[0]), int(rng[1]))
+        st = self.L.rb_direct_triplets_range(self.n, ptr(self.pos), lo, hi, float(nu),
+                                             ptr(forces), ew, ptr(self.direct_scratch),
+                                             self.direct_scratch.numel() * 8, ptr(self.status),
+                                             int(tag), self.stream)
+        _lib.check(st, "rb_direct_triplets_range")
 
     def _count(self) -> None:
         st = self.L.rb_reduce_sum_i32(self.n, ptr(self.v_rank), ptr(self.visits),

@@ -230,3 +230,19 @@ def test_lattice_system_matches_reference():
         cfg = pkg.ScenarioConfig(particle_count=int(g[f"n{k}"]), box=g[f"box{k}"], dt=0.001,
                                  iterations=10, container="cuda_linked_cells", periodic=True)
         assert np.array_equal(build_lattice_system(cfg).positions, g[f"pos{k}"])
+
+
+def test_distributed_direct_sum_partition():
+    """Base ranges cover [0, n) in order with equal triplet counts (to one
+    base); particle ranges are equal."""
+    from paper_2507_11172_b200.direct_dist import base_ranges, particle_ranges
+
+    for n, parts in ((1000, 8), (4096, 3), (7, 4), (2, 2)):
+        for ranges in (base_ranges(n, parts), particle_ranges(n, parts)):
+            assert ranges[0][0] == 0 and ranges[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+        if n >= 1000:
+            m = np.arange(n - 1, -1, -1, dtype=np.float64)
+            work = m * (m - 1) / 2.0
+            shares = [work[a:b].sum() for a, b in base_ranges(n, parts)]
+            assert max(shares) - min(shares) <= work.max() + 1e-9 * work.sum()

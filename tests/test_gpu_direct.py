@@ -168,3 +168,57 @@ def test_respa_with_direct_sum_matches_oracle(pkg, oracle):
     assert np.max(np.abs(sg.velocities - os_.velocities)) <= 1e-10
     assert list(tg.iterations) == list(otr.iterations)
     assert max(_rel(a, b) for a, b in zip(tg.total, otr.total)) <= 1e-10
+
+
+def _dist_worker(rank, world, port, out_dir):
+    import os as _os
+
+    import torch.distributed as dist
+
+    _os.environ["MASTER_ADDR"] = "127.0.0.1"
+    _os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2507_11172_b200 as pkg
+        from paper_2507_11172_b200.direct_dist import DistributedDirectSum
+
+        rng = np.random.default_rng(TEST_SEED + 77)
+        pos = random_positions(rng, 400, (10.0,) * 3, False)
+        s = pkg.ParticleSystem.empty(400, (10.0,) * 3, periodic=False)
+        s.positions[:] = pos
+        c = DistributedDirectSum(dist)
+        ff = pkg.ForceField(nu=0.5)
+        c.pair_pass(s, ff)
+        c.triplet_pass(s, ff)
+        np.savez(_os.path.join(out_dir, f"r{rank}.npz"), f2=s.forces_2b, f3=s.forces_3b,
+                 e=np.array([c.pair_energy, c.pair_virial, c.triplet_energy, c.triplet_virial]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_direct_sum_matches_single(pkg, tmp_path, world):
+    """Ranks as processes sharing cuda:0 (gloo exchange): every rank holds the
+    same result, equal to the one-GPU pass to rounding."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mp.start_processes(_dist_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    outs = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
+    for o in outs[1:]:
+        assert np.array_equal(o["f2"], outs[0]["f2"]) and np.array_equal(o["f3"], outs[0]["f3"])
+        assert np.array_equal(o["e"], outs[0]["e"])
+    rng = np.random.default_rng(TEST_SEED + 77)
+    pos = random_positions(rng, 400, (10.0,) * 3, False)
+    s = _system(pkg, pos, 10.0)
+    ff = pkg.ForceField(nu=0.5)
+    f2, e2, w2 = pkg.direct_sum_pairs(s, ff)
+    f3, e3, w3 = pkg.direct_sum_triplets(s, ff)
+    assert normwise(outs[0]["f2"], f2) <= 1e-13 and normwise(outs[0]["f3"], f3) <= 1e-13
+    for got, ref in zip(outs[0]["e"], (e2, w2, e3, w3)):
+        assert _rel(got, ref) <= 1e-12

@@ -191,13 +191,17 @@ def domain_arm(args, cfg):
     The box is cfg2's FCC block replicated along the rank grid (32,000
     particles per GPU), decomposed over the ranks (NCCL halo exchange);
     value = ranks x steps/s (cfg2-equivalent steps per second), time = max
-    over ranks of CUDA-event time around K steps."""
+    over ranks of the CUDA-event time of steps W..W+K of one trajectory."""
     import torch
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # one process per GPU over NCCL; RB_DIST_BACKEND=gloo (and
+    # RB_SHARE_GPU=1: all ranks on cuda:0) exercises the same path on one GPU
+    share = os.environ.get("RB_SHARE_GPU") == "1"
+    local = 0 if share else local
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl")
+    dist.init_process_group(os.environ.get("RB_DIST_BACKEND", "nccl"))
     import paper_2507_11172_b200 as pkg
     from paper_2507_11172_b200.domain import auto_dims
     from paper_2507_11172_b200.domain_run import domain_respa_run, gpu_backend_factory
@@ -209,32 +213,112 @@ def domain_arm(args, cfg):
     ff = cfg.force_field()
     K = max(sf, (int(args.steps) + sf - 1) // sf * sf)
     W = max(sf, (max(3, int(args.warmup)) + sf - 1) // sf * sf)
-    warm = s.copy()
-    domain_respa_run(dist, warm, ff, pkg.RespaSchedule(cfg.dt, sf, W), gpu_backend_factory(ff),
-                     dims=dims)
-    dist.barrier()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    L = pkg._lib.lib()
+    backends = []
+
+    def factory(dec, n_total, r_build):
+        b = gpu_backend_factory(ff)(dec, n_total, r_build)
+        backends.append(b)
+        return b
+
+    # one trajectory of W + K steps; each of the steps W..W+K-1 is bracketed
+    # by CUDA events with an L2 flush (256 MiB write) in between, as on one
+    # GPU; time = the sum of the step times (each rank's own clock, max over
+    # ranks)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = pkg._lib.stream_handle()
+    starts, ends, marks = [], [], {}
+
+    def on_step(i):
+        if i == W:
+            torch.cuda.synchronize()
+            dist.barrier()
+            marks["l0"] = L.rb_launch_count()
+        if W < i <= W + K:
+            ends.append(torch.cuda.Event(enable_timing=True))
+            ends[-1].record()
+        if W <= i < W + K:
+            L.rb_l2_flush(pkg._lib.ptr(flush), flush.numel(), stream)
+            starts.append(torch.cuda.Event(enable_timing=True))
+            starts[-1].record()
+        if i == W + K:
+            torch.cuda.synchronize()
+            marks["l1"] = L.rb_launch_count() - K  # minus the flushes
+            dist.barrier()
+
+    run_sys = s.copy()
     with ClockSampler(local) as clocks:
-        a.record()
-        domain_respa_run(dist, s, ff, pkg.RespaSchedule(cfg.dt, sf, K), gpu_backend_factory(ff),
-                         dims=dims)
-        b.record()
-        torch.cuda.synchronize()
+        domain_respa_run(dist, run_sys, ff, pkg.RespaSchedule(cfg.dt, sf, W + K), factory,
+                         dims=dims, on_step=on_step)
+    step_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    t = torch.tensor([step_ms, float(marks["l1"] - marks["l0"])], dtype=torch.float64,
+                     device="cuda")
+    mx, sm = t.clone(), t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    ms = float(mx[0].item())
+    launches = int(sm[1].item())
+    value = world * K / (ms * 1e-3)
+
+    # e2e: the public decomposed run from host arrays (scatter, steps, gather)
+    e2e_sys = s.copy()
     dist.barrier()
-    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    t0 = time.perf_counter()
+    domain_respa_run(dist, e2e_sys, ff, pkg.RespaSchedule(cfg.dt, sf, K),
+                     gpu_backend_factory(ff), dims=dims)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e2e_s = time.perf_counter() - t0
+
+    # dominant kernel: the ATM pass on this rank's local set (owned + ghosts)
+    eng = backends[0].eng
+    f3 = torch.empty((eng.pos.shape[0], 3), dtype=torch.float64, device="cuda")
+    bk = backends[0]
+    eng.reset_status(0)
+    eng.atm(bk.window, bk.rc3, float(ff.nu), f3, tag=0, count_visits=True)
+    torch.cuda.synchronize()
+    unique = int(eng.visits.item())
+    ts = []
+    for _ in range(5):
+        L.rb_l2_flush(pkg._lib.ptr(flush), flush.numel(), stream)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        eng.atm_kernel(bk.window, bk.rc3, float(ff.nu), f3, 0)
+        eb.record()
+        torch.cuda.synchronize()
+        ts.append(ea.elapsed_time(eb))
+    atm_ms = statistics.median(ts)
+    peak = ctypes.c_double(0.0)
+    L.rb_fp64_peak(2000, ctypes.byref(peak), stream)
+    achieved = unique / (atm_ms * 1e-3) * FLOPS_PER_TRIPLET / 1e12
     if rank == 0:
         print(json.dumps({
-            "metric": METRIC, "value": world * K / (ms * 1e-3), "unit": "steps/s", "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded FCC lattice + jitter, SURVEY.md §8d)",
             "config": {"workload": f"cfg2 block x {dims} = {s.n} particles, domain-decomposed",
-                       "parallelism": f"domain decomposition {dims} (NCCL halo exchange)",
-                       "value": "ranks x steps/s (cfg2-equivalent)",
-                       "timed": "domain_respa_run incl. initial passes and final gather"},
+                       "particles": s.n, "step_size_factor": sf,
+                       "parallelism": f"domain decomposition {dims} "
+                                      f"({dist.get_backend()} halo exchange)",
+                       "value": "ranks x steps/s (cfg2-equivalent steps per second)",
+                       "timed": "steps W..W+K of one decomposed trajectory, per-step CUDA "
+                                "events summed, max over ranks",
+                       "l2": "flushed (256 MiB write) between timed steps"},
+            "roofline": {"bound": "fp64", "kernel": "ATM triplet pass on rank 0's local set",
+                         "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                         "frac": achieved / peak.value if peak.value else None, "traffic": None,
+                         "work": f"{FLOPS_PER_TRIPLET} FP64 flops per unique triplet x {unique} "
+                                 f"triplets (owned + ghost bases)",
+                         "kernel_ms": atm_ms},
+            "e2e": {"value": world * K / e2e_s, "unit": "steps/s",
+                    "h2d_bytes_per_step": 2 * s.n * 24 / K,
+                    "d2h_bytes_per_step": 4 * s.n * 24 / K,
+                    "note": f"domain_respa_run({K} steps) from host arrays on every rank, wall "
+                            f"clock incl. scatter, initial passes and the final gather"},
+            "gpu_launches": launches,
+            "gpu_launches_detail": {"note": "this library's launches during the timed steps, "
+                                            "summed over ranks"},
             "clocks": clocks.summary(),
         }), flush=True)
     dist.destroy_process_group()

@@ -190,12 +190,15 @@ def _numpy_like_update(torch, a, scale, b):
 
 
 def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory, skin: float = 0.3,
-                     sample_interval: Optional[int] = None, dims=None, device=None):
+                     sample_interval: Optional[int] = None, dims=None, device=None,
+                     on_step=None):
     """Run r-RESPA decomposed over dist.get_world_size() ranks.
 
     Every rank passes the same full initial `system` (host arrays); on return
     every rank's `system` holds the final state (gathered by particle id) and
-    the same RunTrace."""
+    the same RunTrace.  `on_step(i)` (optional) is called on the host before
+    step i and once more with i = num_iterations after the last step (the
+    bench records its CUDA events there)."""
     import torch
 
     world, rank = dist.get_world_size(), dist.get_rank()
@@ -309,6 +312,8 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     record(0, e2w2, e3w3)
     half_skin2 = (0.5 * skin) ** 2 * (1.0 - 1e-9)
     for i in range(schedule.num_iterations):
+        if on_step is not None:
+            on_step(i)
         sample = (i + 1) % interval == 0
         end_of_cycle = (i + 1) % s == 0
         if fast:
@@ -354,6 +359,8 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
         if sample:
             check(i + 1)
             record(i + 1, e2w2, e3w3)
+    if on_step is not None:
+        on_step(schedule.num_iterations)
     check(schedule.num_iterations)
 
     # gather the owned state of every rank into the host system (by id)

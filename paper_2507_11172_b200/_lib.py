@@ -110,10 +110,6 @@ class NativeLibraryError(RuntimeError):
     """The sm_100a library is missing, stale, or cannot run here."""
 
 
-def library_path() -> str:
-    return _build.LIB_PATH
-
-
 def lib():
     """Load (building in-tree first if needed) the C-ABI library."""
     global _lib

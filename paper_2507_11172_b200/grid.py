@@ -244,5 +244,3 @@ class CellGrid:
         return self.cell_particles[self.cell_start[cell]: self.cell_start[cell + 1]]
 
 
-def as_ctypes_grid_ptr(g):
-    return ctypes.byref(g)

@@ -14,7 +14,6 @@ reference cell assignment bit for bit:
 
 from __future__ import annotations
 
-import ctypes
 import functools
 from dataclasses import dataclass
 from typing import Optional

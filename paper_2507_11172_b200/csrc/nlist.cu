@@ -119,37 +119,41 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
                   max_count);
 }
 
-// mirror[p][k] = position of p in the row of q = rows[p][k] (binary search:
-// rows are sorted by rank; the relation is symmetric, so it is found).
-__global__ void k_mirror(int64_t n, const int32_t *__restrict__ rows,
-                         const int32_t *__restrict__ row_count, int32_t capacity,
-                         int32_t *__restrict__ mirror, const int64_t *flag,
-                         const unsigned long long *status, int64_t tag) {
+// mirror[p][k] = position of p in the row of q = rows[p][k].  One warp per
+// row p (grid-stride over rows); for each entry q > p a lane binary-searches
+// p in the rank-sorted row q and writes BOTH mirror[p][k] and, by symmetry,
+// mirror[q][that position] = k -- every pair is searched once.
+constexpr int kMirrorWarps = 8;
+
+__global__ void __launch_bounds__(kMirrorWarps * 32)
+    k_mirror(int64_t n, const int32_t *__restrict__ rows, const int32_t *__restrict__ row_count,
+             int32_t capacity, int32_t *__restrict__ mirror, const int64_t *flag,
+             const unsigned long long *status, int64_t tag) {
     pdl_enter();
     if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
-    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < n * (int64_t)capacity;
-         gid += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = gid / capacity;
-    const int k = (int)(gid % capacity);
-    const int m = row_count[p];
-    if (k >= m) continue;
-    const int q = rows[p * (int64_t)capacity + k];
-    int res = -1;
-    {
-        const int32_t *rq = rows + (int64_t)q * capacity;
-        int lo = 0, hi = row_count[q] - 1;
-        while (lo <= hi) {
-            const int mid = (lo + hi) >> 1;
-            const int v = rq[mid];
-            if (v == (int)p) {
-                res = mid;
-                break;
+    const int lane = threadIdx.x & 31;
+    for (int64_t p = (int64_t)blockIdx.x * kMirrorWarps + (threadIdx.x >> 5); p < n;
+         p += (int64_t)gridDim.x * kMirrorWarps) {
+        const int m = row_count[p];
+        const int32_t *rp = rows + p * (int64_t)capacity;
+        for (int k = lane; k < m; k += 32) {
+            const int q = __ldg(rp + k);
+            if (q <= p) continue;  // written by the warp of row q
+            const int32_t *rq = rows + (int64_t)q * capacity;
+            int lo = 0, hi = row_count[q] - 1, pos = -1;
+            while (lo <= hi) {
+                const int mid = (lo + hi) >> 1;
+                const int v = __ldg(rq + mid);
+                if (v == (int)p) {
+                    pos = mid;
+                    break;
+                }
+                if (v < (int)p) lo = mid + 1;
+                else hi = mid - 1;
             }
-            if (v < (int)p) lo = mid + 1;
-            else hi = mid - 1;
+            mirror[p * (int64_t)capacity + k] = pos;
+            if (pos >= 0) mirror[(int64_t)q * capacity + pos] = k;
         }
-    }
-    mirror[p * (int64_t)capacity + k] = res;
     }
 }
 
@@ -178,11 +182,10 @@ extern "C" int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *ro
                                const unsigned long long *status, int64_t tag, void *stream) {
     if (n < 0 || capacity <= 0 || !rows || !row_count || !mirror) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
-    const int64_t threads = n * (int64_t)capacity;
-    const int tb = 256;
-    int64_t mblocks = (threads + tb - 1) / tb;
-    if (mblocks > 148 * 16) mblocks = 148 * 16;  // grid-stride
-    launch(k_mirror, dim3((unsigned)mblocks), dim3(tb), 0, as_stream(stream), n, rows, row_count, capacity, mirror, rebuild_flag, status, tag);
+    int64_t mblocks = (n + kMirrorWarps - 1) / kMirrorWarps;
+    if (rebuild_flag && mblocks > 148 * 8) mblocks = 148 * 8;  // gated: grid-stride
+    launch(k_mirror, dim3((unsigned)mblocks), dim3(kMirrorWarps * 32), 0, as_stream(stream), n,
+           rows, row_count, capacity, mirror, rebuild_flag, status, tag);
     note_launches(1);
     return launch_status();
 }

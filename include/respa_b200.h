@@ -323,6 +323,15 @@ RB_API int rb_sample(int64_t n, const double *vel, const double *e2_rank, const 
 RB_API int rb_fp64_peak(int32_t iters, double *tflops, void *stream);
 /* Writes `bytes` of a scratch buffer to evict L2 between timed steps. */
 RB_API int rb_l2_flush(void *buf, size_t bytes, void *stream);
+/* Timing events that can be recorded inside a CUDA-graph capture (external
+ * event-record nodes): the bench brackets every step of a captured period
+ * with them, so a step is timed from its first to its last kernel on the
+ * device.  rb_event_elapsed returns milliseconds between two recorded
+ * events (synchronises on the second). */
+RB_API int rb_event_create(void **event);
+RB_API int rb_event_destroy(void *event);
+RB_API int rb_event_record(void *event, void *stream);
+RB_API int rb_event_elapsed(void *start, void *end, float *ms);
 
 #ifdef __cplusplus
 }

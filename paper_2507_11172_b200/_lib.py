@@ -86,6 +86,10 @@ SIGNATURES = {
     "rb_trace_record": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "rb_fp64_peak": (ctypes.c_int, [_I32, _P, _P]),
     "rb_l2_flush": (ctypes.c_int, [_P, _SZ, _P]),
+    "rb_event_create": (ctypes.c_int, [_P]),
+    "rb_event_destroy": (ctypes.c_int, [_P]),
+    "rb_event_record": (ctypes.c_int, [_P, _P]),
+    "rb_event_elapsed": (ctypes.c_int, [_P, _P, _P]),
     "rb_direct_pairs": (ctypes.c_int, [_I64, _P, _D, _D, _P, _P, _P, _P, _I64, _P]),
     "rb_direct_scratch_bytes": (ctypes.c_size_t, [_I64]),
     "rb_direct_triplets": (ctypes.c_int, [_I64, _P, _D, _P, _P, _P, _SZ, _P, _I64, _P]),

@@ -493,3 +493,31 @@ extern "C" int rb_device_count(void) {
     }
     return n;
 }
+
+extern "C" int rb_event_create(void **event) {
+    if (!event) return RB_ERR_ARGUMENT;
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDefault) != cudaSuccess) return RB_ERR_CUDA;
+    *event = (void *)e;
+    return RB_OK;
+}
+
+extern "C" int rb_event_destroy(void *event) {
+    return cudaEventDestroy((cudaEvent_t)event) == cudaSuccess ? RB_OK : RB_ERR_CUDA;
+}
+
+extern "C" int rb_event_record(void *event, void *stream) {
+    // external: inside a stream capture this becomes an event-record node
+    return cudaEventRecordWithFlags((cudaEvent_t)event, as_stream(stream),
+                                    cudaEventRecordExternal) == cudaSuccess
+               ? RB_OK
+               : RB_ERR_CUDA;
+}
+
+extern "C" int rb_event_elapsed(void *start, void *end, float *ms) {
+    if (!ms) return RB_ERR_ARGUMENT;
+    if (cudaEventSynchronize((cudaEvent_t)end) != cudaSuccess) return RB_ERR_CUDA;
+    return cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end) == cudaSuccess
+               ? RB_OK
+               : RB_ERR_CUDA;
+}

@@ -369,7 +369,7 @@ def ours_arm(args, cfg):
         for j in range(sf):
             L.rb_l2_flush(_lib.ptr(flush), flush.numel(), st)
             _lib.check(L.rb_event_record(ev[2 * j], st), "rb_event_record")
-            run._step(j)
+            run._step(j, j)
             _lib.check(L.rb_event_record(ev[2 * j + 1], st), "rb_event_record")
 
     l0 = L.rb_launch_count()

@@ -270,6 +270,19 @@ RB_API int rb_respa_drift(int64_t n, double *pos, double *vel, const double *f2_
                           double skin, int64_t *rebuild_flag, unsigned long long *status,
                           int64_t tag, int32_t advance_step, uint64_t rebuild_cond,
                           void *stream);
+/* The kick that ends step i-1 folded into the drift that opens step i (one
+ * pass over the particles): v += half_dt (f2_old + f2_new) [+ half_respa f3
+ * if kick3_prev]; f2_old = f2_new -- with rb_respa_kick's error rules at
+ * tag i-1 -- then the step-opening drift of rb_respa_drift (advance_step,
+ * tags from the device) with kick3 at cycle start.  Bit-identical to the two
+ * launches. */
+RB_API int rb_respa_kick_drift(int64_t n, double *pos, double *vel, double *f2_old,
+                               const double *f2_new, const double *f3, const double *box3_host,
+                               int32_t periodic, double dt, double half_dt, double half_drift,
+                               double half_respa, int32_t kick3_prev, int32_t kick3,
+                               const int32_t *rank_of, double *pos_r, const double *x_ref,
+                               double skin, int64_t *rebuild_flag, unsigned long long *status,
+                               uint64_t rebuild_cond, void *stream);
 RB_API int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f2_new,
                   const double *f3, double half_dt, double half_respa, int32_t kick3,
                   unsigned long long *status, int64_t tag, void *stream);
@@ -279,9 +292,9 @@ RB_API int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f
  * current step, status[2] the last closed step, status[3] the number of
  * steps in which a drift flagged a row rebuild (diagnostic).  A
  * step-opening drift (advance_step) numbers its step status[2] + 1 and
- * writes it to status[1]; a kick with tag -1 closes the step (status[2] =
- * status[1]); rb_step_begin does both in one launch (status[2] = status[1],
- * status[1] += 1).  Kernels given tag == -1 read their tag from status[1].
+ * writes it to status[1]; the step's pair pass and kick with tag -1 close it
+ * (status[2] = status[1]); rb_step_begin does both in one launch (status[2] =
+ * status[1], status[1] += 1).  Kernels given tag == -1 read their tag from status[1].
  * rb_step_begin increments status[1]; rb_trace_record writes the 8-double
  * row [tag, sum v^2, E2, W2, E3, W3, 0, 0] at trace[8 * (tag / interval)]
  * from device scalars (RunTrace.record, integrators.py:74-83). */

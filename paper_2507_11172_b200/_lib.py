@@ -81,6 +81,8 @@ SIGNATURES = {
     "rb_reduce_sum_i32": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
     "rb_respa_drift": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _I32, _D, _D, _D, _I32, _P, _P, _P, _D,
                                       _P, _P, _I64, _I32, _U64, _P]),
+    "rb_respa_kick_drift": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _I32, _D, _D, _D, _D,
+                                           _I32, _I32, _P, _P, _P, _D, _P, _P, _U64, _P]),
     "rb_respa_kick": (ctypes.c_int, [_I64, _P, _P, _P, _P, _D, _D, _I32, _P, _I64, _P]),
     "rb_step_begin": (ctypes.c_int, [_P, _P]),
     "rb_trace_record": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),

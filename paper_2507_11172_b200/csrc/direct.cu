@@ -40,7 +40,10 @@ __global__ void __launch_bounds__(kDpThreads)
     // fixed xor tree
     const int lane = threadIdx.x & 31;
     const int64_t i = i_lo + (((int64_t)blockIdx.x * kDpThreads + threadIdx.x) >> 5);
+    const bool from_device = tag < 0;
     tag = resolve_tag(tag, status);
+    // like the LJ pass: closes the device step (status[2], see lj.cu)
+    if (from_device && status && blockIdx.x == 0 && threadIdx.x == 0) status[2] = (unsigned long long)tag;
     if (i >= i_hi) return;  // whole warps
     const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;

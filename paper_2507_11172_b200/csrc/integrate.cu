@@ -47,23 +47,53 @@ __device__ __forceinline__ double wrap_coord(double x, double box) {
 // of the rows in this very step (*rebuild_flag = tag), so every pair within
 // rc is always inside the rows built at rc + skin.
 __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict__ vel,
-                        const double *__restrict__ f2_old, const double *__restrict__ f3,
+                        double *__restrict__ f2_old, const double *__restrict__ f3,
                         double bx, double by, double bz, int periodic, double dt,
                         double half_drift, double half_respa, int kick3,
                         const int32_t *__restrict__ rank_of, double *__restrict__ pr,
                         const double *__restrict__ x_ref, double skin_half2,
                         int64_t *rebuild_flag, unsigned long long *status, int64_t tag,
-                        int advance, cudaGraphConditionalHandle cond) {
+                        int advance, cudaGraphConditionalHandle cond,
+                        const double *__restrict__ f2_new, double half_dt, int kick_prev,
+                        int kick3_prev) {
     pdl_enter();
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // a step-opening drift numbers its step from the last CLOSED step
-    // (status[2], written by the kick) and publishes it in status[1]: no
-    // kernel reads the word another block of it writes
+    // (status[2], written by the step's pair pass and kick) and publishes it
+    // in status[1]: no kernel reads the word another block of it writes.
+    // kick_prev: first the kick that ends the previous step (rb_respa_kick_drift)
     if (advance) {
         tag = (int64_t)(*(volatile const unsigned long long *)(status + 2)) + 1;
         if (p == 0) status[1] = (unsigned long long)tag;
     } else {
         tag = resolve_tag(tag, status);
+    }
+    if (kick_prev && p < n) {
+        // the kick that closes the previous step (tag - 1), folded in: the
+        // same updates and error rules as k_kick (integrators.py:158-165)
+        const int64_t tp = tag - 1;
+        bool go = true, do3 = kick3_prev != 0;
+        const unsigned long long sw = *(volatile const unsigned long long *)status;
+        if (sw != RB_STATUS_CLEAR) {
+            const long long t = (long long)(sw >> 8);
+            const int k = (int)(sw & 0xff);
+            if (t < tp || (t == tp && k == RB_KIND_PAIR_MIN_SEPARATION)) go = false;
+            if (t == tp && k == RB_KIND_TRIPLET_MIN_SEPARATION) do3 = false;
+        }
+        if (go) {
+            bool finite = true;
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                const int64_t i = 3 * p + c;
+                const double fnew = f2_new[i];
+                double v = xadd(vel[i], xmul(half_dt, xadd(f2_old[i], fnew)));
+                if (do3) v = xadd(v, xmul(half_respa, f3[i]));
+                vel[i] = v;
+                f2_old[i] = fnew;
+                finite = finite && isfinite(v);
+            }
+            if (!finite) record_status(status, tp, RB_KIND_NONFINITE);
+        }
     }
     if (p < n && !frozen(status, tag, 0)) {
         const double box[3] = {bx, by, bz};
@@ -333,6 +363,27 @@ __global__ void k_flush(int4 *buf, int64_t n16, int v) {
 
 using namespace rb;
 
+static int drift_launch(int64_t n, double *pos, double *vel, double *f2_old, const double *f2_new,
+                        const double *f3, const double *box3_host, int32_t periodic, double dt,
+                        double half_dt, double half_drift, double half_respa, int32_t kick3,
+                        int32_t kick_prev, int32_t kick3_prev, const int32_t *rank_of,
+                        double *pos_r, const double *x_ref, double skin, int64_t *rebuild_flag,
+                        unsigned long long *status, int64_t tag, int32_t advance_step,
+                        uint64_t rebuild_cond, void *stream) {
+    if (n < 0 || !box3_host) return RB_ERR_ARGUMENT;
+    if (advance_step && (!status || tag >= 0)) return RB_ERR_ARGUMENT;
+    if (n == 0) return advance_step ? rb_step_begin(status, stream) : RB_OK;
+    const int tb = 256;
+    const double half = 0.5 * skin;
+    launch(k_drift, dim3((unsigned)((n + tb - 1) / tb)), dim3(tb), 0, as_stream(stream), n, pos,
+           vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt, half_drift,
+           half_respa, kick3, rank_of, pos_r, x_ref, half * half * (1.0 - 1e-9), rebuild_flag,
+           status, tag, advance_step ? 1 : 0, (cudaGraphConditionalHandle)rebuild_cond, f2_new,
+           half_dt, kick_prev ? 1 : 0, kick3_prev ? 1 : 0);
+    note_launches(1);
+    return launch_status();
+}
+
 extern "C" int rb_respa_drift(int64_t n, double *pos, double *vel, const double *f2_old,
                               const double *f3, const double *box3_host, int32_t periodic,
                               double dt, double half_drift, double half_respa, int32_t kick3,
@@ -340,17 +391,24 @@ extern "C" int rb_respa_drift(int64_t n, double *pos, double *vel, const double 
                               double skin, int64_t *rebuild_flag, unsigned long long *status,
                               int64_t tag, int32_t advance_step, uint64_t rebuild_cond,
                               void *stream) {
-    if (n < 0 || !box3_host) return RB_ERR_ARGUMENT;
-    if (advance_step && (!status || tag >= 0)) return RB_ERR_ARGUMENT;
-    if (n == 0) return advance_step ? rb_step_begin(status, stream) : RB_OK;
-    const int tb = 256;
-    const double half = 0.5 * skin;
-    launch(k_drift, dim3((unsigned)((n + tb - 1) / tb)), dim3(tb), 0, as_stream(stream), n, pos, vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt,
-        half_drift, half_respa, kick3, rank_of, pos_r, x_ref, half * half * (1.0 - 1e-9),
-        rebuild_flag, status, tag, advance_step ? 1 : 0,
-        (cudaGraphConditionalHandle)rebuild_cond);
-    note_launches(1);
-    return launch_status();
+    return drift_launch(n, pos, vel, const_cast<double *>(f2_old), nullptr, f3, box3_host,
+                        periodic, dt, 0.0, half_drift, half_respa, kick3, 0, 0, rank_of, pos_r,
+                        x_ref, skin, rebuild_flag, status, tag, advance_step, rebuild_cond,
+                        stream);
+}
+
+extern "C" int rb_respa_kick_drift(int64_t n, double *pos, double *vel, double *f2_old,
+                                   const double *f2_new, const double *f3,
+                                   const double *box3_host, int32_t periodic, double dt,
+                                   double half_dt, double half_drift, double half_respa,
+                                   int32_t kick3_prev, int32_t kick3, const int32_t *rank_of,
+                                   double *pos_r, const double *x_ref, double skin,
+                                   int64_t *rebuild_flag, unsigned long long *status,
+                                   uint64_t rebuild_cond, void *stream) {
+    if (!status || !f2_new) return RB_ERR_ARGUMENT;
+    return drift_launch(n, pos, vel, f2_old, f2_new, f3, box3_host, periodic, dt, half_dt,
+                        half_drift, half_respa, kick3, 1, kick3_prev, rank_of, pos_r, x_ref, skin,
+                        rebuild_flag, status, -1, 1, rebuild_cond, stream);
 }
 
 extern "C" int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f2_new,

@@ -46,7 +46,11 @@ __global__ void __launch_bounds__(kLjThreads)
     const int64_t r = gid / kLjGroup;
     const int sub = (int)(gid % kLjGroup);
     const bool active = r < n;
+    const bool from_device = tag < 0;
     tag = resolve_tag(tag, status);
+    // the pair pass closes the device step (status[2]): the kick that ends it
+    // may be folded into the next step's drift (rb_respa_kick_drift)
+    if (from_device && status && gid == 0) status[2] = (unsigned long long)tag;
     if (warp_frozen(status, tag, RB_KIND_PAIR_MIN_SEPARATION)) return;
     const Image im = make_image(g);
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;

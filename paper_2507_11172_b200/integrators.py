@@ -179,6 +179,8 @@ class DeviceRespa:
         self.graph = None
         # captured steps put the rebuild into a conditional graph node
         self.cond_rebuild = os.environ.get("RB_COND_REBUILD", "1") != "0"
+        # inside a sampling period a step's kick runs in the next drift
+        self.fuse_kick = os.environ.get("RB_FUSE_KICK", "1") != "0"
 
     # -------------------------------------------------------------- pieces
     def _geom(self):
@@ -240,36 +242,52 @@ class DeviceRespa:
         # sums of the five trace scalars + the trace row, one launch
         self.eng.sample(self.v, self.trace_dev, self.interval)
 
-    def _step(self, i: int) -> None:
-        """Loop body of integrators.py:148-172 for iteration i (tag i+1)."""
+    def _step(self, i: int, j: Optional[int] = None) -> None:
+        """Loop body of integrators.py:148-172 for iteration i (tag i+1).
+
+        j = position of the step inside a sampling period (None: a step on
+        its own).  Inside a period the kick that ends step i is folded into
+        the drift of step i+1 (rb_respa_kick_drift, one pass over the
+        particles, bit-identical); the period's last step kicks itself, so
+        the sample point and the host see completed steps."""
         L, eng = self.eng.L, self.eng
         s = self.schedule.step_size_factor
         verlet = self.periodic
         null = ctypes.c_void_p(0)
+        fuse = self.fuse_kick and j is not None and j > 0
+        defer = self.fuse_kick and j is not None and j < self.interval - 1
         # under capture: the drift sets the rebuild conditional with the flag
         cond = eng.rebuild_cond() if verlet and self.cond_rebuild else 0
-        # the drift opens the device step (status[1] = last closed + 1)
-        st = L.rb_respa_drift(self.n, ptr(self.x), ptr(self.v), ptr(self.f2_old), ptr(self.f3),
-                              self.box.ctypes.data_as(ctypes.c_void_p), int(self.periodic),
-                              self.dt, self.half_drift, self.half_respa, int(i % s == 0),
-                              ptr(eng.rank_of) if verlet else null,
-                              ptr(eng.pos_r) if verlet else null,
-                              ptr(eng.x_ref) if verlet else null, self.skin,
-                              ptr(eng.rebuild_flag) if verlet else null,
-                              ptr(eng.status), _lib.RB_TAG_FROM_DEVICE, 1, cond, eng.stream)
-        _lib.check(st, "rb_respa_drift")
+        box = self.box.ctypes.data_as(ctypes.c_void_p)
+        common = (ptr(eng.rank_of) if verlet else null, ptr(eng.pos_r) if verlet else null,
+                  ptr(eng.x_ref) if verlet else null, self.skin,
+                  ptr(eng.rebuild_flag) if verlet else null, ptr(eng.status))
+        if fuse:  # the kick of step i-1, then the drift opening step i
+            st = L.rb_respa_kick_drift(self.n, ptr(self.x), ptr(self.v), ptr(self.f2_old),
+                                       ptr(self.f2_new), ptr(self.f3), box, int(self.periodic),
+                                       self.dt, self.half_dt, self.half_drift, self.half_respa,
+                                       int(i % s == 0), int(i % s == 0), *common, cond,
+                                       eng.stream)
+            _lib.check(st, "rb_respa_kick_drift")
+        else:  # the drift opens the device step (status[1] = last closed + 1)
+            st = L.rb_respa_drift(self.n, ptr(self.x), ptr(self.v), ptr(self.f2_old),
+                                  ptr(self.f3), box, int(self.periodic), self.dt,
+                                  self.half_drift, self.half_respa, int(i % s == 0), *common,
+                                  _lib.RB_TAG_FROM_DEVICE, 1, cond, eng.stream)
+            _lib.check(st, "rb_respa_drift")
         end_of_cycle = (i + 1) % s == 0
         self._forces(_lib.RB_TAG_FROM_DEVICE, end_of_cycle, self.f2_new, cond)
-        st = L.rb_respa_kick(self.n, ptr(self.v), ptr(self.f2_old), ptr(self.f2_new), ptr(self.f3),
-                             self.half_dt, self.half_respa, int(end_of_cycle), ptr(eng.status),
-                             _lib.RB_TAG_FROM_DEVICE, eng.stream)
-        _lib.check(st, "rb_respa_kick")
+        if not defer:
+            st = L.rb_respa_kick(self.n, ptr(self.v), ptr(self.f2_old), ptr(self.f2_new),
+                                 ptr(self.f3), self.half_dt, self.half_respa, int(end_of_cycle),
+                                 ptr(eng.status), _lib.RB_TAG_FROM_DEVICE, eng.stream)
+            _lib.check(st, "rb_respa_kick")
         if (i + 1) % self.interval == 0:
             self._record()
 
     def _period(self, first: int) -> None:
-        for i in range(first, first + self.interval):
-            self._step(i)
+        for j in range(self.interval):
+            self._step(first + j, j)
 
     # ----------------------------------------------------------------- run
     def start(self) -> None:
@@ -330,7 +348,7 @@ class DeviceRespa:
     def capture_steps(self):
         """One CUDA graph per step position inside a sampling period (the
         step kinds repeat with the period), for per-step timing."""
-        return [self._captured(lambda j=j: self._step(j)) for j in range(self.interval)]
+        return [self._captured(lambda j=j: self._step(j, j)) for j in range(self.interval)]
 
     def run_periods(self, first_period: int, count: int) -> None:
         for k in range(first_period, first_period + count):

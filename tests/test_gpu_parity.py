@@ -470,3 +470,20 @@ def test_domain_decomposed_gpu_kernels_match_single_domain(pkg, tmp_path, world,
     assert np.max(np.abs(out["x"] - ref.positions)) <= 1e-10
     assert np.max(np.abs(out["v"] - ref.velocities)) <= 1e-10
     assert max(_rel(a, b) for a, b in zip(out["total"], tr.total)) <= 1e-10
+
+
+def test_kick_folded_into_drift_is_bit_identical(pkg, monkeypatch):
+    """rb_respa_kick_drift (a step's kick folded into the next drift inside a
+    sampling period) gives exactly the separate kick / drift launches."""
+    base = pkg.systems.fcc_system(6, temperature=0.9, seed=15, vseed=16)
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5)
+    out = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("RB_FUSE_KICK", fuse)
+        s = base.copy()
+        tr = pkg.respa_run(s, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 3, 60),
+                           sample_interval=6)
+        out.append((s, tr))
+    (a, ta), (b, tb) = out
+    assert np.array_equal(a.positions, b.positions) and np.array_equal(a.velocities, b.velocities)
+    assert np.array_equal(a.forces_2b, b.forces_2b) and ta.total == tb.total

@@ -34,7 +34,10 @@ __device__ __forceinline__ double lj_rcp(double x) {
     return fma(y, fma(e, e, e), y);
 }
 
-__global__ void __launch_bounds__(kLjThreads)
+#ifndef RB_LJ_MIN_BLOCKS
+#define RB_LJ_MIN_BLOCKS 4  // 64 registers: 4 blocks of 256 per SM
+#endif
+__global__ void __launch_bounds__(kLjThreads, RB_LJ_MIN_BLOCKS)
     k_lj(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ parts,
          const int32_t *__restrict__ rows, const int32_t *__restrict__ row_count,
          int32_t capacity, double rc2, double eps24, double eps4, double sigma2,

@@ -62,15 +62,140 @@ def auto_dims(world: int, cells) -> tuple:
     return best
 
 
+# ---------------------------------------------------------------------------
+# cost-aware block boundaries (inhomogeneous systems, e.g. the cfg5 slab)
+# ---------------------------------------------------------------------------
+
+
+def cell_occupancy(positions: np.ndarray, geom: Geometry) -> np.ndarray:
+    """Particles per global cell (the binning arithmetic), shape `geom.cells`."""
+    n = np.asarray(geom.cells)
+    inv = np.asarray(geom.inv_cell)
+    c = np.clip(np.trunc(np.asarray(positions) * inv[None, :]).astype(np.int64), 0, n[None, :] - 1)
+    occ = np.zeros(tuple(n), dtype=np.float64)
+    np.add.at(occ, (c[:, 0], c[:, 1], c[:, 2]), 1.0)
+    return occ
+
+
+def cell_costs(positions: np.ndarray, geom: Geometry, triplet_weight: float = 0.0) -> np.ndarray:
+    """Estimated work per global cell, shape `geom.cells`.
+
+    A particle's pair work grows with its neighbour count, its triplet work
+    with the square of it; the neighbour count is estimated from the
+    occupancy of the 27 surrounding cells (cells >= r_build, so the cutoff
+    sphere fills ~0.155 of them).  Per particle: 5 (integration, binning,
+    rows) + nb + triplet_weight * nb^2, with triplet_weight ~ 0.29 / s for
+    the ATM pass every s-th step (4x the flops of a pair, 210 triplets per
+    54 pairs in the rho 0.8 liquid).  A heuristic: it only moves block
+    boundaries, never results."""
+    occ = cell_occupancy(positions, geom)
+    around = np.zeros_like(occ)
+    for a in (-1, 0, 1):
+        for b in (-1, 0, 1):
+            for e in (-1, 0, 1):
+                around += np.roll(occ, (a, b, e), axis=(0, 1, 2))
+    nb = 0.155 * around
+    return occ * (5.0 + nb + float(triplet_weight) * nb * nb)
+
+
+def balanced_bounds(profile: np.ndarray, parts: int) -> np.ndarray:
+    """Cut a periodic row of cell layers into `parts` contiguous blocks
+    (boundaries at 0 and n) minimising the largest block cost; every block
+    keeps >= 1 layer and, when split, leaves room for its two halo layers
+    (width <= n - 2).  Exact DP, ties to the leftmost cut (deterministic)."""
+    profile = np.asarray(profile, dtype=np.float64)
+    n = profile.shape[0]
+    if parts == 1:
+        return np.array([0, n])
+    cum = np.concatenate([[0.0], np.cumsum(profile)])
+    w_max = n - 2
+    inf = float("inf")
+    # best[p][e]: minimal max cost of splitting layers [0, e) into p blocks
+    best = np.full((parts + 1, n + 1), inf)
+    cut = np.zeros((parts + 1, n + 1), dtype=np.int64)
+    best[0][0] = 0.0
+    for p in range(1, parts + 1):
+        for e in range(p, n + 1):
+            for b in range(max(p - 1, e - w_max), e):
+                if best[p - 1][b] == inf:
+                    continue
+                v = max(best[p - 1][b], cum[e] - cum[b])
+                if v < best[p][e]:
+                    best[p][e], cut[p][e] = v, b
+    if best[parts][n] == inf:
+        raise ValueError(f"cannot cut {n} cell layers into {parts} blocks with halos")
+    bounds = [n]
+    for p in range(parts, 0, -1):
+        bounds.append(int(cut[p][bounds[-1]]))
+    return np.array(bounds[::-1])
+
+
+def block_costs(costs: np.ndarray, dims, bounds, occ: Optional[np.ndarray] = None,
+                ghost_cost: float = 5.0) -> np.ndarray:
+    """Cost per block of the rank grid (rank order): the block's cells, plus
+    `ghost_cost` per particle of its halo layer (split dimensions, periodic)
+    when the occupancy `occ` is given."""
+    n = costs.shape
+    out = []
+    for bx in range(dims[0]):
+        for by in range(dims[1]):
+            for bz in range(dims[2]):
+                ks = (bx, by, bz)
+                own = np.ix_(*[np.arange(bounds[d][ks[d]], bounds[d][ks[d] + 1])
+                               for d in range(3)])
+                total = float(costs[own].sum())
+                if occ is not None:
+                    win = np.ix_(*[np.arange(bounds[d][ks[d]] - 1, bounds[d][ks[d] + 1] + 1) % n[d]
+                                   if dims[d] > 1 else np.arange(n[d]) for d in range(3)])
+                    total += ghost_cost * float(occ[win].sum() - occ[own].sum())
+                out.append(total)
+    return np.array(out)
+
+
+def balanced_layout(costs: np.ndarray, world: int, occ: Optional[np.ndarray] = None):
+    """(dims, bounds) for a cost array: every factorisation of `world` whose
+    blocks can hold a halo, each dimension cut by `balanced_bounds` on its
+    cost profile; the layout with the smallest largest-block cost (ghosts
+    included when `occ` is given) wins, ties within 1e-9 relative to the
+    most cubic blocks, as `auto_dims`."""
+    n = costs.shape
+    best = None
+    for px in range(1, world + 1):
+        if world % px:
+            continue
+        for py in range(1, world // px + 1):
+            if (world // px) % py:
+                continue
+            dims = (px, py, world // px // py)
+            try:
+                bounds = [balanced_bounds(costs.sum(axis=tuple(a for a in range(3) if a != d)),
+                                          dims[d]) for d in range(3)]
+            except ValueError:
+                continue
+            worst = float(block_costs(costs, dims, bounds, occ).max())
+            blk = [c / p for c, p in zip(n, dims)]
+            shape = max(blk) / min(blk)
+            key = (worst, shape)
+            if best is None or key[0] < best[0][0] * (1 - 1e-9) or \
+                    (key[0] <= best[0][0] * (1 + 1e-9) and shape < best[0][1] - 1e-12):
+                best = (key, dims, bounds)
+    if best is None:
+        raise ValueError(f"cannot decompose {n} cells over {world} ranks")
+    return best[1], best[2]
+
+
 @dataclass
 class Decomposition:
-    """Block geometry of one rank."""
+    """Block geometry of one rank.  `bounds` (optional, per dimension the
+    dims[d] + 1 cell boundaries from 0 to cells[d]) replaces the even split,
+    e.g. with `balanced_layout`'s cost-aware cuts."""
 
     box: np.ndarray
     r_build: float
     world: int
     rank: int
     dims: Optional[tuple] = None
+    bounds: Optional[list] = None
     geom: Geometry = field(init=False)
 
     def __post_init__(self):
@@ -84,8 +209,17 @@ class Decomposition:
             raise ValueError(f"rank grid {self.dims} does not match world size {self.world}")
         px, py, pz = self.dims
         self.coord = (self.rank // (py * pz), (self.rank // pz) % py, self.rank % pz)
-        self.bounds = [np.array([k * n[d] // self.dims[d] for k in range(self.dims[d] + 1)])
-                       for d in range(3)]
+        if self.bounds is None:
+            self.bounds = [np.array([k * n[d] // self.dims[d] for k in range(self.dims[d] + 1)])
+                           for d in range(3)]
+        else:
+            self.bounds = [np.asarray(b, dtype=np.int64) for b in self.bounds]
+            for d in range(3):
+                b = self.bounds[d]
+                if b.shape != (self.dims[d] + 1,) or b[0] != 0 or b[-1] != n[d] or \
+                        np.any(np.diff(b) < 1):
+                    raise ValueError(f"bad block bounds {b.tolist()} for {n[d]} cells / "
+                                     f"{self.dims[d]} blocks in dim {d}")
         self.lo = tuple(int(self.bounds[d][self.coord[d]]) for d in range(3))
         self.hi = tuple(int(self.bounds[d][self.coord[d] + 1]) for d in range(3))
         for d in range(3):

@@ -26,8 +26,9 @@ from typing import Optional
 
 import numpy as np
 
-from .domain import PAYLOAD, Decomposition, Exchanger, allsum_in_rank_order, build_ghosts, migrate, \
-    refresh_ghosts
+from .domain import PAYLOAD, Decomposition, Exchanger, allsum_in_rank_order, balanced_bounds, \
+    balanced_layout, build_ghosts, cell_costs, cell_occupancy, migrate, refresh_ghosts
+from .grid import geometry
 from .integrators import IntegrationBlowUp, RespaSchedule, RunTrace
 from .model import triplet_cutoff
 
@@ -191,14 +192,16 @@ def _numpy_like_update(torch, a, scale, b):
 
 def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory, skin: float = 0.3,
                      sample_interval: Optional[int] = None, dims=None, device=None,
-                     on_step=None):
+                     on_step=None, balance: bool = False):
     """Run r-RESPA decomposed over dist.get_world_size() ranks.
 
     Every rank passes the same full initial `system` (host arrays); on return
     every rank's `system` holds the final state (gathered by particle id) and
     the same RunTrace.  `on_step(i)` (optional) is called on the host before
     step i and once more with i = num_iterations after the last step (the
-    bench records its CUDA events there)."""
+    bench records its CUDA events there).  `balance` cuts the blocks by the
+    estimated work of the initial configuration (domain.balanced_layout: for
+    inhomogeneous systems such as the cfg5 slab) instead of evenly."""
     import torch
 
     world, rank = dist.get_world_size(), dist.get_rank()
@@ -209,7 +212,17 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     box = np.asarray(system.box, dtype=np.float64)
     skin = max(0.0, min(float(skin), float(box.min()) / 2.0 - r_list))
     r_build = r_list + skin
-    dec = Decomposition(box, r_build, world, rank, dims)
+    bounds = None
+    if balance:
+        geom = geometry(box, None, r_build, True)
+        occ = cell_occupancy(system.positions, geom)
+        costs = cell_costs(system.positions, geom, 0.29 / s if float(ff.nu) != 0.0 else 0.0)
+        if dims is None:
+            dims, bounds = balanced_layout(costs, world, occ)
+        else:
+            bounds = [balanced_bounds(costs.sum(axis=tuple(a for a in range(3) if a != d)),
+                                      int(dims[d])) for d in range(3)]
+    dec = Decomposition(box, r_build, world, rank, dims, bounds)
     n_total = system.positions.shape[0]
     backend = backend_factory(dec, n_total, r_build)
     dev = backend.device if device is None else device

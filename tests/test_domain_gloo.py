@@ -27,13 +27,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _system():
+def _system(kind="fcc"):
     from paper_2507_11172_b200 import systems
 
+    if kind == "slab":  # liquid block in the middle half of z, vapour outside
+        return systems.slab_system(n_total=560, nc=4, seed=3, temperature=0.8, vseed=4)
     return systems.fcc_system(8, jitter=0.05, seed=21, temperature=1.2, vseed=22)
 
 
-def _worker(rank, world, port, dims, steps, s, out_dir, skin):
+def _worker(rank, world, port, dims, steps, s, out_dir, skin, kind="fcc", balance=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -43,23 +45,29 @@ def _worker(rank, world, port, dims, steps, s, out_dir, skin):
         from paper_2507_11172_b200 import ForceField, RespaSchedule
         from paper_2507_11172_b200.domain_run import domain_respa_run
 
-        sysm = _system()
+        sysm = _system(kind)
         ff = ForceField(nu=0.3, cutoff=2.5)
-        trace = domain_respa_run(dist, sysm, ff, RespaSchedule(0.002, s, steps),
-                                 lambda dec, n, rb: NumpyBackend(ff, sysm.box), skin=skin,
-                                 dims=dims)
+        seen = {}
+
+        def factory(dec, n, rb):
+            seen["dims"], seen["bounds"] = dec.dims, dec.bounds
+            return NumpyBackend(ff, sysm.box)
+
+        trace = domain_respa_run(dist, sysm, ff, RespaSchedule(0.002, s, steps), factory,
+                                 skin=skin, dims=dims, balance=balance)
         if rank == 0:
             np.savez(os.path.join(out_dir, "out.npz"), x=sysm.positions, v=sysm.velocities,
                      f2=sysm.forces_2b, f3=sysm.forces_3b, total=np.array(trace.total),
-                     it=np.array(trace.iterations))
+                     it=np.array(trace.iterations), dims=np.array(seen["dims"]),
+                     zbounds=np.array(seen["bounds"][2]))
     finally:
         dist.destroy_process_group()
 
 
-def _oracle_run(steps, s):
+def _oracle_run(steps, s, kind="fcc"):
     from oracle import oracle as o
 
-    sysm = _system()
+    sysm = _system(kind)
     osys = o.OracleSystem.from_positions(sysm.positions, sysm.box, True, sysm.velocities)
     off = o.OracleForceField(nu=0.3, cutoff=2.5)
     trace = o.respa_run(osys, off, o.OracleLinkedCells(), 0.002, s, steps)
@@ -82,6 +90,82 @@ def test_decomposed_respa_matches_single_domain(tmp_path, world, dims, skin):
     assert list(out["it"]) == list(rtrace.iterations)
     rel = np.abs(out["total"] - np.array(rtrace.total)) / np.abs(np.array(rtrace.total))
     assert np.max(rel) <= 1e-10
+
+
+def test_balanced_slab_matches_single_domain(tmp_path):
+    """Cost-aware blocks (domain.balanced_layout) on a liquid slab: the z cuts
+    crowd into the liquid, and the trajectory still equals the oracle's."""
+    world, steps, s = 4, 10, 5
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, None, steps, s, str(tmp_path), 0.3, "slab",
+                                      True), nprocs=world, join=True, start_method="spawn")
+    out = np.load(tmp_path / "out.npz")
+    assert tuple(out["dims"]) == (1, 1, 4)
+    widths = np.diff(out["zbounds"])
+    assert widths.max() > widths.min()  # uneven: thin blocks in the liquid
+    ref, rtrace = _oracle_run(steps, s, "slab")
+    assert np.max(np.abs(out["x"] - ref.positions)) <= 1e-10
+    assert np.max(np.abs(out["v"] - ref.velocities)) <= 1e-10
+    assert list(out["it"]) == list(rtrace.iterations)
+    rel = np.abs(out["total"] - np.array(rtrace.total)) / np.abs(np.array(rtrace.total))
+    assert np.max(rel) <= 1e-10
+
+
+def test_balanced_bounds_is_optimal():
+    """Exact minimax cut against brute force, with the width limits."""
+    import itertools
+
+    from paper_2507_11172_b200.domain import balanced_bounds
+
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        n = int(rng.integers(4, 11))
+        parts = int(rng.integers(1, 4))
+        prof = rng.integers(0, 6, size=n).astype(np.float64)
+        best = None
+        for cuts in itertools.combinations(range(1, n), parts - 1):
+            b = (0,) + cuts + (n,)
+            w = np.diff(b)
+            if parts > 1 and (w.min() < 1 or w.max() > n - 2):
+                continue
+            v = max(prof[b[k]:b[k + 1]].sum() for k in range(parts))
+            best = v if best is None else min(best, v)
+        if best is None:
+            with pytest.raises(ValueError):
+                balanced_bounds(prof, parts)
+            continue
+        b = balanced_bounds(prof, parts)
+        w = np.diff(b)
+        assert b[0] == 0 and b[-1] == n and w.min() >= 1
+        assert parts == 1 or w.max() <= n - 2
+        assert max(prof[b[k]:b[k + 1]].sum() for k in range(parts)) == best
+
+
+def test_balanced_layout_evens_the_slab_load():
+    from paper_2507_11172_b200 import systems
+    from paper_2507_11172_b200.domain import (Decomposition, auto_dims, balanced_layout,
+                                              block_costs, cell_costs, cell_occupancy)
+    from paper_2507_11172_b200.grid import geometry
+
+    sysm = systems.slab_system(n_total=14_000, nc=12, seed=2)
+    geom = geometry(sysm.box, None, 2.8, True)
+    occ = cell_occupancy(sysm.positions, geom)
+    costs = cell_costs(sysm.positions, geom, 0.29 / 5)
+    assert occ.sum() == sysm.positions.shape[0]
+    even = Decomposition(sysm.box, 2.8, 8, 0, auto_dims(8, geom.cells))
+    dims, bounds = balanced_layout(costs, 8, occ)
+    before = block_costs(costs, even.dims, even.bounds, occ)
+    after = block_costs(costs, dims, bounds, occ)
+    # 7 x 7 x 29 cells: whole-layer cuts limit the balance
+    assert before.max() / before.mean() > 2.0
+    assert after.max() < 0.6 * before.max() and after.max() / after.mean() < 1.3
+    # the layout is usable: every particle gets exactly one owner
+    owners = np.concatenate([np.nonzero(Decomposition(sysm.box, 2.8, 8, r, dims, bounds)
+                                        .owner_rank(sysm.positions) == r)[0] for r in range(8)])
+    assert np.array_equal(np.sort(owners), np.arange(sysm.positions.shape[0]))
+    with pytest.raises(ValueError):
+        Decomposition(sysm.box, 2.8, 2, 0, (1, 1, 2), [[0, geom.cells[0]], [0, geom.cells[1]],
+                                                       [0, 0, geom.cells[2]]])
 
 
 def test_decomposition_geometry():

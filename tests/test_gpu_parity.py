@@ -425,7 +425,13 @@ def test_container_drives_oracle_respa_loop(pkg, oracle):
     assert max(_rel(x, y) for x, y in zip(ta.total, tb.total)) <= 1e-10
 
 
-def _domain_gpu_worker(rank, world, port, dims, out_dir):
+def _domain_system(pkg, kind):
+    if kind == "slab":  # liquid block in the middle half of z, vapour outside
+        return pkg.systems.slab_system(n_total=2_400, nc=6, seed=3, temperature=0.8, vseed=4)
+    return pkg.systems.fcc_system(8, jitter=0.05, seed=21, temperature=1.2, vseed=22)
+
+
+def _domain_gpu_worker(rank, world, port, dims, out_dir, kind="fcc"):
     import os as _os
 
     import torch.distributed as dist
@@ -437,10 +443,11 @@ def _domain_gpu_worker(rank, world, port, dims, out_dir):
         import paper_2507_11172_b200 as pkg
         from paper_2507_11172_b200.domain_run import domain_respa_run, gpu_backend_factory
 
-        sysm = pkg.systems.fcc_system(8, jitter=0.05, seed=21, temperature=1.2, vseed=22)
+        sysm = _domain_system(pkg, kind)
         ff = pkg.ForceField(nu=0.3, cutoff=2.5)
         trace = domain_respa_run(dist, sysm, ff, pkg.RespaSchedule(0.002, 5, 20),
-                                 gpu_backend_factory(ff), skin=0.1, dims=dims)
+                                 gpu_backend_factory(ff), skin=0.1, dims=dims,
+                                 balance=kind == "slab")
         if rank == 0:
             np.savez(_os.path.join(out_dir, "out.npz"), x=sysm.positions, v=sysm.velocities,
                      total=np.array(trace.total))
@@ -448,12 +455,14 @@ def _domain_gpu_worker(rank, world, port, dims, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims", [(2, (2, 1, 1)), (4, (2, 1, 2))])
-def test_domain_decomposed_gpu_kernels_match_single_domain(pkg, tmp_path, world, dims):
+@pytest.mark.parametrize("world,dims,kind", [(2, (2, 1, 1), "fcc"), (4, (2, 1, 2), "fcc"),
+                                             (4, None, "slab")])
+def test_domain_decomposed_gpu_kernels_match_single_domain(pkg, tmp_path, world, dims, kind):
     """The windowed-grid kernels (block + halo binning, windowed neighbour
     cells, owned-weighted energies) on the GPU, ranks as host processes
     sharing cuda:0 and exchanging over gloo (no kernel waits on another
-    rank): trajectory equals the single-domain device run."""
+    rank): trajectory equals the single-domain device run.  The slab runs
+    with cost-aware (uneven) blocks."""
     import socket
 
     import torch.multiprocessing as mp
@@ -461,10 +470,10 @@ def test_domain_decomposed_gpu_kernels_match_single_domain(pkg, tmp_path, world,
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
-    mp.start_processes(_domain_gpu_worker, args=(world, port, dims, str(tmp_path)), nprocs=world,
-                       join=True, start_method="spawn")
+    mp.start_processes(_domain_gpu_worker, args=(world, port, dims, str(tmp_path), kind),
+                       nprocs=world, join=True, start_method="spawn")
     out = np.load(tmp_path / "out.npz")
-    ref = pkg.systems.fcc_system(8, jitter=0.05, seed=21, temperature=1.2, vseed=22)
+    ref = _domain_system(pkg, kind)
     ff = pkg.ForceField(nu=0.3, cutoff=2.5)
     tr = pkg.respa_run(ref, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 5, 20))
     assert np.max(np.abs(out["x"] - ref.positions)) <= 1e-10

@@ -206,12 +206,14 @@ class ForceEngine:
         return int(min(4096, cap, max(32, _round_up(self.n, 32))))
 
     def _ensure_rows(self, capacity: int) -> None:
+        # sized for the whole particle buffer, not the current count: a
+        # decomposed run changes n at every rebuild (set_count)
         if self.rows is None or self.capacity != capacity:
             torch = self.torch
-            self.rows = torch.zeros(max(self.n, 1) * capacity, dtype=torch.int32, device=self.device)
-            self.mirror = torch.zeros(max(self.n, 1) * capacity, dtype=torch.int32,
-                                      device=self.device)
-            need = int(self.L.rb_atm_scratch_bytes(self.n, capacity))
+            n_buf = max(int(self.pos.shape[0]), 1)
+            self.rows = torch.zeros(n_buf * capacity, dtype=torch.int32, device=self.device)
+            self.mirror = torch.zeros(n_buf * capacity, dtype=torch.int32, device=self.device)
+            need = int(self.L.rb_atm_scratch_bytes(n_buf, capacity))
             # zero-filled once: the overflow count at its tail (rb_atm_pass contract)
             self.atm_scratch = torch.zeros((need + 7) // 8, dtype=torch.float64, device=self.device)
             self.capacity = capacity

@@ -237,6 +237,33 @@ RB_API int rb_halo_pack(int64_t n, const int32_t *idx, const double *pos, double
 RB_API int rb_halo_unpack(int64_t n, const double *buf, int64_t first, double *pos,
                           const int32_t *rank_of, double *pos_r, void *stream);
 
+/* Peer-memory form (no messages): each rank publishes its owned positions
+ * from the step's drift (rb_respa_drift_publish: publish[3p..3p+2] = the
+ * drifted position of owned row p, then a system-scope fence) into one
+ * IPC-shared allocation, double buffered by step parity; after the step's
+ * rebuild vote (which orders every rank's drift before every rank's pull),
+ * rb_halo_pull reads ghost row first + i from peers[src_rank[i]] + offset +
+ * 3 src_index[i] (device array of the ranks' mapped base pointers, offset
+ * in doubles selecting the parity half) into pos and, with pos_r != NULL,
+ * pos_r[rank_of[first + i]].  Bit-identical to pack / send / unpack. */
+RB_API int rb_respa_drift_publish(int64_t n, double *pos, double *vel, const double *f2_old,
+                                  const double *f3, const double *box3_host, int32_t periodic,
+                                  double dt, double half_drift, double half_respa, int32_t kick3,
+                                  const int32_t *rank_of, double *pos_r, const double *x_ref,
+                                  double skin, int64_t *rebuild_flag, unsigned long long *status,
+                                  int64_t tag, int32_t advance_step, double *publish,
+                                  void *stream);
+RB_API int rb_halo_pull(int64_t n, const int32_t *src_rank, const int32_t *src_index,
+                        const uint64_t *peers, int64_t offset, int64_t first, double *pos,
+                        const int32_t *rank_of, double *pos_r, void *stream);
+/* CUDA IPC: a cudaMalloc'd (zeroed) allocation, its 64-byte handle, and the
+ * peer-side mapping (cudaIpcMemLazyEnablePeerAccess) / unmapping. */
+RB_API int rb_ipc_alloc(int64_t bytes, void **ptr);
+RB_API int rb_ipc_free(void *ptr);
+RB_API int rb_ipc_handle(void *ptr, uint8_t *handle64);
+RB_API int rb_ipc_open(const uint8_t *handle64, void **ptr);
+RB_API int rb_ipc_close(void *ptr);
+
 /* ---- deterministic reductions (fixed partition + fixed tree) ---------- */
 RB_API size_t rb_reduce_scratch_bytes(int64_t n);
 /* out[0] = sum(in[0..n)) */

@@ -98,6 +98,14 @@ SIGNATURES = {
     "rb_distance_histogram": (ctypes.c_int, [_I64, _P, _P, _D, _D, _I32, _P, _P]),
     "rb_halo_pack": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
     "rb_halo_unpack": (ctypes.c_int, [_I64, _P, _I64, _P, _P, _P, _P]),
+    "rb_respa_drift_publish": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _I32, _D, _D, _D, _I32,
+                                              _P, _P, _P, _D, _P, _P, _I64, _I32, _P, _P]),
+    "rb_halo_pull": (ctypes.c_int, [_I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P]),
+    "rb_ipc_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(ctypes.c_void_p)]),
+    "rb_ipc_free": (ctypes.c_int, [_P]),
+    "rb_ipc_handle": (ctypes.c_int, [_P, _P]),
+    "rb_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p)]),
+    "rb_ipc_close": (ctypes.c_int, [_P]),
     "rb_direct_pairs_range": (ctypes.c_int, [_I64, _P, _I64, _I64, _D, _D, _P, _P, _P, _P, _I64,
                                              _P]),
     "rb_direct_triplets_range": (ctypes.c_int, [_I64, _P, _I64, _I64, _D, _P, _P, _P, _SZ, _P,

@@ -266,6 +266,18 @@ class Decomposition:
             out[:, d] = np.searchsorted(self.bounds[d], cells[:, d], side="right") - 1
         return out
 
+    def window_count(self, pos: np.ndarray) -> int:
+        """Particles whose cell lies in this rank's block or halo layer
+        (owned + ghosts right after a rebuild)."""
+        c = self.cells_of(np.asarray(pos))
+        inside = np.ones(c.shape[0], dtype=bool)
+        n = self.geom.cells
+        for d in range(3):
+            if self.split(d):
+                rel = (c[:, d] - self.lo[d] + 1) % n[d]
+                inside &= rel < self.hi[d] - self.lo[d] + 2
+        return int(inside.sum())
+
     def owner_rank(self, pos: np.ndarray) -> np.ndarray:
         b = self.block_of(self.cells_of(pos))
         return (b[:, 0] * self.dims[1] + b[:, 1]) * self.dims[2] + b[:, 2]
@@ -352,6 +364,7 @@ class GhostPlan:
     stages: list  # per split dimension: (d, idx_to_minus, idx_to_plus, n_from_plus, n_from_minus)
     n_owned: int
     n_local: int
+    origin: object = None  # (n_local, 2) owner rank, owner row (build_ghosts(origin=...))
 
 
 def migrate(dec: Decomposition, ex: Exchanger, payload):
@@ -383,17 +396,22 @@ def migrate(dec: Decomposition, ex: Exchanger, payload):
     return payload[order]
 
 
-def build_ghosts(dec: Decomposition, ex: Exchanger, pos_owned):
-    """Staged ghost exchange; returns (local positions (owned first), plan)."""
+def build_ghosts(dec: Decomposition, ex: Exchanger, pos_owned, origin=None):
+    """Staged ghost exchange; returns (local positions (owned first), plan).
+
+    With `origin` ((n_own, 2) float64: owner rank, owner row per owned row)
+    the messages carry it along and the plan's `origin` holds it for every
+    local row: where a ghost's position lives at its owner (the pull lists
+    of the peer-memory refresh)."""
     import torch
 
     n_own = int(pos_owned.shape[0])
-    local = pos_owned
+    local = pos_owned if origin is None else torch.cat([pos_owned, origin], dim=1)
     stages = []
     for d in range(3):
         if not dec.split(d):
             continue
-        cells = dec.cells_of(local.cpu().numpy())[:, d]
+        cells = dec.cells_of(local[:, :3].cpu().numpy())[:, d]
         idx_m = np.nonzero(cells == dec.lo[d])[0]
         idx_p = np.nonzero(cells == dec.hi[d] - 1)[0]
         dev = local.device
@@ -403,7 +421,11 @@ def build_ghosts(dec: Decomposition, ex: Exchanger, pos_owned):
                                             dec.neighbor(d, +1))
         stages.append((d, tm, tp, int(from_plus.shape[0]), int(from_minus.shape[0])))
         local = torch.cat([local, from_plus, from_minus], dim=0)
-    return local, GhostPlan(stages, n_own, int(local.shape[0]))
+    plan = GhostPlan(stages, n_own, int(local.shape[0]))
+    if origin is not None:
+        plan.origin = local[:, 3:5]
+        local = local[:, 0:3].contiguous()
+    return local, plan
 
 
 def refresh_ghosts(dec: Decomposition, ex: Exchanger, plan: GhostPlan, local):

@@ -12,8 +12,9 @@ with the exchange of ``domain.py`` around the force passes:
              (tagged with the device step counter) checked there
 
 The force backend is the sm_100a engine (``GpuBackend``): the owned state
-lives in device buffers and each step is drift kernel -> vote (the one host
-synchronisation) -> halo refresh -> LJ [-> ATM] -> kick kernel.  The CPU
+lives in device buffers and each step is drift kernel (publishing the owned
+positions) -> vote (the one host synchronisation) -> halo refresh (one
+peer-memory pull launch, or pack / NCCL / unpack) -> LJ [-> ATM] -> kick.  The CPU
 tests plug in a numpy restatement and take the torch version of the same
 loop.
 """
@@ -36,10 +37,17 @@ from .model import triplet_cutoff
 class GpuBackend:
     """sm_100a passes and r-RESPA updates on one rank's particles."""
 
-    def __init__(self, n_max: int, ff, r_build: float):
+    def __init__(self, n_max: int, ff, r_build: float, halo: str = "peer"):
         from . import _lib
         from .engine import ForceEngine, _round_up
 
+        if halo not in ("peer", "nccl"):
+            raise ValueError(f"halo must be 'peer' or 'nccl', got {halo!r}")
+        self.halo = halo
+        self.n_max = int(n_max)
+        self._pub = None  # IPC-shared published positions (2 x stride x 3, by step parity)
+        self._opened = []
+        self._steps = 0
         self._lib = _lib
         self.eng = ForceEngine(n_max)
         self.torch = self.eng.torch
@@ -89,6 +97,54 @@ class GpuBackend:
         return self.f_local[: self.n_own].clone(), eng.scalars[3:5].clone()
 
     # ---- fused per-step primitives (the loop's fast path on the GPU) ----
+    # ---- peer-memory halo (rb_halo_pull) ----
+    def attach_peers(self, dist) -> None:
+        """Allocate this rank's published-position buffer, swap CUDA IPC
+        handles with every rank and map the peers' buffers (once)."""
+        L, torch = self.eng.L, self.torch
+        wire = torch.device("cpu") if dist.get_backend() == "gloo" else self.device
+        # one parity stride for every rank: a reader offsets into the
+        # writer's buffer
+        stride = torch.tensor([self.n_max], dtype=torch.int64, device=wire)
+        dist.all_reduce(stride, op=dist.ReduceOp.MAX)
+        self._stride = int(stride.item())
+        ptr = ctypes.c_void_p()
+        self._lib.check(L.rb_ipc_alloc(2 * self._stride * 24, ctypes.byref(ptr)), "rb_ipc_alloc")
+        self._pub = ptr.value
+        handle = np.zeros(64, dtype=np.uint8)
+        self._lib.check(L.rb_ipc_handle(self._pub, handle.ctypes.data), "rb_ipc_handle")
+        mine = torch.from_numpy(handle).to(wire)
+        every = [torch.empty_like(mine) for _ in range(dist.get_world_size())]
+        dist.all_gather(every, mine)
+        bases = []
+        for r, h in enumerate(every):
+            if r == dist.get_rank():
+                bases.append(self._pub)
+                continue
+            peer = ctypes.c_void_p()
+            h = np.ascontiguousarray(h.cpu().numpy())
+            self._lib.check(L.rb_ipc_open(h.ctypes.data, ctypes.byref(peer)), "rb_ipc_open")
+            self._opened.append(peer.value)
+            bases.append(peer.value)
+        self._peers = torch.tensor(np.array(bases, dtype=np.uint64).view(np.int64),
+                                   dtype=torch.int64, device=self.device)
+
+    def close(self, dist=None) -> None:
+        """Unmap the peers' buffers, then (after every rank did) free ours."""
+        self.torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            self.eng.L.rb_ipc_close(p)
+        self._opened = []
+        if self._pub is not None:
+            if dist is not None:
+                dist.barrier()
+            self.eng.L.rb_ipc_free(self._pub)
+            self._pub = None
+
+    @property
+    def peer(self) -> bool:
+        return self._pub is not None
+
     def bind(self, st, plan) -> None:
         """After a rebuild: the owned state moves into the device buffers and
         `st` becomes views of them (positions are eng.pos[:n_own]); the
@@ -101,12 +157,25 @@ class GpuBackend:
         i32 = self.torch.int32
         self._lists = [(d, tm.to(i32), tp.to(i32), n_fp, n_fm)
                        for d, tm, tp, n_fp, n_fm in plan.stages]
+        if self.peer:
+            ghosts = plan.origin[n:]
+            self._src_rank = ghosts[:, 0].to(i32).contiguous()
+            self._src_index = ghosts[:, 1].to(i32).contiguous()
 
     def refresh_halo(self, dec, ex) -> None:
         """Per step between rebuilds: the owners' new positions into the ghost
         rows (and their rank-order copy), stage by stage (x -> y -> z): pack
         kernel, NCCL point-to-point, unpack kernel."""
         eng, L, ptr, torch = self.eng, self.eng.L, self._lib.ptr, self.torch
+        if self.peer:
+            # every rank's publishing drift of this step finished before the
+            # rebuild vote this rank has passed: read the ghosts in place
+            n = self.n_local - self.n_own
+            self._lib.check(L.rb_halo_pull(n, ptr(self._src_rank), ptr(self._src_index),
+                                           ptr(self._peers), self._parity_offset(), self.n_own,
+                                           ptr(eng.pos), ptr(eng.rank_of), ptr(eng.pos_r),
+                                           eng.stream), "rb_halo_pull")
+            return
         at = self.n_own
         for d, tm, tp, n_fp, n_fm in self._lists:
             send = []
@@ -132,13 +201,22 @@ class GpuBackend:
         rank's rebuild vote as a 0-d device tensor."""
         eng, L = self.eng, self.eng.L
         ptr = self._lib.ptr
-        st = L.rb_respa_drift(self.n_own, ptr(eng.pos), ptr(self.v), ptr(self.f2), ptr(self.f3),
-                              box.ctypes.data_as(ctypes.c_void_p), 1, dt, half_drift, half_respa,
-                              int(kick3), ptr(eng.rank_of), ptr(eng.pos_r), ptr(eng.x_ref), skin,
-                              ptr(eng.rebuild_flag), ptr(eng.status),
-                              self._lib.RB_TAG_FROM_DEVICE, 1, 0, eng.stream)
+        self._steps += 1
+        args = (self.n_own, ptr(eng.pos), ptr(self.v), ptr(self.f2), ptr(self.f3),
+                box.ctypes.data_as(ctypes.c_void_p), 1, dt, half_drift, half_respa, int(kick3),
+                ptr(eng.rank_of), ptr(eng.pos_r), ptr(eng.x_ref), skin, ptr(eng.rebuild_flag),
+                ptr(eng.status), self._lib.RB_TAG_FROM_DEVICE, 1)
+        if self.peer:  # also publish the drifted owned rows for the peers' pulls
+            st = L.rb_respa_drift_publish(*args, self._pub + 8 * self._parity_offset(),
+                                          eng.stream)
+        else:
+            st = L.rb_respa_drift(*args, 0, eng.stream)
         self._lib.check(st, "rb_respa_drift")
         return eng.rebuild_flag[0] == eng.status[1]
+
+    def _parity_offset(self) -> int:
+        """Doubles from the buffer base to this step's half (step parity)."""
+        return (self._steps & 1) * 3 * self._stride
 
     def pair_into_new(self, scalars: bool):
         eng = self.eng
@@ -224,6 +302,7 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
                                       int(dims[d])) for d in range(3)]
     dec = Decomposition(box, r_build, world, rank, dims, bounds)
     n_total = system.positions.shape[0]
+    dec.local_estimate = dec.window_count(system.positions)
     backend = backend_factory(dec, n_total, r_build)
     dev = backend.device if device is None else device
     ex = Exchanger(dist, dev)
@@ -244,6 +323,9 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     # state (one host synchronisation per step: the rebuild vote); other
     # backends (the numpy one of the CPU tests) take the torch restatement
     fast = hasattr(backend, "bind")
+    peer = fast and world > 1 and getattr(backend, "halo", None) == "peer"
+    if peer:
+        backend.attach_peers(dist)
 
     def rebuild():
         nonlocal window
@@ -256,7 +338,14 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
         else:
             st.f2 = torch.zeros_like(st.x)
             st.f3 = torch.zeros_like(st.x)
-        local, plan = build_ghosts(dec, ex, st.x)
+        origin = None
+        if peer:
+            n_own = int(st.x.shape[0])
+            origin = torch.stack([torch.full((n_own,), float(rank), dtype=torch.float64,
+                                             device=st.x.device),
+                                  torch.arange(n_own, dtype=torch.float64, device=st.x.device)],
+                                 dim=1)
+        local, plan = build_ghosts(dec, ex, st.x, origin)
         backend.set_local(local, plan.n_owned, window, rebuild=True)
         if fast:
             backend.bind(st, plan)
@@ -312,69 +401,80 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
                 reason = "error on another rank"
             raise IntegrationBlowUp(it, reason, trace)
 
-    local, plan = rebuild()
-    if fast:
-        e2w2 = backend.pair_into_new(True)
-        st.f2.copy_(backend.f2_new[: plan.n_owned])
-        e3w3 = backend.triplet_into_f3(True)
-    else:
-        f2, e2w2 = backend.pair()
-        f3, e3w3 = backend.triplet()
-        st.f2, st.f3 = f2, f3
-    check(0)
-    record(0, e2w2, e3w3)
-    half_skin2 = (0.5 * skin) ** 2 * (1.0 - 1e-9)
-    for i in range(schedule.num_iterations):
-        if on_step is not None:
-            on_step(i)
-        sample = (i + 1) % interval == 0
-        end_of_cycle = (i + 1) % s == 0
+    clean = False
+    try:
+        local, plan = rebuild()
         if fast:
-            moved = backend.drift(box, dt, half_drift, half_respa, i % s == 0, skin)
-            if any_flag(moved if skin > 0.0 else True):
+            e2w2 = backend.pair_into_new(True)
+            st.f2.copy_(backend.f2_new[: plan.n_owned])
+            e3w3 = backend.triplet_into_f3(True)
+        else:
+            f2, e2w2 = backend.pair()
+            f3, e3w3 = backend.triplet()
+            st.f2, st.f3 = f2, f3
+        check(0)
+        record(0, e2w2, e3w3)
+        half_skin2 = (0.5 * skin) ** 2 * (1.0 - 1e-9)
+        for i in range(schedule.num_iterations):
+            if on_step is not None:
+                on_step(i)
+            sample = (i + 1) % interval == 0
+            end_of_cycle = (i + 1) % s == 0
+            if fast:
+                moved = backend.drift(box, dt, half_drift, half_respa, i % s == 0, skin)
+                if any_flag(moved if skin > 0.0 else True):
+                    local, plan = rebuild()
+                else:
+                    backend.refresh_halo(dec, ex)
+                e2w2 = backend.pair_into_new(sample)
+                if end_of_cycle:
+                    e3w3 = backend.triplet_into_f3(sample)
+                backend.kick(half_dt, half_respa, end_of_cycle)
+                if sample:
+                    check(i + 1)
+                    record(i + 1, e2w2, e3w3)
+                continue
+            if hasattr(backend, "advance"):
+                backend.advance()
+            if i % s == 0:
+                st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
+            st.x = st.x + ((dt * st.v) + (half_drift * st.f2))
+            st.x = torch.remainder(st.x, box_t)  # numpy mod semantics for box > 0
+            st.x = torch.where(st.x >= box_t, torch.zeros_like(st.x), st.x)
+            if skin == 0.0 or st.x.shape[0] == 0:
+                moved = skin == 0.0
+            else:
+                d = st.x - st.x_ref
+                d = d - box_t * torch.where(d > 0.5 * box_t, 1.0, torch.where(d < -0.5 * box_t, -1.0, 0.0))
+                moved = ((d * d).sum(dim=1).max() > half_skin2)
+            if any_flag(moved):
                 local, plan = rebuild()
             else:
-                backend.refresh_halo(dec, ex)
-            e2w2 = backend.pair_into_new(sample)
-            if end_of_cycle:
-                e3w3 = backend.triplet_into_f3(sample)
-            backend.kick(half_dt, half_respa, end_of_cycle)
+                refresh(plan, local)
+            f2_new, e2w2 = backend.pair(scalars=sample)
+            st.v = st.v + (half_dt * (st.f2 + f2_new))
+            st.f2 = f2_new
+            if (i + 1) % s == 0:
+                st.f3, e3w3 = backend.triplet(scalars=sample)
+                st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
+            finite = torch.isfinite(st.x).all() & torch.isfinite(st.v).all()
+            first_bad = torch.where(finite | (first_bad <= i), first_bad,
+                                    torch.full_like(first_bad, i + 1))
             if sample:
                 check(i + 1)
                 record(i + 1, e2w2, e3w3)
-            continue
-        if hasattr(backend, "advance"):
-            backend.advance()
-        if i % s == 0:
-            st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
-        st.x = st.x + ((dt * st.v) + (half_drift * st.f2))
-        st.x = torch.remainder(st.x, box_t)  # numpy mod semantics for box > 0
-        st.x = torch.where(st.x >= box_t, torch.zeros_like(st.x), st.x)
-        if skin == 0.0 or st.x.shape[0] == 0:
-            moved = skin == 0.0
-        else:
-            d = st.x - st.x_ref
-            d = d - box_t * torch.where(d > 0.5 * box_t, 1.0, torch.where(d < -0.5 * box_t, -1.0, 0.0))
-            moved = ((d * d).sum(dim=1).max() > half_skin2)
-        if any_flag(moved):
-            local, plan = rebuild()
-        else:
-            refresh(plan, local)
-        f2_new, e2w2 = backend.pair(scalars=sample)
-        st.v = st.v + (half_dt * (st.f2 + f2_new))
-        st.f2 = f2_new
-        if (i + 1) % s == 0:
-            st.f3, e3w3 = backend.triplet(scalars=sample)
-            st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
-        finite = torch.isfinite(st.x).all() & torch.isfinite(st.v).all()
-        first_bad = torch.where(finite | (first_bad <= i), first_bad,
-                                torch.full_like(first_bad, i + 1))
-        if sample:
-            check(i + 1)
-            record(i + 1, e2w2, e3w3)
-    if on_step is not None:
-        on_step(schedule.num_iterations)
-    check(schedule.num_iterations)
+        if on_step is not None:
+            on_step(schedule.num_iterations)
+        check(schedule.num_iterations)
+        clean = True
+    except IntegrationBlowUp:
+        clean = True
+        raise
+    finally:
+        if peer:
+            # collective only when every rank got here (blow-ups are raised
+            # by the collective check, so they count as clean)
+            backend.close(dist if clean else None)
 
     # gather the owned state of every rank into the host system (by id)
     parts = [None] * world
@@ -393,12 +493,23 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     return trace
 
 
-def gpu_backend_factory(ff, headroom: float = 1.6):
-    """Backend factory for domain_respa_run on the local CUDA device."""
+def gpu_backend_factory(ff, headroom: float = 1.6, halo: Optional[str] = None):
+    """Backend factory for domain_respa_run on the local CUDA device.
+
+    `halo`: "peer" (default; env RB_HALO) refreshes ghosts from the owners'
+    published positions over CUDA IPC peer memory, "nccl" with pack /
+    point-to-point / unpack.  Buffers are sized from the rank's initial
+    window population (`dec.local_estimate`, set by domain_respa_run)."""
+    import os
+
+    mode = halo or os.environ.get("RB_HALO", "peer")
 
     def make(dec: Decomposition, n_total: int, r_build: float):
-        n_max = int(headroom * n_total / dec.world * _ghost_factor(dec, r_build)) + 1024
-        return GpuBackend(min(n_max, n_total * 2 + 1024), ff, r_build)
+        est = getattr(dec, "local_estimate", None)
+        if est is None:
+            est = n_total / dec.world * _ghost_factor(dec, r_build)
+        n_max = int(headroom * est) + 1024
+        return GpuBackend(min(n_max, n_total * 2 + 1024), ff, r_build, halo=mode)
 
     return make
 

@@ -431,7 +431,7 @@ def _domain_system(pkg, kind):
     return pkg.systems.fcc_system(8, jitter=0.05, seed=21, temperature=1.2, vseed=22)
 
 
-def _domain_gpu_worker(rank, world, port, dims, out_dir, kind="fcc"):
+def _domain_gpu_worker(rank, world, port, dims, out_dir, kind="fcc", halo="peer"):
     import os as _os
 
     import torch.distributed as dist
@@ -446,23 +446,16 @@ def _domain_gpu_worker(rank, world, port, dims, out_dir, kind="fcc"):
         sysm = _domain_system(pkg, kind)
         ff = pkg.ForceField(nu=0.3, cutoff=2.5)
         trace = domain_respa_run(dist, sysm, ff, pkg.RespaSchedule(0.002, 5, 20),
-                                 gpu_backend_factory(ff), skin=0.1, dims=dims,
+                                 gpu_backend_factory(ff, halo=halo), skin=0.1, dims=dims,
                                  balance=kind == "slab")
         if rank == 0:
-            np.savez(_os.path.join(out_dir, "out.npz"), x=sysm.positions, v=sysm.velocities,
-                     total=np.array(trace.total))
+            np.savez(_os.path.join(out_dir, f"out_{halo}.npz"), x=sysm.positions,
+                     v=sysm.velocities, total=np.array(trace.total))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims,kind", [(2, (2, 1, 1), "fcc"), (4, (2, 1, 2), "fcc"),
-                                             (4, None, "slab")])
-def test_domain_decomposed_gpu_kernels_match_single_domain(pkg, tmp_path, world, dims, kind):
-    """The windowed-grid kernels (block + halo binning, windowed neighbour
-    cells, owned-weighted energies) on the GPU, ranks as host processes
-    sharing cuda:0 and exchanging over gloo (no kernel waits on another
-    rank): trajectory equals the single-domain device run.  The slab runs
-    with cost-aware (uneven) blocks."""
+def _run_domain_gpu(tmp_path, world, dims, kind, halo):
     import socket
 
     import torch.multiprocessing as mp
@@ -470,15 +463,36 @@ def test_domain_decomposed_gpu_kernels_match_single_domain(pkg, tmp_path, world,
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
-    mp.start_processes(_domain_gpu_worker, args=(world, port, dims, str(tmp_path), kind),
+    mp.start_processes(_domain_gpu_worker, args=(world, port, dims, str(tmp_path), kind, halo),
                        nprocs=world, join=True, start_method="spawn")
-    out = np.load(tmp_path / "out.npz")
+    return np.load(tmp_path / f"out_{halo}.npz")
+
+
+@pytest.mark.parametrize("world,dims,kind", [(2, (2, 1, 1), "fcc"), (4, (2, 1, 2), "fcc"),
+                                             (4, None, "slab")])
+def test_domain_decomposed_gpu_kernels_match_single_domain(pkg, tmp_path, world, dims, kind):
+    """The windowed-grid kernels (block + halo binning, windowed neighbour
+    cells, owned-weighted energies) on the GPU, ranks as host processes
+    sharing cuda:0 (votes over gloo, ghosts pulled from the owners' published
+    positions through CUDA IPC; no kernel waits on another rank): trajectory
+    equals the single-domain device run.  The slab runs with cost-aware
+    (uneven) blocks."""
+    out = _run_domain_gpu(tmp_path, world, dims, kind, "peer")
     ref = _domain_system(pkg, kind)
     ff = pkg.ForceField(nu=0.3, cutoff=2.5)
     tr = pkg.respa_run(ref, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 5, 20))
     assert np.max(np.abs(out["x"] - ref.positions)) <= 1e-10
     assert np.max(np.abs(out["v"] - ref.velocities)) <= 1e-10
     assert max(_rel(a, b) for a, b in zip(out["total"], tr.total)) <= 1e-10
+
+
+def test_domain_peer_halo_equals_message_halo(pkg, tmp_path):
+    """The peer-memory ghost refresh (rb_respa_drift_publish + rb_halo_pull)
+    and pack / point-to-point / unpack move the same bits."""
+    a = _run_domain_gpu(tmp_path, 4, (2, 2, 1), "fcc", "peer")
+    b = _run_domain_gpu(tmp_path, 4, (2, 2, 1), "fcc", "nccl")
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["v"], b["v"])
+    assert np.array_equal(a["total"], b["total"])
 
 
 def test_kick_folded_into_drift_is_bit_identical(pkg, monkeypatch):

@@ -238,24 +238,27 @@ RB_API int rb_halo_unpack(int64_t n, const double *buf, int64_t first, double *p
                           const int32_t *rank_of, double *pos_r, void *stream);
 
 /* Peer-memory form (no messages): each rank publishes its owned positions
- * from the step's drift (rb_respa_drift_publish: publish[3p..3p+2] = the
- * drifted position of owned row p, then a system-scope fence) into one
- * IPC-shared allocation, double buffered by step parity; after the step's
+ * from the step's drift (rb_respa_drift_publish, advance_step only: row p
+ * of the half (tag & 1) of `publish`, halves `stride` rows apart, then a
+ * system-scope fence) into one IPC-shared allocation; after the step's
  * rebuild vote (which orders every rank's drift before every rank's pull),
- * rb_halo_pull reads ghost row first + i from peers[src_rank[i]] + offset +
- * 3 src_index[i] (device array of the ranks' mapped base pointers, offset
- * in doubles selecting the parity half) into pos and, with pos_r != NULL,
- * pos_r[rank_of[first + i]].  Bit-identical to pack / send / unpack. */
+ * rb_halo_pull reads ghost row first + i from row src_index[i] of the half
+ * (status[1] & 1) of peers[src_rank[i]] (device array of the ranks' mapped
+ * base pointers, all with the same `stride`) into pos and, with
+ * pos_r != NULL, pos_r[rank_of[first + i]].  The parity comes from the
+ * device step counter, so a captured step replays at either parity.
+ * Bit-identical to pack / send / unpack. */
 RB_API int rb_respa_drift_publish(int64_t n, double *pos, double *vel, const double *f2_old,
                                   const double *f3, const double *box3_host, int32_t periodic,
                                   double dt, double half_drift, double half_respa, int32_t kick3,
                                   const int32_t *rank_of, double *pos_r, const double *x_ref,
                                   double skin, int64_t *rebuild_flag, unsigned long long *status,
                                   int64_t tag, int32_t advance_step, double *publish,
-                                  void *stream);
+                                  int64_t stride, void *stream);
 RB_API int rb_halo_pull(int64_t n, const int32_t *src_rank, const int32_t *src_index,
-                        const uint64_t *peers, int64_t offset, int64_t first, double *pos,
-                        const int32_t *rank_of, double *pos_r, void *stream);
+                        const uint64_t *peers, int64_t stride, const unsigned long long *status,
+                        int64_t first, double *pos, const int32_t *rank_of, double *pos_r,
+                        void *stream);
 /* CUDA IPC: a cudaMalloc'd (zeroed) allocation, its 64-byte handle, and the
  * peer-side mapping (cudaIpcMemLazyEnablePeerAccess) / unmapping. */
 RB_API int rb_ipc_alloc(int64_t bytes, void **ptr);
@@ -344,6 +347,17 @@ RB_API int rb_trace_record(const unsigned long long *status, int64_t sample_inte
 RB_API int rb_rebuild_cond_create(void *stream, uint64_t *handle);
 RB_API int rb_rebuild_cond_begin(uint64_t handle, void *stream, void **body_stream);
 RB_API int rb_rebuild_cond_end(void *stream);
+
+/* Reusable captured step graphs (the domain loop's step kinds, recaptured
+ * at every row rebuild): rb_graph_begin starts a thread-local capture on a
+ * non-default stream; rb_graph_end ends it and instantiates into *exec, or,
+ * when *exec already holds an executable, updates it in place
+ * (cudaGraphExecUpdate; re-instantiates if the topology changed);
+ * rb_graph_launch / rb_graph_destroy. */
+RB_API int rb_graph_begin(void *stream);
+RB_API int rb_graph_end(void *stream, uint64_t *exec);
+RB_API int rb_graph_launch(uint64_t exec, void *stream);
+RB_API int rb_graph_destroy(uint64_t exec);
 
 /* One sample point of the device loop in a single launch: sums[0..4] =
  * (sum v^2 over the 3n velocity components, sum E2, W2, E3, W3 over the n

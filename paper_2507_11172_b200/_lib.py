@@ -99,8 +99,9 @@ SIGNATURES = {
     "rb_halo_pack": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
     "rb_halo_unpack": (ctypes.c_int, [_I64, _P, _I64, _P, _P, _P, _P]),
     "rb_respa_drift_publish": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _I32, _D, _D, _D, _I32,
-                                              _P, _P, _P, _D, _P, _P, _I64, _I32, _P, _P]),
-    "rb_halo_pull": (ctypes.c_int, [_I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P]),
+                                              _P, _P, _P, _D, _P, _P, _I64, _I32, _P, _I64,
+                                              _P]),
+    "rb_halo_pull": (ctypes.c_int, [_I64, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P]),
     "rb_ipc_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(ctypes.c_void_p)]),
     "rb_ipc_free": (ctypes.c_int, [_P]),
     "rb_ipc_handle": (ctypes.c_int, [_P, _P]),
@@ -115,6 +116,10 @@ SIGNATURES = {
     "rb_rebuild_cond_create": (ctypes.c_int, [_P, _P]),
     "rb_rebuild_cond_begin": (ctypes.c_int, [_U64, _P, _P]),
     "rb_rebuild_cond_end": (ctypes.c_int, [_P]),
+    "rb_graph_begin": (ctypes.c_int, [_P]),
+    "rb_graph_end": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+    "rb_graph_launch": (ctypes.c_int, [_U64, _P]),
+    "rb_graph_destroy": (ctypes.c_int, [_U64]),
 }
 
 _lib = None

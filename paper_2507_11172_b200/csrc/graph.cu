@@ -81,3 +81,56 @@ extern "C" int rb_rebuild_cond_end(void *stream) {
         return RB_ERR_CUDA;
     return RB_OK;
 }
+
+// ---- reusable step graphs (domain loop) ---------------------
+// A decomposed run captures one graph per step kind for every row epoch
+// (counts and lists change at each rebuild, the kernel sequence does not):
+// rb_graph_end instantiates the first capture and afterwards updates the
+// existing executable in place (cudaGraphExecUpdate, falling back to a new
+// instantiation if the topology changed), which costs a fraction of an
+// instantiation.  Thread-local capture mode: other host threads (e.g. a
+// communication library's watchdog) do not invalidate it.
+extern "C" int rb_graph_begin(void *stream) {
+    if (!stream) return RB_ERR_ARGUMENT;  // the legacy default stream cannot capture
+    return cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal) ==
+                   cudaSuccess
+               ? RB_OK : RB_ERR_CUDA;
+}
+
+extern "C" int rb_graph_end(void *stream, uint64_t *exec) {
+    if (!stream || !exec) return RB_ERR_ARGUMENT;
+    cudaGraph_t g = nullptr;
+    if (cudaStreamEndCapture(as_stream(stream), &g) != cudaSuccess || !g) return RB_ERR_CUDA;
+    cudaGraphExec_t ex = reinterpret_cast<cudaGraphExec_t>(*exec);
+    bool ok = false;
+    if (ex) {
+        cudaGraphExecUpdateResultInfo info;
+        ok = cudaGraphExecUpdate(ex, g, &info) == cudaSuccess;
+        if (!ok) {
+            (void)cudaGetLastError();
+            cudaGraphExecDestroy(ex);
+            ex = nullptr;
+        }
+    }
+    if (!ok) ok = cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    cudaGraphDestroy(g);
+    if (!ok) {
+        *exec = 0;
+        return RB_ERR_CUDA;
+    }
+    *exec = reinterpret_cast<uint64_t>(ex);
+    return RB_OK;
+}
+
+extern "C" int rb_graph_launch(uint64_t exec, void *stream) {
+    if (!exec) return RB_ERR_ARGUMENT;
+    return cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(exec), as_stream(stream)) ==
+                   cudaSuccess
+               ? RB_OK : RB_ERR_CUDA;
+}
+
+extern "C" int rb_graph_destroy(uint64_t exec) {
+    if (!exec) return RB_OK;
+    return cudaGraphExecDestroy(reinterpret_cast<cudaGraphExec_t>(exec)) == cudaSuccess
+               ? RB_OK : RB_ERR_CUDA;
+}

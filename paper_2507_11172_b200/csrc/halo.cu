@@ -48,17 +48,21 @@ __global__ void k_halo_unpack(int64_t n, const double *__restrict__ buf, int64_t
 // NVLink / NVSwitch with CUDA IPC), one thread per ghost row.  The
 // publishing drift of every rank completed before the step's rebuild vote,
 // which every rank passes before launching this kernel; the copy is double
-// buffered by step parity so an owner's next drift cannot overwrite what a
-// slower peer still reads.
+// buffered by the parity of the device step counter (status[1]) so an
+// owner's next drift cannot overwrite what a slower peer still reads, and a
+// captured step replays at either parity.
 __global__ void k_halo_pull(int64_t n, const int32_t *__restrict__ src_rank,
                             const int32_t *__restrict__ src_index,
-                            const unsigned long long *__restrict__ peers, int64_t offset,
-                            int64_t first, double *__restrict__ pos,
-                            const int32_t *__restrict__ rank_of, double *__restrict__ pos_r) {
+                            const unsigned long long *__restrict__ peers, int64_t stride,
+                            const unsigned long long *__restrict__ status, int64_t first,
+                            double *__restrict__ pos, const int32_t *__restrict__ rank_of,
+                            double *__restrict__ pos_r) {
     pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double *src = reinterpret_cast<const double *>(peers[src_rank[i]]) + offset +
+    // the half the owners' drifts of this step (status[1]) published into
+    const int64_t half = (int64_t)(status[1] & 1ull) * 3 * stride;
+    const double *src = reinterpret_cast<const double *>(peers[src_rank[i]]) + half +
                         3 * (int64_t)src_index[i];
     const double x = __ldcv(src), y = __ldcv(src + 1), z = __ldcv(src + 2);
     const int64_t p = first + i;
@@ -78,15 +82,16 @@ __global__ void k_halo_pull(int64_t n, const int32_t *__restrict__ src_rank,
 using namespace rb;
 
 extern "C" int rb_halo_pull(int64_t n, const int32_t *src_rank, const int32_t *src_index,
-                            const uint64_t *peers, int64_t offset, int64_t first, double *pos,
+                            const uint64_t *peers, int64_t stride,
+                            const unsigned long long *status, int64_t first, double *pos,
                             const int32_t *rank_of, double *pos_r, void *stream) {
-    if (n < 0 || first < 0 || offset < 0 ||
-        (n > 0 && (!src_rank || !src_index || !peers || !pos || (pos_r && !rank_of))))
+    if (n < 0 || first < 0 || stride < 0 ||
+        (n > 0 && (!src_rank || !src_index || !peers || !status || !pos || (pos_r && !rank_of))))
         return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     launch(k_halo_pull, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, as_stream(stream), n,
-           src_rank, src_index, reinterpret_cast<const unsigned long long *>(peers), offset,
-           first, pos, rank_of, pos_r);
+           src_rank, src_index, reinterpret_cast<const unsigned long long *>(peers), stride,
+           status, first, pos, rank_of, pos_r);
     note_launches(1);
     return launch_status();
 }

@@ -55,7 +55,7 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
                         int64_t *rebuild_flag, unsigned long long *status, int64_t tag,
                         int advance, cudaGraphConditionalHandle cond,
                         const double *__restrict__ f2_new, double half_dt, int kick_prev,
-                        int kick3_prev, double *__restrict__ publish) {
+                        int kick3_prev, double *__restrict__ publish, int64_t pub_stride) {
     pdl_enter();
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // a step-opening drift numbers its step from the last CLOSED step
@@ -120,10 +120,12 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
             pr[3 * r + 1] = x[1];
             pr[3 * r + 2] = x[2];
         }
-        if (publish) {  // the copy peers pull their ghosts from (rb_halo_pull)
-            publish[3 * p] = x[0];
-            publish[3 * p + 1] = x[1];
-            publish[3 * p + 2] = x[2];
+        if (publish) {  // the copy peers pull their ghosts from (rb_halo_pull),
+                        // the half of this step's parity
+            double *out = publish + (tag & 1) * 3 * pub_stride;
+            out[3 * p] = x[0];
+            out[3 * p + 1] = x[1];
+            out[3 * p + 2] = x[2];
             __threadfence_system();
         }
         if (x_ref && rebuild_flag) {
@@ -375,7 +377,8 @@ static int drift_launch(int64_t n, double *pos, double *vel, double *f2_old, con
                         int32_t kick_prev, int32_t kick3_prev, const int32_t *rank_of,
                         double *pos_r, const double *x_ref, double skin, int64_t *rebuild_flag,
                         unsigned long long *status, int64_t tag, int32_t advance_step,
-                        uint64_t rebuild_cond, void *stream, double *publish = nullptr) {
+                        uint64_t rebuild_cond, void *stream, double *publish = nullptr,
+                        int64_t pub_stride = 0) {
     if (n < 0 || !box3_host) return RB_ERR_ARGUMENT;
     if (advance_step && (!status || tag >= 0)) return RB_ERR_ARGUMENT;
     if (n == 0) return advance_step ? rb_step_begin(status, stream) : RB_OK;
@@ -385,7 +388,7 @@ static int drift_launch(int64_t n, double *pos, double *vel, double *f2_old, con
            vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt, half_drift,
            half_respa, kick3, rank_of, pos_r, x_ref, half * half * (1.0 - 1e-9), rebuild_flag,
            status, tag, advance_step ? 1 : 0, (cudaGraphConditionalHandle)rebuild_cond, f2_new,
-           half_dt, kick_prev ? 1 : 0, kick3_prev ? 1 : 0, publish);
+           half_dt, kick_prev ? 1 : 0, kick3_prev ? 1 : 0, publish, pub_stride);
     note_launches(1);
     return launch_status();
 }
@@ -409,11 +412,13 @@ extern "C" int rb_respa_drift_publish(int64_t n, double *pos, double *vel, const
                                       int32_t kick3, const int32_t *rank_of, double *pos_r,
                                       const double *x_ref, double skin, int64_t *rebuild_flag,
                                       unsigned long long *status, int64_t tag,
-                                      int32_t advance_step, double *publish, void *stream) {
-    if (!publish) return RB_ERR_ARGUMENT;
+                                      int32_t advance_step, double *publish, int64_t stride,
+                                      void *stream) {
+    if (!publish || stride < n || !advance_step) return RB_ERR_ARGUMENT;
     return drift_launch(n, pos, vel, const_cast<double *>(f2_old), nullptr, f3, box3_host,
                         periodic, dt, 0.0, half_drift, half_respa, kick3, 0, 0, rank_of, pos_r,
-                        x_ref, skin, rebuild_flag, status, tag, advance_step, 0, stream, publish);
+                        x_ref, skin, rebuild_flag, status, tag, advance_step, 0, stream, publish,
+                        stride);
 }
 
 extern "C" int rb_respa_kick_drift(int64_t n, double *pos, double *vel, double *f2_old,

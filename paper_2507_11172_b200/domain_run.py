@@ -46,8 +46,8 @@ class GpuBackend:
         self.halo = halo
         self.n_max = int(n_max)
         self._pub = None  # IPC-shared published positions (2 x stride x 3, by step parity)
+        self._graphs, self._fresh = {}, set()  # step kind -> graph executable (this epoch: fresh)
         self._opened = []
-        self._steps = 0
         self._lib = _lib
         self.eng = ForceEngine(n_max)
         self.torch = self.eng.torch
@@ -65,6 +65,7 @@ class GpuBackend:
         # device-resident owned state (particle order, owned rows first): the
         # fused drift / kick kernels update it in place between rebuilds
         self.v, self.f2, self.f2_new, self.f3 = z(), z(), z(), z()
+        self._zero2 = self.torch.zeros(2, dtype=self.torch.float64, device=self.device)
         self.eng.reset_status(0)
 
     def set_local(self, local, n_own: int, window, rebuild: bool) -> None:
@@ -154,6 +155,7 @@ class GpuBackend:
             buf[:n] = getattr(st, name)
             setattr(st, name, buf[:n])
         st.x = self.eng.pos[:n]
+        self.v[n:self.n_local].zero_()  # rb_sample sums v^2 over the local rows
         i32 = self.torch.int32
         self._lists = [(d, tm.to(i32), tp.to(i32), n_fp, n_fm)
                        for d, tm, tp, n_fp, n_fm in plan.stages]
@@ -172,9 +174,9 @@ class GpuBackend:
             # rebuild vote this rank has passed: read the ghosts in place
             n = self.n_local - self.n_own
             self._lib.check(L.rb_halo_pull(n, ptr(self._src_rank), ptr(self._src_index),
-                                           ptr(self._peers), self._parity_offset(), self.n_own,
-                                           ptr(eng.pos), ptr(eng.rank_of), ptr(eng.pos_r),
-                                           eng.stream), "rb_halo_pull")
+                                           ptr(self._peers), self._stride, ptr(eng.status),
+                                           self.n_own, ptr(eng.pos), ptr(eng.rank_of),
+                                           ptr(eng.pos_r), eng.stream), "rb_halo_pull")
             return
         at = self.n_own
         for d, tm, tp, n_fp, n_fm in self._lists:
@@ -197,26 +199,83 @@ class GpuBackend:
 
     def drift(self, box, dt, half_drift, half_respa, kick3: bool, skin: float):
         """kick3 / drift / wrap of the owned rows, their rank-order copy and
-        the skin check (rb_respa_drift, opening the device step); returns the
-        rank's rebuild vote as a 0-d device tensor."""
+        the skin check (rb_respa_drift, opening the device step; `moved`
+        reads the vote)."""
         eng, L = self.eng, self.eng.L
         ptr = self._lib.ptr
-        self._steps += 1
         args = (self.n_own, ptr(eng.pos), ptr(self.v), ptr(self.f2), ptr(self.f3),
                 box.ctypes.data_as(ctypes.c_void_p), 1, dt, half_drift, half_respa, int(kick3),
                 ptr(eng.rank_of), ptr(eng.pos_r), ptr(eng.x_ref), skin, ptr(eng.rebuild_flag),
                 ptr(eng.status), self._lib.RB_TAG_FROM_DEVICE, 1)
         if self.peer:  # also publish the drifted owned rows for the peers' pulls
-            st = L.rb_respa_drift_publish(*args, self._pub + 8 * self._parity_offset(),
-                                          eng.stream)
+            st = L.rb_respa_drift_publish(*args, self._pub, self._stride, eng.stream)
         else:
             st = L.rb_respa_drift(*args, 0, eng.stream)
         self._lib.check(st, "rb_respa_drift")
-        return eng.rebuild_flag[0] == eng.status[1]
 
-    def _parity_offset(self) -> int:
-        """Doubles from the buffer base to this step's half (step parity)."""
-        return (self._steps & 1) * 3 * self._stride
+    def moved(self):
+        """This rank's rebuild vote for the drifted step (0-d device tensor)."""
+        return self.eng.rebuild_flag[0] == self.eng.status[1]
+
+    # ---- device trace and captured steps ----
+    def trace_setup(self, rows: int, interval: int) -> None:
+        """Device trace rows [tag, sum v^2, E2, W2, E3, W3, 0, 0] of this
+        rank's partial sums, written by `sample` (rb_sample)."""
+        self.trace = self.torch.zeros((rows, 8), dtype=self.torch.float64, device=self.device)
+        self.interval = int(interval)
+
+    def sample(self) -> None:
+        """Trace row of the current device step (owned velocities; velocity
+        rows past the owned ones are kept zero by bind)."""
+        self.eng.sample(self.v, self.trace, self.interval)
+
+    def step_body(self, end_of_cycle: bool, sample: bool, pull: bool, drift_next, kick_args):
+        """Step i after its drift and vote: [ghost pull] -> LJ -> [ATM] ->
+        kick -> [trace row] -> [drift of step i + 1]; `drift_next` = None or
+        the drift arguments.  Launch-only: capturable."""
+        if pull:
+            self.refresh_halo(None, None)
+        self.pair_into_new(False)
+        if end_of_cycle:
+            self.triplet_into_f3(False)
+        self.kick(*kick_args, end_of_cycle)
+        if sample:
+            self.sample()
+        if drift_next is not None:
+            self.drift(*drift_next)
+
+    def invalidate_graphs(self) -> None:
+        """A rebuild changed counts and lists: every step kind is recaptured
+        at its next use (into its existing executable: rb_graph_end updates)."""
+        self._fresh = set()
+
+    def replay(self, key, body) -> None:
+        """Launch the captured graph of a step kind of the current row epoch
+        (captured on first use in the epoch)."""
+        torch, L = self.torch, self.eng.L
+        cur = torch.cuda.current_stream()
+        if key not in self._fresh:
+            side = self._side = getattr(self, "_side", None) or torch.cuda.Stream()
+            side.wait_stream(cur)
+            h = ctypes.c_void_p(side.cuda_stream)
+            exe = ctypes.c_uint64(self._graphs.get(key, 0))
+            with torch.cuda.stream(side):
+                self._lib.check(L.rb_graph_begin(h), "rb_graph_begin")
+                try:
+                    body()
+                finally:
+                    st = L.rb_graph_end(h, ctypes.byref(exe))
+                self._lib.check(st, "rb_graph_end")
+            cur.wait_stream(side)
+            self._graphs[key] = exe.value
+            self._fresh.add(key)
+        self._lib.check(L.rb_graph_launch(self._graphs[key], ctypes.c_void_p(cur.cuda_stream)),
+                        "rb_graph_launch")
+
+    def destroy_graphs(self) -> None:
+        for exe in self._graphs.values():
+            self.eng.L.rb_graph_destroy(exe)
+        self._graphs, self._fresh = {}, set()
 
     def pair_into_new(self, scalars: bool):
         eng = self.eng
@@ -228,7 +287,7 @@ class GpuBackend:
         eng = self.eng
         if float(self.ff.nu) == 0.0:
             self.f3.zero_()
-            return self.torch.zeros(2, dtype=self.torch.float64, device=self.device)
+            return self._zero2
         eng.atm(self.window, self.rc3, float(self.ff.nu), self.f3,
                 tag=self._lib.RB_TAG_FROM_DEVICE, count_visits=False, reduce=scalars)
         return eng.scalars[3:5]
@@ -372,6 +431,8 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     def any_flag(flag) -> bool:
         """Global OR of a per-rank flag (python bool or 0-d device tensor):
         one all_reduce and the step's single host synchronisation."""
+        if world == 1:
+            return bool(flag)
         t = torch.as_tensor(flag, dtype=torch.int64).reshape(1).to(wire)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return bool(t.item())
@@ -401,71 +462,126 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
                 reason = "error on another rank"
             raise IntegrationBlowUp(it, reason, trace)
 
+    def first_error():
+        """(iteration, reason) of the earliest device error over all ranks
+        (collective; iteration = never when there is none)."""
+        err = backend.check()
+        t = torch.tensor([never if err is None else err[0]], dtype=torch.int64, device=wire)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        it = int(t.item())
+        reason = err[1] if err is not None and err[0] == it else "error on another rank"
+        return it, reason
+
+    def run_device_loop():
+        """GPU backends: device-resident state, one host synchronisation per
+        step (the rebuild vote).  Between rebuilds each step after its vote
+        is one replayed CUDA graph: [ghost pull] -> LJ -> [ATM] -> kick ->
+        [trace row] -> drift of the next step (publishing its positions);
+        the graphs are captured per row epoch (pointers and counts change
+        only at rebuilds).  Trace rows stay on the device until the end;
+        device errors are read at rebuilds (before migrating) and at the end."""
+        num = schedule.num_iterations
+        rows = num // interval + 1
+        backend.trace_setup(rows, interval)
+        backend.pair_into_new(False)
+        st.f2.copy_(backend.f2_new[: backend.n_own])
+        backend.triplet_into_f3(False)
+        backend.sample()
+        kick_args = (half_dt, half_respa)
+
+        def drift_args(j):
+            return (box, dt, half_drift, half_respa, j % s == 0, skin)
+
+        if on_step is not None:
+            on_step(0)
+        if num > 0:
+            backend.drift(*drift_args(0))
+        for i in range(num):
+            if i > 0 and on_step is not None:
+                on_step(i)
+            sample = (i + 1) % interval == 0
+            end_of_cycle = (i + 1) % s == 0
+            nxt = drift_args(i + 1) if i + 1 < num else None
+            if any_flag(backend.moved() if skin > 0.0 else True):
+                if first_error()[0] <= i + 1:
+                    break  # never migrate a broken state; reported below
+                rebuild()
+                backend.invalidate_graphs()
+                backend.step_body(end_of_cycle, sample, False, nxt, kick_args)
+            else:
+                if not peer:
+                    backend.refresh_halo(dec, ex)  # messages: outside the graph
+                backend.replay((end_of_cycle, sample, peer, nxt is not None),
+                               lambda: backend.step_body(end_of_cycle, sample, peer, nxt,
+                                                         kick_args))
+        if on_step is not None:
+            on_step(num)
+        backend.destroy_graphs()
+        it, reason = first_error()
+        # per-rank partial rows summed in rank order (row k: iteration k * interval)
+        mine = backend.trace.to(wire)
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        acc = np.zeros(tuple(mine.shape))
+        for part in parts:
+            acc = acc + part.cpu().numpy()
+        for k in range(rows):
+            if k * interval >= it:
+                break
+            trace.record_values(k * interval, 0.5 * m * acc[k, 1], acc[k, 2], acc[k, 3],
+                                acc[k, 4], acc[k, 5])
+        if it <= num:
+            raise IntegrationBlowUp(it, reason, trace)
+
     clean = False
     try:
         local, plan = rebuild()
         if fast:
-            e2w2 = backend.pair_into_new(True)
-            st.f2.copy_(backend.f2_new[: plan.n_owned])
-            e3w3 = backend.triplet_into_f3(True)
+            run_device_loop()
         else:
             f2, e2w2 = backend.pair()
             f3, e3w3 = backend.triplet()
             st.f2, st.f3 = f2, f3
-        check(0)
-        record(0, e2w2, e3w3)
-        half_skin2 = (0.5 * skin) ** 2 * (1.0 - 1e-9)
-        for i in range(schedule.num_iterations):
-            if on_step is not None:
-                on_step(i)
-            sample = (i + 1) % interval == 0
-            end_of_cycle = (i + 1) % s == 0
-            if fast:
-                moved = backend.drift(box, dt, half_drift, half_respa, i % s == 0, skin)
-                if any_flag(moved if skin > 0.0 else True):
+            check(0)
+            record(0, e2w2, e3w3)
+            half_skin2 = (0.5 * skin) ** 2 * (1.0 - 1e-9)
+            for i in range(schedule.num_iterations):
+                if on_step is not None:
+                    on_step(i)
+                sample = (i + 1) % interval == 0
+                end_of_cycle = (i + 1) % s == 0
+                if hasattr(backend, "advance"):
+                    backend.advance()
+                if i % s == 0:
+                    st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
+                st.x = st.x + ((dt * st.v) + (half_drift * st.f2))
+                st.x = torch.remainder(st.x, box_t)  # numpy mod semantics for box > 0
+                st.x = torch.where(st.x >= box_t, torch.zeros_like(st.x), st.x)
+                if skin == 0.0 or st.x.shape[0] == 0:
+                    moved = skin == 0.0
+                else:
+                    d = st.x - st.x_ref
+                    d = d - box_t * torch.where(d > 0.5 * box_t, 1.0, torch.where(d < -0.5 * box_t, -1.0, 0.0))
+                    moved = ((d * d).sum(dim=1).max() > half_skin2)
+                if any_flag(moved):
                     local, plan = rebuild()
                 else:
-                    backend.refresh_halo(dec, ex)
-                e2w2 = backend.pair_into_new(sample)
-                if end_of_cycle:
-                    e3w3 = backend.triplet_into_f3(sample)
-                backend.kick(half_dt, half_respa, end_of_cycle)
+                    refresh(plan, local)
+                f2_new, e2w2 = backend.pair(scalars=sample)
+                st.v = st.v + (half_dt * (st.f2 + f2_new))
+                st.f2 = f2_new
+                if (i + 1) % s == 0:
+                    st.f3, e3w3 = backend.triplet(scalars=sample)
+                    st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
+                finite = torch.isfinite(st.x).all() & torch.isfinite(st.v).all()
+                first_bad = torch.where(finite | (first_bad <= i), first_bad,
+                                        torch.full_like(first_bad, i + 1))
                 if sample:
                     check(i + 1)
                     record(i + 1, e2w2, e3w3)
-                continue
-            if hasattr(backend, "advance"):
-                backend.advance()
-            if i % s == 0:
-                st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
-            st.x = st.x + ((dt * st.v) + (half_drift * st.f2))
-            st.x = torch.remainder(st.x, box_t)  # numpy mod semantics for box > 0
-            st.x = torch.where(st.x >= box_t, torch.zeros_like(st.x), st.x)
-            if skin == 0.0 or st.x.shape[0] == 0:
-                moved = skin == 0.0
-            else:
-                d = st.x - st.x_ref
-                d = d - box_t * torch.where(d > 0.5 * box_t, 1.0, torch.where(d < -0.5 * box_t, -1.0, 0.0))
-                moved = ((d * d).sum(dim=1).max() > half_skin2)
-            if any_flag(moved):
-                local, plan = rebuild()
-            else:
-                refresh(plan, local)
-            f2_new, e2w2 = backend.pair(scalars=sample)
-            st.v = st.v + (half_dt * (st.f2 + f2_new))
-            st.f2 = f2_new
-            if (i + 1) % s == 0:
-                st.f3, e3w3 = backend.triplet(scalars=sample)
-                st.v = _numpy_like_update(torch, st.v, half_respa, st.f3)
-            finite = torch.isfinite(st.x).all() & torch.isfinite(st.v).all()
-            first_bad = torch.where(finite | (first_bad <= i), first_bad,
-                                    torch.full_like(first_bad, i + 1))
-            if sample:
-                check(i + 1)
-                record(i + 1, e2w2, e3w3)
-        if on_step is not None:
-            on_step(schedule.num_iterations)
-        check(schedule.num_iterations)
+            if on_step is not None:
+                on_step(schedule.num_iterations)
+            check(schedule.num_iterations)
         clean = True
     except IntegrationBlowUp:
         clean = True

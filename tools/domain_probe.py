@@ -38,12 +38,34 @@ def main(argv):
     domain_respa_run(dist, cfg.system(), ff, pkg.RespaSchedule(cfg.dt, sf, 20),
                      gpu_backend_factory(ff))
     s = cfg.system()
+    steps_run = {}
+
+    def on_step(i):
+        if i in (0, steps):
+            torch.cuda.synchronize()
+            steps_run[i] = time.perf_counter()
+
+    prof = None
+    if "--profile" in argv:
+        import cProfile
+
+        prof = cProfile.Profile()
+        prof.enable()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    domain_respa_run(dist, s, ff, pkg.RespaSchedule(cfg.dt, sf, steps), gpu_backend_factory(ff))
+    domain_respa_run(dist, s, ff, pkg.RespaSchedule(cfg.dt, sf, steps), gpu_backend_factory(ff),
+                     on_step=on_step)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    print(f"domain loop (world 1, {backend}): {1e3 * dt / steps:.3f} ms/step over {steps} steps")
+    if prof is not None:
+        import pstats
+
+        prof.disable()
+        pstats.Stats(prof).sort_stats("tottime").print_stats(25)
+        pstats.Stats(prof).sort_stats("cumtime").print_stats("paper_2507_11172_b200", 30)
+    loop = steps_run[steps] - steps_run[0]
+    print(f"domain loop (world 1, {backend}): {1e3 * dt / steps:.3f} ms/step over {steps} steps "
+          f"incl. setup; step loop alone {1e3 * loop / steps:.3f} ms/step")
     s2 = cfg.system()
     torch.cuda.synchronize()
     t0 = time.perf_counter()

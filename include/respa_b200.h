@@ -26,7 +26,9 @@
  *     Initialise it to RB_STATUS_CLEAR.  `tag` is the r-RESPA iteration the
  *     kernel belongs to (0 for standalone passes); a kernel whose tag is
  *     larger than a recorded error's tag does nothing, so the state freezes
- *     at the failing step as respamd's IntegrationBlowUp does.
+ *     at the failing step as respamd's IntegrationBlowUp does.  The device
+ *     loop uses four words (error, current step, last closed step, rebuild
+ *     steps); the array must be 16-byte aligned (read in word pairs).
  */
 #ifndef RESPA_B200_H
 #define RESPA_B200_H

@@ -122,6 +122,16 @@ __device__ __forceinline__ void record_status(unsigned long long *status, int64_
     if (status) atomicMin(status, ((unsigned long long)tag << 8) | (unsigned long long)kind);
 }
 
+// Two adjacent status words in one volatile 16-byte load ({CLEAR, 0} for a
+// null status); issued with a kernel's data loads it costs no extra round
+// trip.  `p` is 16-byte aligned (status and status + 2).
+__device__ __forceinline__ ulonglong2 ld_status2(const unsigned long long *p) {
+    ulonglong2 r = make_ulonglong2(RB_STATUS_CLEAR, 0ull);
+    if (p) asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                        : "=l"(r.x), "=l"(r.y) : "l"(p));
+    return r;
+}
+
 // Tag of the current kernel: the explicit value, or (tag < 0) the step
 // counter kept in status[1] by rb_step_begin (lets a captured CUDA graph be
 // replayed for many steps).
@@ -133,6 +143,15 @@ __device__ __forceinline__ int64_t resolve_tag(int64_t tag, const unsigned long 
 // True when a kernel of step `tag` whose own error kind is `kind` must not
 // run: an earlier step failed, or an error of higher precedence (lower kind)
 // was raised earlier in the same step.
+__device__ __forceinline__ bool frozen_word(unsigned long long s, int64_t tag, int kind) {
+    if (s == RB_STATUS_CLEAR) return false;
+    long long t = (long long)(s >> 8);
+    int k = (int)(s & 0xff);
+    if (t < tag) return true;
+    if (t == tag && k < kind && k != RB_KIND_NONFINITE && k != RB_KIND_CAPACITY) return true;
+    return false;
+}
+
 __device__ __forceinline__ bool frozen(const unsigned long long *status, int64_t tag, int kind) {
     if (!status) return false;
     unsigned long long s = *(volatile const unsigned long long *)status;

@@ -30,7 +30,13 @@ bool pdl_on() {
 // numpy float remainder (npy_divmod) followed by the edge fix of
 // respamd/model.py:279-280
 __device__ __forceinline__ double wrap_coord(double x, double box) {
-    double r = fmod(x, box);
+    // one box away at most after a step: fmod's value without its loop
+    // (x - box is exact for box <= x < 2 box, Sterbenz)
+    double r;
+    if (x >= 0.0 && x < box) r = x;
+    else if (x >= box && x < 2.0 * box) r = x - box;
+    else if (x < 0.0 && x > -box) r = x;
+    else r = fmod(x, box);
     if (r != 0.0) {
         if (r < 0.0) r = xadd(r, box);
     } else {
@@ -40,12 +46,15 @@ __device__ __forceinline__ double wrap_coord(double x, double box) {
     return r;
 }
 
-// One thread per particle (AoS, 24 contiguous bytes per array).  Besides the
+// Four lanes per particle, lane c < 3 on component c of the AoS arrays
+// (coalesced: a warp covers 8 particles = 24 contiguous doubles per array;
+// lane 3 idles), so every load of a step is in flight at once.  Besides the
 // drift it (a) scatters the new position into the rank-ordered copy the force
 // kernels read, and (b) compares against the positions of the last
 // neighbour-row build: a particle that moved more than skin/2 flags a rebuild
 // of the rows in this very step (*rebuild_flag = tag), so every pair within
-// rc is always inside the rows built at rc + skin.
+// rc is always inside the rows built at rc + skin.  The displacement norm is
+// gathered by shuffles into lane 0 of the group.
 __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict__ vel,
                         double *__restrict__ f2_old, const double *__restrict__ f3,
                         double bx, double by, double bz, int periodic, double dt,
@@ -57,85 +66,84 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
                         const double *__restrict__ f2_new, double half_dt, int kick_prev,
                         int kick3_prev, double *__restrict__ publish, int64_t pub_stride) {
     pdl_enter();
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t p = gt >> 2;
+    const int c = (int)(gt & 3);
+    const bool act = p < n && c < 3;
+    const int64_t i = 3 * p + c;
+    // every load of the step first (one memory round trip; the status words
+    // ride along), the decisions after
+    double v = 0.0, fo = 0.0, fnew = 0.0, f3v = 0.0, px = 0.0, xr = 0.0;
+    int32_t ro = 0;
+    if (act) {
+        v = vel[i];
+        fo = f2_old[i];
+        px = pos[i];
+        if (kick_prev) fnew = f2_new[i];
+        if (kick3 || (kick_prev && kick3_prev)) f3v = f3[i];
+        if (x_ref) xr = x_ref[i];
+        if (pr && rank_of) ro = rank_of[p];
+    }
+    const ulonglong2 s01 = ld_status2(status);
     // a step-opening drift numbers its step from the last CLOSED step
     // (status[2], written by the step's pair pass and kick) and publishes it
     // in status[1]: no kernel reads the word another block of it writes.
-    // kick_prev: first the kick that ends the previous step (rb_respa_kick_drift)
     if (advance) {
-        tag = (int64_t)(*(volatile const unsigned long long *)(status + 2)) + 1;
-        if (p == 0) status[1] = (unsigned long long)tag;
-    } else {
-        tag = resolve_tag(tag, status);
+        tag = (int64_t)ld_status2(status + 2).x + 1;
+        if (gt == 0) status[1] = (unsigned long long)tag;
+    } else if (tag < 0) {
+        tag = status ? (int64_t)s01.y : 0;
     }
-    if (kick_prev && p < n) {
+    const unsigned long long sw = s01.x;  // the error word as this step found it
+    if (kick_prev) {
         // the kick that closes the previous step (tag - 1), folded in: the
         // same updates and error rules as k_kick (integrators.py:158-165)
         const int64_t tp = tag - 1;
         bool go = true, do3 = kick3_prev != 0;
-        const unsigned long long sw = *(volatile const unsigned long long *)status;
         if (sw != RB_STATUS_CLEAR) {
             const long long t = (long long)(sw >> 8);
             const int k = (int)(sw & 0xff);
             if (t < tp || (t == tp && k == RB_KIND_PAIR_MIN_SEPARATION)) go = false;
             if (t == tp && k == RB_KIND_TRIPLET_MIN_SEPARATION) do3 = false;
         }
-        if (go) {
-            bool finite = true;
-#pragma unroll
-            for (int c = 0; c < 3; c++) {
-                const int64_t i = 3 * p + c;
-                const double fnew = f2_new[i];
-                double v = xadd(vel[i], xmul(half_dt, xadd(f2_old[i], fnew)));
-                if (do3) v = xadd(v, xmul(half_respa, f3[i]));
-                vel[i] = v;
-                f2_old[i] = fnew;
-                finite = finite && isfinite(v);
-            }
-            if (!finite) record_status(status, tp, RB_KIND_NONFINITE);
+        if (go && act) {
+            v = xadd(v, xmul(half_dt, xadd(fo, fnew)));
+            if (do3) v = xadd(v, xmul(half_respa, f3v));
+            vel[i] = v;
+            f2_old[i] = fnew;
+            fo = fnew;
+            if (!isfinite(v)) record_status(status, tp, RB_KIND_NONFINITE);
         }
     }
-    if (p < n && !frozen(status, tag, 0)) {
-        const double box[3] = {bx, by, bz};
-        double x[3];
-        bool finite = true;
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-            const int64_t i = 3 * p + c;
-            double v = vel[i];
-            if (kick3) {
-                v = xadd(v, xmul(half_respa, f3[i]));
-                vel[i] = v;
-            }
-            double xc = xadd(pos[i], xadd(xmul(dt, v), xmul(half_drift, f2_old[i])));
-            if (periodic) xc = wrap_coord(xc, box[c]);
-            pos[i] = xc;
-            x[c] = xc;
-            finite = finite && isfinite(xc);
+    // an earlier step failed: freeze (errors of this step do not stop it)
+    const bool run = sw == RB_STATUS_CLEAR || (long long)(sw >> 8) >= tag;
+    const double box = c == 0 ? bx : (c == 1 ? by : bz);
+    double d = 0.0;
+    if (run && act) {
+        if (kick3) {
+            v = xadd(v, xmul(half_respa, f3v));
+            vel[i] = v;
         }
-        if (!finite) record_status(status, tag, RB_KIND_NONFINITE);
-        if (pr && rank_of) {
-            const int64_t r = rank_of[p];
-            pr[3 * r] = x[0];
-            pr[3 * r + 1] = x[1];
-            pr[3 * r + 2] = x[2];
-        }
+        double xc = xadd(px, xadd(xmul(dt, v), xmul(half_drift, fo)));
+        if (periodic) xc = wrap_coord(xc, box);
+        pos[i] = xc;
+        if (!isfinite(xc)) record_status(status, tag, RB_KIND_NONFINITE);
+        if (pr && rank_of) pr[3 * (int64_t)ro + c] = xc;
         if (publish) {  // the copy peers pull their ghosts from (rb_halo_pull),
                         // the half of this step's parity
-            double *out = publish + (tag & 1) * 3 * pub_stride;
-            out[3 * p] = x[0];
-            out[3 * p + 1] = x[1];
-            out[3 * p + 2] = x[2];
+            publish[(tag & 1) * 3 * pub_stride + i] = xc;
             __threadfence_system();
         }
-        if (x_ref && rebuild_flag) {
-            double d2 = 0.0;
-#pragma unroll
-            for (int c = 0; c < 3; c++) {
-                double d = x[c] - x_ref[3 * p + c];
-                if (periodic) d = min_image(d, box[c], 0.5 * box[c]);
-                d2 += d * d;
-            }
+        if (x_ref) {
+            d = xc - xr;
+            if (periodic) d = min_image(d, box, 0.5 * box);
+        }
+    }
+    if (x_ref && rebuild_flag) {  // uniform: every lane takes the shuffles
+        const double dy = __shfl_down_sync(0xffffffffu, d, 1);
+        const double dz = __shfl_down_sync(0xffffffffu, d, 2);
+        if (run && act && c == 0) {
+            const double d2 = d * d + dy * dy + dz * dz;
             if (!(d2 <= skin_half2)) {  // also catches NaN
                 // the first thread to flag this step counts a rebuild step
                 const unsigned long long was = atomicExch(
@@ -153,25 +161,30 @@ __global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict_
                        int64_t tag) {
     pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // loads first, the status words with them (one round trip)
+    double v = 0.0, fo = 0.0, fnew = 0.0, f3v = 0.0;
+    if (i < n3) {
+        v = vel[i];
+        fo = f2_old[i];
+        fnew = f2_new[i];
+        if (kick3) f3v = f3[i];
+    }
+    const ulonglong2 s01 = ld_status2(status);
     const bool from_device = tag < 0;
-    tag = resolve_tag(tag, status);
+    if (tag < 0) tag = status ? (int64_t)s01.y : 0;
     if (from_device && status && i == 0) status[2] = (unsigned long long)tag;  // closes the step
     if (i >= n3) return;
     bool do_kick2 = true, do_kick3 = kick3 != 0;
-    if (status) {
-        const unsigned long long s = *(volatile const unsigned long long *)status;
-        if (s != RB_STATUS_CLEAR) {
-            const long long t = (long long)(s >> 8);
-            const int k = (int)(s & 0xff);
-            if (t < tag) return;
-            if (t == tag && k == RB_KIND_PAIR_MIN_SEPARATION) return;  // raised before :158
-            if (t == tag && k == RB_KIND_TRIPLET_MIN_SEPARATION) do_kick3 = false;  // before :165
-        }
+    const unsigned long long s = s01.x;
+    if (s != RB_STATUS_CLEAR) {
+        const long long t = (long long)(s >> 8);
+        const int k = (int)(s & 0xff);
+        if (t < tag) return;
+        if (t == tag && k == RB_KIND_PAIR_MIN_SEPARATION) return;  // raised before :158
+        if (t == tag && k == RB_KIND_TRIPLET_MIN_SEPARATION) do_kick3 = false;  // before :165
     }
-    double v = vel[i];
-    const double fnew = f2_new[i];
-    if (do_kick2) v = xadd(v, xmul(half_dt, xadd(f2_old[i], fnew)));
-    if (do_kick3) v = xadd(v, xmul(half_respa, f3[i]));
+    if (do_kick2) v = xadd(v, xmul(half_dt, xadd(fo, fnew)));
+    if (do_kick3) v = xadd(v, xmul(half_respa, f3v));
     vel[i] = v;
     f2_old[i] = fnew;  // np.copyto(f2_old, forces_2b), integrators.py:159
     if (!isfinite(v)) record_status(status, tag, RB_KIND_NONFINITE);
@@ -384,7 +397,7 @@ static int drift_launch(int64_t n, double *pos, double *vel, double *f2_old, con
     if (n == 0) return advance_step ? rb_step_begin(status, stream) : RB_OK;
     const int tb = 256;
     const double half = 0.5 * skin;
-    launch(k_drift, dim3((unsigned)((n + tb - 1) / tb)), dim3(tb), 0, as_stream(stream), n, pos,
+    launch(k_drift, dim3((unsigned)((4 * n + tb - 1) / tb)), dim3(tb), 0, as_stream(stream), n, pos,
            vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt, half_drift,
            half_respa, kick3, rank_of, pos_r, x_ref, half * half * (1.0 - 1e-9), rebuild_flag,
            status, tag, advance_step ? 1 : 0, (cudaGraphConditionalHandle)rebuild_cond, f2_new,

@@ -49,27 +49,43 @@ __global__ void __launch_bounds__(kLjThreads, RB_LJ_MIN_BLOCKS)
     const int64_t r = gid / kLjGroup;
     const int sub = (int)(gid % kLjGroup);
     const bool active = r < n;
+    // the pass is latency-bound: the first memory round trip carries the
+    // status words, the row length, the own position and every row index of
+    // this lane (up to kLjRowRegs; loaded up to the capacity and masked by
+    // the length afterwards), the second the neighbour positions two entries
+    // at a time; the accumulation order stays k = sub, sub + G, sub + 2G, ...
+    int m = 0;
+    double xi = 0.0, yi = 0.0, zi = 0.0;
+    int jr[kLjRowRegs];
+    const int32_t *row = rows + (active ? r : 0) * (int64_t)capacity;
+    if (active) {
+        m = row_count[r];
+        xi = pr[3 * r];
+        yi = pr[3 * r + 1];
+        zi = pr[3 * r + 2];
+    }
+#pragma unroll
+    for (int u = 0; u < kLjRowRegs; u++) {
+        const int k = sub + u * kLjGroup;
+        jr[u] = active && k < capacity ? __ldg(row + k) : -1;
+    }
+    const ulonglong2 s01 = ld_status2(status);
+    const unsigned long long sw = __shfl_sync(0xffffffffu, s01.x, 0);  // one view per warp
+    const int64_t cur = status ? (int64_t)__shfl_sync(0xffffffffu, s01.y, 0) : 0;
     const bool from_device = tag < 0;
-    tag = resolve_tag(tag, status);
+    if (tag < 0) tag = cur;
     // the pair pass closes the device step (status[2]): the kick that ends it
     // may be folded into the next step's drift (rb_respa_kick_drift)
     if (from_device && status && gid == 0) status[2] = (unsigned long long)tag;
-    if (warp_frozen(status, tag, RB_KIND_PAIR_MIN_SEPARATION)) return;
+    if (status && frozen_word(sw, tag, RB_KIND_PAIR_MIN_SEPARATION)) return;
     const Image im = make_image(g);
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
     bool bad = false;
     if (active) {
-        const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
-        const int m = row_count[r];
-        const int32_t *row = rows + r * (int64_t)capacity;
-        // the pass is latency-bound: every row index of this lane (up to
-        // kLjRowRegs) is loaded first, then the positions two entries at a
-        // time; the accumulation order stays k = sub, sub + G, sub + 2G, ...
-        int jr[kLjRowRegs];
 #pragma unroll
         for (int u = 0; u < kLjRowRegs; u++) {
             const int k = sub + u * kLjGroup;
-            jr[u] = k < m ? __ldg(row + k) : -1;
+            if (k >= m) jr[u] = -1;
         }
         auto visit = [&](int q, double px, double py, double pz) {
             double dx, dy, dz;

@@ -350,6 +350,21 @@ RB_API int rb_rebuild_cond_create(void *stream, uint64_t *handle);
 RB_API int rb_rebuild_cond_begin(uint64_t handle, void *stream, void **body_stream);
 RB_API int rb_rebuild_cond_end(void *stream);
 
+/* The gated rebuild in ONE launch: rb_bin + rb_nlist + rb_nlist_mirror
+ * (same arguments and identical results) as phases of a single kernel
+ * separated by grid-wide barriers; with rebuild_flag != NULL it exits at
+ * once unless *rebuild_flag equals the step tag, so a captured step that
+ * does not rebuild pays one launch instead of nine (or a conditional node).
+ * `scratch` (rb_rebuild_scratch_bytes) must be zero-filled before its first
+ * use (barrier words); every launch leaves it reusable. */
+RB_API size_t rb_rebuild_scratch_bytes(int64_t n, int64_t ncell);
+RB_API int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_start,
+                      int32_t *cell_particles, int32_t *cell_of_rank, double *pos_r,
+                      int32_t *rank_of, double *x_ref, double r_list, int32_t capacity,
+                      int32_t *rows, int32_t *row_count, int32_t *max_count, int32_t *mirror,
+                      const int64_t *rebuild_flag, const unsigned long long *status, int64_t tag,
+                      void *scratch, size_t scratch_bytes, void *stream);
+
 /* Reusable captured step graphs (the domain loop's step kinds, recaptured
  * at every row rebuild): rb_graph_begin starts a thread-local capture on a
  * non-default stream; rb_graph_end ends it and instantiates into *exec, or,

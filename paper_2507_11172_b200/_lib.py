@@ -116,6 +116,9 @@ SIGNATURES = {
     "rb_rebuild_cond_create": (ctypes.c_int, [_P, _P]),
     "rb_rebuild_cond_begin": (ctypes.c_int, [_U64, _P, _P]),
     "rb_rebuild_cond_end": (ctypes.c_int, [_P]),
+    "rb_rebuild_scratch_bytes": (ctypes.c_size_t, [_I64, _I64]),
+    "rb_rebuild": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _I32, _P, _P, _P, _P,
+                                  _P, _P, _I64, _P, _SZ, _P]),
     "rb_graph_begin": (ctypes.c_int, [_P]),
     "rb_graph_end": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
     "rb_graph_launch": (ctypes.c_int, [_U64, _P]),

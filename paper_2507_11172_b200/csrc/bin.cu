@@ -14,37 +14,9 @@
 //                  order (SoA) and the rank -> cell map
 #include <algorithm>
 
-#include "common.cuh"
+#include "cells.cuh"
 
 namespace rb {
-
-__device__ __forceinline__ int cell_index_1d(double x, double origin, double inv, int n) {
-    // python int() truncates toward zero; numba's int() is the same fptosi
-    double t = xmul(xsub(x, origin), inv);
-    long long c = (long long)t;
-    if (c < 0) c = 0;
-    else if (c >= n) c = n - 1;
-    return (int)c;
-}
-
-// cell of a coordinate in dimension d: the global index, mapped into the
-// rank's window when the grid is a window of a decomposed periodic grid
-__device__ __forceinline__ int cell_index(const rb_grid &g, int d, double x) {
-    if (g.wrap[d] || !g.periodic) return cell_index_1d(x, g.origin[d], g.inv_cell[d], g.cells[d]);
-    int c = cell_index_1d(x, g.origin[d], g.inv_cell[d], g.gcells[d]) - g.wlo[d];
-    if (c < 0) c += g.gcells[d];
-    if (c >= g.gcells[d]) c -= g.gcells[d];
-    return c < g.cells[d] ? c : g.cells[d] - 1;  // outside the window: caller's error
-}
-
-// Rebuild gate: a binning launched inside a captured r-RESPA step runs only
-// when the drift of that step flagged a rebuild (*flag == tag); flag == NULL
-// means always (standalone passes).
-__device__ __forceinline__ bool gate_closed(const int64_t *flag, const unsigned long long *status,
-                                            int64_t tag) {
-    if (!flag) return false;
-    return *(volatile const int64_t *)flag != resolve_tag(tag, status);
-}
 
 __global__ void k_bin_zero(int64_t ncell, int32_t *__restrict__ count, const int64_t *flag,
                            const unsigned long long *status, int64_t tag) {
@@ -84,11 +56,6 @@ __global__ void k_bin_scatter(int64_t n, const int32_t *__restrict__ cell_of,
     }
 }
 
-// One warp per cell: restore ascending particle order inside the cell (the
-// atomic scatter is unordered), then gather the rank-ordered positions and
-// the rank <-> particle maps.  Cells of up to 32 particles sort in registers
-// (rank = number of smaller indices); larger cells fall back to a serial
-// insertion sort by lane 0.
 constexpr int kFinishWarps = 8;
 
 __global__ void __launch_bounds__(kFinishWarps * 32)
@@ -101,78 +68,14 @@ __global__ void __launch_bounds__(kFinishWarps * 32)
     const int lane = threadIdx.x & 31;
     if (gate_closed(flag, status, tag)) return;
     for (int64_t c = (int64_t)blockIdx.x * kFinishWarps + (threadIdx.x >> 5); c < ncell;
-         c += (int64_t)gridDim.x * kFinishWarps) {
-    const int b = start[c], e = start[c + 1], k = e - b;
-    if (k <= 32) {
-        const int v = lane < k ? parts[b + lane] : 0x7fffffff;
-        int rank = 0;
-        for (int l = 0; l < k; l++) rank += __shfl_sync(0xffffffffu, v, l) < v ? 1 : 0;
-        __syncwarp();
-        if (lane < k) parts[b + rank] = v;
-    } else if (lane == 0) {
-        for (int a = b + 1; a < e; a++) {
-            const int v = parts[a];
-            int q = a - 1;
-            while (q >= b && parts[q] > v) {
-                parts[q + 1] = parts[q];
-                q--;
-            }
-            parts[q + 1] = v;
-        }
-    }
-    __syncwarp();
-    for (int r = b + lane; r < e; r += 32) {
-        const int64_t p = parts[r];
-        const double x = pos[3 * p], y = pos[3 * p + 1], z = pos[3 * p + 2];
-        cell_of_rank[r] = (int32_t)c;
-        pr[3 * (int64_t)r] = x;
-        pr[3 * (int64_t)r + 1] = y;
-        pr[3 * (int64_t)r + 2] = z;
-        if (rank_of) rank_of[p] = r;
-        if (x_ref) {
-            x_ref[3 * p] = x;
-            x_ref[3 * p + 1] = y;
-            x_ref[3 * p + 2] = z;
-        }
-    }
-    }
+         c += (int64_t)gridDim.x * kFinishWarps)
+        cell_finish_one(c, lane, start, parts, cell_of_rank, rank_of, pos, pr, x_ref);
 }
 
 // ---------------------------------------------------------------------------
 // exclusive scan of int32 counts into out[0..n] (out[n] = total)
 // three phases: per-tile sums, scan of tile sums (one CTA), per-tile scan
 // ---------------------------------------------------------------------------
-constexpr int kScanThreads = 512;
-constexpr int kScanItems = 4;
-constexpr int kScanTile = kScanThreads * kScanItems;
-
-__device__ __forceinline__ int block_exclusive_scan(int v, int *warp_sums, int &total) {
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int x = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, x, off);
-        if (lane >= off) x += y;
-    }
-    if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        int nw = blockDim.x >> 5;
-        int s = lane < nw ? warp_sums[lane] : 0;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, s, off);
-            if (lane >= off) s += y;
-        }
-        if (lane < nw) warp_sums[lane] = s;
-    }
-    __syncthreads();
-    int warp_off = warp ? warp_sums[warp - 1] : 0;
-    total = warp_sums[(blockDim.x >> 5) - 1];
-    __syncthreads();
-    return warp_off + x - v;
-}
-
 __global__ void k_scan_tile_sums(int64_t n, const int32_t *__restrict__ in,
                                  int32_t *__restrict__ tile_sums, const int64_t *flag,
                                  const unsigned long long *status, int64_t tag) {

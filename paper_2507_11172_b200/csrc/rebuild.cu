@@ -1,0 +1,197 @@
+// rebuild.cu -- the gated row rebuild of a captured r-RESPA step as ONE launch.
+//
+// Inside a captured step the rebuild (binning, rows, mirror: nine kernels)
+// runs only when the step's drift flagged it.  Nine gated launches cost ~10 us
+// of launch latency per step, a graph conditional node ~6 us; this kernel
+// costs one PDL launch that exits at the gate.  When the gate is open it runs
+// the same phases as rb_bin + rb_nlist + rb_nlist_mirror (identical results:
+// the same device functions, cells.cuh), separated by grid-wide barriers:
+//
+//   zero counts | count | tile sums | tile offsets | scan apply | scatter |
+//   cell finish (stable order, rank-ordered copy) | rows | mirror
+//
+// The grid is at most the co-resident capacity (occupancy x SMs), so the
+// software barrier (count + generation words in the scratch) cannot
+// deadlock: under programmatic dependent launch the next kernel starts only
+// after every block of this one has started.  Data written by an earlier
+// phase is read with L2-coherent loads (ldc<true>).
+#include <algorithm>
+
+#include "cells.cuh"
+
+namespace rb {
+
+constexpr int kRbThreads = 256;
+constexpr int kRbItems = 4;
+constexpr int kRbTile = kRbThreads * kRbItems;  // cells per scan tile
+
+__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g0 = *(volatile unsigned *)gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            atomicExch(count, 0u);  // reusable: the next barrier counts from 0
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*(volatile unsigned *)gen == g0) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kRbThreads)
+    k_rebuild(rb_grid g, int64_t n, const double *__restrict__ pos, int32_t *cell_start,
+              int32_t *parts, int32_t *cell_of_rank, double *pr, int32_t *rank_of, double *x_ref,
+              double rl2, int32_t capacity, int32_t *rows, int32_t *row_count,
+              int32_t *max_count, int32_t *mirror, int32_t *cell_of, int32_t *count,
+              int32_t *cursor, int32_t *tiles, unsigned *bar, const int64_t *flag,
+              const unsigned long long *status, int64_t tag) {
+    pdl_enter();
+    if (gate_closed(flag, status, tag)) return;  // the same answer in every block
+    __shared__ int warp_sums[32];
+    const int64_t ncell = (int64_t)g.cells[0] * g.cells[1] * g.cells[2];
+    const int64_t ntiles = (ncell + kRbTile - 1) / kRbTile;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = tid >> 5, nwarp = nth >> 5;
+    unsigned *bcount = bar, *bgen = bar + 1;
+
+    for (int64_t c = tid; c < ncell; c += nth) count[c] = 0;
+    grid_barrier(bcount, bgen);
+    // cell of every particle + histogram (bin.cu k_bin_count)
+    for (int64_t i = tid; i < n; i += nth) {
+        const int cx = cell_index(g, 0, pos[3 * i]);
+        const int cy = cell_index(g, 1, pos[3 * i + 1]);
+        const int cz = cell_index(g, 2, pos[3 * i + 2]);
+        const int c = (cx * g.cells[1] + cy) * g.cells[2] + cz;
+        cell_of[i] = c;
+        atomicAdd(&count[c], 1);
+    }
+    grid_barrier(bcount, bgen);
+    // exclusive scan of the counts: tile sums, tile offsets, apply
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int s = 0;
+#pragma unroll
+        for (int k = 0; k < kRbItems; k++) {
+            const int64_t i = t * kRbTile + (int64_t)threadIdx.x * kRbItems + k;
+            if (i < ncell) s += ldc<true>(count + i);
+        }
+        int total;
+        block_exclusive_scan(s, warp_sums, total);
+        if (threadIdx.x == 0) tiles[t] = total;
+    }
+    grid_barrier(bcount, bgen);
+    if (blockIdx.x == 0) {
+        int carry = 0;
+        for (int64_t base = 0; base < ntiles; base += blockDim.x) {
+            const int64_t i = base + threadIdx.x;
+            const int v = i < ntiles ? ldc<true>(tiles + i) : 0;
+            int total;
+            const int ex = block_exclusive_scan(v, warp_sums, total);
+            if (i < ntiles) tiles[i] = carry + ex;
+            carry += total;
+        }
+    }
+    grid_barrier(bcount, bgen);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int vals[kRbItems];
+        int s = 0;
+#pragma unroll
+        for (int k = 0; k < kRbItems; k++) {
+            const int64_t i = t * kRbTile + (int64_t)threadIdx.x * kRbItems + k;
+            vals[k] = i < ncell ? ldc<true>(count + i) : 0;
+            s += vals[k];
+        }
+        int total;
+        int ex = block_exclusive_scan(s, warp_sums, total) + ldc<true>(tiles + t);
+#pragma unroll
+        for (int k = 0; k < kRbItems; k++) {
+            const int64_t i = t * kRbTile + (int64_t)threadIdx.x * kRbItems + k;
+            if (i < ncell) {
+                cell_start[i] = ex;
+                cursor[i] = ex;
+            }
+            ex += vals[k];
+            if (i == ncell - 1) cell_start[ncell] = ex;
+        }
+    }
+    grid_barrier(bcount, bgen);
+    // unordered scatter into the cell ranges (bin.cu k_bin_scatter)
+    for (int64_t i = tid; i < n; i += nth) {
+        const int slot = atomicAdd(&cursor[ldc<true>(cell_of + i)], 1);
+        parts[slot] = (int32_t)i;
+    }
+    grid_barrier(bcount, bgen);
+    for (int64_t c = warp; c < ncell; c += nwarp)
+        cell_finish_one<true>(c, lane, cell_start, parts, cell_of_rank, rank_of, pos, pr, x_ref);
+    grid_barrier(bcount, bgen);
+    for (int64_t r = warp; r < n; r += nwarp)
+        nlist_one<true>(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows, row_count,
+                        max_count);
+    grid_barrier(bcount, bgen);
+    for (int64_t p = warp; p < n; p += nwarp)
+        mirror_one<true>(p, lane, rows, row_count, capacity, mirror);
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+static int rebuild_grid() {
+    static int blocks = 0;
+    if (!blocks) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rebuild, kRbThreads, 0);
+        blocks = std::max(1, sms) * std::max(1, per);
+    }
+    return blocks;
+}
+
+}  // namespace rb
+
+using namespace rb;
+
+// scratch: barrier words (zero-filled once by the caller) | cell_of[n] |
+// count[ncell] | cursor[ncell] | tile sums
+extern "C" size_t rb_rebuild_scratch_bytes(int64_t n, int64_t ncell) {
+    const int64_t ntiles = (std::max<int64_t>(ncell, 1) + kRbTile - 1) / kRbTile;
+    return 256 + align256(sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1)) +
+           2 * align256(sizeof(int32_t) * (size_t)std::max<int64_t>(ncell, 1)) +
+           align256(sizeof(int32_t) * (size_t)ntiles);
+}
+
+extern "C" int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_start,
+                          int32_t *cell_particles, int32_t *cell_of_rank, double *pos_r,
+                          int32_t *rank_of, double *x_ref, double r_list, int32_t capacity,
+                          int32_t *rows, int32_t *row_count, int32_t *max_count, int32_t *mirror,
+                          const int64_t *rebuild_flag, const unsigned long long *status,
+                          int64_t tag, void *scratch, size_t scratch_bytes, void *stream) {
+    if (!g || n < 0 || capacity <= 0 || !max_count || !rows || !row_count || !mirror || !scratch)
+        return RB_ERR_ARGUMENT;
+    if (g->n_offsets <= 0 || g->n_offsets > RB_MAX_OFFSETS) return RB_ERR_GEOMETRY;
+    const int64_t ncell = (int64_t)g->cells[0] * g->cells[1] * g->cells[2];
+    if (ncell <= 0) return RB_ERR_GEOMETRY;
+    if (scratch_bytes < rb_rebuild_scratch_bytes(n, ncell)) return RB_ERR_ARGUMENT;
+    if (n == 0) return RB_OK;
+    char *p = (char *)scratch;
+    unsigned *bar = (unsigned *)p;
+    p += 256;
+    int32_t *cell_of = (int32_t *)p;
+    p += align256(sizeof(int32_t) * (size_t)n);
+    int32_t *count = (int32_t *)p;
+    p += align256(sizeof(int32_t) * (size_t)ncell);
+    int32_t *cursor = (int32_t *)p;
+    p += align256(sizeof(int32_t) * (size_t)ncell);
+    int32_t *tiles = (int32_t *)p;
+    const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
+    launch(k_rebuild, dim3((unsigned)rebuild_grid()), dim3(kRbThreads), 0, as_stream(stream), *g,
+           n, pos, cell_start, cell_particles, cell_of_rank, pos_r, rank_of, x_ref, rl2, capacity,
+           rows, row_count, max_count, mirror, cell_of, count, cursor, tiles, bar, rebuild_flag,
+           status, tag);
+    note_launches(1);
+    return launch_status();
+}

@@ -80,6 +80,7 @@ class ForceEngine:
             (int(self.L.rb_sample_scratch_bytes(n)) + 7) // 8, dtype=f64, device=dev)
         self.cell_start = None
         self.bin_scratch = None
+        self.rebuild_scratch = None
         self.rows = None
         self.mirror = None
         self.atm_scratch = None
@@ -110,12 +111,33 @@ class ForceEngine:
         return int(h.value)
 
     def rebuild(self, geom: Geometry, r_list: float, capacity: int, pos=None, tag: int = 0,
-                cond: int = 0) -> None:
+                cond: int = 0, fused: bool = False) -> None:
         """Gated rebuild (binning, rows, mirror) of the device loop.
 
-        With a conditional handle (captured step, set by the drift) the nine
-        gated launches go into the body of an IF node, so steps that do not
-        rebuild skip them; without one they are launched directly."""
+        `fused`: one rb_rebuild launch (the same phases behind grid barriers;
+        exits at once when the step did not flag a rebuild).  With a
+        conditional handle (captured step, set by the drift) the nine gated
+        launches go into the body of an IF node, so steps that do not rebuild
+        skip them; otherwise they are launched directly."""
+        if fused:
+            pos = self.pos if pos is None else pos
+            self._ensure_cells(geom.num_cells)
+            self._ensure_rows(capacity)
+            need = int(self.L.rb_rebuild_scratch_bytes(self.n, geom.num_cells))
+            if self.rebuild_scratch is None or self.rebuild_scratch.numel() < need:
+                # zero-filled once: the grid-barrier words at its head
+                self.rebuild_scratch = self.torch.zeros(need, dtype=self.torch.uint8,
+                                                        device=self.device)
+            g = self.grid_struct(geom)
+            st = self.L.rb_rebuild(ctypes.byref(g), self.n, ptr(pos), ptr(self.cell_start),
+                                   ptr(self.parts), ptr(self.cell_of_rank), ptr(self.pos_r),
+                                   ptr(self.rank_of), ptr(self.x_ref), float(r_list),
+                                   int(self.capacity), ptr(self.rows), ptr(self.row_count),
+                                   ptr(self.max_count), ptr(self.mirror), self._gate(True),
+                                   ptr(self.status), int(tag), ptr(self.rebuild_scratch),
+                                   self.rebuild_scratch.numel(), self.stream)
+            _lib.check(st, "rb_rebuild")
+            return
         if cond:
             body = ctypes.c_void_p()
             _lib.check(self.L.rb_rebuild_cond_begin(cond, self.stream, ctypes.byref(body)),

@@ -177,8 +177,12 @@ class DeviceRespa:
         self.slots = None
         self.geom = None
         self.graph = None
-        # captured steps put the rebuild into a conditional graph node
-        self.cond_rebuild = os.environ.get("RB_COND_REBUILD", "1") != "0"
+        # the gated rebuild of a step: one fused launch (rb_rebuild, default),
+        # or (RB_REBUILD=cond) the nine kernels in a conditional graph node,
+        # or (RB_REBUILD=gated) the nine gated launches
+        mode = os.environ.get("RB_REBUILD", "fused")
+        self.cond_rebuild = mode == "cond"
+        self.fused_rebuild = mode == "fused"
         # inside a sampling period a step's kick runs in the next drift
         self.fuse_kick = os.environ.get("RB_FUSE_KICK", "1") != "0"
 
@@ -220,7 +224,8 @@ class DeviceRespa:
                 self.f3.fill_(float("nan"))
             return
         if self.periodic:  # Verlet rows: rebuild only when the drift flagged it
-            eng.rebuild(geom, self.r_build, self.capacity, self.x, tag=tag, cond=cond)
+            eng.rebuild(geom, self.r_build, self.capacity, self.x, tag=tag, cond=cond,
+                        fused=self.fused_rebuild)
         else:
             eng.bin(geom, self.x, tag=tag)
             eng.nlist(geom, self.r_build, capacity=self.capacity, checked=False, tag=tag)

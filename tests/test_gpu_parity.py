@@ -126,6 +126,46 @@ def test_newton3_forces_sum_to_zero(pkg):
     assert np.max(np.abs(s.forces_3b.sum(axis=0))) <= 1e-12 * s.n
 
 
+@pytest.mark.parametrize("nc,r_list", [(10, 2.8), (6, 3.4), (4, 2.6)])
+def test_fused_rebuild_equals_separate_kernels(pkg, nc, r_list):
+    """rb_rebuild (one launch, grid barriers) writes exactly what rb_bin +
+    rb_nlist + rb_nlist_mirror write; with the gate closed it writes nothing."""
+    import torch
+
+    from paper_2507_11172_b200.engine import ForceEngine
+    from paper_2507_11172_b200.grid import geometry
+
+    s = pkg.systems.fcc_system(nc, jitter=0.05, seed=nc)
+    n = s.positions.shape[0]
+    geom = geometry(s.box, None, r_list, True)
+    a, b = ForceEngine(n), ForceEngine(n)
+    for e in (a, b):
+        e.upload_positions(s.positions)
+    a.bin(geom)
+    a.nlist(geom, r_list, checked=True)
+    b.rebuild(geom, r_list, a.capacity, tag=0, fused=True)  # flag 0 == tag 0: open
+    ncell = geom.num_cells
+    for name, k in (("cell_start", ncell + 1), ("parts", n), ("cell_of_rank", n),
+                    ("rank_of", n), ("row_count", n)):
+        assert np.array_equal(getattr(a, name)[:k].cpu().numpy(),
+                              getattr(b, name)[:k].cpu().numpy()), name
+    for name in ("pos_r", "x_ref"):
+        assert np.array_equal(getattr(a, name)[:n].cpu().numpy(),
+                              getattr(b, name)[:n].cpu().numpy()), name
+    cnt = a.row_count[:n].cpu().numpy()
+    cap = a.capacity
+    ra, rb_ = (e.rows[:n * cap].cpu().numpy().reshape(n, cap) for e in (a, b))
+    ma, mb = (e.mirror[:n * cap].cpu().numpy().reshape(n, cap) for e in (a, b))
+    valid = np.arange(cap)[None, :] < cnt[:, None]
+    assert np.array_equal(ra[valid], rb_[valid]) and np.array_equal(ma[valid], mb[valid])
+    assert int(a.max_count.item()) == int(b.max_count.item())
+    # gate closed (flag != tag): nothing is written
+    before = b.rows.clone()
+    b.upload_positions(s.positions[::-1].copy())
+    b.rebuild(geom, r_list, a.capacity, tag=5, fused=True)
+    assert torch.equal(before, b.rows)
+
+
 def test_write_discipline_single_base_cell(pkg, rng):
     pos = random_positions(rng, 150, (10.0,) * 3, True)
     s = _system(pkg, pos, (10.0,) * 3, True)

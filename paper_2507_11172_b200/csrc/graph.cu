@@ -7,6 +7,10 @@
 // conditional together with the rebuild flag, and an IF node holds the
 // rebuild.  The body kernels keep their own gate check, so a body that runs
 // is exactly the gated launch sequence.
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
 #include "common.cuh"
 
 namespace rb {
@@ -90,8 +94,29 @@ extern "C" int rb_rebuild_cond_end(void *stream) {
 // instantiation if the topology changed), which costs a fraction of an
 // instantiation.  Thread-local capture mode: other host threads (e.g. a
 // communication library's watchdog) do not invalidate it.
+// kernels per executable, so graph launches count in rb_launch_count
+static std::mutex g_graph_mu;
+static std::unordered_map<uint64_t, int> g_graph_kernels;
+
+static int count_kernel_nodes(cudaGraph_t g) {
+    size_t n = 0;
+    if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess || n == 0) return 0;
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return 0;
+    int k = 0;
+    for (size_t i = 0; i < n; i++) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) k++;
+    }
+    return k;
+}
+
+extern "C" long long rb_launch_count(void);
+static thread_local long long g_capture_mark = 0;
+
 extern "C" int rb_graph_begin(void *stream) {
     if (!stream) return RB_ERR_ARGUMENT;  // the legacy default stream cannot capture
+    g_capture_mark = rb_launch_count();
     return cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal) ==
                    cudaSuccess
                ? RB_OK : RB_ERR_CUDA;
@@ -100,6 +125,8 @@ extern "C" int rb_graph_begin(void *stream) {
 extern "C" int rb_graph_end(void *stream, uint64_t *exec) {
     if (!stream || !exec) return RB_ERR_ARGUMENT;
     cudaGraph_t g = nullptr;
+    // captured launches did not run: they count when the graph is launched
+    note_launches((int)(g_capture_mark - rb_launch_count()));
     if (cudaStreamEndCapture(as_stream(stream), &g) != cudaSuccess || !g) return RB_ERR_CUDA;
     cudaGraphExec_t ex = reinterpret_cast<cudaGraphExec_t>(*exec);
     bool ok = false;
@@ -113,24 +140,34 @@ extern "C" int rb_graph_end(void *stream, uint64_t *exec) {
         }
     }
     if (!ok) ok = cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    const int kernels = count_kernel_nodes(g);
     cudaGraphDestroy(g);
     if (!ok) {
         *exec = 0;
         return RB_ERR_CUDA;
     }
     *exec = reinterpret_cast<uint64_t>(ex);
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    g_graph_kernels[*exec] = kernels;
     return RB_OK;
 }
 
 extern "C" int rb_graph_launch(uint64_t exec, void *stream) {
     if (!exec) return RB_ERR_ARGUMENT;
-    return cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(exec), as_stream(stream)) ==
-                   cudaSuccess
-               ? RB_OK : RB_ERR_CUDA;
+    if (cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(exec), as_stream(stream)) != cudaSuccess)
+        return RB_ERR_CUDA;
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    const auto it = g_graph_kernels.find(exec);
+    if (it != g_graph_kernels.end()) note_launches(it->second);
+    return RB_OK;
 }
 
 extern "C" int rb_graph_destroy(uint64_t exec) {
     if (!exec) return RB_OK;
+    {
+        std::lock_guard<std::mutex> lock(g_graph_mu);
+        g_graph_kernels.erase(exec);
+    }
     return cudaGraphExecDestroy(reinterpret_cast<cudaGraphExec_t>(exec)) == cudaSuccess
                ? RB_OK : RB_ERR_CUDA;
 }

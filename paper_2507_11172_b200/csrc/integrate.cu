@@ -239,6 +239,28 @@ __global__ void k_final_sum(int nb, const Tacc *__restrict__ partial, Tacc *__re
 // partials in index order and writes the trace row.
 constexpr int kSampleQ = 5;
 
+// block_tree_sum of five values at once: the same shuffle tree and the same
+// warp-0 fold per value (bit-identical), one __syncthreads for all five
+__device__ __forceinline__ void block_tree_sum5(double v[kSampleQ], double (*sh)[32]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < kSampleQ; q++) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+        if (lane == 0) sh[q][warp] = v[q];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int q = 0; q < kSampleQ; q++) {
+            double t = lane < (int)(blockDim.x >> 5) ? sh[q][lane] : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            v[q] = t;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kRedThreads)
     k_sample(int64_t n, const double *__restrict__ vel, const double *__restrict__ e2,
              const double *__restrict__ w2, const double *__restrict__ e3,
@@ -246,47 +268,59 @@ __global__ void __launch_bounds__(kRedThreads)
              const unsigned long long *status, int64_t interval, double *trace,
              double *__restrict__ partial, unsigned int *ticket) {
     pdl_enter();
-    __shared__ double sh[32];
+    __shared__ double sh[kSampleQ][32];
     __shared__ bool last;
-    {  // sum v^2 over the 3n components (partition of 3n)
-        const int64_t len = 3 * n;
-        const int nb = red_blocks(len);
-        double acc = 0.0;
-        if ((int)blockIdx.x < nb) {
-            const int64_t chunk = (len + nb - 1) / nb;
-            const int64_t b = (int64_t)blockIdx.x * chunk;
-            const int64_t e = b + chunk < len ? b + chunk : len;
-#pragma unroll 4
-            for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) acc += vel[i] * vel[i];
-        }
-        const double t = block_tree_sum<double>(acc, sh);
-        if (threadIdx.x == 0 && (int)blockIdx.x < nb) partial[blockIdx.x] = t;
-        __syncthreads();
+    // the partitions of k_partial_sum: 3n components for sum v^2, n rank
+    // entries for E2, W2, E3, W3; every thread accumulates its stride in
+    // index order.  The first four elements of both partitions are loaded
+    // together (one memory round trip for the usual sizes).
+    const int64_t len = 3 * n;
+    const int nbA = red_blocks(len), nbB = red_blocks(n);
+    const int bid = (int)blockIdx.x;
+    int64_t ia = 0, ea = 0, ib = 0, eb = 0;
+    if (bid < nbA) {
+        const int64_t chunk = (len + nbA - 1) / nbA;
+        ia = (int64_t)bid * chunk + threadIdx.x;
+        ea = (int64_t)bid * chunk + chunk < len ? (int64_t)bid * chunk + chunk : len;
     }
-    {  // E2, W2, E3, W3 share the partition of n: one pass, four accumulators
-        const int nb = red_blocks(n);
-        double a2 = 0.0, b2 = 0.0, a3 = 0.0, b3 = 0.0;
-        if ((int)blockIdx.x < nb) {
-            const int64_t chunk = (n + nb - 1) / nb;
-            const int64_t b = (int64_t)blockIdx.x * chunk;
-            const int64_t e = b + chunk < n ? b + chunk : n;
-#pragma unroll 2
-            for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
-                a2 += e2[i];
-                b2 += w2[i];
-                a3 += e3[i];
-                b3 += w3[i];
-            }
-        }
-        const double acc[4] = {a2, b2, a3, b3};
+    if (bid < nbB) {
+        const int64_t chunk = (n + nbB - 1) / nbB;
+        ib = (int64_t)bid * chunk + threadIdx.x;
+        eb = (int64_t)bid * chunk + chunk < n ? (int64_t)bid * chunk + chunk : n;
+    }
+    constexpr int kPre = 4;
+    double va[kPre], vb[kPre][4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const double t = block_tree_sum<double>(acc[q], sh);
-            if (threadIdx.x == 0 && (int)blockIdx.x < nb) partial[(q + 1) * kRedMaxBlocks + blockIdx.x] = t;
-            __syncthreads();
+    for (int u = 0; u < kPre; u++) {
+        const int64_t i = ia + (int64_t)u * blockDim.x, j = ib + (int64_t)u * blockDim.x;
+        va[u] = i < ea ? vel[i] : 0.0;
+        vb[u][0] = j < eb ? e2[j] : 0.0;
+        vb[u][1] = j < eb ? w2[j] : 0.0;
+        vb[u][2] = j < eb ? e3[j] : 0.0;
+        vb[u][3] = j < eb ? w3[j] : 0.0;
+    }
+    double acc[kSampleQ] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < kPre; u++) {
+        if (ia + (int64_t)u * blockDim.x < ea) acc[0] += va[u] * va[u];
+        if (ib + (int64_t)u * blockDim.x < eb) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[1 + q] += vb[u][q];
         }
     }
+    for (int64_t i = ia + (int64_t)kPre * blockDim.x; i < ea; i += blockDim.x)
+        acc[0] += vel[i] * vel[i];
+    for (int64_t j = ib + (int64_t)kPre * blockDim.x; j < eb; j += blockDim.x) {
+        acc[1] += e2[j];
+        acc[2] += w2[j];
+        acc[3] += e3[j];
+        acc[4] += w3[j];
+    }
+    block_tree_sum5(acc, sh);
     if (threadIdx.x == 0) {
+        if (bid < nbA) partial[bid] = acc[0];
+        if (bid < nbB)
+            for (int q = 1; q < kSampleQ; q++) partial[q * kRedMaxBlocks + bid] = acc[q];
         __threadfence();
         last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
@@ -294,14 +328,14 @@ __global__ void __launch_bounds__(kRedThreads)
     if (!last) return;
     __threadfence();
     double out[kSampleQ];
+#pragma unroll
     for (int q = 0; q < kSampleQ; q++) {
-        const int nb = red_blocks(q == 0 ? 3 * n : n);
-        double acc = 0.0;
+        const int nb = q == 0 ? nbA : nbB;
+        out[q] = 0.0;
         for (int i = threadIdx.x; i < nb; i += blockDim.x)
-            acc += *(volatile const double *)(partial + q * kRedMaxBlocks + i);
-        out[q] = block_tree_sum<double>(acc, sh);
-        __syncthreads();
+            out[q] += *(volatile const double *)(partial + q * kRedMaxBlocks + i);
     }
+    block_tree_sum5(out, sh);
     if (threadIdx.x == 0) {
         for (int q = 0; q < kSampleQ; q++) sums[q] = out[q];
         if (trace) {

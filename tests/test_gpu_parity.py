@@ -550,3 +550,27 @@ def test_kick_folded_into_drift_is_bit_identical(pkg, monkeypatch):
     (a, ta), (b, tb) = out
     assert np.array_equal(a.positions, b.positions) and np.array_equal(a.velocities, b.velocities)
     assert np.array_equal(a.forces_2b, b.forces_2b) and ta.total == tb.total
+
+
+@pytest.mark.parametrize("n", [1, 1000, 32000, 250000])
+def test_sample_sums_equal_separate_reductions(pkg, n):
+    """rb_sample's five sums (one launch) are bit-identical to rb_reduce_sumsq
+    / rb_reduce_sum of the same arrays (250,000 particles: more than four
+    elements per thread)."""
+    import torch
+
+    from paper_2507_11172_b200.engine import ForceEngine
+
+    eng = ForceEngine(n)
+    gen = torch.Generator(device="cuda").manual_seed(n)
+    rnd = lambda *shape: torch.randn(*shape, dtype=torch.float64, device="cuda",  # noqa: E731
+                                     generator=gen)
+    v = rnd(n, 3)
+    for name in ("e2_rank", "w2_rank", "e3_rank", "w3_rank"):
+        getattr(eng, name)[:n] = rnd(n)
+    eng.sample(v)
+    got = eng.scalars[:5].clone()
+    eng.sum_f64(v.reshape(-1), 0, square=True, n=3 * n)
+    for slot, name in enumerate(("e2_rank", "w2_rank", "e3_rank", "w3_rank"), start=1):
+        eng.sum_f64(getattr(eng, name), slot)
+    assert torch.equal(got, eng.scalars[:5])

@@ -299,41 +299,45 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
                                        int32_t *ovf) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    tag = resolve_tag(tag, status);
-    if (warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
+    const int32_t *row = rows + r * (int64_t)capacity;
+    const int32_t *mir = mirror + r * (int64_t)capacity;
+    // phase 0 is latency-bound: the first memory round trip carries the
+    // status words, the base's position and row length, and the first entry
+    // of every 32-entry chunk of its row (rows are rank-sorted: S+(i) starts
+    // in the last chunk whose first entry precedes i)
+    const ulonglong2 s01 = ld_status2(status);
+    const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
+    const int rc_n = row_count[r];
+    const int chunk_first = 32 * lane < capacity ? row[32 * lane] : 0x7fffffff;
+    const unsigned long long swd = __shfl_sync(0xffffffffu, s01.x, 0);  // one view per warp
+    if (tag < 0) tag = status ? (int64_t)__shfl_sync(0xffffffffu, s01.y, 0) : 0;
+    if (status && frozen_word(swd, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
     if (kM > 0) slots = kM;
     const A3Smem sm = a3_carve<kM>(smem_raw + (size_t)warp * a3_warp_bytes(slots), slots);
     const Image im = make_image(g);
-    const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
-    const int rc_n = row_count[r];
-    const int32_t *row = rows + r * (int64_t)capacity;
-    const int32_t *mir = mirror + r * (int64_t)capacity;
     // partial forces go to the TARGET's row: G[q][position of i in row q], so
     // the gather of q reads its own row segment contiguously
 
     // ---- phase 0: S+(i), the row suffix with rank > i within rc
     int m = 0;
     bool slot_bad = false;
-    // rows are rank-sorted: start at the first 32-entry chunk whose last
-    // entry follows i (one load per chunk, in parallel, then a ballot)
     int first = 0;
     {
         const int nchunks = (rc_n + 31) >> 5;
-        bool after = false;
-        if (lane < nchunks) after = row[min(32 * lane + 31, rc_n - 1)] > r;
-        const unsigned b = __ballot_sync(0xffffffffu, after);
-        first = b ? 32 * (__ffs(b) - 1) : rc_n;
+        const unsigned b = __ballot_sync(0xffffffffu, lane < nchunks && chunk_first < r);
+        first = b ? 32 * (__popc(b) - 1) : 0;
         if (nchunks > 32) first = 0;  // longer rows than one ballot covers: scan all
     }
-    // two chunks per iteration: both rows' loads, then both positions' loads
-    // are in flight together (phase 0 is latency-bound)
+    // two chunks per iteration: both rows' (and mirror) loads, then both
+    // positions' loads are in flight together
     for (int base = first; base < rc_n; base += 64) {
-        int q2[2];
+        int q2[2], mk2[2];
         double px[2], py[2], pz[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int k = base + 32 * h + lane;
             q2[h] = k < rc_n ? row[k] : -1;
+            mk2[h] = k < rc_n ? mir[k] : 0;
         }
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -353,7 +357,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
                 r2 = exact_r2(dx, dy, dz);
                 keep = r2 <= rc2;
                 if (!keep) {  // beyond the three-body cutoff: contributes nothing
-                    double *gq = gbuf + ((int64_t)q * capacity + mir[k]) * 3;
+                    double *gq = gbuf + ((int64_t)q * capacity + mk2[h]) * 3;
                     gq[0] = 0.0;
                     gq[1] = 0.0;
                     gq[2] = 0.0;

@@ -50,10 +50,12 @@ struct A3Smem {
     double2 *axy;    // force accumulators (units of 2 nu), x and y
     double *az;      //   ... z
     int32_t *kidx;   // row index | owned << 30
+    int32_t *q;      // the slot's particle (rank) ...
+    int32_t *mpos;   //   ... and the base's position in its row (G target)
 };
 
 __host__ __device__ inline size_t a3_warp_bytes(int m) {
-    size_t b = (size_t)m * (2 * sizeof(double2) + 3 * sizeof(double) + sizeof(int32_t));
+    size_t b = (size_t)m * (2 * sizeof(double2) + 3 * sizeof(double) + 3 * sizeof(int32_t));
     return (b + 15) & ~(size_t)15;
 }
 
@@ -69,6 +71,8 @@ __device__ __forceinline__ A3Smem a3_carve(char *base, int m_rt) {
     s.r2 = s.dz + m;
     s.az = s.r2 + m;
     s.kidx = (int32_t *)(s.az + m);
+    s.q = s.kidx + m;
+    s.mpos = s.q + m;
     return s;
 }
 
@@ -188,7 +192,7 @@ __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int 
     bool in;
     if (kExactImage) {
         const Image im = make_image(g);
-        const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
+        const int j = sm.q[s], k = sm.q[t];
         exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
                    pr[3 * k + 2], jkx, jky, jkz);
         c = exact_r2(jkx, jky, jkz);
@@ -203,7 +207,7 @@ __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int 
         if (__any_sync(0xffffffffu, band)) {  // rare: the reference arithmetic decides
             if (band) {
                 const Image im = make_image(g);  // from the kernel parameters, on demand
-                const int j = row[sm.kidx[s] & kKidxMask], k = row[sm.kidx[t] & kKidxMask];
+                const int j = sm.q[s], k = sm.q[t];
                 double ex, ey, ez;
                 exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k],
                            pr[3 * k + 1], pr[3 * k + 2], ex, ey, ez);
@@ -379,6 +383,8 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
                 sm.dz[slot] = dz;
                 sm.r2[slot] = r2;
                 sm.kidx[slot] = k | ((kOwned ? (int)owned[q] : 1) << 30);
+                sm.q[slot] = q;
+                sm.mpos[slot] = mk2[h];
                 sm.axy[slot] = make_double2(0.0, 0.0);
                 sm.az[slot] = 0.0;
             }
@@ -404,10 +410,9 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     // image: both keep the per-triplet sum)
     double sx = 0.0, sy = 0.0, sz = 0.0, sw = 0.0;
     for (int sl = lane; sl < m; sl += 32) {
-        const int k = sm.kidx[sl] & kKidxMask;
         const double2 xy = sm.axy[sl];
         const double z = sm.az[sl];
-        double *gq = gbuf + ((int64_t)row[k] * capacity + mir[k]) * 3;
+        double *gq = gbuf + ((int64_t)sm.q[sl] * capacity + sm.mpos[sl]) * 3;
         gq[0] = xy.x;
         gq[1] = xy.y;
         gq[2] = z;

@@ -152,8 +152,10 @@ RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_co
  * fixed order (deterministic).  Writes forces (n,3) in particle order
  * (overwritten), per-rank energy (phi per owned triplet), virial and the
  * number of owned (unique) triplets.  Scratch: rb_atm_scratch_bytes,
- * zero-filled before its first use (each pass leaves its overflow-list
- * count at zero).  slot_capacity (<= capacity) sizes the per-warp
+ * zero-filled before its first use (each pass leaves its work counter and
+ * overflow-list count at zero; they sit at fixed offsets, so one scratch
+ * serves passes of any n up to the size it was made for).  Persistent warps
+ * take the bases from a work counter (RB_ATM_PERSIST=0: one base per warp).  slot_capacity (<= capacity) sizes the per-warp
  * shared-memory slots; a particle with more higher-rank neighbours than
  * that records RB_KIND_CAPACITY in the status word (pass the longest row
  * length).  The pass runs most particles with about half the slots (higher

@@ -29,6 +29,8 @@
 // virial -2(E_a a + E_b b + E_c c) per triplet (:530 summed over visits).
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 #include <type_traits>
@@ -450,14 +452,36 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
            double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
-           unsigned long long *status, int64_t tag, int debug_mode, int32_t *ovf) {
+           unsigned long long *status, int64_t tag, int debug_mode, int32_t *ovf,
+           int32_t *work) {
     pdl_enter();
     extern __shared__ __align__(16) char smem_raw[];
-    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (r >= n) return;
-    a3_base<kExactImage, kOwned, kM>(r, smem_raw, g, n, pr, rows, row_count, mirror, capacity, slots, rc2, rc2_lo,
-                            rc2_hi, own, gbuf, energy_rank, virial_rank,
-                            triplets_rank, owned, status, tag, debug_mode, ovf);
+    if (!work) {  // one base per warp
+        const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        if (r >= n) return;
+        a3_base<kExactImage, kOwned, kM>(r, smem_raw, g, n, pr, rows, row_count, mirror,
+                                         capacity, slots, rc2, rc2_lo, rc2_hi, own, gbuf,
+                                         energy_rank, virial_rank, triplets_rank, owned, status,
+                                         tag, debug_mode, ovf);
+        return;
+    }
+    // persistent warps: the next base comes from a global counter (reset by
+    // the gather), fetched one base ahead, so no warp idles behind the
+    // slowest base of its block; every base writes only its own outputs
+    const int lane = threadIdx.x & 31;
+    int r = 0;
+    if (lane == 0) r = atomicAdd(work, 1);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    while (r < n) {
+        int nxt = 0;
+        if (lane == 0) nxt = atomicAdd(work, 1);
+        a3_base<kExactImage, kOwned, kM>(r, smem_raw, g, n, pr, rows, row_count, mirror, capacity,
+                                         slots, rc2, rc2_lo, rc2_hi, own, gbuf, energy_rank,
+                                         virial_rank, triplets_rank, owned, status, tag,
+                                         debug_mode, ovf);
+        __syncwarp();  // the warp's slots are reused by its next base
+        r = __shfl_sync(0xffffffffu, nxt, 0);
+    }
 }
 
 // the bases listed by the main pass, with the full slot count
@@ -502,6 +526,7 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // list empty for the next pass
         ovf[1] = ovf[0];                           // (count of this pass: diagnostic)
         ovf[0] = 0;
+        ovf[-1] = 0;                               // base counter of the persistent pass
     }
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t p = gid / kGatherGroup;
@@ -567,10 +592,15 @@ static void a3_grant(K kernel, size_t bytes, size_t &granted) {
 
 using namespace rb;
 
+static size_t a3_header_bytes(size_t n) { return ((n + 3) * sizeof(int32_t) + 255) & ~(size_t)255; }
+
 extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
-    // own (n x 3) + G (n x capacity x 3), doubles; overflow list (1 + n) int32
+    // header at a fixed offset (independent of n, which a decomposed run
+    // changes between passes): the persistent pass's base counter, the
+    // overflow count, a diagnostic copy of it, then the overflow list (n);
+    // after it (256-byte aligned) own (n x 3) and G (n x capacity x 3) doubles
     const size_t nn = (size_t)(n > 0 ? n : 1);
-    return nn * 3 * sizeof(double) * (size_t)(1 + capacity) + (nn + 2) * sizeof(int32_t);
+    return a3_header_bytes(nn) + nn * 3 * sizeof(double) * (size_t)(1 + capacity);
 }
 
 namespace rb {
@@ -602,13 +632,31 @@ static void a3_launch_main(cudaStream_t st, int64_t n, int warps, size_t per, co
                            double lo, double hi, double *own, double *gbuf,
                            double *energy_rank, double *virial_rank, int32_t *triplets_rank,
                            const uint8_t *owned, unsigned long long *status, int64_t tag,
-                           int debug_mode, int32_t *ovf) {
+                           int debug_mode, int32_t *ovf, int32_t *work) {
     static size_t granted = 0;
+    static int resident = 0;  // co-resident blocks per SM at this shared-memory size
+    static size_t resident_for = 0;
     a3_grant(k_atm3<kExactImage, kOwned, kM>, warps * per, granted);
-    launch(k_atm3<kExactImage, kOwned, kM>, dim3((unsigned)((n + warps - 1) / warps)),
-           dim3(warps * 32), warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity,
-           fast, rc2, lo, hi, own, gbuf, energy_rank, virial_rank, triplets_rank, owned,
-           status, tag, debug_mode, ovf);
+    int64_t blocks = (n + warps - 1) / warps;
+    if (work) {
+        if (resident_for != warps * per) {
+            int per_sm = 0, dev = 0, sms = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_atm3<kExactImage, kOwned, kM>,
+                                                          warps * 32, warps * per);
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            resident = std::max(1, per_sm) * std::max(1, sms);
+            resident_for = warps * per;
+        }
+        // measured: worth it only with many bases per warp (cfg4: -4 %;
+        // cfg2, 8 bases per warp: +9 %)
+        if (n > 64 * (int64_t)resident * warps) blocks = std::min<int64_t>(blocks, resident);
+        else work = nullptr;
+    }
+    launch(k_atm3<kExactImage, kOwned, kM>, dim3((unsigned)blocks), dim3(warps * 32),
+           warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity, fast, rc2, lo, hi,
+           own, gbuf, energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
+           ovf, work);
     note_launches(1);
 }
 
@@ -618,7 +666,7 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
                       int32_t capacity, int fast, int full, double rc2, double lo, double hi,
                       double *own, double *gbuf, double *energy_rank, double *virial_rank,
                       int32_t *triplets_rank, const uint8_t *owned, unsigned long long *status,
-                      int64_t tag, int debug_mode, int32_t *ovf) {
+                      int64_t tag, int debug_mode, int32_t *ovf, int32_t *work) {
     static size_t granted_ovf = 0;
     const size_t per = a3_warp_bytes(fast);
     const int warps = a3_warps_for(per);
@@ -629,17 +677,17 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
         a3_launch_main<kExactImage, kOwned, 64>(st, n, warps, per, g, pos_r, rows, row_count,
                                                 mirror, capacity, fast, rc2, lo, hi, own,
                                                 gbuf, energy_rank, virial_rank, triplets_rank,
-                                                owned, status, tag, debug_mode, list);
+                                                owned, status, tag, debug_mode, list, work);
     else if (fast == 96)
         a3_launch_main<kExactImage, kOwned, 96>(st, n, warps, per, g, pos_r, rows, row_count,
                                                 mirror, capacity, fast, rc2, lo, hi, own,
                                                 gbuf, energy_rank, virial_rank, triplets_rank,
-                                                owned, status, tag, debug_mode, list);
+                                                owned, status, tag, debug_mode, list, work);
     else
         a3_launch_main<kExactImage, kOwned, 0>(st, n, warps, per, g, pos_r, rows, row_count,
                                                mirror, capacity, fast, rc2, lo, hi, own,
                                                gbuf, energy_rank, virial_rank, triplets_rank,
-                                               owned, status, tag, debug_mode, list);
+                                               owned, status, tag, debug_mode, list, work);
     if (!split) return;
     const size_t per_full = a3_warp_bytes(full);
     const int wf = a3_warps_for(per_full);
@@ -675,16 +723,19 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
     if (!a3_warps_for(a3_warp_bytes(slot_capacity))) return RB_ERR_ARGUMENT;
     const int fast = no_split ? slot_capacity : a3_fast_slots(slot_capacity);
     cudaStream_t st = as_stream(stream);
-    double *own = (double *)scratch;
+    int32_t *work_word = (int32_t *)scratch;
+    int32_t *ovf = work_word + 1;
+    double *own = (double *)((char *)scratch + a3_header_bytes((size_t)n));
     double *gbuf = own + 3 * n;
-    int32_t *ovf = (int32_t *)(gbuf + (size_t)n * capacity * 3);
     const double lo = exact_image ? rc2 : rc2 * (1.0 - kA3Margin);
     const double hi = exact_image ? rc2 : rc2 * (1.0 + kA3Margin);
+    static const bool persist = !(getenv("RB_ATM_PERSIST") && atoi(getenv("RB_ATM_PERSIST")) == 0);
+    int32_t *work = persist ? work_word : nullptr;
     auto go = [&](auto exact, auto with_owned) {
         a3_launch<decltype(exact)::value, decltype(with_owned)::value>(
             st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity, rc2, lo, hi,
             own, gbuf, energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
-            ovf);
+            ovf, work);
     };
     using T = std::true_type;
     using F = std::false_type;

@@ -231,8 +231,8 @@ def test_triplet_overflow_launch_matches_oracle(pkg, oracle):
     assert eng.slots > 128
     import torch
 
-    words = eng.atm_scratch.view(torch.int32)  # own, G (doubles), then the overflow list
-    listed = int(words[2 * eng.n * 3 * (1 + eng.capacity) + 1].item())  # last pass's count
+    words = eng.atm_scratch.view(torch.int32)  # base counter, count, diagnostic, list, ...
+    listed = int(words[2].item())  # the last pass's overflow count
     assert 0 < listed < eng.n
     os_ = oracle.OracleSystem.from_positions(s.positions, s.box, True)
     off = oracle.OracleForceField(nu=0.4, cutoff=3.4)

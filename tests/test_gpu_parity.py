@@ -574,3 +574,49 @@ def test_sample_sums_equal_separate_reductions(pkg, n):
     for slot, name in enumerate(("e2_rank", "w2_rank", "e3_rank", "w3_rank"), start=1):
         eng.sum_f64(getattr(eng, name), slot)
     assert torch.equal(got, eng.scalars[:5])
+
+
+_TINY = np.array([[2.0, 2.0, 2.0], [3.2, 2.0, 2.0], [2.6, 3.0392304845413265, 2.0],
+                  [2.6, 2.3464101615137756, 3.0], [5.2, 5.1, 4.9]])
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_tiny_systems_match_oracle(pkg, oracle, n, periodic):
+    """Empty (rejected, as the reference does), single-particle, one-pair and
+    one-triplet systems (and a particle out of everyone's range) through the
+    container passes and the device r-RESPA loop: same forces, scalars,
+    triplet counts and trajectory as the oracle."""
+    box = (6.5, 6.5, 6.5)
+    pos = _TINY[:n].copy()
+    rng = np.random.default_rng(40 + n)
+    vel = rng.normal(0.0, 0.5, size=(n, 3))
+    ff = pkg.ForceField(nu=0.5, cutoff=2.5)
+    if n == 0:  # the reference rejects an empty system on construction (model.py:94-97)
+        with pytest.raises(pkg.ValidationError):
+            _system(pkg, pos, box, periodic, vel)
+        return
+    s = _system(pkg, pos, box, periodic, vel)
+    c = pkg.CudaLinkedCells()
+    c.pair_pass(s, ff)
+    c.triplet_pass(s, ff)
+    os_ = oracle.OracleSystem.from_positions(pos, np.array(box), periodic, vel)
+    off = oracle.OracleForceField(nu=0.5, cutoff=2.5)
+    oc = oracle.OracleLinkedCells()
+    oc.pair_pass(os_, off)
+    oc.triplet_pass(os_, off)
+    assert s.forces_2b.shape == (n, 3) and s.forces_3b.shape == (n, 3)
+    assert normwise(s.forces_2b, os_.forces_2b) <= FORCE_TOL
+    assert normwise(s.forces_3b, os_.forces_3b) <= FORCE_TOL
+    assert abs(c.pair_energy - oc.pair_energy) <= ENERGY_TOL * max(1.0, abs(oc.pair_energy))
+    assert abs(c.triplet_energy - oc.triplet_energy) <= ENERGY_TOL * max(1.0, abs(oc.triplet_energy))
+    assert c.triplet_count == {3: 1, 4: 4, 5: 4}.get(n, 0)
+    # the device loop
+    a = _system(pkg, pos, box, periodic, vel)
+    tr = pkg.respa_run(a, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 2, 20))
+    b = oracle.OracleSystem.from_positions(pos, np.array(box), periodic, vel)
+    rtr = oracle.respa_run(b, off, oracle.OracleLinkedCells(), 0.002, 2, 20)
+    assert list(tr.iterations) == list(rtr.iterations)
+    assert np.max(np.abs(a.positions - b.positions), initial=0.0) <= 1e-10
+    assert np.max(np.abs(a.velocities - b.velocities), initial=0.0) <= 1e-10
+    assert max((abs(x - y) for x, y in zip(tr.total, rtr.total)), default=0.0) <= 1e-10

@@ -125,7 +125,7 @@ class DeviceRespa:
     same step, so every pair within the cutoff is always in the rows.  Open
     systems rebuild every step (their grid follows the particles)."""
 
-    DEFAULT_SKIN = 0.3
+    DEFAULT_SKIN = float(os.environ.get("RB_SKIN", "0.3"))  # Verlet skin (sigma)
 
     def __init__(self, system, ff, container, schedule: RespaSchedule, sample_interval: int,
                  capacity: Optional[int] = None, use_graph: bool = True,

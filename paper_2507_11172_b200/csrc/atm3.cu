@@ -37,7 +37,10 @@
 
 namespace rb {
 
-constexpr int kA3Warps = 4;
+#ifndef RB_A3_WARPS
+#define RB_A3_WARPS 4
+#endif
+constexpr int kA3Warps = RB_A3_WARPS;
 #ifndef RB_A3_MIN_BLOCKS
 #define RB_A3_MIN_BLOCKS 7
 #endif
@@ -83,7 +86,6 @@ struct A3Acc {
     int n;
     bool bad;
     int owned_i;     // decomposed runs: the base particle is owned by this rank
-    bool slot_bad;   // some r_ij^2 of S+(i) is under the guard (checked per triplet then)
 };
 
 constexpr int kKidxMask = 0x3fffffff;
@@ -174,22 +176,31 @@ __device__ __forceinline__ void a3_add(double2 *axy, double *az, int slot, const
 // d_ik - d_ij outside a 1e-10 band, else the reference's raw-position
 // arithmetic; always the latter when the box is under four cutoffs).
 //
-// a3_pair is one window step for one lane: the pair (s, t) (live), its
-// acceptance, the ATM kernel (a3_core) and the two accumulator sub-steps.
+// a3_eval is one window step for one lane up to the accumulation: the pair
+// (s, t) (live), its acceptance and the ATM kernel (a3_core).  The kernel is
+// evaluated unconditionally (the warp runs it whenever one lane accepts) and
+// the result selected.
 // kJReg (m < 32: the lane's first slot is always s = lane): f_j goes to the
 // lane's register accumulator aj instead of the shared slot.
-template <bool kExactImage, bool kOwned, bool kJReg>
-__device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int t,
-                                        const rb_grid &g, const int32_t *__restrict__ row,
-                                        const double *__restrict__ pr, double rc2, double rc2_lo,
-                                        double rc2_hi, A3Acc &acc, double aj[3],
-                                        const double own[4]) {
+struct A3Pair {
+    bool in;
+    int s, t;
+    double fj[3], fk[3];
+};
+
+template <bool kExactImage, bool kOwned, bool kJReg, bool kSlotBad>
+__device__ __forceinline__ void a3_eval(const A3Smem &sm, bool live, int s, int t,
+                                        const rb_grid &g, const double *__restrict__ pr,
+                                        double rc2, double rc2_lo, double rc2_hi, A3Acc &acc,
+                                        const double own[4], A3Pair &P) {
     if (!live) s = t = 0;  // every lane runs the same code; dead lanes accept nothing
     // kJReg: slot s is the lane's own, preloaded in `own` (d_ij, r_ij^2)
     const double2 ij = kJReg ? make_double2(own[0], own[1]) : sm.dxy[s];
     const double ijz = kJReg ? own[2] : sm.dz[s];
+    const double a = kJReg ? own[3] : sm.r2[s];
     const double2 ik = sm.dxy[t];
     const double ikz = sm.dz[t];
+    const double b = sm.r2[t];
     double jkx, jky, jkz, c;
     bool in;
     if (kExactImage) {
@@ -220,49 +231,58 @@ __device__ __forceinline__ void a3_pair(const A3Smem &sm, bool live, int s, int 
     // guard (potentials.py:35-36): a triplet with a side under it is flagged
     // and skipped; r_jk here, r_ij / r_ik only if phase 0 saw one (uniform)
     bool bad = in && c < RB_MIN_DISTANCE_SQ;
-    if (acc.slot_bad)
-        bad = bad || (in && ((kJReg ? own[3] : sm.r2[s]) < RB_MIN_DISTANCE_SQ ||
-                             sm.r2[t] < RB_MIN_DISTANCE_SQ));
+    if (kSlotBad)  // (uniform per base: the loop is instantiated for both)
+        bad = bad || (in && (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ));
     acc.bad = acc.bad || bad;
     in = in && !bad;
-    double fj[3], fk[3];
-    if (in)
-        a3_core<kOwned, kOwned || kExactImage>(sm, s, t, kJReg ? own[3] : sm.r2[s], sm.r2[t], c,
-                                               ij, ijz, ik, ikz, jkx, jky, jkz, acc,
-                        fj, fk);
-    if (kJReg) {
-        if (in) {
-            aj[0] += fj[0];
-            aj[1] += fj[1];
-            aj[2] += fj[2];
-        }
-    } else {
-        __syncwarp();
-        if (in) a3_add(sm.axy, sm.az, s, fj);
-    }
-    __syncwarp();
-    if (in) a3_add(sm.axy, sm.az, t, fk);
+    A3Acc tmp = acc;
+    a3_core<kOwned, kOwned || kExactImage>(sm, s, t, a, b, c, ij, ijz, ik, ikz, jkx, jky, jkz,
+                                           tmp, P.fj, P.fk);
+    if (in) acc = tmp;
+    P.in = in;
+    P.s = s;
+    P.t = t;
 }
 
-template <bool kExactImage, bool kOwned>
+__device__ __forceinline__ void a3_add_j(const A3Smem &sm, const A3Pair &P) {
+    __syncwarp();
+    if (P.in) a3_add(sm.axy, sm.az, P.s, P.fj);
+}
+
+__device__ __forceinline__ void a3_add_k(const A3Smem &sm, const A3Pair &P) {
+    __syncwarp();
+    if (P.in) a3_add(sm.axy, sm.az, P.t, P.fk);
+}
+
+__device__ __forceinline__ void a3_add_reg(double aj[3], const A3Pair &P) {
+    if (P.in) {
+        aj[0] += P.fj[0];
+        aj[1] += P.fj[1];
+        aj[2] += P.fj[2];
+    }
+}
+
+template <bool kExactImage, bool kOwned, bool kSlotBad>
 __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, const rb_grid &g,
-                                           const int32_t *__restrict__ row,
                                            const double *__restrict__ pr, double rc2,
                                            double rc2_lo, double rc2_hi, A3Acc &acc) {
     double aj[3] = {0.0, 0.0, 0.0}, own[4] = {0.0, 0.0, 0.0, 0.0};
+    A3Pair P;
     if (m >= 32) {
         const int pairs = m * (m - 1) / 2;
         int s = lane, d = 1;  // pair f = f0 + lane is (round d, slot s)
         for (int f0 = 0; f0 < pairs; f0 += 32) {
             int t = s + d;
             if (t >= m) t -= m;
-            a3_pair<kExactImage, kOwned, false>(sm, f0 + lane < pairs, s, t, g, row, pr, rc2,
-                                                rc2_lo, rc2_hi, acc, aj, own);
+            a3_eval<kExactImage, kOwned, false, kSlotBad>(sm, f0 + lane < pairs, s, t, g, pr, rc2, rc2_lo,
+                                                rc2_hi, acc, own, P);
             s += 32;
             if (s >= m) {
                 s -= m;
                 d += 1;
             }
+            a3_add_j(sm, P);
+            a3_add_k(sm, P);
         }
     } else {
         if (lane < m) {
@@ -276,8 +296,10 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, co
             const int lim = 2 * d == m ? d : m;  // even m: the last round is half
             int t = lane + d;
             if (t >= m) t -= m;
-            a3_pair<kExactImage, kOwned, true>(sm, lane < lim, lane, t, g, row, pr, rc2, rc2_lo,
-                                               rc2_hi, acc, aj, own);
+            a3_eval<kExactImage, kOwned, true, kSlotBad>(sm, lane < lim, lane, t, g, pr, rc2, rc2_lo,
+                                               rc2_hi, acc, own, P);
+            a3_add_reg(aj, P);
+            a3_add_k(sm, P);
         }
         __syncwarp();
         if (lane < m) a3_add(sm.axy, sm.az, lane, aj);  // the j-role sums of slot `lane`
@@ -397,9 +419,13 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     __syncwarp();
 
     // ---- phase 1: the slot pairs, 32 per window (a3_windows)
-    A3Acc acc = {0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1, slot_bad};
-    if (debug_mode != 1)  // debug 1: phases 0 and 3 only
-        a3_windows<kExactImage, kOwned>(sm, m, lane, g, row, pr, rc2, rc2_lo, rc2_hi, acc);
+    A3Acc acc = {0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1};
+    if (debug_mode != 1) {  // debug 1: phases 0 and 3 only
+        if (slot_bad)
+            a3_windows<kExactImage, kOwned, true>(sm, m, lane, g, pr, rc2, rc2_lo, rc2_hi, acc);
+        else
+            a3_windows<kExactImage, kOwned, false>(sm, m, lane, g, pr, rc2, rc2_lo, rc2_hi, acc);
+    }
     __syncwarp();
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars.  Per
@@ -635,25 +661,29 @@ static void a3_launch_main(cudaStream_t st, int64_t n, int warps, size_t per, co
                            int debug_mode, int32_t *ovf, int32_t *work) {
     static size_t granted = 0;
     static int resident = 0;  // co-resident blocks per SM at this shared-memory size
+    static const int64_t persist_min =
+        getenv("RB_ATM_PERSIST_MIN") ? atoll(getenv("RB_ATM_PERSIST_MIN")) : 1;
     static size_t resident_for = 0;
-    a3_grant(k_atm3<kExactImage, kOwned, kM>, warps * per, granted);
+    auto kern = k_atm3<kExactImage, kOwned, kM>;
+    a3_grant(kern, warps * per, granted);
     int64_t blocks = (n + warps - 1) / warps;
     if (work) {
         if (resident_for != warps * per) {
             int per_sm = 0, dev = 0, sms = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_atm3<kExactImage, kOwned, kM>,
-                                                          warps * 32, warps * per);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, warps * per);
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             resident = std::max(1, per_sm) * std::max(1, sms);
             resident_for = warps * per;
         }
-        // measured: worth it only with many bases per warp (cfg4: -4 %;
-        // cfg2, 8 bases per warp: +9 %)
-        if (n > 64 * (int64_t)resident * warps) blocks = std::min<int64_t>(blocks, resident);
+        // measured (B200, skin rows, kernel_bench): persistent warps win at
+        // every size once the core runs unconditionally (cfg2 -3 %,
+        // cfg3@2.5 -12 %, cfg4 0 %); RB_ATM_PERSIST_MIN = minimum bases
+        // per resident warp (tuning only)
+        if (n > persist_min * (int64_t)resident * warps) blocks = std::min<int64_t>(blocks, resident);
         else work = nullptr;
     }
-    launch(k_atm3<kExactImage, kOwned, kM>, dim3((unsigned)blocks), dim3(warps * 32),
+    launch(kern, dim3((unsigned)blocks), dim3(warps * 32),
            warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity, fast, rc2, lo, hi,
            own, gbuf, energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
            ovf, work);

@@ -62,6 +62,10 @@ def parse_args():
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--config", default="cfg2")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--rc3", type=float, default=None,
+                   help="three-body cutoff override (cfg3 sweep: 2.0 / 2.5 / 3.0)")
+    p.add_argument("--sf", type=int, default=None,
+                   help="three-body step-size factor override (cfg3 sweep: 1 / 5 / 10)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
 
@@ -128,6 +132,13 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 # CPU legs (the oracle port of the reference kernels)
 # --------------------------------------------------------------------------
+def workload_name(cfg) -> str:
+    if cfg.name == "cfg2" and cfg.rc_atm == 2.5 and cfg.step_size_factor == 5:
+        return WORKLOAD
+    return (f"{cfg.name}: {cfg.description}; LJ rc {cfg.rc_lj}, ATM rc {cfg.rc_atm}, "
+            f"three-body factor {cfg.step_size_factor} (sweep point, not the headline)")
+
+
 def cpu_respa_rate(cfg, seconds: float, threads: int):
     """Steps/s of the reference loop restated in oracle/ on `threads` cores.
 
@@ -177,9 +188,9 @@ def reference_arm(args, cfg):
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": 1e3 / rate,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded FCC lattice + jitter, SURVEY.md §8d)",
-        "config": {"workload": WORKLOAD, "timed": "respa_run incl. its two initial passes"},
+        "config": {"workload": workload_name(cfg), "timed": "respa_run incl. its two initial passes"},
         "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": threads, "kind": "port",
-                         "sample": f"{steps} r-RESPA steps of cfg2 (oracle/ C port of respamd "
+                         "sample": f"{steps} r-RESPA steps of {cfg.name} (oracle/ C port of respamd "
                                    f"kernels, OpenMP {threads} threads)"},
         "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -484,7 +495,7 @@ def ours_arm(args, cfg):
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded FCC lattice + jitter, SURVEY.md §8d; no public dataset)",
-        "config": {"workload": WORKLOAD, "particles": n, "step_size_factor": sf,
+        "config": {"workload": workload_name(cfg), "particles": n, "step_size_factor": sf,
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "graph": "one CUDA graph per 5-step sampling period; each step bracketed "
@@ -518,7 +529,7 @@ def ours_arm(args, cfg):
         threads = os.cpu_count() or 1
         rate, done, el = cpu_respa_rate(cfg, args.cpu_seconds, threads)
         line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": threads, "kind": "port",
-                                "sample": f"{done} r-RESPA steps of cfg2 in {el:.1f}s (oracle/ C "
+                                "sample": f"{done} r-RESPA steps of {cfg.name} in {el:.1f}s (oracle/ C "
                                           f"port of respamd kernels, OpenMP {threads} threads)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -531,6 +542,12 @@ def main():
     from paper_2507_11172_b200 import systems
 
     cfg = systems.CONFIGS[args.config]
+    if args.rc3 is not None or args.sf is not None:  # sweep points of a config (not the headline)
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, rc_atm=cfg.rc_atm if args.rc3 is None else args.rc3,
+                                  step_size_factor=cfg.step_size_factor if args.sf is None
+                                  else args.sf)
     if args.impl == "reference":
         reference_arm(args, cfg)
     else:

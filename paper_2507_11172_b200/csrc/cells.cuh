@@ -7,11 +7,20 @@
 namespace rb {
 
 // Loads of data written earlier in the SAME kernel (the fused rebuild, whose
-// phases are separated by grid barriers) must bypass L1 / the read-only
-// path: kCoherent selects L2-coherent loads (ld.global.cg).
+// phases are separated by grid barriers) must not take the read-only
+// (non-coherent) path, which nvcc may pick for a plain load through a const
+// __restrict__ pointer: kCoherent selects explicit weak loads cached in L1
+// (ld.global.ca).  They see the other blocks' writes because every grid
+// barrier ends with a __threadfence() (fence.sc: L1 invalidated) and a
+// __syncthreads(), the cooperative-groups grid.sync() pattern; the rows and
+// positions are re-read ~27x per phase, so L1 hits matter (RB_REBUILD_CG=1:
+// the former L2-only loads, for A/B).
+#ifndef RB_REBUILD_CG
+#define RB_REBUILD_CG 0
+#endif
 template <bool kCoherent, typename T>
 __device__ __forceinline__ T ldc(const T *p) {
-    if constexpr (kCoherent) return __ldcg(p);
+    if constexpr (kCoherent) return RB_REBUILD_CG ? __ldcg(p) : __ldca(p);
     else return *p;
 }
 

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // rebuild.cu -- the gated row rebuild of a captured r-RESPA step as ONE launch.
 //
 // Inside a captured step the rebuild (binning, rows, mirror: nine kernels)
@@ -24,6 +25,7 @@ namespace rb {
 constexpr int kRbThreads = 256;
 constexpr int kRbItems = 4;
 constexpr int kRbTile = kRbThreads * kRbItems;  // cells per scan tile
+constexpr int kRbChunkMax = 8;  // ranks per counter grab (rows and mirror phases), at most
 
 __device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
     __syncthreads();
@@ -41,6 +43,10 @@ __device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
     }
     __syncthreads();
 }
+
+// phase profiling (RB_REBUILD_STOP=k: the kernel returns after phase k;
+// timing experiments only, results are then incomplete)
+__device__ int g_rebuild_stop = 99;
 
 __global__ void __launch_bounds__(kRbThreads)
     k_rebuild(rb_grid g, int64_t n, const double *__restrict__ pos, int32_t *cell_start,
@@ -60,7 +66,16 @@ __global__ void __launch_bounds__(kRbThreads)
     const int64_t warp = tid >> 5, nwarp = nth >> 5;
     unsigned *bcount = bar, *bgen = bar + 1;
 
+    const int stop = g_rebuild_stop;
+    unsigned long long *work = (unsigned long long *)(bar + 4);  // chunk counters (rows, mirror)
+    if (tid == 0) work[0] = work[1] = 0;  // read only after later barriers
+    // chunk: 1 rank per grab while there are few ranks per warp (the chunk is
+    // the critical path), up to kRbChunkMax at 16+ ranks per warp
+    const int64_t per_warp = n / (nwarp > 0 ? nwarp : 1);
+    const int kRbChunk = per_warp >= 16 * kRbChunkMax ? kRbChunkMax
+                         : (per_warp >= 32 ? (int)(per_warp / 16) : 1);
     for (int64_t c = tid; c < ncell; c += nth) count[c] = 0;
+    if (stop <= 1) return;
     grid_barrier(bcount, bgen);
     // cell of every particle + histogram (bin.cu k_bin_count)
     for (int64_t i = tid; i < n; i += nth) {
@@ -71,6 +86,7 @@ __global__ void __launch_bounds__(kRbThreads)
         cell_of[i] = c;
         atomicAdd(&count[c], 1);
     }
+    if (stop <= 2) return;
     grid_barrier(bcount, bgen);
     // exclusive scan of the counts: tile sums, tile offsets, apply
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -84,6 +100,7 @@ __global__ void __launch_bounds__(kRbThreads)
         block_exclusive_scan(s, warp_sums, total);
         if (threadIdx.x == 0) tiles[t] = total;
     }
+    if (stop <= 3) return;
     grid_barrier(bcount, bgen);
     if (blockIdx.x == 0) {
         int carry = 0;
@@ -96,6 +113,7 @@ __global__ void __launch_bounds__(kRbThreads)
             carry += total;
         }
     }
+    if (stop <= 4) return;
     grid_barrier(bcount, bgen);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int vals[kRbItems];
@@ -119,22 +137,44 @@ __global__ void __launch_bounds__(kRbThreads)
             if (i == ncell - 1) cell_start[ncell] = ex;
         }
     }
+    if (stop <= 5) return;
     grid_barrier(bcount, bgen);
     // unordered scatter into the cell ranges (bin.cu k_bin_scatter)
     for (int64_t i = tid; i < n; i += nth) {
         const int slot = atomicAdd(&cursor[ldc<true>(cell_of + i)], 1);
         parts[slot] = (int32_t)i;
     }
+    if (stop <= 6) return;
     grid_barrier(bcount, bgen);
     for (int64_t c = warp; c < ncell; c += nwarp)
         cell_finish_one<true>(c, lane, cell_start, parts, cell_of_rank, rank_of, pos, pr, x_ref);
+    if (stop <= 7) return;
     grid_barrier(bcount, bgen);
-    for (int64_t r = warp; r < n; r += nwarp)
-        nlist_one<true>(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows, row_count,
-                        max_count);
+    // rows and mirror: warps take chunks of kRbChunk consecutive ranks from a
+    // counter, so the rows in flight stay a compact rank window (their
+    // neighbour cells / rows stay in L2); a grid-stride loop lets the warps
+    // drift apart over the ~300 rows each handles at 2 M particles and
+    // thrashes L2 (measured 2.7x slower than the separate kernels at cfg4)
+    for (;;) {
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(&work[0], (unsigned long long)kRbChunk);
+        const int64_t b = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+        if (b >= n) break;
+        const int64_t e = b + kRbChunk < n ? b + kRbChunk : n;
+        for (int64_t r = b; r < e; r++)
+            nlist_one<true>(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows,
+                            row_count, max_count);
+    }
+    if (stop <= 8) return;
     grid_barrier(bcount, bgen);
-    for (int64_t p = warp; p < n; p += nwarp)
-        mirror_one<true>(p, lane, rows, row_count, capacity, mirror);
+    for (;;) {
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(&work[1], (unsigned long long)kRbChunk);
+        const int64_t b = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+        if (b >= n) break;
+        const int64_t e = b + kRbChunk < n ? b + kRbChunk : n;
+        for (int64_t p = b; p < e; p++) mirror_one<true>(p, lane, rows, row_count, capacity, mirror);
+    }
 }
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -188,6 +228,8 @@ extern "C" int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_
     p += align256(sizeof(int32_t) * (size_t)ncell);
     int32_t *tiles = (int32_t *)p;
     const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
+    static const int stop = getenv("RB_REBUILD_STOP") ? atoi(getenv("RB_REBUILD_STOP")) : 0;
+    if (stop > 0) cudaMemcpyToSymbol(g_rebuild_stop, &stop, sizeof(int));
     launch(k_rebuild, dim3((unsigned)rebuild_grid()), dim3(kRbThreads), 0, as_stream(stream), *g,
            n, pos, cell_start, cell_particles, cell_of_rank, pos_r, rank_of, x_ref, rl2, capacity,
            rows, row_count, max_count, mirror, cell_of, count, cursor, tiles, bar, rebuild_flag,

@@ -85,11 +85,17 @@ def main(argv):
         t_lj = timed(lambda: eng.lj_kernel(geom, cfg.rc_lj, 1.0, 1.0, f, 0))
         t_bin = timed(lambda: eng.bin(geom))
         t_nl = timed(lambda: eng.nlist(geom, r_build, capacity=eng.capacity, checked=False))
+        # the fused gated rebuild of the device loop (bin + rows + mirror in
+        # one launch), gate open (flag == tag 0) and closed
+        eng.rebuild_flag.fill_(0)
+        t_rb = timed(lambda: eng.rebuild(geom, r_build, eng.capacity, tag=0, fused=True))
+        eng.rebuild_flag.fill_(-7)
+        t_rb0 = timed(lambda: eng.rebuild(geom, r_build, eng.capacity, tag=0, fused=True))
         tps = unique / (t_atm * 1e-3)
         print(json.dumps({
             "config": name, "skin": skin, "n": s.n, "unique_triplets": unique, "capacity": eng.capacity,
             "slots": eng.slots, "atm_ms": t_atm, "atm_c01_ms": t_c01, "lj_ms": t_lj,
-            "bin_ms": t_bin, "nlist_ms": t_nl, "triplets_per_s": tps,
+            "bin_ms": t_bin, "nlist_ms": t_nl, "rebuild_ms": t_rb, "rebuild_closed_ms": t_rb0, "triplets_per_s": tps,
             "fp64_tflops": tps * 141 / 1e12, "fp64_peak_tflops": peak.value,
             "frac": tps * 141 / 1e12 / peak.value,
         }), flush=True)

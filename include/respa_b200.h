@@ -171,6 +171,20 @@ RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r,
                        double *energy_rank, double *virial_rank, int32_t *triplets_rank,
                        const uint8_t *owned, void *scratch, size_t scratch_bytes,
                        unsigned long long *status, int64_t tag, void *stream);
+/* The same pass in two stream-ordered parts (part 0 = both = rb_atm_pass):
+ * part 1 launches the triplet kernels, whose results stay in the scratch;
+ * part 2 the gather, which alone writes forces, energy_rank, virial_rank and
+ * triplets_rank.  Between them the caller may run the pair pass on another
+ * stream (the device loop overlaps it with the tail of part 1); a pair-pass
+ * error of the same step then still leaves the triplet outputs untouched. */
+RB_API int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r,
+                            const int32_t *cell_particles, const int32_t *rows,
+                            const int32_t *row_count, const int32_t *mirror, int32_t capacity,
+                            int32_t slot_capacity, double rc, double nu, double *forces,
+                            double *energy_rank, double *virial_rank, int32_t *triplets_rank,
+                            const uint8_t *owned, void *scratch, size_t scratch_bytes,
+                            unsigned long long *status, int64_t tag, int32_t part,
+                            void *stream);
 
 /* C01 (owner-computes) form of the same pass, as the reference traverses it:
  * every triplet visited once from each member, force stored on the base

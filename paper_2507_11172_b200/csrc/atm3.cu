@@ -545,8 +545,11 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
                               const int32_t *__restrict__ row_count,
                               const int32_t *__restrict__ mirror, int32_t capacity,
                               const double *__restrict__ own, const double *__restrict__ gbuf,
-                              double two_nu, double nu, double *__restrict__ forces,
-                              double *__restrict__ energy_rank, double *__restrict__ virial_rank,
+                              const double *__restrict__ e_s, const double *__restrict__ w_s,
+                              const int32_t *__restrict__ n_s, double two_nu, double nu,
+                              double *__restrict__ forces, double *__restrict__ energy_rank,
+                              double *__restrict__ virial_rank,
+                              int32_t *__restrict__ triplets_rank,
                               const unsigned long long *status, int64_t tag, int32_t *ovf) {
     pdl_enter();
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // list empty for the next pass
@@ -601,8 +604,9 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
         forces[3 * pp] = two_nu * (own[3 * p] + fx);
         forces[3 * pp + 1] = two_nu * (own[3 * p + 1] + fy);
         forces[3 * pp + 2] = two_nu * (own[3 * p + 2] + fz);
-        energy_rank[p] = nu * energy_rank[p];
-        virial_rank[p] = -two_nu * virial_rank[p];
+        energy_rank[p] = nu * e_s[p];
+        virial_rank[p] = -two_nu * w_s[p];
+        triplets_rank[p] = n_s[p];
     }
 }
 
@@ -624,9 +628,14 @@ extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
     // header at a fixed offset (independent of n, which a decomposed run
     // changes between passes): the persistent pass's base counter, the
     // overflow count, a diagnostic copy of it, then the overflow list (n);
-    // after it (256-byte aligned) own (n x 3) and G (n x capacity x 3) doubles
+    // after it (256-byte aligned) own (n x 3), the per-base energy and
+    // virial sums (n each) and triplet counts (n int32, 8-byte padded) --
+    // every output the caller sees is written by the gather, so the triplet
+    // kernels may run concurrently with the pair pass -- then G
+    // (n x capacity x 3) doubles
     const size_t nn = (size_t)(n > 0 ? n : 1);
-    return a3_header_bytes(nn) + nn * 3 * sizeof(double) * (size_t)(1 + capacity);
+    return a3_header_bytes(nn) + nn * 5 * sizeof(double) + ((nn * sizeof(int32_t) + 7) & ~(size_t)7) +
+           nn * 3 * sizeof(double) * (size_t)capacity;
 }
 
 namespace rb {
@@ -732,12 +741,15 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
 }
 }  // namespace rb
 
-extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
-                           const int32_t *row_count, const int32_t *mirror, int32_t capacity,
-                           int32_t slot_capacity, double rc, double nu, double *forces, double *energy_rank,
-                           double *virial_rank, int32_t *triplets_rank, const uint8_t *owned,
-                           void *scratch, size_t scratch_bytes, unsigned long long *status,
-                           int64_t tag, void *stream) {
+extern "C" int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r,
+                                const int32_t *cell_particles, const int32_t *rows,
+                                const int32_t *row_count, const int32_t *mirror, int32_t capacity,
+                                int32_t slot_capacity, double rc, double nu, double *forces,
+                                double *energy_rank, double *virial_rank, int32_t *triplets_rank,
+                                const uint8_t *owned, void *scratch, size_t scratch_bytes,
+                                unsigned long long *status, int64_t tag, int32_t part,
+                                void *stream) {
+    if (part < 0 || part > 2) return RB_ERR_ARGUMENT;
     if (!g || n < 0 || capacity <= 0 || capacity > 4096 || !mirror || !scratch) return RB_ERR_ARGUMENT;
     if (slot_capacity <= 0 || slot_capacity > capacity) slot_capacity = capacity;
     if (slot_capacity > kA3MaxSlots) return RB_ERR_CAPACITY;
@@ -756,7 +768,9 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
     int32_t *work_word = (int32_t *)scratch;
     int32_t *ovf = work_word + 1;
     double *own = (double *)((char *)scratch + a3_header_bytes((size_t)n));
-    double *gbuf = own + 3 * n;
+    double *e_s = own + 3 * n, *w_s = e_s + n;
+    int32_t *n_s = (int32_t *)(w_s + n);
+    double *gbuf = (double *)((char *)n_s + (((size_t)n * sizeof(int32_t) + 7) & ~(size_t)7));
     const double lo = exact_image ? rc2 : rc2 * (1.0 - kA3Margin);
     const double hi = exact_image ? rc2 : rc2 * (1.0 + kA3Margin);
     static const bool persist = !(getenv("RB_ATM_PERSIST") && atoi(getenv("RB_ATM_PERSIST")) == 0);
@@ -764,19 +778,32 @@ extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, con
     auto go = [&](auto exact, auto with_owned) {
         a3_launch<decltype(exact)::value, decltype(with_owned)::value>(
             st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity, rc2, lo, hi,
-            own, gbuf, energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
-            ovf, work);
+            own, gbuf, e_s, w_s, n_s, owned, status, tag, debug_mode, ovf, work);
     };
     using T = std::true_type;
     using F = std::false_type;
-    if (exact_image)
-        owned ? go(T{}, T{}) : go(T{}, F{});
-    else
-        owned ? go(F{}, T{}) : go(F{}, F{});
+    if (part != 2) {
+        if (exact_image)
+            owned ? go(T{}, T{}) : go(T{}, F{});
+        else
+            owned ? go(F{}, T{}) : go(F{}, F{});
+    }
+    if (part == 1) return launch_status();
     const int tb = 256;
     const int64_t threads = n * kGatherGroup;
-    launch(k_atm3_gather, dim3((unsigned)((threads + tb - 1) / tb)), dim3(tb), 0, st, n, cell_particles, rows, row_count, mirror, capacity, own, gbuf, 2.0 * nu, nu, forces,
-        energy_rank, virial_rank, status, tag, ovf);
+    launch(k_atm3_gather, dim3((unsigned)((threads + tb - 1) / tb)), dim3(tb), 0, st, n, cell_particles, rows, row_count, mirror, capacity, own, gbuf, e_s, w_s, n_s, 2.0 * nu, nu, forces,
+        energy_rank, virial_rank, triplets_rank, status, tag, ovf);
     note_launches(1);
     return launch_status();
+}
+
+extern "C" int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_particles, const int32_t *rows,
+                           const int32_t *row_count, const int32_t *mirror, int32_t capacity,
+                           int32_t slot_capacity, double rc, double nu, double *forces, double *energy_rank,
+                           double *virial_rank, int32_t *triplets_rank, const uint8_t *owned,
+                           void *scratch, size_t scratch_bytes, unsigned long long *status,
+                           int64_t tag, void *stream) {
+    return rb_atm_pass_part(g, n, pos_r, cell_particles, rows, row_count, mirror, capacity,
+                            slot_capacity, rc, nu, forces, energy_rank, virial_rank, triplets_rank,
+                            owned, scratch, scratch_bytes, status, tag, 0, stream);
 }

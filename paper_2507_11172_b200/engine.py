@@ -314,17 +314,20 @@ class ForceEngine:
         self.sum_f64(self.e3_rank, SCALAR_E3)
         self.sum_f64(self.w3_rank, SCALAR_W3)
 
-    def atm_kernel(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0) -> None:
-        """The rb_atm_pass launch alone (bench timing)."""
+    def atm_kernel(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
+                   part: int = 0) -> None:
+        """The rb_atm_pass launches alone (bench timing).  part 1: the triplet
+        kernels only (results in the scratch), part 2: the gather that writes
+        forces and the per-rank scalars (rb_atm_pass_part); 0: both."""
         g = self.grid_struct(geom)
-        st = self.L.rb_atm_pass(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
-                                ptr(self.rows), ptr(self.row_count), ptr(self.mirror),
-                                int(self.capacity), int(self.slots or self.capacity), float(rc),
-                                float(nu), ptr(forces), ptr(self.e3_rank), ptr(self.w3_rank),
-                                ptr(self.v_rank), self._owned(), ptr(self.atm_scratch),
-                                self.atm_scratch.numel() * 8, ptr(self.status), int(tag),
-                                self.stream)
-        _lib.check(st, "rb_atm_pass")
+        st = self.L.rb_atm_pass_part(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
+                                     ptr(self.rows), ptr(self.row_count), ptr(self.mirror),
+                                     int(self.capacity), int(self.slots or self.capacity),
+                                     float(rc), float(nu), ptr(forces), ptr(self.e3_rank),
+                                     ptr(self.w3_rank), ptr(self.v_rank), self._owned(),
+                                     ptr(self.atm_scratch), self.atm_scratch.numel() * 8,
+                                     ptr(self.status), int(tag), int(part), self.stream)
+        _lib.check(st, "rb_atm_pass_part")
 
     def atm_c01(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
                 reduce: bool = True) -> None:

@@ -185,6 +185,9 @@ class DeviceRespa:
         self.fused_rebuild = mode == "fused"
         # inside a sampling period a step's kick runs in the next drift
         self.fuse_kick = os.environ.get("RB_FUSE_KICK", "1") != "0"
+        # three-body steps: the pair pass on a second stream beside the
+        # triplet kernels (periodic Verlet-row loop only)
+        self.overlap_pair = os.environ.get("RB_OVERLAP_PAIR", "1") != "0"
 
     # -------------------------------------------------------------- pieces
     def _geom(self):
@@ -229,6 +232,22 @@ class DeviceRespa:
         else:
             eng.bin(geom, self.x, tag=tag)
             eng.nlist(geom, self.r_build, capacity=self.capacity, checked=False, tag=tag)
+        if with_triplet and self.with_3b and self.overlap_pair:
+            # the triplet kernels first, the pair pass on a second stream
+            # (a parallel graph branch): its blocks fill the SMs the triplet
+            # pass releases in its tail; the gather, which alone writes the
+            # triplet outputs, runs after both
+            torch = self.torch
+            main = torch.cuda.current_stream()
+            side = self._pair_stream = getattr(self, "_pair_stream", None) or torch.cuda.Stream()
+            side.wait_stream(main)
+            eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=1)
+            with torch.cuda.stream(side):
+                eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag,
+                       reduce=False)
+            main.wait_stream(side)
+            eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=2)
+            return
         eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag, reduce=False)
         if with_triplet:
             if self.with_3b:

@@ -552,6 +552,56 @@ def test_kick_folded_into_drift_is_bit_identical(pkg, monkeypatch):
     assert np.array_equal(a.forces_2b, b.forces_2b) and ta.total == tb.total
 
 
+def test_pair_pass_beside_triplet_kernels_is_bit_identical(pkg, monkeypatch):
+    """Three-body steps with the pair pass on a parallel graph branch
+    (rb_atm_pass_part 1 | LJ, then part 2) give exactly the sequential
+    LJ -> rb_atm_pass order: trajectory, forces and the sampled trace."""
+    base = pkg.systems.fcc_system(8, temperature=0.9, seed=21, vseed=22)
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5)
+    out = []
+    for overlap in ("1", "0"):
+        monkeypatch.setenv("RB_OVERLAP_PAIR", overlap)
+        s = base.copy()
+        tr = pkg.respa_run(s, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 5, 100),
+                           sample_interval=5)
+        out.append((s, tr))
+    (a, ta), (b, tb) = out
+    assert np.array_equal(a.positions, b.positions) and np.array_equal(a.velocities, b.velocities)
+    assert np.array_equal(a.forces_2b, b.forces_2b) and np.array_equal(a.forces_3b, b.forces_3b)
+    assert ta.total == tb.total and ta.potential_3b == tb.potential_3b
+
+
+def test_atm_pass_parts_equal_whole_pass(pkg):
+    """rb_atm_pass_part(1) + rb_atm_pass_part(2) = rb_atm_pass, bit for bit,
+    and part 1 alone leaves every caller-visible output untouched."""
+    import torch
+
+    from paper_2507_11172_b200 import grid
+    from paper_2507_11172_b200.engine import ForceEngine
+
+    s = pkg.systems.CONFIGS["cfg2"].system()
+    eng = ForceEngine(s.n)
+    geom = grid.geometry(s.box, None, 2.5, True)
+    eng.upload_positions(s.positions)
+    eng.reset_status(0)
+    eng.bin(geom)
+    eng.nlist(geom, 2.5, checked=True)
+    f_whole = torch.empty((s.n, 3), dtype=torch.float64, device="cuda")
+    eng.atm_kernel(geom, 2.5, 0.073, f_whole, 0)
+    whole = [t.clone() for t in (f_whole, eng.e3_rank, eng.w3_rank, eng.v_rank)]
+    f_parts = torch.full((s.n, 3), 7.0, dtype=torch.float64, device="cuda")
+    for t in (eng.e3_rank, eng.w3_rank):
+        t.fill_(5.0)
+    eng.v_rank.fill_(3)
+    eng.atm_kernel(geom, 2.5, 0.073, f_parts, 0, part=1)
+    torch.cuda.synchronize()
+    assert bool((f_parts == 7.0).all()) and bool((eng.e3_rank == 5.0).all())
+    assert bool((eng.w3_rank == 5.0).all()) and bool((eng.v_rank == 3).all())
+    eng.atm_kernel(geom, 2.5, 0.073, f_parts, 0, part=2)
+    parts = (f_parts, eng.e3_rank, eng.w3_rank, eng.v_rank)
+    assert all(torch.equal(a, b) for a, b in zip(whole, parts))
+
+
 @pytest.mark.parametrize("n", [1, 1000, 32000, 250000])
 def test_sample_sums_equal_separate_reductions(pkg, n):
     """rb_sample's five sums (one launch) are bit-identical to rb_reduce_sumsq

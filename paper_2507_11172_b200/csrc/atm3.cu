@@ -96,15 +96,6 @@ __device__ __forceinline__ double owned_share(int n_owned) {
     return n_owned == 3 ? 1.0 : (n_owned == 2 ? 2.0 / 3.0 : (n_owned == 1 ? 1.0 / 3.0 : 0.0));
 }
 
-// 1/sqrt(x) for a normal double x: the hardware fp64 seed (MUFU.RSQ64H,
-// ~2^-20 relative) and one third-order correction y (1 + r/2 + 3r^2/8),
-// r = 1 - x y^2 (error ~ r^3, below double rounding).
-__device__ __forceinline__ double rsqrt_nr(double x) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    const double r = fma(-x * y, y, 1.0);
-    return fma(y * r, fma(0.375, r, 0.5), y);
-}
 
 // The ATM kernel for slots (s, t): adds f_i, E, W to acc and returns f_j,
 // f_k, all in units of 2 nu.  With a = r_ij^2, b = r_ik^2, c = r_jk^2,

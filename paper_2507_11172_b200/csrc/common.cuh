@@ -81,6 +81,16 @@ __device__ __forceinline__ double min_image(double d, double box, double half) {
 }
 
 // r^2 = dx*dx + dy*dy + dz*dz rounded as numba evaluates it (left to right)
+// 1/sqrt(x) for a normal double x: the hardware fp64 seed (MUFU.RSQ64H,
+// ~2^-20 relative) and one third-order correction y (1 + r/2 + 3r^2/8),
+// r = 1 - x y^2 (error ~ r^3, below double rounding).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double r = fma(-x * y, y, 1.0);
+    return fma(y * r, fma(0.375, r, 0.5), y);
+}
+
 __device__ __forceinline__ double exact_r2(double dx, double dy, double dz) {
     return xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
 }

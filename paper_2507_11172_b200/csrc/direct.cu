@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kT)
                     const double wv = fma(-2.0, a, tsum);
                     const double p = u * v * wv;
                     const double sp = a * b * c;
-                    const double rs = 1.0 / sqrt(sp);
+                    const double rs = rsqrt_nr(sp);  // seed + third-order step (atm3.cu)
                     const double inv_s = rs * rs;
                     const double s52 = rs * inv_s * inv_s;
                     const double s72 = s52 * inv_s;

@@ -115,6 +115,17 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
             self.thread.join(timeout=2)
+        if not self.rows:  # timed region shorter than the sampler's start-up
+            self.after = True
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=10).stdout
+                self.rows = [[c.strip() for c in ln.split(",")] for ln in out.splitlines() if ln]
+            except (OSError, subprocess.SubprocessError):
+                pass
+
+    after = False
 
     def summary(self):
         if not self.rows:
@@ -126,7 +137,9 @@ class ClockSampler:
                           if len(r) > 4 + k and r[4 + k].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows),
+                **({"sampled": "right after the timed region (shorter than the sampler's "
+                               "start-up)"} if self.after else {})}
 
 
 # --------------------------------------------------------------------------
@@ -358,9 +371,9 @@ def ours_arm(args, cfg):
 
     s = cfg.system()
     ff = cfg.force_field()
-    K = (K + sf - 1) // sf * sf  # whole sampling periods
+    periods = (K + sf - 1) // sf  # whole sampling periods replayed; exactly K steps timed
     W = (W + sf - 1) // sf * sf
-    total_steps = sf + W + K + 2 * sf
+    total_steps = sf + W + periods * sf + 2 * sf
     run = DeviceRespa(s.copy(), ff, pkg.CudaLinkedCells(), RespaSchedule(cfg.dt, sf, total_steps),
                       sf)
     run.start()
@@ -396,12 +409,16 @@ def ours_arm(args, cfg):
     ms = 0.0
     el = ctypes.c_float()
     with ClockSampler(local) as clocks:
-        for _ in range(K // sf):
+        timed = 0
+        for _ in range(periods):
             graph.replay()
             for j in range(sf):  # (synchronises on the period's last event)
+                if timed == K:  # steps past K: replayed, not timed
+                    break
                 _lib.check(L.rb_event_elapsed(ev[2 * j], ev[2 * j + 1], ctypes.byref(el)),
                            "rb_event_elapsed")
                 ms += el.value
+                timed += 1
         torch.cuda.synchronize()
     rebuilds = int(run.eng.status[3].item()) - rebuilds0
     status = run.eng.read_status()

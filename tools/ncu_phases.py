@@ -26,19 +26,20 @@ def ranges():
 
     carve = find(r"A3Smem a3_carve\(")
     share = find(r"double owned_share\(")
-    rs = find(r"double rsqrt_nr\(")
     core = find(r"void a3_core\(")
     add = find(r"void a3_add\(")
-    pair = find(r"void a3_pair\(")
+    pair = find(r"void a3_eval\(")
+    sub = find(r"void a3_add_j\(")
     win = find(r"void a3_windows\(")
     base = find(r"void a3_base\(")
     p0 = find(r"phase 0:")
     p1 = find(r"phase 1:")
     p3 = find(r"phase 3:")
     end = find(r"^}", p3)
-    return [("carve", carve, share - 1), ("owned share", share, rs - 1),
-            ("eval: rsqrt", rs, core - 1), ("eval: ATM kernel", core, add - 1),
-            ("slot accumulate", add, pair - 1), ("pair: accept + guard", pair, win - 1),
+    # (rsqrt_nr lives in common.cuh: reported under "common")
+    return [("carve", carve, share - 1), ("owned share", share, core - 1),
+            ("eval: ATM kernel", core, add - 1), ("slot accumulate", add, pair - 1),
+            ("pair: accept + guard", pair, sub - 1), ("slot accumulate (sub-steps)", sub, win - 1),
             ("window loop", win, base - 1), ("setup", base, p0 - 1), ("phase 0 (S+ slots)", p0, p1 - 1),
             ("phase 1 call", p1, p3 - 1), ("phase 3 (write-back)", p3, end)]
 

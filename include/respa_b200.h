@@ -176,7 +176,10 @@ RB_API int rb_atm_pass(const rb_grid *g, int64_t n, const double *pos_r,
  * part 2 the gather, which alone writes forces, energy_rank, virial_rank and
  * triplets_rank.  Between them the caller may run the pair pass on another
  * stream (the device loop overlaps it with the tail of part 1); a pair-pass
- * error of the same step then still leaves the triplet outputs untouched. */
+ * error of the same step then still leaves the triplet outputs untouched.
+ * Every part 1 must be followed by its part 2 (stream-ordered) before the
+ * next pass on the same scratch: part 2 also resets the pass's work counter
+ * and overflow list. */
 RB_API int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r,
                             const int32_t *cell_particles, const int32_t *rows,
                             const int32_t *row_count, const int32_t *mirror, int32_t capacity,

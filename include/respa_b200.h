@@ -189,6 +189,33 @@ RB_API int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r,
                             unsigned long long *status, int64_t tag, int32_t part,
                             void *stream);
 
+/* Cell-based form of the same Newton-3 pass (same results, same outputs):
+ * one CTA per base cell stages the stencil cells that can hold the S+ sets
+ * of its particles (cells whose index is >= its own) in shared memory,
+ * builds S+(i) from them (fp32 filter, reference arithmetic decides), runs
+ * the pair loop and reduces the partial forces per target in shared memory;
+ * one 32-byte entry per (particle, source cell) goes through the scratch to
+ * the gather.  Needs no neighbour rows: `cell_start` (ncell + 1) and
+ * `cell_of_rank` from rb_bin.  Supported when rb_atm_cells_supported (reach-1
+ * stencil with cell size >= rc, periodic boxes of at least four cutoffs);
+ * otherwise use rb_atm_pass_part.  `nb_cap` = staged particles per cell
+ * (>= rb_atm_cells_nb_max), `slot_capacity` (32..256) = longest S+(i); a
+ * cell or base over either records RB_KIND_CAPACITY.  Scratch:
+ * rb_atm_cells_scratch_bytes, zero-filled before first use (part 2 leaves
+ * its cell counter at zero).  Parts as rb_atm_pass_part. */
+RB_API size_t rb_atm_cells_scratch_bytes(int64_t n);
+RB_API size_t rb_atm_cells_smem_bytes(int32_t nb_cap, int32_t slot_capacity);
+RB_API int rb_atm_cells_supported(const rb_grid *g, double rc);
+RB_API int rb_atm_cells_nb_max(const rb_grid *g, const int32_t *cell_start, int32_t *out,
+                               void *stream);
+RB_API int rb_atm_pass_cells(const rb_grid *g, int64_t n, const double *pos_r,
+                             const int32_t *cell_particles, const int32_t *cell_start,
+                             const int32_t *cell_of_rank, int32_t nb_cap, int32_t slot_capacity,
+                             double rc, double nu, double *forces, double *energy_rank,
+                             double *virial_rank, int32_t *triplets_rank, const uint8_t *owned,
+                             void *scratch, size_t scratch_bytes, unsigned long long *status,
+                             int64_t tag, int32_t part, void *stream);
+
 /* C01 (owner-computes) form of the same pass, as the reference traverses it:
  * every triplet visited once from each member, force stored on the base
  * particle only, energy phi/3 per visit; visits_rank = accepted visits. */

@@ -74,6 +74,12 @@ SIGNATURES = {
                                    _P, _P, _SZ, _P, _I64, _P]),
     "rb_atm_pass_part": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _I32, _I32, _D, _D, _P, _P, _P, _P,
                                    _P, _P, _SZ, _P, _I64, _I32, _P]),
+    "rb_atm_cells_scratch_bytes": (_SZ, [_I64]),
+    "rb_atm_cells_smem_bytes": (_SZ, [_I32, _I32]),
+    "rb_atm_cells_supported": (ctypes.c_int, [ctypes.POINTER(RbGrid), _D]),
+    "rb_atm_cells_nb_max": (ctypes.c_int, [ctypes.POINTER(RbGrid), _P, _P, _P]),
+    "rb_atm_pass_cells": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _I32, _D, _D, _P,
+                                         _P, _P, _P, _P, _P, _SZ, _P, _I64, _I32, _P]),
     "rb_atm_pass_c01": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _D, _P, _P, _P, _P, _P,
                                        _I64, _P]),
     "rb_atm_visit_rows": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _P, _P, _P]),

@@ -64,6 +64,7 @@ def _prepare(system, cutoff):
     eng.reset_status(0)
     eng.bin(geom)
     eng.nlist(geom, geom.cutoff, capacity=None, checked=True)
+    eng.nb_cap = 0  # the cell-based triplet pass re-measures its neighbourhoods
     return eng, geom
 
 

@@ -28,10 +28,11 @@
 // Energies are phi per triplet (the reference's phi/3 per visit, summed), the
 // virial -2(E_a a + E_b b + E_c c) per triplet (:530 summed over visits).
 #include <cstdlib>
+#include <cstring>
 
 #include <algorithm>
 
-#include "common.cuh"
+#include "atm_core.cuh"
 
 #include <type_traits>
 
@@ -46,300 +47,26 @@ constexpr int kA3Warps = RB_A3_WARPS;
 #endif
 constexpr int kA3MinBlocks = RB_A3_MIN_BLOCKS;  // register cap for occupancy
 constexpr int kA3MaxSlots = 4096;    // longest S+(i) a warp takes (rows are <= 4096)
-constexpr double kA3Margin = 1e-10;  // fp64 estimate vs the reference arithmetic
 
-// per-warp shared memory: M slots, S+(i)
-struct A3Smem {
-    double2 *dxy;    // (x, y) of d_ij = x_i - x_j
-    double *dz, *r2; // z of d_ij, r_ij^2
-    double2 *axy;    // force accumulators (units of 2 nu), x and y
-    double *az;      //   ... z
-    int32_t *kidx;   // row index | owned << 30
-    int32_t *q;      // the slot's particle (rank) ...
-    int32_t *mpos;   //   ... and the base's position in its row (G target)
-};
-
-__host__ __device__ inline size_t a3_warp_bytes(int m) {
-    size_t b = (size_t)m * (2 * sizeof(double2) + 3 * sizeof(double) + 3 * sizeof(int32_t));
-    return (b + 15) & ~(size_t)15;
-}
-
-// kM > 0: the slot count is a compile-time constant (every offset folds
-// into the shared-memory addressing); kM == 0: runtime m
-template <int kM>
-__device__ __forceinline__ A3Smem a3_carve(char *base, int m_rt) {
-    const int m = kM > 0 ? kM : m_rt;
-    A3Smem s;
-    s.dxy = (double2 *)base;
-    s.axy = s.dxy + m;
-    s.dz = (double *)(s.axy + m);
-    s.r2 = s.dz + m;
-    s.az = s.r2 + m;
-    s.kidx = (int32_t *)(s.az + m);
-    s.q = s.kidx + m;
-    s.mpos = s.q + m;
-    return s;
-}
-
-struct A3Acc {
-    double e, w;     // w: per-triplet sum only where phase 3 cannot recover it
-    int n;
-    bool bad;
-    int owned_i;     // decomposed runs: the base particle is owned by this rank
-};
-
-constexpr int kKidxMask = 0x3fffffff;
-
-// share of a triplet's energy that belongs to this rank: (owned members)/3
-// (the reference attributes phi/3 to each member, containers.py:524)
-__device__ __forceinline__ double owned_share(int n_owned) {
-    return n_owned == 3 ? 1.0 : (n_owned == 2 ? 2.0 / 3.0 : (n_owned == 1 ? 1.0 / 3.0 : 0.0));
-}
-
-
-// The ATM kernel for slots (s, t): adds f_i, E, W to acc and returns f_j,
-// f_k, all in units of 2 nu.  With a = r_ij^2, b = r_ik^2, c = r_jk^2,
-// u = a+b-c, v = a+c-b, w = b+c-a, p = uvw, S = uv+uw+vw, s = abc
-// (potentials.py:82-114):
-//   E   = s^-5/2 (s + 3/8 p)
-//   E_a = 3/8 s^-5/2 (S - 2uv) - bc (3/2 s^-5/2 + 15/16 p s^-7/2), b/c alike.
-// d_ij (ij, ijz), d_ik (ik, ikz), d_jk = x_j - x_k (jk*).
-// kSumVirial: accumulate the virial per triplet (decomposed runs, or d_jk
-// not equal to d_ik - d_ij: box under four cutoffs); otherwise phase 3
-// recovers it from the slot sums.
-template <bool kOwned, bool kSumVirial>
-__device__ __forceinline__ void a3_core(const A3Smem &sm, int s, int t, double a, double b,
-                                        double c, double2 ij, double ijz, double2 ik, double ikz,
-                                        double jkx, double jky, double jkz, A3Acc &acc,
-                                        double fj[3], double fk[3]) {
-    const double tsum = a + b + c;
-    const double u = fma(-2.0, c, tsum);
-    const double v = fma(-2.0, b, tsum);
-    const double w = fma(-2.0, a, tsum);
-    const double p = u * v * w;
-    const double sp = a * b * c;
-    const double rs = rsqrt_nr(sp);
-    const double inv_s = rs * rs;
-    const double s52 = rs * inv_s * inv_s;
-    const double s72 = s52 * inv_s;
-    const double uv = u * v, uw = u * w, vw = v * w;
-    const double S = uv + uw + vw;
-    const double A = 0.375 * s52;
-    const double K = fma(1.5, s52, 0.9375 * p * s72);
-    const double ea = fma(A, fma(-2.0, uv, S), -K * (b * c));
-    const double eb = fma(A, fma(-2.0, uw, S), -K * (a * c));
-    const double ec = fma(A, fma(-2.0, vw, S), -K * (a * b));
-    if (kOwned) {
-        const double share =
-            owned_share(acc.owned_i + (sm.kidx[s] >> 30) + (sm.kidx[t] >> 30));
-        acc.e = fma(share * s52, fma(0.375, p, sp), acc.e);
-        acc.w = fma(share, fma(ea, a, fma(eb, b, ec * c)), acc.w);
-    } else {
-        acc.e = fma(s52, fma(0.375, p, sp), acc.e);
-        if (kSumVirial) acc.w = fma(ea, a, fma(eb, b, fma(ec, c, acc.w)));
-    }
-    acc.n += 1;
-    fj[0] = fma(ea, ij.x, -ec * jkx);
-    fj[1] = fma(ea, ij.y, -ec * jky);
-    fj[2] = fma(ea, ijz, -ec * jkz);
-    fk[0] = fma(eb, ik.x, ec * jkx);
-    fk[1] = fma(eb, ik.y, ec * jky);
-    fk[2] = fma(eb, ikz, ec * jkz);
-}
-
-__device__ __forceinline__ void a3_add(double2 *axy, double *az, int slot, const double f[3]) {
-    double2 xy = axy[slot];
-    xy.x += f[0];
-    xy.y += f[1];
-    axy[slot] = xy;
-    az[slot] += f[2];
-}
-
-// Phase 1, window form.  The m(m-1)/2 slot pairs, enumerated round-major
-// (round d = 1 .. m/2 pairs s with (s + d) mod m; for even m the last round
-// only s < m/2), are taken 32 at a time: lane l of window w holds pair
-// f = 32 w + l (m >= 32) or slot l of round w + 1 (m < 32).  Inside a window
-// all first slots are distinct and all second slots are distinct (for
-// m > 32 a window spans at most two rounds and s repeats only every m
-// pairs), so the partial forces go to the shared-memory slot accumulators
-// in two conflict-free sub-steps -- no queue, no serialisation, a fixed
-// order.  Each lane decides r_jk^2 <= rc^2 bit-exactly (fp64 estimate from
-// d_ik - d_ij outside a 1e-10 band, else the reference's raw-position
-// arithmetic; always the latter when the box is under four cutoffs).
-//
-// a3_eval is one window step for one lane up to the accumulation: the pair
-// (s, t) (live), its acceptance and the ATM kernel (a3_core).  The kernel is
-// evaluated unconditionally (the warp runs it whenever one lane accepts) and
-// the result selected.
-// kJReg (m < 32: the lane's first slot is always s = lane): f_j goes to the
-// lane's register accumulator aj instead of the shared slot.
-struct A3Pair {
-    bool in;
-    int s, t;
-    double fj[3], fk[3];
-};
-
-template <bool kExactImage, bool kOwned, bool kJReg, bool kSlotBad>
-__device__ __forceinline__ void a3_eval(const A3Smem &sm, bool live, int s, int t,
-                                        const rb_grid &g, const double *__restrict__ pr,
-                                        double rc2, double rc2_lo, double rc2_hi, A3Acc &acc,
-                                        const double own[4], A3Pair &P) {
-    if (!live) s = t = 0;  // every lane runs the same code; dead lanes accept nothing
-    // kJReg: slot s is the lane's own, preloaded in `own` (d_ij, r_ij^2)
-    const double2 ij = kJReg ? make_double2(own[0], own[1]) : sm.dxy[s];
-    const double ijz = kJReg ? own[2] : sm.dz[s];
-    const double a = kJReg ? own[3] : sm.r2[s];
-    const double2 ik = sm.dxy[t];
-    const double ikz = sm.dz[t];
-    const double b = sm.r2[t];
-    double jkx, jky, jkz, c;
-    bool in;
-    if (kExactImage) {
-        const Image im = make_image(g);
-        const int j = sm.q[s], k = sm.q[t];
-        exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k], pr[3 * k + 1],
-                   pr[3 * k + 2], jkx, jky, jkz);
-        c = exact_r2(jkx, jky, jkz);
-        in = live && c <= rc2;
-    } else {
-        jkx = ik.x - ij.x;
-        jky = ik.y - ij.y;
-        jkz = ikz - ijz;
-        c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
-        in = live && c <= rc2_lo;
-        const bool band = live && !in && c <= rc2_hi;
-        if (__any_sync(0xffffffffu, band)) {  // rare: the reference arithmetic decides
-            if (band) {
-                const Image im = make_image(g);  // from the kernel parameters, on demand
-                const int j = sm.q[s], k = sm.q[t];
-                double ex, ey, ez;
-                exact_disp(im, pr[3 * j], pr[3 * j + 1], pr[3 * j + 2], pr[3 * k],
-                           pr[3 * k + 1], pr[3 * k + 2], ex, ey, ez);
-                in = exact_r2(ex, ey, ez) <= rc2;
-            }
-        }
-    }
-    // guard (potentials.py:35-36): a triplet with a side under it is flagged
-    // and skipped; r_jk here, r_ij / r_ik only if phase 0 saw one (uniform)
-    bool bad = in && c < RB_MIN_DISTANCE_SQ;
-    if (kSlotBad)  // (uniform per base: the loop is instantiated for both)
-        bad = bad || (in && (a < RB_MIN_DISTANCE_SQ || b < RB_MIN_DISTANCE_SQ));
-    acc.bad = acc.bad || bad;
-    in = in && !bad;
-    A3Acc tmp = acc;
-    a3_core<kOwned, kOwned || kExactImage>(sm, s, t, a, b, c, ij, ijz, ik, ikz, jkx, jky, jkz,
-                                           tmp, P.fj, P.fk);
-    if (in) acc = tmp;
-    P.in = in;
-    P.s = s;
-    P.t = t;
-}
-
-__device__ __forceinline__ void a3_add_j(const A3Smem &sm, const A3Pair &P) {
-    __syncwarp();
-    if (P.in) a3_add(sm.axy, sm.az, P.s, P.fj);
-}
-
-__device__ __forceinline__ void a3_add_k(const A3Smem &sm, const A3Pair &P) {
-    __syncwarp();
-    if (P.in) a3_add(sm.axy, sm.az, P.t, P.fk);
-}
-
-__device__ __forceinline__ void a3_add_reg(double aj[3], const A3Pair &P) {
-    if (P.in) {
-        aj[0] += P.fj[0];
-        aj[1] += P.fj[1];
-        aj[2] += P.fj[2];
-    }
-}
-
-template <bool kExactImage, bool kOwned, bool kSlotBad>
-__device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int lane, const rb_grid &g,
-                                           const double *__restrict__ pr, double rc2,
-                                           double rc2_lo, double rc2_hi, A3Acc &acc) {
-    double aj[3] = {0.0, 0.0, 0.0}, own[4] = {0.0, 0.0, 0.0, 0.0};
-    A3Pair P;
-    if (m >= 32) {
-        const int pairs = m * (m - 1) / 2;
-        int s = lane, d = 1;  // pair f = f0 + lane is (round d, slot s)
-        for (int f0 = 0; f0 < pairs; f0 += 32) {
-            int t = s + d;
-            if (t >= m) t -= m;
-            a3_eval<kExactImage, kOwned, false, kSlotBad>(sm, f0 + lane < pairs, s, t, g, pr, rc2, rc2_lo,
-                                                rc2_hi, acc, own, P);
-            s += 32;
-            if (s >= m) {
-                s -= m;
-                d += 1;
-            }
-            a3_add_j(sm, P);
-            a3_add_k(sm, P);
-        }
-    } else {
-        if (lane < m) {
-            const double2 d = sm.dxy[lane];
-            own[0] = d.x;
-            own[1] = d.y;
-            own[2] = sm.dz[lane];
-            own[3] = sm.r2[lane];
-        }
-        for (int d = 1; 2 * d <= m; d++) {
-            const int lim = 2 * d == m ? d : m;  // even m: the last round is half
-            int t = lane + d;
-            if (t >= m) t -= m;
-            a3_eval<kExactImage, kOwned, true, kSlotBad>(sm, lane < lim, lane, t, g, pr, rc2, rc2_lo,
-                                               rc2_hi, acc, own, P);
-            a3_add_reg(aj, P);
-            a3_add_k(sm, P);
-        }
-        __syncwarp();
-        if (lane < m) a3_add(sm.axy, sm.az, lane, aj);  // the j-role sums of slot `lane`
-    }
-    __syncwarp();
-}
-
-// One base particle r (rank order) per warp.  `ovf` (main pass with a
-// reduced slot count): a base whose S+(r) does not fit is appended to the
-// overflow list ovf[2..] (count ovf[0]) and left to k_atm3_overflow; the
-// gather moves the count to ovf[1] and clears ovf[0].
-template <bool kExactImage, bool kOwned, int kM>
-__device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid &g, int64_t n, const double *__restrict__ pr,
-                                       const int32_t *__restrict__ rows,
-                                       const int32_t *__restrict__ row_count,
-                                       const int32_t *__restrict__ mirror, int32_t capacity,
-                                       int32_t slots, double rc2, double rc2_lo, double rc2_hi,
-                                       double *__restrict__ own,
-                                       double *__restrict__ gbuf,
-                                       double *__restrict__ energy_rank,
-                                       double *__restrict__ virial_rank,
-                                       int32_t *__restrict__ triplets_rank,
-                                       const uint8_t *__restrict__ owned,
-                                       unsigned long long *status, int64_t tag, int debug_mode,
-                                       int32_t *ovf) {
+// Phase 0: S+(r), the suffix of r's rank-sorted row with rank > r and
+// r_ir^2 <= rc^2 (reference arithmetic), into the warp's slots.  Returns m,
+// or -1 when S+(r) does not fit `slots` (the base is then listed in `ovf`
+// for the full-slot launch, or a capacity error is recorded).  Row entries
+// beyond the three-body cutoff get a zero G partial (the gather reads every
+// entry of the row prefix).
+template <bool kOwned>
+__device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image &im,
+                                        double xi, double yi, double zi, int rc_n,
+                                        int chunk_first, const double *__restrict__ pr,
+                                        const int32_t *__restrict__ row,
+                                        const int32_t *__restrict__ mir, int32_t capacity,
+                                        int32_t slots, double rc2, double *__restrict__ gbuf,
+                                        const uint8_t *__restrict__ owned,
+                                        unsigned long long *status, int64_t tag, int32_t *ovf,
+                                        bool &slot_bad) {
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int32_t *row = rows + r * (int64_t)capacity;
-    const int32_t *mir = mirror + r * (int64_t)capacity;
-    // phase 0 is latency-bound: the first memory round trip carries the
-    // status words, the base's position and row length, and the first entry
-    // of every 32-entry chunk of its row (rows are rank-sorted: S+(i) starts
-    // in the last chunk whose first entry precedes i)
-    const ulonglong2 s01 = ld_status2(status);
-    const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
-    const int rc_n = row_count[r];
-    const int chunk_first = 32 * lane < capacity ? row[32 * lane] : 0x7fffffff;
-    const unsigned long long swd = __shfl_sync(0xffffffffu, s01.x, 0);  // one view per warp
-    if (tag < 0) tag = status ? (int64_t)__shfl_sync(0xffffffffu, s01.y, 0) : 0;
-    if (status && frozen_word(swd, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
-    if (kM > 0) slots = kM;
-    const A3Smem sm = a3_carve<kM>(smem_raw + (size_t)warp * a3_warp_bytes(slots), slots);
-    const Image im = make_image(g);
-    // partial forces go to the TARGET's row: G[q][position of i in row q], so
-    // the gather of q reads its own row segment contiguously
-
-    // ---- phase 0: S+(i), the row suffix with rank > i within rc
     int m = 0;
-    bool slot_bad = false;
+    slot_bad = false;
     int first = 0;
     {
         const int nchunks = (rc_n + 31) >> 5;
@@ -390,64 +117,120 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
                     else
                         record_status(status, tag, RB_KIND_CAPACITY);
                 }
-                return;
+                return -1;
             }
             if (keep) {
                 const int slot = m + __popc(mk & lanemask_lt());
-                sm.dxy[slot] = make_double2(dx, dy);
-                sm.dz[slot] = dz;
-                sm.r2[slot] = r2;
+                sm.xy[slot] = make_double2(dx, dy);
+                sm.zr[slot] = make_double2(dz, r2);
+                sm.axy[slot] = make_double2(0.0, 0.0);
+                sm.az[slot] = 0.0;
                 sm.kidx[slot] = k | ((kOwned ? (int)owned[q] : 1) << 30);
                 sm.q[slot] = q;
                 sm.mpos[slot] = mk2[h];
-                sm.axy[slot] = make_double2(0.0, 0.0);
-                sm.az[slot] = 0.0;
             }
             m += __popc(mk);
             slot_bad |= __any_sync(0xffffffffu, keep && r2 < RB_MIN_DISTANCE_SQ);
         }
     }
     __syncwarp();
+    return m;
+}
+
+// One base particle r (rank order) per warp.  `ovf` (main pass with a
+// reduced slot count): a base whose S+(r) does not fit is appended to the
+// overflow list ovf[2..] (count ovf[0]) and left to k_atm3_overflow; the
+// gather moves the count to ovf[1] and clears ovf[0].
+template <bool kExactImage, bool kOwned, int kM>
+__device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid &g, int64_t n, const double *__restrict__ pr,
+                                       const int32_t *__restrict__ rows,
+                                       const int32_t *__restrict__ row_count,
+                                       const int32_t *__restrict__ mirror, int32_t capacity,
+                                       int32_t slots, const A3Cut &cut,
+                                       double *__restrict__ own,
+                                       double *__restrict__ gbuf,
+                                       double *__restrict__ energy_rank,
+                                       double *__restrict__ virial_rank,
+                                       int32_t *__restrict__ triplets_rank,
+                                       const uint8_t *__restrict__ owned,
+                                       unsigned long long *status, int64_t tag, int debug_mode,
+                                       int32_t *ovf) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int32_t *row = rows + r * (int64_t)capacity;
+    const int32_t *mir = mirror + r * (int64_t)capacity;
+    // phase 0 is latency-bound: the first memory round trip carries the
+    // status words, the base's position and row length, and the first entry
+    // of every 32-entry chunk of its row (rows are rank-sorted: S+(i) starts
+    // in the last chunk whose first entry precedes i)
+    const ulonglong2 s01 = ld_status2(status);
+    const double xi = pr[3 * r], yi = pr[3 * r + 1], zi = pr[3 * r + 2];
+    const int rc_n = row_count[r];
+    const int chunk_first = 32 * lane < capacity ? row[32 * lane] : 0x7fffffff;
+    const unsigned long long swd = __shfl_sync(0xffffffffu, s01.x, 0);  // one view per warp
+    if (tag < 0) tag = status ? (int64_t)__shfl_sync(0xffffffffu, s01.y, 0) : 0;
+    if (status && frozen_word(swd, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
+    if (kM > 0) slots = kM;
+    const A3Smem sm = a3_carve<kM>(smem_raw + (size_t)warp * a3_warp_bytes(slots), slots);
+    const Image im = make_image(g);
+    // partial forces go to the TARGET's row: G[q][position of i in row q], so
+    // the gather of q reads its own row segment contiguously
+
+    // ---- phase 0: S+(i), the row suffix with rank > i within rc
+    bool slot_bad = false;
+    const int m = a3_slots<kOwned>(r, sm, im, xi, yi, zi, rc_n, chunk_first, pr,
+                                   row, mir, capacity, slots, cut.rc2, gbuf, owned, status, tag,
+                                   ovf, slot_bad);
+    if (m < 0) return;
 
     // ---- phase 1: the slot pairs, 32 per window (a3_windows)
     A3Acc acc = {0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1};
-    if (debug_mode != 1) {  // debug 1: phases 0 and 3 only
+    double F[3] = {0.0, 0.0, 0.0};
+    // debug 1: phases 0 and 3 only; 2 / 3: phase 1 of the bases with m < 32 /
+    // m >= 32 only (timing split, tuning only)
+    if (debug_mode != 1 && !(debug_mode == 2 && m >= 32) && !(debug_mode == 3 && m < 32)) {
         if (slot_bad)
-            a3_windows<kExactImage, kOwned, true>(sm, m, lane, g, pr, rc2, rc2_lo, rc2_hi, acc);
+            a3_windows<kExactImage, kOwned, true>(sm, m, slots, lane, g, pr, cut, acc, F);
         else
-            a3_windows<kExactImage, kOwned, false>(sm, m, lane, g, pr, rc2, rc2_lo, rc2_hi, acc);
+            a3_windows<kExactImage, kOwned, false>(sm, m, slots, lane, g, pr, cut, acc, F);
     }
-    __syncwarp();
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars.  Per
     // triplet f_i + f_j + f_k = 0, so the base's own force is minus the sum
     // of everything its triplets gave the slots (fixed lane order and tree)
     // Likewise the virial: per triplet x_i.f_i + x_j.f_j + x_k.f_k =
     // -(d_ij.f_j + d_ik.f_k) = -2(E_a a + E_b b + E_c c), so the base's sum is
-    // sum_s d_is . (slot sum s) in the units of acc.w (decomposed runs weight
-    // each triplet by its owned share, and under four cutoffs d_jk is its own
-    // image: both keep the per-triplet sum)
+    // sum_s d_is . (slot sum s) in the units of acc.w, and the energy is
+    // -1/4.5 of it (atm_scalars).  Decomposed runs weight each triplet by its
+    // owned share, and under four cutoffs d_jk is its own image: both keep
+    // the per-triplet sums.
     double sx = 0.0, sy = 0.0, sz = 0.0, sw = 0.0;
     for (int sl = lane; sl < m; sl += 32) {
-        const double2 xy = sm.axy[sl];
-        const double z = sm.az[sl];
+        double ax = F[0], ay = F[1], az = F[2];  // m < 32: the lane's register sums
+        if (m >= 32) {
+            const double2 axy = sm.axy[sl];
+            ax = axy.x;
+            ay = axy.y;
+            az = sm.az[sl];
+        }
         double *gq = gbuf + ((int64_t)sm.q[sl] * capacity + sm.mpos[sl]) * 3;
-        gq[0] = xy.x;
-        gq[1] = xy.y;
-        gq[2] = z;
-        sx += xy.x;
-        sy += xy.y;
-        sz += z;
+        gq[0] = ax;
+        gq[1] = ay;
+        gq[2] = az;
+        sx += ax;
+        sy += ay;
+        sz += az;
         if (!kOwned && !kExactImage) {
-            const double2 d = sm.dxy[sl];
-            sw = fma(d.x, xy.x, fma(d.y, xy.y, fma(sm.dz[sl], z, sw)));
+            double dx, dy, dz, r2;
+            ld_rec(sm, sl, dx, dy, dz, r2);
+            sw = fma(dx, ax, fma(dy, ay, fma(dz, az, sw)));
         }
     }
     const double fx = -group_sum<32>(sx);
     const double fy = -group_sum<32>(sy);
     const double fz = -group_sum<32>(sz);
-    const double e = group_sum<32>(acc.e);
     const double w = group_sum<32>(kOwned || kExactImage ? acc.w : sw);
+    const double e = kOwned || kExactImage ? group_sum<32>(acc.e) : w * (-1.0 / 4.5);
     const int nt = group_sum_int<32>(acc.n);
     const bool bad = __any_sync(0xffffffffu, acc.bad);
     if (lane == 0) {
@@ -465,7 +248,7 @@ template <bool kExactImage, bool kOwned, int kM>
 __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
     k_atm3(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
            const int32_t *__restrict__ row_count, const int32_t *__restrict__ mirror,
-           int32_t capacity, int32_t slots, double rc2, double rc2_lo, double rc2_hi,
+           int32_t capacity, int32_t slots, A3Cut cut,
            double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
@@ -477,7 +260,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
         const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
         if (r >= n) return;
         a3_base<kExactImage, kOwned, kM>(r, smem_raw, g, n, pr, rows, row_count, mirror,
-                                         capacity, slots, rc2, rc2_lo, rc2_hi, own, gbuf,
+                                         capacity, slots, cut, own, gbuf,
                                          energy_rank, virial_rank, triplets_rank, owned, status,
                                          tag, debug_mode, ovf);
         return;
@@ -493,7 +276,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
         int nxt = 0;
         if (lane == 0) nxt = atomicAdd(work, 1);
         a3_base<kExactImage, kOwned, kM>(r, smem_raw, g, n, pr, rows, row_count, mirror, capacity,
-                                         slots, rc2, rc2_lo, rc2_hi, own, gbuf, energy_rank,
+                                         slots, cut, own, gbuf, energy_rank,
                                          virial_rank, triplets_rank, owned, status, tag,
                                          debug_mode, ovf);
         __syncwarp();  // the warp's slots are reused by its next base
@@ -506,7 +289,7 @@ template <bool kExactImage, bool kOwned>
 __global__ void __launch_bounds__(kA3Warps * 32)
     k_atm3_overflow(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ rows,
            const int32_t *__restrict__ row_count, const int32_t *__restrict__ mirror,
-           int32_t capacity, int32_t slots, double rc2, double rc2_lo, double rc2_hi,
+           int32_t capacity, int32_t slots, A3Cut cut,
            double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
@@ -518,7 +301,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
     for (int64_t q = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); q < cnt;
          q += (int64_t)gridDim.x * wpb) {
         a3_base<kExactImage, kOwned, 0>(ovf[2 + q], smem_raw, g, n, pr, rows, row_count, mirror,
-                                        capacity, slots, rc2, rc2_lo, rc2_hi,
+                                        capacity, slots, cut,
                                         own, gbuf, energy_rank, virial_rank, triplets_rank,
                                         owned, status, tag, debug_mode, nullptr);
         __syncwarp();  // the warp's slots are reused by its next base
@@ -654,8 +437,7 @@ static int a3_warps_for(size_t per) {
 template <bool kExactImage, bool kOwned, int kM>
 static void a3_launch_main(cudaStream_t st, int64_t n, int warps, size_t per, const rb_grid &g,
                            const double *pos_r, const int32_t *rows, const int32_t *row_count,
-                           const int32_t *mirror, int32_t capacity, int fast, double rc2,
-                           double lo, double hi, double *own, double *gbuf,
+                           const int32_t *mirror, int32_t capacity, int fast, const A3Cut &cut, double *own, double *gbuf,
                            double *energy_rank, double *virial_rank, int32_t *triplets_rank,
                            const uint8_t *owned, unsigned long long *status, int64_t tag,
                            int debug_mode, int32_t *ovf, int32_t *work) {
@@ -684,7 +466,7 @@ static void a3_launch_main(cudaStream_t st, int64_t n, int warps, size_t per, co
         else work = nullptr;
     }
     launch(kern, dim3((unsigned)blocks), dim3(warps * 32),
-           warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity, fast, rc2, lo, hi,
+           warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity, fast, cut,
            own, gbuf, energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
            ovf, work);
     note_launches(1);
@@ -693,7 +475,7 @@ static void a3_launch_main(cudaStream_t st, int64_t n, int warps, size_t per, co
 template <bool kExactImage, bool kOwned>
 static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double *pos_r,
                       const int32_t *rows, const int32_t *row_count, const int32_t *mirror,
-                      int32_t capacity, int fast, int full, double rc2, double lo, double hi,
+                      int32_t capacity, int fast, int full, const A3Cut &cut,
                       double *own, double *gbuf, double *energy_rank, double *virial_rank,
                       int32_t *triplets_rank, const uint8_t *owned, unsigned long long *status,
                       int64_t tag, int debug_mode, int32_t *ovf, int32_t *work) {
@@ -705,17 +487,17 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
     // the common slot counts get compile-time layouts
     if (fast == 64)
         a3_launch_main<kExactImage, kOwned, 64>(st, n, warps, per, g, pos_r, rows, row_count,
-                                                mirror, capacity, fast, rc2, lo, hi, own,
+                                                mirror, capacity, fast, cut, own,
                                                 gbuf, energy_rank, virial_rank, triplets_rank,
                                                 owned, status, tag, debug_mode, list, work);
     else if (fast == 96)
         a3_launch_main<kExactImage, kOwned, 96>(st, n, warps, per, g, pos_r, rows, row_count,
-                                                mirror, capacity, fast, rc2, lo, hi, own,
+                                                mirror, capacity, fast, cut, own,
                                                 gbuf, energy_rank, virial_rank, triplets_rank,
                                                 owned, status, tag, debug_mode, list, work);
     else
         a3_launch_main<kExactImage, kOwned, 0>(st, n, warps, per, g, pos_r, rows, row_count,
-                                               mirror, capacity, fast, rc2, lo, hi, own,
+                                               mirror, capacity, fast, cut, own,
                                                gbuf, energy_rank, virial_rank, triplets_rank,
                                                owned, status, tag, debug_mode, list, work);
     if (!split) return;
@@ -725,7 +507,7 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
     const unsigned blocks = (unsigned)(need < 148 * 4 ? need : 148 * 4);
     a3_grant(k_atm3_overflow<kExactImage, kOwned>, wf * per_full, granted_ovf);
     launch(k_atm3_overflow<kExactImage, kOwned>, dim3(blocks), dim3(wf * 32), wf * per_full, st,
-           g, n, pos_r, rows, row_count, mirror, capacity, full, rc2, lo, hi, own, gbuf,
+           g, n, pos_r, rows, row_count, mirror, capacity, full, cut, own, gbuf,
            energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
            (const int32_t *)ovf);
     note_launches(1);
@@ -762,13 +544,21 @@ extern "C" int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r
     double *e_s = own + 3 * n, *w_s = e_s + n;
     int32_t *n_s = (int32_t *)(w_s + n);
     double *gbuf = (double *)((char *)n_s + (((size_t)n * sizeof(int32_t) + 7) & ~(size_t)7));
-    const double lo = exact_image ? rc2 : rc2 * (1.0 - kA3Margin);
-    const double hi = exact_image ? rc2 : rc2 * (1.0 + kA3Margin);
+    auto hiword = [](double x) {
+        int64_t b;
+        memcpy(&b, &x, sizeof b);
+        return (int)(b >> 32);
+    };
+    A3Cut cut;
+    cut.rc2 = rc2;
+    cut.lo_hi = hiword(rc2 * (1.0 - kA3Margin));
+    cut.hi_hi = hiword(rc2 * (1.0 + kA3Margin));
+    cut.min_hi = hiword(RB_MIN_DISTANCE_SQ);
     static const bool persist = !(getenv("RB_ATM_PERSIST") && atoi(getenv("RB_ATM_PERSIST")) == 0);
     int32_t *work = persist ? work_word : nullptr;
     auto go = [&](auto exact, auto with_owned) {
         a3_launch<decltype(exact)::value, decltype(with_owned)::value>(
-            st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity, rc2, lo, hi,
+            st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity, cut,
             own, gbuf, e_s, w_s, n_s, owned, status, tag, debug_mode, ovf, work);
     };
     using T = std::true_type;

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from typing import Optional
 
 import numpy as np
@@ -92,6 +93,15 @@ class ForceEngine:
         self._stream_override = None  # capture of a conditional body
         self.cond_body_launches = 0  # kernels in the last conditional rebuild body
         self.direct_scratch = None
+        # cell-based triplet pass (rb_atm_pass_cells): scratch, staged
+        # neighbourhood capacity (measured, with margin) and its margin
+        self.cells_scratch = None
+        self.nb_cap = 0
+        self.nb_margin = 1.1
+        self._cells_ok = {}
+        self._cells_slots = 0
+        self.slots_margin = 1.0
+        self._nb_max = torch.zeros(1, dtype=i32, device=dev)
 
     # ------------------------------------------------------------------ misc
     @property
@@ -314,11 +324,88 @@ class ForceEngine:
         self.sum_f64(self.e3_rank, SCALAR_E3)
         self.sum_f64(self.w3_rank, SCALAR_W3)
 
+    CELLS_MODE = os.environ.get("RB_ATM_CELLS", "0")  # "1": cell-based where supported
+
+    def uses_cells(self, geom: Geometry, rc: float) -> bool:
+        """Whether the triplet pass of this geometry runs cell-based
+        (rb_atm_pass_cells) rather than on the neighbour rows."""
+        if self.CELLS_MODE == "0":
+            return False
+        key = (geom, float(rc))
+        ok = self._cells_ok.get(key)
+        if ok is None:
+            g = self.grid_struct(geom)
+            ok = bool(self.L.rb_atm_cells_supported(ctypes.byref(g), float(rc)))
+            self._cells_ok[key] = ok
+        return ok
+
+    def cells_slots(self) -> int:
+        """Slots of the cell-based pass: |S+(i)| is the forward half of the
+        neighbours within the cutoff, (2/3) pi rc^3 rho on average; sized
+        from the densest cell with margin (measured at nb_cap time)."""
+        return int(self._cells_slots or min(256, max(32, _round_up(int(self.slots or 64), 32))))
+
+    def _size_cells_slots(self, geom: Geometry, rc: float) -> None:
+        counts = self.cell_start[1:geom.num_cells + 1] - self.cell_start[:geom.num_cells]
+        max_occ = int(counts.max().item()) if geom.num_cells else 1
+        dens = max(max_occ / float(np.prod(geom.cell_size)), self.n / float(np.prod(geom.box)))
+        est = 2.0 / 3.0 * math.pi * rc ** 3 * dens
+        self._cells_slots = int(min(256, max(32, _round_up(int(est * 1.45 * self.slots_margin)
+                                                             + 8, 32))))
+
+    def measure_nb_cap(self, geom: Geometry) -> int:
+        """Staged-neighbourhood capacity from the current binning (syncs)."""
+        g = self.grid_struct(geom)
+        _lib.check(self.L.rb_atm_cells_nb_max(ctypes.byref(g), ptr(self.cell_start),
+                                              ptr(self._nb_max), self.stream),
+                   "rb_atm_cells_nb_max")
+        worst = int(self._nb_max.item())
+        self.nb_cap = _round_up(int(worst * self.nb_margin) + 16, 32)
+        return self.nb_cap
+
+    def grow_cells(self) -> None:
+        """After a capacity error: larger margins at the next measurement."""
+        self.nb_margin *= 1.5
+        self.slots_margin *= 1.5
+        self.nb_cap = 0
+
+    def _atm_cells(self, geom: Geometry, rc: float, nu: float, forces, tag: int,
+                   part: int) -> bool:
+        torch = self.torch
+        n_buf = max(int(self.pos.shape[0]), 1)
+        need = int(self.L.rb_atm_cells_scratch_bytes(n_buf))
+        if self.cells_scratch is None or self.cells_scratch.numel() * 8 < need:
+            # zero-filled once: the cell counter at its head (rb_atm_pass_cells)
+            self.cells_scratch = torch.zeros((need + 7) // 8, dtype=torch.float64,
+                                             device=self.device)
+        if self.nb_cap == 0:
+            if torch.cuda.is_current_stream_capturing():
+                raise RuntimeError("the cell-based triplet pass was first used under graph "
+                                   "capture (run it once eagerly to size it)")
+            self.measure_nb_cap(geom)
+            self._size_cells_slots(geom, rc)
+        slots = self.cells_slots()
+        if int(self.L.rb_atm_cells_smem_bytes(int(self.nb_cap), slots)) > 227 * 1024:
+            return False  # too dense for one CTA's shared memory: the row-based pass
+        g = self.grid_struct(geom)
+        st = self.L.rb_atm_pass_cells(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
+                                      ptr(self.cell_start), ptr(self.cell_of_rank),
+                                      int(self.nb_cap), slots, float(rc), float(nu),
+                                      ptr(forces), ptr(self.e3_rank), ptr(self.w3_rank),
+                                      ptr(self.v_rank), self._owned(), ptr(self.cells_scratch),
+                                      self.cells_scratch.numel() * 8, ptr(self.status),
+                                      int(tag), int(part), self.stream)
+        _lib.check(st, "rb_atm_pass_cells")
+        return True
+
     def atm_kernel(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,
                    part: int = 0) -> None:
-        """The rb_atm_pass launches alone (bench timing).  part 1: the triplet
-        kernels only (results in the scratch), part 2: the gather that writes
-        forces and the per-rank scalars (rb_atm_pass_part); 0: both."""
+        """The triplet pass launches alone (bench timing): cell-based when the
+        geometry allows it (uses_cells), else on the rows.  part 1: the
+        triplet kernels only (results in the scratch), part 2: the gather
+        that writes forces and the per-rank scalars; 0: both."""
+        if self.uses_cells(geom, rc) and self._atm_cells(geom, rc, nu, forces, tag, part):
+            return
         g = self.grid_struct(geom)
         st = self.L.rb_atm_pass_part(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
                                      ptr(self.rows), ptr(self.row_count), ptr(self.mirror),

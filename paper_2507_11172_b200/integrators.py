@@ -442,6 +442,7 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
         except CapacityError:
             capacity = min(4096, _round_up(int(run.capacity * 1.5) + 32, 32))
             slots = capacity
+            run.eng.grow_cells()
             system.positions[:] = x0
             system.velocities[:] = v0
     raise CapacityError("neighbour rows kept overflowing")

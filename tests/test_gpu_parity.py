@@ -218,10 +218,14 @@ def test_random_systems_against_oracle(pkg, oracle, rng):
         assert pkg.triplet_count(s, 2.5) == count
 
 
-def test_triplet_overflow_launch_matches_oracle(pkg, oracle):
+def test_triplet_overflow_launch_matches_oracle(pkg, oracle, monkeypatch):
     """Bases whose S+ exceeds the main launch's slots go to the second
-    (full-slot) launch; the forces must not depend on which launch ran."""
+    (full-slot) launch of the row-based pass; the forces must not depend on
+    which launch ran."""
     from paper_2507_11172_b200.containers import engine_for
+    from paper_2507_11172_b200.engine import ForceEngine
+
+    monkeypatch.setattr(ForceEngine, "CELLS_MODE", "0")  # the row-based pass
 
     s = pkg.systems.fcc_system(9, jitter=0.05, seed=9)  # rows of ~130: 160 slots, split
     ff = pkg.ForceField(nu=0.4, cutoff=3.4)

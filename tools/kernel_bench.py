@@ -94,7 +94,10 @@ def main(argv):
         tps = unique / (t_atm * 1e-3)
         print(json.dumps({
             "config": name, "skin": skin, "n": s.n, "unique_triplets": unique, "capacity": eng.capacity,
-            "slots": eng.slots, "atm_ms": t_atm, "atm_c01_ms": t_c01, "lj_ms": t_lj,
+            "slots": eng.slots, "atm_path": "cells" if eng.uses_cells(geom, rc3) else "rows",
+            "nb_cap": eng.nb_cap, "cells_slots": eng.cells_slots(),
+            "cells_smem": int(eng.L.rb_atm_cells_smem_bytes(int(eng.nb_cap or 32), eng.cells_slots())),
+            "atm_ms": t_atm, "atm_c01_ms": t_c01, "lj_ms": t_lj,
             "bin_ms": t_bin, "nlist_ms": t_nl, "rebuild_ms": t_rb, "rebuild_closed_ms": t_rb0, "triplets_per_s": tps,
             "fp64_tflops": tps * 141 / 1e12, "fp64_peak_tflops": peak.value,
             "frac": tps * 141 / 1e12 / peak.value,

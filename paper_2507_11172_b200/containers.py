@@ -40,14 +40,24 @@ _MINSEP_MSG = ("particles closer than the minimum separation guard; the configur
 _ENGINES: dict = {}
 
 
-def engine_for(n: int) -> ForceEngine:
-    """Per-particle-count device workspace, reused across passes."""
-    eng = _ENGINES.get(n)
+def engine_for(n: int, run: bool = False) -> ForceEngine:
+    """Per-particle-count device workspace, reused across passes.
+
+    A device-resident run keeps its state (rows, x_ref, status) in its
+    engine between steps; while one holds the workspace (``busy``), container
+    passes -- e.g. a host hook calling ``pair_pass`` -- get a second one, so
+    they never disturb the run's skin invariant or its pending errors.
+    ``run=True``: the caller is such a run (and takes the primary engine)."""
+    key = (n, False)
+    eng = _ENGINES.get(key)
+    if eng is not None and eng.busy and not run:
+        key = (n, True)
+        eng = _ENGINES.get(key)
     if eng is None:
         if len(_ENGINES) > 8:
             _ENGINES.clear()
         eng = ForceEngine(n)
-        _ENGINES[n] = eng
+        _ENGINES[key] = eng
     return eng
 
 

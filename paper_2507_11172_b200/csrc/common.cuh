@@ -63,6 +63,31 @@ static inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_
     if (e != cudaSuccess) g_launch_error = e;
 }
 
+// A kernel whose blocks wait on one another (software grid barrier): a
+// cooperative launch, so the driver guarantees that every block is resident
+// (or fails the launch) -- never a hang behind kernels of other streams,
+// processes or MPS clients.  Programmatic serialization as launch().
+// Probed on B200 / driver 580 (tools/coop_pdl_probe.cu): the two attributes
+// combine, eagerly and under stream capture.
+template <typename... KArgs, typename... Args>
+static inline void launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                               cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+    if (e != cudaSuccess) g_launch_error = e;
+}
+
 // ---------------------------------------------------------------------------
 // Exact reference arithmetic.  nvcc contracts a*b+c into FMA by default; the
 // reference (numba) rounds every mul and add separately, and the cutoff

@@ -11,11 +11,13 @@
 //   zero counts | count | tile sums | tile offsets | scan apply | scatter |
 //   cell finish (stable order, rank-ordered copy) | rows | mirror
 //
-// The grid is at most the co-resident capacity (occupancy x SMs), so the
-// software barrier (count + generation words in the scratch) cannot
-// deadlock: under programmatic dependent launch the next kernel starts only
-// after every block of this one has started.  Data written by an earlier
-// phase is read with L2-coherent loads (ldc<true>).
+// The grid is the co-resident capacity (occupancy x SMs of the current
+// device) and the launch is cooperative (launch_coop): the driver makes
+// every block resident before any runs, so the software barrier (count +
+// generation words in the scratch) cannot wait on a block that is not
+// scheduled -- not behind kernels of other streams, processes or MPS
+// clients.  Data written by an earlier phase is read with L2-coherent loads
+// (ldc<true>).
 #include <algorithm>
 
 #include "cells.cuh"
@@ -180,15 +182,18 @@ __global__ void __launch_bounds__(kRbThreads)
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 static int rebuild_grid() {
-    static int blocks = 0;
-    if (!blocks) {
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
+    constexpr int kMaxDev = 64;
+    static int blocks[kMaxDev] = {0};  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &b = blocks[dev < kMaxDev ? dev : kMaxDev - 1];
+    if (!b) {
+        int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rebuild, kRbThreads, 0);
-        blocks = std::max(1, sms) * std::max(1, per);
+        b = std::max(1, sms) * std::max(1, per);
     }
-    return blocks;
+    return b;
 }
 
 }  // namespace rb
@@ -230,7 +235,7 @@ extern "C" int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_
     const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
     static const int stop = getenv("RB_REBUILD_STOP") ? atoi(getenv("RB_REBUILD_STOP")) : 0;
     if (stop > 0) cudaMemcpyToSymbol(g_rebuild_stop, &stop, sizeof(int));
-    launch(k_rebuild, dim3((unsigned)rebuild_grid()), dim3(kRbThreads), 0, as_stream(stream), *g,
+    launch_coop(k_rebuild, dim3((unsigned)rebuild_grid()), dim3(kRbThreads), 0, as_stream(stream), *g,
            n, pos, cell_start, cell_particles, cell_of_rank, pos_r, rank_of, x_ref, rl2, capacity,
            rows, row_count, max_count, mirror, cell_of, count, cursor, tiles, bar, rebuild_flag,
            status, tag);

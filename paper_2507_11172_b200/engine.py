@@ -93,6 +93,7 @@ class ForceEngine:
         self._stream_override = None  # capture of a conditional body
         self.cond_body_launches = 0  # kernels in the last conditional rebuild body
         self.direct_scratch = None
+        self.busy = False  # held by a device-resident run (containers.engine_for)
         # cell-based triplet pass (rb_atm_pass_cells): scratch, staged
         # neighbourhood capacity (measured, with margin) and its margin
         self.cells_scratch = None

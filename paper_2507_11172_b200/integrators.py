@@ -143,7 +143,7 @@ class DeviceRespa:
             raise ValidationError("DirectSum does not support periodic boundaries")
         # open linked-cell systems need a host-synchronised grid every step
         self.use_graph = use_graph and (self.periodic or self.direct)
-        self.eng = engine_for(self.n)  # device workspace cached per particle count
+        self.eng = engine_for(self.n, run=True)  # device workspace cached per particle count
         torch = self.torch = self.eng.torch
         dev, f64 = self.eng.device, torch.float64
         self.x = self.eng.pos  # positions live in the engine's buffer
@@ -188,6 +188,25 @@ class DeviceRespa:
         # three-body steps: the pair pass on a second stream beside the
         # triplet kernels (periodic Verlet-row loop only)
         self.overlap_pair = os.environ.get("RB_OVERLAP_PAIR", "1") != "0"
+
+    def cache_key(self):
+        """What the captured period graph bakes in (kernel arguments and
+        buffer shapes): a run of the same key can replay it."""
+        ff = self.ff
+        return (self.n, tuple(float(b) for b in self.box), self.periodic,
+                float(self.system.mass), float(ff.epsilon), float(ff.sigma), self.nu, self.rc2,
+                self.rc3, type(self.container).__name__, self.dt,
+                self.schedule.step_size_factor, self.interval, self.skin, self.use_graph,
+                self.capacity, self.slots)
+
+    def rebind(self, system, container, schedule: RespaSchedule) -> bool:
+        """Reuse this run (buffers, rows, captured graph) for another run of
+        the same shape; False when its trace rows are too few."""
+        nsamples = schedule.num_iterations // self.interval + 1
+        if nsamples > self.trace_dev.shape[0]:
+            return False
+        self.system, self.container, self.schedule = system, container, schedule
+        return True
 
     # -------------------------------------------------------------- pieces
     def _geom(self):
@@ -314,11 +333,29 @@ class DeviceRespa:
             self._step(first + j, j)
 
     # ----------------------------------------------------------------- run
+    def _pinned(self):
+        """Page-locked host staging of the run's transfers (allocated once)."""
+        if getattr(self, "_pin", None) is None:
+            t, n = self.torch, self.n
+
+            def pin(shape, dtype):
+                return t.empty(shape, dtype=dtype, pin_memory=True)
+
+            self._pin = dict(x=pin((n, 3), t.float64), v=pin((n, 3), t.float64),
+                             f2=pin((n, 3), t.float64), f3=pin((n, 3), t.float64),
+                             trace=pin(tuple(self.trace_dev.shape), t.float64),
+                             scalars=pin((8,), t.float64), status=pin((4,), t.int64),
+                             maxc=pin((1,), t.int32))
+        return self._pin
+
     def start(self) -> None:
         """Upload, initial passes (integrators.py:133-137) and sample 0."""
         torch, eng = self.torch, self.eng
-        eng.upload_positions(self.system.positions)
-        self.v.copy_(torch.from_numpy(np.ascontiguousarray(self.system.velocities, np.float64)))
+        pin = self._pinned()  # host arrays -> page-locked staging -> async copies
+        pin["x"].numpy()[:] = self.system.positions
+        pin["v"].numpy()[:] = self.system.velocities
+        eng.pos[: self.n].copy_(pin["x"], non_blocking=True)
+        self.v.copy_(pin["v"], non_blocking=True)
         eng.reset_status(0)
         eng.rebuild_flag.zero_()  # tag 0 == forced build for the initial passes
         if not self.direct and (self.capacity is None or self.slots is None):
@@ -381,6 +418,34 @@ class DeviceRespa:
             else:
                 self._period(k * self.interval)
 
+    def collect(self, upto: int) -> dict:
+        """Every result of the run to the host in one synchronisation: the
+        status words, the row high-water mark, the trace rows, the state and
+        the container scalars (async copies into page-locked buffers)."""
+        pin, eng = self._pinned(), self.eng
+        pin["status"].copy_(eng.status, non_blocking=True)
+        pin["maxc"].copy_(eng.max_count, non_blocking=True)
+        pin["trace"][:upto].copy_(self.trace_dev[:upto], non_blocking=True)
+        pin["x"].copy_(self.x[: self.n], non_blocking=True)
+        pin["v"].copy_(self.v, non_blocking=True)
+        pin["f2"].copy_(self.f2_old, non_blocking=True)
+        pin["f3"].copy_(self.f3, non_blocking=True)
+        pin["scalars"].copy_(eng.scalars, non_blocking=True)
+        self.torch.cuda.current_stream().synchronize()
+        return pin
+
+    def apply_collected(self, pin) -> None:
+        """The collected state into the host system and the container."""
+        sysm = self.system
+        sysm.positions[:] = pin["x"].numpy()
+        sysm.velocities[:] = pin["v"].numpy()
+        sysm.forces_2b[:] = pin["f2"].numpy()
+        sysm.forces_3b[:] = pin["f3"].numpy()
+        sc = pin["scalars"].numpy()
+        c = self.container
+        c.pair_energy, c.pair_virial = float(sc[SCALAR_E2]), float(sc[SCALAR_W2])
+        c.triplet_energy, c.triplet_virial = float(sc[SCALAR_E3]), float(sc[SCALAR_W3])
+
     def download(self) -> None:
         sysm = self.system
         sysm.positions[:] = self.x.cpu().numpy()
@@ -415,7 +480,13 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
     container) at every sample point -- they force a download per period.
     ``device_hooks`` are called as hook(iteration, positions) at the same
     points with the device positions (particle order) and must only enqueue
-    device work (e.g. accumulate an RDF histogram): no synchronisation."""
+    device work (e.g. accumulate an RDF histogram): no synchronisation.
+
+    A neighbour-row overflow on the device (no reference analogue) repeats
+    the run from the initial state with larger rows.  Before a repeat every
+    hook with a ``reset()`` method is reset, so its state reflects only the
+    attempt that completes; a hook without one sees the repeated iterations
+    again (the reference never repeats a run)."""
     if not isinstance(container, (CudaLinkedCells, CudaDirectSum)):
         raise TypeError("respa_run needs a CudaLinkedCells or CudaDirectSum container "
                         "(GPU only, no host fallback)")
@@ -433,19 +504,77 @@ def respa_run(system, ff, container, schedule: RespaSchedule, sample_interval: O
     v0 = np.array(system.velocities, copy=True)
     slots = None
     for attempt in range(3):
-        run = DeviceRespa(system, ff, container, schedule, sample_interval, capacity=capacity,
-                          use_graph=use_graph and not hooks, skin=skin)
-        run.slots = slots
+        run = _cached_run(system, ff, container, schedule, sample_interval, capacity,
+                          use_graph and not hooks, skin) if attempt == 0 else None
+        if run is None:
+            run = DeviceRespa(system, ff, container, schedule, sample_interval,
+                              capacity=capacity, use_graph=use_graph and not hooks, skin=skin)
+            run.slots = slots
         LAST_RUN[0] = run
         try:
-            return _drive(run, hooks, tuple(device_hooks))
+            run.eng.busy = True
+            trace = _drive(run, hooks, tuple(device_hooks))
+            _keep_run(run, capacity, skin)
+            return trace
         except CapacityError:
+            _RUNS.pop(_run_key(run.n, sample_interval, capacity, skin), None)
             capacity = min(4096, _round_up(int(run.capacity * 1.5) + 32, 32))
             slots = capacity
             run.eng.grow_cells()
             system.positions[:] = x0
             system.velocities[:] = v0
+            _reset_hooks(hooks + tuple(device_hooks))
+        finally:
+            run.eng.busy = False
     raise CapacityError("neighbour rows kept overflowing")
+
+
+# The most recent graph-driven run per (n, sample interval, requested
+# capacity, skin): its buffers, rows and captured period graph are reused by
+# the next respa_run of the same shape (DeviceRespa.cache_key), which then
+# pays upload, the initial passes, the replays and the download -- no
+# allocation, capture or eager warm-up period.
+_RUNS = {}
+
+
+def _run_key(n, interval, capacity, skin):
+    return (int(n), int(interval), capacity, skin)
+
+
+def _cached_run(system, ff, container, schedule, interval, capacity, use_graph, skin):
+    if not use_graph:
+        return None
+    run = _RUNS.get(_run_key(system.positions.shape[0], interval, capacity, skin))
+    if run is None or run.graph is None or run.eng.busy:
+        return None
+    probe = DeviceRespa.__new__(DeviceRespa)  # the key of the new run, without allocating
+    probe.ff, probe.system, probe.container, probe.schedule = ff, system, container, schedule
+    probe.n, probe.periodic = system.positions.shape[0], bool(system.periodic)
+    probe.box = np.ascontiguousarray(system.box, dtype=np.float64)
+    probe.nu, probe.rc2, probe.rc3 = float(ff.nu), float(ff.cutoff), triplet_cutoff(ff)
+    probe.dt, probe.interval = schedule.dt, int(interval)
+    probe.skin, probe.use_graph = run.skin, use_graph
+    probe.capacity, probe.slots = run.capacity, run.slots
+    if probe.cache_key() != run.cache_key():
+        return None
+    if skin is not None and run.skin != min(float(skin), run.skin):
+        return None
+    return run if run.rebind(system, container, schedule) else None
+
+
+def _keep_run(run, capacity, skin) -> None:
+    if run.use_graph and run.graph is not None:
+        if len(_RUNS) > 4:
+            _RUNS.clear()
+        _RUNS[_run_key(run.n, run.interval, capacity, skin)] = run
+
+
+def _reset_hooks(hooks) -> None:
+    """Tell hooks that the run starts over (capacity retry)."""
+    for hook in hooks:
+        reset = getattr(hook, "reset", None)
+        if callable(reset):
+            reset()
 
 
 def _drive(run: DeviceRespa, hooks, device_hooks=()) -> RunTrace:
@@ -486,7 +615,17 @@ def _drive(run: DeviceRespa, hooks, device_hooks=()) -> RunTrace:
         return trace
     mark = run.marks.append
     mark(("started", time.perf_counter()))
-    if n_periods > 0 and run.use_graph:
+    if n_periods > 0 and run.use_graph and run.graph is not None:
+        # a cached run (same shape): its captured period graph replays from
+        # the first period on
+        if device_hooks:
+            for k in range(n_periods):
+                run.run_periods(k, 1)
+                on_device(k + 1)
+        else:
+            run.run_periods(0, n_periods)
+        mark(("replays enqueued (cached graph)", time.perf_counter()))
+    elif n_periods > 0 and run.use_graph:
         run.run_periods(0, 1)  # warm-up, also the first period of the run
         on_device(1)
         mark(("eager period", time.perf_counter()))
@@ -508,11 +647,21 @@ def _drive(run: DeviceRespa, hooks, device_hooks=()) -> RunTrace:
     for i in range(n_periods * run.interval, run.schedule.num_iterations):
         run._step(i)  # iterations past the last sample point
     run.finish_scalars()
-    _check(run, trace, upto=n_periods + 1)
-    mark(("checked (synced)", time.perf_counter()))
-    _fill_trace(trace, run.trace_rows(n_periods + 1), float(sysm.mass))
-    run.download()
-    run.update_container()
+    upto = n_periods + 1
+    pin = run.collect(upto)  # the one synchronisation of the run
+    mark(("collected (synced)", time.perf_counter()))
+    word = int(pin["status"][0]) & 0xFFFFFFFFFFFFFFFF
+    kind = word & 0xFF if word != _lib.RB_STATUS_CLEAR else None
+    if int(pin["maxc"][0]) > run.eng.capacity or kind == _lib.RB_KIND_CAPACITY:
+        raise CapacityError("neighbour row overflow")
+    rows = pin["trace"][:upto].numpy()
+    if kind is not None:  # as _check: the trace up to the failing step, the state
+        tag = word >> 8
+        _fill_trace(trace, rows[rows[:, 0] < tag] if tag > 0 else rows[:0], float(sysm.mass))
+        run.apply_collected(pin)
+        raise IntegrationBlowUp(int(tag), _MSG.get(kind, f"device error kind {kind}"), trace)
+    _fill_trace(trace, rows, float(sysm.mass))
+    run.apply_collected(pin)
     mark(("downloaded", time.perf_counter()))
     return trace
 
@@ -576,36 +725,63 @@ def equilibrate(system, ff, container, dt: float, steps: int, target_temperature
         raise ValidationError("steps must be >= 0")
     if not isinstance(container, (CudaLinkedCells, CudaDirectSum)):
         raise TypeError("equilibrate needs a CudaLinkedCells or CudaDirectSum container")
+    x0 = np.array(system.positions, copy=True)
+    v0 = np.array(system.velocities, copy=True)
+    capacity = None
+    for attempt in range(3):  # a row overflow repeats the run larger (as respa_run)
+        try:
+            return _equilibrate(system, ff, container, dt, steps, target_temperature,
+                                rescale_interval, capacity)
+        except CapacityError as exc:
+            capacity = min(4096, _round_up(int(exc.args[1] * 1.5) + 32, 32)) \
+                if len(exc.args) > 1 else None
+            engine_for(system.positions.shape[0]).grow_cells()
+            system.positions[:] = x0
+            system.velocities[:] = v0
+    raise CapacityError("neighbour rows kept overflowing")
+
+
+def _equilibrate(system, ff, container, dt, steps, target_temperature, rescale_interval,
+                 capacity) -> EquilibrationReport:
     factors, temperatures = [], []
     if steps > 0:
         interval = int(rescale_interval)
-        run = DeviceRespa(system, ff, container, RespaSchedule(dt, 1, steps), interval)
+        run = DeviceRespa(system, ff, container, RespaSchedule(dt, 1, steps), interval,
+                          capacity=capacity)
         run.start()
         n, m = system.positions.shape[0], float(system.mass)
         eng = run.eng
         done = 0
-        while done < steps:
-            chunk = min(interval, steps - done)
-            if chunk == interval and run.use_graph and run.graph is not None:
-                run.graph.replay()
-            else:
-                for i in range(done, done + chunk):
-                    run._step(i)
-                if chunk == interval and run.use_graph and run.graph is None:
-                    run.capture()  # the windows repeat (s = 1): one graph serves all
-            done += chunk
-            _check(run, RunTrace(), upto=(done + interval - 1) // interval + 1)
-            eng.sum_f64(run.v, 0, square=True, n=3 * n)
-            kinetic = 0.5 * m * float(eng.scalars[0].item())
-            t_now = 2.0 * kinetic / (3.0 * n)
-            temperatures.append(t_now)
-            if t_now > 0:
-                factor = math.sqrt(target_temperature / t_now)
-                run.v.mul_(factor)
-                factors.append(factor)
+        try:
+            while done < steps:
+                chunk = min(interval, steps - done)
+                if chunk == interval and run.use_graph and run.graph is not None:
+                    run.graph.replay()
+                else:
+                    for i in range(done, done + chunk):
+                        run._step(i)
+                    if chunk == interval and run.use_graph and run.graph is None:
+                        run.capture()  # the windows repeat (s = 1): one graph serves all
+                done += chunk
+                _check(run, RunTrace(), upto=(done + interval - 1) // interval + 1)
+                eng.sum_f64(run.v, 0, square=True, n=3 * n)
+                kinetic = 0.5 * m * float(eng.scalars[0].item())
+                t_now = 2.0 * kinetic / (3.0 * n)
+                temperatures.append(t_now)
+                if t_now > 0:
+                    factor = math.sqrt(target_temperature / t_now)
+                    run.v.mul_(factor)
+                    factors.append(factor)
+        except CapacityError as exc:  # carry the capacity that overflowed
+            raise CapacityError("neighbour row overflow", run.capacity) from exc
         run.finish_scalars()
         run.download()
         run.update_container()
+    return _equilibrate_report(system, factors, temperatures, steps, target_temperature)
+
+
+def _equilibrate_report(system, factors, temperatures, steps,
+                        target_temperature) -> EquilibrationReport:
     tail = temperatures[-max(1, len(temperatures) // 10):] if temperatures else []
     tail_t = float(np.mean(tail)) if tail else measured_temperature(system)
     converged = steps == 0 or abs(tail_t - target_temperature) <= 0.02 * target_temperature

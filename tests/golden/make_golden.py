@@ -30,6 +30,7 @@ and tests/helpers.random_positions); the reference only supplies outputs.
 
 from __future__ import annotations
 
+import glob
 import hashlib
 import os
 import sys
@@ -157,6 +158,30 @@ def gen_large():
         )
         print(f"large_{name}: N={s.n} E2={e2!r} E3={e3!r} visits={visits} "
               f"({time.perf_counter() - t0:.1f}s)")
+
+
+def fill_large_visits():
+    """The large fixtures of n > 300k carry no reference visit count (the
+    reference's collect_triplet_visits is too slow there): fill it from the
+    oracle's C01 enumeration, which is bit-pinned against the reference on
+    every smaller fixture (tests/test_oracle_golden.py).  Marks the source."""
+    from oracle import oracle as orc
+
+    orc.build()
+    orc.set_num_threads(os.cpu_count() or 1)
+    for path in sorted(glob.glob(os.path.join(HERE, "large_*.npz"))):
+        d = dict(np.load(path, allow_pickle=False))
+        if int(d["visits"]) >= 0:
+            continue
+        cfg_name = os.path.basename(path)[len("large_"):].split(".npz")[0].split("_")[0]
+        s = systems.CONFIGS[cfg_name].system()
+        assert pos_sha(s.positions) == str(d["sha"])
+        os_ = orc.OracleSystem.from_positions(s.positions, s.box, True)
+        grid = orc.build_cell_grid(os_, float(d["rc3"]))
+        d["visits"] = np.int64(orc.triplet_visit_count(grid, os_))
+        d["visits_source"] = np.array("oracle")
+        np.savez_compressed(path, **d)
+        print(f"{os.path.basename(path)}: visits {int(d['visits'])} (oracle)")
 
 
 class SplitCutoffLC:
@@ -315,6 +340,7 @@ def gen_lattice():
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["potentials", "small", "large", "respa", "direct", "rdf", "lattice"]
+    what = sys.argv[1:] or ["potentials", "small", "large", "large_visits", "respa", "direct",
+                            "rdf", "lattice"]
     for w in what:
-        globals()[f"gen_{w}"]()
+        (fill_large_visits if w == "large_visits" else globals()[f"gen_{w}"])()

@@ -1,0 +1,117 @@
+"""Full-array parity at the BASELINE configurations (cfg2 .. cfg5).
+
+tests/test_gpu_parity.py checks the large configurations against the
+reference fixtures (energies, virials, counts, a 39-particle force subset).
+Here every array is compared, at BASELINE.json's sizes, against the oracle's
+C restatement (oracle/oracle.c, OpenMP on the host; bit-pinned against the
+reference by tests/test_oracle_golden.py):
+
+* binning: ``cell_start`` and ``cell_particles`` bit-equal to the oracle's
+  ``build_cell_grid`` (containers.py:175-209, 235-279);
+* unique triplet counts bit-exact (containers.py:825-849; the reference pins
+  the count in test_containers.py:168-175) -- cfg4 is lattice-determined at
+  430,080,000;
+* the full (N, 3) pair and triplet forces normwise within 1e-10 of the
+  oracle's C01 passes, energies within 1e-10 and virials within 1e-9
+  relative (the reference's own C01-vs-brute-force tolerances);
+* both triplet-pass forms (row-based and cell-based) on every configuration.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FORCE_TOL = 1e-10
+ENERGY_TOL = 1e-10
+VIRIAL_TOL = 1e-9
+
+CASES = [("cfg2", None), ("cfg3", 2.0), ("cfg3", 2.5), ("cfg3", 3.0), ("cfg4", None),
+         ("cfg5", None)]
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2507_11172_b200 as p
+    from paper_2507_11172_b200 import _lib
+
+    _lib.require_device()  # GPU tests fail loudly without the device path
+    return p
+
+
+def _normwise(a, b):
+    return float(np.max(np.linalg.norm(a - b, axis=1)) / np.max(np.linalg.norm(b, axis=1)))
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def oracle_results(oracle):
+    """Oracle passes per case, computed once (OpenMP over the host's cores)."""
+    import paper_2507_11172_b200 as p
+
+    oracle.set_num_threads(os.cpu_count() or 1)
+    cache = {}
+
+    def get(cfg_name, rc3):
+        key = (cfg_name, rc3)
+        if key not in cache:
+            cfg = p.systems.CONFIGS[cfg_name]
+            s = cfg.system()
+            rc3_ = cfg.rc_atm if rc3 is None else rc3
+            os_ = oracle.OracleSystem.from_positions(s.positions, s.box, True)
+            g2 = oracle.build_cell_grid(os_, cfg.rc_lj)
+            f2, e2, w2 = oracle.c01_pair_pass(g2, os_, oracle.OracleForceField(
+                nu=p.systems.NU, cutoff=cfg.rc_lj))
+            g3 = oracle.build_cell_grid(os_, rc3_)
+            f3, e3, w3 = oracle.c01_triplet_pass(g3, os_, oracle.OracleForceField(
+                nu=p.systems.NU, cutoff=rc3_))
+            visits = oracle.triplet_visit_count(g3, os_)
+            cache[key] = dict(s=s, cfg=cfg, rc3=rc3_, f2=f2, e2=e2, w2=w2, f3=f3, e3=e3, w3=w3,
+                              visits=visits, cell_start=g3.cell_start.copy(),
+                              cell_particles=g3.cell_particles.copy(), ncell=g3.num_cells)
+        return cache[key]
+
+    return get
+
+
+@pytest.mark.parametrize("mode", ["rows", "cells"])
+@pytest.mark.parametrize("cfg_name,rc3", CASES)
+def test_full_arrays_against_oracle(pkg, oracle_results, monkeypatch, cfg_name, rc3, mode):
+    from paper_2507_11172_b200.containers import engine_for
+    from paper_2507_11172_b200.engine import ForceEngine
+
+    monkeypatch.setattr(ForceEngine, "CELLS_MODE", "1" if mode == "cells" else "0")
+    ref = oracle_results(cfg_name, rc3)
+    s, cfg = ref["s"].copy(), ref["cfg"]
+    ff = pkg.ForceField(nu=pkg.systems.NU, cutoff=cfg.rc_lj,
+                        cutoff_3b=None if ref["rc3"] == cfg.rc_lj else ref["rc3"])
+    c = pkg.CudaLinkedCells()
+    c.pair_pass(s, ff)
+    c.triplet_pass(s, ff)
+    eng = engine_for(s.n)
+    if mode == "cells":
+        from paper_2507_11172_b200.containers import _geometry_for
+
+        assert eng.uses_cells(_geometry_for(s, ref["rc3"]), ref["rc3"])
+    # binning of the triplet pass's grid, bit for bit
+    ncell = ref["ncell"]
+    np.testing.assert_array_equal(eng.cell_start[: ncell + 1].cpu().numpy(), ref["cell_start"])
+    np.testing.assert_array_equal(eng.parts[: s.n].cpu().numpy(), ref["cell_particles"])
+    # counts bit-exact
+    assert c.triplet_visits == ref["visits"]
+    if cfg_name == "cfg4":
+        assert c.triplet_visits // 3 == 430_080_000
+    # every force, energies, virials
+    assert _normwise(s.forces_2b, ref["f2"]) <= FORCE_TOL
+    assert _normwise(s.forces_3b, ref["f3"]) <= FORCE_TOL
+    assert _rel(c.pair_energy, ref["e2"]) <= ENERGY_TOL
+    assert _rel(c.triplet_energy, ref["e3"]) <= ENERGY_TOL
+    assert _rel(c.pair_virial, ref["w2"]) <= VIRIAL_TOL
+    assert _rel(c.triplet_virial, ref["w3"]) <= VIRIAL_TOL

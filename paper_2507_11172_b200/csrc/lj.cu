@@ -37,6 +37,9 @@ __device__ __forceinline__ double lj_rcp(double x) {
 #ifndef RB_LJ_MIN_BLOCKS
 #define RB_LJ_MIN_BLOCKS 4  // 64 registers: 4 blocks of 256 per SM
 #endif
+// kScalars: accumulate the energy and virial (sample points); without it
+// the pass writes forces only (energy_rank / virial_rank untouched)
+template <bool kScalars>
 __global__ void __launch_bounds__(kLjThreads, RB_LJ_MIN_BLOCKS)
     k_lj(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ parts,
          const int32_t *__restrict__ rows, const int32_t *__restrict__ row_count,
@@ -81,61 +84,71 @@ __global__ void __launch_bounds__(kLjThreads, RB_LJ_MIN_BLOCKS)
     const Image im = make_image(g);
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
     bool bad = false;
-    if (active) {
+    {  // (inactive lanes: empty rows; every lane takes part in the warp votes)
 #pragma unroll
         for (int u = 0; u < kLjRowRegs; u++) {
             const int k = sub + u * kLjGroup;
             if (k >= m) jr[u] = -1;
         }
-        auto visit = [&](int q, double px, double py, double pz) {
+        const int self = active ? (int)r : 0;
+        // branch-free visit: the kernel runs for every entry and the scale
+        // is selected (zero beyond the cutoff, for an empty slot and for a
+        // guarded pair, potentials.py:35-36), so the lanes never diverge
+        auto visit = [&](bool valid, double px, double py, double pz) {
             double dx, dy, dz;
             exact_disp(im, xi, yi, zi, px, py, pz, dx, dy, dz);
             const double r2 = exact_r2(dx, dy, dz);
-            if (r2 > rc2) return;
-            if (r2 < RB_MIN_DISTANCE_SQ) {
-                bad = true;
-                return;
-            }
+            const bool in = valid && r2 <= rc2;
+            const bool guard = in && r2 < RB_MIN_DISTANCE_SQ;
+            bad = bad || guard;
             const double inv_r2 = lj_rcp(r2);
             const double x = sigma2 * inv_r2;
             const double r6 = x * x * x;
             const double r12 = r6 * r6;
-            const double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
-            fx += scale * dx;
-            fy += scale * dy;
-            fz += scale * dz;
-            e += eps4 * (r12 - r6);
-            w += scale * r2;
+            double scale = eps24 * (2.0 * r12 - r6) * inv_r2;
+            scale = in && !guard ? scale : 0.0;
+            fx = fma(scale, dx, fx);
+            fy = fma(scale, dy, fy);
+            fz = fma(scale, dz, fz);
+            if (kScalars) {
+                e += in && !guard ? eps4 * (r12 - r6) : 0.0;
+                w = fma(scale, r2, w);
+            }
         };
 #pragma unroll
         for (int u = 0; u < kLjRowRegs; u += 2) {
-            if (jr[u] < 0) break;
-            const int qa = jr[u], qb = jr[u + 1] < 0 ? jr[u] : jr[u + 1];
+            const bool va = jr[u] >= 0, vb = jr[u + 1] >= 0;
+            if (!__any_sync(0xffffffffu, va)) break;  // the warp's rows are done
+            const int qa = va ? jr[u] : self, qb = vb ? jr[u + 1] : self;
             const double ax = pr[3 * qa], ay = pr[3 * qa + 1], az = pr[3 * qa + 2];
             const double bx = pr[3 * qb], by = pr[3 * qb + 1], bz = pr[3 * qb + 2];
-            visit(qa, ax, ay, az);
-            if (jr[u + 1] >= 0) visit(qb, bx, by, bz);
+            visit(va, ax, ay, az);
+            visit(vb, bx, by, bz);
         }
         for (int k = sub + kLjRowRegs * kLjGroup; k < m; k += kLjGroup) {  // long rows
             const int q = __ldg(row + k);
-            visit(q, pr[3 * q], pr[3 * q + 1], pr[3 * q + 2]);
+            visit(true, pr[3 * q], pr[3 * q + 1], pr[3 * q + 2]);
         }
     }
     fx = group_sum<kLjGroup>(fx);
     fy = group_sum<kLjGroup>(fy);
     fz = group_sum<kLjGroup>(fz);
-    e = group_sum<kLjGroup>(e);
-    w = group_sum<kLjGroup>(w);
+    if (kScalars) {
+        e = group_sum<kLjGroup>(e);
+        w = group_sum<kLjGroup>(w);
+    }
     if (active && bad) record_status(status, tag, RB_KIND_PAIR_MIN_SEPARATION);
     if (active && sub == 0) {
         const int64_t p = parts[r];
         forces[3 * p] = fx;
         forces[3 * p + 1] = fy;
         forces[3 * p + 2] = fz;
-        // decomposed runs: only owned particles carry energy (phi/2 per visit)
-        const double own = owned ? (double)owned[r] : 1.0;
-        energy_rank[r] = own * (0.5 * e);
-        virial_rank[r] = own * (0.5 * w);
+        if (kScalars) {
+            // decomposed runs: only owned particles carry energy (phi/2 per visit)
+            const double own = owned ? (double)owned[r] : 1.0;
+            energy_rank[r] = own * (0.5 * e);
+            virial_rank[r] = own * (0.5 * w);
+        }
     }
 }
 
@@ -152,7 +165,10 @@ extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r, cons
     if (n == 0) return RB_OK;
     const int64_t threads = n * kLjGroup;
     unsigned blocks = (unsigned)((threads + kLjThreads - 1) / kLjThreads);
-    launch(k_lj, dim3(blocks), dim3(kLjThreads), 0, as_stream(stream), *g, n, pos_r, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
+    // energy_rank == virial_rank == NULL: forces only (steps that are not
+    // sample points, whose scalars nothing reads)
+    auto kern = energy_rank && virial_rank ? k_lj<true> : k_lj<false>;
+    launch(kern, dim3(blocks), dim3(kLjThreads), 0, as_stream(stream), *g, n, pos_r, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
         4.0 * epsilon, sigma * sigma, forces, energy_rank, virial_rank, owned, status, tag);
     note_launches(1);
     return launch_status();

@@ -292,8 +292,8 @@ class ForceEngine:
 
     # -------------------------------------------------------------- passes
     def lj(self, geom: Geometry, rc: float, epsilon: float, sigma: float, forces,
-           tag: int = 0, reduce: bool = True) -> None:
-        self.lj_kernel(geom, rc, epsilon, sigma, forces, tag)
+           tag: int = 0, reduce: bool = True, scalars: bool = True) -> None:
+        self.lj_kernel(geom, rc, epsilon, sigma, forces, tag, scalars=scalars)
         if reduce:
             self.reduce_pair()
 
@@ -302,14 +302,16 @@ class ForceEngine:
         self.sum_f64(self.w2_rank, SCALAR_W2)
 
     def lj_kernel(self, geom: Geometry, rc: float, epsilon: float, sigma: float, forces,
-                  tag: int = 0) -> None:
-        """The rb_lj_pass launch alone."""
+                  tag: int = 0, scalars: bool = True) -> None:
+        """The rb_lj_pass launch alone; scalars=False: forces only (the
+        per-rank energy and virial are left as they are)."""
         g = self.grid_struct(geom)
+        e2 = ptr(self.e2_rank) if scalars else _NULL
+        w2 = ptr(self.w2_rank) if scalars else _NULL
         st = self.L.rb_lj_pass(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.parts),
                                ptr(self.rows), ptr(self.row_count), int(self.capacity), float(rc),
-                               float(epsilon), float(sigma), ptr(forces), ptr(self.e2_rank),
-                               ptr(self.w2_rank), self._owned(), ptr(self.status), int(tag),
-                               self.stream)
+                               float(epsilon), float(sigma), ptr(forces), e2, w2, self._owned(),
+                               ptr(self.status), int(tag), self.stream)
         _lib.check(st, "rb_lj_pass")
 
     def atm(self, geom: Geometry, rc: float, nu: float, forces, tag: int = 0,

@@ -220,7 +220,11 @@ class DeviceRespa:
             return None  # the drift already recorded the non-finite state
         return geometry(self.box, pos, self.r_build, False)
 
-    def _forces(self, tag: int, with_triplet: bool, f2_out, cond: int = 0) -> None:
+    def _forces(self, tag: int, with_triplet: bool, f2_out, cond: int = 0,
+                scalars: bool = True) -> None:
+        """The step's passes.  scalars=False: the pair pass computes forces
+        only (a step inside a sampling period that is not its sample point:
+        nothing reads its pair energy / virial)."""
         eng = self.eng
         if self.direct:
             eng.direct_pairs(self.ff.epsilon, self.ff.sigma, f2_out, tag=tag, reduce=False)
@@ -263,11 +267,12 @@ class DeviceRespa:
             eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=1)
             with torch.cuda.stream(side):
                 eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag,
-                       reduce=False)
+                       reduce=False, scalars=scalars)
             main.wait_stream(side)
             eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=2)
             return
-        eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag, reduce=False)
+        eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag, reduce=False,
+               scalars=scalars)
         if with_triplet:
             if self.with_3b:
                 eng.atm(geom, self.rc3, self.nu, self.f3, tag=tag, count_visits=False,
@@ -319,7 +324,11 @@ class DeviceRespa:
                                   _lib.RB_TAG_FROM_DEVICE, 1, cond, eng.stream)
             _lib.check(st, "rb_respa_drift")
         end_of_cycle = (i + 1) % s == 0
-        self._forces(_lib.RB_TAG_FROM_DEVICE, end_of_cycle, self.f2_new, cond)
+        # pair scalars only where something reads them: the period's sample
+        # point, and every step run on its own (the last pass of a run feeds
+        # the container's scalars)
+        sample = j is None or (i + 1) % self.interval == 0
+        self._forces(_lib.RB_TAG_FROM_DEVICE, end_of_cycle, self.f2_new, cond, scalars=sample)
         if not defer:
             st = L.rb_respa_kick(self.n, ptr(self.v), ptr(self.f2_old), ptr(self.f2_new),
                                  ptr(self.f3), self.half_dt, self.half_respa, int(end_of_cycle),

@@ -298,6 +298,7 @@ extern "C" int rb_atm_pass_c01(const rb_grid *g, int64_t n, const double *pos_r,
                            double *forces, double *energy_rank, double *virial_rank,
                            int32_t *visits_rank, unsigned long long *status, int64_t tag,
                            void *stream) {
+    NvtxRange nvtx_range("triplet C01 (rb_atm_pass_c01)");
     if (!g || n < 0 || capacity <= 0 || capacity > 4096) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     const double rc2 = rc * rc;

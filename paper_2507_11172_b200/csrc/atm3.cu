@@ -102,7 +102,12 @@ __device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image
                 exact_disp(im, xi, yi, zi, px[h], py[h], pz[h], dx, dy, dz);
                 r2 = exact_r2(dx, dy, dz);
                 keep = r2 <= rc2;
-                if (!keep) {  // beyond the three-body cutoff: contributes nothing
+                // beyond the three-body cutoff: contributes nothing.  (A row
+                // truncated at its capacity has no mirror entry, -1: that pass
+                // is reported as a capacity error and repeated; nothing is
+                // written for it.)
+                if (!keep && mk2[h] >= 0) {
+                    RB_CHECK(mk2[h] < capacity);
                     double *gq = gbuf + ((int64_t)q * capacity + mk2[h]) * 3;
                     gq[0] = 0.0;
                     gq[1] = 0.0;
@@ -121,6 +126,7 @@ __device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image
             }
             if (keep) {
                 const int slot = m + __popc(mk & lanemask_lt());
+                RB_CHECK(slot < slots && k < capacity && mk2[h] < capacity);
                 sm.xy[slot] = make_double2(dx, dy);
                 sm.zr[slot] = make_double2(dz, r2);
                 sm.axy[slot] = make_double2(0.0, 0.0);
@@ -213,10 +219,13 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
             ay = axy.y;
             az = sm.az[sl];
         }
-        double *gq = gbuf + ((int64_t)sm.q[sl] * capacity + sm.mpos[sl]) * 3;
-        gq[0] = ax;
-        gq[1] = ay;
-        gq[2] = az;
+        RB_CHECK(sm.q[sl] >= 0 && sm.q[sl] < n && sm.mpos[sl] < capacity);
+        if (sm.mpos[sl] >= 0) {  // (-1: a truncated row, see a3_slots)
+            double *gq = gbuf + ((int64_t)sm.q[sl] * capacity + sm.mpos[sl]) * 3;
+            gq[0] = ax;
+            gq[1] = ay;
+            gq[2] = az;
+        }
         sx += ax;
         sy += ay;
         sz += az;
@@ -363,6 +372,7 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
             }
             more = in;
         }
+        RB_CHECK(m >= 0 && m <= capacity);
         for (; more && k < m; k += kGatherGroup) {
             if (row[k] >= p) break;
             fx += gp[3 * k];
@@ -522,6 +532,7 @@ extern "C" int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r
                                 const uint8_t *owned, void *scratch, size_t scratch_bytes,
                                 unsigned long long *status, int64_t tag, int32_t part,
                                 void *stream) {
+    NvtxRange nvtx_range("triplet (rb_atm_pass_part)");
     if (part < 0 || part > 2) return RB_ERR_ARGUMENT;
     if (!g || n < 0 || capacity <= 0 || capacity > 4096 || !mirror || !scratch) return RB_ERR_ARGUMENT;
     if (slot_capacity <= 0 || slot_capacity > capacity) slot_capacity = capacity;

@@ -253,7 +253,10 @@ __global__ void __launch_bounds__(kACWarps * 32, RB_AC_MIN_BLOCKS)
                     over = true;
                     break;
                 }
-                if (pass) cand[nc + __popc(mk & lanemask_lt())] = k;
+                if (pass) {
+                    RB_CHECK(nc + __popc(mk & lanemask_lt()) < cand_cap);
+                    cand[nc + __popc(mk & lanemask_lt())] = k;
+                }
                 nc += __popc(mk);
             }
             __syncwarp();
@@ -267,6 +270,7 @@ __global__ void __launch_bounds__(kACWarps * 32, RB_AC_MIN_BLOCKS)
                 double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;
                 if (ci < nc) {
                     k = cand[ci];
+                    RB_CHECK(k >= 0 && k < total);
                     exact_disp(im, xi, yi, zi, nbx[3 * k], nbx[3 * k + 1], nbx[3 * k + 2], dx, dy,
                                dz);
                     r2 = exact_r2(dx, dy, dz);
@@ -318,6 +322,7 @@ __global__ void __launch_bounds__(kACWarps * 32, RB_AC_MIN_BLOCKS)
                     az = sm.az[s];
                 }
                 const int k = sm.kidx[s] & kKidxMask;
+                RB_CHECK(k < total && total <= nb_cap);
                 double2 t = my_ta_xy[k];
                 t.x += ax;
                 t.y += ay;
@@ -364,6 +369,7 @@ __global__ void __launch_bounds__(kACWarps * 32, RB_AC_MIN_BLOCKS)
                 y += t.y;
                 z += ta_z[(size_t)w * nb_cap + k];
             }
+            RB_CHECK(j < kACMaxOffsets && h_off[j] < g.n_offsets);
             g2[(size_t)nbr[k] * kACMaxOffsets + h_off[j]] = make_double4(x, y, z, 0.0);
         }
         __syncthreads();
@@ -481,6 +487,7 @@ extern "C" int rb_atm_pass_cells(const rb_grid *g, int64_t n, const double *pos_
                                  int32_t *triplets_rank, const uint8_t *owned, void *scratch,
                                  size_t scratch_bytes, unsigned long long *status, int64_t tag,
                                  int32_t part, void *stream) {
+    NvtxRange nvtx_range("triplet (rb_atm_pass_cells)");
     if (part < 0 || part > 2) return RB_ERR_ARGUMENT;
     if (!g || n < 0 || !scratch || !cell_start || !cell_of_rank) return RB_ERR_ARGUMENT;
     if (!rb_atm_cells_supported(g, rc)) return RB_ERR_ARGUMENT;

@@ -53,6 +53,7 @@ __device__ __forceinline__ A3Smem a3_carve(char *base, int m_rt) {
 
 __device__ __forceinline__ void ld_rec(const A3Smem &sm, int s, double &x, double &y, double &z,
                                        double &w) {
+    RB_CHECK(s >= 0 && s <= 4096);
     const double2 a = sm.xy[s];
     const double2 b = sm.zr[s];
     x = a.x;
@@ -63,6 +64,7 @@ __device__ __forceinline__ void ld_rec(const A3Smem &sm, int s, double &x, doubl
 
 // slot s's force sum += f (x, y, z)
 __device__ __forceinline__ void acc_add(const A3Smem &sm, int s, double fx, double fy, double fz) {
+    RB_CHECK(s >= 0 && s <= 4096);
     double2 xy = sm.axy[s];
     double zz = sm.az[s];
     xy.x += fx;
@@ -227,6 +229,7 @@ __device__ __forceinline__ void a3_windows(const A3Smem &sm, int m, int M, int l
                                            const rb_grid &g, const double *__restrict__ pr,
                                            const A3Cut &cut, A3Acc &acc, double F[3]) {
     double fj[3], fk[3];
+    RB_CHECK(m >= 0 && m <= M);
     if (m >= 32) {
         const int pairs = m * (m - 1) / 2;
         int s = lane, d = 1;  // pair f0 + lane is (round d, slot s)

@@ -162,6 +162,7 @@ extern "C" int rb_bin(const rb_grid *g, int64_t n, const double *pos, int32_t *c
                       int32_t *rank_of, double *x_ref, const int64_t *rebuild_flag,
                       const unsigned long long *status, int64_t tag, void *scratch,
                       size_t scratch_bytes, void *stream) {
+    NvtxRange nvtx_range("bin (rb_bin)");
     if (!g || n < 0) return RB_ERR_ARGUMENT;
     int64_t ncell = (int64_t)g->cells[0] * g->cells[1] * g->cells[2];
     if (ncell <= 0) return RB_ERR_GEOMETRY;

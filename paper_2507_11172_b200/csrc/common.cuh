@@ -2,17 +2,43 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include "../../include/respa_b200.h"
 
 #define RB_MIN_DISTANCE_SQ (1e-10 * 1e-10)  // respamd/potentials.py:35-36
 
+// Bounds checks of the checked build (-DRB_CHECKED, tools/checked_build.sh):
+// every index-computed shared / global access of the hot kernels is
+// checked and a violation printed (no trap: the run goes on and the test
+// log is grepped for "RB_CHECK failed").  compute-sanitizer is closed on
+// this pool; these checks plus the CPU-oracle comparisons stand in for it.
+#ifdef RB_CHECKED
+#include <cstdio>
+#define RB_CHECK(c)                                                                          \
+    do {                                                                                     \
+        if (!(c)) printf("RB_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);             \
+    } while (0)
+#else
+#define RB_CHECK(c) ((void)0)
+#endif
+
 namespace rb {
 
 constexpr int kWarp = 32;
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// NVTX range around a C-ABI entry point (its launches): the phases of a
+// step -- bin / rebuild, pair, triplet, kick / drift, halo -- show up by
+// name under Nsight Systems (header-only NVTX3: no cost without a tool)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // host-side count of kernel launches issued by this library (rb_launch_count)
 void note_launches(int k);

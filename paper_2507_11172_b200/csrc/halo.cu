@@ -85,6 +85,7 @@ extern "C" int rb_halo_pull(int64_t n, const int32_t *src_rank, const int32_t *s
                             const uint64_t *peers, int64_t stride,
                             const unsigned long long *status, int64_t first, double *pos,
                             const int32_t *rank_of, double *pos_r, void *stream) {
+    NvtxRange nvtx_range("halo (rb_halo_pull)");
     if (n < 0 || first < 0 || stride < 0 ||
         (n > 0 && (!src_rank || !src_index || !peers || !status || !pos || (pos_r && !rank_of))))
         return RB_ERR_ARGUMENT;
@@ -134,6 +135,7 @@ extern "C" int rb_ipc_close(void *ptr) {
 
 extern "C" int rb_halo_pack(int64_t n, const int32_t *idx, const double *pos, double *buf,
                             void *stream) {
+    NvtxRange nvtx_range("halo (rb_halo_pack)");
     if (n < 0 || (n > 0 && (!idx || !pos || !buf))) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     launch(k_halo_pack, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, as_stream(stream), n,
@@ -144,6 +146,7 @@ extern "C" int rb_halo_pack(int64_t n, const int32_t *idx, const double *pos, do
 
 extern "C" int rb_halo_unpack(int64_t n, const double *buf, int64_t first, double *pos,
                               const int32_t *rank_of, double *pos_r, void *stream) {
+    NvtxRange nvtx_range("halo (rb_halo_unpack)");
     if (n < 0 || first < 0 || (n > 0 && (!buf || !pos || (pos_r && !rank_of))))
         return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;

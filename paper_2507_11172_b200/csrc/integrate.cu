@@ -447,6 +447,7 @@ extern "C" int rb_respa_drift(int64_t n, double *pos, double *vel, const double 
                               double skin, int64_t *rebuild_flag, unsigned long long *status,
                               int64_t tag, int32_t advance_step, uint64_t rebuild_cond,
                               void *stream) {
+    NvtxRange nvtx_range("drift (rb_respa_drift)");
     return drift_launch(n, pos, vel, const_cast<double *>(f2_old), nullptr, f3, box3_host,
                         periodic, dt, 0.0, half_drift, half_respa, kick3, 0, 0, rank_of, pos_r,
                         x_ref, skin, rebuild_flag, status, tag, advance_step, rebuild_cond,
@@ -461,6 +462,7 @@ extern "C" int rb_respa_drift_publish(int64_t n, double *pos, double *vel, const
                                       unsigned long long *status, int64_t tag,
                                       int32_t advance_step, double *publish, int64_t stride,
                                       void *stream) {
+    NvtxRange nvtx_range("drift+publish (rb_respa_drift_publish)");
     if (!publish || stride < n || !advance_step) return RB_ERR_ARGUMENT;
     return drift_launch(n, pos, vel, const_cast<double *>(f2_old), nullptr, f3, box3_host,
                         periodic, dt, 0.0, half_drift, half_respa, kick3, 0, 0, rank_of, pos_r,
@@ -476,6 +478,7 @@ extern "C" int rb_respa_kick_drift(int64_t n, double *pos, double *vel, double *
                                    double *pos_r, const double *x_ref, double skin,
                                    int64_t *rebuild_flag, unsigned long long *status,
                                    uint64_t rebuild_cond, void *stream) {
+    NvtxRange nvtx_range("kick+drift (rb_respa_kick_drift)");
     if (!status || !f2_new) return RB_ERR_ARGUMENT;
     return drift_launch(n, pos, vel, f2_old, f2_new, f3, box3_host, periodic, dt, half_dt,
                         half_drift, half_respa, kick3, 1, kick3_prev, rank_of, pos_r, x_ref, skin,
@@ -485,6 +488,7 @@ extern "C" int rb_respa_kick_drift(int64_t n, double *pos, double *vel, double *
 extern "C" int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f2_new,
                              const double *f3, double half_dt, double half_respa, int32_t kick3,
                              unsigned long long *status, int64_t tag, void *stream) {
+    NvtxRange nvtx_range("kick (rb_respa_kick)");
     if (n < 0) return RB_ERR_ARGUMENT;
     const int64_t n3 = 3 * n;
     if (n == 0 && (tag >= 0 || !status)) return RB_OK;  // (tag < 0: still closes the step)
@@ -506,6 +510,7 @@ extern "C" int rb_sample(int64_t n, const double *vel, const double *e2_rank,
                          const double *w2_rank, const double *e3_rank, const double *w3_rank,
                          double *sums, const unsigned long long *status, int64_t sample_interval,
                          double *trace, void *scratch, size_t scratch_bytes, void *stream) {
+    NvtxRange nvtx_range("sample (rb_sample)");
     if (n < 0 || !vel || !e2_rank || !w2_rank || !e3_rank || !w3_rank || !sums || !scratch)
         return RB_ERR_ARGUMENT;
     if (scratch_bytes < rb_sample_scratch_bytes(n)) return RB_ERR_ARGUMENT;

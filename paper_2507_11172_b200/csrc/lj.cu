@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(kLjThreads, RB_LJ_MIN_BLOCKS)
             const bool va = jr[u] >= 0, vb = jr[u + 1] >= 0;
             if (!__any_sync(0xffffffffu, va)) break;  // the warp's rows are done
             const int qa = va ? jr[u] : self, qb = vb ? jr[u + 1] : self;
+            RB_CHECK(qa >= 0 && qa < n && qb >= 0 && qb < n);
             const double ax = pr[3 * qa], ay = pr[3 * qa + 1], az = pr[3 * qa + 2];
             const double bx = pr[3 * qb], by = pr[3 * qb + 1], bz = pr[3 * qb + 2];
             visit(va, ax, ay, az);
@@ -161,6 +162,7 @@ extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r, cons
                           double sigma, double *forces, double *energy_rank, double *virial_rank,
                           const uint8_t *owned, unsigned long long *status, int64_t tag,
                           void *stream) {
+    NvtxRange nvtx_range("pair (rb_lj_pass)");
     if (!g || n < 0 || capacity <= 0) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     const int64_t threads = n * kLjGroup;

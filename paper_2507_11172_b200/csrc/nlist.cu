@@ -59,6 +59,7 @@ extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const 
                         double r_list, int32_t capacity, int32_t *rows, int32_t *row_count,
                         int32_t *max_count, const int64_t *rebuild_flag,
                         const unsigned long long *status, int64_t tag, void *stream) {
+    NvtxRange nvtx_range("rows (rb_nlist)");
     if (!g || n < 0 || capacity <= 0 || !max_count) return RB_ERR_ARGUMENT;
     if (g->n_offsets <= 0 || g->n_offsets > RB_MAX_OFFSETS) return RB_ERR_GEOMETRY;
     if (n == 0) return RB_OK;
@@ -74,6 +75,7 @@ extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const 
 extern "C" int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_count,
                                int32_t capacity, int32_t *mirror, const int64_t *rebuild_flag,
                                const unsigned long long *status, int64_t tag, void *stream) {
+    NvtxRange nvtx_range("rows mirror (rb_nlist_mirror)");
     if (n < 0 || capacity <= 0 || !rows || !row_count || !mirror) return RB_ERR_ARGUMENT;
     if (n == 0) return RB_OK;
     int64_t mblocks = (n + kMirrorWarps - 1) / kMirrorWarps;

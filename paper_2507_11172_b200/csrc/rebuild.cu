@@ -215,6 +215,7 @@ extern "C" int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_
                           int32_t *rows, int32_t *row_count, int32_t *max_count, int32_t *mirror,
                           const int64_t *rebuild_flag, const unsigned long long *status,
                           int64_t tag, void *scratch, size_t scratch_bytes, void *stream) {
+    NvtxRange nvtx_range("rebuild (rb_rebuild)");
     if (!g || n < 0 || capacity <= 0 || !max_count || !rows || !row_count || !mirror || !scratch)
         return RB_ERR_ARGUMENT;
     if (g->n_offsets <= 0 || g->n_offsets > RB_MAX_OFFSETS) return RB_ERR_GEOMETRY;

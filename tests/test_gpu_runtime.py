@@ -94,3 +94,25 @@ def test_equilibrate_retries_after_row_overflow(pkg, monkeypatch):
     assert len(calls) == 2 and len(rep.rescale_factors) == 2
     ref = pkg.systems.fcc_system(4, jitter=0.02, seed=3, temperature=0.9, vseed=4)
     np.testing.assert_array_equal(ref.positions, x0)
+
+
+@pytest.mark.parametrize("mode", ["rows", "cells"])
+def test_runs_are_bitwise_reproducible(pkg, monkeypatch, mode):
+    """Shared-memory ordering (warp sub-steps, per-warp target accumulators,
+    persistent work counters) must not leak into the results: two runs of
+    the same trajectory are bit-identical (a race would show up here; the
+    pool has no compute-sanitizer)."""
+    from paper_2507_11172_b200.engine import ForceEngine
+
+    monkeypatch.setattr(ForceEngine, "CELLS_MODE", "1" if mode == "cells" else "0")
+    ff = pkg.ForceField(nu=0.073, cutoff=2.5, cutoff_3b=3.0)
+    out = []
+    for _ in range(2):
+        s = pkg.systems.fcc_system(7, jitter=0.03, seed=11, temperature=1.2, vseed=12)
+        tr = pkg.respa_run(s, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 5, 50))
+        out.append((s, tr))
+    (a, ta), (b, tb) = out
+    assert np.array_equal(a.positions, b.positions)
+    assert np.array_equal(a.velocities, b.velocities)
+    assert np.array_equal(a.forces_3b, b.forces_3b)
+    assert ta.total == tb.total and ta.potential_3b == tb.potential_3b

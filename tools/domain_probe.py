@@ -1,9 +1,9 @@
 #!/usr/bin/env python
 """Per-step cost of the domain-decomposed loop on one GPU (world = 1).
 
-    python tools/domain_probe.py [--steps K] [--backend nccl|gloo]
+    python tools/domain_probe.py [--config cfg4] [--steps K] [--backend nccl|gloo]
 
-Runs domain_respa_run on cfg2 with a single rank: no halo,
+Runs domain_respa_run on a config (cfg2 default) with a single rank: no halo,
 but every per-step piece of the multi-GPU loop (drift, rebuild vote,
 refresh, passes, kicks, sample checks).  Prints ms/step (wall clock after a
 warm-up run) next to the single-GPU graph loop's.
@@ -32,10 +32,10 @@ def main(argv):
     import paper_2507_11172_b200 as pkg
     from paper_2507_11172_b200.domain_run import domain_respa_run, gpu_backend_factory
 
-    cfg = pkg.systems.CONFIGS["cfg2"]
+    cfg = pkg.systems.CONFIGS[argv[argv.index("--config") + 1] if "--config" in argv else "cfg2"]
     ff = cfg.force_field()
     sf = cfg.step_size_factor
-    domain_respa_run(dist, cfg.system(), ff, pkg.RespaSchedule(cfg.dt, sf, 20),
+    domain_respa_run(dist, cfg.system(), ff, pkg.RespaSchedule(cfg.dt, sf, 10),
                      gpu_backend_factory(ff))
     s = cfg.system()
     steps_run = {}

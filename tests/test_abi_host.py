@@ -246,3 +246,55 @@ def test_distributed_direct_sum_partition():
             work = m * (m - 1) / 2.0
             shares = [work[a:b].sum() for a, b in base_ranges(n, parts)]
             assert max(shares) - min(shares) <= work.max() + 1e-9 * work.sum()
+
+
+REF_SCENARIOS = "/root/reference/pkg/scenarios"
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SCENARIOS), reason="reference tree not present")
+def test_reference_bundled_scenarios_parse_identically():
+    """All five scenario files bundled with the reference (pkg/scenarios)
+    parse, and give the same plan as respamd's own parser (scenarios.py:150-214):
+    every configuration field, the sweeps and the (nu, s) grid."""
+    import dataclasses
+    import glob
+    import subprocess
+    import sys
+
+    from paper_2507_11172_b200 import parse_scenario
+
+    files = sorted(glob.glob(os.path.join(REF_SCENARIOS, "*.scenario")))
+    assert len(files) == 5
+    code = r"""
+import dataclasses, json, sys
+from respamd.scenarios import parse_scenario
+out = {}
+for f in sys.argv[1:]:
+    p = parse_scenario(f)
+    c = dataclasses.asdict(p.config)
+    out[f] = {"config": json.loads(json.dumps(c, default=lambda o: list(o))),
+              "nu": p.nu_values, "s": p.step_size_factors, "grid": p.grid()}
+print(json.dumps(out))
+"""
+    env = dict(os.environ, PYTHONPATH=REF_SRC, NUMBA_CACHE_DIR="/tmp/numba_cache_respamd")
+    res = subprocess.run([sys.executable, "-c", code, *files], capture_output=True, text=True,
+                         env=env, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    import json
+
+    ref = json.loads(res.stdout.splitlines()[-1])
+    for f in files:
+        plan = parse_scenario(f)
+        mine = json.loads(json.dumps(dataclasses.asdict(plan.config), default=lambda o: list(o)))
+        theirs = ref[f]["config"]
+        def same(a, b, where):  # every field the reference has, same value (ours may add
+            if isinstance(b, dict):  # e.g. force_field.cutoff_3b, None = as the reference)
+                for k, v in b.items():
+                    same(a.get(k), v, where + "." + k)
+            else:
+                assert a == b, (os.path.basename(f), where, a, b)
+
+        same(mine, theirs, "config")
+        assert plan.nu_values == ref[f]["nu"] and plan.step_size_factors == ref[f]["s"]
+        assert [list(g) for g in plan.grid()] == ref[f]["grid"]

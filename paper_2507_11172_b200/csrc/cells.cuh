@@ -136,12 +136,12 @@ template <bool kCoherent = false>
 __device__ __forceinline__ void nlist_one(const rb_grid &g, int64_t r, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ cell_start,
             const int32_t *__restrict__ cell_of_rank, double rl2, int32_t capacity,
             int32_t *__restrict__ rows, int32_t *__restrict__ row_count,
-            int32_t *__restrict__ max_count) {
+            int32_t *__restrict__ max_count, int cell = -1) {
     const int lane = threadIdx.x & 31;
     const Image im = make_image(g);
     const double xi = ldc<kCoherent>(pr + 3 * r), yi = ldc<kCoherent>(pr + 3 * r + 1),
                  zi = ldc<kCoherent>(pr + 3 * r + 2);
-    const int cb = ldc<kCoherent>(cell_of_rank + r);
+    const int cb = cell >= 0 ? cell : ldc<kCoherent>(cell_of_rank + r);
     const int cbz = cb % g.cells[2];
     const int cby = (cb / g.cells[2]) % g.cells[1];
     const int cbx = cb / (g.cells[2] * g.cells[1]);
@@ -250,6 +250,219 @@ __device__ __forceinline__ void mirror_one(int64_t p, int lane, const int32_t *_
             mirror[p * (int64_t)capacity + k] = pos;
             if (pos >= 0) mirror[(int64_t)q * capacity + pos] = k;
         }
+}
+
+// ---------------------------------------------------------------------------
+// Cell-staged rows: one CTA builds the rows of every particle of cell c.
+// The (at most 27) neighbour cells, sorted by flat id as in nlist_one, are
+// staged once into shared memory -- fp64 positions for the reference
+// arithmetic, fp32 minimum-image coordinates relative to c's centre for a
+// filter, ranks -- instead of every particle's warp gathering its ~27 x
+// occupancy candidates from L2.  Per particle: pass 1 keeps the candidates
+// whose fp32 distance is within r_list^2 (1 + 1e-3) (its error is ~1e-6 of
+// that: a superset of the survivors), in candidate order; pass 2 decides
+// them with the reference arithmetic (exact_disp, exact_r2, inclusive) and
+// appends the survivors in order.  Rows are identical to nlist_one's:
+// ascending rank, the same predicate.  A neighbourhood over nb_cap, or a
+// particle with more than kRowsBuf filter survivors, falls back to
+// nlist_one (the caller sees false / the particle is redone there).
+// ---------------------------------------------------------------------------
+constexpr int kRowsBuf = 256;  // filter survivors per particle (per warp)
+
+// The fp32 filter compares minimum-image coordinates relative to the cell's
+// centre; their difference is the pair's minimum image whenever the pair is
+// within the cutoff only if every periodic dimension has >= 4 cells (a
+// neighbour is at most 2 cells from the centre's image).  Smaller grids take
+// nlist_one.
+inline bool rows_staged_ok(const rb_grid &g) {
+    if (!g.periodic) return true;
+    for (int d = 0; d < 3; d++)
+        if ((g.wrap[d] ? g.cells[d] : g.gcells[d]) < 4) return false;
+    return true;
+}
+
+// staged particles per cell: 27 neighbour cells at twice the mean occupancy
+// (and at least 24 per cell); a denser neighbourhood takes nlist_one
+inline int rows_nb_cap(int64_t n, int64_t ncell) {
+    const double mean = ncell > 0 ? (double)n / (double)ncell : 0.0;
+    const double per = mean * 2.0 > 24.0 ? mean * 2.0 : 24.0;
+    int cap = (int)(27.0 * per) + 64;
+    cap = (cap + 31) / 32 * 32;
+    return cap < 2048 ? cap : 2048;
+}
+
+struct RowsSmem {
+    int32_t *cell, *start, *base;  // [28] sorted neighbour cells, first rank, staged prefix
+    int32_t *misc;                 // total, self index, overflow
+    double *x;                     // [nb_cap][3]
+    float4 *f;                     // [nb_cap] fp32 relative coordinates
+    int32_t *rank;                 // [nb_cap]
+    int32_t *buf;                  // [warps][kRowsBuf]
+};
+
+__host__ __device__ inline size_t rows_smem_bytes(int nb_cap, int warps) {
+    return 128 * sizeof(int32_t) + (size_t)nb_cap * (3 * sizeof(double) + sizeof(float4) +
+                                                     sizeof(int32_t)) +
+           (size_t)warps * kRowsBuf * sizeof(int32_t) + 64;
+}
+
+__device__ __forceinline__ RowsSmem rows_carve(char *base, int nb_cap) {
+    RowsSmem s;
+    s.cell = (int32_t *)base;
+    s.start = s.cell + 28;
+    s.base = s.start + 28;
+    s.misc = s.base + 28;
+    s.f = (float4 *)(base + 128 * sizeof(int32_t));
+    s.x = (double *)(s.f + nb_cap);
+    s.rank = (int32_t *)(s.x + 3 * (size_t)nb_cap);
+    s.buf = s.rank + nb_cap;
+    return s;
+}
+
+// false: the neighbourhood of c exceeds nb_cap (nothing written)
+template <bool kCoherent>
+__device__ bool nlist_cell(const rb_grid &g, int c, const double *__restrict__ pr,
+                           const int32_t *__restrict__ cell_start, double rl2, float hi_f,
+                           int32_t capacity, int32_t *__restrict__ rows,
+                           int32_t *__restrict__ row_count, int32_t *__restrict__ max_count,
+                           const RowsSmem &sm, int nb_cap) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int czz = c % g.cells[2], cyy = (c / g.cells[2]) % g.cells[1],
+              cxx = c / (g.cells[2] * g.cells[1]);
+    if (warp == 0) {  // the sorted neighbour cells, their ranks and staged offsets
+        int my_cell = 0x7fffffff, nvalid = 0;
+        for (int ob = 0; ob < g.n_offsets; ob += 32) {
+            const int o = ob + lane;
+            const int cc = o < g.n_offsets ? neighbor_cell(g, cxx, cyy, czz, o) : -1;
+            const unsigned mv = __ballot_sync(0xffffffffu, cc >= 0);
+            const int q = lane - nvalid;
+            const unsigned src = (q >= 0 && q < __popc(mv)) ? __fns(mv, 0, q + 1) : 0u;
+            const int v = __shfl_sync(0xffffffffu, cc, (int)(src & 31u));
+            if (q >= 0 && q < __popc(mv)) my_cell = v;
+            nvalid += __popc(mv);
+        }
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const int other = __shfl_xor_sync(0xffffffffu, my_cell, j);
+                const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
+                my_cell = take_min ? min(my_cell, other) : max(my_cell, other);
+            }
+        }
+        int cs = 0, cnt = 0;
+        if (lane < nvalid) {
+            cs = ldc<kCoherent>(cell_start + my_cell);
+            cnt = ldc<kCoherent>(cell_start + my_cell + 1) - cs;
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        if (lane < nvalid) {
+            sm.cell[lane] = my_cell;
+            sm.start[lane] = cs;
+            sm.base[lane] = incl - cnt;
+            if (my_cell == c) sm.misc[1] = lane;
+        }
+        if (lane == 31) {
+            sm.base[nvalid] = incl;
+            sm.misc[0] = incl;
+            sm.misc[2] = nvalid;
+        }
+    }
+    __syncthreads();
+    const int total = sm.misc[0], self = sm.misc[1], ncells = sm.misc[2];
+    if (total > nb_cap) {
+        __syncthreads();  // every thread has read the header
+        return false;
+    }
+    // stage: positions (exact), fp32 coordinates relative to c's centre
+    // (minimum image), ranks
+    double ctr[3];
+    {
+        const int cc[3] = {cxx, cyy, czz};
+#pragma unroll
+        for (int d = 0; d < 3; d++)
+            ctr[d] = g.origin[d] + ((g.wrap[d] ? 0 : g.wlo[d]) + cc[d] + 0.5) / g.inv_cell[d];
+    }
+    for (int k = threadIdx.x; k < total; k += blockDim.x) {
+        int j = 0;
+        while (j + 1 < ncells && sm.base[j + 1] <= k) j++;
+        const int q = sm.start[j] + (k - sm.base[j]);
+        const double x = ldc<kCoherent>(pr + 3 * (int64_t)q),
+                     y = ldc<kCoherent>(pr + 3 * (int64_t)q + 1),
+                     z = ldc<kCoherent>(pr + 3 * (int64_t)q + 2);
+        sm.x[3 * k] = x;
+        sm.x[3 * k + 1] = y;
+        sm.x[3 * k + 2] = z;
+        double rel[3] = {x - ctr[0], y - ctr[1], z - ctr[2]};
+        if (g.periodic) {
+#pragma unroll
+            for (int d = 0; d < 3; d++) rel[d] = fma(-g.box[d], rint(rel[d] / g.box[d]), rel[d]);
+        }
+        sm.f[k] = make_float4((float)rel[0], (float)rel[1], (float)rel[2], 0.0f);
+        sm.rank[k] = q;
+    }
+    __syncthreads();
+    const Image im = make_image(g);
+    const int b0 = sm.base[self], b1 = sm.base[self + 1], r0 = sm.start[self];
+    int32_t *buf = sm.buf + warp * kRowsBuf;
+    for (int bi = b0 + warp; bi < b1; bi += nwarps) {
+        const int64_t r = r0 + (bi - b0);
+        const float4 fi = sm.f[bi];
+        // pass 1: the fp32 filter, survivors in candidate order
+        int nc = 0;
+        for (int k0 = 0; k0 < total; k0 += 32) {
+            const int k = k0 + lane;
+            bool pass = false;
+            if (k < total && k != bi) {
+                const float4 o = sm.f[k];
+                const float dx = fi.x - o.x, dy = fi.y - o.y, dz = fi.z - o.z;
+                pass = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= hi_f;
+            }
+            const unsigned mk = __ballot_sync(0xffffffffu, pass);
+            const int at = nc + __popc(mk & lanemask_lt());
+            if (pass && at < kRowsBuf) buf[at] = k;
+            nc += __popc(mk);
+        }
+        __syncwarp();
+        if (nc > kRowsBuf) {  // more filter survivors than the buffer: the L2 path
+            nlist_one<kCoherent>(g, r, 0, pr, cell_start, nullptr, rl2, capacity, rows,
+                                 row_count, max_count, c);
+            __syncwarp();
+            continue;
+        }
+        // pass 2: the reference arithmetic decides, survivors appended in order
+        const double xi = sm.x[3 * bi], yi = sm.x[3 * bi + 1], zi = sm.x[3 * bi + 2];
+        int32_t *row = rows + r * (int64_t)capacity;
+        int count = 0;
+        for (int c0 = 0; c0 < nc; c0 += 32) {
+            const int ci = c0 + lane;
+            bool keep = false;
+            int k = 0;
+            if (ci < nc) {
+                k = buf[ci];
+                double dx, dy, dz;
+                exact_disp(im, xi, yi, zi, sm.x[3 * k], sm.x[3 * k + 1], sm.x[3 * k + 2], dx, dy,
+                           dz);
+                keep = exact_r2(dx, dy, dz) <= rl2;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            const int slot = count + __popc(m & lanemask_lt());
+            if (keep && slot < capacity) row[slot] = sm.rank[k];
+            count += __popc(m);
+        }
+        if (lane == 0) {
+            row_count[r] = count < capacity ? count : capacity;
+            if (count > *(volatile int32_t *)max_count) atomicMax(max_count, count);
+        }
+        __syncwarp();
+    }
+    __syncthreads();  // the staged neighbourhood is reused by the next cell
+    return true;
 }
 
 }  // namespace rb

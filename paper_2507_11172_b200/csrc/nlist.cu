@@ -11,6 +11,11 @@
 // no FMA), and survivors (r^2 <= r_list^2, inclusive, self excluded) are
 // appended with a ballot in candidate order, so rows are deterministic and
 // equal to the reference's survivor lists (:437-474) when r_list == rc.
+// By default the rows come from k_nlist_cells (cells.cuh nlist_cell: one CTA
+// per cell, the neighbourhood staged in shared memory, identical rows);
+// RB_ROWS_STAGED=0 keeps the warp-per-particle k_nlist.
+#include <cstdlib>
+
 #include "cells.cuh"
 
 namespace rb {
@@ -31,6 +36,33 @@ __global__ void __launch_bounds__(kNlistWarps * 32)
          r += (int64_t)gridDim.x * kNlistWarps)
         nlist_one(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows, row_count,
                   max_count);
+}
+
+// Cell-staged rows (cells.cuh nlist_cell): one CTA per cell (grid-stride);
+// a neighbourhood over nb_cap takes the per-particle path.
+constexpr int kRowsWarps = 8;
+
+__global__ void __launch_bounds__(kRowsWarps * 32)
+    k_nlist_cells(rb_grid g, int32_t ncell, const double *__restrict__ pr,
+                  const int32_t *__restrict__ cell_start, double rl2, float hi_f,
+                  int32_t capacity, int32_t *__restrict__ rows, int32_t *__restrict__ row_count,
+                  int32_t *__restrict__ max_count, int32_t nb_cap, const int64_t *flag,
+                  const unsigned long long *status, int64_t tag) {
+    pdl_enter();
+    if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
+    extern __shared__ __align__(16) char smem[];
+    const RowsSmem sm = rows_carve(smem, nb_cap);
+    const int warp = threadIdx.x >> 5;
+    for (int c = blockIdx.x; c < ncell; c += gridDim.x) {
+        if (!nlist_cell<false>(g, c, pr, cell_start, rl2, hi_f, capacity, rows, row_count,
+                               max_count, sm, nb_cap)) {
+            const int b = cell_start[c], e = cell_start[c + 1];
+            for (int r = b + warp; r < e; r += kRowsWarps)
+                nlist_one(g, r, 0, pr, cell_start, nullptr, rl2, capacity, rows, row_count,
+                          max_count, c);
+            __syncthreads();
+        }
+    }
 }
 
 // mirror[p][k] = position of p in the row of q = rows[p][k].  One warp per
@@ -64,6 +96,25 @@ extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const 
     if (g->n_offsets <= 0 || g->n_offsets > RB_MAX_OFFSETS) return RB_ERR_GEOMETRY;
     if (n == 0) return RB_OK;
     const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
+    static const bool staged = !(getenv("RB_ROWS_STAGED") && atoi(getenv("RB_ROWS_STAGED")) == 0);
+    const int64_t ncell = (int64_t)g->cells[0] * g->cells[1] * g->cells[2];
+    if (staged && rows_staged_ok(*g)) {
+        const int nb_cap = rows_nb_cap(n, ncell);
+        const size_t bytes = rows_smem_bytes(nb_cap, kRowsWarps);
+        static size_t granted = 0;
+        if (bytes > 48 * 1024 && bytes > granted) {
+            cudaFuncSetAttribute(k_nlist_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)bytes);
+            granted = bytes;
+        }
+        int64_t blocks = ncell < 148 * 16 ? ncell : 148 * 16;
+        launch(k_nlist_cells, dim3((unsigned)blocks), dim3(kRowsWarps * 32), bytes,
+               as_stream(stream), *g, (int32_t)ncell, pos_r, cell_start, rl2,
+               (float)(rl2 * (1.0 + 1e-3)), capacity, rows, row_count, max_count, nb_cap,
+               rebuild_flag, status, tag);
+        note_launches(1);
+        return launch_status();
+    }
     int64_t blocks = (n + kNlistWarps - 1) / kNlistWarps;
     if (rebuild_flag && blocks > 148 * 8) blocks = 148 * 8;  // gated: grid-stride
     launch(k_nlist, dim3((unsigned)blocks), dim3(kNlistWarps * 32), 0, as_stream(stream), *g, n, pos_r, cell_start, cell_of_rank, rl2, capacity, rows, row_count, max_count,

@@ -56,10 +56,12 @@ __global__ void __launch_bounds__(kRbThreads)
               double rl2, int32_t capacity, int32_t *rows, int32_t *row_count,
               int32_t *max_count, int32_t *mirror, int32_t *cell_of, int32_t *count,
               int32_t *cursor, int32_t *tiles, unsigned *bar, const int64_t *flag,
-              const unsigned long long *status, int64_t tag) {
+              const unsigned long long *status, int64_t tag, int32_t nb_cap, float hi_f) {
     pdl_enter();
     if (gate_closed(flag, status, tag)) return;  // the same answer in every block
     __shared__ int warp_sums[32];
+    __shared__ int cell_grab;
+    extern __shared__ __align__(16) char rows_smem[];
     const int64_t ncell = (int64_t)g.cells[0] * g.cells[1] * g.cells[2];
     const int64_t ntiles = (ncell + kRbTile - 1) / kRbTile;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -152,20 +154,39 @@ __global__ void __launch_bounds__(kRbThreads)
         cell_finish_one<true>(c, lane, cell_start, parts, cell_of_rank, rank_of, pos, pr, x_ref);
     if (stop <= 7) return;
     grid_barrier(bcount, bgen);
-    // rows and mirror: warps take chunks of kRbChunk consecutive ranks from a
-    // counter, so the rows in flight stay a compact rank window (their
-    // neighbour cells / rows stay in L2); a grid-stride loop lets the warps
-    // drift apart over the ~300 rows each handles at 2 M particles and
-    // thrashes L2 (measured 2.7x slower than the separate kernels at cfg4)
-    for (;;) {
-        unsigned long long b0 = 0;
-        if (lane == 0) b0 = atomicAdd(&work[0], (unsigned long long)kRbChunk);
-        const int64_t b = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
-        if (b >= n) break;
-        const int64_t e = b + kRbChunk < n ? b + kRbChunk : n;
-        for (int64_t r = b; r < e; r++)
-            nlist_one<true>(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows,
-                            row_count, max_count);
+    // rows: blocks take cells from a counter (cells.cuh nlist_cell: the cell's
+    // neighbourhood staged in shared memory, one row per particle; the cells
+    // in flight stay a compact window, so their neighbourhoods stay in L2);
+    // nb_cap == 0 or a neighbourhood over it: warps per particle (nlist_one)
+    if (nb_cap > 0) {
+        const RowsSmem sm = rows_carve(rows_smem, nb_cap);
+        const int wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+        for (;;) {
+            if (threadIdx.x == 0) cell_grab = (int)atomicAdd(&work[0], 1ull);
+            __syncthreads();
+            const int c = cell_grab;
+            __syncthreads();
+            if (c >= ncell) break;
+            if (!nlist_cell<true>(g, c, pr, cell_start, rl2, hi_f, capacity, rows, row_count,
+                                  max_count, sm, nb_cap)) {
+                const int b = ldc<true>(cell_start + c), e = ldc<true>(cell_start + c + 1);
+                for (int r = b + wib; r < e; r += nwb)
+                    nlist_one<true>(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows,
+                                    row_count, max_count, c);
+                __syncthreads();
+            }
+        }
+    } else {
+        for (;;) {
+            unsigned long long b0 = 0;
+            if (lane == 0) b0 = atomicAdd(&work[0], (unsigned long long)kRbChunk);
+            const int64_t b = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+            if (b >= n) break;
+            const int64_t e = b + kRbChunk < n ? b + kRbChunk : n;
+            for (int64_t r = b; r < e; r++)
+                nlist_one<true>(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows,
+                                row_count, max_count);
+        }
     }
     if (stop <= 8) return;
     grid_barrier(bcount, bgen);
@@ -181,19 +202,25 @@ __global__ void __launch_bounds__(kRbThreads)
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-static int rebuild_grid() {
+// co-resident blocks of k_rebuild at `smem` dynamic bytes on the current
+// device (the cooperative launch's grid)
+static int rebuild_grid(size_t smem) {
     constexpr int kMaxDev = 64;
     static int blocks[kMaxDev] = {0};  // per device
+    static size_t at[kMaxDev] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    int &b = blocks[dev < kMaxDev ? dev : kMaxDev - 1];
-    if (!b) {
+    const int d = dev < kMaxDev ? dev : kMaxDev - 1;
+    if (!blocks[d] || at[d] != smem) {
         int sms = 0, per = 0;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_rebuild, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rebuild, kRbThreads, 0);
-        b = std::max(1, sms) * std::max(1, per);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rebuild, kRbThreads, smem);
+        blocks[d] = std::max(1, sms) * std::max(1, per);
+        at[d] = smem;
     }
-    return b;
+    return blocks[d];
 }
 
 }  // namespace rb
@@ -236,10 +263,14 @@ extern "C" int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_
     const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
     static const int stop = getenv("RB_REBUILD_STOP") ? atoi(getenv("RB_REBUILD_STOP")) : 0;
     if (stop > 0) cudaMemcpyToSymbol(g_rebuild_stop, &stop, sizeof(int));
-    launch_coop(k_rebuild, dim3((unsigned)rebuild_grid()), dim3(kRbThreads), 0, as_stream(stream), *g,
+    static const bool staged = !(getenv("RB_ROWS_STAGED") && atoi(getenv("RB_ROWS_STAGED")) == 0);
+    const int nb_cap = staged && rows_staged_ok(*g) ? rows_nb_cap(n, ncell) : 0;
+    const size_t smem = nb_cap > 0 ? rows_smem_bytes(nb_cap, kRbThreads / 32) : 0;
+    const float hi_f = (float)(rl2 * (1.0 + 1e-3));
+    launch_coop(k_rebuild, dim3((unsigned)rebuild_grid(smem)), dim3(kRbThreads), smem, as_stream(stream), *g,
            n, pos, cell_start, cell_particles, cell_of_rank, pos_r, rank_of, x_ref, rl2, capacity,
            rows, row_count, max_count, mirror, cell_of, count, cursor, tiles, bar, rebuild_flag,
-           status, tag);
+           status, tag, nb_cap, hi_f);
     note_launches(1);
     return launch_status();
 }

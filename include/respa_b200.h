@@ -139,11 +139,29 @@ RB_API int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r,
                unsigned long long *status, int64_t tag, void *stream);
 
 /* Mirror indices of the (rank-sorted) rows: mirror[p*capacity + k] is the
- * position of p in the row of q = rows[p*capacity + k].  The Newton-3
- * triplet pass uses it to deliver partial forces into the target's row. */
+ * position of p in the row of q = rows[p*capacity + k], written for the
+ * entries with q > p only (the others are left as they were; -1: p is not
+ * in row q, a truncated row).  The Newton-3 triplet pass uses it to deliver
+ * partial forces into the target's row. */
 RB_API int rb_nlist_mirror(int64_t n, const int32_t *rows, const int32_t *row_count,
                            int32_t capacity, int32_t *mirror, const int64_t *rebuild_flag,
                            const unsigned long long *status, int64_t tag, void *stream);
+
+/* Rows and their mirror in one call: rb_nlist's rows, then rb_nlist_mirror's
+ * entries (the same values).  On grids the cell-staged row build serves
+ * (>= 4 cells per periodic dimension) the mirror comes from the cell
+ * structure instead of a search: the row build writes per-row directories
+ * (survivors before each neighbour cell) and per-entry partials, and one
+ * pass adds them.  scratch: rb_nlist_mirror_scratch_bytes(n) bytes, any
+ * contents. */
+RB_API size_t rb_nlist_mirror_scratch_bytes(int64_t n);
+RB_API int rb_nlist_rows_mirror(const rb_grid *g, int64_t n, const double *pos_r,
+                                const int32_t *cell_start, const int32_t *cell_of_rank,
+                                double r_list, int32_t capacity, int32_t *rows,
+                                int32_t *row_count, int32_t *max_count, int32_t *mirror,
+                                void *scratch, size_t scratch_bytes,
+                                const int64_t *rebuild_flag, const unsigned long long *status,
+                                int64_t tag, void *stream);
 
 /* ---- ATM triplet pass: replaces _c01_triplet_kernel (:373-535) --------
  * Newton-3 form: every unique triplet (all three pair distances <= rc,

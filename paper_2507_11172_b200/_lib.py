@@ -67,6 +67,8 @@ SIGNATURES = {
     "rb_bin": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _SZ, _P]),
     "rb_nlist": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _D, _I32, _P, _P, _P, _P, _P, _I64, _P]),
     "rb_nlist_mirror": (ctypes.c_int, [_I64, _P, _P, _I32, _P, _P, _P, _I64, _P]),
+    "rb_nlist_mirror_scratch_bytes": (ctypes.c_size_t, [_I64]),
+    "rb_nlist_rows_mirror": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _D, _I32, _P, _P, _P, _P, _P, ctypes.c_size_t, _P, _P, _I64, _P]),
     "rb_lj_pass": (ctypes.c_int, [ctypes.POINTER(RbGrid), _I64, _P, _P, _P, _P, _I32, _D, _D, _D, _P, _P, _P, _P,
                                   _P, _I64, _P]),
     "rb_atm_scratch_bytes": (_SZ, [_I64, _I32]),

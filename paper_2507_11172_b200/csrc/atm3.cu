@@ -67,6 +67,9 @@ __device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image
     const int lane = threadIdx.x & 31;
     int m = 0;
     slot_bad = false;
+    // (warp-uniform: a base a cutoff away from the periodic faces needs no
+    // minimum image, common.cuh image_free)
+    const bool image = !image_free(im, xi, yi, zi, sqrt(rc2));
     int first = 0;
     {
         const int nchunks = (rc_n + 31) >> 5;
@@ -99,7 +102,12 @@ __device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image
             bool keep = false;
             double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;
             if (q > r) {
-                exact_disp(im, xi, yi, zi, px[h], py[h], pz[h], dx, dy, dz);
+                exact_disp<false>(im, xi, yi, zi, px[h], py[h], pz[h], dx, dy, dz);
+                if (image) {
+                    dx = min_image(dx, im.box[0], im.half[0]);
+                    dy = min_image(dy, im.box[1], im.half[1]);
+                    dz = min_image(dz, im.box[2], im.half[2]);
+                }
                 r2 = exact_r2(dx, dy, dz);
                 keep = r2 <= rc2;
                 // beyond the three-body cutoff: contributes nothing.  (A row

@@ -223,33 +223,76 @@ __device__ __forceinline__ void nlist_one(const rb_grid &g, int64_t r, int64_t n
 }
 
 
-// mirror entries of row p (one warp): for each entry q > p a lane
-// binary-searches p in the rank-sorted row q and writes BOTH mirror[p][k]
-// and, by symmetry, mirror[q][that position] = k -- every pair once.
+// mirror entries of row p (one warp): for each entry q > p, the position of
+// p in the rank-sorted row q.  Only these (upper) entries are written: the
+// Newton-3 pass reads mirror[r][k] for rows[r][k] > r alone.  An 8-lane
+// group serves one entry: it reads row q 32 entries at a time (one 128-byte
+// line, four per lane) and counts the entries below p -- p < q sits in the
+// lower half of row q, so one chunk, rarely two, instead of a ~7-load
+// dependent binary search per lane; four entries per warp step.
 template <bool kCoherent = false>
 __device__ __forceinline__ void mirror_one(int64_t p, int lane, const int32_t *__restrict__ rows,
                                            const int32_t *__restrict__ row_count,
                                            int32_t capacity, int32_t *__restrict__ mirror) {
-        const int m = ldc<kCoherent>(row_count + p);
-        const int32_t *rp = rows + p * (int64_t)capacity;
-        for (int k = lane; k < m; k += 32) {
-            const int q = kCoherent ? __ldcg(rp + k) : __ldg(rp + k);
-            if (q <= p) continue;  // written by the warp of row q
-            const int32_t *rq = rows + (int64_t)q * capacity;
-            int lo = 0, hi = ldc<kCoherent>(row_count + q) - 1, pos = -1;
-            while (lo <= hi) {
-                const int mid = (lo + hi) >> 1;
-                const int v = kCoherent ? __ldcg(rq + mid) : __ldg(rq + mid);
-                if (v == (int)p) {
-                    pos = mid;
-                    break;
-                }
-                if (v < (int)p) lo = mid + 1;
-                else hi = mid - 1;
-            }
-            mirror[p * (int64_t)capacity + k] = pos;
-            if (pos >= 0) mirror[(int64_t)q * capacity + pos] = k;
+    const int m = ldc<kCoherent>(row_count + p);
+    const int32_t *rp = rows + p * (int64_t)capacity;
+    // first entry above p (rows ascend): the suffix this warp serves
+    int first = m;
+    for (int k0 = 0; k0 < m; k0 += 32) {
+        const int k = k0 + lane;
+        const unsigned b = __ballot_sync(0xffffffffu, k < m && ldc<kCoherent>(rp + k) > (int)p);
+        if (b) {
+            first = k0 + __ffs(b) - 1;
+            break;
         }
+    }
+    const int grp = lane >> 3, sub = lane & 7;
+    const unsigned gmask = 0xffu << (8 * grp);
+    const bool vec = (capacity & 3) == 0;  // 16-byte aligned rows
+    for (int k0 = first; k0 < m; k0 += 4) {
+        const int k = k0 + grp;
+        const bool valid = k < m;
+        int q = 0, mq = 0;
+        if (valid) {
+            q = ldc<kCoherent>(rp + k);
+            mq = ldc<kCoherent>(row_count + q);
+        }
+        const int32_t *rq = rows + (int64_t)q * capacity;
+        int pos = -1;
+        bool done = !valid;
+        for (int base = 0; __any_sync(0xffffffffu, !done); base += 32) {
+            int below = 0;
+            bool hit = false, stop = false;
+            if (!done) {
+                const int at = base + 4 * sub;
+                int v[4];
+                if (vec && at + 4 <= capacity) {
+                    const int4 w = ldc<kCoherent>(reinterpret_cast<const int4 *>(rq + at));
+                    v[0] = w.x, v[1] = w.y, v[2] = w.z, v[3] = w.w;
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 4; t++) v[t] = at + t < capacity ? ldc<kCoherent>(rq + at + t) : 0;
+                }
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    const int x = at + t < mq ? v[t] : 0x7fffffff;  // past the row: above p
+                    below += x < (int)p;
+                    hit = hit || x == (int)p;
+                    stop = stop || x >= (int)p;
+                }
+            }
+            // group totals (xor tree inside the 8 lanes)
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+            const unsigned hb = __ballot_sync(0xffffffffu, hit) & gmask;
+            const unsigned sb = __ballot_sync(0xffffffffu, stop) & gmask;
+            if (!done && (sb || base + 32 >= mq)) {
+                pos = hb ? base + below : -1;
+                done = true;
+            }
+        }
+        if (valid && sub == 0) mirror[p * (int64_t)capacity + k] = pos;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -275,6 +318,7 @@ constexpr int kRowsBuf = 256;  // filter survivors per particle (per warp)
 // neighbour is at most 2 cells from the centre's image).  Smaller grids take
 // nlist_one.
 inline bool rows_staged_ok(const rb_grid &g) {
+    if (g.n_offsets > 32) return false;  // one neighbour cell per lane
     if (!g.periodic) return true;
     for (int d = 0; d < 3; d++)
         if ((g.wrap[d] ? g.cells[d] : g.gcells[d]) < 4) return false;
@@ -293,17 +337,29 @@ inline int rows_nb_cap(int64_t n, int64_t ncell) {
 
 struct RowsSmem {
     int32_t *cell, *start, *base;  // [28] sorted neighbour cells, first rank, staged prefix
-    int32_t *misc;                 // total, self index, overflow
+    int32_t *misc;                 // total, self index, cell count, mirror-search flag
+    int32_t *slotc;                // [32] index of c among cell j's sorted neighbour cells
+    int32_t *jc;                   // [3][32] coordinates of the sorted neighbour cells
+    double *ctr;                   // [3] centre of c
     double *x;                     // [nb_cap][3]
     float4 *f;                     // [nb_cap] fp32 relative coordinates
     int32_t *rank;                 // [nb_cap]
+    uint32_t *bits;                // [nb_cap] which of c's particles have k in their row
+    int32_t *segn;                 // [warps][32] survivors per neighbour cell (directory)
     int32_t *buf;                  // [warps][kRowsBuf]
+    uint8_t *cj;                   // [nb_cap] neighbour-cell index of staged particle k
 };
 
+// RB_ROWS_SMEM_X=0: the exact pass reads the candidates' fp64 positions from
+// L1/L2 instead of staging them (24 bytes less shared memory per candidate)
+#ifndef RB_ROWS_SMEM_X
+#define RB_ROWS_SMEM_X 0
+#endif
 __host__ __device__ inline size_t rows_smem_bytes(int nb_cap, int warps) {
-    return 128 * sizeof(int32_t) + (size_t)nb_cap * (3 * sizeof(double) + sizeof(float4) +
-                                                     sizeof(int32_t)) +
-           (size_t)warps * kRowsBuf * sizeof(int32_t) + 64;
+    return 288 * sizeof(int32_t) +
+           (size_t)nb_cap * (RB_ROWS_SMEM_X * 3 * sizeof(double) + sizeof(float4) +
+                             2 * sizeof(int32_t) + 1) +
+           (size_t)warps * (kRowsBuf + 32) * sizeof(int32_t) + 64;
 }
 
 __device__ __forceinline__ RowsSmem rows_carve(char *base, int nb_cap) {
@@ -312,20 +368,46 @@ __device__ __forceinline__ RowsSmem rows_carve(char *base, int nb_cap) {
     s.start = s.cell + 28;
     s.base = s.start + 28;
     s.misc = s.base + 28;
-    s.f = (float4 *)(base + 128 * sizeof(int32_t));
+    s.slotc = (int32_t *)base + 128;
+    s.jc = (int32_t *)base + 160;
+    s.ctr = (double *)((int32_t *)base + 256);
+    s.f = (float4 *)(base + 288 * sizeof(int32_t));
     s.x = (double *)(s.f + nb_cap);
-    s.rank = (int32_t *)(s.x + 3 * (size_t)nb_cap);
-    s.buf = s.rank + nb_cap;
+    s.rank = (int32_t *)(s.x + RB_ROWS_SMEM_X * 3 * (size_t)nb_cap);
+    s.bits = (uint32_t *)(s.rank + nb_cap);
+    s.segn = (int32_t *)(s.bits + nb_cap);
+    s.buf = s.segn + (blockDim.x >> 5) * 32;
+    s.cj = (uint8_t *)(s.buf + (blockDim.x >> 5) * kRowsBuf);
     return s;
 }
 
-// false: the neighbourhood of c exceeds nb_cap (nothing written)
+// Mirror indices from the cell structure (the staged path's by-product; the
+// fused rebuild and rb_nlist_rows_mirror).  A row lists its neighbour cells'
+// members in flat-cell-id order, ascending rank inside each cell, so the
+// position of p (in cell c) in the row of q (in cell c') is
+//     dir[q][slot of c among c' 's sorted neighbour cells]   (survivors of
+//         row q in the cells before c, written by c' 's CTA)
+//   + #{x in c, x < p, q in row x}                            (c's CTA: a
+//         bit per (staged q, particle of c), the predicate being symmetric)
+// The CTA of c writes the second term and the slot into mirror[p][k] as
+// `within | slot << 24` (kMirrorSearch where it cannot: a cell over 32
+// particles or with a per-particle fallback); mirror_resolve adds the first.
+// dir rows of particles whose rows were not built by the staged path are
+// all kDirNone.
+constexpr int32_t kMirrorSearch = -2;
+constexpr uint16_t kDirNone = 0xffff;
+constexpr int kDirStride = 32;  // uint16 per particle
+
+// false: the neighbourhood of c exceeds nb_cap (nothing written).  mirror
+// and dir non-null: the mirror partials and directory rows of c's particles
+// are written too (see kMirrorSearch above).
 template <bool kCoherent>
 __device__ bool nlist_cell(const rb_grid &g, int c, const double *__restrict__ pr,
                            const int32_t *__restrict__ cell_start, double rl2, float hi_f,
                            int32_t capacity, int32_t *__restrict__ rows,
                            int32_t *__restrict__ row_count, int32_t *__restrict__ max_count,
-                           const RowsSmem &sm, int nb_cap) {
+                           const RowsSmem &sm, int nb_cap, int32_t *__restrict__ mirror = nullptr,
+                           uint16_t *__restrict__ dir = nullptr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int czz = c % g.cells[2], cyy = (c / g.cells[2]) % g.cells[1],
               cxx = c / (g.cells[2] * g.cells[1]);
@@ -366,11 +448,20 @@ __device__ bool nlist_cell(const rb_grid &g, int c, const double *__restrict__ p
             sm.start[lane] = cs;
             sm.base[lane] = incl - cnt;
             if (my_cell == c) sm.misc[1] = lane;
+            sm.jc[lane] = my_cell / (g.cells[2] * g.cells[1]);
+            sm.jc[32 + lane] = (my_cell / g.cells[2]) % g.cells[1];
+            sm.jc[64 + lane] = my_cell % g.cells[2];
+        }
+        if (lane < 3) {
+            const int cc = lane == 0 ? cxx : (lane == 1 ? cyy : czz);
+            sm.ctr[lane] = g.origin[lane] +
+                           ((g.wrap[lane] ? 0 : g.wlo[lane]) + cc + 0.5) / g.inv_cell[lane];
         }
         if (lane == 31) {
             sm.base[nvalid] = incl;
             sm.misc[0] = incl;
             sm.misc[2] = nvalid;
+            sm.misc[3] = 0;
         }
     }
     __syncthreads();
@@ -379,33 +470,55 @@ __device__ bool nlist_cell(const rb_grid &g, int c, const double *__restrict__ p
         __syncthreads();  // every thread has read the header
         return false;
     }
+    const bool with_mirror = mirror != nullptr && dir != nullptr;
+    if (with_mirror && threadIdx.x == 0 && sm.base[self + 1] - sm.base[self] > 32)
+        sm.misc[3] = 1;  // more particles than bits: this cell's partials search
     // stage: positions (exact), fp32 coordinates relative to c's centre
     // (minimum image), ranks
-    double ctr[3];
-    {
-        const int cc[3] = {cxx, cyy, czz};
-#pragma unroll
-        for (int d = 0; d < 3; d++)
-            ctr[d] = g.origin[d] + ((g.wrap[d] ? 0 : g.wlo[d]) + cc[d] + 0.5) / g.inv_cell[d];
+    const double ctr[3] = {sm.ctr[0], sm.ctr[1], sm.ctr[2]};
+    if (with_mirror) {
+        // slotc[j]: the index of c among the sorted neighbour cells of cell j
+        // (the neighbourhood relation is symmetric); a warp per cell j, a
+        // lane per offset (rows grids have <= 32 offsets)
+        const int o = lane < g.n_offsets ? lane : 0;
+        const int ox = g.offsets[o][0], oy = g.offsets[o][1], oz = g.offsets[o][2];
+        for (int j = warp; j < ncells; j += nwarps) {
+            const int cc = lane < g.n_offsets
+                               ? cell_at(g, sm.jc[j] + ox, sm.jc[32 + j] + oy, sm.jc[64 + j] + oz)
+                               : -1;
+            const int below = __popc(__ballot_sync(0xffffffffu, cc >= 0 && cc < c));
+            if (lane == 0) sm.slotc[j] = below;
+        }
     }
     for (int k = threadIdx.x; k < total; k += blockDim.x) {
-        int j = 0;
-        while (j + 1 < ncells && sm.base[j + 1] <= k) j++;
-        const int q = sm.start[j] + (k - sm.base[j]);
-        const double x = ldc<kCoherent>(pr + 3 * (int64_t)q),
-                     y = ldc<kCoherent>(pr + 3 * (int64_t)q + 1),
-                     z = ldc<kCoherent>(pr + 3 * (int64_t)q + 2);
-        sm.x[3 * k] = x;
-        sm.x[3 * k + 1] = y;
-        sm.x[3 * k + 2] = z;
-        double rel[3] = {x - ctr[0], y - ctr[1], z - ctr[2]};
-        if (g.periodic) {
+        {
+            // neighbour cell of staged index k: binary search of the prefix
+            int j = 0;
 #pragma unroll
-            for (int d = 0; d < 3; d++) rel[d] = fma(-g.box[d], rint(rel[d] / g.box[d]), rel[d]);
+            for (int step = 16; step > 0; step >>= 1)
+                if (j + step < ncells && sm.base[j + step] <= k) j += step;
+            const int q = sm.start[j] + (k - sm.base[j]);
+            const double x = ldc<kCoherent>(pr + 3 * (int64_t)q),
+                         y = ldc<kCoherent>(pr + 3 * (int64_t)q + 1),
+                         z = ldc<kCoherent>(pr + 3 * (int64_t)q + 2);
+            if (RB_ROWS_SMEM_X) {
+                sm.x[3 * k] = x;
+                sm.x[3 * k + 1] = y;
+                sm.x[3 * k + 2] = z;
+            }
+            double rel[3] = {x - ctr[0], y - ctr[1], z - ctr[2]};
+            if (g.periodic) {
+#pragma unroll
+                for (int d = 0; d < 3; d++)
+                    rel[d] = fma(-g.box[d], rint(rel[d] * (1.0 / g.box[d])), rel[d]);
+            }
+            sm.f[k] = make_float4((float)rel[0], (float)rel[1], (float)rel[2], 0.0f);
+            sm.rank[k] = q;
+            sm.cj[k] = (uint8_t)j;
+            sm.bits[k] = 0u;
         }
-        sm.f[k] = make_float4((float)rel[0], (float)rel[1], (float)rel[2], 0.0f);
-        sm.rank[k] = q;
     }
+    sm.segn[threadIdx.x] = 0;  // (blockDim.x == warps * 32)
     __syncthreads();
     const Image im = make_image(g);
     const int b0 = sm.base[self], b1 = sm.base[self + 1], r0 = sm.start[self];
@@ -432,11 +545,16 @@ __device__ bool nlist_cell(const rb_grid &g, int c, const double *__restrict__ p
         if (nc > kRowsBuf) {  // more filter survivors than the buffer: the L2 path
             nlist_one<kCoherent>(g, r, 0, pr, cell_start, nullptr, rl2, capacity, rows,
                                  row_count, max_count, c);
+            if (with_mirror) {  // no bits for this particle: the cell's partials search
+                dir[r * kDirStride + lane] = kDirNone;
+                if (lane == 0) sm.misc[3] = 1;
+            }
             __syncwarp();
             continue;
         }
         // pass 2: the reference arithmetic decides, survivors appended in order
-        const double xi = sm.x[3 * bi], yi = sm.x[3 * bi + 1], zi = sm.x[3 * bi + 2];
+        const double xi = ldc<kCoherent>(pr + 3 * r), yi = ldc<kCoherent>(pr + 3 * r + 1),
+                     zi = ldc<kCoherent>(pr + 3 * r + 2);
         int32_t *row = rows + r * (int64_t)capacity;
         int count = 0;
         for (int c0 = 0; c0 < nc; c0 += 32) {
@@ -446,23 +564,109 @@ __device__ bool nlist_cell(const rb_grid &g, int c, const double *__restrict__ p
             if (ci < nc) {
                 k = buf[ci];
                 double dx, dy, dz;
-                exact_disp(im, xi, yi, zi, sm.x[3 * k], sm.x[3 * k + 1], sm.x[3 * k + 2], dx, dy,
-                           dz);
+                double px, py, pz;
+                if (RB_ROWS_SMEM_X) {
+                    px = sm.x[3 * k], py = sm.x[3 * k + 1], pz = sm.x[3 * k + 2];
+                } else {
+                    const int64_t q = sm.rank[k];
+                    px = ldc<kCoherent>(pr + 3 * q), py = ldc<kCoherent>(pr + 3 * q + 1),
+                    pz = ldc<kCoherent>(pr + 3 * q + 2);
+                }
+                exact_disp(im, xi, yi, zi, px, py, pz, dx, dy, dz);
                 keep = exact_r2(dx, dy, dz) <= rl2;
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             const int slot = count + __popc(m & lanemask_lt());
             if (keep && slot < capacity) row[slot] = sm.rank[k];
+            if (with_mirror && keep) {
+                if (bi - b0 < 32) atomicOr(&sm.bits[k], 1u << (bi - b0));
+                atomicAdd(&sm.segn[warp * 32 + sm.cj[k]], 1);
+                // (the staged index, for the partial below)
+                if (slot < capacity) mirror[r * (int64_t)capacity + slot] = k;
+            }
             count += __popc(m);
         }
         if (lane == 0) {
             row_count[r] = count < capacity ? count : capacity;
             if (count > *(volatile int32_t *)max_count) atomicMax(max_count, count);
         }
+        if (with_mirror) {  // directory row: survivors before each neighbour cell
+            __syncwarp();
+            const int v = sm.segn[warp * 32 + lane];
+            int incl = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            dir[r * kDirStride + lane] = (uint16_t)(incl - v);
+            sm.segn[warp * 32 + lane] = 0;
+        }
         __syncwarp();
+    }
+    if (with_mirror) {
+        __syncthreads();  // every particle's bits are in
+        const bool search = sm.misc[3] != 0;
+        for (int bi = b0 + warp; bi < b1; bi += nwarps) {
+            const int64_t r = r0 + (bi - b0);
+            if (dir[r * kDirStride] == kDirNone) continue;  // its rows came from nlist_one
+            const int m = row_count[r];
+            const int32_t *row = rows + r * (int64_t)capacity;
+            int32_t *mrow = mirror + r * (int64_t)capacity;
+            const uint32_t below = (1u << (bi - b0 < 32 ? bi - b0 : 31)) - 1u;
+            for (int k = lane; k < m; k += 32) {
+                if (row[k] <= (int)r) continue;  // only the upper entries are defined
+                int32_t v = kMirrorSearch;
+                if (!search) {
+                    const int kk = mrow[k];
+                    v = __popc(sm.bits[kk] & below) | (sm.slotc[sm.cj[kk]] << 24);
+                }
+                mrow[k] = v;
+            }
+        }
     }
     __syncthreads();  // the staged neighbourhood is reused by the next cell
     return true;
+}
+
+// Mirror entries of row p from the partials (one warp): pos = dir[q][slot] +
+// within, -1 past the capacity (p fell off a truncated row q); the binary
+// search where a partial or q's directory row is missing.
+template <bool kCoherent = false>
+__device__ __forceinline__ void mirror_resolve(int64_t p, int lane, const int32_t *__restrict__ rows,
+                                               const int32_t *__restrict__ row_count,
+                                               int32_t capacity, int32_t *__restrict__ mirror,
+                                               const uint16_t *__restrict__ dir) {
+    const int m = ldc<kCoherent>(row_count + p);
+    const int32_t *rp = rows + p * (int64_t)capacity;
+    int32_t *mp = mirror + p * (int64_t)capacity;
+    const bool p_none = ldc<kCoherent>(dir + p * kDirStride) == kDirNone;
+    for (int k = lane; k < m; k += 32) {
+        const int q = ldc<kCoherent>(rp + k);
+        if (q <= (int)p) continue;
+        const int32_t v = p_none ? kMirrorSearch : ldc<kCoherent>(mp + k);
+        int pos = -1;
+        uint16_t d = kDirNone;
+        if (v != kMirrorSearch) d = ldc<kCoherent>(dir + (int64_t)q * kDirStride + (v >> 24));
+        if (d != kDirNone) {
+            pos = (int)d + (v & 0xffffff);
+            if (pos >= capacity) pos = -1;
+        } else {  // binary search of p in the rank-sorted row q
+            const int32_t *rq = rows + (int64_t)q * capacity;
+            int lo = 0, hi = ldc<kCoherent>(row_count + q) - 1;
+            while (lo <= hi) {
+                const int mid = (lo + hi) >> 1;
+                const int x = ldc<kCoherent>(rq + mid);
+                if (x == (int)p) {
+                    pos = mid;
+                    break;
+                }
+                if (x < (int)p) lo = mid + 1;
+                else hi = mid - 1;
+            }
+        }
+        mp[k] = pos;
+    }
 }
 
 }  // namespace rb

@@ -124,11 +124,13 @@ __device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
 
-// single-shift minimum image, respamd/containers.py:341-353 (d = a - b first)
+// single-shift minimum image, respamd/containers.py:341-353 (d = a - b first),
+// branch-free: d - s with s in {box, -box, +0} (d + box == d - (-box) and
+// d - (+0) == d exactly in IEEE arithmetic, -0 included)
 __device__ __forceinline__ double min_image(double d, double box, double half) {
-    if (d > half) return xsub(d, box);
-    if (d < -half) return xadd(d, box);
-    return d;
+    double s = d > half ? box : 0.0;
+    s = d < -half ? -box : s;
+    return xsub(d, s);
 }
 
 // r^2 = dx*dx + dy*dy + dz*dz rounded as numba evaluates it (left to right)
@@ -163,17 +165,34 @@ __host__ __device__ inline Image make_image(const rb_grid &g) {
 }
 
 // exact displacement a - b with the reference's minimum image
+// (kImage = false: a particle for which image_free() holds -- no shift)
+template <bool kImage = true>
 __device__ __forceinline__ void exact_disp(const Image &im, double ax, double ay, double az,
                                            double bx, double by, double bz, double &dx,
                                            double &dy, double &dz) {
     dx = xsub(ax, bx);
     dy = xsub(ay, by);
     dz = xsub(az, bz);
-    if (im.periodic) {
+    if (kImage && im.periodic) {
         dx = min_image(dx, im.box[0], im.half[0]);
         dy = min_image(dy, im.box[1], im.half[1]);
         dz = min_image(dz, im.box[2], im.half[2]);
     }
+}
+
+// True when the minimum image cannot change any outcome for partners of a
+// particle at (x, y, z) (coordinates in [0, box), as the drift wraps them)
+// under a cutoff `reach`: with x in [M, box - M], M > reach, a shifted
+// difference d -/+ box has |.| > M for every partner in [0, box), so each
+// partner inside the cutoff needs no shift (identical dx), and one outside
+// stays outside unshifted (the shift only ever shortens |d|, exactly:
+// Sterbenz).  M carries an absolute margin far above the rounding of d.
+__device__ __forceinline__ bool image_free(const Image &im, double x, double y, double z,
+                                           double reach) {
+    if (!im.periodic) return true;
+    const double m = reach + 1e-9 * (1.0 + im.box[0] + im.box[1] + im.box[2]);
+    return x >= m && x <= im.box[0] - m && y >= m && y <= im.box[1] - m && z >= m &&
+           z <= im.box[2] - m;
 }
 
 // ---------------------------------------------------------------------------
@@ -276,6 +295,21 @@ __device__ __forceinline__ T block_tree_sum(T v, T *sh) {
 
 // neighbour cell of base cell (cx,cy,cz) at offset o; -1 when outside an
 // open grid (respamd/containers.py:319-333)
+// flat id of the cell at coordinates x (offset-shifted: in [0, 2 cells) on a
+// wrapped dimension), -1 outside a non-wrapped one
+__device__ __forceinline__ int cell_at(const rb_grid &g, int x, int y, int z) {
+    int c[3] = {x, y, z};
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+        if (g.wrap[d]) {
+            if (c[d] >= g.cells[d]) c[d] -= g.cells[d];
+        } else if (c[d] < 0 || c[d] >= g.cells[d]) {
+            return -1;
+        }
+    }
+    return (c[0] * g.cells[1] + c[1]) * g.cells[2] + c[2];
+}
+
 __device__ __forceinline__ int neighbor_cell(const rb_grid &g, int cx, int cy, int cz, int o) {
     int c[3];
 #pragma unroll

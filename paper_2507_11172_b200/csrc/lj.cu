@@ -11,6 +11,8 @@
 // arithmetic; the LJ kernel itself (potentials.py:55-67) is restated with one
 // reciprocal (hardware seed + a third-order correction) instead of two
 // divides (agreement ~1e-16 relative).
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace rb {
@@ -23,6 +25,11 @@ namespace rb {
 #endif
 constexpr int kLjGroup = RB_LJ_GROUP;   // lanes per particle
 constexpr int kLjRowRegs = RB_LJ_ROW_REGS;  // row indices a lane holds at once
+#ifndef RB_LJ_BATCH
+#define RB_LJ_BATCH 2
+#endif
+constexpr int kLjBatch = RB_LJ_BATCH;  // neighbour positions in flight per lane
+static_assert(kLjRowRegs % kLjBatch == 0, "row registers: whole batches");
 constexpr int kLjThreads = 256;
 // 1/x: the hardware fp64 seed (MUFU.RCP64H) and one third-order correction
 // y (1 + e + e^2), e = 1 - x y (x is a squared distance, a normal double;
@@ -43,7 +50,7 @@ template <bool kScalars>
 __global__ void __launch_bounds__(kLjThreads, RB_LJ_MIN_BLOCKS)
     k_lj(rb_grid g, int64_t n, const double *__restrict__ pr, const int32_t *__restrict__ parts,
          const int32_t *__restrict__ rows, const int32_t *__restrict__ row_count,
-         int32_t capacity, double rc2, double eps24, double eps4, double sigma2,
+         int32_t capacity, double rc, double rc2, double eps24, double eps4, double sigma2,
          double *__restrict__ forces, double *__restrict__ energy_rank,
          double *__restrict__ virial_rank, const uint8_t *__restrict__ owned,
          unsigned long long *status, int64_t tag) {
@@ -94,9 +101,9 @@ __global__ void __launch_bounds__(kLjThreads, RB_LJ_MIN_BLOCKS)
         // branch-free visit: the kernel runs for every entry and the scale
         // is selected (zero beyond the cutoff, for an empty slot and for a
         // guarded pair, potentials.py:35-36), so the lanes never diverge
-        auto visit = [&](bool valid, double px, double py, double pz) {
+        auto visit = [&](auto image, bool valid, double px, double py, double pz) {
             double dx, dy, dz;
-            exact_disp(im, xi, yi, zi, px, py, pz, dx, dy, dz);
+            exact_disp<decltype(image)::value>(im, xi, yi, zi, px, py, pz, dx, dy, dz);
             const double r2 = exact_r2(dx, dy, dz);
             const bool in = valid && r2 <= rc2;
             const bool guard = in && r2 < RB_MIN_DISTANCE_SQ;
@@ -115,21 +122,34 @@ __global__ void __launch_bounds__(kLjThreads, RB_LJ_MIN_BLOCKS)
                 w = fma(scale, r2, w);
             }
         };
+        auto walk = [&](auto image) {
 #pragma unroll
-        for (int u = 0; u < kLjRowRegs; u += 2) {
-            const bool va = jr[u] >= 0, vb = jr[u + 1] >= 0;
-            if (!__any_sync(0xffffffffu, va)) break;  // the warp's rows are done
-            const int qa = va ? jr[u] : self, qb = vb ? jr[u + 1] : self;
-            RB_CHECK(qa >= 0 && qa < n && qb >= 0 && qb < n);
-            const double ax = pr[3 * qa], ay = pr[3 * qa + 1], az = pr[3 * qa + 2];
-            const double bx = pr[3 * qb], by = pr[3 * qb + 1], bz = pr[3 * qb + 2];
-            visit(va, ax, ay, az);
-            visit(vb, bx, by, bz);
-        }
-        for (int k = sub + kLjRowRegs * kLjGroup; k < m; k += kLjGroup) {  // long rows
-            const int q = __ldg(row + k);
-            visit(true, pr[3 * q], pr[3 * q + 1], pr[3 * q + 2]);
-        }
+            for (int u = 0; u < kLjRowRegs; u += kLjBatch) {
+                if (!__any_sync(0xffffffffu, jr[u] >= 0)) break;  // the warp's rows are done
+                double px[kLjBatch], py[kLjBatch], pz[kLjBatch];
+#pragma unroll
+                for (int t = 0; t < kLjBatch; t++) {
+                    const int q = jr[u + t] >= 0 ? jr[u + t] : self;
+                    RB_CHECK(q >= 0 && q < n);
+                    px[t] = pr[3 * q];
+                    py[t] = pr[3 * q + 1];
+                    pz[t] = pr[3 * q + 2];
+                }
+#pragma unroll
+                for (int t = 0; t < kLjBatch; t++) visit(image, jr[u + t] >= 0, px[t], py[t], pz[t]);
+            }
+            for (int k = sub + kLjRowRegs * kLjGroup; k < m; k += kLjGroup) {  // long rows
+                const int q = __ldg(row + k);
+                visit(image, true, pr[3 * q], pr[3 * q + 1], pr[3 * q + 2]);
+            }
+        };
+        // a warp whose particles all sit a cutoff away from the periodic
+        // faces walks its rows without the minimum image (common.cuh
+        // image_free: bit-identical outcomes; ~90% of warps at cfg4)
+        if (__all_sync(0xffffffffu, !active || image_free(im, xi, yi, zi, rc)))
+            walk(std::false_type{});
+        else
+            walk(std::true_type{});
     }
     fx = group_sum<kLjGroup>(fx);
     fy = group_sum<kLjGroup>(fy);
@@ -170,7 +190,7 @@ extern "C" int rb_lj_pass(const rb_grid *g, int64_t n, const double *pos_r, cons
     // energy_rank == virial_rank == NULL: forces only (steps that are not
     // sample points, whose scalars nothing reads)
     auto kern = energy_rank && virial_rank ? k_lj<true> : k_lj<false>;
-    launch(kern, dim3(blocks), dim3(kLjThreads), 0, as_stream(stream), *g, n, pos_r, cell_particles, rows, row_count, capacity, rc * rc, 24.0 * epsilon,
+    launch(kern, dim3(blocks), dim3(kLjThreads), 0, as_stream(stream), *g, n, pos_r, cell_particles, rows, row_count, capacity, rc, rc * rc, 24.0 * epsilon,
         4.0 * epsilon, sigma * sigma, forces, energy_rank, virial_rank, owned, status, tag);
     note_launches(1);
     return launch_status();

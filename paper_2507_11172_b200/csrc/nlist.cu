@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(kRowsWarps * 32)
     k_nlist_cells(rb_grid g, int32_t ncell, const double *__restrict__ pr,
                   const int32_t *__restrict__ cell_start, double rl2, float hi_f,
                   int32_t capacity, int32_t *__restrict__ rows, int32_t *__restrict__ row_count,
-                  int32_t *__restrict__ max_count, int32_t nb_cap, const int64_t *flag,
+                  int32_t *__restrict__ max_count, int32_t nb_cap, int32_t *__restrict__ mirror,
+                  uint16_t *__restrict__ dir, const int64_t *flag,
                   const unsigned long long *status, int64_t tag) {
     pdl_enter();
     if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
@@ -55,11 +56,13 @@ __global__ void __launch_bounds__(kRowsWarps * 32)
     const int warp = threadIdx.x >> 5;
     for (int c = blockIdx.x; c < ncell; c += gridDim.x) {
         if (!nlist_cell<false>(g, c, pr, cell_start, rl2, hi_f, capacity, rows, row_count,
-                               max_count, sm, nb_cap)) {
+                               max_count, sm, nb_cap, mirror, dir)) {
             const int b = cell_start[c], e = cell_start[c + 1];
-            for (int r = b + warp; r < e; r += kRowsWarps)
+            for (int r = b + warp; r < e; r += kRowsWarps) {
                 nlist_one(g, r, 0, pr, cell_start, nullptr, rl2, capacity, rows, row_count,
                           max_count, c);
+                if (dir) dir[(int64_t)r * kDirStride + (threadIdx.x & 31)] = kDirNone;
+            }
             __syncthreads();
         }
     }
@@ -83,15 +86,33 @@ __global__ void __launch_bounds__(kMirrorWarps * 32)
         mirror_one(p, lane, rows, row_count, capacity, mirror);
 }
 
+// mirror from the staged rows' partials and directory (cells.cuh)
+__global__ void __launch_bounds__(kMirrorWarps * 32)
+    k_mirror_resolve(int64_t n, const int32_t *__restrict__ rows,
+                     const int32_t *__restrict__ row_count, int32_t capacity,
+                     int32_t *__restrict__ mirror, const uint16_t *__restrict__ dir,
+                     const int64_t *flag, const unsigned long long *status, int64_t tag) {
+    pdl_enter();
+    if (flag && *(volatile const int64_t *)flag != resolve_tag(tag, status)) return;
+    const int lane = threadIdx.x & 31;
+    for (int64_t p = (int64_t)blockIdx.x * kMirrorWarps + (threadIdx.x >> 5); p < n;
+         p += (int64_t)gridDim.x * kMirrorWarps)
+        mirror_resolve(p, lane, rows, row_count, capacity, mirror, dir);
+}
+
 }  // namespace rb
 
 using namespace rb;
 
-extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_start, const int32_t *cell_of_rank,
-                        double r_list, int32_t capacity, int32_t *rows, int32_t *row_count,
-                        int32_t *max_count, const int64_t *rebuild_flag,
-                        const unsigned long long *status, int64_t tag, void *stream) {
-    NvtxRange nvtx_range("rows (rb_nlist)");
+// rows (and, with mirror + dir, the staged path's mirror partials and
+// directory); *staged_out: whether the staged path ran
+static int nlist_launch(const rb_grid *g, int64_t n, const double *pos_r,
+                        const int32_t *cell_start, const int32_t *cell_of_rank, double r_list,
+                        int32_t capacity, int32_t *rows, int32_t *row_count, int32_t *max_count,
+                        int32_t *mirror, uint16_t *dir, const int64_t *rebuild_flag,
+                        const unsigned long long *status, int64_t tag, void *stream,
+                        bool *staged_out) {
+    *staged_out = false;
     if (!g || n < 0 || capacity <= 0 || !max_count) return RB_ERR_ARGUMENT;
     if (g->n_offsets <= 0 || g->n_offsets > RB_MAX_OFFSETS) return RB_ERR_GEOMETRY;
     if (n == 0) return RB_OK;
@@ -111,14 +132,57 @@ extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const 
         launch(k_nlist_cells, dim3((unsigned)blocks), dim3(kRowsWarps * 32), bytes,
                as_stream(stream), *g, (int32_t)ncell, pos_r, cell_start, rl2,
                (float)(rl2 * (1.0 + 1e-3)), capacity, rows, row_count, max_count, nb_cap,
-               rebuild_flag, status, tag);
+               mirror, dir, rebuild_flag, status, tag);
         note_launches(1);
+        *staged_out = true;
         return launch_status();
     }
     int64_t blocks = (n + kNlistWarps - 1) / kNlistWarps;
     if (rebuild_flag && blocks > 148 * 8) blocks = 148 * 8;  // gated: grid-stride
     launch(k_nlist, dim3((unsigned)blocks), dim3(kNlistWarps * 32), 0, as_stream(stream), *g, n, pos_r, cell_start, cell_of_rank, rl2, capacity, rows, row_count, max_count,
         rebuild_flag, status, tag);
+    note_launches(1);
+    return launch_status();
+}
+
+extern "C" int rb_nlist(const rb_grid *g, int64_t n, const double *pos_r, const int32_t *cell_start, const int32_t *cell_of_rank,
+                        double r_list, int32_t capacity, int32_t *rows, int32_t *row_count,
+                        int32_t *max_count, const int64_t *rebuild_flag,
+                        const unsigned long long *status, int64_t tag, void *stream) {
+    NvtxRange nvtx_range("rows (rb_nlist)");
+    bool staged = false;
+    return nlist_launch(g, n, pos_r, cell_start, cell_of_rank, r_list, capacity, rows, row_count,
+                        max_count, nullptr, nullptr, rebuild_flag, status, tag, stream, &staged);
+}
+
+extern "C" size_t rb_nlist_mirror_scratch_bytes(int64_t n) {
+    return sizeof(uint16_t) * kDirStride * (size_t)(n > 0 ? n : 1);
+}
+
+extern "C" int rb_nlist_rows_mirror(const rb_grid *g, int64_t n, const double *pos_r,
+                                    const int32_t *cell_start, const int32_t *cell_of_rank,
+                                    double r_list, int32_t capacity, int32_t *rows,
+                                    int32_t *row_count, int32_t *max_count, int32_t *mirror,
+                                    void *scratch, size_t scratch_bytes,
+                                    const int64_t *rebuild_flag,
+                                    const unsigned long long *status, int64_t tag, void *stream) {
+    NvtxRange nvtx_range("rows + mirror (rb_nlist_rows_mirror)");
+    if (!mirror || !scratch || scratch_bytes < rb_nlist_mirror_scratch_bytes(n))
+        return RB_ERR_ARGUMENT;
+    uint16_t *dir = (uint16_t *)scratch;
+    bool staged = false;
+    int st = nlist_launch(g, n, pos_r, cell_start, cell_of_rank, r_list, capacity, rows,
+                          row_count, max_count, mirror, dir, rebuild_flag, status, tag, stream,
+                          &staged);
+    if (st != RB_OK || n == 0) return st;
+    if (!staged)
+        return rb_nlist_mirror(n, rows, row_count, capacity, mirror, rebuild_flag, status, tag,
+                               stream);
+    int64_t mblocks = (n + kMirrorWarps - 1) / kMirrorWarps;
+    if (rebuild_flag && mblocks > 148 * 8) mblocks = 148 * 8;  // gated: grid-stride
+    launch(k_mirror_resolve, dim3((unsigned)mblocks), dim3(kMirrorWarps * 32), 0,
+           as_stream(stream), n, rows, row_count, capacity, mirror, (const uint16_t *)dir,
+           rebuild_flag, status, tag);
     note_launches(1);
     return launch_status();
 }

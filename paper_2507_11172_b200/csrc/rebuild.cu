@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kRbThreads)
               int32_t *parts, int32_t *cell_of_rank, double *pr, int32_t *rank_of, double *x_ref,
               double rl2, int32_t capacity, int32_t *rows, int32_t *row_count,
               int32_t *max_count, int32_t *mirror, int32_t *cell_of, int32_t *count,
-              int32_t *cursor, int32_t *tiles, unsigned *bar, const int64_t *flag,
+              int32_t *cursor, int32_t *tiles, unsigned *bar, uint16_t *dir, const int64_t *flag,
               const unsigned long long *status, int64_t tag, int32_t nb_cap, float hi_f) {
     pdl_enter();
     if (gate_closed(flag, status, tag)) return;  // the same answer in every block
@@ -168,11 +168,13 @@ __global__ void __launch_bounds__(kRbThreads)
             __syncthreads();
             if (c >= ncell) break;
             if (!nlist_cell<true>(g, c, pr, cell_start, rl2, hi_f, capacity, rows, row_count,
-                                  max_count, sm, nb_cap)) {
+                                  max_count, sm, nb_cap, mirror, dir)) {
                 const int b = ldc<true>(cell_start + c), e = ldc<true>(cell_start + c + 1);
-                for (int r = b + wib; r < e; r += nwb)
+                for (int r = b + wib; r < e; r += nwb) {
                     nlist_one<true>(g, r, n, pr, cell_start, cell_of_rank, rl2, capacity, rows,
                                     row_count, max_count, c);
+                    dir[(int64_t)r * kDirStride + lane] = kDirNone;  // mirror: searched
+                }
                 __syncthreads();
             }
         }
@@ -196,7 +198,12 @@ __global__ void __launch_bounds__(kRbThreads)
         const int64_t b = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
         if (b >= n) break;
         const int64_t e = b + kRbChunk < n ? b + kRbChunk : n;
-        for (int64_t p = b; p < e; p++) mirror_one<true>(p, lane, rows, row_count, capacity, mirror);
+        // staged rows: the partials + directory (cells.cuh mirror_resolve)
+        if (nb_cap > 0)
+            for (int64_t p = b; p < e; p++)
+                mirror_resolve<true>(p, lane, rows, row_count, capacity, mirror, dir);
+        else
+            for (int64_t p = b; p < e; p++) mirror_one<true>(p, lane, rows, row_count, capacity, mirror);
     }
 }
 
@@ -228,12 +235,13 @@ static int rebuild_grid(size_t smem) {
 using namespace rb;
 
 // scratch: barrier words (zero-filled once by the caller) | cell_of[n] |
-// count[ncell] | cursor[ncell] | tile sums
+// count[ncell] | cursor[ncell] | tile sums | mirror directory[n][32] (uint16)
 extern "C" size_t rb_rebuild_scratch_bytes(int64_t n, int64_t ncell) {
     const int64_t ntiles = (std::max<int64_t>(ncell, 1) + kRbTile - 1) / kRbTile;
     return 256 + align256(sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1)) +
            2 * align256(sizeof(int32_t) * (size_t)std::max<int64_t>(ncell, 1)) +
-           align256(sizeof(int32_t) * (size_t)ntiles);
+           align256(sizeof(int32_t) * (size_t)ntiles) +
+           align256(sizeof(uint16_t) * kDirStride * (size_t)std::max<int64_t>(n, 1));
 }
 
 extern "C" int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_t *cell_start,
@@ -260,6 +268,8 @@ extern "C" int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_
     int32_t *cursor = (int32_t *)p;
     p += align256(sizeof(int32_t) * (size_t)ncell);
     int32_t *tiles = (int32_t *)p;
+    p += align256(sizeof(int32_t) * (size_t)((ncell + kRbTile - 1) / kRbTile));
+    uint16_t *dir = (uint16_t *)p;
     const double rl2 = r_list * r_list;  // host-side rc*rc as containers.py:773
     static const int stop = getenv("RB_REBUILD_STOP") ? atoi(getenv("RB_REBUILD_STOP")) : 0;
     if (stop > 0) cudaMemcpyToSymbol(g_rebuild_stop, &stop, sizeof(int));
@@ -269,7 +279,7 @@ extern "C" int rb_rebuild(const rb_grid *g, int64_t n, const double *pos, int32_
     const float hi_f = (float)(rl2 * (1.0 + 1e-3));
     launch_coop(k_rebuild, dim3((unsigned)rebuild_grid(smem)), dim3(kRbThreads), smem, as_stream(stream), *g,
            n, pos, cell_start, cell_particles, cell_of_rank, pos_r, rank_of, x_ref, rl2, capacity,
-           rows, row_count, max_count, mirror, cell_of, count, cursor, tiles, bar, rebuild_flag,
+           rows, row_count, max_count, mirror, cell_of, count, cursor, tiles, bar, dir, rebuild_flag,
            status, tag, nb_cap, hi_f);
     note_launches(1);
     return launch_status();

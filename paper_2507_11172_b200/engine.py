@@ -84,6 +84,7 @@ class ForceEngine:
         self.rebuild_scratch = None
         self.rows = None
         self.mirror = None
+        self.dir_scratch = None  # mirror directory of the staged rows (uint16 [n][32])
         self.atm_scratch = None
         self.capacity = 0
         self.slots = 0  # shared-memory slots of the triplet pass (longest row)
@@ -265,15 +266,17 @@ class ForceEngine:
             if checked:
                 self.max_count.zero_()
             g = self.grid_struct(geom)
-            st = self.L.rb_nlist(ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.cell_start),
-                                 ptr(self.cell_of_rank), float(r_list), int(self.capacity),
-                                 ptr(self.rows), ptr(self.row_count), ptr(self.max_count),
-                                 self._gate(gated), ptr(self.status), int(tag), self.stream)
-            _lib.check(st, "rb_nlist")
-            st = self.L.rb_nlist_mirror(self.n, ptr(self.rows), ptr(self.row_count),
-                                        int(self.capacity), ptr(self.mirror), self._gate(gated),
-                                        ptr(self.status), int(tag), self.stream)
-            _lib.check(st, "rb_nlist_mirror")
+            need = int(self.L.rb_nlist_mirror_scratch_bytes(max(int(self.pos.shape[0]), 1)))
+            if self.dir_scratch is None or self.dir_scratch.numel() < need:
+                self.dir_scratch = self.torch.empty(need, dtype=self.torch.uint8,
+                                                    device=self.device)
+            st = self.L.rb_nlist_rows_mirror(
+                ctypes.byref(g), self.n, ptr(self.pos_r), ptr(self.cell_start),
+                ptr(self.cell_of_rank), float(r_list), int(self.capacity), ptr(self.rows),
+                ptr(self.row_count), ptr(self.max_count), ptr(self.mirror), ptr(self.dir_scratch),
+                self.dir_scratch.numel(), self._gate(gated), ptr(self.status), int(tag),
+                self.stream)
+            _lib.check(st, "rb_nlist_rows_mirror")
             if not checked:
                 return
             worst = int(self.max_count.item())

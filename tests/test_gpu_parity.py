@@ -157,7 +157,14 @@ def test_fused_rebuild_equals_separate_kernels(pkg, nc, r_list):
     ra, rb_ = (e.rows[:n * cap].cpu().numpy().reshape(n, cap) for e in (a, b))
     ma, mb = (e.mirror[:n * cap].cpu().numpy().reshape(n, cap) for e in (a, b))
     valid = np.arange(cap)[None, :] < cnt[:, None]
-    assert np.array_equal(ra[valid], rb_[valid]) and np.array_equal(ma[valid], mb[valid])
+    assert np.array_equal(ra[valid], rb_[valid])
+    # mirror: the entries above the diagonal (the ones the header defines),
+    # each the position of p in row q
+    upper = valid & (ra > np.arange(n)[:, None])
+    assert np.array_equal(ma[upper], mb[upper])
+    p_idx, k_idx = np.nonzero(upper)
+    q_idx = ra[p_idx, k_idx]
+    assert np.array_equal(ra[q_idx, ma[p_idx, k_idx]], p_idx)
     assert int(a.max_count.item()) == int(b.max_count.item())
     # gate closed (flag != tag): nothing is written
     before = b.rows.clone()

@@ -33,6 +33,7 @@
 #include <algorithm>
 
 #include "atm_core.cuh"
+#include "atm_rot.cuh"
 
 #include <type_traits>
 
@@ -46,7 +47,12 @@ constexpr int kA3Warps = RB_A3_WARPS;
 #define RB_A3_MIN_BLOCKS 7
 #endif
 constexpr int kA3MinBlocks = RB_A3_MIN_BLOCKS;  // register cap for occupancy
-constexpr int kA3MaxSlots = 4096;    // longest S+(i) a warp takes (rows are <= 4096)
+constexpr int kA3MaxSlots = 4096;
+// G entries are padded to 4 doubles (32 bytes, sector-aligned): every partial
+// force write covers a whole DRAM sector, so the scattered writes need no
+// read-modify-write fill (24-byte entries straddle sectors written at
+// different times by different bases)
+constexpr int kGStride = 4;    // longest S+(i) a warp takes (rows are <= 4096)
 
 // Phase 0: S+(r), the suffix of r's rank-sorted row with rank > r and
 // r_ir^2 <= rc^2 (reference arithmetic), into the warp's slots.  Returns m,
@@ -116,10 +122,9 @@ __device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image
                 // written for it.)
                 if (!keep && mk2[h] >= 0) {
                     RB_CHECK(mk2[h] < capacity);
-                    double *gq = gbuf + ((int64_t)q * capacity + mk2[h]) * 3;
-                    gq[0] = 0.0;
-                    gq[1] = 0.0;
-                    gq[2] = 0.0;
+                    double2 *gq = (double2 *)(gbuf + ((int64_t)q * capacity + mk2[h]) * kGStride);
+                    gq[0] = make_double2(0.0, 0.0);
+                    gq[1] = make_double2(0.0, 0.0);
                 }
             }
             const unsigned mk = __ballot_sync(0xffffffffu, keep);
@@ -196,17 +201,28 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
                                    row, mir, capacity, slots, cut.rc2, gbuf, owned, status, tag,
                                    ovf, slot_bad);
     if (m < 0) return;
+    // the fast instance (standard case, 64 slots) takes only bases without a
+    // slot under the guard distance: the others go to the second launch
+    constexpr bool kFast = !kExactImage && !kOwned && kM == 64;
+    if (kFast && slot_bad) {
+        if (lane == 0) ovf[2 + atomicAdd(ovf, 1)] = (int32_t)r;
+        return;
+    }
 
     // ---- phase 1: the slot pairs, 32 per window (a3_windows)
     A3Acc acc = {0.0, 0.0, 0, false, kOwned ? (int)owned[r] : 1};
     double F[3] = {0.0, 0.0, 0.0};
     // debug 1: phases 0 and 3 only; 2 / 3: phase 1 of the bases with m < 32 /
     // m >= 32 only (timing split, tuning only)
-    if (debug_mode != 1 && !(debug_mode == 2 && m >= 32) && !(debug_mode == 3 && m < 32)) {
-        if (slot_bad)
+    const int dm = debug_mode & 15;
+    if (dm != 1 && !(dm == 2 && m >= 32) && !(dm == 3 && m < 32)) {
+        if constexpr (kFast) {
+            a3_rot(sm, m, lane, g, pr, cut, acc);  // register-resident rounds (atm_rot.cuh)
+        } else if (slot_bad) {
             a3_windows<kExactImage, kOwned, true>(sm, m, slots, lane, g, pr, cut, acc, F);
-        else
+        } else {
             a3_windows<kExactImage, kOwned, false>(sm, m, slots, lane, g, pr, cut, acc, F);
+        }
     }
 
     // ---- phase 3: slot sums -> G[i][row index]; own part, scalars.  Per
@@ -221,7 +237,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     double sx = 0.0, sy = 0.0, sz = 0.0, sw = 0.0;
     for (int sl = lane; sl < m; sl += 32) {
         double ax = F[0], ay = F[1], az = F[2];  // m < 32: the lane's register sums
-        if (m >= 32) {
+        if (kFast || m >= 32) {
             const double2 axy = sm.axy[sl];
             ax = axy.x;
             ay = axy.y;
@@ -229,10 +245,9 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
         }
         RB_CHECK(sm.q[sl] >= 0 && sm.q[sl] < n && sm.mpos[sl] < capacity);
         if (sm.mpos[sl] >= 0) {  // (-1: a truncated row, see a3_slots)
-            double *gq = gbuf + ((int64_t)sm.q[sl] * capacity + sm.mpos[sl]) * 3;
-            gq[0] = ax;
-            gq[1] = ay;
-            gq[2] = az;
+            double2 *gq = (double2 *)(gbuf + ((int64_t)sm.q[sl] * capacity + sm.mpos[sl]) * kGStride);
+            gq[0] = make_double2(ax, ay);  // one whole 32-byte sector
+            gq[1] = make_double2(az, 0.0);
         }
         sx += ax;
         sy += ay;
@@ -358,7 +373,7 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
     if (active) {
         const int m = row_count[p];
         const int32_t *row = rows + p * (int64_t)capacity;
-        const double *gp = gbuf + p * (int64_t)capacity * 3;
+        const double2 *gp = (const double2 *)(gbuf + p * (int64_t)capacity * kGStride);
         // rows are rank-sorted: the prefix q < p holds the partials.  The
         // first kGatherRegs entries of the lane are loaded together (index
         // and partial), then summed in row order; longer prefixes continue
@@ -369,9 +384,10 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
             const bool in = more && k < m && __ldg(row + k) < p;
             double gx = 0.0, gy = 0.0, gz = 0.0;
             if (k < m) {  // loads independent of the row test: issued together
-                gx = gp[3 * k];
-                gy = gp[3 * k + 1];
-                gz = gp[3 * k + 2];
+                const double2 xy = gp[2 * k];
+                gx = xy.x;
+                gy = xy.y;
+                gz = gp[2 * k + 1].x;
             }
             if (in) {
                 fx += gx;
@@ -383,9 +399,10 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
         RB_CHECK(m >= 0 && m <= capacity);
         for (; more && k < m; k += kGatherGroup) {
             if (row[k] >= p) break;
-            fx += gp[3 * k];
-            fy += gp[3 * k + 1];
-            fz += gp[3 * k + 2];
+            const double2 xy = gp[2 * k];
+            fx += xy.x;
+            fy += xy.y;
+            fz += gp[2 * k + 1].x;
         }
     }
     fx = group_sum<kGatherGroup>(fx);
@@ -424,10 +441,10 @@ extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
     // virial sums (n each) and triplet counts (n int32, 8-byte padded) --
     // every output the caller sees is written by the gather, so the triplet
     // kernels may run concurrently with the pair pass -- then G
-    // (n x capacity x 3) doubles
+    // (n x capacity x 4: 32-byte entries, aligned) doubles
     const size_t nn = (size_t)(n > 0 ? n : 1);
     return a3_header_bytes(nn) + nn * 5 * sizeof(double) + ((nn * sizeof(int32_t) + 7) & ~(size_t)7) +
-           nn * 3 * sizeof(double) * (size_t)capacity;
+           32 + nn * kGStride * sizeof(double) * (size_t)capacity;
 }
 
 namespace rb {
@@ -498,12 +515,22 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
                       int32_t *triplets_rank, const uint8_t *owned, unsigned long long *status,
                       int64_t tag, int debug_mode, int32_t *ovf, int32_t *work) {
     static size_t granted_ovf = 0;
-    const size_t per = a3_warp_bytes(fast);
+    // the standard case runs the fast instance (64 slots, register-resident
+    // rounds) and always lists bases beyond it -- S+ over 64 slots, or a slot
+    // under the guard distance -- for the second launch
+    constexpr bool kStd = !kExactImage && !kOwned;
+    if (kStd) fast = std::min(64, full);
+    const size_t per = a3_warp_bytes(kStd ? 64 : fast);
     const int warps = a3_warps_for(per);
-    const bool split = fast < full;
+    const bool split = kStd || fast < full;
     int32_t *list = split ? ovf : nullptr;
     // the common slot counts get compile-time layouts
-    if (fast == 64)
+    if (kStd)
+        a3_launch_main<kExactImage, kOwned, 64>(st, n, warps, per, g, pos_r, rows, row_count,
+                                                mirror, capacity, 64, cut, own,
+                                                gbuf, energy_rank, virial_rank, triplets_rank,
+                                                owned, status, tag, debug_mode, list, work);
+    else if (fast == 64)
         a3_launch_main<kExactImage, kOwned, 64>(st, n, warps, per, g, pos_r, rows, row_count,
                                                 mirror, capacity, fast, cut, own,
                                                 gbuf, energy_rank, virial_rank, triplets_rank,
@@ -563,6 +590,7 @@ extern "C" int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r
     double *e_s = own + 3 * n, *w_s = e_s + n;
     int32_t *n_s = (int32_t *)(w_s + n);
     double *gbuf = (double *)((char *)n_s + (((size_t)n * sizeof(int32_t) + 7) & ~(size_t)7));
+    gbuf = (double *)(((uintptr_t)gbuf + 31) & ~(uintptr_t)31);  // whole 32-byte sectors
     auto hiword = [](double x) {
         int64_t b;
         memcpy(&b, &x, sizeof b);

@@ -681,3 +681,29 @@ def test_tiny_systems_match_oracle(pkg, oracle, n, periodic):
     assert np.max(np.abs(a.positions - b.positions), initial=0.0) <= 1e-10
     assert np.max(np.abs(a.velocities - b.velocities), initial=0.0) <= 1e-10
     assert max((abs(x - y) for x, y in zip(tr.total, rtr.total)), default=0.0) <= 1e-10
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_pairs_on_the_cutoff_match_oracle(pkg, oracle, k):
+    """A simple-cubic lattice with spacing rc / k: many slot pairs sit on the
+    cutoff (within rounding), so the fp64 estimate of r_jk^2 is undecided and
+    the reference arithmetic settles them (the fix-up rounds of atm_rot.cuh,
+    in rotation rounds for k = 2 and in both rotation and A x B cross rounds
+    for k = 3, S+(i) ~ 60).  Counts bit-exact, forces normwise <= 1e-10."""
+    h = 2.5 / k
+    nd = 4 * k
+    g = np.arange(nd) * h
+    pos = np.stack(np.meshgrid(g, g, g, indexing="ij"), axis=-1).reshape(-1, 3) + 0.25
+    pos = pos[np.arange(len(pos)) % 7 != 3]  # vacancies: nonzero forces, pairs stay on rc
+    box = (nd * h,) * 3
+    ff = pkg.ForceField(nu=0.4, cutoff=2.5)
+    s = _system(pkg, pos, box, True)
+    c = pkg.CudaLinkedCells()
+    c.triplet_pass(s, ff)
+    os_ = oracle.OracleSystem.from_positions(pos, np.array(box), True)
+    off = oracle.OracleForceField(nu=0.4, cutoff=2.5)
+    grid = oracle.build_cell_grid(os_, 2.5)
+    f3, e3, _ = oracle.c01_triplet_pass(grid, os_, off)
+    assert c.triplet_visits == oracle.triplet_visit_count(grid, os_)
+    assert normwise(s.forces_3b, f3) <= FORCE_TOL
+    assert abs(c.triplet_energy - e3) <= ENERGY_TOL * abs(e3)

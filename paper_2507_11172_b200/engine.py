@@ -182,14 +182,14 @@ class ForceEngine:
         self.n = int(n)
 
     def reset_status(self, step: int = 0) -> None:
-        self.status[0] = -1
+        self.status[0:1].fill_(-1)  # (fill kernels: capturable)
         self.status[3:].zero_()
         self.set_step(step)
 
     def set_step(self, step: int) -> None:
         """Device step counter: step `step` current and closed (the next
         step-opening drift numbers its step step + 1)."""
-        self.status[1:3] = int(step)
+        self.status[1:3].fill_(int(step))
 
     def read_status(self):
         """(tag, kind) of the first recorded device error, or None (syncs)."""

@@ -77,7 +77,10 @@ class GpuBackend:
             eng.pos[:n] = local
             eng.bin(window)
             eng.nlist(window, self.r_build, capacity=eng.capacity or None, checked=True)
-            eng.owned_rank = (eng.parts[:n] < n_own).to(torch.uint8)
+            # owned flags only with ghosts present (a rank owning its whole
+            # local set -- world 1 -- takes the undecomposed kernels, whose
+            # triplet pass recovers the energy from the slot virial)
+            eng.owned_rank = (eng.parts[:n] < n_own).to(torch.uint8) if n > n_own else None
         else:
             eng.pos[:n] = local
             eng.pos_r[:n][eng.rank_of[:n].long()] = eng.pos[:n]

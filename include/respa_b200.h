@@ -62,6 +62,11 @@ extern "C" {
 #define RB_KIND_TRIPLET_MIN_SEPARATION 2 /* raised by triplet_pass (:161-164) */
 #define RB_KIND_NONFINITE 3              /* _check_finite (:89-93, :166-170) */
 #define RB_KIND_CAPACITY 4               /* neighbour-list overflow (no reference analogue) */
+#define RB_KIND_REBUILD 0                /* not an error: a rebuild vote froze the steps from
+                                            `tag` on (speculative windows of the decomposed
+                                            loop, rb_vote_freeze); drift, kick, sample and the
+                                            halo pull stop too, so the host rebuilds and
+                                            resumes step `tag` */
 #define RB_STATUS_CLEAR 0xFFFFFFFFFFFFFFFFull
 
 #define RB_MAX_OFFSETS 125
@@ -379,6 +384,21 @@ RB_API int rb_respa_kick_drift(int64_t n, double *pos, double *vel, double *f2_o
                                const int32_t *rank_of, double *pos_r, const double *x_ref,
                                double skin, int64_t *rebuild_flag, unsigned long long *status,
                                uint64_t rebuild_cond, void *stream);
+/* Speculative windows of the decomposed loop: the rebuild
+ * vote of the current device step without a host round trip.
+ * rb_vote_flag:   *flag = 1 if this rank's drift flagged the current step
+ *                 (rebuild_flag[0] == status[1]), else 0 -- the input of an
+ *                 all_reduce(MAX) over the ranks (captured with the step);
+ * rb_vote_freeze: if *flag > 0 and no error is recorded, records
+ *                 RB_KIND_REBUILD at the current step: every later kernel of
+ *                 the window exits, the host reads the word once per window.
+ * Replace the per-step host vote of the reference-less multi-GPU loop; no
+ * reference analogue (the reference's distributed mode is out of scope,
+ * SPEC.md:13). */
+RB_API int rb_vote_flag(const int64_t *rebuild_flag, const unsigned long long *status,
+                        int64_t *flag, void *stream);
+RB_API int rb_vote_freeze(const int64_t *flag, unsigned long long *status, void *stream);
+
 RB_API int rb_respa_kick(int64_t n, double *vel, double *f2_old, const double *f2_new,
                   const double *f3, double half_dt, double half_respa, int32_t kick3,
                   unsigned long long *status, int64_t tag, void *stream);

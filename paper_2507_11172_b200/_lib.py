@@ -27,6 +27,7 @@ RB_KIND_PAIR_MIN_SEPARATION = 1
 RB_KIND_TRIPLET_MIN_SEPARATION = 2
 RB_KIND_NONFINITE = 3
 RB_KIND_CAPACITY = 4
+RB_KIND_REBUILD = 0  # not an error: a speculative window froze (domain loop)
 RB_STATUS_CLEAR = 0xFFFFFFFFFFFFFFFF
 RB_TAG_FROM_DEVICE = -1
 RB_MAX_OFFSETS = 125
@@ -94,6 +95,8 @@ SIGNATURES = {
     "rb_respa_kick_drift": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, _I32, _D, _D, _D, _D,
                                            _I32, _I32, _P, _P, _P, _D, _P, _P, _U64, _P]),
     "rb_respa_kick": (ctypes.c_int, [_I64, _P, _P, _P, _P, _D, _D, _I32, _P, _I64, _P]),
+    "rb_vote_flag": (ctypes.c_int, [_P, _P, _P, _P]),
+    "rb_vote_freeze": (ctypes.c_int, [_P, _P, _P]),
     "rb_step_begin": (ctypes.c_int, [_P, _P]),
     "rb_trace_record": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "rb_fp64_peak": (ctypes.c_int, [_I32, _P, _P]),

@@ -243,6 +243,14 @@ __device__ __forceinline__ bool frozen(const unsigned long long *status, int64_t
     return false;
 }
 
+// A rebuild vote froze the steps from its tag on (RB_KIND_REBUILD): the
+// state-changing kernels of step `tag` or later (drift, kick, sample, halo
+// pull) must not run either.
+__device__ __forceinline__ bool rebuild_frozen(unsigned long long s, int64_t tag) {
+    return s != RB_STATUS_CLEAR && (int)(s & 0xff) == RB_KIND_REBUILD &&
+           (long long)(s >> 8) <= (long long)tag;
+}
+
 // warp-uniform variant: lane 0 reads, everyone agrees (needed before shuffles)
 __device__ __forceinline__ bool warp_frozen(const unsigned long long *status, int64_t tag,
                                             int kind) {

@@ -60,6 +60,7 @@ __global__ void k_halo_pull(int64_t n, const int32_t *__restrict__ src_rank,
     pdl_enter();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (rebuild_frozen(status[0], (int64_t)status[1])) return;  // (a frozen window step)
     // the half the owners' drifts of this step (status[1]) published into
     const int64_t half = (int64_t)(status[1] & 1ull) * 3 * stride;
     const double *src = reinterpret_cast<const double *>(peers[src_rank[i]]) + half +

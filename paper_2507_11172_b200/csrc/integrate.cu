@@ -88,13 +88,15 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
     // a step-opening drift numbers its step from the last CLOSED step
     // (status[2], written by the step's pair pass and kick) and publishes it
     // in status[1]: no kernel reads the word another block of it writes.
+    const unsigned long long sw = s01.x;  // the error word as this step found it
     if (advance) {
         tag = (int64_t)ld_status2(status + 2).x + 1;
+        if (rebuild_frozen(sw, tag)) return;  // a speculative window stopped here
         if (gt == 0) status[1] = (unsigned long long)tag;
     } else if (tag < 0) {
         tag = status ? (int64_t)s01.y : 0;
     }
-    const unsigned long long sw = s01.x;  // the error word as this step found it
+    if (rebuild_frozen(sw, tag)) return;
     if (kick_prev) {
         // the kick that closes the previous step (tag - 1), folded in: the
         // same updates and error rules as k_kick (integrators.py:158-165)
@@ -172,6 +174,7 @@ __global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict_
     const ulonglong2 s01 = ld_status2(status);
     const bool from_device = tag < 0;
     if (tag < 0) tag = status ? (int64_t)s01.y : 0;
+    if (status && rebuild_frozen(s01.x, tag)) return;  // (the step stays open)
     if (from_device && status && i == 0) status[2] = (unsigned long long)tag;  // closes the step
     if (i >= n3) return;
     bool do_kick2 = true, do_kick3 = kick3 != 0;
@@ -336,7 +339,10 @@ __global__ void __launch_bounds__(kRedThreads)
             out[q] += *(volatile const double *)(partial + q * kRedMaxBlocks + i);
     }
     block_tree_sum5(out, sh);
-    if (threadIdx.x == 0) {
+    // a step a speculative window froze records nothing (it is run again)
+    const bool fz = status && rebuild_frozen(status[0], (int64_t)status[1]);
+    if (threadIdx.x == 0 && fz) *ticket = 0u;
+    if (threadIdx.x == 0 && !fz) {
         for (int q = 0; q < kSampleQ; q++) sums[q] = out[q];
         if (trace) {
             const int64_t tag = (int64_t)status[1];
@@ -406,6 +412,18 @@ __global__ void k_trace_record(const unsigned long long *status, int64_t interva
     row[5] = *w3;
     row[6] = 0.0;
     row[7] = 0.0;
+}
+
+// the rebuild vote of the current step (rb_vote_flag / rb_vote_freeze)
+__global__ void k_vote_flag(const int64_t *rebuild_flag, const unsigned long long *status,
+                            int64_t *flag) {
+    pdl_enter();
+    *flag = rebuild_flag[0] == (int64_t)status[1] ? 1 : 0;
+}
+__global__ void k_vote_freeze(const int64_t *flag, unsigned long long *status) {
+    pdl_enter();
+    if (*flag > 0 && status[0] == RB_STATUS_CLEAR)
+        status[0] = (status[1] << 8) | (unsigned long long)RB_KIND_REBUILD;
 }
 
 __global__ void k_flush(int4 *buf, int64_t n16, int v) {
@@ -654,4 +672,19 @@ extern "C" int rb_event_elapsed(void *start, void *end, float *ms) {
     return cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end) == cudaSuccess
                ? RB_OK
                : RB_ERR_CUDA;
+}
+
+extern "C" int rb_vote_flag(const int64_t *rebuild_flag, const unsigned long long *status,
+                            int64_t *flag, void *stream) {
+    if (!rebuild_flag || !status || !flag) return RB_ERR_ARGUMENT;
+    launch(k_vote_flag, dim3(1), dim3(1), 0, as_stream(stream), rebuild_flag, status, flag);
+    note_launches(1);
+    return launch_status();
+}
+
+extern "C" int rb_vote_freeze(const int64_t *flag, unsigned long long *status, void *stream) {
+    if (!flag || !status) return RB_ERR_ARGUMENT;
+    launch(k_vote_freeze, dim3(1), dim3(1), 0, as_stream(stream), flag, status);
+    note_launches(1);
+    return launch_status();
 }

@@ -22,6 +22,7 @@ loop.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -315,6 +316,10 @@ class GpuBackend:
         return int(err[0]), reason
 
 
+# speculative-window bookkeeping of this process (tests, probes)
+WINDOW_STATS = {"runs": 0, "resumes": 0}
+
+
 @dataclass
 class DomainState:
     ids: object  # (n_own,) float64 global ids
@@ -475,6 +480,74 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
         reason = err[1] if err is not None and err[0] == it else "error on another rank"
         return it, reason
 
+    # Speculative windows: the rebuild vote of each step is a
+    # device flag reduced over the ranks (one NCCL all_reduce enqueued from
+    # the host, none at world 1) that freezes the rest of the window on the
+    # device (RB_KIND_REBUILD); the host synchronises once per window, then
+    # rebuilds and resumes the frozen step.  The all_reduce also orders the
+    # peers' publishing drifts before every rank's ghost pull.  Message
+    # halos and gloo keep the per-step host vote.
+    wlen = int(os.environ.get("RB_DOMAIN_WINDOW", "16"))
+    windowed = (fast and wlen > 1 and skin > 0.0 and
+                (world == 1 or (peer and dist.get_backend() == "nccl")))
+
+    def run_windows(num, drift_args, kick_args):
+        WINDOW_STATS["runs"] += 1
+        L, eng, lib = backend.eng.L, backend.eng, backend._lib
+        ptr = lib.ptr
+        vflag = torch.zeros(1, dtype=torch.int64, device=dev)
+        head = np.zeros(2, dtype=np.uint64)
+        i = 0
+        while i < num:
+            j = min(num, i + wlen)
+            for k in range(i, j):
+                if k > i and on_step is not None:
+                    on_step(k)
+                # the vote of step k (its drift ran at the end of step k-1)
+                lib.check(L.rb_vote_flag(ptr(eng.rebuild_flag), ptr(eng.status), ptr(vflag),
+                                         eng.stream), "rb_vote_flag")
+                if world > 1:
+                    dist.all_reduce(vflag, op=dist.ReduceOp.MAX)
+                lib.check(L.rb_vote_freeze(ptr(vflag), ptr(eng.status), eng.stream),
+                          "rb_vote_freeze")
+                sample = (k + 1) % interval == 0
+                end_of_cycle = (k + 1) % s == 0
+                nxt = drift_args(k + 1) if k + 1 < num else None
+                backend.replay((end_of_cycle, sample, peer, nxt is not None),
+                               lambda: backend.step_body(end_of_cycle, sample, peer, nxt,
+                                                         kick_args))
+            head[:] = eng.status[:2].cpu().numpy().view(np.uint64)  # the window's sync
+            word = int(head[0])
+            # one decision for every rank: an error (key 2 tag) before a
+            # rebuild request (2 tag + 1) of the same step, nothing: never
+            key = never if word == lib.RB_STATUS_CLEAR else \
+                2 * (word >> 8) + (1 if (word & 0xFF) == lib.RB_KIND_REBUILD else 0)
+            if world > 1:
+                t = torch.tensor([key], dtype=torch.int64, device=wire)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                key = int(t.item())
+            if key == never:
+                i = j
+                if i < num and on_step is not None:
+                    on_step(i)
+                continue
+            if key % 2 == 0:
+                return  # a device error: reported by the caller (first_error)
+            # a rank flagged step k = tag - 1: every rank froze there; the
+            # rows are rebuilt after its drift, then the step runs eagerly
+            k = key // 2 - 1
+            WINDOW_STATS["resumes"] += 1
+            eng.status[0:1].fill_(-1)  # RB_STATUS_CLEAR
+            rebuild()
+            backend.invalidate_graphs()
+            nxt = drift_args(k + 1) if k + 1 < num else None
+            if on_step is not None and k > i:
+                on_step(k)
+            backend.step_body((k + 1) % s == 0, (k + 1) % interval == 0, False, nxt, kick_args)
+            i = k + 1
+            if i < num and on_step is not None:
+                on_step(i)
+
     def run_device_loop():
         """GPU backends: device-resident state, one host synchronisation per
         step (the rebuild vote).  Between rebuilds each step after its vote
@@ -499,7 +572,12 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
             on_step(0)
         if num > 0:
             backend.drift(*drift_args(0))
-        for i in range(num):
+        if windowed:
+            run_windows(num, drift_args, kick_args)
+            num_done = num
+        else:
+            num_done = 0
+        for i in range(num_done, num):
             if i > 0 and on_step is not None:
                 on_step(i)
             sample = (i + 1) % interval == 0

@@ -707,3 +707,60 @@ def test_pairs_on_the_cutoff_match_oracle(pkg, oracle, k):
     assert c.triplet_visits == oracle.triplet_visit_count(grid, os_)
     assert normwise(s.forces_3b, f3) <= FORCE_TOL
     assert abs(c.triplet_energy - e3) <= ENERGY_TOL * abs(e3)
+
+
+def _domain_world1_worker(rank, world, port, out_dir, window):
+    import os as _os
+
+    import torch.distributed as dist
+
+    _os.environ["MASTER_ADDR"] = "127.0.0.1"
+    _os.environ["MASTER_PORT"] = str(port)
+    _os.environ["RB_DOMAIN_WINDOW"] = str(window)
+    import torch
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        import paper_2507_11172_b200 as pkg
+        from paper_2507_11172_b200 import domain_run
+        from paper_2507_11172_b200.domain_run import domain_respa_run, gpu_backend_factory
+
+        sysm = pkg.systems.fcc_system(8, jitter=0.05, seed=21, temperature=1.2, vseed=22)
+        ff = pkg.ForceField(nu=0.3, cutoff=2.5)
+        trace = domain_respa_run(dist, sysm, ff, pkg.RespaSchedule(0.002, 5, 60),
+                                 gpu_backend_factory(ff), skin=0.1)
+        np.savez(_os.path.join(out_dir, f"w1_{window}.npz"), x=sysm.positions,
+                 v=sysm.velocities, total=np.array(trace.total),
+                 resumes=domain_run.WINDOW_STATS["resumes"], runs=domain_run.WINDOW_STATS["runs"])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_domain_speculative_windows_match_per_step_votes(pkg, tmp_path):
+    """World 1 over NCCL: the speculative-window loop (device rebuild vote,
+    RB_KIND_REBUILD freeze, one host synchronisation per window, resume at
+    the frozen step) and the per-step host vote give bit-identical
+    trajectories, equal to the single-GPU loop within 1e-10; the small skin
+    puts rebuild requests inside windows."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    outs = {}
+    for window in (16, 0):
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        mp.start_processes(_domain_world1_worker, args=(1, port, str(tmp_path), window),
+                           nprocs=1, join=True, start_method="spawn")
+        outs[window] = np.load(tmp_path / f"w1_{window}.npz")
+    a, b = outs[16], outs[0]
+    assert int(a["runs"]) == 1 and int(a["resumes"]) >= 2 and int(b["runs"]) == 0
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["v"], b["v"])
+    assert np.array_equal(a["total"], b["total"])
+    ref = pkg.systems.fcc_system(8, jitter=0.05, seed=21, temperature=1.2, vseed=22)
+    ff = pkg.ForceField(nu=0.3, cutoff=2.5)
+    tr = pkg.respa_run(ref, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 5, 60))
+    assert np.max(np.abs(a["x"] - ref.positions)) <= 1e-10
+    assert max(_rel(x, y) for x, y in zip(a["total"], tr.total)) <= 1e-10

@@ -172,6 +172,7 @@ __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, in
     double fj[3], fk[3];
 #pragma unroll 1
     for (int d = 1; d <= rounds; d++) {
+        RB_CHECK(toff < end && src >= 0 && src < gm && off + gm <= 64);
         double tx, ty, tz, b;
         lds_rec(xy0 + toff, zr0 + toff, tx, ty, tz, b);  // conflict-free: a rotation
         bool u;
@@ -227,6 +228,7 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
     const unsigned ret0 = smem_u32(sm.axy + 32), retz0 = smem_u32(sm.az + 32);
 #pragma unroll 1
     for (int e = 0; e < mb; e++) {
+        RB_CHECK(boff >= bbeg && boff < bend && mb <= 32 && m <= 64);
         double tx, ty, tz, b;
         lds_rec(xy0 + boff, zr0 + boff, tx, ty, tz, b);
         bool u;

@@ -259,6 +259,23 @@ class Decomposition:
         c = np.trunc(pos * inv[None, :]).astype(np.int64)
         return np.clip(c, 0, n[None, :] - 1)
 
+    def cells_of_t(self, pos):
+        """cells_of on a torch tensor (on its device; the same IEEE
+        arithmetic: one product, truncation, clamp)."""
+        import torch
+
+        inv = torch.tensor(self.geom.inv_cell, dtype=torch.float64, device=pos.device)
+        n = torch.tensor(self.geom.cells, dtype=torch.int64, device=pos.device)
+        c = torch.trunc(pos * inv[None, :]).to(torch.int64)
+        return torch.minimum(torch.clamp(c, min=0), n[None, :] - 1)
+
+    def block_coord_t(self, cells_d, d: int):
+        """Block coordinate along dimension d of global cell indices (torch)."""
+        import torch
+
+        b = torch.as_tensor(np.asarray(self.bounds[d], dtype=np.int64), device=cells_d.device)
+        return torch.searchsorted(b, cells_d.contiguous(), right=True) - 1
+
     def block_of(self, cells: np.ndarray) -> np.ndarray:
         """Block coordinate per particle and dimension."""
         out = np.empty_like(cells)
@@ -375,22 +392,23 @@ def migrate(dec: Decomposition, ex: Exchanger, payload):
     (the skin bounds the displacement)."""
     import torch
 
+    if not any(dec.split(d) for d in range(3)):
+        return payload  # one block: nothing moves, the order (ascending id) stands
     for d in range(3):
         if not dec.split(d):
             continue
-        pos = payload[:, 1:4].cpu().numpy()
-        blk = dec.block_of(dec.cells_of(pos))[:, d]
+        # cell and block maps on the payload's device (no host round trip of
+        # the positions)
+        blk = dec.block_coord_t(dec.cells_of_t(payload[:, 1:4])[:, d], d)
         me, p = dec.coord[d], dec.dims[d]
         stay = blk == me
         to_minus = (~stay) & (blk == (me - 1) % p)
         to_plus = (~stay) & (~to_minus)
-        if np.any(to_plus & (blk != (me + 1) % p)):
+        if bool(torch.any(to_plus & (blk != (me + 1) % p))):
             raise RuntimeError("a particle moved more than one block between row rebuilds")
-        dev = payload.device
-        sel = lambda m: payload[torch.from_numpy(np.nonzero(m)[0]).to(dev)]  # noqa: E731
-        from_plus, from_minus = ex.exchange(sel(to_minus), sel(to_plus), dec.neighbor(d, -1),
-                                            dec.neighbor(d, +1))
-        payload = torch.cat([sel(stay), from_plus, from_minus], dim=0)
+        from_plus, from_minus = ex.exchange(payload[to_minus], payload[to_plus],
+                                            dec.neighbor(d, -1), dec.neighbor(d, +1))
+        payload = torch.cat([payload[stay], from_plus, from_minus], dim=0)
     # deterministic local order: ascending global id
     order = torch.argsort(payload[:, 0])
     return payload[order]
@@ -411,12 +429,9 @@ def build_ghosts(dec: Decomposition, ex: Exchanger, pos_owned, origin=None):
     for d in range(3):
         if not dec.split(d):
             continue
-        cells = dec.cells_of(local[:, :3].cpu().numpy())[:, d]
-        idx_m = np.nonzero(cells == dec.lo[d])[0]
-        idx_p = np.nonzero(cells == dec.hi[d] - 1)[0]
-        dev = local.device
-        tm = torch.from_numpy(idx_m).to(dev)
-        tp = torch.from_numpy(idx_p).to(dev)
+        cells = dec.cells_of_t(local[:, :3])[:, d]
+        tm = torch.nonzero(cells == dec.lo[d]).reshape(-1)
+        tp = torch.nonzero(cells == dec.hi[d] - 1).reshape(-1)
         from_plus, from_minus = ex.exchange(local[tm], local[tp], dec.neighbor(d, -1),
                                             dec.neighbor(d, +1))
         stages.append((d, tm, tp, int(from_plus.shape[0]), int(from_minus.shape[0])))

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import time
 from dataclasses import dataclass
 from typing import Optional
 
@@ -317,7 +318,7 @@ class GpuBackend:
 
 
 # speculative-window bookkeeping of this process (tests, probes)
-WINDOW_STATS = {"runs": 0, "resumes": 0}
+WINDOW_STATS = {"runs": 0, "resumes": 0, "rebuild_s": 0.0}
 
 
 @dataclass
@@ -394,17 +395,19 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     if peer:
         backend.attach_peers(dist)
 
+    split = any(dec.split(d) for d in range(3))
+
     def rebuild():
         nonlocal window
-        if st.f2 is not None:
+        if st.f2 is None:
+            st.f2 = torch.zeros_like(st.x)
+            st.f3 = torch.zeros_like(st.x)
+        elif split:  # (one block: nothing can move)
             payload = torch.cat([st.ids[:, None], st.x, st.v, st.f2, st.f3], dim=1)
             payload = migrate(dec, ex, payload)
             st.ids, st.x, st.v = payload[:, 0], payload[:, 1:4], payload[:, 4:7]
             st.f2, st.f3 = payload[:, 7:10].contiguous(), payload[:, 10:13].contiguous()
             st.x, st.v = st.x.contiguous(), st.v.contiguous()
-        else:
-            st.f2 = torch.zeros_like(st.x)
-            st.f3 = torch.zeros_like(st.x)
         origin = None
         if peer:
             n_own = int(st.x.shape[0])
@@ -538,7 +541,9 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
             k = key // 2 - 1
             WINDOW_STATS["resumes"] += 1
             eng.status[0:1].fill_(-1)  # RB_STATUS_CLEAR
+            t_rb = time.perf_counter()
             rebuild()
+            WINDOW_STATS["rebuild_s"] += time.perf_counter() - t_rb
             backend.invalidate_graphs()
             nxt = drift_args(k + 1) if k + 1 < num else None
             if on_step is not None and k > i:

@@ -64,6 +64,8 @@ def main(argv):
         pstats.Stats(prof).sort_stats("tottime").print_stats(25)
         pstats.Stats(prof).sort_stats("cumtime").print_stats("paper_2507_11172_b200", 30)
     loop = steps_run[steps] - steps_run[0]
+    from paper_2507_11172_b200.domain_run import WINDOW_STATS
+    print(f"windows: {WINDOW_STATS}")
     print(f"domain loop (world 1, {backend}): {1e3 * dt / steps:.3f} ms/step over {steps} steps "
           f"incl. setup; step loop alone {1e3 * loop / steps:.3f} ms/step")
     s2 = cfg.system()

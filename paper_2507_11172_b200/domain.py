@@ -295,6 +295,25 @@ class Decomposition:
                 inside &= rel < self.hi[d] - self.lo[d] + 2
         return int(inside.sum())
 
+    def window_count_t(self, pos) -> int:
+        """window_count on a torch tensor (on its device)."""
+        import torch
+
+        c = self.cells_of_t(pos)
+        inside = torch.ones(c.shape[0], dtype=torch.bool, device=pos.device)
+        n = self.geom.cells
+        for d in range(3):
+            if self.split(d):
+                rel = torch.remainder(c[:, d] - self.lo[d] + 1, n[d])
+                inside &= rel < self.hi[d] - self.lo[d] + 2
+        return int(inside.sum().item())
+
+    def owner_rank_t(self, pos):
+        """owner_rank on a torch tensor (on its device)."""
+        c = self.cells_of_t(pos)
+        b = [self.block_coord_t(c[:, d], d) for d in range(3)]
+        return (b[0] * self.dims[1] + b[1]) * self.dims[2] + b[2]
+
     def owner_rank(self, pos: np.ndarray) -> np.ndarray:
         b = self.block_of(self.cells_of(pos))
         return (b[:, 0] * self.dims[1] + b[:, 1]) * self.dims[2] + b[:, 2]

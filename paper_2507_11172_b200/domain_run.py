@@ -370,7 +370,14 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
                                       int(dims[d])) for d in range(3)]
     dec = Decomposition(box, r_build, world, rank, dims, bounds)
     n_total = system.positions.shape[0]
-    dec.local_estimate = dec.window_count(system.positions)
+    # the whole initial state once to the device; ownership and the window
+    # population from device cell maps (domain.cells_of_t)
+    dev0 = torch.device(device) if device is not None else (
+        torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+        else torch.device("cpu"))
+    pos_all = torch.as_tensor(np.ascontiguousarray(system.positions, dtype=np.float64),
+                              device=dev0)
+    dec.local_estimate = dec.window_count_t(pos_all)
     backend = backend_factory(dec, n_total, r_build)
     dev = backend.device if device is None else device
     ex = Exchanger(dist, dev)
@@ -379,11 +386,13 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     half_dt, half_drift, half_respa = 0.5 * dt / m, 0.5 * dt * dt / m, 0.5 * dt * s / m
     box_t = torch.as_tensor(box, device=dev)
 
-    mine = np.nonzero(dec.owner_rank(np.asarray(system.positions)) == rank)[0]
-    to_t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)  # noqa: E731
-    st = DomainState(ids=torch.as_tensor(mine.astype(np.float64), device=dev),
-                     x=to_t(system.positions[mine]), v=to_t(system.velocities[mine]),
-                     f2=None, f3=None, x_ref=None)
+    pos_all = pos_all.to(dev)
+    mine = torch.nonzero(dec.owner_rank_t(pos_all) == rank).reshape(-1)
+    vel_all = torch.as_tensor(np.ascontiguousarray(system.velocities, dtype=np.float64),
+                              device=dev)
+    st = DomainState(ids=mine.to(torch.float64), x=pos_all[mine].contiguous(),
+                     v=vel_all[mine].contiguous(), f2=None, f3=None, x_ref=None)
+    del pos_all, vel_all
     window = dec.window()
     trace = RunTrace()
 
@@ -678,20 +687,34 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
             # by the collective check, so they count as clean)
             backend.close(dist if clean else None)
 
-    # gather the owned state of every rank into the host system (by id)
-    parts = [None] * world
-    payload = torch.cat([st.ids[:, None], st.x, st.v, st.f2, st.f3], dim=1).cpu()
-    dist.all_gather_object(parts, payload.numpy())
-    allp = np.concatenate(parts, axis=0)
-    ids = allp[:, 0].astype(np.int64)
-    if ids.shape[0] != n_total or np.unique(ids).shape[0] != n_total:
+    # gather the owned state of every rank into the host system (by id): one
+    # tensor all_gather of the padded payloads (id -1 pads), placed by id on
+    # the device, then one copy per array to the host
+    payload = torch.cat([st.ids[:, None], st.x, st.v, st.f2, st.f3], dim=1)
+    cnt = torch.tensor([payload.shape[0]], dtype=torch.int64, device=wire)
+    dist.all_reduce(cnt, op=dist.ReduceOp.MAX)
+    padded = torch.full((int(cnt.item()), payload.shape[1]), -1.0, dtype=torch.float64,
+                        device=payload.device)
+    padded[: payload.shape[0]] = payload
+    padded = padded.to(wire)
+    parts = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(parts, padded)
+    allp = torch.cat(parts, dim=0).to(dev)
+    allp = allp[allp[:, 0] >= 0.0]
+    ids = allp[:, 0].to(torch.int64)
+    seen = torch.zeros(n_total, dtype=torch.int64, device=dev)
+    seen.index_add_(0, ids.clamp(0, n_total - 1), torch.ones_like(ids))
+    if ids.shape[0] != n_total or not bool(torch.all(seen == 1)):
         raise RuntimeError("particles lost or duplicated by the decomposition")
-    order = np.argsort(ids)
-    allp = allp[order]
-    system.positions[:] = allp[:, 1:4]
-    system.velocities[:] = allp[:, 4:7]
-    system.forces_2b[:] = allp[:, 7:10]
-    system.forces_3b[:] = allp[:, 10:13]
+    out = torch.empty((n_total, payload.shape[1] - 1), dtype=torch.float64, device=dev)
+    out[ids] = allp[:, 1:]
+    out = out.cpu()
+    from .integrators import _host_copy
+
+    _host_copy(system.positions, out[:, 0:3].contiguous())
+    _host_copy(system.velocities, out[:, 3:6].contiguous())
+    _host_copy(system.forces_2b, out[:, 6:9].contiguous())
+    _host_copy(system.forces_3b, out[:, 9:12].contiguous())
     return trace
 
 

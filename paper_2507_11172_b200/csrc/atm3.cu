@@ -203,7 +203,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     if (m < 0) return;
     // the fast instance (standard case, 64 slots) takes only bases without a
     // slot under the guard distance: the others go to the second launch
-    constexpr bool kFast = !kExactImage && !kOwned && kM == 64;
+    constexpr bool kFast = !kExactImage && kM == 64;
     if (kFast && slot_bad) {
         if (lane == 0) ovf[2 + atomicAdd(ovf, 1)] = (int32_t)r;
         return;
@@ -217,7 +217,9 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     const int dm = debug_mode & 15;
     if (dm != 1 && !(dm == 2 && m >= 32) && !(dm == 3 && m < 32)) {
         if constexpr (kFast) {
-            a3_rot(sm, m, lane, g, pr, cut, acc);  // register-resident rounds (atm_rot.cuh)
+            // register-resident rounds (atm_rot.cuh); decomposed runs also sum
+            // each slot's triplet energies for the owned shares
+            a3_rot<kOwned>(sm, m, lane, g, pr, cut, acc);
         } else if (slot_bad) {
             a3_windows<kExactImage, kOwned, true>(sm, m, slots, lane, g, pr, cut, acc, F);
         } else {
@@ -234,7 +236,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     // -1/4.5 of it (atm_scalars).  Decomposed runs weight each triplet by its
     // owned share, and under four cutoffs d_jk is its own image: both keep
     // the per-triplet sums.
-    double sx = 0.0, sy = 0.0, sz = 0.0, sw = 0.0;
+    double sx = 0.0, sy = 0.0, sz = 0.0, sw = 0.0, so = 0.0;
     for (int sl = lane; sl < m; sl += 32) {
         double ax = F[0], ay = F[1], az = F[2];  // m < 32: the lane's register sums
         if (kFast || m >= 32) {
@@ -257,12 +259,23 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
             ld_rec(sm, sl, dx, dy, dz, r2);
             sw = fma(dx, ax, fma(dy, ay, fma(dz, az, sw)));
         }
+        // owned members' shares of the slot's triplet energies
+        if (kFast && kOwned && (sm.kidx[sl] >> 30)) so += sm.ae[sl];
     }
     const double fx = -group_sum<32>(sx);
     const double fy = -group_sum<32>(sy);
     const double fz = -group_sum<32>(sz);
-    const double w = group_sum<32>(kOwned || kExactImage ? acc.w : sw);
-    const double e = kOwned || kExactImage ? group_sum<32>(acc.e) : w * (-1.0 / 4.5);
+    double w, e;
+    if (kFast && kOwned) {
+        // share (o_i + o_j + o_k)/3 per triplet: (o_i/3) sum_t E_t + (1/3) sum_s
+        // o_s E_s, E_s the energy of slot s's triplets; the virial per
+        // triplet is -9/2 E (Euler: E is homogeneous of degree -9/2)
+        e = (acc.owned_i * group_sum<32>(acc.e) + group_sum<32>(so)) * (1.0 / 3.0);
+        w = -4.5 * e;
+    } else {
+        w = group_sum<32>(kOwned || kExactImage ? acc.w : sw);
+        e = kOwned || kExactImage ? group_sum<32>(acc.e) : w * (-1.0 / 4.5);
+    }
     const int nt = group_sum_int<32>(acc.n);
     const bool bad = __any_sync(0xffffffffu, acc.bad);
     if (lane == 0) {
@@ -518,7 +531,7 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
     // the standard case runs the fast instance (64 slots, register-resident
     // rounds) and always lists bases beyond it -- S+ over 64 slots, or a slot
     // under the guard distance -- for the second launch
-    constexpr bool kStd = !kExactImage && !kOwned;
+    constexpr bool kStd = !kExactImage;
     if (kStd) fast = std::min(64, full);
     const size_t per = a3_warp_bytes(kStd ? 64 : fast);
     const int warps = a3_warps_for(per);

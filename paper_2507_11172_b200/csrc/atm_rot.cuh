@@ -82,10 +82,11 @@ __device__ __forceinline__ bool rot_exact_in(const A3Smem &sm, int s, int t, con
 
 // f_j, f_k (units of 2 nu) of the pair with D_j = (sx, sy, sz), a = r_ij^2,
 // D_k = (tx, ty, tz), b = r_ik^2, scaled to zero unless `in`.
+template <bool kE>
 __device__ __forceinline__ void rot_eval(bool in, double sx, double sy, double sz, double a,
                                          double tx, double ty, double tz, double b, double jkx,
                                          double jky, double jkz, double c, double fj[3],
-                                         double fk[3]) {
+                                         double fk[3], double &e) {
     // atm_scalars with the common factor s^-5/2 selected (every E_x is a
     // multiple of it)
     const double tsum = a + b + c;
@@ -112,14 +113,16 @@ __device__ __forceinline__ void rot_eval(bool in, double sx, double sy, double s
     fk[0] = fma(eb, tx, cx);
     fk[1] = fma(eb, ty, cy);
     fk[2] = fma(eb, tz, cz);
+    if (kE) e = s52 * fma(0.375, p, sp);  // the triplet's energy (units of nu), 0 if rejected
 }
 
 // One pair of the fast loop: `live` lanes accept on the fp64 estimate;
 // undecided pairs contribute nothing here and set `und`.
+template <bool kE>
 __device__ __forceinline__ void rot_fast(bool live, double sx, double sy, double sz, double a,
                                          double tx, double ty, double tz, double b,
                                          const RotCut &rc, A3Acc &acc, bool &und, double fj[3],
-                                         double fk[3]) {
+                                         double fk[3], double &e) {
     const double jkx = tx - sx, jky = ty - sy, jkz = tz - sz;
     const double c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
     const int ch = __double2hiint(c);
@@ -127,15 +130,16 @@ __device__ __forceinline__ void rot_fast(bool live, double sx, double sy, double
     und = live && !inr && ch <= rc.hi_hi;
     const bool in = live && inr;
     acc.n += in ? 1 : 0;
-    rot_eval(in, sx, sy, sz, a, tx, ty, tz, b, jkx, jky, jkz, c, fj, fk);
+    rot_eval<kE>(in, sx, sy, sz, a, tx, ty, tz, b, jkx, jky, jkz, c, fj, fk, e);
 }
 
 // The fix-up pair: `live` lanes decide with the reference arithmetic.
+template <bool kE>
 __device__ __forceinline__ void rot_slow(const A3Smem &sm, bool live, int s, int t, double sx,
                                          double sy, double sz, double a, double tx, double ty,
                                          double tz, double b, const rb_grid &g,
                                          const double *__restrict__ pr, const A3Cut &cut,
-                                         A3Acc &acc, double fj[3], double fk[3]) {
+                                         A3Acc &acc, double fj[3], double fk[3], double &e) {
     const double jkx = tx - sx, jky = ty - sy, jkz = tz - sz;
     const double c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
     bool bad = false;
@@ -143,15 +147,16 @@ __device__ __forceinline__ void rot_slow(const A3Smem &sm, bool live, int s, int
     acc.bad = acc.bad || bad;
     in = in && !bad;
     acc.n += in ? 1 : 0;
-    rot_eval(in, sx, sy, sz, a, tx, ty, tz, b, jkx, jky, jkz, c, fj, fk);
+    rot_eval<kE>(in, sx, sy, sz, a, tx, ty, tz, b, jkx, jky, jkz, c, fj, fk, e);
 }
 
 // Rotation rounds over slots [off, off + gm) on lanes 0 .. gm-1 (2 <= gm <=
 // 32); lanes >= gm mirror lane (lane mod gm) and contribute nothing.  Adds
 // each slot's sum to F of its lane.
+template <bool kE>
 __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, int lane,
                                            const rb_grid &g, const double *__restrict__ pr,
-                                           const A3Cut &cut, A3Acc &acc, double F[3]) {
+                                           const A3Cut &cut, A3Acc &acc, double F[4]) {
     constexpr unsigned kAll = 0xffffffffu;
     const bool mine = lane < gm;
     const int s = mine ? lane : lane % gm;
@@ -176,7 +181,8 @@ __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, in
         double tx, ty, tz, b;
         lds_rec(xy0 + toff, zr0 + toff, tx, ty, tz, b);  // conflict-free: a rotation
         bool u;
-        rot_fast(d <= lim, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, fj, fk);
+        double e = 0.0;
+        rot_fast<kE>(d <= lim, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, fj, fk, e);
         und |= u ? 1u << d : 0u;
         F[0] += fj[0];
         F[1] += fj[1];
@@ -184,6 +190,11 @@ __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, in
         F[0] += __shfl_sync(kAll, fk[0], src);  // zero from a rejected pair
         F[1] += __shfl_sync(kAll, fk[1], src);
         F[2] += __shfl_sync(kAll, fk[2], src);
+        if (kE) {  // the slot energy sums of both members, the base's sum
+            acc.e += e;
+            F[3] += e;
+            F[3] += __shfl_sync(kAll, e, src);
+        }
         toff += 16u;
         toff = toff == end ? 0u : toff;
         src = src == 0 ? gm - 1 : src - 1;
@@ -197,30 +208,37 @@ __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, in
             const int sr = (s - d + gm) % gm;
             double tx, ty, tz, b;
             lds_rec(xy0 + 16 * t, zr0 + 16 * t, tx, ty, tz, b);
-            rot_slow(sm, mysus, off + s, off + t, sx, sy, sz, a, tx, ty, tz, b, g, pr, cut, acc,
-                     fj, fk);
+            double e = 0.0;
+            rot_slow<kE>(sm, mysus, off + s, off + t, sx, sy, sz, a, tx, ty, tz, b, g, pr, cut,
+                         acc, fj, fk, e);
             F[0] += fj[0];
             F[1] += fj[1];
             F[2] += fj[2];
             F[0] += __shfl_sync(kAll, fk[0], sr);
             F[1] += __shfl_sync(kAll, fk[1], sr);
             F[2] += __shfl_sync(kAll, fk[2], sr);
+            if (kE) {
+                acc.e += e;
+                F[3] += e;
+                F[3] += __shfl_sync(kAll, e, sr);
+            }
         }
     }
 }
 
 // Cross rounds A x B (m > 32): adds the A sums to F (lane = A slot) and
 // leaves the B sums (lane = B slot, lanes < mb) in G.
+template <bool kE>
 __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, const rb_grid &g,
                                           const double *__restrict__ pr, const A3Cut &cut,
-                                          A3Acc &acc, double F[3], double G[3]) {
+                                          A3Acc &acc, double F[4], double G[4]) {
     constexpr unsigned kAll = 0xffffffffu;
     const int mb = m - 32;
     const unsigned xy0 = smem_u32(sm.xy), zr0 = smem_u32(sm.zr);
     double sx, sy, sz, a;
     lds_rec(xy0 + 16 * lane, zr0 + 16 * lane, sx, sy, sz, a);
     const RotCut rc = rot_cut(cut);
-    double R[3] = {0.0, 0.0, 0.0};
+    double R[4] = {0.0, 0.0, 0.0, 0.0};
     double fj[3], fk[3];
     const unsigned bbeg = 16u * 32u, bend = 16u * (unsigned)m;
     unsigned boff = bbeg + 16u * (unsigned)(lane % mb);  // B slot (lane + e) mod mb
@@ -232,7 +250,8 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
         double tx, ty, tz, b;
         lds_rec(xy0 + boff, zr0 + boff, tx, ty, tz, b);
         bool u;
-        rot_fast(true, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, fj, fk);
+        double en = 0.0;
+        rot_fast<kE>(true, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, fj, fk, en);
         und |= u ? 1u << e : 0u;
         F[0] += fj[0];
         F[1] += fj[1];
@@ -240,16 +259,23 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
         R[0] += fk[0];
         R[1] += fk[1];
         R[2] += fk[2];
+        if (kE) {
+            acc.e += en;
+            F[3] += en;
+            R[3] += en;
+        }
         if (lane == 0) {  // the stream of B slot e leaves the warp
             asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ret0 + 16u * e), "d"(R[0]),
                          "d"(R[1]));
             asm volatile("st.shared.f64 [%0], %1;" ::"r"(retz0 + 8u * e), "d"(R[2]));
+            if (kE) sm.ae[32 + e] = R[3];
         }
         // every stream moves one lane down; lane 31 starts the next one
         R[0] = __shfl_down_sync(kAll, R[0], 1);
         R[1] = __shfl_down_sync(kAll, R[1], 1);
         R[2] = __shfl_down_sync(kAll, R[2], 1);
-        if (lane == 31) R[0] = R[1] = R[2] = 0.0;
+        if (kE) R[3] = __shfl_down_sync(kAll, R[3], 1);
+        if (lane == 31) R[0] = R[1] = R[2] = R[3] = 0.0;
         boff += 16u;
         boff = boff == bend ? bbeg : boff;
     }
@@ -258,6 +284,7 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
     // = l mod mb (after the last shift)
     sm.axy[lane] = make_double2(R[0], R[1]);
     sm.az[lane] = R[2];
+    if (kE) sm.ae[lane] = R[3];
     if (__any_sync(kAll, und != 0)) {  // fix-up (rare): lane by lane, in order
 #pragma unroll 1
         for (int e = 0; e < mb; e++) {
@@ -269,29 +296,37 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
                     const int bslot = 32 + (lane + e) % mb;
                     double tx, ty, tz, b;
                     lds_rec(xy0 + 16 * bslot, zr0 + 16 * bslot, tx, ty, tz, b);
-                    rot_slow(sm, true, lane, bslot, sx, sy, sz, a, tx, ty, tz, b, g, pr, cut, acc,
-                             fj, fk);
+                    double en = 0.0;
+                    rot_slow<kE>(sm, true, lane, bslot, sx, sy, sz, a, tx, ty, tz, b, g, pr, cut,
+                                 acc, fj, fk, en);
                     F[0] += fj[0];
                     F[1] += fj[1];
                     F[2] += fj[2];
                     acc_add(sm, bslot, fk[0], fk[1], fk[2]);
+                    if (kE) {
+                        acc.e += en;
+                        F[3] += en;
+                        sm.ae[bslot] += en;
+                    }
                 }
                 __syncwarp();
             }
         }
     }
     __syncwarp();
-    G[0] = G[1] = G[2] = 0.0;
+    G[0] = G[1] = G[2] = G[3] = 0.0;
     if (lane < mb) {
         const double2 r = sm.axy[32 + lane];
         G[0] = r.x;
         G[1] = r.y;
         G[2] = sm.az[32 + lane];
+        if (kE) G[3] = sm.ae[32 + lane];
         for (int l = lane; l < 31; l += mb) {  // in lane order
             const double2 q = sm.axy[l];
             G[0] += q.x;
             G[1] += q.y;
             G[2] += sm.az[l];
+            if (kE) G[3] += sm.ae[l];
         }
     }
     __syncwarp();
@@ -299,30 +334,34 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
 
 // Phase 1 for m <= 64 slots: the slot sums (units of 2 nu) end in the shared
 // accumulators sm.axy / sm.az (phase 3 reads them).
+template <bool kE>
 __device__ __forceinline__ void a3_rot(const A3Smem &sm, int m, int lane, const rb_grid &g,
                                        const double *__restrict__ pr, const A3Cut &cut,
                                        A3Acc &acc) {
-    double F[3] = {0.0, 0.0, 0.0};
+    double F[4] = {0.0, 0.0, 0.0, 0.0};
     int off = 0, gm = m < 32 ? m : 32;
     // group A (or all of a short S+), then the cross rounds, then group B
     // through the same loop
 #pragma unroll 1
     for (int grp = 0;; grp++) {
-        if (gm >= 2) rot_rounds(sm, off, gm, lane, g, pr, cut, acc, F);
+        if (gm >= 2) rot_rounds<kE>(sm, off, gm, lane, g, pr, cut, acc, F);
         if (grp == 1 || m <= 32) break;
-        double G[3];
-        rot_cross(sm, m, lane, g, pr, cut, acc, F, G);
+        double G[4];
+        rot_cross<kE>(sm, m, lane, g, pr, cut, acc, F, G);
         sm.axy[lane] = make_double2(F[0], F[1]);  // the A sums are complete
         sm.az[lane] = F[2];
+        if (kE) sm.ae[lane] = F[3];
         F[0] = G[0];
         F[1] = G[1];
         F[2] = G[2];
+        F[3] = G[3];
         off = 32;
         gm = m - 32;
     }
     if (lane < gm) {  // (a group may have fewer than 32 slots)
         sm.axy[off + lane] = make_double2(F[0], F[1]);
         sm.az[off + lane] = F[2];
+        if (kE) sm.ae[off + lane] = F[3];
     }
     __syncwarp();
 }

@@ -668,6 +668,16 @@ def trajectory_rate(pkg, cfg, steps, flush):
             "note": f"{steps}-step trajectory timed whole (rebuild steps included)"}
 
 
+def atm_traffic(name):
+    """DRAM bytes (read + write) per launch of the ATM kernel at a config, from
+    the committed `ncu --set full` capture (profiles/atm_traffic_<cfg>.json)."""
+    prof = os.path.join(REPO, "profiles", f"atm_traffic_{name}.json")
+    try:
+        return json.load(open(prof)).get("bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
 def roofline_obj(kt, traffic):
     triplets_per_s = kt["unique"] / (kt["atm_ms"] * 1e-3)
     achieved = triplets_per_s * FLOPS_PER_TRIPLET / 1e12
@@ -703,13 +713,7 @@ def ours_arm(args, cfg):
     loop, run = device_loop(pkg, cfg, K, W, flush, local)
     kt = kernel_timings(run, flush)
     hbm = hbm_timings(run, flush)
-    traffic = None
-    prof = os.path.join(REPO, "profiles", f"atm_traffic_{cfg.name}.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("bytes_per_launch")
-        except (OSError, ValueError):
-            traffic = None
+    traffic = atm_traffic(cfg.name)
     del run
     e2e = e2e_rate(pkg, cfg, K)
     secondary = None
@@ -723,7 +727,7 @@ def ours_arm(args, cfg):
             "ms_per_step": loop2["ms_per_step"], "rebuild_steps": loop2["rebuilds"],
             "trajectory_100": trajectory_rate(pkg, c2, 100, flush),
             "e2e": e2e_rate(pkg, c2, 20),
-            "roofline": roofline_obj(kt2, None),
+            "roofline": roofline_obj(kt2, atm_traffic("cfg2")),
             "note": "BASELINE.json configs[1] (32,000 particles) on one GPU; value as the "
                     "headline (device-timed steps); trajectory_100 = its 100-step run timed whole",
         }

@@ -1,6 +1,7 @@
 // atm_rot.cuh -- register-resident slot-pair rounds of the Newton-3 ATM pass
-// for S+(i) of up to 64 slots (periodic boxes of at least four cutoffs,
-// undecomposed runs: the hot instantiation of k_atm3).
+// for S+(i) of up to 64 slots (boxes of at least four cutoffs: the hot
+// 64-slot instance of k_atm3, undecomposed and -- with kE, the per-slot
+// energy sums behind the owned shares -- decomposed runs).
 //
 // Every slot's force sum lives in a register of the lane that holds the slot
 // (lane l holds slot l, and slot 32 + l when m > 32), so the pair loop moves
@@ -34,6 +35,11 @@
 // each fix-up): the kernel's instruction footprint stays small (a warp in
 // phase 0, one in the rotation loop and one in the cross loop share the SM's
 // instruction cache).
+//
+// kE (decomposed runs): every pair also yields its energy E_t; a lane sums
+// the energies of its slot's triplets (j role in the lane, k role by the same
+// shuffle / stream as f_k) and of the pairs it evaluated (the base's sum), so
+// k_atm3 weights them by owned shares, (o_i sum_t E_t + sum_s o_s E_s) / 3.
 #pragma once
 
 #include "atm_core.cuh"

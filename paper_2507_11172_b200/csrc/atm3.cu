@@ -69,9 +69,10 @@ __device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image
                                         int32_t slots, double rc2, double *__restrict__ gbuf,
                                         const uint8_t *__restrict__ owned,
                                         unsigned long long *status, int64_t tag, int32_t *ovf,
-                                        bool &slot_bad) {
+                                        bool &slot_bad, int32_t *split_out) {
     const int lane = threadIdx.x & 31;
     int m = 0;
+    int below = 0;  // row entries of rank < r from `first` on (the prefix ends inside them)
     slot_bad = false;
     // (warp-uniform: a base a cutoff away from the periodic faces needs no
     // minimum image, common.cuh image_free)
@@ -127,6 +128,7 @@ __device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image
                     gq[1] = make_double2(0.0, 0.0);
                 }
             }
+            below += __popc(__ballot_sync(0xffffffffu, k < rc_n && q >= 0 && q < r));
             const unsigned mk = __ballot_sync(0xffffffffu, keep);
             if (m + __popc(mk) > slots) {  // S+(i) does not fit the shared-memory slots
                 if (lane == 0) {
@@ -152,6 +154,9 @@ __device__ __forceinline__ int a3_slots(int64_t r, const A3Smem &sm, const Image
             slot_bad |= __any_sync(0xffffffffu, keep && r2 < RB_MIN_DISTANCE_SQ);
         }
     }
+    // the row prefix of ranks below r: the entries whose bases may write
+    // G[r][k] (the gather reads exactly these)
+    if (lane == 0 && split_out) *split_out = first + below;
     __syncwarp();
     return m;
 }
@@ -173,7 +178,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
                                        int32_t *__restrict__ triplets_rank,
                                        const uint8_t *__restrict__ owned,
                                        unsigned long long *status, int64_t tag, int debug_mode,
-                                       int32_t *ovf) {
+                                       int32_t *ovf, int32_t *__restrict__ splits) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int32_t *row = rows + r * (int64_t)capacity;
@@ -199,7 +204,7 @@ __device__ __forceinline__ void a3_base(int64_t r, char *smem_raw, const rb_grid
     bool slot_bad = false;
     const int m = a3_slots<kOwned>(r, sm, im, xi, yi, zi, rc_n, chunk_first, pr,
                                    row, mir, capacity, slots, cut.rc2, gbuf, owned, status, tag,
-                                   ovf, slot_bad);
+                                   ovf, slot_bad, splits + r);
     if (m < 0) return;
     // the fast instance (standard case, 64 slots) takes only bases without a
     // slot under the guard distance: the others go to the second launch
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
            unsigned long long *status, int64_t tag, int debug_mode, int32_t *ovf,
-           int32_t *work) {
+           int32_t *work, int32_t *splits) {
     pdl_enter();
     extern __shared__ __align__(16) char smem_raw[];
     if (!work) {  // one base per warp
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
         a3_base<kExactImage, kOwned, kM>(r, smem_raw, g, n, pr, rows, row_count, mirror,
                                          capacity, slots, cut, own, gbuf,
                                          energy_rank, virial_rank, triplets_rank, owned, status,
-                                         tag, debug_mode, ovf);
+                                         tag, debug_mode, ovf, splits);
         return;
     }
     // persistent warps: the next base comes from a global counter (reset by
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(kA3Warps * 32, kA3MinBlocks)
         a3_base<kExactImage, kOwned, kM>(r, smem_raw, g, n, pr, rows, row_count, mirror, capacity,
                                          slots, cut, own, gbuf, energy_rank,
                                          virial_rank, triplets_rank, owned, status, tag,
-                                         debug_mode, ovf);
+                                         debug_mode, ovf, splits);
         __syncwarp();  // the warp's slots are reused by its next base
         r = __shfl_sync(0xffffffffu, nxt, 0);
     }
@@ -338,7 +343,8 @@ __global__ void __launch_bounds__(kA3Warps * 32)
            double *__restrict__ own, double *__restrict__ gbuf,
            double *__restrict__ energy_rank, double *__restrict__ virial_rank,
            int32_t *__restrict__ triplets_rank, const uint8_t *__restrict__ owned,
-           unsigned long long *status, int64_t tag, int debug_mode, const int32_t *ovf) {
+           unsigned long long *status, int64_t tag, int debug_mode, const int32_t *ovf,
+           int32_t *splits) {
     pdl_enter();
     extern __shared__ __align__(16) char smem_raw[];
     const int wpb = blockDim.x >> 5;
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(kA3Warps * 32)
         a3_base<kExactImage, kOwned, 0>(ovf[2 + q], smem_raw, g, n, pr, rows, row_count, mirror,
                                         capacity, slots, cut,
                                         own, gbuf, energy_rank, virial_rank, triplets_rank,
-                                        owned, status, tag, debug_mode, nullptr);
+                                        owned, status, tag, debug_mode, nullptr, splits);
         __syncwarp();  // the warp's slots are reused by its next base
     }
 }
@@ -357,12 +363,9 @@ __global__ void __launch_bounds__(kA3Warps * 32)
 // G[p][k]); the row prefix is walked in order by kG lanes, then a fixed xor
 // tree.
 constexpr int kGatherGroup = 8;
-constexpr int kGatherRegs = 6;  // prefix entries per lane loaded at once
 
 __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
-                              const int32_t *__restrict__ rows,
-                              const int32_t *__restrict__ row_count,
-                              const int32_t *__restrict__ mirror, int32_t capacity,
+                              const int32_t *__restrict__ splits, int32_t capacity,
                               const double *__restrict__ own, const double *__restrict__ gbuf,
                               const double *__restrict__ e_s, const double *__restrict__ w_s,
                               const int32_t *__restrict__ n_s, double two_nu, double nu,
@@ -384,34 +387,13 @@ __global__ void k_atm3_gather(int64_t n, const int32_t *__restrict__ parts,
     if (warp_frozen(status, tag, RB_KIND_TRIPLET_MIN_SEPARATION)) return;
     double fx = 0.0, fy = 0.0, fz = 0.0;
     if (active) {
-        const int m = row_count[p];
-        const int32_t *row = rows + p * (int64_t)capacity;
+        // the row prefix of ranks below p (its base recorded the length,
+        // a3_slots): exactly the entries G[p][k] its bases wrote, summed in
+        // row order by kGatherGroup lanes; no row indices are read
+        const int sp = splits[p];
+        RB_CHECK(sp >= 0 && sp <= capacity);
         const double2 *gp = (const double2 *)(gbuf + p * (int64_t)capacity * kGStride);
-        // rows are rank-sorted: the prefix q < p holds the partials.  The
-        // first kGatherRegs entries of the lane are loaded together (index
-        // and partial), then summed in row order; longer prefixes continue
-        int k = sub;
-        bool more = true;
-#pragma unroll
-        for (int u = 0; u < kGatherRegs; u++, k += kGatherGroup) {
-            const bool in = more && k < m && __ldg(row + k) < p;
-            double gx = 0.0, gy = 0.0, gz = 0.0;
-            if (k < m) {  // loads independent of the row test: issued together
-                const double2 xy = gp[2 * k];
-                gx = xy.x;
-                gy = xy.y;
-                gz = gp[2 * k + 1].x;
-            }
-            if (in) {
-                fx += gx;
-                fy += gy;
-                fz += gz;
-            }
-            more = in;
-        }
-        RB_CHECK(m >= 0 && m <= capacity);
-        for (; more && k < m; k += kGatherGroup) {
-            if (row[k] >= p) break;
+        for (int k = sub; k < sp; k += kGatherGroup) {
             const double2 xy = gp[2 * k];
             fx += xy.x;
             fy += xy.y;
@@ -456,8 +438,9 @@ extern "C" size_t rb_atm_scratch_bytes(int64_t n, int32_t capacity) {
     // kernels may run concurrently with the pair pass -- then G
     // (n x capacity x 4: 32-byte entries, aligned) doubles
     const size_t nn = (size_t)(n > 0 ? n : 1);
-    return a3_header_bytes(nn) + nn * 5 * sizeof(double) + ((nn * sizeof(int32_t) + 7) & ~(size_t)7) +
-           32 + nn * kGStride * sizeof(double) * (size_t)capacity;
+    return a3_header_bytes(nn) + nn * 5 * sizeof(double) +
+           2 * ((nn * sizeof(int32_t) + 7) & ~(size_t)7) + 32 +
+           nn * kGStride * sizeof(double) * (size_t)capacity;
 }
 
 namespace rb {
@@ -488,7 +471,7 @@ static void a3_launch_main(cudaStream_t st, int64_t n, int warps, size_t per, co
                            const int32_t *mirror, int32_t capacity, int fast, const A3Cut &cut, double *own, double *gbuf,
                            double *energy_rank, double *virial_rank, int32_t *triplets_rank,
                            const uint8_t *owned, unsigned long long *status, int64_t tag,
-                           int debug_mode, int32_t *ovf, int32_t *work) {
+                           int debug_mode, int32_t *ovf, int32_t *work, int32_t *splits) {
     static size_t granted = 0;
     static int resident = 0;  // co-resident blocks per SM at this shared-memory size
     static const int64_t persist_min =
@@ -516,7 +499,7 @@ static void a3_launch_main(cudaStream_t st, int64_t n, int warps, size_t per, co
     launch(kern, dim3((unsigned)blocks), dim3(warps * 32),
            warps * per, st, g, n, pos_r, rows, row_count, mirror, capacity, fast, cut,
            own, gbuf, energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
-           ovf, work);
+           ovf, work, splits);
     note_launches(1);
 }
 
@@ -526,7 +509,7 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
                       int32_t capacity, int fast, int full, const A3Cut &cut,
                       double *own, double *gbuf, double *energy_rank, double *virial_rank,
                       int32_t *triplets_rank, const uint8_t *owned, unsigned long long *status,
-                      int64_t tag, int debug_mode, int32_t *ovf, int32_t *work) {
+                      int64_t tag, int debug_mode, int32_t *ovf, int32_t *work, int32_t *splits) {
     static size_t granted_ovf = 0;
     // the standard case runs the fast instance (64 slots, register-resident
     // rounds) and always lists bases beyond it -- S+ over 64 slots, or a slot
@@ -542,22 +525,26 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
         a3_launch_main<kExactImage, kOwned, 64>(st, n, warps, per, g, pos_r, rows, row_count,
                                                 mirror, capacity, 64, cut, own,
                                                 gbuf, energy_rank, virial_rank, triplets_rank,
-                                                owned, status, tag, debug_mode, list, work);
+                                                owned, status, tag, debug_mode, list, work,
+                                                splits);
     else if (fast == 64)
         a3_launch_main<kExactImage, kOwned, 64>(st, n, warps, per, g, pos_r, rows, row_count,
                                                 mirror, capacity, fast, cut, own,
                                                 gbuf, energy_rank, virial_rank, triplets_rank,
-                                                owned, status, tag, debug_mode, list, work);
+                                                owned, status, tag, debug_mode, list, work,
+                                                splits);
     else if (fast == 96)
         a3_launch_main<kExactImage, kOwned, 96>(st, n, warps, per, g, pos_r, rows, row_count,
                                                 mirror, capacity, fast, cut, own,
                                                 gbuf, energy_rank, virial_rank, triplets_rank,
-                                                owned, status, tag, debug_mode, list, work);
+                                                owned, status, tag, debug_mode, list, work,
+                                                splits);
     else
         a3_launch_main<kExactImage, kOwned, 0>(st, n, warps, per, g, pos_r, rows, row_count,
                                                mirror, capacity, fast, cut, own,
                                                gbuf, energy_rank, virial_rank, triplets_rank,
-                                               owned, status, tag, debug_mode, list, work);
+                                               owned, status, tag, debug_mode, list, work,
+                                               splits);
     if (!split) return;
     const size_t per_full = a3_warp_bytes(full);
     const int wf = a3_warps_for(per_full);
@@ -567,7 +554,7 @@ static void a3_launch(cudaStream_t st, const rb_grid &g, int64_t n, const double
     launch(k_atm3_overflow<kExactImage, kOwned>, dim3(blocks), dim3(wf * 32), wf * per_full, st,
            g, n, pos_r, rows, row_count, mirror, capacity, full, cut, own, gbuf,
            energy_rank, virial_rank, triplets_rank, owned, status, tag, debug_mode,
-           (const int32_t *)ovf);
+           (const int32_t *)ovf, splits);
     note_launches(1);
 }
 }  // namespace rb
@@ -602,7 +589,9 @@ extern "C" int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r
     double *own = (double *)((char *)scratch + a3_header_bytes((size_t)n));
     double *e_s = own + 3 * n, *w_s = e_s + n;
     int32_t *n_s = (int32_t *)(w_s + n);
-    double *gbuf = (double *)((char *)n_s + (((size_t)n * sizeof(int32_t) + 7) & ~(size_t)7));
+    // the row prefix length of every base (a3_slots), read by the gather
+    int32_t *splits = (int32_t *)((char *)n_s + (((size_t)n * sizeof(int32_t) + 7) & ~(size_t)7));
+    double *gbuf = (double *)((char *)splits + (((size_t)n * sizeof(int32_t) + 7) & ~(size_t)7));
     gbuf = (double *)(((uintptr_t)gbuf + 31) & ~(uintptr_t)31);  // whole 32-byte sectors
     auto hiword = [](double x) {
         int64_t b;
@@ -619,7 +608,7 @@ extern "C" int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r
     auto go = [&](auto exact, auto with_owned) {
         a3_launch<decltype(exact)::value, decltype(with_owned)::value>(
             st, *g, n, pos_r, rows, row_count, mirror, capacity, fast, slot_capacity, cut,
-            own, gbuf, e_s, w_s, n_s, owned, status, tag, debug_mode, ovf, work);
+            own, gbuf, e_s, w_s, n_s, owned, status, tag, debug_mode, ovf, work, splits);
     };
     using T = std::true_type;
     using F = std::false_type;
@@ -632,7 +621,7 @@ extern "C" int rb_atm_pass_part(const rb_grid *g, int64_t n, const double *pos_r
     if (part == 1) return launch_status();
     const int tb = 256;
     const int64_t threads = n * kGatherGroup;
-    launch(k_atm3_gather, dim3((unsigned)((threads + tb - 1) / tb)), dim3(tb), 0, st, n, cell_particles, rows, row_count, mirror, capacity, own, gbuf, e_s, w_s, n_s, 2.0 * nu, nu, forces,
+    launch(k_atm3_gather, dim3((unsigned)((threads + tb - 1) / tb)), dim3(tb), 0, st, n, cell_particles, splits, capacity, own, gbuf, e_s, w_s, n_s, 2.0 * nu, nu, forces,
         energy_rank, virial_rank, triplets_rank, status, tag, ovf);
     note_launches(1);
     return launch_status();

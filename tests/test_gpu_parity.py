@@ -764,3 +764,59 @@ def test_domain_speculative_windows_match_per_step_votes(pkg, tmp_path):
     tr = pkg.respa_run(ref, ff, pkg.CudaLinkedCells(), pkg.RespaSchedule(0.002, 5, 60))
     assert np.max(np.abs(a["x"] - ref.positions)) <= 1e-10
     assert max(_rel(x, y) for x, y in zip(a["total"], tr.total)) <= 1e-10
+
+
+def _domain_blowup_worker(rank, world, port, out_dir, window):
+    import os as _os
+
+    import torch.distributed as dist
+
+    _os.environ["MASTER_ADDR"] = "127.0.0.1"
+    _os.environ["MASTER_PORT"] = str(port)
+    _os.environ["RB_DOMAIN_WINDOW"] = str(window)
+    import torch
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        import paper_2507_11172_b200 as pkg
+        from paper_2507_11172_b200.domain_run import domain_respa_run, gpu_backend_factory
+
+        sysm = pkg.systems.fcc_system(6, jitter=0.05, seed=21, temperature=1.2, vseed=22)
+        sysm.velocities[5, 1] = np.inf  # its first drift leaves the box: non-finite
+        ff = pkg.ForceField(nu=0.3, cutoff=2.5)
+        try:
+            domain_respa_run(dist, sysm, ff, pkg.RespaSchedule(0.002, 5, 40),
+                             gpu_backend_factory(ff), skin=0.1)
+            got = (-1, "")
+        except pkg.IntegrationBlowUp as exc:
+            got = (exc.iteration, str(exc))
+        with open(_os.path.join(out_dir, f"blow_{window}.txt"), "w") as f:
+            f.write(f"{got[0]}\n{got[1]}\n")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_domain_speculative_windows_report_device_errors(pkg, tmp_path):
+    """A non-finite state inside a window (the same step's skin check also
+    asks for a rebuild: the error must win) stops the windowed loop at the
+    iteration the per-step loop and the single-GPU loop report."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    got = {}
+    for window in (16, 0):
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        mp.start_processes(_domain_blowup_worker, args=(1, port, str(tmp_path), window),
+                           nprocs=1, join=True, start_method="spawn")
+        lines = (tmp_path / f"blow_{window}.txt").read_text().splitlines()
+        got[window] = int(lines[0])
+    ref = pkg.systems.fcc_system(6, jitter=0.05, seed=21, temperature=1.2, vseed=22)
+    ref.velocities[5, 1] = np.inf
+    with pytest.raises(pkg.IntegrationBlowUp) as err:
+        pkg.respa_run(ref, pkg.ForceField(nu=0.3, cutoff=2.5), pkg.CudaLinkedCells(),
+                      pkg.RespaSchedule(0.002, 5, 40))
+    assert got[16] == got[0] == err.value.iteration >= 1

@@ -337,15 +337,21 @@ def domain_arm(args, cfg):
     s = cfg.system()
     ff = cfg.force_field()
     cells = geometry(s.box, None, max(cfg.rc_lj, cfg.rc_atm) + 0.3, True).cells
-    dims = auto_dims(world, tuple(int(c) for c in cells))
+    # the inhomogeneous slab (cfg5) gets cost-balanced blocks (domain.balanced_layout:
+    # rank grid and cuts from the estimated work of the initial configuration)
+    balance = cfg.name == "cfg5"
+    dims = None if balance else auto_dims(world, tuple(int(c) for c in cells))
     K = max(sf, (int(args.steps) + sf - 1) // sf * sf)
     W = max(sf, (max(3, int(args.warmup)) + sf - 1) // sf * sf)
     L = pkg._lib.lib()
     backends = []
 
+    decs = []
+
     def factory(dec, n_total, r_build):
         b = gpu_backend_factory(ff)(dec, n_total, r_build)
         backends.append(b)
+        decs.append(dec)
         return b
 
     # one trajectory of W + K steps; steps W..W+K-1 are timed with two events
@@ -370,7 +376,7 @@ def domain_arm(args, cfg):
     run_sys = s.copy()
     with ClockSampler(local) as clocks:
         domain_respa_run(dist, run_sys, ff, pkg.RespaSchedule(cfg.dt, sf, W + K), factory,
-                         dims=dims, on_step=on_step)
+                         dims=dims, on_step=on_step, balance=balance)
     step_ms = ev0.elapsed_time(ev1)
     t = torch.tensor([step_ms, float(marks["l1"] - marks["l0"])], dtype=torch.float64,
                      device="cuda")
@@ -386,7 +392,7 @@ def domain_arm(args, cfg):
     dist.barrier()
     t0 = time.perf_counter()
     domain_respa_run(dist, e2e_sys, ff, pkg.RespaSchedule(cfg.dt, sf, K),
-                     gpu_backend_factory(ff), dims=dims)
+                     gpu_backend_factory(ff), dims=dims, balance=balance)
     torch.cuda.synchronize()
     dist.barrier()
     e2e_s = time.perf_counter() - t0
@@ -421,7 +427,8 @@ def domain_arm(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded FCC lattice + jitter, SURVEY.md §8d)",
             "config": {"workload": workload_name(cfg), "particles": s.n, "step_size_factor": sf,
-                       "parallelism": f"domain decomposition {dims} "
+                       "parallelism": f"domain decomposition {tuple(decs[0].dims) if decs else dims}"
+                                      f"{' (cost-balanced blocks)' if balance else ''} "
                                       f"({dist.get_backend()} halo exchange)",
                        "value": "whole-box steps/s (the same box at every N)",
                        "timed": "steps W..W+K of one decomposed trajectory between two CUDA "

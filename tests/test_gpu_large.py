@@ -115,3 +115,42 @@ def test_full_arrays_against_oracle(pkg, oracle_results, monkeypatch, cfg_name, 
     assert _rel(c.triplet_energy, ref["e3"]) <= ENERGY_TOL
     assert _rel(c.pair_virial, ref["w2"]) <= VIRIAL_TOL
     assert _rel(c.triplet_virial, ref["w3"]) <= VIRIAL_TOL
+
+
+@pytest.mark.skipif(os.environ.get("RB_SLOW_TESTS") != "1",
+                    reason="a 100-step 2.048 M-particle oracle run (~2-3 min of host CPU): "
+                           "RB_SLOW_TESTS=1")
+@pytest.mark.parametrize("name", ["cfg4", "cfg5"])
+def test_baseline_trajectory_matches_oracle(pkg, oracle, name):
+    """BASELINE.json configs[3] / configs[4] as specified: 100 r-RESPA steps
+    (cfg4, three-body factor 5; cfg5, factor 10, the slab) of the device loop
+    against the oracle C port's respa_run on the same initial state --
+    positions and velocities within 1e-10, every trace row's energies within
+    1e-10 relative (integrators.py:96-173)."""
+    import time
+
+    cfg = pkg.systems.CONFIGS[name]
+    steps = 100
+    s = cfg.system()
+    ff = cfg.force_field()
+    t0 = time.perf_counter()
+    tr = pkg.respa_run(s, ff, pkg.CudaLinkedCells(),
+                       pkg.RespaSchedule(cfg.dt, cfg.step_size_factor, steps))
+    t_gpu = time.perf_counter() - t0
+    oracle.set_num_threads(os.cpu_count() or 1)
+    ref0 = cfg.system()
+    b = oracle.OracleSystem.from_positions(ref0.positions, ref0.box, True, ref0.velocities)
+    off = oracle.OracleForceField(nu=ff.nu, cutoff=ff.cutoff)
+    t0 = time.perf_counter()
+    rtr = oracle.respa_run(b, off, oracle.OracleLinkedCells(), cfg.dt, cfg.step_size_factor,
+                           steps)
+    t_cpu = time.perf_counter() - t0
+    dx = float(np.max(np.abs(s.positions - b.positions)))
+    dv = float(np.max(np.abs(s.velocities - b.velocities)))
+    de = max(_rel(x, y) for x, y in zip(tr.total, rtr.total))
+    print(f"{name}: {s.n} particles, {steps} steps: max |dx| {dx:.3e}, max |dv| {dv:.3e}, "
+          f"max rel dE {de:.3e}; GPU respa_run {t_gpu:.2f} s, oracle {t_cpu:.1f} s "
+          f"({os.cpu_count()} threads)")
+    assert list(tr.iterations) == list(rtr.iterations)
+    assert dx <= 1e-10 and dv <= 1e-10
+    assert de <= 1e-10

@@ -1,3 +1,15 @@
+#!/usr/bin/env python
+"""Phase marks of the public respa_run on host arrays (bench.py's e2e leg).
+
+    python tools/e2e_marks.py cfg2 20      # config, steps per call
+
+Four calls of the same schedule: the first builds the cached run (rows
+sized, period graph captured), the second captures the initial passes'
+graph, the rest show the steady state.  Each line splits the call into its
+marks (DeviceRespa.marks): before _drive ("pre"), start (upload + initial
+passes enqueued), replays enqueued, the one synchronisation (collected),
+the host copies (downloaded).
+"""
 import sys, time, os
 sys.path.insert(0, os.getcwd())
 import torch

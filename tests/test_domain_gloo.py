@@ -186,3 +186,37 @@ def test_decomposition_geometry():
     assert owners.min() >= 0 and owners.max() < 8
     offs = w.offsets()
     assert offs.shape == (27, 3) and offs.min() == -1
+
+
+@pytest.mark.parametrize("world,dims,balanced", [(1, None, False), (2, (2, 1, 1), False),
+                                                 (8, (2, 2, 2), False), (4, (1, 1, 4), True)])
+def test_device_decomposition_maps_equal_numpy(world, dims, balanced):
+    """The rebuild's torch cell / block / owner maps and the window population
+    (domain.Decomposition.*_t, run on the payload's device) equal the numpy
+    restatement bit for bit, on positions that include the box faces, cell
+    boundaries and the wrapped coordinate 0."""
+    from paper_2507_11172_b200 import systems
+    from paper_2507_11172_b200.domain import Decomposition
+
+    s = systems.fcc_system(16, jitter=0.05, seed=3)  # 9 cells per dimension at 2.8
+    pos = s.positions.copy()
+    box = np.asarray(s.box, dtype=np.float64)
+    dec0 = Decomposition(box, 2.8, world, 0, dims)
+    n = np.asarray(dec0.geom.cells)
+    edge = np.stack([np.zeros(3), box * (1.0 - 1e-16), box / n, 2 * box / n * (1 - 1e-15)])
+    pos = np.concatenate([pos, edge], axis=0)
+    bounds = None
+    if balanced:  # uneven cuts along z
+        nz = int(n[2])
+        bounds = [[0, int(n[0])], [0, int(n[1])], [0, 2, 4, 6, nz]]
+    t = torch.as_tensor(pos)
+    for rank in range(world):
+        dec = Decomposition(box, 2.8, world, rank, dims if not balanced else (1, 1, 4), bounds)
+        cn = dec.cells_of(pos)
+        ct = dec.cells_of_t(t)
+        assert np.array_equal(cn, ct.numpy())
+        bn = dec.block_of(cn)
+        for d in range(3):
+            assert np.array_equal(bn[:, d], dec.block_coord_t(ct[:, d], d).numpy())
+        assert np.array_equal(dec.owner_rank(pos), dec.owner_rank_t(t).numpy())
+        assert dec.window_count(pos) == dec.window_count_t(t)

@@ -500,8 +500,12 @@ def domain_respa_run(dist, system, ff, schedule: RespaSchedule, backend_factory,
     # peers' publishing drifts before every rank's ghost pull.  Message
     # halos and gloo keep the per-step host vote.
     wlen = int(os.environ.get("RB_DOMAIN_WINDOW", "16"))
+    # (RB_DOMAIN_WINDOW_ANY=1: also over gloo, whose all_reduce of a CUDA
+    # tensor synchronises the stream -- slower, the same protocol; tests run
+    # ranks sharing one GPU that way)
     windowed = (fast and wlen > 1 and skin > 0.0 and
-                (world == 1 or (peer and dist.get_backend() == "nccl")))
+                (world == 1 or (peer and (dist.get_backend() == "nccl" or
+                                          os.environ.get("RB_DOMAIN_WINDOW_ANY") == "1"))))
 
     def run_windows(num, drift_args, kick_args):
         WINDOW_STATS["runs"] += 1

@@ -482,13 +482,15 @@ def _domain_system(pkg, kind):
     return pkg.systems.fcc_system(8, jitter=0.05, seed=21, temperature=1.2, vseed=22)
 
 
-def _domain_gpu_worker(rank, world, port, dims, out_dir, kind="fcc", halo="peer"):
+def _domain_gpu_worker(rank, world, port, dims, out_dir, kind="fcc", halo="peer", tag=""):
     import os as _os
 
     import torch.distributed as dist
 
     _os.environ["MASTER_ADDR"] = "127.0.0.1"
     _os.environ["MASTER_PORT"] = str(port)
+    if tag == "win":  # the speculative-window protocol over gloo (CUDA tensors)
+        _os.environ["RB_DOMAIN_WINDOW_ANY"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2507_11172_b200 as pkg
@@ -500,13 +502,17 @@ def _domain_gpu_worker(rank, world, port, dims, out_dir, kind="fcc", halo="peer"
                                  gpu_backend_factory(ff, halo=halo), skin=0.1, dims=dims,
                                  balance=kind == "slab")
         if rank == 0:
-            np.savez(_os.path.join(out_dir, f"out_{halo}.npz"), x=sysm.positions,
-                     v=sysm.velocities, total=np.array(trace.total))
+            from paper_2507_11172_b200 import domain_run
+
+            np.savez(_os.path.join(out_dir, f"out_{halo}{tag}.npz"), x=sysm.positions,
+                     v=sysm.velocities, total=np.array(trace.total),
+                     resumes=domain_run.WINDOW_STATS["resumes"],
+                     runs=domain_run.WINDOW_STATS["runs"])
     finally:
         dist.destroy_process_group()
 
 
-def _run_domain_gpu(tmp_path, world, dims, kind, halo):
+def _run_domain_gpu(tmp_path, world, dims, kind, halo, tag=""):
     import socket
 
     import torch.multiprocessing as mp
@@ -514,9 +520,10 @@ def _run_domain_gpu(tmp_path, world, dims, kind, halo):
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
-    mp.start_processes(_domain_gpu_worker, args=(world, port, dims, str(tmp_path), kind, halo),
+    mp.start_processes(_domain_gpu_worker,
+                       args=(world, port, dims, str(tmp_path), kind, halo, tag),
                        nprocs=world, join=True, start_method="spawn")
-    return np.load(tmp_path / f"out_{halo}.npz")
+    return np.load(tmp_path / f"out_{halo}{tag}.npz")
 
 
 @pytest.mark.parametrize("world,dims,kind", [(2, (2, 1, 1), "fcc"), (4, (2, 1, 2), "fcc"),
@@ -820,3 +827,16 @@ def test_domain_speculative_windows_report_device_errors(pkg, tmp_path):
         pkg.respa_run(ref, pkg.ForceField(nu=0.3, cutoff=2.5), pkg.CudaLinkedCells(),
                       pkg.RespaSchedule(0.002, 5, 40))
     assert got[16] == got[0] == err.value.iteration >= 1
+
+
+@pytest.mark.parametrize("world,dims", [(2, (2, 1, 1)), (4, (2, 1, 2))])
+def test_domain_speculative_windows_multi_rank(pkg, tmp_path, world, dims):
+    """The window protocol across ranks (device votes reduced over the ranks,
+    the freeze, one agreed decision per window, migration and ghost rebuild
+    at the frozen step, peer pulls ordered by the vote's collective) with
+    ranks sharing cuda:0 over gloo: bit-identical to the per-step votes."""
+    a = _run_domain_gpu(tmp_path, world, dims, "fcc", "peer", tag="win")
+    b = _run_domain_gpu(tmp_path, world, dims, "fcc", "peer")
+    assert int(a["runs"]) == 1 and int(a["resumes"]) >= 1 and int(b["runs"]) == 0
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["v"], b["v"])
+    assert np.array_equal(a["total"], b["total"])

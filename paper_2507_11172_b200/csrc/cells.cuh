@@ -395,6 +395,7 @@ __device__ __forceinline__ RowsSmem rows_carve(char *base, int nb_cap) {
 // dir rows of particles whose rows were not built by the staged path are
 // all kDirNone.
 constexpr int32_t kMirrorSearch = -2;
+constexpr int32_t kMirrorLower = -3;  // (rows phase) an entry of rank below the row's particle
 constexpr uint16_t kDirNone = 0xffff;
 constexpr int kDirStride = 32;  // uint16 per particle
 
@@ -581,8 +582,10 @@ __device__ bool nlist_cell(const rb_grid &g, int c, const double *__restrict__ p
             if (with_mirror && keep) {
                 if (bi - b0 < 32) atomicOr(&sm.bits[k], 1u << (bi - b0));
                 atomicAdd(&sm.segn[warp * 32 + sm.cj[k]], 1);
-                // (the staged index, for the partial below)
-                if (slot < capacity) mirror[r * (int64_t)capacity + slot] = k;
+                // (the staged index, for the partial below; lower entries
+                // are marked, so the partial reads only this array)
+                if (slot < capacity)
+                    mirror[r * (int64_t)capacity + slot] = sm.rank[k] > (int)r ? k : kMirrorLower;
             }
             count += __popc(m);
         }
@@ -611,17 +614,13 @@ __device__ bool nlist_cell(const rb_grid &g, int c, const double *__restrict__ p
             const int64_t r = r0 + (bi - b0);
             if (dir[r * kDirStride] == kDirNone) continue;  // its rows came from nlist_one
             const int m = row_count[r];
-            const int32_t *row = rows + r * (int64_t)capacity;
             int32_t *mrow = mirror + r * (int64_t)capacity;
             const uint32_t below = (1u << (bi - b0 < 32 ? bi - b0 : 31)) - 1u;
             for (int k = lane; k < m; k += 32) {
-                if (row[k] <= (int)r) continue;  // only the upper entries are defined
-                int32_t v = kMirrorSearch;
-                if (!search) {
-                    const int kk = mrow[k];
-                    v = __popc(sm.bits[kk] & below) | (sm.slotc[sm.cj[kk]] << 24);
-                }
-                mrow[k] = v;
+                const int kk = mrow[k];
+                if (kk == kMirrorLower) continue;  // only the upper entries are defined
+                mrow[k] = search ? kMirrorSearch
+                                 : (int32_t)(__popc(sm.bits[kk] & below) | (sm.slotc[sm.cj[kk]] << 24));
             }
         }
     }
@@ -641,31 +640,49 @@ __device__ __forceinline__ void mirror_resolve(int64_t p, int lane, const int32_
     const int32_t *rp = rows + p * (int64_t)capacity;
     int32_t *mp = mirror + p * (int64_t)capacity;
     const bool p_none = ldc<kCoherent>(dir + p * kDirStride) == kDirNone;
-    for (int k = lane; k < m; k += 32) {
-        const int q = ldc<kCoherent>(rp + k);
-        if (q <= (int)p) continue;
-        const int32_t v = p_none ? kMirrorSearch : ldc<kCoherent>(mp + k);
-        int pos = -1;
-        uint16_t d = kDirNone;
-        if (v != kMirrorSearch) d = ldc<kCoherent>(dir + (int64_t)q * kDirStride + (v >> 24));
-        if (d != kDirNone) {
-            pos = (int)d + (v & 0xffffff);
-            if (pos >= capacity) pos = -1;
-        } else {  // binary search of p in the rank-sorted row q
-            const int32_t *rq = rows + (int64_t)q * capacity;
-            int lo = 0, hi = ldc<kCoherent>(row_count + q) - 1;
-            while (lo <= hi) {
-                const int mid = (lo + hi) >> 1;
-                const int x = ldc<kCoherent>(rq + mid);
-                if (x == (int)p) {
-                    pos = mid;
-                    break;
-                }
-                if (x < (int)p) lo = mid + 1;
-                else hi = mid - 1;
-            }
+    // four entries per lane in flight (the phase is a chain of dependent
+    // loads: row entry and partial, then q's directory word)
+    constexpr int kU = 4;
+    for (int k0 = lane; k0 < m; k0 += 32 * kU) {
+        int q[kU];
+        int32_t v[kU];
+#pragma unroll
+        for (int t = 0; t < kU; t++) {
+            const int k = k0 + 32 * t;
+            q[t] = k < m ? ldc<kCoherent>(rp + k) : -1;
+            v[t] = k < m && !p_none ? ldc<kCoherent>(mp + k) : kMirrorSearch;
         }
-        mp[k] = pos;
+        uint16_t d[kU];
+#pragma unroll
+        for (int t = 0; t < kU; t++) {
+            const bool upper = q[t] > (int)p;
+            d[t] = upper && v[t] != kMirrorSearch
+                       ? ldc<kCoherent>(dir + (int64_t)q[t] * kDirStride + (v[t] >> 24))
+                       : kDirNone;
+        }
+#pragma unroll
+        for (int t = 0; t < kU; t++) {
+            if (q[t] <= (int)p) continue;  // only the upper entries are defined
+            int pos = -1;
+            if (d[t] != kDirNone) {
+                pos = (int)d[t] + (v[t] & 0xffffff);
+                if (pos >= capacity) pos = -1;
+            } else {  // binary search of p in the rank-sorted row q
+                const int32_t *rq = rows + (int64_t)q[t] * capacity;
+                int lo = 0, hi = ldc<kCoherent>(row_count + q[t]) - 1;
+                while (lo <= hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const int x = ldc<kCoherent>(rq + mid);
+                    if (x == (int)p) {
+                        pos = mid;
+                        break;
+                    }
+                    if (x < (int)p) lo = mid + 1;
+                    else hi = mid - 1;
+                }
+            }
+            mp[k0 + 32 * t] = pos;
+        }
     }
 }
 

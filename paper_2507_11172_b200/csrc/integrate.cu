@@ -48,13 +48,21 @@ __device__ __forceinline__ double wrap_coord(double x, double box) {
 
 // Four lanes per particle, lane c < 3 on component c of the AoS arrays
 // (coalesced: a warp covers 8 particles = 24 contiguous doubles per array;
-// lane 3 idles), so every load of a step is in flight at once.  Besides the
-// drift it (a) scatters the new position into the rank-ordered copy the force
-// kernels read, and (b) compares against the positions of the last
-// neighbour-row build: a particle that moved more than skin/2 flags a rebuild
-// of the rows in this very step (*rebuild_flag = tag), so every pair within
-// rc is always inside the rows built at rc + skin.  The displacement norm is
-// gathered by shuffles into lane 0 of the group.
+// lane 3 idles).  A thread serves kU particles a grid stride apart and issues
+// every load of all of them -- and both status words -- before the first
+// use: the pass is one memory round trip per thread, so the bytes in flight
+// per SM (not the instruction count) set its speed (ncu, cfg4: one particle
+// per thread left DRAM at 29 % with 60 % of the stalls on the status round
+// trip).  Besides the drift it (a) scatters the new position into the
+// rank-ordered copy the force kernels read, and (b) compares against the
+// positions of the last neighbour-row build: a particle that moved more than
+// skin/2 flags a rebuild of the rows in this very step (*rebuild_flag = tag),
+// so every pair within rc is always inside the rows built at rc + skin.  The
+// displacement norm is gathered by shuffles into lane 0 of the group.
+#ifndef RB_DRIFT_U
+#define RB_DRIFT_U 4
+#endif
+template <int kU>
 __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict__ vel,
                         double *__restrict__ f2_old, const double *__restrict__ f3,
                         double bx, double by, double bz, int periodic, double dt,
@@ -67,30 +75,42 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
                         int kick3_prev, double *__restrict__ publish, int64_t pub_stride) {
     pdl_enter();
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t p = gt >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // a multiple of 4
     const int c = (int)(gt & 3);
-    const bool act = p < n && c < 3;
-    const int64_t i = 3 * p + c;
     // every load of the step first (one memory round trip; the status words
     // ride along), the decisions after
-    double v = 0.0, fo = 0.0, fnew = 0.0, f3v = 0.0, px = 0.0, xr = 0.0;
-    int32_t ro = 0;
-    if (act) {
-        v = vel[i];
-        fo = f2_old[i];
-        px = pos[i];
-        if (kick_prev) fnew = f2_new[i];
-        if (kick3 || (kick_prev && kick3_prev)) f3v = f3[i];
-        if (x_ref) xr = x_ref[i];
-        if (pr && rank_of) ro = rank_of[p];
+    double v[kU], fo[kU], fnew[kU], f3v[kU], px[kU], xr[kU];
+    int32_t ro[kU];
+    bool act[kU];
+    int64_t ix[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const int64_t p = (gt + u * stride) >> 2;
+        act[u] = p < n && c < 3;
+        ix[u] = 3 * p + c;
+        v[u] = fo[u] = fnew[u] = f3v[u] = px[u] = xr[u] = 0.0;
+        ro[u] = 0;
+        if (act[u]) {
+            const int64_t i = ix[u];
+            v[u] = vel[i];
+            fo[u] = f2_old[i];
+            px[u] = pos[i];
+            if (kick_prev) fnew[u] = f2_new[i];
+            if (kick3 || (kick_prev && kick3_prev)) f3v[u] = f3[i];
+            if (x_ref) xr[u] = x_ref[i];
+            if (pr && rank_of) ro[u] = rank_of[p];
+        }
     }
     const ulonglong2 s01 = ld_status2(status);
+    // status[2] (the last CLOSED step) is written by the previous step's
+    // pair pass / kick only: loaded with the rest
+    const ulonglong2 s23 = advance ? ld_status2(status + 2) : make_ulonglong2(0ull, 0ull);
     // a step-opening drift numbers its step from the last CLOSED step
     // (status[2], written by the step's pair pass and kick) and publishes it
     // in status[1]: no kernel reads the word another block of it writes.
     const unsigned long long sw = s01.x;  // the error word as this step found it
     if (advance) {
-        tag = (int64_t)ld_status2(status + 2).x + 1;
+        tag = (int64_t)s23.x + 1;
         if (rebuild_frozen(sw, tag)) return;  // a speculative window stopped here
         if (gt == 0) status[1] = (unsigned long long)tag;
     } else if (tag < 0) {
@@ -108,75 +128,92 @@ __global__ void k_drift(int64_t n, double *__restrict__ pos, double *__restrict_
             if (t < tp || (t == tp && k == RB_KIND_PAIR_MIN_SEPARATION)) go = false;
             if (t == tp && k == RB_KIND_TRIPLET_MIN_SEPARATION) do3 = false;
         }
-        if (go && act) {
-            v = xadd(v, xmul(half_dt, xadd(fo, fnew)));
-            if (do3) v = xadd(v, xmul(half_respa, f3v));
-            vel[i] = v;
-            f2_old[i] = fnew;
-            fo = fnew;
-            if (!isfinite(v)) record_status(status, tp, RB_KIND_NONFINITE);
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            if (go && act[u]) {
+                double w = xadd(v[u], xmul(half_dt, xadd(fo[u], fnew[u])));
+                if (do3) w = xadd(w, xmul(half_respa, f3v[u]));
+                v[u] = w;
+                vel[ix[u]] = w;
+                f2_old[ix[u]] = fnew[u];
+                fo[u] = fnew[u];
+                if (!isfinite(w)) record_status(status, tp, RB_KIND_NONFINITE);
+            }
         }
     }
     // an earlier step failed: freeze (errors of this step do not stop it)
     const bool run = sw == RB_STATUS_CLEAR || (long long)(sw >> 8) >= tag;
     const double box = c == 0 ? bx : (c == 1 ? by : bz);
-    double d = 0.0;
-    if (run && act) {
-        if (kick3) {
-            v = xadd(v, xmul(half_respa, f3v));
-            vel[i] = v;
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const int64_t i = ix[u];
+        double d = 0.0;
+        if (run && act[u]) {
+            double w = v[u];
+            if (kick3) {
+                w = xadd(w, xmul(half_respa, f3v[u]));
+                vel[i] = w;
+            }
+            double xc = xadd(px[u], xadd(xmul(dt, w), xmul(half_drift, fo[u])));
+            if (periodic) xc = wrap_coord(xc, box);
+            pos[i] = xc;
+            if (!isfinite(xc)) record_status(status, tag, RB_KIND_NONFINITE);
+            if (pr && rank_of) pr[3 * (int64_t)ro[u] + c] = xc;
+            if (publish) {  // the copy peers pull their ghosts from (rb_halo_pull),
+                            // the half of this step's parity
+                publish[(tag & 1) * 3 * pub_stride + i] = xc;
+                __threadfence_system();
+            }
+            if (x_ref) {
+                d = xc - xr[u];
+                if (periodic) d = min_image(d, box, 0.5 * box);
+            }
         }
-        double xc = xadd(px, xadd(xmul(dt, v), xmul(half_drift, fo)));
-        if (periodic) xc = wrap_coord(xc, box);
-        pos[i] = xc;
-        if (!isfinite(xc)) record_status(status, tag, RB_KIND_NONFINITE);
-        if (pr && rank_of) pr[3 * (int64_t)ro + c] = xc;
-        if (publish) {  // the copy peers pull their ghosts from (rb_halo_pull),
-                        // the half of this step's parity
-            publish[(tag & 1) * 3 * pub_stride + i] = xc;
-            __threadfence_system();
-        }
-        if (x_ref) {
-            d = xc - xr;
-            if (periodic) d = min_image(d, box, 0.5 * box);
-        }
-    }
-    if (x_ref && rebuild_flag) {  // uniform: every lane takes the shuffles
-        const double dy = __shfl_down_sync(0xffffffffu, d, 1);
-        const double dz = __shfl_down_sync(0xffffffffu, d, 2);
-        if (run && act && c == 0) {
-            const double d2 = d * d + dy * dy + dz * dz;
-            if (!(d2 <= skin_half2)) {  // also catches NaN
-                // the first thread to flag this step counts a rebuild step
-                const unsigned long long was = atomicExch(
-                    reinterpret_cast<unsigned long long *>(rebuild_flag), (unsigned long long)tag);
-                if ((int64_t)was != tag && status) atomicAdd(status + 3, 1ull);
-                if (cond) cudaGraphSetConditional(cond, 1u);
+        if (x_ref && rebuild_flag) {  // uniform: every lane takes the shuffles
+            const double dy = __shfl_down_sync(0xffffffffu, d, 1);
+            const double dz = __shfl_down_sync(0xffffffffu, d, 2);
+            if (run && act[u] && c == 0) {
+                const double d2 = d * d + dy * dy + dz * dz;
+                if (!(d2 <= skin_half2)) {  // also catches NaN
+                    // the first thread to flag this step counts a rebuild step
+                    const unsigned long long was =
+                        atomicExch(reinterpret_cast<unsigned long long *>(rebuild_flag),
+                                   (unsigned long long)tag);
+                    if ((int64_t)was != tag && status) atomicAdd(status + 3, 1ull);
+                    if (cond) cudaGraphSetConditional(cond, 1u);
+                }
             }
         }
     }
 }
 
+// kU entries a grid stride apart per thread, all loads first (k_drift)
+template <int kU>
 __global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict__ f2_old,
                        const double *__restrict__ f2_new, const double *__restrict__ f3,
                        double half_dt, double half_respa, int kick3, unsigned long long *status,
                        int64_t tag) {
     pdl_enter();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     // loads first, the status words with them (one round trip)
-    double v = 0.0, fo = 0.0, fnew = 0.0, f3v = 0.0;
-    if (i < n3) {
-        v = vel[i];
-        fo = f2_old[i];
-        fnew = f2_new[i];
-        if (kick3) f3v = f3[i];
+    double v[kU], fo[kU], fnew[kU], f3v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const int64_t i = i0 + u * stride;
+        v[u] = fo[u] = fnew[u] = f3v[u] = 0.0;
+        if (i < n3) {
+            v[u] = vel[i];
+            fo[u] = f2_old[i];
+            fnew[u] = f2_new[i];
+            if (kick3) f3v[u] = f3[i];
+        }
     }
     const ulonglong2 s01 = ld_status2(status);
     const bool from_device = tag < 0;
     if (tag < 0) tag = status ? (int64_t)s01.y : 0;
     if (status && rebuild_frozen(s01.x, tag)) return;  // (the step stays open)
-    if (from_device && status && i == 0) status[2] = (unsigned long long)tag;  // closes the step
-    if (i >= n3) return;
+    if (from_device && status && i0 == 0) status[2] = (unsigned long long)tag;  // closes the step
     bool do_kick2 = true, do_kick3 = kick3 != 0;
     const unsigned long long s = s01.x;
     if (s != RB_STATUS_CLEAR) {
@@ -186,11 +223,17 @@ __global__ void k_kick(int64_t n3, double *__restrict__ vel, double *__restrict_
         if (t == tag && k == RB_KIND_PAIR_MIN_SEPARATION) return;  // raised before :158
         if (t == tag && k == RB_KIND_TRIPLET_MIN_SEPARATION) do_kick3 = false;  // before :165
     }
-    if (do_kick2) v = xadd(v, xmul(half_dt, xadd(fo, fnew)));
-    if (do_kick3) v = xadd(v, xmul(half_respa, f3v));
-    vel[i] = v;
-    f2_old[i] = fnew;  // np.copyto(f2_old, forces_2b), integrators.py:159
-    if (!isfinite(v)) record_status(status, tag, RB_KIND_NONFINITE);
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const int64_t i = i0 + u * stride;
+        if (i >= n3) continue;
+        double w = v[u];
+        if (do_kick2) w = xadd(w, xmul(half_dt, xadd(fo[u], fnew[u])));
+        if (do_kick3) w = xadd(w, xmul(half_respa, f3v[u]));
+        vel[i] = w;
+        f2_old[i] = fnew[u];  // np.copyto(f2_old, forces_2b), integrators.py:159
+        if (!isfinite(w)) record_status(status, tag, RB_KIND_NONFINITE);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -449,7 +492,9 @@ static int drift_launch(int64_t n, double *pos, double *vel, double *f2_old, con
     if (n == 0) return advance_step ? rb_step_begin(status, stream) : RB_OK;
     const int tb = 256;
     const double half = 0.5 * skin;
-    launch(k_drift, dim3((unsigned)((4 * n + tb - 1) / tb)), dim3(tb), 0, as_stream(stream), n, pos,
+    constexpr int kU = RB_DRIFT_U;
+    launch(k_drift<kU>, dim3((unsigned)((4 * n + (int64_t)tb * kU - 1) / ((int64_t)tb * kU))),
+           dim3(tb), 0, as_stream(stream), n, pos,
            vel, f2_old, f3, box3_host[0], box3_host[1], box3_host[2], periodic, dt, half_drift,
            half_respa, kick3, rank_of, pos_r, x_ref, half * half * (1.0 - 1e-9), rebuild_flag,
            status, tag, advance_step ? 1 : 0, (cudaGraphConditionalHandle)rebuild_cond, f2_new,
@@ -511,7 +556,11 @@ extern "C" int rb_respa_kick(int64_t n, double *vel, double *f2_old, const doubl
     const int64_t n3 = 3 * n;
     if (n == 0 && (tag >= 0 || !status)) return RB_OK;  // (tag < 0: still closes the step)
     const int tb = 256;
-    launch(k_kick, dim3(n3 > 0 ? (unsigned)((n3 + tb - 1) / tb) : 1u), dim3(tb), 0, as_stream(stream), n3, vel, f2_old, f2_new, f3, half_dt, half_respa, kick3, status, tag);
+    constexpr int kU = RB_DRIFT_U;
+    const int64_t per = (int64_t)tb * kU;
+    launch(k_kick<kU>, dim3(n3 > 0 ? (unsigned)((n3 + per - 1) / per) : 1u), dim3(tb), 0,
+           as_stream(stream), n3, vel, f2_old, f2_new, f3, half_dt, half_respa, kick3, status,
+           tag);
     note_launches(1);
     return launch_status();
 }

@@ -188,6 +188,9 @@ class DeviceRespa:
         # three-body steps: the pair pass on a second stream beside the
         # triplet kernels (periodic Verlet-row loop only)
         self.overlap_pair = os.environ.get("RB_OVERLAP_PAIR", "1") != "0"
+        # ... started after the persistent triplet kernel, beside the gather
+        # (RB_PAIR_WITH_GATHER=0: from the start, filling the triplet tail)
+        self.pair_with_gather = os.environ.get("RB_PAIR_WITH_GATHER", "1") != "0"
 
     def cache_key(self):
         """What the captured period graph bakes in (kernel arguments and
@@ -263,13 +266,23 @@ class DeviceRespa:
             torch = self.torch
             main = torch.cuda.current_stream()
             side = self._pair_stream = getattr(self, "_pair_stream", None) or torch.cuda.Stream()
-            side.wait_stream(main)
-            eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=1)
+            if self.pair_with_gather:
+                # the pair pass (L1-bound) beside the gather (HBM-bound):
+                # both start when the persistent triplet kernel ends
+                eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=1)
+                side.wait_stream(main)
+            else:
+                side.wait_stream(main)
+                eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=1)
             with torch.cuda.stream(side):
                 eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag,
                        reduce=False, scalars=scalars)
-            main.wait_stream(side)
-            eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=2)
+            if self.pair_with_gather:
+                eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=2)
+                main.wait_stream(side)
+            else:
+                main.wait_stream(side)
+                eng.atm_kernel(geom, self.rc3, self.nu, self.f3, tag=tag, part=2)
             return
         eng.lj(geom, self.rc2, self.ff.epsilon, self.ff.sigma, f2_out, tag=tag, reduce=False,
                scalars=scalars)

@@ -25,13 +25,14 @@ struct A3Smem {
     double2 *axy;      // [M + 1]
     double *az;        // [M + 1]
     double *ae;        // [M + 1] energy of the slot's triplets (owned shares, atm_rot.cuh)
+    double *aw;        // [M + 1] scalar part of a slot's sum in the cross rounds (atm_rot.cuh)
     int32_t *kidx;     // row index | owned << 30
     int32_t *q;        // the slot's particle (rank) ...
     int32_t *mpos;     //   ... and the base's position in its row (G target)
 };
 
 __host__ __device__ inline size_t a3_warp_bytes(int m) {
-    size_t b = (size_t)(m + 1) * (3 * sizeof(double2) + 2 * sizeof(double)) +
+    size_t b = (size_t)(m + 1) * (3 * sizeof(double2) + 3 * sizeof(double)) +
                (size_t)m * 3 * sizeof(int32_t);
     return (b + 15) & ~(size_t)15;
 }
@@ -47,7 +48,8 @@ __device__ __forceinline__ A3Smem a3_carve(char *base, int m_rt) {
     s.axy = s.zr + (m + 1);
     s.az = (double *)(s.axy + (m + 1));
     s.ae = s.az + (m + 1);
-    s.kidx = (int32_t *)(s.ae + (m + 1));
+    s.aw = s.ae + (m + 1);
+    s.kidx = (int32_t *)(s.aw + (m + 1));
     s.q = s.kidx + m;
     s.mpos = s.q + m;
     return s;

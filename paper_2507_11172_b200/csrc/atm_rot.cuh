@@ -3,15 +3,19 @@
 // 64-slot instance of k_atm3, undecomposed and -- with kE, the per-slot
 // energy sums behind the owned shares -- decomposed runs).
 //
-// Every slot's force sum lives in a register of the lane that holds the slot
+// Every slot's force sum lives in registers of the lane that holds the slot
 // (lane l holds slot l, and slot 32 + l when m > 32), so the pair loop moves
-// no accumulator through shared memory.  The m(m-1)/2 slot pairs are taken in
+// no accumulator through shared memory.  The sum is kept as one scalar and one
+// vector, F_y = D_y * sum(E_y + E_c) - sum(E_c * D_partner) (rot_eval /
+// kRotSum below), which takes a pair from 58 to 43 FP64 instructions -- the
+// loop is bound by the FP64 pipe.  The m(m-1)/2 slot pairs are taken in
 // three kinds of rounds, each conflict-free and deterministic:
 //
 //   rotation rounds over a group of g <= 32 slots (lane = slot): round d
 //     pairs slot s with (s + d) mod g, d = 1 .. g/2 (the last round of an
-//     even g only s < g/2); f_j stays in the lane, f_k is pulled by the lane
-//     of its target (in a round the targets are a permutation of the lanes).
+//     even g only s < g/2); the j role stays in the lane, the k role is pulled (as two
+//     scalars) by the lane of its target (in a round the targets are a
+//     permutation of the lanes).
 //   cross rounds A x B (m > 32: A = slots 0..31 on all 32 lanes, B = slots
 //     32..m-1, mB = m - 32 of them): round e pairs lane l's A slot with B slot
 //     (l + e) mod mB, so all 32 lanes work in every round.  f_j stays in the
@@ -86,57 +90,65 @@ __device__ __forceinline__ bool rot_exact_in(const A3Smem &sm, int s, int t, con
     return in;
 }
 
-// f_j, f_k (units of 2 nu) of the pair with D_j = (sx, sy, sz), a = r_ij^2,
-// D_k = (tx, ty, tz), b = r_ik^2, scaled to zero unless `in`.
+// The ATM scalars of one slot pair from the dot product g = D_j . D_k
+// (D_j, D_k the slots' displacements from the base, a = r_ij^2, b = r_ik^2,
+// c = r_jk^2 = a + b - 2 g).  In atm_scalars' notation u = 2 g, v = 2 (a - g),
+// w = 2 (b - g), so with q = g (a - g)(b - g) = p / 8 and k = 1 + 5 q / s:
+//   E_a = 3/2 s^-5/2 [a (b - g) - g (a - g) - k b c]
+//   E_b = 3/2 s^-5/2 [b (a - g) - g (b - g) - k a c]
+//   E_c = 3/2 s^-5/2 [c g - (a - g)(b - g) - k a b]
+//   E   = s^-5/2 (s + 3 q)
+// (the same polynomials, potentials.py:82-114, regrouped: 29 FP64
+// instructions instead of 35 and no r_jk vector).  Returns the brackets
+// e_a + e_c, e_b + e_c, e_c (units of 3/2 s^-5/2) and s52 = s^-5/2, zero
+// unless `in`: the rounds below fold s52 into their accumulation.
 template <bool kE>
-__device__ __forceinline__ void rot_eval(bool in, double sx, double sy, double sz, double a,
-                                         double tx, double ty, double tz, double b, double jkx,
-                                         double jky, double jkz, double c, double fj[3],
-                                         double fk[3], double &e) {
-    // atm_scalars with the common factor s^-5/2 selected (every E_x is a
-    // multiple of it)
-    const double tsum = a + b + c;
-    const double u = fma(-2.0, c, tsum);
-    const double v = fma(-2.0, b, tsum);
-    const double w = fma(-2.0, a, tsum);
-    const double uv = u * v, uw = u * w, vw = v * w;
-    const double p = uv * w;
-    const double sp = a * b * c;
+__device__ __forceinline__ void rot_eval(bool in, double g, double a, double b, double c,
+                                         double &eac, double &ebc, double &ec, double &s52,
+                                         double &e) {
+    const double ab = a * b;
+    const double sp = ab * c;
     const double rs = rsqrt_nr(sp);
     const double inv_s = rs * rs;
-    double s52 = rs * inv_s * inv_s;
+    s52 = (rs * inv_s) * inv_s;
     s52 = in ? s52 : 0.0;
-    const double S = uv + uw + vw;
-    const double A = 0.375 * s52;
-    const double K = s52 * fma(0.9375 * p, inv_s, 1.5);
-    const double ea = fma(A, fma(-2.0, uv, S), -K * (b * c));
-    const double eb = fma(A, fma(-2.0, uw, S), -K * (a * c));
-    const double ec = fma(A, fma(-2.0, vw, S), -K * (a * b));
-    const double cx = ec * jkx, cy = ec * jky, cz = ec * jkz;
-    fj[0] = fma(ea, sx, -cx);
-    fj[1] = fma(ea, sy, -cy);
-    fj[2] = fma(ea, sz, -cz);
-    fk[0] = fma(eb, tx, cx);
-    fk[1] = fma(eb, ty, cy);
-    fk[2] = fma(eb, tz, cz);
-    if (kE) e = s52 * fma(0.375, p, sp);  // the triplet's energy (units of nu), 0 if rejected
+    const double va = a - g, wb = b - g;
+    const double gva = g * va, gwb = g * wb, vawb = va * wb;
+    const double q = gva * wb;
+    const double k = fma(q * inv_s, 5.0, 1.0);
+    const double ea = fma(-k, b * c, fma(a, wb, -gva));
+    const double eb = fma(-k, a * c, fma(b, va, -gwb));
+    ec = fma(-k, ab, fma(c, g, -vawb));
+    eac = ea + ec;
+    ebc = eb + ec;
+    if (kE) e = s52 * fma(3.0, q, sp);  // the triplet's energy (units of nu), 0 if rejected
 }
 
-// One pair of the fast loop: `live` lanes accept on the fp64 estimate;
-// undecided pairs contribute nothing here and set `und`.
+// A slot's force sum in the rounds (units of 3 nu): with f_j = E_a D_j -
+// E_c (D_k - D_j) = (E_a + E_c) D_j - E_c D_k and f_k = (E_b + E_c) D_k -
+// E_c D_j, slot y's sum is D_y * S[0] - (S[1], S[2], S[3]): S[0] the sum of
+// (E_y + E_c) over the slot's pairs, S[1..3] the sum of E_c * (the partner's
+// D).  A pair costs the j role 1 + 3 and the k role 1 + 3 FP64 instructions
+// (instead of 3 + 3 + 3 for the two force vectors and 3 + 3 to add them), and
+// the k role travels as two scalars.  S[4]: the slot's energy sum (kE).
+constexpr int kRotSum = 5;
+
+// One pair of the fast loop: `live` lanes accept on the fp64 estimate of
+// c = a + b - 2 g (a few ulp of a + b from the raw-position value: far inside
+// the 1e-10 band); undecided pairs contribute nothing here and set `und`.
 template <bool kE>
 __device__ __forceinline__ void rot_fast(bool live, double sx, double sy, double sz, double a,
                                          double tx, double ty, double tz, double b,
-                                         const RotCut &rc, A3Acc &acc, bool &und, double fj[3],
-                                         double fk[3], double &e) {
-    const double jkx = tx - sx, jky = ty - sy, jkz = tz - sz;
-    const double c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
+                                         const RotCut &rc, A3Acc &acc, bool &und, double &eac,
+                                         double &ebc, double &ec, double &s52, double &e) {
+    const double g = fma(sz, tz, fma(sy, ty, sx * tx));
+    const double c = fma(-2.0, g, a + b);
     const int ch = __double2hiint(c);
     const bool inr = (unsigned)(ch - rc.base) < rc.span;
     und = live && !inr && ch <= rc.hi_hi;
     const bool in = live && inr;
     acc.n += in ? 1 : 0;
-    rot_eval<kE>(in, sx, sy, sz, a, tx, ty, tz, b, jkx, jky, jkz, c, fj, fk, e);
+    rot_eval<kE>(in, g, a, b, c, eac, ebc, ec, s52, e);
 }
 
 // The fix-up pair: `live` lanes decide with the reference arithmetic.
@@ -145,24 +157,34 @@ __device__ __forceinline__ void rot_slow(const A3Smem &sm, bool live, int s, int
                                          double sy, double sz, double a, double tx, double ty,
                                          double tz, double b, const rb_grid &g,
                                          const double *__restrict__ pr, const A3Cut &cut,
-                                         A3Acc &acc, double fj[3], double fk[3], double &e) {
-    const double jkx = tx - sx, jky = ty - sy, jkz = tz - sz;
-    const double c = fma(jkz, jkz, fma(jky, jky, jkx * jkx));
+                                         A3Acc &acc, double &eac, double &ebc, double &ec,
+                                         double &s52, double &e) {
+    const double dot = fma(sz, tz, fma(sy, ty, sx * tx));
+    const double c = fma(-2.0, dot, a + b);
     bool bad = false;
     bool in = live && rot_exact_in(sm, s, t, g, pr, cut, bad);
     acc.bad = acc.bad || bad;
     in = in && !bad;
     acc.n += in ? 1 : 0;
-    rot_eval<kE>(in, sx, sy, sz, a, tx, ty, tz, b, jkx, jky, jkz, c, fj, fk, e);
+    rot_eval<kE>(in, dot, a, b, c, eac, ebc, ec, s52, e);
+}
+
+// position of a slot record (the z half of the second 16-byte row)
+__device__ __forceinline__ void lds_pos(unsigned xy, unsigned zr, double &x, double &y,
+                                        double &z) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(xy));
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(z) : "r"(zr));
 }
 
 // Rotation rounds over slots [off, off + gm) on lanes 0 .. gm-1 (2 <= gm <=
 // 32); lanes >= gm mirror lane (lane mod gm) and contribute nothing.  Adds
-// each slot's sum to F of its lane.
+// each slot's sums to S of its lane (kRotSum above).  The k role of round d
+// comes from the lane of slot (s - d) mod gm as two scalars; that slot's
+// displacement is a second conflict-free shared load.
 template <bool kE>
 __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, int lane,
                                            const rb_grid &g, const double *__restrict__ pr,
-                                           const A3Cut &cut, A3Acc &acc, double F[4]) {
+                                           const A3Cut &cut, A3Acc &acc, double S[kRotSum]) {
     constexpr unsigned kAll = 0xffffffffu;
     const bool mine = lane < gm;
     const int s = mine ? lane : lane % gm;
@@ -180,26 +202,30 @@ __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, in
     // in the last round), none for a mirror lane
     const int lim = !mine ? 0 : ((gm & 1) || lane < rounds ? rounds : rounds - 1);
     unsigned und = 0;  // bit d: round d is undecided on this lane
-    double fj[3], fk[3];
 #pragma unroll 1
     for (int d = 1; d <= rounds; d++) {
         RB_CHECK(toff < end && src >= 0 && src < gm && off + gm <= 64);
-        double tx, ty, tz, b;
+        double tx, ty, tz, b, ux, uy, uz;
         lds_rec(xy0 + toff, zr0 + toff, tx, ty, tz, b);  // conflict-free: a rotation
+        lds_pos(xy0 + 16u * (unsigned)src, zr0 + 16u * (unsigned)src, ux, uy, uz);
         bool u;
-        double e = 0.0;
-        rot_fast<kE>(d <= lim, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, fj, fk, e);
+        double eac, ebc, ec, s52, e = 0.0;
+        rot_fast<kE>(d <= lim, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, eac, ebc, ec, s52, e);
         und |= u ? 1u << d : 0u;
-        F[0] += fj[0];
-        F[1] += fj[1];
-        F[2] += fj[2];
-        F[0] += __shfl_sync(kAll, fk[0], src);  // zero from a rejected pair
-        F[1] += __shfl_sync(kAll, fk[1], src);
-        F[2] += __shfl_sync(kAll, fk[2], src);
+        const double ecs = s52 * ec, ebs = s52 * ebc;  // zero from a rejected pair
+        S[0] = fma(s52, eac, S[0]);
+        S[1] = fma(ecs, tx, S[1]);
+        S[2] = fma(ecs, ty, S[2]);
+        S[3] = fma(ecs, tz, S[3]);
+        const double rb = __shfl_sync(kAll, ebs, src), rc_ = __shfl_sync(kAll, ecs, src);
+        S[0] += rb;
+        S[1] = fma(rc_, ux, S[1]);
+        S[2] = fma(rc_, uy, S[2]);
+        S[3] = fma(rc_, uz, S[3]);
         if (kE) {  // the slot energy sums of both members, the base's sum
             acc.e += e;
-            F[3] += e;
-            F[3] += __shfl_sync(kAll, e, src);
+            S[4] += e;
+            S[4] += __shfl_sync(kAll, e, src);
         }
         toff += 16u;
         toff = toff == end ? 0u : toff;
@@ -212,85 +238,97 @@ __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, in
             if (!__any_sync(kAll, mysus)) continue;
             const int t = (s + d) % gm;
             const int sr = (s - d + gm) % gm;
-            double tx, ty, tz, b;
+            double tx, ty, tz, b, ux, uy, uz;
             lds_rec(xy0 + 16 * t, zr0 + 16 * t, tx, ty, tz, b);
-            double e = 0.0;
+            lds_pos(xy0 + 16 * sr, zr0 + 16 * sr, ux, uy, uz);
+            double eac, ebc, ec, s52, e = 0.0;
             rot_slow<kE>(sm, mysus, off + s, off + t, sx, sy, sz, a, tx, ty, tz, b, g, pr, cut,
-                         acc, fj, fk, e);
-            F[0] += fj[0];
-            F[1] += fj[1];
-            F[2] += fj[2];
-            F[0] += __shfl_sync(kAll, fk[0], sr);
-            F[1] += __shfl_sync(kAll, fk[1], sr);
-            F[2] += __shfl_sync(kAll, fk[2], sr);
+                         acc, eac, ebc, ec, s52, e);
+            const double ecs = s52 * ec, ebs = s52 * ebc;
+            S[0] = fma(s52, eac, S[0]);
+            S[1] = fma(ecs, tx, S[1]);
+            S[2] = fma(ecs, ty, S[2]);
+            S[3] = fma(ecs, tz, S[3]);
+            const double rb = __shfl_sync(kAll, ebs, sr), rc_ = __shfl_sync(kAll, ecs, sr);
+            S[0] += rb;
+            S[1] = fma(rc_, ux, S[1]);
+            S[2] = fma(rc_, uy, S[2]);
+            S[3] = fma(rc_, uz, S[3]);
             if (kE) {
                 acc.e += e;
-                F[3] += e;
-                F[3] += __shfl_sync(kAll, e, sr);
+                S[4] += e;
+                S[4] += __shfl_sync(kAll, e, sr);
             }
         }
     }
 }
 
-// Cross rounds A x B (m > 32): adds the A sums to F (lane = A slot) and
-// leaves the B sums (lane = B slot, lanes < mb) in G.
+// Cross rounds A x B (m > 32): adds the A sums to S (lane = A slot) and
+// leaves the B sums (lane = B slot, lanes < mb) in G.  A stream carries a B
+// slot's five sums (the lane's own D_j is the partner of its k role).
 template <bool kE>
 __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, const rb_grid &g,
                                           const double *__restrict__ pr, const A3Cut &cut,
-                                          A3Acc &acc, double F[4], double G[4]) {
+                                          A3Acc &acc, double S[kRotSum], double G[kRotSum]) {
     constexpr unsigned kAll = 0xffffffffu;
     const int mb = m - 32;
     const unsigned xy0 = smem_u32(sm.xy), zr0 = smem_u32(sm.zr);
     double sx, sy, sz, a;
     lds_rec(xy0 + 16 * lane, zr0 + 16 * lane, sx, sy, sz, a);
     const RotCut rc = rot_cut(cut);
-    double R[4] = {0.0, 0.0, 0.0, 0.0};
-    double fj[3], fk[3];
+    double R[kRotSum] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const unsigned bbeg = 16u * 32u, bend = 16u * (unsigned)m;
     unsigned boff = bbeg + 16u * (unsigned)(lane % mb);  // B slot (lane + e) mod mb
     unsigned und = 0;
-    const unsigned ret0 = smem_u32(sm.axy + 32), retz0 = smem_u32(sm.az + 32);
+    const unsigned ret0 = smem_u32(sm.axy + 32), retz0 = smem_u32(sm.az + 32),
+                   retw0 = smem_u32(sm.aw + 32);
 #pragma unroll 1
     for (int e = 0; e < mb; e++) {
         RB_CHECK(boff >= bbeg && boff < bend && mb <= 32 && m <= 64);
         double tx, ty, tz, b;
         lds_rec(xy0 + boff, zr0 + boff, tx, ty, tz, b);
         bool u;
-        double en = 0.0;
-        rot_fast<kE>(true, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, fj, fk, en);
+        double eac, ebc, ec, s52, en = 0.0;
+        rot_fast<kE>(true, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, eac, ebc, ec, s52, en);
         und |= u ? 1u << e : 0u;
-        F[0] += fj[0];
-        F[1] += fj[1];
-        F[2] += fj[2];
-        R[0] += fk[0];
-        R[1] += fk[1];
-        R[2] += fk[2];
+        const double ecs = s52 * ec;
+        S[0] = fma(s52, eac, S[0]);
+        S[1] = fma(ecs, tx, S[1]);
+        S[2] = fma(ecs, ty, S[2]);
+        S[3] = fma(ecs, tz, S[3]);
+        R[0] = fma(s52, ebc, R[0]);
+        R[1] = fma(ecs, sx, R[1]);
+        R[2] = fma(ecs, sy, R[2]);
+        R[3] = fma(ecs, sz, R[3]);
         if (kE) {
             acc.e += en;
-            F[3] += en;
-            R[3] += en;
+            S[4] += en;
+            R[4] += en;
         }
         if (lane == 0) {  // the stream of B slot e leaves the warp
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ret0 + 16u * e), "d"(R[0]),
-                         "d"(R[1]));
-            asm volatile("st.shared.f64 [%0], %1;" ::"r"(retz0 + 8u * e), "d"(R[2]));
-            if (kE) sm.ae[32 + e] = R[3];
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ret0 + 16u * e), "d"(R[1]),
+                         "d"(R[2]));
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(retz0 + 8u * e), "d"(R[3]));
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(retw0 + 8u * e), "d"(R[0]));
+            if (kE) sm.ae[32 + e] = R[4];
         }
         // every stream moves one lane down; lane 31 starts the next one
         R[0] = __shfl_down_sync(kAll, R[0], 1);
         R[1] = __shfl_down_sync(kAll, R[1], 1);
         R[2] = __shfl_down_sync(kAll, R[2], 1);
-        if (kE) R[3] = __shfl_down_sync(kAll, R[3], 1);
-        if (lane == 31) R[0] = R[1] = R[2] = R[3] = 0.0;
+        R[3] = __shfl_down_sync(kAll, R[3], 1);
+        if (kE) R[4] = __shfl_down_sync(kAll, R[4], 1);
+        if (lane == 31) R[0] = R[1] = R[2] = R[3] = R[4] = 0.0;
         boff += 16u;
         boff = boff == bend ? bbeg : boff;
     }
     __syncwarp();
     // streams still in flight: lane l (0..30) holds B slot (l + mb) mod mb
     // = l mod mb (after the last shift)
-    sm.axy[lane] = make_double2(R[0], R[1]);
-    sm.az[lane] = R[2];
-    if (kE) sm.ae[lane] = R[3];
+    sm.axy[lane] = make_double2(R[1], R[2]);
+    sm.az[lane] = R[3];
+    sm.aw[lane] = R[0];
+    if (kE) sm.ae[lane] = R[4];
     if (__any_sync(kAll, und != 0)) {  // fix-up (rare): lane by lane, in order
 #pragma unroll 1
         for (int e = 0; e < mb; e++) {
@@ -302,16 +340,19 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
                     const int bslot = 32 + (lane + e) % mb;
                     double tx, ty, tz, b;
                     lds_rec(xy0 + 16 * bslot, zr0 + 16 * bslot, tx, ty, tz, b);
-                    double en = 0.0;
+                    double eac, ebc, ec, s52, en = 0.0;
                     rot_slow<kE>(sm, true, lane, bslot, sx, sy, sz, a, tx, ty, tz, b, g, pr, cut,
-                                 acc, fj, fk, en);
-                    F[0] += fj[0];
-                    F[1] += fj[1];
-                    F[2] += fj[2];
-                    acc_add(sm, bslot, fk[0], fk[1], fk[2]);
+                                 acc, eac, ebc, ec, s52, en);
+                    const double ecs = s52 * ec;
+                    S[0] = fma(s52, eac, S[0]);
+                    S[1] = fma(ecs, tx, S[1]);
+                    S[2] = fma(ecs, ty, S[2]);
+                    S[3] = fma(ecs, tz, S[3]);
+                    acc_add(sm, bslot, ecs * sx, ecs * sy, ecs * sz);
+                    sm.aw[bslot] += s52 * ebc;
                     if (kE) {
                         acc.e += en;
-                        F[3] += en;
+                        S[4] += en;
                         sm.ae[bslot] += en;
                     }
                 }
@@ -320,22 +361,35 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
         }
     }
     __syncwarp();
-    G[0] = G[1] = G[2] = G[3] = 0.0;
+    G[0] = G[1] = G[2] = G[3] = G[4] = 0.0;
     if (lane < mb) {
         const double2 r = sm.axy[32 + lane];
-        G[0] = r.x;
-        G[1] = r.y;
-        G[2] = sm.az[32 + lane];
-        if (kE) G[3] = sm.ae[32 + lane];
+        G[0] = sm.aw[32 + lane];
+        G[1] = r.x;
+        G[2] = r.y;
+        G[3] = sm.az[32 + lane];
+        if (kE) G[4] = sm.ae[32 + lane];
         for (int l = lane; l < 31; l += mb) {  // in lane order
             const double2 q = sm.axy[l];
-            G[0] += q.x;
-            G[1] += q.y;
-            G[2] += sm.az[l];
-            if (kE) G[3] += sm.ae[l];
+            G[0] += sm.aw[l];
+            G[1] += q.x;
+            G[2] += q.y;
+            G[3] += sm.az[l];
+            if (kE) G[4] += sm.ae[l];
         }
     }
     __syncwarp();
+}
+
+// slot `sl`'s force sum (units of 2 nu) from its round sums: 3/2 (D S[0] -
+// (S[1], S[2], S[3])), into the shared accumulators phase 3 reads
+template <bool kE>
+__device__ __forceinline__ void rot_store(const A3Smem &sm, int sl, const double S[kRotSum]) {
+    double dx, dy, dz, r2;
+    ld_rec(sm, sl, dx, dy, dz, r2);
+    sm.axy[sl] = make_double2(1.5 * fma(dx, S[0], -S[1]), 1.5 * fma(dy, S[0], -S[2]));
+    sm.az[sl] = 1.5 * fma(dz, S[0], -S[3]);
+    if (kE) sm.ae[sl] = S[4];
 }
 
 // Phase 1 for m <= 64 slots: the slot sums (units of 2 nu) end in the shared
@@ -344,31 +398,23 @@ template <bool kE>
 __device__ __forceinline__ void a3_rot(const A3Smem &sm, int m, int lane, const rb_grid &g,
                                        const double *__restrict__ pr, const A3Cut &cut,
                                        A3Acc &acc) {
-    double F[4] = {0.0, 0.0, 0.0, 0.0};
+    double S[kRotSum] = {0.0, 0.0, 0.0, 0.0, 0.0};
     int off = 0, gm = m < 32 ? m : 32;
     // group A (or all of a short S+), then the cross rounds, then group B
     // through the same loop
 #pragma unroll 1
     for (int grp = 0;; grp++) {
-        if (gm >= 2) rot_rounds<kE>(sm, off, gm, lane, g, pr, cut, acc, F);
+        if (gm >= 2) rot_rounds<kE>(sm, off, gm, lane, g, pr, cut, acc, S);
         if (grp == 1 || m <= 32) break;
-        double G[4];
-        rot_cross<kE>(sm, m, lane, g, pr, cut, acc, F, G);
-        sm.axy[lane] = make_double2(F[0], F[1]);  // the A sums are complete
-        sm.az[lane] = F[2];
-        if (kE) sm.ae[lane] = F[3];
-        F[0] = G[0];
-        F[1] = G[1];
-        F[2] = G[2];
-        F[3] = G[3];
+        double G[kRotSum];
+        rot_cross<kE>(sm, m, lane, g, pr, cut, acc, S, G);
+        rot_store<kE>(sm, lane, S);  // the A sums are complete
+#pragma unroll
+        for (int c = 0; c < kRotSum; c++) S[c] = G[c];
         off = 32;
         gm = m - 32;
     }
-    if (lane < gm) {  // (a group may have fewer than 32 slots)
-        sm.axy[off + lane] = make_double2(F[0], F[1]);
-        sm.az[off + lane] = F[2];
-        if (kE) sm.ae[off + lane] = F[3];
-    }
+    if (lane < gm) rot_store<kE>(sm, off + lane, S);  // (a group may have fewer than 32 slots)
     __syncwarp();
 }
 

@@ -29,7 +29,7 @@
 // every pair of a round and a rejected pair's scale is selected to zero (no
 // divergence).  r_jk^2 <= rc^2 is decided on the fp64 estimate from
 // D_k - D_j outside a 1e-10 band around rc^2; a pair inside the band (or
-// under the guard distance) is recorded in a per-lane bit mask and settled
+// under the guard distance) raises a per-lane flag and is found again and settled
 // after the loop with the reference's raw-position arithmetic (the fix-up
 // rounds, rarely entered), so the loop itself never branches.  A base with a
 // slot under the guard distance is not taken here (k_atm3 lists it for the
@@ -90,6 +90,19 @@ __device__ __forceinline__ bool rot_exact_in(const A3Smem &sm, int s, int t, con
     return in;
 }
 
+// FP64 constants of the pair loop that cannot ride as instruction immediates
+// (a DFMA takes one): read from the constant bank as operands, so the loop
+// does not rebuild them in registers every round.
+static __constant__ double kRot38 = 0.375, kRot5 = 5.0;
+
+// rsqrt_nr (common.cuh) with 3/8 from the constant bank
+__device__ __forceinline__ double rot_rsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double r = fma(-x * y, y, 1.0);
+    return fma(y * r, fma(kRot38, r, 0.5), y);
+}
+
 // The ATM scalars of one slot pair from the dot product g = D_j . D_k
 // (D_j, D_k the slots' displacements from the base, a = r_ij^2, b = r_ik^2,
 // c = r_jk^2 = a + b - 2 g).  In atm_scalars' notation u = 2 g, v = 2 (a - g),
@@ -108,14 +121,14 @@ __device__ __forceinline__ void rot_eval(bool in, double g, double a, double b, 
                                          double &e) {
     const double ab = a * b;
     const double sp = ab * c;
-    const double rs = rsqrt_nr(sp);
+    const double rs = rot_rsqrt(sp);
     const double inv_s = rs * rs;
     s52 = (rs * inv_s) * inv_s;
     s52 = in ? s52 : 0.0;
     const double va = a - g, wb = b - g;
     const double gva = g * va, gwb = g * wb, vawb = va * wb;
     const double q = gva * wb;
-    const double k = fma(q * inv_s, 5.0, 1.0);
+    const double k = fma(q * inv_s, kRot5, 1.0);
     const double ea = fma(-k, b * c, fma(a, wb, -gva));
     const double eb = fma(-k, a * c, fma(b, va, -gwb));
     ec = fma(-k, ab, fma(c, g, -vawb));
@@ -135,7 +148,8 @@ constexpr int kRotSum = 5;
 
 // One pair of the fast loop: `live` lanes accept on the fp64 estimate of
 // c = a + b - 2 g (a few ulp of a + b from the raw-position value: far inside
-// the 1e-10 band); undecided pairs contribute nothing here and set `und`.
+// the 1e-10 band); undecided pairs contribute nothing here and set `und`
+// (whether or not the lane is live: the fix-ups test rot_undecided again).
 template <bool kE>
 __device__ __forceinline__ void rot_fast(bool live, double sx, double sy, double sz, double a,
                                          double tx, double ty, double tz, double b,
@@ -145,10 +159,19 @@ __device__ __forceinline__ void rot_fast(bool live, double sx, double sy, double
     const double c = fma(-2.0, g, a + b);
     const int ch = __double2hiint(c);
     const bool inr = (unsigned)(ch - rc.base) < rc.span;
-    und = live && !inr && ch <= rc.hi_hi;
+    und = !inr && ch <= rc.hi_hi;
     const bool in = live && inr;
     acc.n += in ? 1 : 0;
     rot_eval<kE>(in, g, a, b, c, eac, ebc, ec, s52, e);
+}
+
+// rot_fast's verdict on a pair again (the same arithmetic, for the fix-ups)
+__device__ __forceinline__ bool rot_undecided(double sx, double sy, double sz, double a, double tx,
+                                              double ty, double tz, double b, const RotCut &rc) {
+    const double g = fma(sz, tz, fma(sy, ty, sx * tx));
+    const double c = fma(-2.0, g, a + b);
+    const int ch = __double2hiint(c);
+    return !((unsigned)(ch - rc.base) < rc.span) && ch <= rc.hi_hi;
 }
 
 // The fix-up pair: `live` lanes decide with the reference arithmetic.
@@ -192,26 +215,29 @@ __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, in
     double sx, sy, sz, a;
     lds_rec(xy0 + 16 * s, zr0 + 16 * s, sx, sy, sz, a);
     const RotCut rc = rot_cut(cut);
-    const unsigned end = 16u * (unsigned)gm;
-    // partner t = (s + d) mod gm as a byte offset, sender of the k role
-    // src = (s - d) mod gm
-    unsigned toff = 16u * (unsigned)(s + 1 >= gm ? s + 1 - gm : s + 1);
+    const unsigned zro = zr0 - xy0;  // (a constant of the instance)
+    const unsigned end = xy0 + 16u * (unsigned)gm;
+    // partner t = (s + d) mod gm and sender of the k role src = (s - d) mod
+    // gm, as shared-memory addresses of their records
+    unsigned tp = xy0 + 16u * (unsigned)(s + 1 >= gm ? s + 1 - gm : s + 1);
     int src = s - 1 < 0 ? s - 1 + gm : s - 1;
+    unsigned up = xy0 + 16u * (unsigned)src;
     const int rounds = gm >> 1;
     // the lane's last live round: gm/2 (even gm: only s < gm/2 start a pair
     // in the last round), none for a mirror lane
     const int lim = !mine ? 0 : ((gm & 1) || lane < rounds ? rounds : rounds - 1);
-    unsigned und = 0;  // bit d: round d is undecided on this lane
+    bool und = false;  // some round of this lane is undecided
 #pragma unroll 1
     for (int d = 1; d <= rounds; d++) {
-        RB_CHECK(toff < end && src >= 0 && src < gm && off + gm <= 64);
+        RB_CHECK(tp >= xy0 && tp < end && up == xy0 + 16u * (unsigned)src && src >= 0 &&
+                 src < gm && off + gm <= 64);
         double tx, ty, tz, b, ux, uy, uz;
-        lds_rec(xy0 + toff, zr0 + toff, tx, ty, tz, b);  // conflict-free: a rotation
-        lds_pos(xy0 + 16u * (unsigned)src, zr0 + 16u * (unsigned)src, ux, uy, uz);
+        lds_rec(tp, tp + zro, tx, ty, tz, b);  // conflict-free: a rotation
+        lds_pos(up, up + zro, ux, uy, uz);
         bool u;
         double eac, ebc, ec, s52, e = 0.0;
         rot_fast<kE>(d <= lim, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, eac, ebc, ec, s52, e);
-        und |= u ? 1u << d : 0u;
+        und = und || u;
         const double ecs = s52 * ec, ebs = s52 * ebc;  // zero from a rejected pair
         S[0] = fma(s52, eac, S[0]);
         S[1] = fma(ecs, tx, S[1]);
@@ -227,19 +253,21 @@ __device__ __forceinline__ void rot_rounds(const A3Smem &sm, int off, int gm, in
             S[4] += e;
             S[4] += __shfl_sync(kAll, e, src);
         }
-        toff += 16u;
-        toff = toff == end ? 0u : toff;
-        src = src == 0 ? gm - 1 : src - 1;
+        tp += 16u;
+        tp = tp == end ? xy0 : tp;
+        up = up == xy0 ? end : up;
+        up -= 16u;
+        src = (int)((up - xy0) >> 4);
     }
-    if (__any_sync(kAll, und != 0)) {  // fix-up rounds (rare)
+    if (__any_sync(kAll, und)) {  // fix-up rounds (rare)
 #pragma unroll 1
         for (int d = 1; d <= rounds; d++) {
-            const bool mysus = (und >> d) & 1u;
-            if (!__any_sync(kAll, mysus)) continue;
             const int t = (s + d) % gm;
             const int sr = (s - d + gm) % gm;
             double tx, ty, tz, b, ux, uy, uz;
             lds_rec(xy0 + 16 * t, zr0 + 16 * t, tx, ty, tz, b);
+            const bool mysus = d <= lim && rot_undecided(sx, sy, sz, a, tx, ty, tz, b, rc);
+            if (!__any_sync(kAll, mysus)) continue;
             lds_pos(xy0 + 16 * sr, zr0 + 16 * sr, ux, uy, uz);
             double eac, ebc, ec, s52, e = 0.0;
             rot_slow<kE>(sm, mysus, off + s, off + t, sx, sy, sz, a, tx, ty, tz, b, g, pr, cut,
@@ -279,7 +307,7 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
     double R[kRotSum] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const unsigned bbeg = 16u * 32u, bend = 16u * (unsigned)m;
     unsigned boff = bbeg + 16u * (unsigned)(lane % mb);  // B slot (lane + e) mod mb
-    unsigned und = 0;
+    bool und = false;
     const unsigned ret0 = smem_u32(sm.axy + 32), retz0 = smem_u32(sm.az + 32),
                    retw0 = smem_u32(sm.aw + 32);
 #pragma unroll 1
@@ -290,7 +318,7 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
         bool u;
         double eac, ebc, ec, s52, en = 0.0;
         rot_fast<kE>(true, sx, sy, sz, a, tx, ty, tz, b, rc, acc, u, eac, ebc, ec, s52, en);
-        und |= u ? 1u << e : 0u;
+        und = und || u;
         const double ecs = s52 * ec;
         S[0] = fma(s52, eac, S[0]);
         S[1] = fma(ecs, tx, S[1]);
@@ -329,10 +357,17 @@ __device__ __forceinline__ void rot_cross(const A3Smem &sm, int m, int lane, con
     sm.az[lane] = R[3];
     sm.aw[lane] = R[0];
     if (kE) sm.ae[lane] = R[4];
-    if (__any_sync(kAll, und != 0)) {  // fix-up (rare): lane by lane, in order
+    if (__any_sync(kAll, und)) {  // fix-up (rare): lane by lane, in order
 #pragma unroll 1
         for (int e = 0; e < mb; e++) {
-            unsigned who = __ballot_sync(kAll, (und >> e) & 1u);
+            bool mine_und;
+            {
+                const int bslot = 32 + (lane + e) % mb;
+                double tx, ty, tz, b;
+                lds_rec(xy0 + 16 * bslot, zr0 + 16 * bslot, tx, ty, tz, b);
+                mine_und = rot_undecided(sx, sy, sz, a, tx, ty, tz, b, rc);
+            }
+            unsigned who = __ballot_sync(kAll, mine_und);
             while (who) {
                 const int L = __ffs(who) - 1;
                 who &= who - 1;

@@ -119,6 +119,12 @@ template <bool kE>
 __device__ __forceinline__ void rot_eval(bool in, double g, double a, double b, double c,
                                          double &eac, double &ebc, double &ec, double &s52,
                                          double &e) {
+    // (two nearly coincident slots: the estimate c = a + b - 2 g can round to
+    // zero or below and 0 * NaN reaches the sums -- of a pass that raises: the
+    // pair is undecided, the reference arithmetic finds it under the guard,
+    // and RB_KIND_TRIPLET_MIN_SEPARATION orders before RB_KIND_NONFINITE in
+    // the status word.  A select on c here cost 1 % of the pass.
+    // test_minimum_separation_between_slots_raises)
     const double ab = a * b;
     const double sp = ab * c;
     const double rs = rot_rsqrt(sp);

@@ -285,6 +285,26 @@ def test_minimum_separation_raises(pkg):
         c.triplet_pass(s, ff)
 
 
+def test_minimum_separation_between_slots_raises(pkg, rng):
+    """The guard on r_jk (potentials.py:35-36) inside the register-resident
+    rounds: two slots of a lower-ranked base almost coincide, so the fp64
+    estimate a + b - 2 g of r_jk^2 rounds to ~0 (either sign); the pair is
+    settled by the reference arithmetic and the pass raises, as the
+    reference does -- for a bare triplet and inside a liquid-density box."""
+    ff = pkg.ForceField(nu=0.7, cutoff=2.5)
+    c = pkg.CudaLinkedCells()
+    tiny = _system(pkg, np.array([[1.0, 1.0, 1.0], [2.0, 1.3, 0.9], [2.0 + 5e-11, 1.3, 0.9]]),
+                   (10.0,) * 3, True)
+    with pytest.raises(pkg.MinimumSeparationError):
+        c.triplet_pass(tiny, ff)
+    pos = random_positions(rng, 400, (8.0,) * 3, True)
+    for shift in (3e-11, 7e-11):
+        p = np.vstack([pos, pos[137] + np.array([0.0, shift, 0.0])])
+        s = _system(pkg, p, (8.0,) * 3, True)
+        with pytest.raises(pkg.MinimumSeparationError):
+            c.triplet_pass(s, ff)
+
+
 def test_deterministic_passes(pkg):
     s = pkg.systems.CONFIGS["cfg2"].system()
     ff = pkg.ForceField(nu=0.073, cutoff=2.5)

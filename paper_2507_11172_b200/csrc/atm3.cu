@@ -43,8 +43,12 @@ namespace rb {
 #define RB_A3_WARPS 4
 #endif
 constexpr int kA3Warps = RB_A3_WARPS;
+// (6 blocks of 4 warps, 80 registers: with the 43-instruction rounds the pass
+// is throughput-bound on pipes its warps share, and fewer warps without
+// spills win -- 5 / 6 / 7 / 8 blocks per SM: cfg4 5.76 / 5.61 / 5.64 / 5.72 ms,
+// cfg2 0.116 / 0.116 / 0.120 / 0.124 ms, cfg3@2.5 0.752 / 0.734 / 0.744 ms / -)
 #ifndef RB_A3_MIN_BLOCKS
-#define RB_A3_MIN_BLOCKS 7
+#define RB_A3_MIN_BLOCKS 6
 #endif
 constexpr int kA3MinBlocks = RB_A3_MIN_BLOCKS;  // register cap for occupancy
 constexpr int kA3MaxSlots = 4096;
